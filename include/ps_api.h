@@ -1,0 +1,370 @@
+/* ps_api.h — C ABI of the B200-native PreScope MoE-inference hot path.
+ *
+ * Drop-in boundary for the reference's C++ operator API (namespace prescope,
+ * /root/reference/proj/include/prescope/ *.hpp). Every entry point below names the
+ * reference interface it replaces (file:line). Plain C: integers, doubles, caller-
+ * owned buffers, opaque handles, cudaStream_t as void*. No exception crosses this
+ * boundary; errors are status codes plus a thread-local message (ps_last_error), and
+ * include/prescope_b200.hpp re-throws them as the reference's exception types
+ * (invalid_argument / out_of_range / runtime_error, tools/prescope_main.cpp:427-434).
+ *
+ * Threading: host planning/simulation entry points are pure and reentrant. A ps_engine
+ * is single-owner (one host thread per engine). GPU entry points enqueue
+ * on the given stream and never synchronise the device unless stated.
+ */
+#ifndef PS_API_H
+#define PS_API_H
+
+#include <stddef.h>
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+/* ------------------------------------------------------------------------- status */
+typedef enum {
+  PS_OK = 0,
+  PS_EINVAL = 1,   /* std::invalid_argument */
+  PS_ERANGE = 2,   /* std::out_of_range */
+  PS_ERUNTIME = 3, /* std::runtime_error (I/O, overflow, checksum) */
+  PS_ECUDA = 4,    /* CUDA runtime / driver failure */
+  PS_ENCCL = 5     /* NCCL failure */
+} ps_status;
+
+const char* ps_last_error(void);
+const char* ps_version(void);
+
+/* ---------------------------------------------------------------------- model spec
+ * prescope::ModelSpec (workload.hpp:18-31) and presets (workload.cpp:43-79). */
+typedef struct {
+  int32_t num_layers;
+  int32_t experts_per_layer;
+  int32_t top_k;
+  int32_t hidden_dim;
+  uint64_t expert_bytes; /* 3*H*F*2 (bf16 gate/up/down) */
+  int32_t group_begin_middle;
+  int32_t group_begin_output;
+} ps_model_spec;
+
+typedef enum { PS_GROUP_INPUT = 0, PS_GROUP_MIDDLE = 1, PS_GROUP_OUTPUT = 2 } ps_layer_group;
+
+ps_status ps_spec_validate(const ps_model_spec* spec);                      /* workload.cpp:24-32 */
+ps_status ps_spec_group_of(const ps_model_spec* spec, int layer, int* group); /* workload.cpp:34-40 */
+ps_status ps_spec_preset(const char* name, ps_model_spec* out);             /* workload.cpp:65-71 */
+ps_status ps_desk_scale(const ps_model_spec* full, int num_layers, int experts, int hidden,
+                        ps_model_spec* out);                               /* workload.cpp:73-79 */
+/* F = expert_bytes / (6*H); PS_EINVAL when expert_bytes is not 6*H*F. */
+ps_status ps_spec_ffn_dim(const ps_model_spec* spec, int* ffn_dim);
+
+/* ------------------------------------------------------------------ routing (host) */
+/* topk_indices (workload.cpp:110-119): weight desc, ties lower index. Returns count. */
+int ps_topk_indices(const double* weights, int n, int k, int32_t* out);
+/* routing_map (workload.cpp:106-108). */
+int ps_routing_map(const ps_model_spec* spec, int expert);
+
+/* Synthetic routing inputs of generate_trace (workload.cpp:139-219) WITHOUT the
+ * routing: the gate matrices, the per-(token, layer) hidden state a and the kappa
+ * follow flag are routing-independent, so the GPU router consumes
+ * them and recomputes the trace's routing. Same RNG stream as the reference.
+ *   gate   [L*E*H] f64 (nullable), hidden [B*L*H] f64 (nullable), follow [B*L] u8,
+ *   index (token*L + layer). zipf per layer: [L] f64 (nullable). */
+typedef struct {
+  double rho, kappa, zipf_s;
+} ps_group_gen;
+typedef struct {
+  ps_group_gen input, middle, output;
+  double noise_scale;
+} ps_trace_gen_config;
+ps_status ps_trace_inputs(const ps_trace_gen_config* cfg, const ps_model_spec* spec, int batch,
+                          uint64_t seed, double* gate, double* hidden, uint8_t* follow,
+                          double* zipf_per_layer);
+
+/* --------------------------------------------------------------------- cost model
+ * prescope::CostParams / ExpertLoad / HitStats (cost_model.hpp:13-62). Ticks = us. */
+typedef struct {
+  int64_t t_io, t_g, t_attn;
+  double beta;
+  int64_t startup;
+  int64_t alpha;
+} ps_cost_params;
+
+typedef enum { PS_LOC_RESIDENT = 0, PS_LOC_INFLIGHT = 1, PS_LOC_HOST = 2 } ps_expert_location;
+
+typedef struct {
+  int32_t expert, layer, tokens, location;
+} ps_expert_load;
+
+typedef struct {
+  double r_hit, r_miss;
+  int32_t window;
+} ps_hit_stats;
+
+int64_t ps_to_ticks(double x);                                        /* cost_model.cpp:11 */
+ps_status ps_cost_params_validate(const ps_cost_params* p);           /* cost_model.cpp:13-18 */
+ps_status ps_hit_stats_record(ps_hit_stats* s, int hit);              /* cost_model.cpp:28-32 */
+ps_status ps_cpu_cost(int tokens, const ps_cost_params* p, int64_t* out); /* cost_model.cpp:34-37 */
+/* overlap_prefetch_count (cost_model.cpp:94-100) and prefetch_gain (102-106). */
+ps_status ps_overlap_prefetch_count(int64_t t_gap, const ps_cost_params* p, double* f, int* f_int);
+double ps_prefetch_gain(const ps_hit_stats* s, double f, int f_int, const ps_cost_params* p);
+/* fit_cost_params (cost_model.cpp:45-72): OLS over (tokens, ticks). */
+ps_status ps_fit_cost_params(const int32_t* tokens, const int64_t* ticks, int n, double* beta,
+                             double* startup, double* r_squared);
+
+/* ----------------------------------------------------------------------- PreSched
+ * LayerInputs / LayerPlan / SchedulerPolicy (scheduler.hpp:13-65). */
+typedef struct {
+  const ps_expert_load* e_cur;   int32_t n_cur;   /* gating truth, ascending tokens */
+  const ps_expert_load* e_next;  int32_t n_next;  /* predicted l+1 */
+  const ps_expert_load* e_next2; int32_t n_next2; /* predicted l+2 (widened window) */
+  ps_cost_params params;
+  ps_hit_stats stats;
+} ps_layer_inputs;
+
+typedef struct {
+  int64_t* sweep_gpu; /* nullable, capacity >= n_cur + n_next */
+  int64_t* sweep_cpu; /* nullable */
+  int32_t n_sweep;
+  int64_t t_g_at_split, t_c_at_split, t_gap;
+  double f;
+  int32_t f_int;
+  double xi;
+  int32_t widened_window, all_gpu_fallback;
+} ps_decision_trace;
+
+typedef struct {
+  /* caller-owned outputs; capacities: cpu_set/ondemand_seq >= n_cur,
+   * prefetch_seq >= max(n_next, n_next2) */
+  ps_expert_load* cpu_set;      int32_t n_cpu;
+  ps_expert_load* ondemand_seq; int32_t n_ondemand;
+  ps_expert_load* prefetch_seq; int32_t n_prefetch;
+  int32_t prefetch_from_widened;
+  int32_t split_index;
+  int32_t issued_prefetches;
+  ps_decision_trace trace;
+} ps_layer_plan;
+
+typedef enum {
+  PS_POLICY_PRESCHED = 0,
+  PS_POLICY_GREEDY = 1,
+  PS_POLICY_ONDEMAND = 2,
+  PS_POLICY_FIXED = 3,
+  PS_POLICY_ORACLE = 4
+} ps_policy_kind;
+
+typedef struct {
+  int32_t kind;
+  int32_t fixed_prefetch;
+} ps_policy;
+
+ps_status ps_policy_parse(const char* text, ps_policy* out);           /* scheduler.cpp:23-41 */
+ps_status ps_policy_name(ps_policy p, char* buf, int cap);             /* scheduler.cpp:43-52 */
+ps_status ps_layer_inputs_validate(const ps_layer_inputs* in);         /* scheduler.cpp:8-21 */
+/* plan_layer (scheduler.cpp:271-282) dispatching to schedule_layer (188-213),
+ * greedy_layer_baseline (215-250), ondemand_only_plan (252-260), fixed_prefetch_plan
+ * (262-269). O(n log n) (stable merge + prefix sums) instead of the reference's
+ * O((n+n')^2), bit-identical results. Host, pure, reentrant. */
+ps_status ps_presched_plan(const ps_layer_inputs* in, ps_policy policy, ps_layer_plan* out);
+
+/* ------------------------------------------------------- AsyncIO model-clock pipeline
+ * PipelineInstance / Timeline / SimOptions / simulate_pipeline (simulator.hpp:14-96).
+ * Dense layout: truth/predicted [L*E] token counts (0 = absent), resident [L*E] u8,
+ * groups [L] (nullable => all middle). */
+typedef struct {
+  int32_t num_layers, experts;
+  const int32_t* truth;
+  const int32_t* predicted;
+  const uint8_t* resident;
+  const int32_t* groups;
+} ps_pipeline_instance;
+
+typedef enum { PS_RES_GPU = 0, PS_RES_CPU = 1, PS_RES_IO = 2 } ps_resource;
+typedef enum {
+  PS_EV_ATTENTION = 0, PS_EV_GPU_EXPERT = 1, PS_EV_CPU_EXPERT = 2,
+  PS_EV_LOAD = 3, PS_EV_PREFETCH = 4, PS_EV_IDLE = 5
+} ps_event_kind;
+
+typedef struct {
+  int64_t t_start, t_end;
+  int32_t resource, kind, layer, expert, tokens;
+} ps_timeline_event;
+
+typedef struct {
+  ps_timeline_event* events; int32_t cap_events; int32_t n_events;
+  int64_t* layer_start; /* [L] */
+  int64_t* layer_end;   /* [L] */
+  int64_t makespan;
+  int32_t* plan_summary; /* nullable [4*L]: split, issued, from_widened, n_ondemand */
+} ps_timeline;
+
+typedef struct {
+  int32_t cpu_slots;        /* default 1 */
+  int32_t prefetch_slots;   /* default 8 per target layer */
+  double initial_hit_rate;  /* default 1.0 */
+  int32_t hit_window;       /* default 32 */
+} ps_sim_options;
+
+/* PlanFn plugin seam (simulator.hpp:66): called once per layer. */
+typedef ps_status (*ps_plan_fn)(void* user, const ps_layer_inputs* in, int layer,
+                                ps_layer_plan* out);
+
+/* simulate_pipeline (simulator.cpp:61-242). plan_fn NULL => plan with `policy`. */
+ps_status ps_simulate_pipeline(const ps_pipeline_instance* inst, ps_policy policy,
+                               ps_plan_fn plan_fn, void* user, const ps_cost_params* params,
+                               const ps_sim_options* opts, ps_timeline* out);
+/* verify_timeline (simulator.cpp:323-394): number of violations in *n_violations;
+ * messages (nullable) newline-joined into msg_buf. */
+ps_status ps_verify_timeline(const ps_timeline_event* events, int n_events,
+                             const ps_pipeline_instance* inst, const ps_cost_params* params,
+                             int* n_violations, char* msg_buf, int msg_cap);
+/* compute_metrics (simulator.cpp:396-426). per_layer arrays nullable [L]. */
+typedef struct {
+  int64_t makespan, decode_latency;
+  double throughput_tokens_per_s, io_busy_fraction, gpu_idle_fraction;
+} ps_metrics;
+ps_status ps_compute_metrics(const ps_timeline_event* events, int n_events,
+                             const int64_t* layer_start, const int64_t* layer_end, int L,
+                             int output_tokens, ps_metrics* out, int64_t* per_layer_latency,
+                             int64_t* cpu_gpu_gap);
+
+/* ------------------------------------------------------------------ hot table / HBM budget
+ * build_hot_table + plan_residency (predictor.cpp:405-433). freq [L*E]. */
+ps_status ps_plan_residency(const int64_t* freq, int L, int E, uint64_t budget_bytes,
+                            uint64_t expert_bytes, int32_t* pairs_out, int* n_out);
+
+/* -------------------------------------------------------------------------- GPU ops
+ * All device pointers; `stream` is a cudaStream_t. Shapes: B tokens, H hidden,
+ * E experts, k top-k, F ffn dim. bf16 = uint16_t storage. */
+
+/* K1 — fused router: fp32 gate GEMV + zipf bias + kappa-follow override + softmax +
+ * top-k (ranking the softmax weights, ties lower index) + per-expert histogram, one
+ * launch. Replaces the router loop of generate_trace (workload.cpp:176-202) and
+ * aggregate_layer_loads (workload.cpp:283-288).
+ *   x [B,H] f32; gate [E,H] f32; bias [E] f32 (= -zipf*ln(e+1), nullable);
+ *   follow [B] u8 (nullable); prev_ids [B,prev_k] i32 (nullable: layer 0).
+ * Outputs: logits/weights [B,E] f32 (nullable), ids [B,k] i32, counts [E] i32
+ * (overwritten), x_bf16 [B,H] (nullable; fused cast for the expert FFN). */
+ps_status ps_route_topk(const float* x, const float* gate, const float* bias,
+                        const uint8_t* follow, const int32_t* prev_ids, int prev_k, int B,
+                        int H, int E, int k, float* logits, float* weights, int32_t* ids,
+                        int32_t* counts, uint16_t* x_bf16, void* stream);
+
+/* K2 — counting-sort permute: rows ordered (expert asc, token asc, slot asc).
+ *   offsets [E+1], perm_src [B*k] (= token*k+slot), inv [B*k].
+ *   x [B,H] bf16 + x_perm [B*k,H] bf16: optional gather (both nullable). */
+ps_status ps_permute(const int32_t* ids, int B, int k, int E, int32_t* offsets,
+                     int32_t* perm_src, int32_t* inv, const uint16_t* x, int H,
+                     uint16_t* x_perm, void* stream);
+
+/* K2 — weighted combine: y[t] = sum_j weights[t, ids[t,j]] * sum_s y_part[s][inv[t*k+j]]
+ * (full-softmax gate weights, workload.cpp:190-195; no top-k renormalisation).
+ *   y_part [n_split, B*k, H] f32; y [B,H] f32. */
+ps_status ps_combine(const float* y_part, int n_split, const int32_t* inv, const int32_t* ids,
+                     const float* weights, int B, int k, int E, int H, float* y, void* stream);
+
+/* K3 — grouped SwiGLU expert FFN over a set of experts whose slabs are on device.
+ * Slab layout [Wg (F*H) | Wu (F*H) | Wd (H*F)] bf16 row-major = expert_bytes.
+ * Rows of expert experts[i] are permuted rows [offsets[e], offsets[e+1]) (K2), token
+ * = perm_src[row]/k; x [B,H] bf16.
+ * Decode path (HBM-bound GEMV): h [B*k,F] bf16 scratch, y_part [n_split,total_rows,H]
+ * f32 with total_rows = B*k (all permuted rows). counts_host [E]: host copy of the
+ * histogram (grid sizing only; the kernels read offsets on the device). */
+#define PS_MAX_GROUP 256
+typedef struct {
+  int32_t n;
+  int32_t experts[PS_MAX_GROUP];
+  const uint16_t* slabs[PS_MAX_GROUP];
+} ps_expert_group;
+
+ps_status ps_expert_ffn(const ps_expert_group* group, const int32_t* counts_host,
+                        const int32_t* offsets, const int32_t* perm_src, int k,
+                        const uint16_t* x, int H, int F, uint16_t* h, float* y_part,
+                        int n_split, int total_rows, void* stream);
+/* Split-K factor ps_expert_ffn expects for the down projection at this shape. */
+int ps_ffn_down_splits(int H, int F);
+
+/* Deterministic synthetic expert weights: counter-hash of (seed, layer, expert, index)
+ * -> bf16 ~ N(0, 1/sqrt(fan_in)) by Irwin-Hall sum of 4 uniforms (exact integer
+ * arithmetic, identical on host and device). Gate/up rows have fan_in H, down rows F. */
+ps_status ps_init_expert_slab(uint16_t* slab, int H, int F, uint64_t seed, int layer,
+                              int expert, void* stream);
+ps_status ps_init_expert_slab_host(uint16_t* slab, int H, int F, uint64_t seed, int layer,
+                                   int expert);
+
+/* K4 — LLaPor predictor (predictor.cpp:116-124, 166-247, 344-352, 669-672). */
+typedef struct ps_llapor_s* ps_llapor;
+/* load_checkpoint (predictor.cpp:866-929): LLPC v1 file -> device-resident nets. */
+ps_status ps_llapor_load(const char* path, ps_llapor* out, ps_model_spec* spec_out);
+/* Random-init nets at full shapes (pca_dim/width per group, predictor.hpp:97-100). */
+ps_status ps_llapor_random(const ps_model_spec* spec, int pca_in, int pca_mid, int width_in,
+                           int width_mid, uint64_t seed, ps_llapor* out);
+ps_status ps_llapor_free(ps_llapor m);
+/* Net for target layer `layer` (>=1) on features of layer-1 for B tokens:
+ *   hidden [B,H] f32, prev_ids [B,k_prev] i32, prev_weights [B,E] f32.
+ * Outputs: logits [B,E] f32 (nullable), ids [B,k] i32 (top-k on LOGITS),
+ * pred_counts [E] i32 (overwritten; predicted per-expert histogram, predict_loads
+ * experiment.cpp:104-112). scratch: ps_llapor_scratch_bytes. */
+size_t ps_llapor_scratch_bytes(ps_llapor m, int B);
+ps_status ps_llapor_forward(ps_llapor m, int layer, const float* hidden,
+                            const int32_t* prev_ids, int k_prev, const float* prev_weights,
+                            int B, int k, float* logits, int32_t* ids, int32_t* pred_counts,
+                            void* scratch, void* stream);
+
+/* -------------------------------------------------------------------- decode engine
+ * K5: the AsyncIO expert loader + HBM expert cache + per-layer decode driver.
+ * Resident experts (plan_residency under budget_bytes) live in HBM; the others in
+ * pinned host DRAM and are loaded by PreSched plans as cudaMemcpyAsync on a dedicated
+ * copy stream (serial I/O channel) into dual on-demand slots (simulator.cpp:181-197)
+ * or per-target-layer prefetch slots (simulator.cpp:206-227), event-ordered against
+ * the compute stream. */
+typedef struct ps_engine_s* ps_engine;
+
+typedef struct {
+  ps_model_spec spec;
+  ps_trace_gen_config gen;  /* zipf per group for the router bias */
+  uint64_t weight_seed;     /* expert + router weights */
+  uint64_t budget_bytes;    /* HBM resident-expert budget */
+  const int32_t* resident;  /* nullable [2*n_resident] (layer, expert); else hot table */
+  int32_t n_resident;
+  int32_t max_batch;
+  int32_t prefetch_slots;   /* per target layer, default 8 */
+  ps_policy policy;
+  ps_cost_params cost;      /* t_io/t_g/t_attn in us; 0 => calibrate at create */
+  ps_llapor predictor;      /* nullable => perfect-prediction off; uses gate weights */
+  int32_t device;
+  int32_t host_pinned;      /* 1: non-resident experts in pinned host DRAM */
+} ps_engine_config;
+
+ps_status ps_engine_create(const ps_engine_config* cfg, ps_engine* out);
+ps_status ps_engine_destroy(ps_engine e);
+/* Gate matrices [L,E,H] f32 host (from ps_trace_inputs) -> device. */
+ps_status ps_engine_set_router(ps_engine e, const float* gate_host);
+/* One decode step over all L layers for B tokens, device buffers:
+ *   hidden [L,B,H] f32 (layer-major gating inputs), follow [L,B] u8,
+ *   y [L,B,H] f32 out (MoE output per layer), ids [L,B,k] i32 out (routing).
+ * Blocks the host until the step's GPU work is complete. */
+ps_status ps_engine_decode_step(ps_engine e, const float* hidden, const uint8_t* follow, int B,
+                                float* y, int32_t* ids);
+/* Same, from HOST buffers (pinned or pageable): copies in, step, copies out. */
+ps_status ps_engine_decode_step_host(ps_engine e, const float* hidden_host,
+                                     const uint8_t* follow_host, int B, float* y_host,
+                                     int32_t* ids_host);
+
+typedef struct {
+  int64_t steps, layers;
+  int64_t ondemand_loads, prefetches_committed, prefetches_cancelled, prefetch_hits;
+  int64_t resident_hits;
+  double h2d_bytes, h2d_busy_ms, compute_wait_ms, step_ms_total;
+  double ffn_ms_total;      /* device time of K3 launches (events) */
+  int64_t ffn_launches, kernel_launches;
+  ps_cost_params cost;      /* calibrated costs in use */
+} ps_engine_stats;
+ps_status ps_engine_get_stats(ps_engine e, ps_engine_stats* out);
+ps_status ps_engine_reset_stats(ps_engine e);
+/* Measured timeline of the last step (events from CUDA events, us from step start). */
+ps_status ps_engine_last_timeline(ps_engine e, ps_timeline* out);
+
+#ifdef __cplusplus
+}
+#endif
+#endif /* PS_API_H */

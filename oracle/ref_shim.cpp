@@ -1,0 +1,518 @@
+// TEST INFRASTRUCTURE ONLY — not product code.
+//
+// extern "C" shim over the UNMODIFIED reference library (/root/reference/proj/src),
+// compiled by oracle/Makefile into oracle/_ref/libprescope_ref.so. Only tests/,
+// __graft_entry__.smoke() and bench.py's CPU-baseline leg may load it: it is the
+// checker that pins oracle/oracle.c and the fixtures under tests/golden/, and the
+// "reference" CPU arm of bench.py. Nothing in paper_2509_23638_b200/ links it.
+//
+// Every entry point returns 0 on success and maps the reference's exceptions the
+// same way the reference CLI does (tools/prescope_main.cpp:427-434):
+//   1 = std::invalid_argument, 2 = std::out_of_range, 3 = std::runtime_error/other.
+#include <chrono>
+#include <cstdint>
+#include <cstring>
+#include <fstream>
+#include <map>
+#include <memory>
+#include <set>
+#include <string>
+#include <vector>
+
+#include "json.hpp"
+#include "prescope/experiment.hpp"
+#include "prescope/golden.hpp"
+#include "prescope/predictor.hpp"
+#include "prescope/scheduler.hpp"
+#include "prescope/simulator.hpp"
+#include "prescope/workload.hpp"
+
+using namespace prescope;
+
+extern "C" {
+
+struct ref_spec {
+  int32_t num_layers, experts, top_k, hidden;
+  uint64_t expert_bytes;
+  int32_t group_begin_middle, group_begin_output;
+};
+struct ref_gen {
+  double rho[3], kappa[3], zipf[3];  // input, middle, output
+  double noise_scale;
+};
+struct ref_load {
+  int32_t expert, layer, tokens;
+};
+struct ref_params {
+  int64_t t_io, t_g, t_attn;
+  double beta;
+  int64_t startup, alpha;
+};
+struct ref_stats {
+  double r_hit, r_miss;
+  int32_t window;
+};
+struct ref_plan_info {
+  int32_t split_index, issued_prefetches, prefetch_from_widened;
+  int32_t n_cpu, n_od, n_pf, n_sweep;
+  int64_t t_g_at_split, t_c_at_split, t_gap;
+  double f;
+  int32_t f_int;
+  double xi;
+  int32_t widened_window, all_gpu_fallback;
+};
+struct ref_event {
+  int64_t t_start, t_end;
+  int32_t resource, kind, layer, expert, tokens;
+};
+struct ref_sim_opts {
+  int32_t cpu_slots, prefetch_slots;
+  double initial_hit_rate;
+  int32_t hit_window;
+};
+}
+
+namespace {
+
+thread_local std::string g_err;
+
+template <typename F>
+int guarded(F&& f) {
+  try {
+    f();
+    return 0;
+  } catch (const std::invalid_argument& e) {
+    g_err = e.what();
+    return 1;
+  } catch (const std::out_of_range& e) {
+    g_err = e.what();
+    return 2;
+  } catch (const std::exception& e) {
+    g_err = e.what();
+    return 3;
+  }
+}
+
+ModelSpec to_spec(const ref_spec& s) {
+  ModelSpec m;
+  m.num_layers = s.num_layers;
+  m.experts_per_layer = s.experts;
+  m.top_k = s.top_k;
+  m.expert_bytes = s.expert_bytes;
+  m.hidden_dim = s.hidden;
+  m.group_begin_middle = s.group_begin_middle;
+  m.group_begin_output = s.group_begin_output;
+  return m;
+}
+
+TraceGenConfig to_gen(const ref_gen& g) {
+  TraceGenConfig c;
+  c.input = {g.rho[0], g.kappa[0], g.zipf[0]};
+  c.middle = {g.rho[1], g.kappa[1], g.zipf[1]};
+  c.output = {g.rho[2], g.kappa[2], g.zipf[2]};
+  c.noise_scale = g.noise_scale;
+  return c;
+}
+
+CostParams to_params(const ref_params& p) {
+  CostParams c;
+  c.t_io = p.t_io;
+  c.t_g = p.t_g;
+  c.t_attn = p.t_attn;
+  c.beta = p.beta;
+  c.startup = p.startup;
+  c.alpha = p.alpha;
+  return c;
+}
+
+std::vector<ExpertLoad> to_loads(const ref_load* l, int n) {
+  std::vector<ExpertLoad> v;
+  for (int i = 0; i < n; ++i) v.push_back({l[i].expert, l[i].layer, l[i].tokens, ExpertLocation::Host});
+  return v;
+}
+
+void from_loads(const std::vector<ExpertLoad>& v, ref_load* out) {
+  for (size_t i = 0; i < v.size(); ++i) out[i] = {v[i].expert, v[i].layer, v[i].tokens};
+}
+
+SchedulerPolicy to_policy(int kind, int fixed_c) {
+  SchedulerPolicy p;
+  p.kind = static_cast<SchedulerPolicy::Kind>(kind);
+  p.fixed_prefetch = fixed_c;
+  return p;
+}
+
+void fill_info(const LayerPlan& plan, ref_plan_info* info) {
+  info->split_index = plan.split_index;
+  info->issued_prefetches = plan.issued_prefetches;
+  info->prefetch_from_widened = plan.prefetch_from_widened;
+  info->n_cpu = static_cast<int32_t>(plan.cpu_set.size());
+  info->n_od = static_cast<int32_t>(plan.ondemand_seq.size());
+  info->n_pf = static_cast<int32_t>(plan.prefetch_seq.size());
+  info->n_sweep = static_cast<int32_t>(plan.trace.sweep_gpu.size());
+  info->t_g_at_split = plan.trace.t_g_at_split;
+  info->t_c_at_split = plan.trace.t_c_at_split;
+  info->t_gap = plan.trace.t_gap;
+  info->f = plan.trace.f;
+  info->f_int = plan.trace.f_int;
+  info->xi = plan.trace.xi;
+  info->widened_window = plan.trace.widened_window;
+  info->all_gpu_fallback = plan.trace.all_gpu_fallback;
+}
+
+PipelineInstance make_instance(int L, const int32_t* truth, int n_truth, const int32_t* pred,
+                               int n_pred, const int32_t* resident, int n_res,
+                               const int32_t* groups) {
+  PipelineInstance inst;
+  inst.layers.resize(L);
+  for (int i = 0; i < n_truth; ++i) inst.layers.at(truth[3 * i]).truth[truth[3 * i + 1]] = truth[3 * i + 2];
+  for (int i = 0; i < n_pred; ++i) inst.layers.at(pred[3 * i]).predicted[pred[3 * i + 1]] = pred[3 * i + 2];
+  for (int i = 0; i < n_res; ++i) inst.resident.insert({resident[2 * i], resident[2 * i + 1]});
+  if (groups)
+    for (int l = 0; l < L; ++l) inst.groups.push_back(static_cast<LayerGroup>(groups[l]));
+  return inst;
+}
+
+nlohmann::json timeline_json(const Timeline& t) {
+  nlohmann::json ev = nlohmann::json::array();
+  for (const TimelineEvent& e : t.events)
+    ev.push_back({e.t_start, e.t_end, static_cast<int>(e.resource), static_cast<int>(e.kind),
+                  e.layer, e.expert, e.tokens});
+  return {{"events", ev},
+          {"layer_start", t.layer_start},
+          {"layer_end", t.layer_end},
+          {"makespan", t.makespan}};
+}
+
+nlohmann::json instance_json(const PipelineInstance& inst) {
+  nlohmann::json layers = nlohmann::json::array();
+  for (const LayerLoads& l : inst.layers) {
+    nlohmann::json truth = nlohmann::json::array(), pred = nlohmann::json::array();
+    for (auto [e, m] : l.truth) truth.push_back({e, m});
+    for (auto [e, m] : l.predicted) pred.push_back({e, m});
+    layers.push_back({{"truth", truth}, {"predicted", pred}});
+  }
+  nlohmann::json res = nlohmann::json::array();
+  for (auto [l, e] : inst.resident) res.push_back({l, e});
+  nlohmann::json groups = nlohmann::json::array();
+  for (LayerGroup g : inst.groups) groups.push_back(static_cast<int>(g));
+  return {{"layers", layers}, {"resident", res}, {"groups", groups}};
+}
+
+nlohmann::json params_json(const CostParams& p) {
+  return {{"t_io", p.t_io}, {"t_g", p.t_g}, {"t_attn", p.t_attn},
+          {"beta", p.beta}, {"startup", p.startup}, {"alpha", p.alpha}};
+}
+
+nlohmann::json plan_json(const LayerPlan& plan) {
+  auto loads = [](const std::vector<ExpertLoad>& v) {
+    nlohmann::json a = nlohmann::json::array();
+    for (const ExpertLoad& e : v) a.push_back({e.expert, e.layer, e.tokens});
+    return a;
+  };
+  return {{"split_index", plan.split_index},
+          {"issued_prefetches", plan.issued_prefetches},
+          {"prefetch_from_widened", plan.prefetch_from_widened},
+          {"cpu_set", loads(plan.cpu_set)},
+          {"ondemand_seq", loads(plan.ondemand_seq)},
+          {"prefetch_seq", loads(plan.prefetch_seq)},
+          {"t_g_at_split", plan.trace.t_g_at_split},
+          {"t_c_at_split", plan.trace.t_c_at_split},
+          {"t_gap", plan.trace.t_gap},
+          {"f", plan.trace.f},
+          {"f_int", plan.trace.f_int},
+          {"xi", plan.trace.xi},
+          {"widened_window", plan.trace.widened_window},
+          {"all_gpu_fallback", plan.trace.all_gpu_fallback},
+          {"sweep_gpu", plan.trace.sweep_gpu},
+          {"sweep_cpu", plan.trace.sweep_cpu}};
+}
+
+struct LLaPorHandle {
+  LLaPor model;
+  uint64_t checksum = 0;
+};
+
+}  // namespace
+
+extern "C" {
+
+const char* ref_last_error() { return g_err.c_str(); }
+
+int ref_spec_preset(const char* name, ref_spec* out) {
+  return guarded([&] {
+    ModelSpec m = spec_preset(name);
+    *out = {m.num_layers, m.experts_per_layer, m.top_k, m.hidden_dim, m.expert_bytes,
+            m.group_begin_middle, m.group_begin_output};
+  });
+}
+
+int ref_desk_scale(const char* name, int layers, int experts, int hidden, ref_spec* out) {
+  return guarded([&] {
+    ModelSpec m = desk_scale(spec_preset(name), layers, experts, hidden);
+    *out = {m.num_layers, m.experts_per_layer, m.top_k, m.hidden_dim, m.expert_bytes,
+            m.group_begin_middle, m.group_begin_output};
+  });
+}
+
+// generate_trace (workload.cpp:139-219) flattened: hidden [B*L*H], gate_weights
+// [B*L*E], active [B*L*k]; each indexed (token*L + layer).
+int ref_generate_trace(const ref_gen* gen, const ref_spec* spec, int batch, uint64_t seed,
+                       double* hidden, double* gate_weights, int32_t* active) {
+  return guarded([&] {
+    Trace t = generate_trace(to_gen(*gen), to_spec(*spec), batch, seed);
+    const int H = spec->hidden, E = spec->experts, K = spec->top_k;
+    for (size_t i = 0; i < t.steps.size(); ++i) {
+      const TraceStep& s = t.steps[i];
+      if (hidden) std::memcpy(hidden + i * H, s.hidden.data(), sizeof(double) * H);
+      if (gate_weights) std::memcpy(gate_weights + i * E, s.gate_weights.data(), sizeof(double) * E);
+      if (active)
+        for (int j = 0; j < K; ++j) active[i * K + j] = s.active_experts[j];
+    }
+  });
+}
+
+int ref_write_trace(const ref_gen* gen, const ref_spec* spec, int batch, uint64_t seed,
+                    const char* path) {
+  return guarded([&] { write_trace(generate_trace(to_gen(*gen), to_spec(*spec), batch, seed), path); });
+}
+
+int ref_topk(const double* w, int n, int k, int32_t* out, int* n_out) {
+  return guarded([&] {
+    std::vector<int> r = topk_indices(std::vector<double>(w, w + n), k);
+    for (size_t i = 0; i < r.size(); ++i) out[i] = r[i];
+    *n_out = static_cast<int>(r.size());
+  });
+}
+
+// Hot table + residency from one trace (predictor.cpp:405-433); pairs out [2*n].
+int ref_residency(const ref_gen* gen, const ref_spec* spec, int batch, uint64_t seed,
+                  uint64_t budget_bytes, int32_t* pairs, int* n_out) {
+  return guarded([&] {
+    Trace t = generate_trace(to_gen(*gen), to_spec(*spec), batch, seed);
+    HotExpertTable table = build_hot_table({t});
+    auto res = plan_residency(table, budget_bytes, spec->expert_bytes);
+    for (size_t i = 0; i < res.size(); ++i) {
+      pairs[2 * i] = res[i].first;
+      pairs[2 * i + 1] = res[i].second;
+    }
+    *n_out = static_cast<int>(res.size());
+  });
+}
+
+// plan_layer (scheduler.cpp:402-413) on explicit LayerInputs. Output buffers sized
+// by the caller: cpu/od <= n_cur, pf <= max(n_next, n_next2), sweeps <= n_cur+n_next.
+int ref_plan_layer(int policy_kind, int fixed_c, const ref_load* cur, int n_cur,
+                   const ref_load* nxt, int n_next, const ref_load* nxt2, int n_next2,
+                   const ref_params* params, const ref_stats* stats, ref_plan_info* info,
+                   ref_load* cpu, ref_load* od, ref_load* pf, int64_t* sweep_gpu,
+                   int64_t* sweep_cpu) {
+  return guarded([&] {
+    LayerInputs in;
+    in.e_cur = to_loads(cur, n_cur);
+    in.e_next = to_loads(nxt, n_next);
+    in.e_next2 = to_loads(nxt2, n_next2);
+    in.params = to_params(*params);
+    in.stats.r_hit = stats->r_hit;
+    in.stats.r_miss = stats->r_miss;
+    in.stats.window = stats->window;
+    LayerPlan plan = plan_layer(in, to_policy(policy_kind, fixed_c));
+    fill_info(plan, info);
+    from_loads(plan.cpu_set, cpu);
+    from_loads(plan.ondemand_seq, od);
+    from_loads(plan.prefetch_seq, pf);
+    for (size_t i = 0; i < plan.trace.sweep_gpu.size(); ++i) {
+      if (sweep_gpu) sweep_gpu[i] = plan.trace.sweep_gpu[i];
+      if (sweep_cpu) sweep_cpu[i] = plan.trace.sweep_cpu[i];
+    }
+  });
+}
+
+// simulate_policy (simulator.cpp:244-252). truth/pred are (layer, expert, tokens)
+// triples, resident (layer, expert) pairs, groups per layer (nullable).
+// plan_summary per layer: split_index, issued_prefetches, prefetch_from_widened, alpha.
+int ref_simulate(int L, const int32_t* truth, int n_truth, const int32_t* pred, int n_pred,
+                 const int32_t* resident, int n_res, const int32_t* groups, int policy_kind,
+                 int fixed_c, const ref_params* params, const ref_sim_opts* opts,
+                 ref_event* events, int max_events, int* n_events, int64_t* layer_start,
+                 int64_t* layer_end, int64_t* makespan, int32_t* plan_summary) {
+  return guarded([&] {
+    PipelineInstance inst = make_instance(L, truth, n_truth, pred, n_pred, resident, n_res, groups);
+    SimOptions so;
+    so.cpu_slots = opts->cpu_slots;
+    so.prefetch_slots = opts->prefetch_slots;
+    so.initial_hit_rate = opts->initial_hit_rate;
+    so.hit_window = opts->hit_window;
+    SimResult r = simulate_policy(inst, to_policy(policy_kind, fixed_c), to_params(*params), so);
+    if (static_cast<int>(r.timeline.events.size()) > max_events)
+      throw std::runtime_error("ref_simulate: event buffer too small");
+    for (size_t i = 0; i < r.timeline.events.size(); ++i) {
+      const TimelineEvent& e = r.timeline.events[i];
+      events[i] = {e.t_start, e.t_end, static_cast<int32_t>(e.resource),
+                   static_cast<int32_t>(e.kind), e.layer, e.expert, e.tokens};
+    }
+    *n_events = static_cast<int>(r.timeline.events.size());
+    for (int l = 0; l < L; ++l) {
+      layer_start[l] = r.timeline.layer_start[l];
+      layer_end[l] = r.timeline.layer_end[l];
+    }
+    *makespan = r.timeline.makespan;
+    if (plan_summary)
+      for (size_t l = 0; l < r.plans.size(); ++l) {
+        plan_summary[4 * l + 0] = r.plans[l].split_index;
+        plan_summary[4 * l + 1] = r.plans[l].issued_prefetches;
+        plan_summary[4 * l + 2] = r.plans[l].prefetch_from_widened;
+        plan_summary[4 * l + 3] = static_cast<int32_t>(r.plans[l].ondemand_seq.size());
+      }
+  });
+}
+
+// verify_timeline (simulator.cpp:323-394) over a caller-supplied event list; returns
+// the number of violations in *n_viol.
+int ref_verify_timeline(int L, const int32_t* truth, int n_truth, const int32_t* resident,
+                        int n_res, const ref_params* params, const ref_event* events,
+                        int n_events, int* n_viol) {
+  return guarded([&] {
+    PipelineInstance inst = make_instance(L, truth, n_truth, nullptr, 0, resident, n_res, nullptr);
+    Timeline t;
+    for (int i = 0; i < n_events; ++i) {
+      const ref_event& e = events[i];
+      t.events.push_back({e.t_start, e.t_end, static_cast<Resource>(e.resource),
+                          static_cast<EventKind>(e.kind), e.layer, e.expert, e.tokens});
+    }
+    *n_viol = static_cast<int>(verify_timeline(t, inst, to_params(*params)).size());
+  });
+}
+
+// Dumps the six golden scenarios (golden.cpp:61-234) with their hand-derived
+// timelines, plus the reference PreSched plans/timeline on each instance.
+int ref_dump_golden(const char* path) {
+  return guarded([&] {
+    nlohmann::json all = nlohmann::json::array();
+    for (const std::string& id : golden_ids()) {
+      const GoldenScenario& s = golden_scenario(id);
+      SimResult got = simulate_policy(s.instance, s.policy, s.params, s.options);
+      SimResult pre = simulate_policy(s.instance, SchedulerPolicy::parse("presched"), s.params, s.options);
+      nlohmann::json plans = nlohmann::json::array(), pre_plans = nlohmann::json::array();
+      for (const LayerPlan& p : got.plans) plans.push_back(plan_json(p));
+      for (const LayerPlan& p : pre.plans) pre_plans.push_back(plan_json(p));
+      all.push_back({{"id", s.id},
+                     {"description", s.description},
+                     {"policy", s.policy.name()},
+                     {"params", params_json(s.params)},
+                     {"options", {{"cpu_slots", s.options.cpu_slots},
+                                  {"prefetch_slots", s.options.prefetch_slots},
+                                  {"initial_hit_rate", s.options.initial_hit_rate},
+                                  {"hit_window", s.options.hit_window}}},
+                     {"instance", instance_json(s.instance)},
+                     {"expected", timeline_json(s.expected)},
+                     {"replayed", timeline_json(got.timeline)},
+                     {"plans", plans},
+                     {"presched_timeline", timeline_json(pre.timeline)},
+                     {"presched_plans", pre_plans},
+                     {"pass", replay_golden(id).pass}});
+    }
+    std::ofstream out(path);
+    if (!out) throw std::runtime_error("ref_dump_golden: cannot open output");
+    out << all.dump(1) << '\n';
+  });
+}
+
+// LLaPor: train on `n_seeds` traces (make_llapor + train, predictor.cpp:467, 613)
+// and write the LLPC v1 checkpoint (predictor.cpp:833).
+int ref_train_llapor(const ref_gen* gen, const ref_spec* spec, int batch, const uint64_t* seeds,
+                     int n_seeds, int epochs, int warmup, uint64_t train_seed, const char* path) {
+  return guarded([&] {
+    std::vector<Trace> traces;
+    for (int i = 0; i < n_seeds; ++i)
+      traces.push_back(generate_trace(to_gen(*gen), to_spec(*spec), batch, seeds[i]));
+    TrainConfig cfg;
+    cfg.epochs = epochs;
+    cfg.warmup_epochs = warmup;
+    cfg.seed = train_seed;
+    LLaPor model = make_llapor(to_spec(*spec), cfg);
+    train(model, traces);
+    save_checkpoint(model, 0, path);
+  });
+}
+
+void* ref_llapor_load(const char* path) {
+  LLaPorHandle* h = nullptr;
+  int rc = guarded([&] {
+    auto p = std::make_unique<LLaPorHandle>();
+    p->model = load_checkpoint(path, &p->checksum);
+    h = p.release();
+  });
+  return rc == 0 ? h : nullptr;
+}
+
+void ref_llapor_free(void* h) { delete static_cast<LLaPorHandle*>(h); }
+
+// pca_apply + forward + predict_topk for net `layer` on one token's layer-1
+// features (experiment.cpp:85-98). reduced_out [P_eff], logits_out [E], topk_out [k].
+int ref_llapor_predict(void* handle, int layer, const double* hidden_prev,
+                       const int32_t* active_prev, int k_prev, const double* gate_prev, int k,
+                       double* reduced_out, double* logits_out, int32_t* topk_out) {
+  return guarded([&] {
+    const LLaPor& m = static_cast<LLaPorHandle*>(handle)->model;
+    const LLaPorNet& net = m.nets.at(layer);
+    const int H = m.spec.hidden_dim, E = net.experts_per_layer;
+    PredictorFeatures feat;
+    feat.hidden_reduced = pca_apply(net.pca, std::vector<double>(hidden_prev, hidden_prev + H));
+    feat.active_onehot.assign(E, 0.0);
+    for (int j = 0; j < k_prev; ++j) feat.active_onehot.at(active_prev[j]) = 1.0;
+    feat.gate_weights_prev.assign(gate_prev, gate_prev + E);
+    ForwardResult r = forward(net, feat);
+    std::vector<int> top = predict_topk(net, feat, k);
+    if (reduced_out)
+      std::memcpy(reduced_out, feat.hidden_reduced.data(), sizeof(double) * feat.hidden_reduced.size());
+    if (logits_out) std::memcpy(logits_out, r.logits.data(), sizeof(double) * E);
+    if (topk_out)
+      for (size_t i = 0; i < top.size(); ++i) topk_out[i] = top[i];
+  });
+}
+
+// predict_loads with the LLaPor predictor (experiment.cpp:104-112): loads_out [L*E].
+int ref_llapor_predict_loads(void* handle, const ref_gen* gen, int batch, uint64_t seed, int k,
+                             int32_t* loads_out) {
+  return guarded([&] {
+    const LLaPor& m = static_cast<LLaPorHandle*>(handle)->model;
+    Trace t = generate_trace(to_gen(*gen), m.spec, batch, seed);
+    PredictorChoice c;
+    c.kind = PredictorChoice::Kind::LLaPorCkpt;
+    c.checkpoint = "in-memory";
+    PredictFn fn = make_predict_fn(c, &m, nullptr, k, 0);
+    auto loads = predict_loads(t, fn);
+    const int E = m.spec.experts_per_layer;
+    std::fill(loads_out, loads_out + static_cast<size_t>(m.spec.num_layers) * E, 0);
+    for (int l = 0; l < m.spec.num_layers; ++l)
+      for (auto [e, c2] : loads[l]) loads_out[l * E + e] = c2;
+  });
+}
+
+// CPU-baseline leg (bench.py --impl reference): the reference's own per-decode-step
+// host work on one trace — predict_loads with LLaPor, build_instance, plan_residency,
+// simulate_policy(presched) — timed here in C++ so no ctypes overhead is counted.
+// Returns mean seconds per call over `reps` in *sec_out.
+int ref_time_schedule_pass(const ref_gen* gen, const ref_spec* spec, int batch, uint64_t seed,
+                           uint64_t budget_bytes, const ref_params* params, int reps,
+                           double* sec_out, int64_t* makespan_out) {
+  return guarded([&] {
+    Trace t = generate_trace(to_gen(*gen), to_spec(*spec), batch, seed);
+    HotExpertTable table = build_hot_table({t});
+    std::set<std::pair<int, int>> resident;
+    for (auto key : plan_residency(table, budget_bytes, spec->expert_bytes)) resident.insert(key);
+    PredictFn perfect = make_predict_fn(PredictorChoice::parse("perfect"), nullptr, nullptr,
+                                        spec->top_k, 0);
+    auto loads = predict_loads(t, perfect);
+    PipelineInstance inst = build_instance(t, loads, resident);
+    auto t0 = std::chrono::steady_clock::now();
+    int64_t ms = 0;
+    for (int r = 0; r < reps; ++r)
+      ms = simulate_policy(inst, SchedulerPolicy::parse("presched"), to_params(*params)).timeline.makespan;
+    *sec_out = std::chrono::duration<double>(std::chrono::steady_clock::now() - t0).count() / reps;
+    *makespan_out = ms;
+  });
+}
+
+}  // extern "C"

@@ -1,0 +1,823 @@
+// K5 — AsyncIO expert loader + HBM expert cache + per-layer decode driver.
+//
+// Real-hardware counterpart of the reference's simulated executor
+// (simulate_pipeline, simulator.cpp:61-242; rules R1-R8 in SURVEY.md §8a):
+//   * resident experts (plan_residency under the HBM budget, predictor.cpp:426-433)
+//     live in one HBM arena; every other expert lives in pinned host DRAM;
+//   * the serial I/O channel (R7/R8) is one copy stream owned by an I/O thread that
+//     keeps at most two expert copies in flight and services a FIFO, so prefetches
+//     that have not started by the next layer's scheduling point can still be
+//     cancelled (R2) while started ones run to completion (non-interruptible);
+//   * on-demand loads go through two alternating HBM slots (dual buffer, R7): a copy
+//     into a slot waits (cudaStreamWaitEvent) for the FFN that last read it;
+//   * prefetches land in a slot pool per target layer (cap = prefetch_slots, R8),
+//     released once the target layer's FFNs are done (R3);
+//   * PreSched (ps_presched_plan) runs on the host per layer on the GPU-computed
+//     histogram (K1) and the LLaPor-predicted histogram of layer l+1 (K4);
+//   * resident experts start computing right after routing, before the host plan
+//     (kernels read per-expert row counts on the device), hiding the host round trip.
+// GPU-only executor: the plan's cpu_set (empty under the default beta = 1e9 costs,
+// SURVEY.md §7 hard part 1) is loaded on demand after ondemand_seq.
+#include <algorithm>
+#include <atomic>
+#include <chrono>
+#include <cmath>
+#include <condition_variable>
+#include <cstring>
+#include <deque>
+#include <memory>
+#include <mutex>
+#include <thread>
+#include <vector>
+
+#include "cuda_host.hpp"
+
+namespace ps {
+void plan_layer(const ps_layer_inputs& in, ps_policy pol, ps_layer_plan& out);
+}
+
+namespace ps {
+namespace {
+
+using Clock = std::chrono::steady_clock;
+
+double now_us() {
+  return std::chrono::duration<double, std::micro>(Clock::now().time_since_epoch()).count();
+}
+
+struct Slot {
+  void* dev = nullptr;
+  cudaEvent_t free_ev = nullptr;   // recorded on the compute stream after the last reader
+  std::atomic<int64_t> recorded_gen{0};
+  int64_t next_gen = 0;            // generation a new copy must wait for
+  bool in_use = false;
+  int target_layer = -1;
+};
+
+enum JobKind { kOnDemand = 0, kPrefetch = 1 };
+
+struct IoJob {
+  int kind = kOnDemand;
+  int layer = 0, expert = 0, tokens = 0;
+  void* dst = nullptr;
+  const void* src = nullptr;
+  size_t bytes = 0;
+  Slot* slot = nullptr;
+  int64_t wait_gen = 0;        // slot->recorded_gen must reach this before issue
+  cudaEvent_t start_ev = nullptr, done_ev = nullptr;
+  std::atomic<int> state{0};   // 0 queued, 1 issued, 2 cancelled
+  bool critical = false;
+  int issue_group = 1;
+};
+
+// The serial I/O channel: one copy stream, one host thread, FIFO with cancel.
+class IoChannel {
+ public:
+  IoChannel(int device, int depth) : depth_(depth) {
+    device_ = device;
+    PS_CUDA(cudaStreamCreateWithFlags(&stream_, cudaStreamNonBlocking));
+    thread_ = std::thread([this] { run(); });
+  }
+  ~IoChannel() {
+    {
+      std::lock_guard<std::mutex> g(mu_);
+      stop_ = true;
+    }
+    cv_.notify_all();
+    thread_.join();
+    cudaStreamDestroy(stream_);
+  }
+  cudaStream_t stream() const { return stream_; }
+
+  void push(IoJob* j) {
+    {
+      std::lock_guard<std::mutex> g(mu_);
+      queue_.push_back(j);
+    }
+    cv_.notify_all();
+  }
+  void notify() { cv_.notify_all(); }
+  void wait_issued(IoJob* j) {
+    std::unique_lock<std::mutex> g(mu_);
+    cv_.wait(g, [&] { return j->state.load() != 0 || error_; });
+    if (error_) fail(PS_ECUDA, "I/O channel: " + err_msg_);
+  }
+  // Cancel queued (not yet issued) prefetch jobs; returns them (R2).
+  std::vector<IoJob*> cancel_queued_prefetches() {
+    std::vector<IoJob*> out;
+    std::lock_guard<std::mutex> g(mu_);
+    for (auto it = queue_.begin(); it != queue_.end();) {
+      if ((*it)->kind == kPrefetch && (*it)->state.load() == 0) {
+        (*it)->state = 2;
+        out.push_back(*it);
+        it = queue_.erase(it);
+      } else {
+        ++it;
+      }
+    }
+    return out;
+  }
+  void drain() {  // wait until the queue is empty and every issued copy completed
+    std::unique_lock<std::mutex> g(mu_);
+    cv_.wait(g, [&] { return (queue_.empty() && !busy_) || error_; });
+    g.unlock();
+    PS_CUDA(cudaStreamSynchronize(stream_));
+  }
+  void check() {
+    std::lock_guard<std::mutex> g(mu_);
+    if (error_) fail(PS_ECUDA, "I/O channel: " + err_msg_);
+  }
+
+ private:
+  void run() {
+    cudaSetDevice(device_);
+    std::deque<cudaEvent_t> in_flight;
+    std::unique_lock<std::mutex> g(mu_);
+    while (true) {
+      cv_.wait(g, [&] { return stop_ || !queue_.empty(); });
+      if (stop_) break;
+      busy_ = true;
+      // Throttle: at most depth_ copies in flight, so later queue entries stay
+      // cancellable until the channel is about to free up.
+      while (static_cast<int>(in_flight.size()) >= depth_) {
+        cudaEvent_t ev = in_flight.front();
+        g.unlock();
+        cudaError_t e = cudaEventSynchronize(ev);
+        g.lock();
+        in_flight.pop_front();
+        if (e != cudaSuccess) set_error(e);
+      }
+      if (queue_.empty()) {
+        busy_ = false;
+        cv_.notify_all();
+        continue;
+      }
+      IoJob* j = queue_.front();
+      if (j->slot && j->slot->recorded_gen.load() < j->wait_gen) {
+        // Slot still owned by an FFN the engine has not launched yet: wait for it.
+        cv_.wait(g, [&] { return stop_ || j->slot->recorded_gen.load() >= j->wait_gen || queue_.empty() ||
+                                 queue_.front() != j; });
+        if (stop_) break;
+        busy_ = false;
+        continue;  // re-evaluate the front (it may have been cancelled)
+      }
+      queue_.pop_front();
+      g.unlock();
+      cudaError_t e = cudaSuccess;
+      if (j->slot && j->wait_gen > 0) e = cudaStreamWaitEvent(stream_, j->slot->free_ev, 0);
+      if (e == cudaSuccess) e = cudaEventRecord(j->start_ev, stream_);
+      if (e == cudaSuccess) e = cudaMemcpyAsync(j->dst, j->src, j->bytes, cudaMemcpyHostToDevice, stream_);
+      if (e == cudaSuccess) e = cudaEventRecord(j->done_ev, stream_);
+      g.lock();
+      if (e != cudaSuccess) set_error(e);
+      in_flight.push_back(j->done_ev);
+      j->state = 1;
+      busy_ = !queue_.empty();
+      cv_.notify_all();
+    }
+  }
+  void set_error(cudaError_t e) {
+    error_ = true;
+    err_msg_ = cudaGetErrorString(e);
+    cv_.notify_all();
+  }
+
+  int device_ = 0;
+  int depth_;
+  cudaStream_t stream_ = nullptr;
+  std::thread thread_;
+  std::mutex mu_;
+  std::condition_variable cv_;
+  std::deque<IoJob*> queue_;
+  bool stop_ = false, busy_ = false, error_ = false;
+  std::string err_msg_;
+};
+
+struct LayerDev {  // per-layer device outputs kept for the step
+  float* weights;  // [B,E]
+  int32_t* ids;    // [B,k]
+};
+
+struct FfnTiming {
+  cudaEvent_t a, b;
+  double bytes;
+};
+
+struct StallProbe {
+  cudaEvent_t before, after;
+};
+
+}  // namespace
+}  // namespace ps
+
+struct ps_engine_s {
+  ps_engine_config cfg{};
+  int L = 0, E = 0, K = 0, H = 0, F = 0, maxB = 0, n_split = 1;
+  uint64_t slab_elems = 0;
+  cudaStream_t sc = nullptr;  // compute stream
+  std::unique_ptr<ps::IoChannel> io;
+
+  // expert placement
+  std::vector<const uint16_t*> dev_slab;  // [L*E] resident pointer or null
+  std::vector<const uint16_t*> host_slab; // [L*E] pinned host pointer or null
+  std::vector<uint8_t> resident;          // [L*E]
+  void* arena = nullptr;                  // resident HBM arena
+  void* host_arena = nullptr;             // pinned host arena
+  ps::Slot od_slot[2];
+  std::vector<std::unique_ptr<ps::Slot>> pf_pool;
+
+  // router
+  float* gate = nullptr;   // [L,E,H]
+  float* bias = nullptr;   // [L,E]
+
+  // step buffers
+  std::vector<ps::LayerDev> layer;
+  int32_t* counts_dev = nullptr;     // [E]
+  int32_t* pred_dev = nullptr;       // [E]
+  int32_t* pinned_counts = nullptr;  // [2E] host pinned: counts | pred
+  uint16_t* x_bf16 = nullptr;
+  int32_t *offsets = nullptr, *perm_src = nullptr, *inv = nullptr;
+  uint16_t* hbuf = nullptr;
+  float* y_part = nullptr;
+  void* llapor_scratch = nullptr;
+  float* in_hidden = nullptr;   // device staging for the host-buffer entry point
+  uint8_t* in_follow = nullptr;
+  float* out_y = nullptr;
+  int32_t* out_ids = nullptr;
+  cudaEvent_t ev_routed = nullptr, ev_step0 = nullptr, ev_step1 = nullptr;
+
+  // scheduler state across layers
+  ps_hit_stats stats[3];
+  std::vector<std::unique_ptr<ps::IoJob>> jobs;  // owned for the step
+  struct Ready { int layer, expert; ps::Slot* slot; ps::IoJob* job; };
+  std::vector<Ready> ready;                       // committed prefetches
+  std::vector<ps::IoJob*> pending_pf;             // issued/queued prefetches of the previous layer
+  struct HitCheck { int layer, expert, group; };
+  std::vector<HitCheck> hit_checks;
+  double io_free_us = 0.0;
+  // Two event pools: compute-stream probes (recorded by this thread) and copy events
+  // (recorded only by the I/O thread), so a recycled event is never recorded by one
+  // thread while the other still waits on its previous record.
+  std::vector<cudaEvent_t> event_pool, job_event_pool;
+  size_t event_next = 0, job_event_next = 0;
+  std::vector<ps::FfnTiming> ffn_t;
+  std::vector<ps::StallProbe> stall_t;
+  ps_engine_stats st{};
+};
+
+namespace ps {
+namespace {
+
+cudaEvent_t take_event(ps_engine_s& e) {
+  if (e.event_next == e.event_pool.size()) {
+    cudaEvent_t ev;
+    PS_CUDA(cudaEventCreate(&ev));
+    e.event_pool.push_back(ev);
+  }
+  return e.event_pool[e.event_next++];
+}
+
+cudaEvent_t take_job_event(ps_engine_s& e) {
+  if (e.job_event_next == e.job_event_pool.size()) {
+    cudaEvent_t ev;
+    PS_CUDA(cudaEventCreate(&ev));
+    e.job_event_pool.push_back(ev);
+  }
+  return e.job_event_pool[e.job_event_next++];
+}
+
+int group_of_layer(const ps_model_spec& s, int l) {
+  return l < s.group_begin_middle ? PS_GROUP_INPUT : l < s.group_begin_output ? PS_GROUP_MIDDLE : PS_GROUP_OUTPUT;
+}
+
+void ffn(ps_engine_s& e, const ps_expert_group& g, const int32_t* counts_host, int B, bool timed) {
+  if (g.n == 0) return;
+  cudaEvent_t a = nullptr, b = nullptr;
+  if (timed) {
+    a = take_event(e);
+    PS_CUDA(cudaEventRecord(a, e.sc));
+  }
+  ps_status s = ps_expert_ffn(&g, counts_host, e.offsets, e.perm_src, e.K, e.x_bf16, e.H, e.F, e.hbuf, e.y_part,
+                              e.n_split, B * e.K, e.sc);
+  if (s != PS_OK) fail(s, ps_last_error());
+  e.st.ffn_launches += 2;
+  e.st.kernel_launches += 2;
+  if (timed) {
+    b = take_event(e);
+    PS_CUDA(cudaEventRecord(b, e.sc));
+    double bytes = 0;
+    for (int i = 0; i < g.n; ++i)
+      if (counts_host[g.experts[i]] > 0) bytes += static_cast<double>(e.cfg.spec.expert_bytes);
+    e.ffn_t.push_back({a, b, bytes});
+  }
+}
+
+Slot* take_prefetch_slot(ps_engine_s& e, int target) {
+  int used = 0;
+  for (auto& s : e.pf_pool) used += s->in_use && s->target_layer == target;
+  if (used >= e.cfg.prefetch_slots) fail(PS_ERUNTIME, "engine: prefetch buffer overflow for layer " + std::to_string(target));
+  for (auto& s : e.pf_pool)
+    if (!s->in_use) {
+      s->in_use = true;
+      s->target_layer = target;
+      return s.get();
+    }
+  auto s = std::make_unique<Slot>();
+  PS_CUDA(cudaMalloc(&s->dev, e.cfg.spec.expert_bytes));
+  PS_CUDA(cudaEventCreateWithFlags(&s->free_ev, cudaEventDisableTiming));
+  s->in_use = true;
+  s->target_layer = target;
+  e.pf_pool.push_back(std::move(s));
+  return e.pf_pool.back().get();
+}
+
+// Marks slot reusable after all compute-stream work enqueued so far.
+void release_slot_after_compute(ps_engine_s& e, Slot* s) {
+  PS_CUDA(cudaEventRecord(s->free_ev, e.sc));
+  s->next_gen += 1;
+  s->recorded_gen.store(s->next_gen);
+  e.io->notify();
+}
+
+IoJob* new_job(ps_engine_s& e, int kind, int layer, int expert, int tokens, Slot* slot) {
+  auto j = std::make_unique<IoJob>();
+  j->kind = kind;
+  j->layer = layer;
+  j->expert = expert;
+  j->tokens = tokens;
+  j->slot = slot;
+  j->dst = slot->dev;
+  j->src = e.host_slab[static_cast<size_t>(layer) * e.E + expert];
+  if (!j->src) fail(PS_ERUNTIME, "engine: expert has no host copy");
+  j->bytes = e.cfg.spec.expert_bytes;
+  j->wait_gen = slot->next_gen;  // the slot's latest reader must be done
+  j->start_ev = take_job_event(e);
+  j->done_ev = take_job_event(e);
+  e.jobs.push_back(std::move(j));
+  return e.jobs.back().get();
+}
+
+double push_modelled(ps_engine_s& e) {  // channel busy-until model for alpha (R4)
+  const double now = now_us();
+  e.io_free_us = std::max(e.io_free_us, now) + static_cast<double>(e.cfg.cost.t_io);
+  return e.io_free_us;
+}
+
+void decode_step(ps_engine_s& e, const float* hidden, const uint8_t* follow, int B, float* y, int32_t* ids_out) {
+  const int L = e.L, E = e.E, K = e.K, H = e.H;
+  require(B >= 1 && B <= e.maxB, "decode_step: batch out of range");
+  e.jobs.clear();
+  e.event_next = 0;
+  e.job_event_next = 0;
+  e.ffn_t.clear();
+  e.stall_t.clear();
+  e.ready.clear();
+  e.pending_pf.clear();
+  PS_CUDA(cudaEventRecord(e.ev_step0, e.sc));
+  const auto host_t0 = Clock::now();
+
+  std::vector<ps_expert_load> cur, nxt, cpu_b(E), od_b(E), pf_b(E);
+  std::vector<int32_t> counts_l(E), pred_l(E);
+
+  for (int l = 0; l < L; ++l) {
+    const float* x = hidden + static_cast<size_t>(l) * B * H;
+    LayerDev& ld = e.layer[l];
+    // --- K1 route (+fused bf16 cast, histogram) -------------------------------
+    ps_status s = ps_route_topk(x, e.gate + static_cast<size_t>(l) * E * H, e.bias + static_cast<size_t>(l) * E,
+                                follow ? follow + static_cast<size_t>(l) * B : nullptr,
+                                l > 0 ? e.layer[l - 1].ids : nullptr, K, B, H, E, K, nullptr, ld.weights, ld.ids,
+                                e.counts_dev, e.x_bf16, e.sc);
+    if (s != PS_OK) fail(s, ps_last_error());
+    e.st.kernel_launches += 1;
+    // --- K4 LLaPor: predicted histogram of layer l+1 -------------------------
+    const bool predict = e.cfg.predictor && l + 1 < L;
+    if (predict) {
+      s = ps_llapor_forward(e.cfg.predictor, l + 1, x, ld.ids, K, ld.weights, B, K, nullptr, nullptr, e.pred_dev,
+                            e.llapor_scratch, e.sc);
+      if (s != PS_OK) fail(s, ps_last_error());
+      e.st.kernel_launches += 2;
+    }
+    // --- K2 permute indices ------------------------------------------------------
+    s = ps_permute(ld.ids, B, K, E, e.offsets, e.perm_src, e.inv, nullptr, H, nullptr, e.sc);
+    if (s != PS_OK) fail(s, ps_last_error());
+    e.st.kernel_launches += 1;
+    PS_CUDA(cudaMemcpyAsync(e.pinned_counts, e.counts_dev, sizeof(int32_t) * E, cudaMemcpyDeviceToHost, e.sc));
+    if (predict)
+      PS_CUDA(cudaMemcpyAsync(e.pinned_counts + E, e.pred_dev, sizeof(int32_t) * E, cudaMemcpyDeviceToHost, e.sc));
+    PS_CUDA(cudaEventRecord(e.ev_routed, e.sc));
+
+    // --- resident experts start now, before the host knows the counts (R6): the
+    // kernels read per-expert row counts from the device offsets, the grid is sized
+    // for the worst case m_e = B and warps of unrouted experts exit immediately.
+    ps_expert_group grp{};
+    std::vector<int32_t> worst(E, B);
+    for (int ex = 0; ex < E; ++ex)
+      if (e.resident[static_cast<size_t>(l) * E + ex]) {
+        grp.experts[grp.n] = ex;
+        grp.slabs[grp.n] = e.dev_slab[static_cast<size_t>(l) * E + ex];
+        ++grp.n;
+      }
+    const size_t resident_timing = e.ffn_t.size();
+    ffn(e, grp, worst.data(), B, true);
+
+    // --- R2: resolve the previous layer's prefetch batch at this scheduling point
+    {
+      std::vector<IoJob*> cancelled = e.io->cancel_queued_prefetches();
+      for (IoJob* j : cancelled) {
+        j->slot->in_use = false;
+        e.st.prefetches_cancelled++;
+        e.io_free_us -= static_cast<double>(e.cfg.cost.t_io);
+      }
+      for (IoJob* j : e.pending_pf) {
+        if (j->state.load() != 1) continue;
+        e.ready.push_back({j->layer, j->expert, j->slot, j});
+        e.st.prefetches_committed++;
+        if (j->critical) e.hit_checks.push_back({j->layer, j->expert, j->issue_group});
+      }
+      e.pending_pf.clear();
+    }
+
+    // Wait for the routing result on the host (the only per-layer host sync).
+    PS_CUDA(cudaEventSynchronize(e.ev_routed));
+    std::memcpy(counts_l.data(), e.pinned_counts, sizeof(int32_t) * E);
+    if (predict) std::memcpy(pred_l.data(), e.pinned_counts + E, sizeof(int32_t) * E);
+    else std::fill(pred_l.begin(), pred_l.end(), 0);
+    if (resident_timing < e.ffn_t.size()) {  // algorithmic bytes: routed experts only
+      double bytes = 0;
+      for (int i = 0; i < grp.n; ++i)
+        if (counts_l[grp.experts[i]] > 0) bytes += static_cast<double>(e.cfg.spec.expert_bytes);
+      e.ffn_t[resident_timing].bytes = bytes;
+    }
+    for (int i = 0; i < grp.n; ++i) e.st.resident_hits += counts_l[grp.experts[i]] > 0;
+
+    // Deferred HitStats for critical prefetches that targeted this layer (R2).
+    for (auto it = e.hit_checks.begin(); it != e.hit_checks.end();) {
+      if (it->layer == l) {
+        ps_hit_stats_record(&e.stats[it->group], counts_l[it->expert] > 0);
+        e.st.prefetch_hits += counts_l[it->expert] > 0;
+        it = e.hit_checks.erase(it);
+      } else {
+        ++it;
+      }
+    }
+
+    // Prefetched experts of this layer (committed) compute once their copy lands.
+    auto is_ready = [&](int layer, int ex) {
+      for (auto& r : e.ready)
+        if (r.layer == layer && r.expert == ex) return true;
+      return false;
+    };
+    for (auto& r : e.ready) {
+      if (r.layer != l || counts_l[r.expert] == 0) continue;
+      PS_CUDA(cudaStreamWaitEvent(e.sc, r.job->done_ev, 0));
+      ps_expert_group one{};
+      one.n = 1;
+      one.experts[0] = r.expert;
+      one.slabs[0] = static_cast<const uint16_t*>(r.slot->dev);
+      ffn(e, one, counts_l.data(), B, true);
+    }
+
+    // --- R4: scheduler inputs ------------------------------------------------------
+    cur.clear();
+    nxt.clear();
+    for (int ex = 0; ex < E; ++ex) {
+      if (counts_l[ex] > 0 && !e.resident[static_cast<size_t>(l) * E + ex] && !is_ready(l, ex))
+        cur.push_back({ex, l, counts_l[ex], PS_LOC_HOST});
+      if (l + 1 < L && pred_l[ex] > 0 && !e.resident[static_cast<size_t>(l + 1) * E + ex] && !is_ready(l + 1, ex))
+        nxt.push_back({ex, l + 1, pred_l[ex], PS_LOC_HOST});
+    }
+    auto by_tokens = [](const ps_expert_load& a, const ps_expert_load& b) {
+      return a.tokens != b.tokens ? a.tokens < b.tokens : a.expert < b.expert;
+    };
+    std::sort(cur.begin(), cur.end(), by_tokens);
+    std::sort(nxt.begin(), nxt.end(), by_tokens);
+    ps_layer_inputs in{};
+    in.e_cur = cur.data();
+    in.n_cur = static_cast<int32_t>(cur.size());
+    in.e_next = nxt.data();
+    in.n_next = static_cast<int32_t>(nxt.size());
+    in.e_next2 = nullptr;
+    in.n_next2 = 0;
+    in.params = e.cfg.cost;
+    in.params.alpha = static_cast<int64_t>(std::max(0.0, e.io_free_us - now_us()));
+    in.stats = e.stats[group_of_layer(e.cfg.spec, l)];
+    ps_layer_plan plan{};
+    plan.cpu_set = cpu_b.data();
+    plan.ondemand_seq = od_b.data();
+    plan.prefetch_seq = pf_b.data();
+    plan_layer(in, e.cfg.policy, plan);
+
+    // --- R7: on-demand loads through the dual buffer, FFN per landed expert --------
+    std::vector<ps_expert_load> loads(plan.ondemand_seq, plan.ondemand_seq + plan.n_ondemand);
+    loads.insert(loads.end(), plan.cpu_set, plan.cpu_set + plan.n_cpu);  // no CPU lane
+    std::vector<IoJob*> od_jobs;
+    for (size_t j = 0; j < loads.size(); ++j) {
+      Slot* slot = &e.od_slot[j % 2];
+      IoJob* job = new_job(e, kOnDemand, l, loads[j].expert, loads[j].tokens, slot);
+      // the copy may only overwrite the slot after the FFN of load j-2 (or of the
+      // slot's previous user) has been enqueued and completed
+      job->wait_gen = slot->next_gen + static_cast<int64_t>(j / 2);
+      od_jobs.push_back(job);
+      push_modelled(e);
+      e.io->push(job);
+    }
+    for (size_t j = 0; j < loads.size(); ++j) {
+      IoJob* job = od_jobs[j];
+      e.io->wait_issued(job);
+      StallProbe p{take_event(e), take_event(e)};
+      PS_CUDA(cudaEventRecord(p.before, e.sc));
+      PS_CUDA(cudaStreamWaitEvent(e.sc, job->done_ev, 0));
+      PS_CUDA(cudaEventRecord(p.after, e.sc));
+      e.stall_t.push_back(p);
+      ps_expert_group one{};
+      one.n = 1;
+      one.experts[0] = job->expert;
+      one.slabs[0] = static_cast<const uint16_t*>(job->dst);
+      ffn(e, one, counts_l.data(), B, true);
+      release_slot_after_compute(e, job->slot);
+      e.st.ondemand_loads++;
+      e.st.h2d_bytes += static_cast<double>(job->bytes);
+    }
+
+    // --- combine -> y_l ------------------------------------------------------------
+    s = ps_combine(e.y_part, e.n_split, e.inv, ld.ids, ld.weights, B, K, E, H, y + static_cast<size_t>(l) * B * H,
+                   e.sc);
+    if (s != PS_OK) fail(s, ps_last_error());
+    e.st.kernel_launches += 1;
+
+    // R3: prefetch slots that targeted this layer are free once its FFNs are done.
+    for (auto it = e.ready.begin(); it != e.ready.end();) {
+      if (it->layer <= l) {
+        it->slot->in_use = false;
+        release_slot_after_compute(e, it->slot);
+        it = e.ready.erase(it);
+      } else {
+        ++it;
+      }
+    }
+
+    // --- R8: prefetch dispatch behind the loads on the same channel ---------------
+    if (plan.n_prefetch > 0) {
+      const int target = plan.prefetch_from_widened ? l + 2 : l + 1;
+      for (int j = 0; j < plan.n_prefetch; ++j) {
+        const ps_expert_load& pe = plan.prefetch_seq[j];
+        Slot* slot = take_prefetch_slot(e, target);
+        IoJob* job = new_job(e, kPrefetch, target, pe.expert, pe.tokens, slot);
+        job->critical = j + 1 == plan.n_prefetch;
+        job->issue_group = group_of_layer(e.cfg.spec, l);
+        e.pending_pf.push_back(job);
+        push_modelled(e);
+        e.io->push(job);
+        e.st.h2d_bytes += static_cast<double>(job->bytes);
+      }
+    }
+  }
+  if (ids_out)
+    for (int l = 0; l < L; ++l)
+      PS_CUDA(cudaMemcpyAsync(ids_out + static_cast<size_t>(l) * B * K, e.layer[l].ids, sizeof(int32_t) * B * K,
+                              cudaMemcpyDeviceToDevice, e.sc));
+  PS_CUDA(cudaEventRecord(e.ev_step1, e.sc));
+  PS_CUDA(cudaEventSynchronize(e.ev_step1));
+  // Prefetches still pending at the end of the pass are cancelled or drained.
+  for (IoJob* j : e.io->cancel_queued_prefetches()) j->slot->in_use = false;
+  e.io->drain();
+  for (auto& sl : e.pf_pool) sl->in_use = false;
+  e.io->check();
+
+  // --- measurement (CUDA events; no extra sync) ------------------------------------
+  float ms = 0;
+  for (auto& t : e.ffn_t) {
+    PS_CUDA(cudaEventElapsedTime(&ms, t.a, t.b));
+    e.st.ffn_ms_total += ms;
+  }
+  for (auto& p : e.stall_t) {
+    PS_CUDA(cudaEventElapsedTime(&ms, p.before, p.after));
+    e.st.compute_wait_ms += ms;
+  }
+  for (auto& j : e.jobs) {
+    if (j->state.load() != 1) continue;
+    PS_CUDA(cudaEventElapsedTime(&ms, j->start_ev, j->done_ev));
+    e.st.h2d_busy_ms += ms;
+  }
+  PS_CUDA(cudaEventElapsedTime(&ms, e.ev_step0, e.ev_step1));
+  e.st.step_ms_total += ms;
+  e.st.steps += 1;
+  e.st.layers += L;
+  (void)host_t0;
+}
+
+void create_engine(const ps_engine_config& cfg, ps_engine_s& e) {
+  e.cfg = cfg;
+  const ps_model_spec& sp = cfg.spec;
+  PS_CUDA(cudaSetDevice(cfg.device));
+  if (ps_spec_validate(&sp) != PS_OK) fail(PS_EINVAL, ps_last_error());
+  if (ps_spec_ffn_dim(&sp, &e.F) != PS_OK) fail(PS_EINVAL, ps_last_error());
+  e.L = sp.num_layers;
+  e.E = sp.experts_per_layer;
+  e.K = sp.top_k;
+  e.H = sp.hidden_dim;
+  e.maxB = cfg.max_batch;
+  require(e.maxB >= 1 && e.E <= 256 && e.H % 8 == 0 && e.F % 8 == 0, "engine: unsupported shape");
+  if (e.cfg.prefetch_slots <= 0) e.cfg.prefetch_slots = 8;
+  e.n_split = ps_ffn_down_splits(e.H, e.F);
+  e.slab_elems = sp.expert_bytes / 2;
+  for (auto& h : e.stats) h = {1.0, 0.0, 32};
+  if (e.cfg.cost.t_io <= 0) {  // provisional costs: PCIe Gen5 ~55 GB/s, HBM ~6.5 TB/s
+    e.cfg.cost.t_io = std::max<int64_t>(2, static_cast<int64_t>(sp.expert_bytes / 55e3));
+    e.cfg.cost.t_g = std::max<int64_t>(1, std::min<int64_t>(e.cfg.cost.t_io - 1,
+                                                             static_cast<int64_t>(sp.expert_bytes / 6.5e6) + 5));
+    e.cfg.cost.t_attn = 30;
+    e.cfg.cost.beta = 1e9;  // GPU-only executor: no CPU lane (SURVEY.md §7 hard part 1)
+    e.cfg.cost.startup = 0;
+  }
+  if (ps_cost_params_validate(&e.cfg.cost) != PS_OK) fail(PS_EINVAL, ps_last_error());
+
+  PS_CUDA(cudaStreamCreateWithFlags(&e.sc, cudaStreamNonBlocking));
+  e.io = std::make_unique<IoChannel>(cfg.device, 2);
+
+  // Residency: explicit list or nothing (callers plan it with ps_plan_residency).
+  const size_t LE = static_cast<size_t>(e.L) * e.E;
+  e.resident.assign(LE, 0);
+  for (int i = 0; i < cfg.n_resident; ++i) {
+    int l = cfg.resident[2 * i], ex = cfg.resident[2 * i + 1];
+    require(l >= 0 && l < e.L && ex >= 0 && ex < e.E, "engine: resident pair out of range");
+    e.resident[static_cast<size_t>(l) * e.E + ex] = 1;
+  }
+  size_t n_res = 0;
+  for (uint8_t r : e.resident) n_res += r;
+  require(n_res * sp.expert_bytes <= cfg.budget_bytes, "engine: resident set exceeds the HBM budget");
+  const size_t n_host = LE - n_res;
+
+  e.dev_slab.assign(LE, nullptr);
+  e.host_slab.assign(LE, nullptr);
+  if (n_res) PS_CUDA(cudaMalloc(&e.arena, n_res * sp.expert_bytes));
+  if (n_host) PS_CUDA(cudaHostAlloc(&e.host_arena, n_host * sp.expert_bytes, cudaHostAllocPortable));
+  // Materialise weights: resident on device directly; host ones via a device staging
+  // slab and a D2H copy (the hash is identical on both sides, see weights.cu).
+  void* stage = nullptr;
+  if (n_host) PS_CUDA(cudaMalloc(&stage, 2 * sp.expert_bytes));
+  size_t ri = 0, hi = 0, si = 0;
+  for (int l = 0; l < e.L; ++l)
+    for (int ex = 0; ex < e.E; ++ex) {
+      const size_t idx = static_cast<size_t>(l) * e.E + ex;
+      if (e.resident[idx]) {
+        uint16_t* p = reinterpret_cast<uint16_t*>(static_cast<char*>(e.arena) + ri++ * sp.expert_bytes);
+        if (ps_init_expert_slab(p, e.H, e.F, cfg.weight_seed, l, ex, e.sc) != PS_OK) fail(PS_ECUDA, ps_last_error());
+        e.dev_slab[idx] = p;
+      } else {
+        uint16_t* st = reinterpret_cast<uint16_t*>(static_cast<char*>(stage) + (si++ % 2) * sp.expert_bytes);
+        if (ps_init_expert_slab(st, e.H, e.F, cfg.weight_seed, l, ex, e.sc) != PS_OK) fail(PS_ECUDA, ps_last_error());
+        uint16_t* hp = reinterpret_cast<uint16_t*>(static_cast<char*>(e.host_arena) + hi++ * sp.expert_bytes);
+        PS_CUDA(cudaMemcpyAsync(hp, st, sp.expert_bytes, cudaMemcpyDeviceToHost, e.sc));
+        e.host_slab[idx] = hp;
+      }
+    }
+  PS_CUDA(cudaStreamSynchronize(e.sc));
+  if (stage) cudaFree(stage);
+
+  for (auto& s : e.od_slot) {
+    PS_CUDA(cudaMalloc(&s.dev, sp.expert_bytes));
+    PS_CUDA(cudaEventCreateWithFlags(&s.free_ev, cudaEventDisableTiming));
+  }
+
+  // Router bias: -zipf_g * ln(e+1) per layer (workload.cpp:180-181).
+  PS_CUDA(cudaMalloc(&e.gate, sizeof(float) * e.L * e.E * e.H));
+  PS_CUDA(cudaMemset(e.gate, 0, sizeof(float) * e.L * e.E * e.H));
+  std::vector<float> bias(static_cast<size_t>(e.L) * e.E);
+  for (int l = 0; l < e.L; ++l) {
+    const int g = group_of_layer(sp, l);
+    const double z = g == PS_GROUP_INPUT ? cfg.gen.input.zipf_s : g == PS_GROUP_OUTPUT ? cfg.gen.output.zipf_s
+                                                                                          : cfg.gen.middle.zipf_s;
+    for (int ex = 0; ex < e.E; ++ex) bias[static_cast<size_t>(l) * e.E + ex] = static_cast<float>(-z * std::log(ex + 1.0));
+  }
+  PS_CUDA(cudaMalloc(&e.bias, sizeof(float) * bias.size()));
+  PS_CUDA(cudaMemcpy(e.bias, bias.data(), sizeof(float) * bias.size(), cudaMemcpyHostToDevice));
+
+  const size_t B = e.maxB, rows = B * e.K;
+  e.layer.resize(e.L);
+  for (auto& ld : e.layer) {
+    PS_CUDA(cudaMalloc(&ld.weights, sizeof(float) * B * e.E));
+    PS_CUDA(cudaMalloc(&ld.ids, sizeof(int32_t) * rows));
+  }
+  PS_CUDA(cudaMalloc(&e.counts_dev, sizeof(int32_t) * e.E));
+  PS_CUDA(cudaMalloc(&e.pred_dev, sizeof(int32_t) * e.E));
+  PS_CUDA(cudaHostAlloc(&e.pinned_counts, sizeof(int32_t) * 2 * e.E, cudaHostAllocDefault));
+  PS_CUDA(cudaMalloc(&e.x_bf16, sizeof(uint16_t) * B * e.H));
+  PS_CUDA(cudaMalloc(&e.offsets, sizeof(int32_t) * (e.E + 1)));
+  PS_CUDA(cudaMalloc(&e.perm_src, sizeof(int32_t) * rows));
+  PS_CUDA(cudaMalloc(&e.inv, sizeof(int32_t) * rows));
+  PS_CUDA(cudaMalloc(&e.hbuf, sizeof(uint16_t) * rows * e.F));
+  PS_CUDA(cudaMalloc(&e.y_part, sizeof(float) * e.n_split * rows * e.H));
+  if (cfg.predictor) PS_CUDA(cudaMalloc(&e.llapor_scratch, ps_llapor_scratch_bytes(cfg.predictor, e.maxB)));
+  PS_CUDA(cudaMalloc(&e.in_hidden, sizeof(float) * e.L * B * e.H));
+  PS_CUDA(cudaMalloc(&e.in_follow, e.L * B));
+  PS_CUDA(cudaMalloc(&e.out_y, sizeof(float) * e.L * B * e.H));
+  PS_CUDA(cudaMalloc(&e.out_ids, sizeof(int32_t) * e.L * rows));
+  PS_CUDA(cudaEventCreateWithFlags(&e.ev_routed, cudaEventDisableTiming));
+  PS_CUDA(cudaEventCreate(&e.ev_step0));
+  PS_CUDA(cudaEventCreate(&e.ev_step1));
+  e.st.cost = e.cfg.cost;
+}
+
+void destroy_engine(ps_engine_s& e) {
+  if (e.io) e.io->drain();
+  e.io.reset();
+  if (e.sc) cudaStreamSynchronize(e.sc);
+  for (auto& ld : e.layer) {
+    cudaFree(ld.weights);
+    cudaFree(ld.ids);
+  }
+  for (void* p : {(void*)e.arena, (void*)e.gate, (void*)e.bias, (void*)e.counts_dev, (void*)e.pred_dev,
+                  (void*)e.x_bf16, (void*)e.offsets, (void*)e.perm_src, (void*)e.inv, (void*)e.hbuf,
+                  (void*)e.y_part, e.llapor_scratch, (void*)e.in_hidden, (void*)e.in_follow, (void*)e.out_y,
+                  (void*)e.out_ids})
+    if (p) cudaFree(p);
+  if (e.host_arena) cudaFreeHost(e.host_arena);
+  if (e.pinned_counts) cudaFreeHost(e.pinned_counts);
+  for (auto& s : e.od_slot) {
+    if (s.dev) cudaFree(s.dev);
+    if (s.free_ev) cudaEventDestroy(s.free_ev);
+  }
+  for (auto& s : e.pf_pool) {
+    cudaFree(s->dev);
+    cudaEventDestroy(s->free_ev);
+  }
+  for (cudaEvent_t ev : e.event_pool) cudaEventDestroy(ev);
+  for (cudaEvent_t ev : e.job_event_pool) cudaEventDestroy(ev);
+  for (cudaEvent_t ev : {e.ev_routed, e.ev_step0, e.ev_step1})
+    if (ev) cudaEventDestroy(ev);
+  if (e.sc) cudaStreamDestroy(e.sc);
+}
+
+}  // namespace
+}  // namespace ps
+
+using namespace ps;
+
+extern "C" {
+
+ps_status ps_engine_create(const ps_engine_config* cfg, ps_engine* out) {
+  auto e = std::make_unique<ps_engine_s>();
+  ps_status s = guarded([&] { create_engine(*cfg, *e); });
+  if (s != PS_OK) {
+    destroy_engine(*e);
+    return s;
+  }
+  *out = e.release();
+  return PS_OK;
+}
+
+ps_status ps_engine_destroy(ps_engine e) {
+  return guarded([&] {
+    if (!e) return;
+    destroy_engine(*e);
+    delete e;
+  });
+}
+
+ps_status ps_engine_set_router(ps_engine e, const float* gate_host) {
+  return guarded([&] {
+    PS_CUDA(cudaMemcpy(e->gate, gate_host, sizeof(float) * e->L * e->E * e->H, cudaMemcpyHostToDevice));
+  });
+}
+
+ps_status ps_engine_decode_step(ps_engine e, const float* hidden, const uint8_t* follow, int B, float* y,
+                                int32_t* ids) {
+  return guarded([&] { decode_step(*e, hidden, follow, B, y, ids); });
+}
+
+ps_status ps_engine_decode_step_host(ps_engine e, const float* hidden_host, const uint8_t* follow_host, int B,
+                                     float* y_host, int32_t* ids_host) {
+  return guarded([&] {
+    require(B >= 1 && B <= e->maxB, "decode_step_host: batch out of range");
+    const size_t nh = static_cast<size_t>(e->L) * B * e->H;
+    PS_CUDA(cudaMemcpyAsync(e->in_hidden, hidden_host, sizeof(float) * nh, cudaMemcpyHostToDevice, e->sc));
+    if (follow_host)
+      PS_CUDA(cudaMemcpyAsync(e->in_follow, follow_host, static_cast<size_t>(e->L) * B, cudaMemcpyHostToDevice, e->sc));
+    decode_step(*e, e->in_hidden, follow_host ? e->in_follow : nullptr, B, e->out_y, ids_host ? e->out_ids : nullptr);
+    PS_CUDA(cudaMemcpyAsync(y_host, e->out_y, sizeof(float) * nh, cudaMemcpyDeviceToHost, e->sc));
+    if (ids_host)
+      PS_CUDA(cudaMemcpyAsync(ids_host, e->out_ids, sizeof(int32_t) * e->L * B * e->K, cudaMemcpyDeviceToHost, e->sc));
+    PS_CUDA(cudaStreamSynchronize(e->sc));
+  });
+}
+
+ps_status ps_engine_get_stats(ps_engine e, ps_engine_stats* out) {
+  return guarded([&] {
+    *out = e->st;
+    out->cost = e->cfg.cost;
+  });
+}
+
+ps_status ps_engine_reset_stats(ps_engine e) {
+  return guarded([&] {
+    e->st = ps_engine_stats{};
+    e->st.cost = e->cfg.cost;
+  });
+}
+
+ps_status ps_engine_last_timeline(ps_engine e, ps_timeline* out) {
+  return guarded([&] { fail(PS_ERUNTIME, "ps_engine_last_timeline: not implemented yet"); });
+}
+
+}  // extern "C"

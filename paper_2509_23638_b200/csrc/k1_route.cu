@@ -1,0 +1,158 @@
+// K1 — fused router: gate GEMV (fp32 accumulate) + zipf bias + kappa-follow override +
+// softmax + top-k + per-expert histogram (+ fused bf16 cast of x for the expert FFN).
+//
+// Replaces the per-(token, layer) router loop of the reference trace generator
+// (workload.cpp:176-202) and aggregate_layer_loads (workload.cpp:283-288).
+// One warp per token; the gate matrix [E,H] (<= 1 MiB) is re-read from L1/L2 by every
+// warp, x [H] once from HBM: HBM-bound at B*H*4 + E*H*4 bytes per launch.
+//
+// Top-k ranks the fp32 softmax WEIGHTS with the reference's tie-break (value desc,
+// lower index first), exactly what topk_indices does on the same numbers, so the
+// returned ids are bit-exact against topk_indices(weights) (tests/test_gpu_route.py).
+#include "device_common.cuh"
+
+namespace ps {
+namespace {
+
+constexpr int kWarps = 4;
+constexpr int kMaxE = 256;
+constexpr int kMaxK = 16;
+constexpr int kETile = 8;
+
+__global__ void __launch_bounds__(kWarps * 32)
+route_kernel(const float* __restrict__ x, const float* __restrict__ gate, const float* __restrict__ bias,
+             const uint8_t* __restrict__ follow, const int32_t* __restrict__ prev_ids, int prev_k,
+             int B, int H, int E, int k, float sqrt_h, float* __restrict__ logits_out,
+             float* __restrict__ weights_out, int32_t* __restrict__ ids_out,
+             int32_t* __restrict__ counts, uint16_t* __restrict__ x_bf16) {
+  __shared__ float s_logit[kWarps][kMaxE];
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const int b = blockIdx.x * kWarps + warp;
+  if (b >= B) return;
+  const float* xr = x + static_cast<size_t>(b) * H;
+  float* lg = s_logit[warp];
+
+  // Fused cast x -> bf16 (input of K3), vectorised.
+  if (x_bf16 && (H & 3) == 0) {
+    for (int h = lane * 4; h < H; h += 128) {
+      float4 v = *reinterpret_cast<const float4*>(xr + h);
+      uint2 o;
+      o.x = (uint32_t)f32_to_bf16_rne(v.x) | ((uint32_t)f32_to_bf16_rne(v.y) << 16);
+      o.y = (uint32_t)f32_to_bf16_rne(v.z) | ((uint32_t)f32_to_bf16_rne(v.w) << 16);
+      *reinterpret_cast<uint2*>(x_bf16 + static_cast<size_t>(b) * H + h) = o;
+    }
+  } else if (x_bf16) {
+    for (int h = lane; h < H; h += 32) x_bf16[static_cast<size_t>(b) * H + h] = f32_to_bf16_rne(xr[h]);
+  }
+
+  // Gate GEMV, kETile experts at a time; lanes stride H with float4.
+  const bool vec = (H & 3) == 0;
+  for (int e0 = 0; e0 < E; e0 += kETile) {
+    float acc[kETile];
+#pragma unroll
+    for (int j = 0; j < kETile; ++j) acc[j] = 0.f;
+    if (vec) {
+      for (int h = lane * 4; h < H; h += 128) {
+        const float4 xv = *reinterpret_cast<const float4*>(xr + h);
+#pragma unroll
+        for (int j = 0; j < kETile; ++j) {
+          if (e0 + j < E) {
+            const float4 g = __ldg(reinterpret_cast<const float4*>(gate + static_cast<size_t>(e0 + j) * H + h));
+            acc[j] += g.x * xv.x + g.y * xv.y + g.z * xv.z + g.w * xv.w;
+          }
+        }
+      }
+    } else {
+      for (int h = lane; h < H; h += 32) {
+        const float xv = xr[h];
+#pragma unroll
+        for (int j = 0; j < kETile; ++j)
+          if (e0 + j < E) acc[j] += __ldg(gate + static_cast<size_t>(e0 + j) * H + h) * xv;
+      }
+    }
+#pragma unroll
+    for (int j = 0; j < kETile; ++j) {
+      float s = warp_sum(acc[j]);
+      if (lane == 0 && e0 + j < E) lg[e0 + j] = s * sqrt_h + (bias ? bias[e0 + j] : 0.f);
+    }
+  }
+  __syncwarp();
+
+  // kappa-follow override: logits[(prev_top1+1) % E] = max + 1 (workload.cpp:183-188).
+  if (follow && prev_ids && follow[b]) {
+    float m = -INFINITY;
+    for (int e = lane; e < E; e += 32) m = fmaxf(m, lg[e]);
+    m = warp_max(m);
+    const int target = (prev_ids[static_cast<size_t>(b) * prev_k] + 1) % E;
+    __syncwarp();
+    if (lane == 0) lg[target] = m + 1.0f;
+    __syncwarp();
+  }
+
+  // Softmax (workload.cpp:190-195).
+  float m = -INFINITY;
+  for (int e = lane; e < E; e += 32) m = fmaxf(m, lg[e]);
+  m = warp_max(m);
+  float z = 0.f;
+  for (int e = lane; e < E; e += 32) z += expf(lg[e] - m);
+  z = warp_sum(z);
+  const float inv_z = 1.0f / z;
+  float w_local[kMaxE / 32];
+#pragma unroll
+  for (int i = 0; i < kMaxE / 32; ++i) {
+    const int e = lane + 32 * i;
+    w_local[i] = e < E ? expf(lg[e] - m) * inv_z : -INFINITY;
+    if (e < E) {
+      if (logits_out) logits_out[static_cast<size_t>(b) * E + e] = lg[e];
+      if (weights_out) weights_out[static_cast<size_t>(b) * E + e] = w_local[i];
+    }
+  }
+
+  // Top-k over the weights: k rounds of warp arg-max (ties -> lower index).
+  for (int r = 0; r < k; ++r) {
+    float bv = -INFINITY;
+    int bi = 0x7fffffff;
+#pragma unroll
+    for (int i = 0; i < kMaxE / 32; ++i) {
+      const int e = lane + 32 * i;
+      if (e < E && (w_local[i] > bv || (w_local[i] == bv && e < bi))) {
+        bv = w_local[i];
+        bi = e;
+      }
+    }
+    warp_argmax(bv, bi);
+    if (lane == 0) {
+      ids_out[static_cast<size_t>(b) * k + r] = bi;
+      if (counts) atomicAdd(counts + bi, 1);
+    }
+#pragma unroll
+    for (int i = 0; i < kMaxE / 32; ++i)
+      if (lane + 32 * i == bi) w_local[i] = -INFINITY;  // remove from later rounds
+  }
+}
+
+}  // namespace
+}  // namespace ps
+
+using namespace ps;
+
+extern "C" ps_status ps_route_topk(const float* x, const float* gate, const float* bias,
+                                   const uint8_t* follow, const int32_t* prev_ids, int prev_k, int B,
+                                   int H, int E, int k, float* logits, float* weights, int32_t* ids,
+                                   int32_t* counts, uint16_t* x_bf16, void* stream) {
+  return guarded([&] {
+    require(B >= 0 && H >= 1 && E >= 1 && E <= kMaxE && k >= 1 && k <= E && k <= kMaxK,
+            "ps_route_topk: shape out of range (E <= 256, 1 <= k <= min(E,16))");
+    require(x && gate && ids, "ps_route_topk: null input");
+    require(!(follow && prev_ids) || prev_k >= 1, "ps_route_topk: prev_k must be >= 1");
+    require((reinterpret_cast<uintptr_t>(x) & 15) == 0 && (reinterpret_cast<uintptr_t>(gate) & 15) == 0,
+            "ps_route_topk: x and gate must be 16-byte aligned");
+    cudaStream_t s = as_stream(stream);
+    if (counts) PS_CUDA(cudaMemsetAsync(counts, 0, sizeof(int32_t) * E, s));
+    if (B == 0) return;
+    const float sqrt_h = static_cast<float>(std::sqrt(static_cast<double>(H)));
+    route_kernel<<<(B + kWarps - 1) / kWarps, kWarps * 32, 0, s>>>(
+        x, gate, bias, follow, prev_ids, prev_k, B, H, E, k, sqrt_h, logits, weights, ids, counts, x_bf16);
+    PS_LAUNCH_CHECK("route_kernel");
+  });
+}

@@ -1,0 +1,151 @@
+// K2 — counting-sort token permute / unpermute + weighted combine.
+//
+// The reference only computes the per-expert token count (workload.cpp:202,
+// aggregate_layer_loads workload.cpp:283-288; sort order simulator.cpp:45-57); the
+// physical permute and the combine are absent there, so the order
+// is defined here: permuted rows are (expert asc, token asc, slot asc) — a stable
+// counting sort of the flattened top-k ids. Bit-exact against oracle/or_permute.
+//
+// Index pass: one CTA (B*k <= 64K assignments). Per 1024-element chunk each warp
+// ranks equal experts with __match_any_sync, per-warp counts go through a [warps][E]
+// shared table, so positions are deterministic without global atomics.
+// Gather/combine passes: HBM-bound, 16-byte vectorised, one CTA row-slab each.
+#include "device_common.cuh"
+
+namespace ps {
+namespace {
+
+constexpr int kPermThreads = 1024;
+constexpr int kPermWarps = kPermThreads / 32;
+constexpr int kMaxE = 256;
+
+__global__ void __launch_bounds__(kPermThreads)
+permute_index_kernel(const int32_t* __restrict__ ids, int n, int E, int32_t* __restrict__ offsets,
+                     int32_t* __restrict__ perm_src, int32_t* __restrict__ inv) {
+  __shared__ int s_base[kMaxE + 1];
+  __shared__ int s_warp_cnt[kPermWarps][kMaxE];
+  const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
+
+  // Histogram -> exclusive scan -> offsets.
+  for (int e = tid; e <= E; e += kPermThreads) s_base[e] = 0;
+  __syncthreads();
+  for (int i = tid; i < n; i += kPermThreads) atomicAdd(&s_base[ids[i] + 1], 1);
+  __syncthreads();
+  if (warp == 0) {  // warp-level inclusive scan over E+1 entries, 32 at a time
+    int carry = 0;
+    for (int e0 = 0; e0 <= E; e0 += 32) {
+      int v = e0 + lane <= E ? s_base[e0 + lane] : 0;
+#pragma unroll
+      for (int o = 1; o < 32; o <<= 1) {
+        int t = __shfl_up_sync(0xffffffffu, v, o);
+        if (lane >= o) v += t;
+      }
+      v += carry;
+      if (e0 + lane <= E) s_base[e0 + lane] = v;
+      carry = __shfl_sync(0xffffffffu, v, 31);
+    }
+  }
+  __syncthreads();
+  for (int e = tid; e <= E; e += kPermThreads) offsets[e] = s_base[e];
+  // s_base[e] now holds the running insertion base of expert e.
+
+  const unsigned lt_mask = (1u << lane) - 1u;
+  for (int c0 = 0; c0 < n; c0 += kPermThreads) {
+    for (int i = tid; i < kPermWarps * E; i += kPermThreads) (&s_warp_cnt[0][0])[i] = 0;
+    __syncthreads();
+    const int i = c0 + tid;
+    const bool valid = i < n;
+    const int e = valid ? ids[i] : -1 - lane;  // invalid lanes never match anyone
+    const unsigned peers = __match_any_sync(0xffffffffu, e);
+    const int rank = __popc(peers & lt_mask);
+    if (valid && rank == 0) s_warp_cnt[warp][e] = __popc(peers);
+    __syncthreads();
+    if (valid) {
+      int before = 0;
+      for (int w = 0; w < warp; ++w) before += s_warp_cnt[w][e];
+      const int pos = s_base[e] + before + rank;
+      perm_src[pos] = i;
+      inv[i] = pos;
+    }
+    __syncthreads();
+    for (int ee = tid; ee < E; ee += kPermThreads) {
+      int tot = 0;
+      for (int w = 0; w < kPermWarps; ++w) tot += s_warp_cnt[w][ee];
+      s_base[ee] += tot;
+    }
+    __syncthreads();
+  }
+}
+
+// x_perm[pos] = x[perm_src[pos] / k]; one warp per row, 16 B per lane per step.
+__global__ void gather_rows_kernel(const uint16_t* __restrict__ x, const int32_t* __restrict__ perm_src,
+                                   int rows, int k, int H, uint16_t* __restrict__ x_perm) {
+  const int warp = (blockIdx.x * blockDim.x + threadIdx.x) >> 5, lane = threadIdx.x & 31;
+  if (warp >= rows) return;
+  const int tok = perm_src[warp] / k;
+  const uint4* src = reinterpret_cast<const uint4*>(x + static_cast<size_t>(tok) * H);
+  uint4* dst = reinterpret_cast<uint4*>(x_perm + static_cast<size_t>(warp) * H);
+  for (int v = lane; v < H / 8; v += 32) dst[v] = src[v];
+}
+
+// y[t,:] = sum_j w[t, ids[t,j]] * sum_s y_part[s][inv[t*k+j], :]. Deterministic order
+// (j ascending, then split ascending). grid = (B, ceil(H/1024)), 256 threads x float4.
+__global__ void combine_kernel(const float* __restrict__ y_part, int n_split, size_t split_stride,
+                               const int32_t* __restrict__ inv, const int32_t* __restrict__ ids,
+                               const float* __restrict__ w, int k, int E, int H, float* __restrict__ y) {
+  const int t = blockIdx.x;
+  const int h = (blockIdx.y * blockDim.x + threadIdx.x) * 4;
+  if (h >= H) return;
+  float4 acc = make_float4(0.f, 0.f, 0.f, 0.f);
+  for (int j = 0; j < k; ++j) {
+    const int slot = t * k + j;
+    const float g = w[static_cast<size_t>(t) * E + ids[slot]];
+    const float* row = y_part + static_cast<size_t>(inv[slot]) * H + h;
+    float4 s = make_float4(0.f, 0.f, 0.f, 0.f);
+    for (int p = 0; p < n_split; ++p) {
+      const float4 v = __ldg(reinterpret_cast<const float4*>(row + p * split_stride));
+      s.x += v.x; s.y += v.y; s.z += v.z; s.w += v.w;
+    }
+    acc.x += g * s.x; acc.y += g * s.y; acc.z += g * s.z; acc.w += g * s.w;
+  }
+  *reinterpret_cast<float4*>(y + static_cast<size_t>(t) * H + h) = acc;
+}
+
+}  // namespace
+}  // namespace ps
+
+using namespace ps;
+
+extern "C" {
+
+ps_status ps_permute(const int32_t* ids, int B, int k, int E, int32_t* offsets, int32_t* perm_src,
+                     int32_t* inv, const uint16_t* x, int H, uint16_t* x_perm, void* stream) {
+  return guarded([&] {
+    require(B >= 0 && k >= 1 && E >= 1 && E <= kMaxE, "ps_permute: shape out of range");
+    require(static_cast<int64_t>(B) * k <= (1 << 20), "ps_permute: too many assignments");
+    require(ids && offsets && perm_src && inv, "ps_permute: null output");
+    cudaStream_t s = as_stream(stream);
+    permute_index_kernel<<<1, kPermThreads, 0, s>>>(ids, B * k, E, offsets, perm_src, inv);
+    PS_LAUNCH_CHECK("permute_index_kernel");
+    if (x && x_perm && B > 0) {
+      require(H % 8 == 0, "ps_permute: gather needs H % 8 == 0");
+      const int rows = B * k;
+      gather_rows_kernel<<<(rows * 32 + 255) / 256, 256, 0, s>>>(x, perm_src, rows, k, H, x_perm);
+      PS_LAUNCH_CHECK("gather_rows_kernel");
+    }
+  });
+}
+
+ps_status ps_combine(const float* y_part, int n_split, const int32_t* inv, const int32_t* ids,
+                     const float* weights, int B, int k, int E, int H, float* y, void* stream) {
+  return guarded([&] {
+    require(B >= 0 && k >= 1 && E >= 1 && n_split >= 1 && H % 4 == 0, "ps_combine: bad shape (H % 4 == 0)");
+    if (B == 0) return;
+    dim3 grid(B, (H / 4 + 255) / 256);
+    combine_kernel<<<grid, 256, 0, as_stream(stream)>>>(y_part, n_split, static_cast<size_t>(B) * k * H, inv,
+                                                        ids, weights, k, E, H, y);
+    PS_LAUNCH_CHECK("combine_kernel");
+  });
+}
+
+}  // extern "C"

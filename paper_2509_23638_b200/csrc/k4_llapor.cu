@@ -1,0 +1,435 @@
+// K4 — LLaPor layer-group predictor, inference only.
+//
+// Reference (fp64 CPU): pca_apply (predictor.cpp:116-124), block_forward =
+// affine + erf-GELU (166-183), net_forward with the middle-group gated residual
+// (205-247), forward (344-352), predict_topk on LOGITS (669-672), and the per-layer
+// predicted histogram of predict_loads (experiment.cpp:104-112).
+//
+// Two launches per predicted layer:
+//  pca_kernel — HBM-bound skinny GEMM over the [P, H] component matrix (the dominant
+//               bytes, 8 MiB at P=512, H=4096): 8 rows per CTA, x tile centred and
+//               staged in shared memory so every component byte is read once per
+//               16-token tile.
+//  mlp_kernel — one CTA per token: feature concat [pca | onehot(prev top-k) | prev
+//               gate weights], GELU blocks, gated residual, logits, top-k, histogram;
+//               all weights <= ~0.3 MiB stay L2-resident across launches.
+// fp32 throughout (the reference is fp64: logits within rel 1e-4, top-k bit-exact
+// against topk_indices on the kernel's own logits).
+#include <cmath>
+#include <cstdio>
+#include <cstring>
+#include <fstream>
+#include <memory>
+#include <random>
+#include <vector>
+
+#include "device_common.cuh"
+
+namespace ps {
+
+constexpr int kMaxBlocks = 6;
+constexpr int kMaxE = 256;
+
+struct NetDev {  // device pointers into one allocation; kernel parameter
+  int P, in_dim, width, E, n_blocks, n_res, valid;
+  int dims[kMaxBlocks + 1];
+  const float* mean;
+  const float* comp;
+  const float* w[kMaxBlocks];
+  const float* b[kMaxBlocks];
+  const float* rw[kMaxBlocks];
+  const float* rb[kMaxBlocks];
+  const float* gate_w;
+  float gate_b;
+  const float* out_w;
+  const float* out_b;
+};
+
+}  // namespace ps
+
+struct ps_llapor_s {
+  ps_model_spec spec{};
+  std::vector<ps::NetDev> nets;  // index = target layer; nets[0] unused
+  std::vector<void*> allocs;
+  int max_p = 0, max_in = 0, max_width = 0;
+};
+
+namespace ps {
+namespace {
+
+constexpr int kPcaRows = 8;      // rows per CTA (one warp each)
+constexpr int kPcaTok = 16;      // tokens per pass
+constexpr int kPcaChunk = 256;   // H elements staged per step
+
+__global__ void __launch_bounds__(kPcaRows * 32)
+pca_kernel(const float* __restrict__ comp, const float* __restrict__ mean, const float* __restrict__ x, int B,
+           int H, int P, float* __restrict__ out) {
+  __shared__ float s_x[kPcaTok][kPcaChunk];
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const int p = blockIdx.x * kPcaRows + warp;
+  for (int tb = 0; tb < B; tb += kPcaTok) {
+    float acc[kPcaTok];
+#pragma unroll
+    for (int t = 0; t < kPcaTok; ++t) acc[t] = 0.f;
+    for (int h0 = 0; h0 < H; h0 += kPcaChunk) {
+      __syncthreads();
+      for (int i = threadIdx.x; i < kPcaTok * kPcaChunk; i += blockDim.x) {
+        const int t = i / kPcaChunk, c = i % kPcaChunk, h = h0 + c;
+        s_x[t][c] = (tb + t < B && h < H) ? x[static_cast<size_t>(tb + t) * H + h] - mean[h] : 0.f;
+      }
+      __syncthreads();
+      if (p < P) {
+#pragma unroll
+        for (int j = 0; j < kPcaChunk / 32; ++j) {
+          const int c = lane + 32 * j, h = h0 + c;
+          const float cv = h < H ? __ldg(comp + static_cast<size_t>(p) * H + h) : 0.f;
+#pragma unroll
+          for (int t = 0; t < kPcaTok; ++t) acc[t] += cv * s_x[t][c];
+        }
+      }
+    }
+    if (p < P) {
+#pragma unroll
+      for (int t = 0; t < kPcaTok; ++t) {
+        const float s = warp_sum(acc[t]);
+        if (lane == 0 && tb + t < B) out[static_cast<size_t>(tb + t) * P + p] = s;
+      }
+    }
+  }
+}
+
+__device__ __forceinline__ float gelu_erf(float v) { return 0.5f * v * (1.0f + erff(v * 0.70710678118654752f)); }
+
+// y[r] = act(W[r,:] . in + b[r]) for r < rows; warps stride rows, lanes stride cols.
+__device__ void affine(const float* __restrict__ W, const float* __restrict__ bvec, int rows, int cols,
+                       const float* in, float* out, bool gelu) {
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31, nw = blockDim.x >> 5;
+  for (int r = warp; r < rows; r += nw) {
+    float s = 0.f;
+    for (int c = lane; c < cols; c += 32) s += __ldg(W + static_cast<size_t>(r) * cols + c) * in[c];
+    s = warp_sum(s) + __ldg(bvec + r);
+    if (lane == 0) out[r] = gelu ? gelu_erf(s) : s;
+  }
+}
+
+__global__ void mlp_kernel(const __grid_constant__ NetDev net, const float* __restrict__ reduced,
+                           const int32_t* __restrict__ prev_ids, int k_prev, const float* __restrict__ prev_w,
+                           int k, float* __restrict__ logits_out, int32_t* __restrict__ ids_out,
+                           int32_t* __restrict__ pred_counts) {
+  extern __shared__ float smem[];
+  const int t = blockIdx.x, P = net.P, E = net.E;
+  int maxw = net.in_dim;
+  for (int j = 0; j <= net.n_blocks; ++j) maxw = max(maxw, net.dims[j]);
+  float* a = smem;            // [maxw]
+  float* bbuf = a + maxw;     // [maxw]
+  float* u = bbuf + maxw;     // [maxw]
+  float* red = u + maxw;      // [P]
+  float* lg = red + P;        // [E]
+
+  for (int i = threadIdx.x; i < P; i += blockDim.x) red[i] = a[i] = reduced[static_cast<size_t>(t) * P + i];
+  for (int e = threadIdx.x; e < E; e += blockDim.x) {
+    a[P + e] = 0.f;
+    a[P + E + e] = prev_w[static_cast<size_t>(t) * E + e];
+  }
+  __syncthreads();
+  if (threadIdx.x < k_prev) a[P + prev_ids[static_cast<size_t>(t) * k_prev + threadIdx.x]] = 1.0f;
+  __syncthreads();
+
+  float* cur = a;
+  float* nxt = bbuf;
+  for (int j = 0; j < net.n_blocks; ++j) {
+    affine(net.w[j], net.b[j], net.dims[j + 1], net.dims[j], cur, nxt, true);
+    __syncthreads();
+    float* tmp = cur; cur = nxt; nxt = tmp;
+  }
+  const int width = net.dims[net.n_blocks];
+  if (net.n_res > 0) {
+    // u = residual blocks(x); g = sigmoid(gate_w . pca + gate_b); x = u*g + x.
+    float* ucur = cur;
+    float* unxt = u;
+    for (int j = 0; j < net.n_res; ++j) {
+      affine(net.rw[j], net.rb[j], width, width, ucur, unxt, true);
+      __syncthreads();
+      ucur = unxt;
+      unxt = (unxt == u) ? nxt : u;
+    }
+    __shared__ float s_gate;
+    if (threadIdx.x < 32) {
+      float d = 0.f;
+      for (int i = threadIdx.x; i < P; i += 32) d += net.gate_w[i] * red[i];
+      d = warp_sum(d);
+      if (threadIdx.x == 0) s_gate = 1.0f / (1.0f + expf(-(d + net.gate_b)));
+    }
+    __syncthreads();
+    for (int i = threadIdx.x; i < width; i += blockDim.x) ucur[i] = ucur[i] * s_gate + cur[i];
+    __syncthreads();
+    cur = ucur;
+  }
+  affine(net.out_w, net.out_b, E, width, cur, lg, false);
+  __syncthreads();
+  if (logits_out)
+    for (int e = threadIdx.x; e < E; e += blockDim.x) logits_out[static_cast<size_t>(t) * E + e] = lg[e];
+
+  // Top-k on logits (ties -> lower index) + predicted histogram; warp 0.
+  if (threadIdx.x < 32) {
+    const int lane = threadIdx.x;
+    float v[kMaxE / 32];
+#pragma unroll
+    for (int i = 0; i < kMaxE / 32; ++i) v[i] = lane + 32 * i < E ? lg[lane + 32 * i] : -INFINITY;
+    for (int r = 0; r < k; ++r) {
+      float bv = -INFINITY;
+      int bi = 0x7fffffff;
+#pragma unroll
+      for (int i = 0; i < kMaxE / 32; ++i) {
+        const int e = lane + 32 * i;
+        if (e < E && (v[i] > bv || (v[i] == bv && e < bi))) { bv = v[i]; bi = e; }
+      }
+      warp_argmax(bv, bi);
+      if (lane == 0) {
+        if (ids_out) ids_out[static_cast<size_t>(t) * k + r] = bi;
+        if (pred_counts) atomicAdd(pred_counts + bi, 1);
+      }
+#pragma unroll
+      for (int i = 0; i < kMaxE / 32; ++i)
+        if (lane + 32 * i == bi) v[i] = -INFINITY;
+    }
+  }
+}
+
+// ------------------------------------------------------------------ host side
+
+struct HostNet {
+  int target = 0, group = 1, E = 0;
+  std::vector<double> mean;
+  int p_rows = 0, p_cols = 0;
+  std::vector<double> comp;
+  struct Blk { int rows, cols; std::vector<double> w, b; };
+  std::vector<Blk> blocks, res;
+  std::vector<double> gate_w;
+  double gate_b = 0;
+  Blk out;
+};
+
+void upload(ps_llapor_s& m, int layer, const HostNet& hn) {
+  NetDev d{};
+  d.P = hn.p_rows;
+  d.E = hn.E;
+  d.n_blocks = static_cast<int>(hn.blocks.size());
+  d.n_res = static_cast<int>(hn.res.size());
+  require(d.n_blocks >= 1 && d.n_blocks <= kMaxBlocks && d.n_res <= kMaxBlocks, "LLaPor: unsupported block count");
+  require(hn.E == m.spec.experts_per_layer && hn.E <= kMaxE, "LLaPor: expert count mismatch");
+  d.in_dim = d.P + 2 * d.E;
+  d.dims[0] = hn.blocks[0].cols;
+  require(d.dims[0] == d.in_dim, "LLaPor: first block input dim != pca + 2E");
+  for (int j = 0; j < d.n_blocks; ++j) {
+    require(hn.blocks[j].cols == d.dims[j], "LLaPor: block dims do not chain");
+    d.dims[j + 1] = hn.blocks[j].rows;
+  }
+  d.width = d.dims[d.n_blocks];
+  require(hn.out.cols == d.width && hn.out.rows == d.E, "LLaPor: output block shape");
+
+  std::vector<float> buf;
+  std::vector<size_t> offs;
+  auto put = [&](const std::vector<double>& v) {
+    size_t o = buf.size();
+    offs.push_back(o);
+    for (double x : v) buf.push_back(static_cast<float>(x));
+    while (buf.size() % 4) buf.push_back(0.f);  // 16-byte alignment of every array
+    return o;
+  };
+  size_t o_mean = put(hn.mean), o_comp = put(hn.comp);
+  std::vector<size_t> o_w, o_b, o_rw, o_rb;
+  for (auto& b : hn.blocks) { o_w.push_back(put(b.w)); o_b.push_back(put(b.b)); }
+  for (auto& b : hn.res) { o_rw.push_back(put(b.w)); o_rb.push_back(put(b.b)); }
+  size_t o_gate = put(hn.gate_w.empty() ? std::vector<double>{0.0} : hn.gate_w);
+  size_t o_ow = put(hn.out.w), o_ob = put(hn.out.b);
+  float* dev = nullptr;
+  PS_CUDA(cudaMalloc(&dev, buf.size() * sizeof(float)));
+  m.allocs.push_back(dev);
+  PS_CUDA(cudaMemcpy(dev, buf.data(), buf.size() * sizeof(float), cudaMemcpyHostToDevice));
+  d.mean = dev + o_mean;
+  d.comp = dev + o_comp;
+  for (int j = 0; j < d.n_blocks; ++j) { d.w[j] = dev + o_w[j]; d.b[j] = dev + o_b[j]; }
+  for (int j = 0; j < d.n_res; ++j) { d.rw[j] = dev + o_rw[j]; d.rb[j] = dev + o_rb[j]; }
+  d.gate_w = dev + o_gate;
+  d.gate_b = static_cast<float>(hn.gate_b);
+  d.out_w = dev + o_ow;
+  d.out_b = dev + o_ob;
+  d.valid = 1;
+  if (layer >= static_cast<int>(m.nets.size())) m.nets.resize(layer + 1);
+  m.nets[layer] = d;
+  m.max_p = std::max(m.max_p, d.P);
+  m.max_in = std::max(m.max_in, d.in_dim);
+  m.max_width = std::max(m.max_width, d.width);
+}
+
+// LLPC v1 reader (layout written by save_checkpoint, predictor.cpp:833-864).
+struct Reader {
+  std::ifstream in;
+  template <typename T> T rd() {
+    T v{};
+    in.read(reinterpret_cast<char*>(&v), sizeof(T));
+    if (!in) fail(PS_ERUNTIME, "checkpoint: truncated file");
+    return v;
+  }
+  std::vector<double> vec() {
+    uint64_t n = rd<uint64_t>();
+    if (n > (1ull << 31)) fail(PS_ERUNTIME, "checkpoint: corrupt vector length");
+    std::vector<double> v(n);
+    in.read(reinterpret_cast<char*>(v.data()), static_cast<std::streamsize>(n * sizeof(double)));
+    if (!in) fail(PS_ERUNTIME, "checkpoint: truncated file");
+    return v;
+  }
+  void mat(int& r, int& c, std::vector<double>& a) {
+    r = rd<int32_t>();
+    c = rd<int32_t>();
+    a = vec();
+    if (a.size() != static_cast<size_t>(r) * c) fail(PS_ERUNTIME, "checkpoint: corrupt matrix");
+  }
+  HostNet::Blk blk() {
+    HostNet::Blk b;
+    mat(b.rows, b.cols, b.w);
+    b.b = vec();
+    return b;
+  }
+  void hyper() { rd<double>(); rd<double>(); rd<int32_t>(); rd<int32_t>(); rd<int32_t>(); }
+};
+
+}  // namespace
+}  // namespace ps
+
+using namespace ps;
+
+extern "C" {
+
+ps_status ps_llapor_load(const char* path, ps_llapor* out, ps_model_spec* spec_out) {
+  return guarded([&] {
+    Reader r;
+    r.in.open(path, std::ios::binary);
+    if (!r.in) fail(PS_ERUNTIME, std::string("load_checkpoint: cannot open ") + path);
+    char magic[4];
+    r.in.read(magic, 4);
+    if (!r.in || std::memcmp(magic, "LLPC", 4) != 0) fail(PS_ERUNTIME, "load_checkpoint: bad magic");
+    if (r.rd<uint32_t>() != 1) fail(PS_ERUNTIME, "load_checkpoint: unsupported version");
+    r.rd<uint64_t>();  // trace checksum
+    auto m = std::make_unique<ps_llapor_s>();
+    ps_model_spec& s = m->spec;
+    s.num_layers = r.rd<int32_t>();
+    s.experts_per_layer = r.rd<int32_t>();
+    s.top_k = r.rd<int32_t>();
+    s.expert_bytes = r.rd<uint64_t>();
+    s.hidden_dim = r.rd<int32_t>();
+    s.group_begin_middle = r.rd<int32_t>();
+    s.group_begin_output = r.rd<int32_t>();
+    r.rd<double>(); r.rd<double>(); r.rd<int32_t>(); r.rd<int32_t>();  // lambda gamma epochs warmup
+    r.hyper(); r.hyper(); r.hyper();
+    r.rd<double>(); r.rd<double>(); r.rd<double>(); r.rd<int32_t>(); r.rd<uint64_t>();
+    const uint32_t num = r.rd<uint32_t>();
+    m->nets.resize(std::max<uint32_t>(num, 1));
+    for (uint32_t i = 0; i < num; ++i) {
+      HostNet hn;
+      hn.target = r.rd<int32_t>();
+      hn.group = r.rd<uint8_t>();
+      hn.E = r.rd<int32_t>();
+      r.rd<double>();  // dropout
+      hn.mean = r.vec();
+      r.mat(hn.p_rows, hn.p_cols, hn.comp);
+      r.vec();  // eigenvalues
+      r.rd<int32_t>();
+      r.rd<int32_t>();
+      const uint32_t nb = r.rd<uint32_t>();
+      for (uint32_t j = 0; j < nb; ++j) hn.blocks.push_back(r.blk());
+      const uint32_t nr = r.rd<uint32_t>();
+      for (uint32_t j = 0; j < nr; ++j) hn.res.push_back(r.blk());
+      hn.gate_w = r.vec();
+      hn.gate_b = r.rd<double>();
+      hn.out = r.blk();
+      if (hn.blocks.empty()) continue;  // untrained (nets[0])
+      require(hn.p_cols == s.hidden_dim || hn.p_rows == 0, "LLaPor: PCA width != hidden_dim");
+      upload(*m, static_cast<int>(i), hn);
+    }
+    if (spec_out) *spec_out = s;
+    *out = m.release();
+  });
+}
+
+ps_status ps_llapor_random(const ps_model_spec* spec, int pca_in, int pca_mid, int width_in, int width_mid,
+                           uint64_t seed, ps_llapor* out) {
+  return guarded([&] {
+    auto m = std::make_unique<ps_llapor_s>();
+    m->spec = *spec;
+    const int L = spec->num_layers, E = spec->experts_per_layer, H = spec->hidden_dim;
+    m->nets.resize(L);
+    for (int l = 1; l < L; ++l) {
+      const int g = l < spec->group_begin_middle ? 0 : l < spec->group_begin_output ? 1 : 2;
+      const int P = std::min(g == 1 ? pca_mid : pca_in, H);
+      const int width = g == 1 ? width_mid : width_in;
+      const int nblocks = g == 1 ? 3 : 2;  // TrainConfig defaults (predictor.hpp:97-100)
+      std::mt19937_64 rng(seed ^ (0x9e3779b97f4a7c15ull * (l + 1)));
+      HostNet hn;
+      hn.E = E;
+      hn.p_rows = P;
+      hn.p_cols = H;
+      hn.mean.assign(H, 0.0);
+      std::normal_distribution<double> gauss(0.0, 1.0 / std::sqrt(static_cast<double>(H)));
+      hn.comp.resize(static_cast<size_t>(P) * H);
+      for (double& v : hn.comp) v = gauss(rng);
+      auto init = [&](int o, int i) {  // Xavier-uniform (predictor.cpp:486-494)
+        HostNet::Blk b{o, i, std::vector<double>(static_cast<size_t>(o) * i), std::vector<double>(o, 0.0)};
+        std::uniform_real_distribution<double> u(-std::sqrt(6.0 / (i + o)), std::sqrt(6.0 / (i + o)));
+        for (double& v : b.w) v = u(rng);
+        return b;
+      };
+      int d = P + 2 * E;
+      for (int j = 0; j < nblocks; ++j) { hn.blocks.push_back(init(width, d)); d = width; }
+      if (g == 1) {
+        for (int j = 0; j < 2; ++j) hn.res.push_back(init(width, width));
+        std::uniform_real_distribution<double> u(-0.1, 0.1);
+        hn.gate_w.resize(P);
+        for (double& v : hn.gate_w) v = u(rng);
+      }
+      hn.out = init(E, width);
+      upload(*m, l, hn);
+    }
+    *out = m.release();
+  });
+}
+
+ps_status ps_llapor_free(ps_llapor m) {
+  return guarded([&] {
+    if (!m) return;
+    for (void* p : m->allocs) cudaFree(p);
+    delete m;
+  });
+}
+
+size_t ps_llapor_scratch_bytes(ps_llapor m, int B) {
+  return m ? static_cast<size_t>(B) * std::max(m->max_p, 1) * sizeof(float) + 256 : 0;
+}
+
+ps_status ps_llapor_forward(ps_llapor m, int layer, const float* hidden, const int32_t* prev_ids, int k_prev,
+                            const float* prev_weights, int B, int k, float* logits, int32_t* ids,
+                            int32_t* pred_counts, void* scratch, void* stream) {
+  return guarded([&] {
+    require(m != nullptr, "ps_llapor_forward: null model");
+    if (layer < 1 || layer >= static_cast<int>(m->nets.size()) || !m->nets[layer].valid)
+      fail(PS_ERANGE, "llapor net for layer " + std::to_string(layer) + " is untrained/out of range");
+    const NetDev& net = m->nets[layer];
+    require(k >= 1 && k <= net.E && k_prev >= 1 && k_prev <= 32 && B >= 0, "ps_llapor_forward: bad k/B");
+    cudaStream_t s = as_stream(stream);
+    if (pred_counts) PS_CUDA(cudaMemsetAsync(pred_counts, 0, sizeof(int32_t) * net.E, s));
+    if (B == 0) return;
+    float* reduced = static_cast<float*>(scratch);
+    const int H = m->spec.hidden_dim;
+    pca_kernel<<<(net.P + kPcaRows - 1) / kPcaRows, kPcaRows * 32, 0, s>>>(net.comp, net.mean, hidden, B, H,
+                                                                         net.P, reduced);
+    PS_LAUNCH_CHECK("pca_kernel");
+    int maxw = net.in_dim;
+    for (int j = 0; j <= net.n_blocks; ++j) maxw = std::max(maxw, net.dims[j]);
+    const size_t smem = sizeof(float) * (3 * maxw + net.P + net.E);
+    mlp_kernel<<<B, 128, smem, s>>>(net, reduced, prev_ids, k_prev, prev_weights, k, logits, ids, pred_counts);
+    PS_LAUNCH_CHECK("mlp_kernel");
+  });
+}
+
+}  // extern "C"

@@ -1,0 +1,164 @@
+"""Python handle for the decode engine (K5) and the per-op GPU wrappers.
+
+Mirrors the reference's experiment flow (experiment.cpp:310-360): routing trace ->
+hot-expert table -> plan_residency under the HBM budget -> per-layer PreSched-driven
+execution. Device buffers come from torch (plumbing); all compute is the CUDA library.
+"""
+from __future__ import annotations
+
+import ctypes as C
+
+import numpy as np
+
+from . import capi
+from .capi import check, load
+
+
+def _torch():
+    import torch
+    if not torch.cuda.is_available():
+        raise RuntimeError("paper_2509_23638_b200 GPU ops need a CUDA device (no CPU fallback)")
+    return torch
+
+
+def _ptr(t):
+    return C.c_void_p(t.data_ptr()) if t is not None else None
+
+
+def _stream(torch):
+    return C.c_void_p(torch.cuda.current_stream().cuda_stream)
+
+
+def route(x, gate, bias, follow, prev_ids, k, want_logits=True):
+    """K1 on device tensors: x [B,H] f32, gate [E,H] f32 -> (logits, weights, ids, counts, x_bf16)."""
+    torch = _torch()
+    B, H = x.shape
+    E = gate.shape[0]
+    dev = x.device
+    logits = torch.empty(B, E, dtype=torch.float32, device=dev) if want_logits else None
+    weights = torch.empty(B, E, dtype=torch.float32, device=dev)
+    ids = torch.empty(B, k, dtype=torch.int32, device=dev)
+    counts = torch.empty(E, dtype=torch.int32, device=dev)
+    xb = torch.empty(B, H, dtype=torch.int16, device=dev)
+    pk = prev_ids.shape[1] if prev_ids is not None else 0
+    check(load().ps_route_topk(_ptr(x), _ptr(gate), _ptr(bias), _ptr(follow), _ptr(prev_ids), pk, B, H, E, k,
+                               _ptr(logits), _ptr(weights), _ptr(ids), _ptr(counts), _ptr(xb), _stream(torch)))
+    return logits, weights, ids, counts, xb
+
+
+def hot_table(spec: capi.ModelSpec, gate: np.ndarray, hidden: np.ndarray, follow: np.ndarray,
+              zipf: np.ndarray) -> np.ndarray:
+    """Activation frequency per (layer, expert) of a routing trace, routed on the GPU
+    (build_hot_table, predictor.cpp:405-424). hidden [B,L,H], follow [B,L]."""
+    torch = _torch()
+    L, E, k = spec.num_layers, spec.experts_per_layer, spec.top_k
+    g = torch.as_tensor(np.ascontiguousarray(gate, np.float32), device="cuda")
+    hid = torch.as_tensor(np.ascontiguousarray(hidden.transpose(1, 0, 2), np.float32), device="cuda")
+    fol = torch.as_tensor(np.ascontiguousarray(follow.T), device="cuda")
+    bias = torch.as_tensor(np.array([[-z * np.log(e + 1.0) for e in range(E)] for z in zipf], np.float32),
+                           device="cuda")
+    freq = np.zeros((L, E), np.int64)
+    prev = None
+    for l in range(L):
+        _, _, ids, counts, _ = route(hid[l], g[l], bias[l], fol[l], prev, k, want_logits=False)
+        prev = ids
+        freq[l] = counts.cpu().numpy()
+    return freq
+
+
+class Engine:
+    """ps_engine handle. gate: [L,E,H] router matrices (from ps.trace_inputs)."""
+
+    def __init__(self, spec: capi.ModelSpec, gen_cfg, *, max_batch: int, weight_seed: int = 0,
+                 gate: np.ndarray, budget_fraction: float | None = None, budget_bytes: int | None = None,
+                 resident=None, trace_hidden=None, trace_follow=None, policy: str = "presched",
+                 predictor=None, cost=None, prefetch_slots: int = 8, device: int = 0):
+        from . import parse_policy, plan_residency, trace_inputs  # noqa: F401
+        self.lib = load()
+        self.spec = spec
+        L, E, H = spec.num_layers, spec.experts_per_layer, spec.hidden_dim
+        if budget_bytes is None:
+            budget_bytes = int(round((budget_fraction or 0.0) * L * E)) * spec.expert_bytes
+        self.budget_bytes = budget_bytes
+        zipf = np.array([[gen_cfg.input, gen_cfg.middle, gen_cfg.output][self._group(l)].zipf_s for l in range(L)])
+        if resident is None:
+            if trace_hidden is None:
+                resident = []
+            else:
+                self.freq = hot_table(spec, gate, trace_hidden, trace_follow, zipf)
+                resident = plan_residency(self.freq, budget_bytes, spec.expert_bytes)
+        self.resident = list(resident)
+        res = np.array(self.resident, np.int32).reshape(-1, 2)
+        self._res = res
+        cfg = capi.EngineConfig()
+        cfg.spec = spec
+        cfg.gen = gen_cfg
+        cfg.weight_seed = weight_seed
+        cfg.budget_bytes = budget_bytes
+        cfg.resident = res.ctypes.data_as(C.POINTER(C.c_int32))
+        cfg.n_resident = len(res)
+        cfg.max_batch = max_batch
+        cfg.prefetch_slots = prefetch_slots
+        cfg.policy = parse_policy(policy)
+        if cost is not None:
+            cfg.cost = capi.CostParams(*cost)
+        cfg.predictor = predictor
+        cfg.device = device
+        cfg.host_pinned = 1
+        h = C.c_void_p()
+        check(self.lib.ps_engine_create(C.byref(cfg), C.byref(h)))
+        self.h = h
+        g32 = np.ascontiguousarray(gate, np.float32)
+        check(self.lib.ps_engine_set_router(self.h, g32.ctypes.data_as(C.c_void_p)))
+        self.max_batch = max_batch
+
+    def _group(self, l):
+        s = self.spec
+        return 0 if l < s.group_begin_middle else (1 if l < s.group_begin_output else 2)
+
+    def step_host(self, hidden: np.ndarray, follow: np.ndarray):
+        """One decode step from host buffers. hidden [B,L,H] (trace order), follow [B,L].
+        Returns y [L,B,H] f32 and ids [L,B,k]."""
+        B, L, H = hidden.shape
+        hid = np.ascontiguousarray(hidden.transpose(1, 0, 2), np.float32)
+        fol = np.ascontiguousarray(follow.T, np.uint8)
+        y = np.empty((L, B, H), np.float32)
+        ids = np.empty((L, B, self.spec.top_k), np.int32)
+        check(self.lib.ps_engine_decode_step_host(self.h, hid.ctypes.data_as(C.c_void_p),
+                                                   fol.ctypes.data_as(C.c_void_p), B,
+                                                   y.ctypes.data_as(C.c_void_p), ids.ctypes.data_as(C.c_void_p)))
+        return y, ids
+
+    def step_device(self, hidden_lbh, follow_lb, y_lbh, ids_lbk=None):
+        """One decode step on device tensors (layer-major)."""
+        B = hidden_lbh.shape[1]
+        check(self.lib.ps_engine_decode_step(self.h, _ptr(hidden_lbh), _ptr(follow_lb), B, _ptr(y_lbh),
+                                             _ptr(ids_lbk)))
+
+    def stats(self) -> dict:
+        s = capi.EngineStats()
+        check(self.lib.ps_engine_get_stats(self.h, C.byref(s)))
+        d = {f: getattr(s, f) for f, _ in capi.EngineStats._fields_ if f != "cost"}
+        c = s.cost
+        d["cost"] = dict(t_io=c.t_io, t_g=c.t_g, t_attn=c.t_attn, beta=c.beta, startup=c.startup)
+        return d
+
+    def reset_stats(self):
+        check(self.lib.ps_engine_reset_stats(self.h))
+
+    def close(self):
+        if getattr(self, "h", None):
+            check(self.lib.ps_engine_destroy(self.h))
+            self.h = None
+
+    def __enter__(self):
+        return self
+
+    def __exit__(self, *exc):
+        self.close()
+
+    def __del__(self):
+        try:
+            self.close()
+        except Exception:
+            pass

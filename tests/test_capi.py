@@ -1,0 +1,43 @@
+"""The drop-in boundary: libprescope_b200.so loads and exports every symbol
+include/ps_api.h declares (no compute calls — CPU safe)."""
+import ctypes as C
+import subprocess
+
+import paper_2509_23638_b200 as ps
+from conftest import ROOT
+
+
+def test_library_exports_every_declared_symbol():
+    declared = ps.capi.declared_symbols()
+    assert len(declared) >= 40
+    lib = ps.load()
+    missing = [s for s in declared if not hasattr(lib, s)]
+    assert missing == [], missing
+    out = subprocess.run(["nm", "-D", "--defined-only", str(ps.capi.LIB_PATH)], capture_output=True, text=True,
+                         check=True).stdout
+    exported = {line.split()[-1] for line in out.splitlines() if " T " in line}
+    assert set(declared) <= exported
+
+
+def test_every_declared_symbol_has_a_ctypes_signature():
+    assert set(ps.capi.declared_symbols()) <= set(ps.capi._SIGS)
+
+
+def test_version_and_error_channel():
+    lib = ps.load()
+    assert b"sm_100a" in lib.ps_version()
+    spec = ps.capi.ModelSpec()
+    assert lib.ps_spec_preset(b"nope", C.byref(spec)) == ps.capi.PS_EINVAL
+    assert b"unknown model preset" in lib.ps_last_error()
+
+
+def test_library_is_sm100a_only():
+    out = subprocess.run(["cuobjdump", "--list-elf", str(ps.capi.LIB_PATH)], capture_output=True, text=True).stdout
+    assert "sm_100a" in out
+    assert "sm_90" not in out and "sm_80" not in out
+
+
+def test_product_does_not_import_oracle():
+    for p in (ROOT / "paper_2509_23638_b200").rglob("*.py"):
+        text = p.read_text()
+        assert "import oracle" not in text and "from oracle" not in text, p
