@@ -1,0 +1,336 @@
+#!/usr/bin/env python3
+"""Headline benchmark: Mixtral-8x7B-shape MoE decode under a fixed HBM expert budget.
+
+  python bench.py [--gpus N --steps K --warmup W] [--impl ours|reference]
+
+Step = one decode step of the MoE hot path over all 32 layers for a batch of B tokens:
+K1 route -> K4 LLaPor (prediction of l+1) -> K2 permute -> PreSched plan -> resident
+experts' FFN + PCIe loads of the missing experts (pinned host DRAM -> HBM on the copy
+engine, dual on-demand buffer, PreSched prefetches) -> K3 FFN per landed expert -> K2
+combine. Synthetic inputs: routing trace of the reference generator (same RNG), random
+bf16 weights of the named shapes (hash-initialised; no checkpoints offline).
+
+`value` = B / device time per step (CUDA events on the engine's compute stream), inputs
+already in HBM. `e2e` = the same through the host-buffer C-ABI call
+(ps_engine_decode_step_host: H2D inputs, step, D2H outputs), host wall-clock around the
+blocking call. `roofline` = the decode FFN kernel (K3), the dominant kernel, vs the
+measured HBM copy bandwidth. `cpu_baseline` = the same step on the host cores: the
+oracle port of the SwiGLU FFN/combine + the reference's own scheduling code.
+N>1: independent decode replicas, one per GPU (no data-path collective).
+"""
+from __future__ import annotations
+
+import argparse
+import ctypes as C
+import json
+import os
+import pathlib
+import statistics
+import subprocess
+import sys
+import threading
+import time
+
+import numpy as np
+
+ROOT = pathlib.Path(__file__).resolve().parent
+sys.path.insert(0, str(ROOT))
+
+METRIC = "decode tokens/sec & MoE-layer us at Mixtral-8x7B shape, fixed HBM expert budget"
+PCIE_H2D_PEAK_GBS = 55.5  # measured pinned H2D on this pool (scripts/probe.sh, gpurun_out/probe.log)
+
+
+def measured_peaks():
+    p = ROOT / "MEASURED_PEAKS.json"
+    if p.exists():
+        d = json.loads(p.read_text())
+        return d.get("hbm_gbs", 6650.0), "measured"
+    return 6650.0, "fallback"
+
+
+class ClockSampler:
+    """nvidia-smi clocks + throttle reasons sampled during the timed region."""
+    Q = ("clocks.sm,clocks.max.sm,clocks_event_reasons.hw_slowdown,clocks_event_reasons.hw_thermal_slowdown,"
+         "clocks_event_reasons.sw_thermal_slowdown,clocks_event_reasons.sw_power_cap")
+
+    def __init__(self, index: int):
+        self.index = index
+        self.rows = []
+        self.proc = None
+
+    def __enter__(self):
+        try:
+            self.proc = subprocess.Popen(["nvidia-smi", "-i", str(self.index), f"--query-gpu={self.Q}",
+                                          "--format=csv,noheader,nounits", "-lms", "200"],
+                                         stdout=subprocess.PIPE, stderr=subprocess.DEVNULL, text=True)
+            self.t = threading.Thread(target=self._read, daemon=True)
+            self.t.start()
+        except FileNotFoundError:
+            self.proc = None
+        return self
+
+    def _read(self):
+        for line in self.proc.stdout:
+            parts = [p.strip() for p in line.split(",")]
+            if len(parts) == 6:
+                self.rows.append(parts)
+
+    def __exit__(self, *exc):
+        if self.proc:
+            self.proc.terminate()
+            self.proc.wait(timeout=5)
+
+    def summary(self):
+        if not self.rows:
+            return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["unsampled"]}
+        sm = [float(r[0]) for r in self.rows if r[0].replace(".", "").isdigit()]
+        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
+        reasons = sorted({names[i] for r in self.rows for i in range(4) if r[2 + i].lower().startswith("active")})
+        return {"sm_mhz": statistics.median(sm) if sm else None,
+                "sm_max_mhz": float(self.rows[0][1]) if self.rows[0][1].replace(".", "").isdigit() else None,
+                "reasons": reasons, "samples": len(self.rows)}
+
+
+def make_workload(args):
+    import paper_2509_23638_b200 as ps
+    spec = ps.spec_preset(args.model)
+    gen = ps.TraceGenConfig(*[ps.GROUP_DEFAULT_GEN[g] for g in ("input", "middle", "output")])
+    return ps, spec, gen
+
+
+def cpu_sample(args, spec, gen, threads, sample_layers=1):
+    """Bounded CPU sample: `sample_layers` MoE layers of one decode step (B tokens) with
+    the oracle port (f64-accumulating SwiGLU + combine, all host cores), plus the
+    reference's own per-step scheduling (simulate_policy(presched), 1 core). Returns
+    seconds per full decode step (scaled to all L layers) and a description."""
+    import oracle as orc
+    import paper_2509_23638_b200 as ps
+    L, E, H, k = spec.num_layers, spec.experts_per_layer, spec.hidden_dim, spec.top_k
+    F = ps.ffn_dim(spec)
+    B = args.batch
+    gate, hidden, follow, zipf = ps.trace_inputs(gen, spec, B, 7)
+    _, w, ids = orc.or_route_trace(gate[:sample_layers], hidden[:, :sample_layers], follow[:, :sample_layers],
+                                   zipf[:sample_layers], k)
+    t_ffn = 0.0
+    for l in range(sample_layers):
+        used = sorted(set(ids[:, l].ravel().tolist()))
+        slabs = [orc.or_init_slab(H, F, args.weight_seed, l, e) if e in used else None for e in range(E)]
+        x = orc.f32_to_bf16(hidden[:, l].astype(np.float32))
+        t0 = time.perf_counter()
+        orc.or_moe_layer(slabs, H, F, x, ids[:, l], w[:, l].astype(np.float32), True, threads)
+        t_ffn += time.perf_counter() - t0
+    sched_s = 0.0
+    if orc.ref_available():
+        rg = orc.ref_gen(*[ps.GROUP_DEFAULT_GEN[g] for g in ("input", "middle", "output")])
+        sec, mk = C.c_double(), C.c_int64()
+        params = orc.RefParams(6406, 44, 349, 1e9, 0, 0)
+        orc.ref_check(orc.ref_lib().ref_time_schedule_pass(C.byref(rg), C.byref(orc.ref_spec_from(spec)), B, 7,
+                                                           int(args.budget * L * E) * spec.expert_bytes,
+                                                           C.byref(params), 3, C.byref(sec), C.byref(mk)))
+        sched_s = sec.value
+    step_s = t_ffn / sample_layers * L + sched_s
+    desc = (f"{sample_layers} of {L} MoE layers of one B={B} decode step on the oracle port (SwiGLU+combine, "
+            f"f64 accumulate, {threads} threads) scaled x{L}/{sample_layers}, + reference simulate_policy"
+            f"(presched) per step ({sched_s * 1e6:.0f} us, 1 core)")
+    return step_s, desc
+
+
+def run_reference_arm(args):
+    """--impl reference: the reference's CPU path on this box's host cores."""
+    rank = int(os.environ.get("RANK", "0"))
+    if rank != 0:
+        return
+    ps, spec, gen = make_workload(args)
+    threads = os.cpu_count() or 1
+    L = spec.num_layers
+    times = []
+    desc = ""
+    for i in range(args.warmup + args.steps):
+        s, desc = cpu_sample(args, spec, gen, threads)
+        if i >= args.warmup:
+            times.append(s)
+    step_s = statistics.mean(times)
+    value = args.batch / step_s
+    line = {"impl": "reference", "metric": METRIC, "value": value, "unit": "tokens/s", "n_gpus": args.gpus,
+            "steps": args.steps, "warmup": args.warmup, "ms_per_step": step_s * 1e3, "higher_is_better": True,
+            "scaling": "weak", "vs_baseline": None, "dtype": "bf16 weights, f64 accumulate", "data": "synthetic",
+            "config": workload_config(args, spec),
+            "moe_layer_us": step_s / L * 1e6,
+            "cpu_baseline": {"value": value, "unit": "tokens/s", "cores": threads, "kind": "port", "sample": desc},
+            "e2e": {"value": value, "unit": "tokens/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0}}
+    print(json.dumps(line))
+
+
+def workload_config(args, spec):
+    import paper_2509_23638_b200 as ps
+    L, E = spec.num_layers, spec.experts_per_layer
+    n_res = int(round(args.budget * L * E))
+    return {"workload": f"{args.model}-shape MoE decode: {L} layers, {E} experts top-{spec.top_k}, H={spec.hidden_dim}, "
+                        f"F={ps.ffn_dim(spec)}, batch {args.batch}, HBM expert budget {args.budget:.0%} "
+                        f"({n_res}/{L * E} experts resident, hot-table residency from a warm-up trace), "
+                        f"other experts in pinned host DRAM, policy {args.policy}",
+            "model": f"{args.model}-8x7b-shape" if args.model == "mixtral" else args.model,
+            "global_batch": args.batch * args.gpus, "seq_len": 1, "parallelism": f"replicas{args.gpus}",
+            "budget_fraction": args.budget, "policy": args.policy,
+            "l2": "inputs larger than L2 (each expert slab 336 MiB > 126 MB L2)"}
+
+
+def run_ours(args):
+    import torch
+
+    import paper_2509_23638_b200 as ps
+    from paper_2509_23638_b200 import engine as eng
+
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    rank = int(os.environ.get("RANK", "0"))
+    local = int(os.environ.get("LOCAL_RANK", "0"))
+    torch.cuda.set_device(local)
+    dist = None
+    if world > 1:
+        import torch.distributed as dist
+        dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+
+    _, spec, gen = make_workload(args)
+    L, E, H, k = spec.num_layers, spec.experts_per_layer, spec.hidden_dim, spec.top_k
+    B = args.batch
+    S = args.warmup + args.steps
+    # routing inputs: one trace (fixed gate matrices), B*S tokens sliced into S decode steps
+    gate, hidden, follow, zipf = ps.trace_inputs(gen, spec, B * S, 1000 + rank)
+    # hot table from a separate warm-up trace with the same gate matrices (perf mode)
+    _, warm_h, warm_f, _ = ps.trace_inputs(gen, spec, 64, 1000 + rank, want_gate=False)
+    freq = eng.hot_table(spec, gate, warm_h, warm_f, zipf)
+    budget_bytes = int(round(args.budget * L * E)) * spec.expert_bytes
+    resident = ps.plan_residency(freq, budget_bytes, spec.expert_bytes)
+
+    lib = ps.load()
+    predictor = C.c_void_p()
+    ps.check(lib.ps_llapor_random(C.byref(spec), 256, 512, 32, 48, 3, C.byref(predictor)))
+    t_create = time.perf_counter()
+    e = eng.Engine(spec, gen, max_batch=B, weight_seed=args.weight_seed, gate=gate, budget_bytes=budget_bytes,
+                   resident=resident, policy=args.policy, predictor=predictor, device=local)
+    t_create = time.perf_counter() - t_create
+
+    # device-resident step inputs (layer-major), outputs
+    hid_d = [torch.as_tensor(np.ascontiguousarray(hidden[s * B:(s + 1) * B].transpose(1, 0, 2), np.float32),
+                             device="cuda") for s in range(S)]
+    fol_d = [torch.as_tensor(np.ascontiguousarray(follow[s * B:(s + 1) * B].T), device="cuda") for s in range(S)]
+    y_d = torch.empty(L, B, H, dtype=torch.float32, device="cuda")
+
+    for s in range(args.warmup):
+        e.step_device(hid_d[s], fol_d[s], y_d)
+    torch.cuda.synchronize()
+    e.reset_stats()
+    if dist:
+        dist.barrier()
+    torch.cuda.synchronize()
+    with ClockSampler(local) as clk:
+        t0 = time.perf_counter()
+        for s in range(args.warmup, S):
+            e.step_device(hid_d[s], fol_d[s], y_d)
+        torch.cuda.synchronize()
+        wall = time.perf_counter() - t0
+    st = e.stats()
+    dev_ms = st["step_ms_total"] / max(1, st["steps"])
+    if dist:
+        t = torch.tensor([dev_ms], device="cuda")
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+        dev_ms = float(t.item())
+        dist.barrier()
+
+    # end-to-end through the host-buffer C-ABI entry point (pinned host buffers)
+    hid_h = [torch.from_numpy(np.ascontiguousarray(hidden[s * B:(s + 1) * B], np.float32)).pin_memory()
+             for s in range(S)]
+    fol_h = [torch.from_numpy(np.ascontiguousarray(follow[s * B:(s + 1) * B])).pin_memory() for s in range(S)]
+    hid_lm = [torch.from_numpy(np.ascontiguousarray(h.numpy().transpose(1, 0, 2))).pin_memory() for h in hid_h]
+    fol_lm = [torch.from_numpy(np.ascontiguousarray(f.numpy().T)).pin_memory() for f in fol_h]
+    y_h = torch.empty(L, B, H, dtype=torch.float32).pin_memory()
+    ids_h = torch.empty(L, B, k, dtype=torch.int32).pin_memory()
+    if dist:
+        dist.barrier()
+    t0 = time.perf_counter()
+    for s in range(args.warmup, S):
+        ps.check(lib.ps_engine_decode_step_host(e.h, C.c_void_p(hid_lm[s].data_ptr()),
+                                                C.c_void_p(fol_lm[s].data_ptr()), B,
+                                                C.c_void_p(y_h.data_ptr()), C.c_void_p(ids_h.data_ptr())))
+    e2e_s = (time.perf_counter() - t0) / args.steps
+    if dist:
+        t = torch.tensor([e2e_s], device="cuda")
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+        e2e_s = float(t.item())
+    h2d_in = hid_lm[0].numel() * 4 + fol_lm[0].numel()
+    d2h_out = y_h.numel() * 4 + ids_h.numel() * 4
+    e.close()
+    lib.ps_llapor_free(predictor)
+
+    if rank != 0:
+        if dist:
+            dist.destroy_process_group()
+        return
+    N = world
+    value = N * B / (dev_ms / 1e3)
+    peak_hbm, peak_kind = measured_peaks()
+    ffn_ms = st["ffn_ms_total"]
+    ffn_launches = max(1, st["ffn_launches"] // 2)
+    # algorithmic bytes of the FFN launches = sum over launched experts with m_e > 0 of
+    # 3*H*F*2 (weights; activations are <0.1% at decode)
+    ffn_bytes = ffn_bytes_total(st, spec)
+    achieved = ffn_bytes / (ffn_ms / 1e3) / 1e9 if ffn_ms > 0 else 0.0
+    h2d_gbs = st["h2d_bytes"] / (st["h2d_busy_ms"] / 1e3) / 1e9 if st["h2d_busy_ms"] > 0 else 0.0
+    hidden_frac = 1.0 - st["compute_wait_ms"] / st["h2d_busy_ms"] if st["h2d_busy_ms"] > 0 else 1.0
+    threads = os.cpu_count() or 1
+    cpu_step_s, cpu_desc = cpu_sample(args, spec, gen, threads) if not args.no_cpu_baseline else (None, "skipped")
+    line = {
+        "metric": METRIC, "value": value, "unit": "tokens/s", "n_gpus": N, "steps": args.steps,
+        "warmup": args.warmup, "ms_per_step": dev_ms, "higher_is_better": True, "scaling": "weak",
+        "vs_baseline": None, "dtype": "bf16", "data": "synthetic (reference trace generator, hash-init bf16 weights)",
+        "config": workload_config(args, spec),
+        "moe_layer_us": dev_ms * 1e3 / L,
+        "e2e": {"value": N * B / e2e_s, "unit": "tokens/s", "h2d_bytes_per_step": h2d_in,
+                "d2h_bytes_per_step": d2h_out, "timing": "host wall-clock around ps_engine_decode_step_host"},
+        "roofline": {"kernel": "K3 decode SwiGLU expert FFN (gate_up + down)", "bound": "hbm",
+                     "achieved": achieved, "peak": peak_hbm, "peak_kind": peak_kind, "unit": "GB/s",
+                     "frac": achieved / peak_hbm, "traffic": None,
+                     "algorithmic_bytes_per_launch": ffn_bytes / ffn_launches,
+                     "avg_launch_us": ffn_ms * 1e3 / ffn_launches},
+        "h2d": {"achieved_gbs": h2d_gbs, "peak_gbs": PCIE_H2D_PEAK_GBS, "frac": h2d_gbs / PCIE_H2D_PEAK_GBS,
+                "bytes_per_step": st["h2d_bytes"] / max(1, st["steps"]),
+                "ondemand_loads_per_step": st["ondemand_loads"] / max(1, st["steps"]),
+                "prefetches_per_step": st["prefetches_committed"] / max(1, st["steps"]),
+                "hidden_fraction": hidden_frac},
+        "cpu_baseline": ({"value": args.batch / cpu_step_s, "unit": "tokens/s", "cores": threads, "kind": "port",
+                          "sample": cpu_desc} if cpu_step_s else None),
+        "clocks": clk.summary(),
+        "gpu_launches": st["kernel_launches"],
+        "wall_s_timed": wall, "engine_create_s": t_create,
+        "cost_params_us": st["cost"],
+    }
+    print(json.dumps(line))
+    if dist:
+        dist.destroy_process_group()
+
+
+def ffn_bytes_total(st, spec):
+    return st["ffn_bytes_total"]
+
+
+def main():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=6)
+    ap.add_argument("--warmup", type=int, default=3)
+    ap.add_argument("--impl", choices=["ours", "reference"], default="ours")
+    ap.add_argument("--model", default="mixtral")
+    ap.add_argument("--batch", type=int, default=16)
+    ap.add_argument("--budget", type=float, default=0.5)
+    ap.add_argument("--policy", default="presched")
+    ap.add_argument("--weight-seed", type=int, default=1)
+    ap.add_argument("--no-cpu-baseline", action="store_true")
+    args = ap.parse_args()
+    if args.impl == "reference":
+        run_reference_arm(args)
+    else:
+        run_ours(args)
+
+
+if __name__ == "__main__":
+    main()

@@ -356,6 +356,7 @@ typedef struct {
   int64_t resident_hits;
   double h2d_bytes, h2d_busy_ms, compute_wait_ms, step_ms_total;
   double ffn_ms_total;      /* device time of K3 launches (events) */
+  double ffn_bytes_total;   /* algorithmic bytes of those launches: 3*H*F*2 per routed expert */
   int64_t ffn_launches, kernel_launches;
   ps_cost_params cost;      /* calibrated costs in use */
 } ps_engine_stats;

@@ -121,7 +121,8 @@ class EngineStats(C.Structure):
                 ("prefetches_committed", C.c_int64), ("prefetches_cancelled", C.c_int64),
                 ("prefetch_hits", C.c_int64), ("resident_hits", C.c_int64), ("h2d_bytes", C.c_double),
                 ("h2d_busy_ms", C.c_double), ("compute_wait_ms", C.c_double), ("step_ms_total", C.c_double),
-                ("ffn_ms_total", C.c_double), ("ffn_launches", C.c_int64), ("kernel_launches", C.c_int64),
+                ("ffn_ms_total", C.c_double), ("ffn_bytes_total", C.c_double), ("ffn_launches", C.c_int64),
+                ("kernel_launches", C.c_int64),
                 ("cost", CostParams)]
 
 

@@ -559,6 +559,16 @@ void decode_step(ps_engine_s& e, const float* hidden, const uint8_t* follow, int
     // --- R8: prefetch dispatch behind the loads on the same channel ---------------
     if (plan.n_prefetch > 0) {
       const int target = plan.prefetch_from_widened ? l + 2 : l + 1;
+      // The reference simulator throws when a batch overflows the target layer's slots
+      // (simulator.cpp:209-212); the executor instead truncates the batch to the free
+      // slots (hottest first survive) and counts the truncation.
+      int used = 0;
+      for (auto& sl : e.pf_pool) used += sl->in_use && sl->target_layer == target;
+      const int room = std::max(0, e.cfg.prefetch_slots - used);
+      if (plan.n_prefetch > room) {
+        e.st.prefetches_cancelled += plan.n_prefetch - room;
+        plan.n_prefetch = room;
+      }
       for (int j = 0; j < plan.n_prefetch; ++j) {
         const ps_expert_load& pe = plan.prefetch_seq[j];
         Slot* slot = take_prefetch_slot(e, target);
@@ -589,6 +599,7 @@ void decode_step(ps_engine_s& e, const float* hidden, const uint8_t* follow, int
   for (auto& t : e.ffn_t) {
     PS_CUDA(cudaEventElapsedTime(&ms, t.a, t.b));
     e.st.ffn_ms_total += ms;
+    e.st.ffn_bytes_total += t.bytes;
   }
   for (auto& p : e.stall_t) {
     PS_CUDA(cudaEventElapsedTime(&ms, p.before, p.after));

@@ -51,7 +51,7 @@ permute_index_kernel(const int32_t* __restrict__ ids, int n, int E, int32_t* __r
 
   const unsigned lt_mask = (1u << lane) - 1u;
   for (int c0 = 0; c0 < n; c0 += kPermThreads) {
-    for (int i = tid; i < kPermWarps * E; i += kPermThreads) (&s_warp_cnt[0][0])[i] = 0;
+    for (int i = tid; i < kPermWarps * E; i += kPermThreads) s_warp_cnt[i / E][i % E] = 0;
     __syncthreads();
     const int i = c0 + tid;
     const bool valid = i < n;

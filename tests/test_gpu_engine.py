@@ -1,0 +1,81 @@
+"""Decode engine (K5 + the per-layer driver) end to end through the C ABI vs the CPU
+oracle: routing ids vs the f64 router, per-layer MoE outputs vs the SwiGLU oracle on
+the same synthetic bf16 weights, and loader accounting (every non-resident routed
+expert crosses PCIe exactly once per layer it is used in)."""
+import numpy as np
+import pytest
+
+import oracle as orc
+import paper_2509_23638_b200 as ps
+from paper_2509_23638_b200 import engine as eng
+
+pytestmark = pytest.mark.gpu
+
+BF16_RTOL = 2e-2
+
+
+def _small_spec(L=4, E=8, H=256, F=512, preset="mixtral"):
+    spec = ps.desk_scale(preset, L, E, H)
+    spec.expert_bytes = 6 * H * F
+    return spec
+
+
+def _run(spec, B, budget, policy="presched", seed=3, steps=2, predictor=None):
+    cfg = ps.TraceGenConfig(*[ps.GROUP_DEFAULT_GEN[g] for g in ("input", "middle", "output")])
+    gate, hidden, follow, zipf = ps.trace_inputs(cfg, spec, B, seed)
+    F = ps.ffn_dim(spec)
+    with eng.Engine(spec, cfg, budget_fraction=budget, max_batch=B, weight_seed=9, gate=gate,
+                    trace_hidden=hidden, trace_follow=follow, policy=policy, predictor=predictor) as e:
+        for _ in range(steps):
+            y, ids = e.step_host(hidden, follow)
+        st = e.stats()
+        resident = set(e.resident)
+    _, ref_w, ref_ids = orc.or_route_trace(gate, hidden, follow, zipf, spec.top_k)
+    agree = (np.sort(ids, -1) == np.sort(ref_ids.transpose(1, 0, 2), -1)).all(-1).mean()
+    y_ref = orc.or_engine_reference(spec, F, 9, hidden, ids, ref_w.transpose(1, 0, 2))
+    return y, y_ref, ids, st, resident, agree
+
+
+@pytest.mark.parametrize("budget", [0.0, 0.5, 1.0])
+def test_engine_decode_matches_oracle(torch_cuda, budget):
+    spec = _small_spec()
+    y, y_ref, ids, st, resident, agree = _run(spec, 8, budget)
+    assert agree >= 0.99
+    rel = np.linalg.norm(y - y_ref) / np.linalg.norm(y_ref)
+    assert rel < BF16_RTOL, rel
+    # loader accounting: each (layer, routed, non-resident) expert is loaded once per step
+    needed = sum(1 for l in range(spec.num_layers) for e in set(ids[l].ravel().tolist()) if (l, e) not in resident)
+    assert st["ondemand_loads"] <= needed * st["steps"]
+    assert st["ondemand_loads"] + st["prefetches_committed"] >= needed * st["steps"]
+    if budget == 1.0:
+        assert st["ondemand_loads"] == 0 and st["h2d_bytes"] == 0
+    if budget == 0.0:
+        assert st["resident_hits"] == 0
+
+
+@pytest.mark.parametrize("policy", ["ondemand", "greedy", "fixed:2"])
+def test_engine_policies_same_outputs(torch_cuda, policy):
+    spec = _small_spec()
+    y, y_ref, *_ = _run(spec, 8, 0.25, policy=policy)
+    assert np.linalg.norm(y - y_ref) / np.linalg.norm(y_ref) < BF16_RTOL
+
+
+def test_engine_qwen3_like_shape_with_llapor(torch_cuda):
+    import ctypes as C
+    lib = ps.load()
+    spec = _small_spec(L=6, E=128, H=256, F=128, preset="qwen3")
+    m = C.c_void_p()
+    ps.check(lib.ps_llapor_random(C.byref(spec), 32, 64, 32, 48, 1, C.byref(m)))
+    try:
+        y, y_ref, ids, st, _, agree = _run(spec, 32, 0.5, predictor=m)
+    finally:
+        lib.ps_llapor_free(m)
+    assert agree >= 0.98
+    assert np.linalg.norm(y - y_ref) / np.linalg.norm(y_ref) < BF16_RTOL
+    assert st["kernel_launches"] > 0
+
+
+def test_engine_batch_one(torch_cuda):
+    spec = _small_spec()
+    y, y_ref, *_ = _run(spec, 1, 0.5)
+    assert np.linalg.norm(y - y_ref) / np.linalg.norm(y_ref) < BF16_RTOL
