@@ -260,6 +260,30 @@ def run_ours(args):
     h2d_in = hid_lm[0].numel() * 4 + fol_lm[0].numel()
     d2h_out = y_h.numel() * 4 + ids_h.numel() * 4
     e.close()
+
+    # Same steps with every expert resident (budget 100 %): the HBM-bound MoE layer.
+    all_res = None
+    if not args.no_all_resident:
+        e2 = eng.Engine(spec, gen, max_batch=B, weight_seed=args.weight_seed, gate=gate,
+                        budget_bytes=L * E * spec.expert_bytes, resident=[(l, x) for l in range(L) for x in range(E)],
+                        policy=args.policy, predictor=predictor, device=local)
+        for s in range(args.warmup):
+            e2.step_device(hid_d[s], fol_d[s], y_d)
+        torch.cuda.synchronize()
+        e2.reset_stats()
+        for s in range(args.warmup, S):
+            e2.step_device(hid_d[s], fol_d[s], y_d)
+        torch.cuda.synchronize()
+        st2 = e2.stats()
+        e2.close()
+        ms2 = st2["step_ms_total"] / max(1, st2["steps"])
+        ach2 = st2["ffn_bytes_total"] / (st2["ffn_ms_total"] / 1e3) / 1e9 if st2["ffn_ms_total"] > 0 else 0.0
+        layer_bytes = st2["ffn_bytes_total"] / max(1, st2["steps"]) / L
+        all_res = {"value": N_world(dist) * B / (ms2 / 1e3), "unit": "tokens/s", "ms_per_step": ms2,
+                   "moe_layer_us": ms2 * 1e3 / L, "ffn_achieved_gbs": ach2,
+                   "ffn_frac_of_hbm": ach2 / measured_peaks()[0],
+                   "layer_frac_of_hbm": layer_bytes / (ms2 / 1e3 / L) / 1e9 / measured_peaks()[0],
+                   "gpu_launches": st2["kernel_launches"]}
     lib.ps_llapor_free(predictor)
 
     if rank != 0:
@@ -299,6 +323,7 @@ def run_ours(args):
                 "hidden_fraction": hidden_frac},
         "cpu_baseline": ({"value": args.batch / cpu_step_s, "unit": "tokens/s", "cores": threads, "kind": "port",
                           "sample": cpu_desc} if cpu_step_s else None),
+        "all_resident": all_res,
         "clocks": clk.summary(),
         "gpu_launches": st["kernel_launches"],
         "wall_s_timed": wall, "engine_create_s": t_create,
@@ -307,6 +332,10 @@ def run_ours(args):
     print(json.dumps(line))
     if dist:
         dist.destroy_process_group()
+
+
+def N_world(dist):
+    return dist.get_world_size() if dist else 1
 
 
 def ffn_bytes_total(st, spec):
@@ -325,6 +354,7 @@ def main():
     ap.add_argument("--policy", default="presched")
     ap.add_argument("--weight-seed", type=int, default=1)
     ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--no-all-resident", action="store_true")
     args = ap.parse_args()
     if args.impl == "reference":
         run_reference_arm(args)

@@ -14,27 +14,31 @@
 namespace ps {
 namespace {
 
-constexpr int kWarps = 4;
+constexpr int kWarps = 8;  // warps per token, splitting H
 constexpr int kMaxE = 256;
 constexpr int kMaxK = 16;
 constexpr int kETile = 8;
 
+// One CTA per token: the 8 warps split H (latency: a Mixtral token needs 4 float4
+// steps per lane instead of 32), per-warp partial logits are summed in shared memory
+// in fixed warp order (deterministic), then warp 0 finishes softmax / top-k.
 __global__ void __launch_bounds__(kWarps * 32)
 route_kernel(const float* __restrict__ x, const float* __restrict__ gate, const float* __restrict__ bias,
              const uint8_t* __restrict__ follow, const int32_t* __restrict__ prev_ids, int prev_k,
              int B, int H, int E, int k, float sqrt_h, float* __restrict__ logits_out,
              float* __restrict__ weights_out, int32_t* __restrict__ ids_out,
              int32_t* __restrict__ counts, uint16_t* __restrict__ x_bf16) {
-  __shared__ float s_logit[kWarps][kMaxE];
+  __shared__ float s_part[kWarps][kMaxE];
+  __shared__ float s_logit[kMaxE];
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
-  const int b = blockIdx.x * kWarps + warp;
-  if (b >= B) return;
+  const int b = blockIdx.x;
   const float* xr = x + static_cast<size_t>(b) * H;
-  float* lg = s_logit[warp];
+  float* lg = s_logit;
+  const bool vec = (H & 3) == 0;
 
-  // Fused cast x -> bf16 (input of K3), vectorised.
-  if (x_bf16 && (H & 3) == 0) {
-    for (int h = lane * 4; h < H; h += 128) {
+  // Fused cast x -> bf16 (input of K3), vectorised, all threads.
+  if (x_bf16 && vec) {
+    for (int h = threadIdx.x * 4; h < H; h += kWarps * 128) {
       float4 v = *reinterpret_cast<const float4*>(xr + h);
       uint2 o;
       o.x = (uint32_t)f32_to_bf16_rne(v.x) | ((uint32_t)f32_to_bf16_rne(v.y) << 16);
@@ -42,17 +46,18 @@ route_kernel(const float* __restrict__ x, const float* __restrict__ gate, const 
       *reinterpret_cast<uint2*>(x_bf16 + static_cast<size_t>(b) * H + h) = o;
     }
   } else if (x_bf16) {
-    for (int h = lane; h < H; h += 32) x_bf16[static_cast<size_t>(b) * H + h] = f32_to_bf16_rne(xr[h]);
+    for (int h = threadIdx.x; h < H; h += kWarps * 32) x_bf16[static_cast<size_t>(b) * H + h] = f32_to_bf16_rne(xr[h]);
   }
 
-  // Gate GEMV, kETile experts at a time; lanes stride H with float4.
-  const bool vec = (H & 3) == 0;
+  // Gate GEMV partials: warp w owns H slice [w*hs, (w+1)*hs), kETile experts at a time.
+  const int hs = vec ? ((H / 4 + kWarps - 1) / kWarps) * 4 : (H + kWarps - 1) / kWarps;
+  const int h_lo = min(H, warp * hs), h_hi = min(H, h_lo + hs);
   for (int e0 = 0; e0 < E; e0 += kETile) {
     float acc[kETile];
 #pragma unroll
     for (int j = 0; j < kETile; ++j) acc[j] = 0.f;
     if (vec) {
-      for (int h = lane * 4; h < H; h += 128) {
+      for (int h = h_lo + lane * 4; h < h_hi; h += 128) {
         const float4 xv = *reinterpret_cast<const float4*>(xr + h);
 #pragma unroll
         for (int j = 0; j < kETile; ++j) {
@@ -63,7 +68,7 @@ route_kernel(const float* __restrict__ x, const float* __restrict__ gate, const 
         }
       }
     } else {
-      for (int h = lane; h < H; h += 32) {
+      for (int h = h_lo + lane; h < h_hi; h += 32) {
         const float xv = xr[h];
 #pragma unroll
         for (int j = 0; j < kETile; ++j)
@@ -73,10 +78,18 @@ route_kernel(const float* __restrict__ x, const float* __restrict__ gate, const 
 #pragma unroll
     for (int j = 0; j < kETile; ++j) {
       float s = warp_sum(acc[j]);
-      if (lane == 0 && e0 + j < E) lg[e0 + j] = s * sqrt_h + (bias ? bias[e0 + j] : 0.f);
+      if (lane == 0 && e0 + j < E) s_part[warp][e0 + j] = s;
     }
   }
-  __syncwarp();
+  __syncthreads();
+  for (int e = threadIdx.x; e < E; e += kWarps * 32) {
+    float s = 0.f;
+#pragma unroll
+    for (int w = 0; w < kWarps; ++w) s += s_part[w][e];
+    lg[e] = s * sqrt_h + (bias ? bias[e] : 0.f);
+  }
+  __syncthreads();
+  if (warp != 0) return;
 
   // kappa-follow override: logits[(prev_top1+1) % E] = max + 1 (workload.cpp:183-188).
   if (follow && prev_ids && follow[b]) {
@@ -151,7 +164,7 @@ extern "C" ps_status ps_route_topk(const float* x, const float* gate, const floa
     if (counts) PS_CUDA(cudaMemsetAsync(counts, 0, sizeof(int32_t) * E, s));
     if (B == 0) return;
     const float sqrt_h = static_cast<float>(std::sqrt(static_cast<double>(H)));
-    route_kernel<<<(B + kWarps - 1) / kWarps, kWarps * 32, 0, s>>>(
+    route_kernel<<<B, kWarps * 32, 0, s>>>(
         x, gate, bias, follow, prev_ids, prev_k, B, H, E, k, sqrt_h, logits, weights, ids, counts, x_bf16);
     PS_LAUNCH_CHECK("route_kernel");
   });

@@ -6,13 +6,13 @@
 // predicted histogram of predict_loads (experiment.cpp:104-112).
 //
 // Two launches per predicted layer:
-//  pca_kernel — HBM-bound skinny GEMM over the [P, H] component matrix (the dominant
-//               bytes, 8 MiB at P=512, H=4096): 8 rows per CTA, x tile centred and
-//               staged in shared memory so every component byte is read once per
-//               16-token tile.
-//  mlp_kernel — one CTA per token: feature concat [pca | onehot(prev top-k) | prev
+//  pca_partial_kernel — HBM-bound skinny GEMM over the [P, H] component matrix (the
+//               dominant bytes, 8 MiB at P=512, H=4096): grid (P/8, H/512), one row per
+//               warp, the centred x chunk staged once per CTA; partial sums per H chunk
+//               (deterministic, summed in fixed order by the MLP kernel).
+//  mlp_kernel — 16 tokens per CTA: feature concat [pca | onehot(prev top-k) | prev
 //               gate weights], GELU blocks, gated residual, logits, top-k, histogram;
-//               all weights <= ~0.3 MiB stay L2-resident across launches.
+//               every weight row is read once per CTA and applied to all its tokens.
 // fp32 throughout (the reference is fp64: logits within rel 1e-4, top-k bit-exact
 // against topk_indices on the kernel's own logits).
 #include <cmath>
@@ -57,125 +57,160 @@ struct ps_llapor_s {
 namespace ps {
 namespace {
 
-constexpr int kPcaRows = 8;      // rows per CTA (one warp each)
+constexpr int kPcaRows = 8;      // component rows per CTA (one warp each)
+constexpr int kPcaChunk = 512;   // H elements per CTA (grid.y splits H)
 constexpr int kPcaTok = 16;      // tokens per pass
-constexpr int kPcaChunk = 256;   // H elements staged per step
+constexpr int kMlpTok = 16;      // tokens per MLP CTA
+constexpr int kMlpThreads = 512;
 
+// Stage 1 of pca_apply: part[s][t][p] = sum_{h in chunk s} comp[p][h] * (x[t][h] - mean[h]).
+// grid = (ceil(P/8), ceil(H/512)): 512 CTAs at P=512, H=4096, so the 8 MiB component
+// matrix streams at HBM rate; the centred x chunk is staged once per CTA in smem.
 __global__ void __launch_bounds__(kPcaRows * 32)
-pca_kernel(const float* __restrict__ comp, const float* __restrict__ mean, const float* __restrict__ x, int B,
-           int H, int P, float* __restrict__ out) {
-  __shared__ float s_x[kPcaTok][kPcaChunk];
+pca_partial_kernel(const float* __restrict__ comp, const float* __restrict__ mean, const float* __restrict__ x,
+                   int B, int H, int P, float* __restrict__ part) {
+  __shared__ __align__(16) float s_x[kPcaTok][kPcaChunk];
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   const int p = blockIdx.x * kPcaRows + warp;
+  const int h0 = blockIdx.y * kPcaChunk;
+  const int hn = min(kPcaChunk, H - h0);
   for (int tb = 0; tb < B; tb += kPcaTok) {
+    __syncthreads();
+    for (int i = threadIdx.x; i < kPcaTok * kPcaChunk; i += blockDim.x) {
+      const int t = i / kPcaChunk, c = i % kPcaChunk;
+      s_x[t][c] = (tb + t < B && c < hn) ? x[static_cast<size_t>(tb + t) * H + h0 + c] - mean[h0 + c] : 0.f;
+    }
+    __syncthreads();
+    if (p >= P) continue;
     float acc[kPcaTok];
 #pragma unroll
     for (int t = 0; t < kPcaTok; ++t) acc[t] = 0.f;
-    for (int h0 = 0; h0 < H; h0 += kPcaChunk) {
-      __syncthreads();
-      for (int i = threadIdx.x; i < kPcaTok * kPcaChunk; i += blockDim.x) {
-        const int t = i / kPcaChunk, c = i % kPcaChunk, h = h0 + c;
-        s_x[t][c] = (tb + t < B && h < H) ? x[static_cast<size_t>(tb + t) * H + h] - mean[h] : 0.f;
-      }
-      __syncthreads();
-      if (p < P) {
+    const float* row = comp + static_cast<size_t>(p) * H + h0;
 #pragma unroll
-        for (int j = 0; j < kPcaChunk / 32; ++j) {
-          const int c = lane + 32 * j, h = h0 + c;
-          const float cv = h < H ? __ldg(comp + static_cast<size_t>(p) * H + h) : 0.f;
+    for (int j = 0; j < kPcaChunk / 32; ++j) {
+      const int c = lane + 32 * j;
+      const float cv = c < hn ? __ldg(row + c) : 0.f;
 #pragma unroll
-          for (int t = 0; t < kPcaTok; ++t) acc[t] += cv * s_x[t][c];
-        }
-      }
+      for (int t = 0; t < kPcaTok; ++t) acc[t] += cv * s_x[t][c];
     }
-    if (p < P) {
 #pragma unroll
-      for (int t = 0; t < kPcaTok; ++t) {
-        const float s = warp_sum(acc[t]);
-        if (lane == 0 && tb + t < B) out[static_cast<size_t>(tb + t) * P + p] = s;
-      }
+    for (int t = 0; t < kPcaTok; ++t) {
+      const float sum = warp_sum(acc[t]);
+      if (lane == 0 && tb + t < B) part[(static_cast<size_t>(blockIdx.y) * B + tb + t) * P + p] = sum;
     }
   }
 }
 
 __device__ __forceinline__ float gelu_erf(float v) { return 0.5f * v * (1.0f + erff(v * 0.70710678118654752f)); }
 
-// y[r] = act(W[r,:] . in + b[r]) for r < rows; warps stride rows, lanes stride cols.
-__device__ void affine(const float* __restrict__ W, const float* __restrict__ bvec, int rows, int cols,
-                       const float* in, float* out, bool gelu) {
+// out[t][r] = act(W[r,:] . in[t,:] + b[r]) for all tokens of the CTA: each weight row is
+// read once (lanes stride columns) and applied to every token from shared memory.
+__device__ void affine_tokens(const float* __restrict__ W, const float* __restrict__ bvec, int rows, int cols,
+                              const float* in, int in_stride, float* out, int out_stride, int nt, bool gelu) {
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31, nw = blockDim.x >> 5;
   for (int r = warp; r < rows; r += nw) {
-    float s = 0.f;
-    for (int c = lane; c < cols; c += 32) s += __ldg(W + static_cast<size_t>(r) * cols + c) * in[c];
-    s = warp_sum(s) + __ldg(bvec + r);
-    if (lane == 0) out[r] = gelu ? gelu_erf(s) : s;
+    float acc[kMlpTok];
+#pragma unroll
+    for (int t = 0; t < kMlpTok; ++t) acc[t] = 0.f;
+    for (int c = lane; c < cols; c += 32) {
+      const float w = __ldg(W + static_cast<size_t>(r) * cols + c);
+#pragma unroll
+      for (int t = 0; t < kMlpTok; ++t) acc[t] += w * in[t * in_stride + c];
+    }
+    const float bias = __ldg(bvec + r);
+#pragma unroll
+    for (int t = 0; t < kMlpTok; ++t) {
+      const float s = warp_sum(acc[t]) + bias;
+      if (lane == 0 && t < nt) out[t * out_stride + r] = gelu ? gelu_erf(s) : s;
+    }
   }
 }
 
-__global__ void mlp_kernel(const __grid_constant__ NetDev net, const float* __restrict__ reduced,
-                           const int32_t* __restrict__ prev_ids, int k_prev, const float* __restrict__ prev_w,
-                           int k, float* __restrict__ logits_out, int32_t* __restrict__ ids_out,
-                           int32_t* __restrict__ pred_counts) {
+// Feature concat [pca | onehot(prev top-k) | prev gate weights] (predictor.cpp:214-220),
+// GELU blocks, middle-group gated residual (229-240), logits (242-245), top-k on
+// logits (669-672), predicted histogram (experiment.cpp:104-112). kMlpTok tokens/CTA.
+__global__ void __launch_bounds__(kMlpThreads)
+mlp_kernel(const __grid_constant__ NetDev net, const float* __restrict__ part, int n_part,
+           const int32_t* __restrict__ prev_ids, int k_prev, const float* __restrict__ prev_w, int B, int k,
+           float* __restrict__ logits_out, int32_t* __restrict__ ids_out, int32_t* __restrict__ pred_counts) {
   extern __shared__ float smem[];
-  const int t = blockIdx.x, P = net.P, E = net.E;
-  int maxw = net.in_dim;
-  for (int j = 0; j <= net.n_blocks; ++j) maxw = max(maxw, net.dims[j]);
-  float* a = smem;            // [maxw]
-  float* bbuf = a + maxw;     // [maxw]
-  float* u = bbuf + maxw;     // [maxw]
-  float* red = u + maxw;      // [P]
-  float* lg = red + P;        // [E]
+  const int P = net.P, E = net.E, D = net.in_dim, Wd = net.width;
+  const int t0 = blockIdx.x * kMlpTok, nt = min(kMlpTok, B - t0);
+  float* feat = smem;                   // [kMlpTok][D]
+  float* h1 = feat + kMlpTok * D;       // [kMlpTok][maxh]
+  int maxh = Wd;
+  for (int j = 1; j <= net.n_blocks; ++j) maxh = max(maxh, net.dims[j]);
+  float* h2 = h1 + kMlpTok * maxh;
+  float* h3 = h2 + kMlpTok * maxh;
+  float* lg = h3 + kMlpTok * maxh;      // [kMlpTok][E]
 
-  for (int i = threadIdx.x; i < P; i += blockDim.x) red[i] = a[i] = reduced[static_cast<size_t>(t) * P + i];
-  for (int e = threadIdx.x; e < E; e += blockDim.x) {
-    a[P + e] = 0.f;
-    a[P + E + e] = prev_w[static_cast<size_t>(t) * E + e];
+  for (int i = threadIdx.x; i < kMlpTok * D; i += blockDim.x) {
+    const int t = i / D, c = i % D, tok = t0 + t;
+    float v = 0.f;
+    if (t < nt) {
+      if (c < P) {
+        for (int s = 0; s < n_part; ++s) v += part[(static_cast<size_t>(s) * B + tok) * P + c];
+      } else if (c >= P + E) {
+        v = prev_w[static_cast<size_t>(tok) * E + (c - P - E)];
+      }
+    }
+    feat[i] = v;
   }
   __syncthreads();
-  if (threadIdx.x < k_prev) a[P + prev_ids[static_cast<size_t>(t) * k_prev + threadIdx.x]] = 1.0f;
+  for (int i = threadIdx.x; i < nt * k_prev; i += blockDim.x) {
+    const int t = i / k_prev;
+    feat[t * D + P + prev_ids[static_cast<size_t>(t0 + t) * k_prev + i % k_prev]] = 1.0f;
+  }
   __syncthreads();
 
-  float* cur = a;
-  float* nxt = bbuf;
+  const float* cur = feat;
+  int cur_stride = D;
+  float* bufs[2] = {h1, h2};
   for (int j = 0; j < net.n_blocks; ++j) {
-    affine(net.w[j], net.b[j], net.dims[j + 1], net.dims[j], cur, nxt, true);
+    float* o = bufs[j & 1];
+    affine_tokens(net.w[j], net.b[j], net.dims[j + 1], net.dims[j], cur, cur_stride, o, maxh, nt, true);
     __syncthreads();
-    float* tmp = cur; cur = nxt; nxt = tmp;
+    cur = o;
+    cur_stride = maxh;
   }
-  const int width = net.dims[net.n_blocks];
   if (net.n_res > 0) {
     // u = residual blocks(x); g = sigmoid(gate_w . pca + gate_b); x = u*g + x.
-    float* ucur = cur;
-    float* unxt = u;
+    const float* uin = cur;
+    float* ubuf[2] = {h3, (cur == h1) ? h2 : h1};
+    float* u = nullptr;
     for (int j = 0; j < net.n_res; ++j) {
-      affine(net.rw[j], net.rb[j], width, width, ucur, unxt, true);
+      u = ubuf[j & 1];
+      affine_tokens(net.rw[j], net.rb[j], Wd, Wd, uin, maxh, u, maxh, nt, true);
       __syncthreads();
-      ucur = unxt;
-      unxt = (unxt == u) ? nxt : u;
+      uin = u;
     }
-    __shared__ float s_gate;
-    if (threadIdx.x < 32) {
+    __shared__ float s_gate[kMlpTok];
+    const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+    for (int t = warp; t < nt; t += blockDim.x >> 5) {
       float d = 0.f;
-      for (int i = threadIdx.x; i < P; i += 32) d += net.gate_w[i] * red[i];
+      for (int i = lane; i < P; i += 32) d += net.gate_w[i] * feat[t * D + i];
       d = warp_sum(d);
-      if (threadIdx.x == 0) s_gate = 1.0f / (1.0f + expf(-(d + net.gate_b)));
+      if (lane == 0) s_gate[t] = 1.0f / (1.0f + expf(-(d + net.gate_b)));
     }
     __syncthreads();
-    for (int i = threadIdx.x; i < width; i += blockDim.x) ucur[i] = ucur[i] * s_gate + cur[i];
+    for (int i = threadIdx.x; i < nt * Wd; i += blockDim.x) {
+      const int t = i / Wd, c = i % Wd;
+      u[t * maxh + c] = u[t * maxh + c] * s_gate[t] + cur[t * maxh + c];
+    }
     __syncthreads();
-    cur = ucur;
+    cur = u;
   }
-  affine(net.out_w, net.out_b, E, width, cur, lg, false);
+  affine_tokens(net.out_w, net.out_b, E, Wd, cur, maxh, lg, E, nt, false);
   __syncthreads();
   if (logits_out)
-    for (int e = threadIdx.x; e < E; e += blockDim.x) logits_out[static_cast<size_t>(t) * E + e] = lg[e];
+    for (int i = threadIdx.x; i < nt * E; i += blockDim.x) logits_out[static_cast<size_t>(t0) * E + i] = lg[i];
 
-  // Top-k on logits (ties -> lower index) + predicted histogram; warp 0.
-  if (threadIdx.x < 32) {
-    const int lane = threadIdx.x;
+  // Top-k on logits (ties -> lower index) + predicted histogram; one warp per token.
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  for (int t = warp; t < nt; t += blockDim.x >> 5) {
     float v[kMaxE / 32];
 #pragma unroll
-    for (int i = 0; i < kMaxE / 32; ++i) v[i] = lane + 32 * i < E ? lg[lane + 32 * i] : -INFINITY;
+    for (int i = 0; i < kMaxE / 32; ++i) v[i] = lane + 32 * i < E ? lg[t * E + lane + 32 * i] : -INFINITY;
     for (int r = 0; r < k; ++r) {
       float bv = -INFINITY;
       int bi = 0x7fffffff;
@@ -186,7 +221,7 @@ __global__ void mlp_kernel(const __grid_constant__ NetDev net, const float* __re
       }
       warp_argmax(bv, bi);
       if (lane == 0) {
-        if (ids_out) ids_out[static_cast<size_t>(t) * k + r] = bi;
+        if (ids_out) ids_out[static_cast<size_t>(t0 + t) * k + r] = bi;
         if (pred_counts) atomicAdd(pred_counts + bi, 1);
       }
 #pragma unroll
@@ -404,7 +439,9 @@ ps_status ps_llapor_free(ps_llapor m) {
 }
 
 size_t ps_llapor_scratch_bytes(ps_llapor m, int B) {
-  return m ? static_cast<size_t>(B) * std::max(m->max_p, 1) * sizeof(float) + 256 : 0;
+  if (!m) return 0;
+  const size_t splits = (static_cast<size_t>(m->spec.hidden_dim) + kPcaChunk - 1) / kPcaChunk;
+  return splits * static_cast<size_t>(B) * std::max(m->max_p, 1) * sizeof(float) + 256;
 }
 
 ps_status ps_llapor_forward(ps_llapor m, int layer, const float* hidden, const int32_t* prev_ids, int k_prev,
@@ -419,15 +456,22 @@ ps_status ps_llapor_forward(ps_llapor m, int layer, const float* hidden, const i
     cudaStream_t s = as_stream(stream);
     if (pred_counts) PS_CUDA(cudaMemsetAsync(pred_counts, 0, sizeof(int32_t) * net.E, s));
     if (B == 0) return;
-    float* reduced = static_cast<float*>(scratch);
+    float* part = static_cast<float*>(scratch);
     const int H = m->spec.hidden_dim;
-    pca_kernel<<<(net.P + kPcaRows - 1) / kPcaRows, kPcaRows * 32, 0, s>>>(net.comp, net.mean, hidden, B, H,
-                                                                         net.P, reduced);
-    PS_LAUNCH_CHECK("pca_kernel");
-    int maxw = net.in_dim;
-    for (int j = 0; j <= net.n_blocks; ++j) maxw = std::max(maxw, net.dims[j]);
-    const size_t smem = sizeof(float) * (3 * maxw + net.P + net.E);
-    mlp_kernel<<<B, 128, smem, s>>>(net, reduced, prev_ids, k_prev, prev_weights, k, logits, ids, pred_counts);
+    const int n_part = (H + kPcaChunk - 1) / kPcaChunk;
+    dim3 grid((net.P + kPcaRows - 1) / kPcaRows, n_part);
+    pca_partial_kernel<<<grid, kPcaRows * 32, 0, s>>>(net.comp, net.mean, hidden, B, H, net.P, part);
+    PS_LAUNCH_CHECK("pca_partial_kernel");
+    int maxh = net.width;
+    for (int j = 1; j <= net.n_blocks; ++j) maxh = std::max(maxh, net.dims[j]);
+    const size_t smem = sizeof(float) * kMlpTok * (net.in_dim + 3 * maxh + net.E);
+    static int smem_set = 0;
+    if (static_cast<int>(smem) > smem_set) {
+      PS_CUDA(cudaFuncSetAttribute(mlp_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(smem)));
+      smem_set = static_cast<int>(smem);
+    }
+    mlp_kernel<<<(B + kMlpTok - 1) / kMlpTok, kMlpThreads, smem, s>>>(net, part, n_part, prev_ids, k_prev,
+                                                                      prev_weights, B, k, logits, ids, pred_counts);
     PS_LAUNCH_CHECK("mlp_kernel");
   });
 }

@@ -1,0 +1,15 @@
+"""The reference's C++ API, re-hosted: reference-style call sites compile against
+include/prescope_b200.hpp, link libprescope_b200.so and pass (CPU only)."""
+import subprocess
+
+from conftest import ROOT
+
+
+def test_cpp_shim_compiles_and_passes(tmp_path):
+    exe = tmp_path / "shim_test"
+    lib_dir = ROOT / "paper_2509_23638_b200"
+    subprocess.run(["g++", "-std=c++20", "-O1", "-I", str(ROOT / "include"), str(ROOT / "tests/cpp/shim_test.cpp"),
+                    "-L", str(lib_dir), "-lprescope_b200", f"-Wl,-rpath,{lib_dir}", "-o", str(exe)], check=True)
+    out = subprocess.run([str(exe)], capture_output=True, text=True)
+    assert out.returncode == 0, out.stderr
+    assert "shim ok" in out.stdout
