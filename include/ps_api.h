@@ -280,6 +280,14 @@ ps_status ps_expert_ffn(const ps_expert_group* group, const int32_t* counts_host
                         const int32_t* offsets, const int32_t* perm_src, int k,
                         const uint16_t* x, int H, int F, uint16_t* h, float* y_part,
                         int n_split, int total_rows, void* stream);
+/* K3 prefill path (tensor-bound): tcgen05/TMEM/TMA grouped GEMM over contiguous
+ * permuted rows. x_perm [total_rows, H] bf16 (K2 gather); offsets_host [E+1] / counts_host
+ * [E] are host copies of K2's offsets / K1's histogram. Outputs h_perm [total_rows, F]
+ * bf16 (SwiGLU activations) and y_perm [total_rows, H] f32 (per-row expert output;
+ * combine with ps_combine, n_split = 1). Requires H % 256 == 0, F % 128 == 0. */
+ps_status ps_expert_ffn_prefill(const ps_expert_group* group, const int32_t* counts_host,
+                                const int32_t* offsets_host, const uint16_t* x_perm, int total_rows,
+                                int H, int F, uint16_t* h_perm, float* y_perm, void* stream);
 /* Split-K factor ps_expert_ffn expects for the down projection at this shape. */
 int ps_ffn_down_splits(int H, int F);
 
@@ -357,6 +365,8 @@ typedef struct {
   double h2d_bytes, h2d_busy_ms, compute_wait_ms, step_ms_total;
   double ffn_ms_total;      /* device time of K3 launches (events) */
   double ffn_bytes_total;   /* algorithmic bytes of those launches: 3*H*F*2 per routed expert */
+  double route_phase_ms_total; /* K1 + K4 + K2-index + counts D2H per layer (the scheduling point) */
+  double combine_ms_total;     /* K2 combine */
   int64_t ffn_launches, kernel_launches;
   ps_cost_params cost;      /* calibrated costs in use */
 } ps_engine_stats;

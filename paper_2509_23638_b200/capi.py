@@ -121,7 +121,8 @@ class EngineStats(C.Structure):
                 ("prefetches_committed", C.c_int64), ("prefetches_cancelled", C.c_int64),
                 ("prefetch_hits", C.c_int64), ("resident_hits", C.c_int64), ("h2d_bytes", C.c_double),
                 ("h2d_busy_ms", C.c_double), ("compute_wait_ms", C.c_double), ("step_ms_total", C.c_double),
-                ("ffn_ms_total", C.c_double), ("ffn_bytes_total", C.c_double), ("ffn_launches", C.c_int64),
+                ("ffn_ms_total", C.c_double), ("ffn_bytes_total", C.c_double),
+                ("route_phase_ms_total", C.c_double), ("combine_ms_total", C.c_double), ("ffn_launches", C.c_int64),
                 ("kernel_launches", C.c_int64),
                 ("cost", CostParams)]
 
@@ -168,6 +169,8 @@ _SIGS = {
     "ps_expert_ffn": (C.c_int, [C.POINTER(ExpertGroup), _P, _P, _P, C.c_int, _P, C.c_int, C.c_int, _P, _P,
                                 C.c_int, C.c_int, _P]),
     "ps_ffn_down_splits": (C.c_int, [C.c_int, C.c_int]),
+    "ps_expert_ffn_prefill": (C.c_int, [C.POINTER(ExpertGroup), _P, _P, _P, C.c_int, C.c_int, C.c_int, _P, _P,
+                                        _P]),
     "ps_init_expert_slab": (C.c_int, [_P, C.c_int, C.c_int, C.c_uint64, C.c_int, C.c_int, _P]),
     "ps_init_expert_slab_host": (C.c_int, [_P, C.c_int, C.c_int, C.c_uint64, C.c_int, C.c_int]),
     "ps_llapor_load": (C.c_int, [C.c_char_p, C.POINTER(C.c_void_p), C.POINTER(ModelSpec)]),

@@ -207,6 +207,10 @@ struct StallProbe {
   cudaEvent_t before, after;
 };
 
+struct PhaseTiming {  // scheduling-point phase (K1+K4+K2+D2H) and combine, per layer
+  cudaEvent_t route0, route1, comb0, comb1;
+};
+
 }  // namespace
 }  // namespace ps
 
@@ -262,6 +266,7 @@ struct ps_engine_s {
   size_t event_next = 0, job_event_next = 0;
   std::vector<ps::FfnTiming> ffn_t;
   std::vector<ps::StallProbe> stall_t;
+  std::vector<ps::PhaseTiming> phase_t;
   ps_engine_stats st{};
 };
 
@@ -371,6 +376,7 @@ void decode_step(ps_engine_s& e, const float* hidden, const uint8_t* follow, int
   e.job_event_next = 0;
   e.ffn_t.clear();
   e.stall_t.clear();
+  e.phase_t.clear();
   e.ready.clear();
   e.pending_pf.clear();
   PS_CUDA(cudaEventRecord(e.ev_step0, e.sc));
@@ -382,6 +388,8 @@ void decode_step(ps_engine_s& e, const float* hidden, const uint8_t* follow, int
   for (int l = 0; l < L; ++l) {
     const float* x = hidden + static_cast<size_t>(l) * B * H;
     LayerDev& ld = e.layer[l];
+    PhaseTiming ph{take_event(e), take_event(e), take_event(e), take_event(e)};
+    PS_CUDA(cudaEventRecord(ph.route0, e.sc));
     // --- K1 route (+fused bf16 cast, histogram) -------------------------------
     ps_status s = ps_route_topk(x, e.gate + static_cast<size_t>(l) * E * H, e.bias + static_cast<size_t>(l) * E,
                                 follow ? follow + static_cast<size_t>(l) * B : nullptr,
@@ -405,6 +413,7 @@ void decode_step(ps_engine_s& e, const float* hidden, const uint8_t* follow, int
     if (predict)
       PS_CUDA(cudaMemcpyAsync(e.pinned_counts + E, e.pred_dev, sizeof(int32_t) * E, cudaMemcpyDeviceToHost, e.sc));
     PS_CUDA(cudaEventRecord(e.ev_routed, e.sc));
+    PS_CUDA(cudaEventRecord(ph.route1, e.sc));
 
     // --- resident experts start now, before the host knows the counts (R6): the
     // kernels read per-expert row counts from the device offsets, the grid is sized
@@ -540,9 +549,12 @@ void decode_step(ps_engine_s& e, const float* hidden, const uint8_t* follow, int
     }
 
     // --- combine -> y_l ------------------------------------------------------------
+    PS_CUDA(cudaEventRecord(ph.comb0, e.sc));
     s = ps_combine(e.y_part, e.n_split, e.inv, ld.ids, ld.weights, B, K, E, H, y + static_cast<size_t>(l) * B * H,
                    e.sc);
     if (s != PS_OK) fail(s, ps_last_error());
+    PS_CUDA(cudaEventRecord(ph.comb1, e.sc));
+    e.phase_t.push_back(ph);
     e.st.kernel_launches += 1;
 
     // R3: prefetch slots that targeted this layer are free once its FFNs are done.
@@ -600,6 +612,12 @@ void decode_step(ps_engine_s& e, const float* hidden, const uint8_t* follow, int
     PS_CUDA(cudaEventElapsedTime(&ms, t.a, t.b));
     e.st.ffn_ms_total += ms;
     e.st.ffn_bytes_total += t.bytes;
+  }
+  for (auto& p : e.phase_t) {
+    PS_CUDA(cudaEventElapsedTime(&ms, p.route0, p.route1));
+    e.st.route_phase_ms_total += ms;
+    PS_CUDA(cudaEventElapsedTime(&ms, p.comb0, p.comb1));
+    e.st.combine_ms_total += ms;
   }
   for (auto& p : e.stall_t) {
     PS_CUDA(cudaEventElapsedTime(&ms, p.before, p.after));

@@ -1,0 +1,467 @@
+// K3 (prefill path) — grouped SwiGLU expert FFN on the 5th-generation tensor cores:
+// TMA -> shared memory (128B swizzle, 4-stage mbarrier ring) -> tcgen05.mma (bf16 in,
+// fp32 accumulate in TMEM, M=128 x N=256 per instruction group) -> tcgen05.ld epilogue.
+//
+// Problem (no reference code): for every routed
+// expert e with m_e permuted rows (K2 order, x_perm contiguous):
+//   gate_up:  D[m_e, 2x128 tile] = X_e . [W_gate tile ; W_up tile]^T   (K = H)
+//             epilogue h = SiLU(g) * u  -> bf16 h_perm[row, F]
+//   down:     D[m_e, 256 tile]   = H_e . W_down tile^T                (K = F)
+//             epilogue fp32 y_perm[row, H]   (summed by K2's combine)
+// Both operands are K-major (row-major with K contiguous): the natural TN layout for
+// kind::f16 with a_major = b_major = K.
+//
+// Kernel structure (one persistent CTA per SM, 192 threads, 1 CTA/SM):
+//   warp 0        TMA producer (one elected lane): A box 64x128, B boxes 64x128 (x2) or
+//                 64x256, arrive.expect_tx on the stage's full barrier.
+//   warp 1        MMA issuer (one lane): 4 x tcgen05.mma (K=16) per 64-wide K block,
+//                 tcgen05.commit -> empty barrier (frees the smem stage) and, after the
+//                 last K block, -> tmem_full barrier of the accumulator stage.
+//   warps 2..5    epilogue: tcgen05.ld 32x32b.x32 of its TMEM lane quarter, activation,
+//                 stores; then arrive on tmem_empty (two accumulator stages of 256 fp32
+//                 columns = all 512 TMEM columns, so epilogue of tile i overlaps MMA of
+//                 tile i+1).
+// Tiles are ordered m-fastest within (expert, n-tile) so CTAs working on the same weight
+// tile run concurrently and the B tile is fetched from HBM once, then served by L2.
+#include <cuda.h>
+
+#include <algorithm>
+#include <cstring>
+#include <mutex>
+#include <vector>
+
+#include "device_common.cuh"
+
+namespace ps {
+namespace {
+
+constexpr int kBM = 128;            // tokens per tile (UMMA M)
+constexpr int kBN = 256;            // accumulator columns per tile (UMMA N)
+constexpr int kBK = 64;             // K elements per stage (128 B rows -> 128B swizzle)
+constexpr int kStages = 4;
+constexpr int kThreads = 192;
+constexpr int kABytes = kBM * kBK * 2;         // 16 KiB
+constexpr int kBBytes = kBN * kBK * 2;         // 32 KiB
+constexpr int kStageBytes = kABytes + kBBytes; // 48 KiB
+constexpr int kSmemBytes = kStages * kStageBytes + 1024 /*align*/ + 256 /*barriers*/;
+constexpr int kMaxExperts = 128;
+
+enum Mode { kSwiGLU = 0, kStoreF32 = 1 };
+
+struct PrefillParams {
+  int n_experts;
+  int mode;
+  int K;                     // reduction length (H for gate_up, F for down)
+  int F, H;                  // model dims
+  int n_tiles_n;             // N tiles per expert (F/128 for gate_up, H/256 for down)
+  int tile_start[kMaxExperts + 1];  // prefix of tiles per entry
+  int m_tiles[kMaxExperts];
+  int row0[kMaxExperts];     // first permuted row of the entry
+  int rows[kMaxExperts];     // m_e
+  const CUtensorMap* b_maps; // device array [n_experts] of weight tensor maps
+  void* out;                 // h (bf16, [rows_total, F]) or y (f32, [rows_total, H])
+  int out_ld;                // leading dimension (elements) of out
+};
+
+// ------------------------------------------------------------------ PTX wrappers
+__device__ __forceinline__ uint32_t smem_u32(const void* p) {
+  return static_cast<uint32_t>(__cvta_generic_to_shared(p));
+}
+
+__device__ __forceinline__ void mbar_init(uint64_t* bar, uint32_t count) {
+  asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;" ::"r"(smem_u32(bar)), "r"(count));
+}
+
+__device__ __forceinline__ void mbar_expect_tx(uint64_t* bar, uint32_t bytes) {
+  asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(smem_u32(bar)), "r"(bytes)
+               : "memory");
+}
+
+__device__ __forceinline__ void mbar_arrive(uint64_t* bar) {
+  asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];" ::"r"(smem_u32(bar)) : "memory");
+}
+
+__device__ __forceinline__ void mbar_wait(uint64_t* bar, uint32_t parity) {
+  asm volatile(
+      "{\n"
+      ".reg .pred P1;\n"
+      "LAB_WAIT:\n"
+      "mbarrier.try_wait.parity.shared::cta.b64 P1, [%0], %1;\n"
+      "@P1 bra DONE;\n"
+      "bra LAB_WAIT;\n"
+      "DONE:\n"
+      "}\n" ::"r"(smem_u32(bar)),
+      "r"(parity)
+      : "memory");
+}
+
+__device__ __forceinline__ void tma_load_2d(void* dst, const CUtensorMap* map, uint64_t* bar, int c0, int c1) {
+  asm volatile(
+      "cp.async.bulk.tensor.2d.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1, {%2, %3}], [%4];" ::"r"(
+          smem_u32(dst)),
+      "l"(map), "r"(c0), "r"(c1), "r"(smem_u32(bar))
+      : "memory");
+}
+
+__device__ __forceinline__ void prefetch_map(const CUtensorMap* map) {
+  asm volatile("prefetch.tensormap [%0];" ::"l"(map) : "memory");
+}
+
+// UMMA shared-memory descriptor, K-major, SWIZZLE_128B: start>>4 [0,14), LBO>>4
+// [16,30) (unused for swizzled K-major, 1 as in CUTLASS), SBO>>4 [32,46) = 1024 B
+// between 8-row atoms, version 1 [46,48), layout 2 = SWIZZLE_128B [61,64).
+__device__ __forceinline__ uint64_t make_desc(uint32_t smem_addr) {
+  uint64_t d = 0;
+  d |= static_cast<uint64_t>((smem_addr >> 4) & 0x3fff);
+  d |= static_cast<uint64_t>(1) << 16;
+  d |= static_cast<uint64_t>(1024 >> 4) << 32;
+  d |= static_cast<uint64_t>(1) << 46;
+  d |= static_cast<uint64_t>(2) << 61;
+  return d;
+}
+
+// Instruction descriptor kind::f16: D=f32 [4,6), A=B=bf16 [7,10)/[10,13), K-major,
+// N>>3 [17,23), M>>4 [24,29).
+constexpr uint32_t kIdesc = (1u << 4) | (1u << 7) | (1u << 10) | (static_cast<uint32_t>(kBN >> 3) << 17) |
+                            (static_cast<uint32_t>(kBM >> 4) << 24);
+
+__device__ __forceinline__ void umma_f16(uint32_t tmem_d, uint64_t adesc, uint64_t bdesc, uint32_t accumulate) {
+  asm volatile(
+      "{\n"
+      ".reg .pred p;\n"
+      "setp.ne.b32 p, %4, 0;\n"
+      "tcgen05.mma.cta_group::1.kind::f16 [%0], %1, %2, %3, p;\n"
+      "}\n" ::"r"(tmem_d),
+      "l"(adesc), "l"(bdesc), "r"(kIdesc), "r"(accumulate));
+}
+
+__device__ __forceinline__ void umma_commit(uint64_t* bar) {
+  asm volatile("tcgen05.commit.cta_group::1.mbarrier::arrive::one.shared::cluster.b64 [%0];" ::"r"(smem_u32(bar))
+               : "memory");
+}
+
+__device__ __forceinline__ void tc_fence_before() { asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory"); }
+__device__ __forceinline__ void tc_fence_after() { asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory"); }
+
+__device__ __forceinline__ void tmem_ld32(uint32_t taddr, uint32_t (&r)[32]) {
+  asm volatile(
+      "tcgen05.ld.sync.aligned.32x32b.x32.b32 {%0,%1,%2,%3,%4,%5,%6,%7,%8,%9,%10,%11,%12,%13,%14,%15,%16,%17,%18,%"
+      "19,%20,%21,%22,%23,%24,%25,%26,%27,%28,%29,%30,%31}, [%32];"
+      : "=r"(r[0]), "=r"(r[1]), "=r"(r[2]), "=r"(r[3]), "=r"(r[4]), "=r"(r[5]), "=r"(r[6]), "=r"(r[7]), "=r"(r[8]),
+        "=r"(r[9]), "=r"(r[10]), "=r"(r[11]), "=r"(r[12]), "=r"(r[13]), "=r"(r[14]), "=r"(r[15]), "=r"(r[16]),
+        "=r"(r[17]), "=r"(r[18]), "=r"(r[19]), "=r"(r[20]), "=r"(r[21]), "=r"(r[22]), "=r"(r[23]), "=r"(r[24]),
+        "=r"(r[25]), "=r"(r[26]), "=r"(r[27]), "=r"(r[28]), "=r"(r[29]), "=r"(r[30]), "=r"(r[31])
+      : "r"(taddr));
+}
+
+__device__ __forceinline__ void tmem_ld_wait() { asm volatile("tcgen05.wait::ld.sync.aligned;" ::: "memory"); }
+
+struct TileCoord {
+  int entry, m_tile, n_tile;
+};
+
+__device__ __forceinline__ TileCoord tile_coord(const PrefillParams& p, int t) {
+  int lo = 0, hi = p.n_experts - 1;
+  while (lo < hi) {
+    int mid = (lo + hi + 1) >> 1;
+    if (p.tile_start[mid] <= t) lo = mid;
+    else hi = mid - 1;
+  }
+  const int local = t - p.tile_start[lo];
+  return {lo, local % p.m_tiles[lo], local / p.m_tiles[lo]};  // m fastest
+}
+
+__global__ void __launch_bounds__(kThreads, 1)
+ffn_prefill_kernel(const __grid_constant__ CUtensorMap a_map, const __grid_constant__ PrefillParams p) {
+  extern __shared__ __align__(1024) uint8_t smem_raw[];
+  uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
+  uint64_t* full_bar = reinterpret_cast<uint64_t*>(smem + kStages * kStageBytes);
+  uint64_t* empty_bar = full_bar + kStages;
+  uint64_t* tfull_bar = empty_bar + kStages;
+  uint64_t* tempty_bar = tfull_bar + 2;
+  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(tempty_bar + 2);
+
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const int n_tiles = p.tile_start[p.n_experts];
+  const int k_blocks = (p.K + kBK - 1) / kBK;
+
+  if (warp == 0 && lane == 0) {
+    for (int s = 0; s < kStages; ++s) {
+      mbar_init(&full_bar[s], 1);
+      mbar_init(&empty_bar[s], 1);
+    }
+    for (int s = 0; s < 2; ++s) {
+      mbar_init(&tfull_bar[s], 1);
+      mbar_init(&tempty_bar[s], 128);
+    }
+    asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+    prefetch_map(&a_map);
+  }
+  if (warp == 1) {  // whole warp: TMEM allocation (512 columns = 2 accumulator stages)
+    asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], 512;" ::"r"(smem_u32(tmem_slot)));
+    asm volatile("tcgen05.relinquish_alloc_permit.cta_group::1.sync.aligned;");
+  }
+  tc_fence_before();
+  __syncthreads();
+  tc_fence_after();
+  const uint32_t tmem_base = *tmem_slot;
+
+  if (warp == 0) {
+    if (lane == 0) {  // ---------------------------------------------- TMA producer
+      int stage = 0;
+      uint32_t phase = 0;
+      for (int t = blockIdx.x; t < n_tiles; t += gridDim.x) {
+        const TileCoord tc = tile_coord(p, t);
+        const CUtensorMap* bmap = p.b_maps + tc.entry;
+        const int arow = p.row0[tc.entry] + tc.m_tile * kBM;
+        for (int kb = 0; kb < k_blocks; ++kb) {
+          mbar_wait(&empty_bar[stage], phase ^ 1);
+          uint8_t* sa = smem + stage * kStageBytes;
+          uint8_t* sb = sa + kABytes;
+          mbar_expect_tx(&full_bar[stage], kStageBytes);
+          tma_load_2d(sa, &a_map, &full_bar[stage], kb * kBK, arow);
+          if (p.mode == kSwiGLU) {
+            const int n0 = tc.n_tile * (kBN / 2);
+            tma_load_2d(sb, bmap, &full_bar[stage], kb * kBK, n0);                      // gate rows
+            tma_load_2d(sb + kBBytes / 2, bmap, &full_bar[stage], kb * kBK, p.F + n0);  // up rows
+          } else {
+            const int n0 = tc.n_tile * kBN;
+            tma_load_2d(sb, bmap, &full_bar[stage], kb * kBK, n0);
+            tma_load_2d(sb + kBBytes / 2, bmap, &full_bar[stage], kb * kBK, n0 + kBN / 2);
+          }
+          if (++stage == kStages) {
+            stage = 0;
+            phase ^= 1;
+          }
+        }
+      }
+    }
+  } else if (warp == 1) {
+    if (lane == 0) {  // ---------------------------------------------- MMA issuer
+      int stage = 0;
+      uint32_t phase = 0;
+      int as = 0;
+      uint32_t aphase = 0;
+      for (int t = blockIdx.x; t < n_tiles; t += gridDim.x) {
+        mbar_wait(&tempty_bar[as], aphase ^ 1);
+        tc_fence_after();
+        const uint32_t d = tmem_base + static_cast<uint32_t>(as * kBN);
+        for (int kb = 0; kb < k_blocks; ++kb) {
+          mbar_wait(&full_bar[stage], phase);
+          tc_fence_after();
+          const uint32_t sa = smem_u32(smem + stage * kStageBytes);
+          const uint32_t sb = sa + kABytes;
+#pragma unroll
+          for (int kk = 0; kk < kBK / 16; ++kk) {  // K=16 per instruction: +32 B in the swizzled row
+            umma_f16(d, make_desc(sa + kk * 32), make_desc(sb + kk * 32), (kb | kk) != 0 ? 1u : 0u);
+          }
+          umma_commit(&empty_bar[stage]);  // smem stage free once these MMAs retire
+          if (++stage == kStages) {
+            stage = 0;
+            phase ^= 1;
+          }
+        }
+        umma_commit(&tfull_bar[as]);  // accumulator ready for the epilogue
+        as ^= 1;
+        if (as == 0) aphase ^= 1;
+      }
+    }
+  } else {  // ------------------------------------------------------- epilogue (4 warps)
+    const int quarter = warp & 3;  // TMEM lanes [32*quarter, +32) for this warp
+    const int r = quarter * 32 + lane;
+    int as = 0;
+    uint32_t aphase = 0;
+    for (int t = blockIdx.x; t < n_tiles; t += gridDim.x) {
+      const TileCoord tc = tile_coord(p, t);
+      mbar_wait(&tfull_bar[as], aphase);
+      tc_fence_after();
+      const uint32_t tbase = tmem_base + static_cast<uint32_t>(as * kBN) + (static_cast<uint32_t>(quarter * 32) << 16);
+      const int row_in_expert = tc.m_tile * kBM + r;
+      const bool valid = row_in_expert < p.rows[tc.entry];
+      const size_t out_row = static_cast<size_t>(p.row0[tc.entry] + row_in_expert);
+      if (p.mode == kSwiGLU) {
+        const int n0 = tc.n_tile * (kBN / 2);
+        uint16_t* out = static_cast<uint16_t*>(p.out) + out_row * p.out_ld + n0;
+#pragma unroll 1
+        for (int c = 0; c < kBN / 2; c += 32) {
+          uint32_t g[32], u[32];
+          tmem_ld32(tbase + c, g);
+          tmem_ld32(tbase + kBN / 2 + c, u);
+          tmem_ld_wait();
+          if (valid) {
+            uint32_t packed[16];
+#pragma unroll
+            for (int j = 0; j < 32; j += 2) {
+              const float g0 = __uint_as_float(g[j]), g1 = __uint_as_float(g[j + 1]);
+              const float h0 = g0 / (1.0f + expf(-g0)) * __uint_as_float(u[j]);
+              const float h1 = g1 / (1.0f + expf(-g1)) * __uint_as_float(u[j + 1]);
+              packed[j / 2] = static_cast<uint32_t>(f32_to_bf16_rne(h0)) |
+                              (static_cast<uint32_t>(f32_to_bf16_rne(h1)) << 16);
+            }
+            if (n0 + c + 32 <= p.F) {
+              uint4* dst = reinterpret_cast<uint4*>(out + c);
+#pragma unroll
+              for (int q = 0; q < 4; ++q)
+                dst[q] = make_uint4(packed[4 * q], packed[4 * q + 1], packed[4 * q + 2], packed[4 * q + 3]);
+            } else {
+              for (int j = 0; j < 32 && n0 + c + j < p.F; ++j)
+                out[c + j] = static_cast<uint16_t>(packed[j / 2] >> (16 * (j & 1)));
+            }
+          }
+        }
+      } else {
+        const int n0 = tc.n_tile * kBN;
+        float* out = static_cast<float*>(p.out) + out_row * p.out_ld + n0;
+#pragma unroll 1
+        for (int c = 0; c < kBN; c += 32) {
+          uint32_t v[32];
+          tmem_ld32(tbase + c, v);
+          tmem_ld_wait();
+          if (valid) {
+            if (n0 + c + 32 <= p.H) {
+              float4* dst = reinterpret_cast<float4*>(out + c);
+#pragma unroll
+              for (int q = 0; q < 8; ++q)
+                dst[q] = make_float4(__uint_as_float(v[4 * q]), __uint_as_float(v[4 * q + 1]),
+                                     __uint_as_float(v[4 * q + 2]), __uint_as_float(v[4 * q + 3]));
+            } else {
+              for (int j = 0; j < 32 && n0 + c + j < p.H; ++j) out[c + j] = __uint_as_float(v[j]);
+            }
+          }
+        }
+      }
+      tc_fence_before();
+      mbar_arrive(&tempty_bar[as]);
+      as ^= 1;
+      if (as == 0) aphase ^= 1;
+    }
+  }
+  __syncthreads();
+  if (warp == 1) {
+    tc_fence_after();
+    asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, 512;" ::"r"(tmem_base));
+  }
+}
+
+// ------------------------------------------------------------------ host helpers
+using EncodeFn = CUresult (*)(CUtensorMap*, CUtensorMapDataType, cuuint32_t, void*, const cuuint64_t*,
+                              const cuuint64_t*, const cuuint32_t*, const cuuint32_t*, CUtensorMapInterleave,
+                              CUtensorMapSwizzle, CUtensorMapL2promotion, CUtensorMapFloatOOBfill);
+
+EncodeFn encode_fn() {
+  static EncodeFn fn = nullptr;
+  static std::once_flag once;
+  std::call_once(once, [] {
+    void* p = nullptr;
+    cudaDriverEntryPointQueryResult q;
+    if (cudaGetDriverEntryPoint("cuTensorMapEncodeTiled", &p, cudaEnableDefault, &q) == cudaSuccess &&
+        q == cudaDriverEntryPointSuccess)
+      fn = reinterpret_cast<EncodeFn>(p);
+  });
+  if (!fn) fail(PS_ECUDA, "cuTensorMapEncodeTiled unavailable");
+  return fn;
+}
+
+// 2D bf16 row-major [rows, cols] tensor map with a {64, box_rows} box, 128B swizzle.
+CUtensorMap make_map(const void* base, uint64_t rows, uint64_t cols, uint32_t box_rows) {
+  CUtensorMap m;
+  cuuint64_t dims[2] = {cols, rows};
+  cuuint64_t strides[1] = {cols * 2};
+  cuuint32_t box[2] = {static_cast<cuuint32_t>(kBK), box_rows};
+  cuuint32_t estr[2] = {1, 1};
+  CUresult r = encode_fn()(&m, CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, 2, const_cast<void*>(base), dims, strides, box, estr,
+                           CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_128B,
+                           CU_TENSOR_MAP_L2_PROMOTION_L2_256B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+  if (r != CUDA_SUCCESS) fail(PS_ECUDA, "cuTensorMapEncodeTiled failed: " + std::to_string(static_cast<int>(r)));
+  return m;
+}
+
+struct MapBuffer {  // device + pinned staging for per-launch weight tensor maps
+  CUtensorMap* dev = nullptr;
+  CUtensorMap* host = nullptr;
+  int cap = 0;
+  void ensure(int n) {
+    if (n <= cap) return;
+    if (dev) cudaFree(dev);
+    if (host) cudaFreeHost(host);
+    cap = std::max(n, 2 * kMaxExperts);
+    PS_CUDA(cudaMalloc(&dev, sizeof(CUtensorMap) * cap));
+    PS_CUDA(cudaHostAlloc(&host, sizeof(CUtensorMap) * cap, cudaHostAllocDefault));
+  }
+};
+
+void launch(const CUtensorMap& amap, PrefillParams& p, cudaStream_t s) {
+  static bool attr = false;
+  if (!attr) {
+    PS_CUDA(cudaFuncSetAttribute(ffn_prefill_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, kSmemBytes));
+    attr = true;
+  }
+  const int tiles = p.tile_start[p.n_experts];
+  if (tiles == 0) return;
+  const int grid = std::min(tiles, kNumSMs);
+  ffn_prefill_kernel<<<grid, kThreads, kSmemBytes, s>>>(amap, p);
+  PS_LAUNCH_CHECK("ffn_prefill_kernel");
+}
+
+}  // namespace
+}  // namespace ps
+
+using namespace ps;
+
+extern "C" ps_status ps_expert_ffn_prefill(const ps_expert_group* group, const int32_t* counts_host,
+                                           const int32_t* offsets_host, const uint16_t* x_perm, int total_rows,
+                                           int H, int F, uint16_t* h_perm, float* y_perm, void* stream) {
+  return guarded([&] {
+    require(group && counts_host && offsets_host && x_perm && h_perm && y_perm, "ps_expert_ffn_prefill: null argument");
+    require(H % 64 == 0 && F % 128 == 0 && H % 256 == 0,
+            "ps_expert_ffn_prefill: needs H % 256 == 0 and F % 128 == 0");
+    require(group->n <= kMaxExperts, "ps_expert_ffn_prefill: too many experts");
+    cudaStream_t s = as_stream(stream);
+    static MapBuffer maps;  // reused across launches (stream-ordered: copy then kernel)
+    static std::mutex mu;
+    std::lock_guard<std::mutex> lock(mu);
+    maps.ensure(2 * group->n);
+
+    PrefillParams gu{}, dn{};
+    gu.mode = kSwiGLU;
+    dn.mode = kStoreF32;
+    gu.K = H;
+    dn.K = F;
+    gu.F = dn.F = F;
+    gu.H = dn.H = H;
+    gu.n_tiles_n = F / (kBN / 2);
+    dn.n_tiles_n = H / kBN;
+    int n = 0;
+    for (int i = 0; i < group->n; ++i) {
+      const int e = group->experts[i];
+      const int m = counts_host[e];
+      if (m == 0) continue;
+      const uint16_t* slab = group->slabs[i];
+      maps.host[n] = make_map(slab, 2ull * F, H, kBN / 2);                                    // [Wg; Wu] [2F, H]
+      maps.host[group->n + n] = make_map(slab + 2ull * F * H, static_cast<uint64_t>(H), F, kBN / 2);  // Wd [H, F]
+      const int mt = (m + kBM - 1) / kBM;
+      for (PrefillParams* p : {&gu, &dn}) {
+        p->m_tiles[n] = mt;
+        p->row0[n] = offsets_host[e];
+        p->rows[n] = m;
+        p->tile_start[n + 1] = p->tile_start[n] + mt * p->n_tiles_n;
+      }
+      ++n;
+    }
+    if (n == 0) return;
+    gu.n_experts = dn.n_experts = n;
+    PS_CUDA(cudaMemcpyAsync(maps.dev, maps.host, sizeof(CUtensorMap) * (group->n + n), cudaMemcpyHostToDevice, s));
+    // the staging buffer is reused by the next call only after this stream has consumed it
+    PS_CUDA(cudaStreamSynchronize(s));
+    gu.b_maps = maps.dev;
+    dn.b_maps = maps.dev + group->n;
+    gu.out = h_perm;
+    gu.out_ld = F;
+    dn.out = y_perm;
+    dn.out_ld = H;
+    const CUtensorMap a_x = make_map(x_perm, static_cast<uint64_t>(total_rows), H, kBM);
+    const CUtensorMap a_h = make_map(h_perm, static_cast<uint64_t>(total_rows), F, kBM);
+    launch(a_x, gu, s);
+    launch(a_h, dn, s);
+  });
+}

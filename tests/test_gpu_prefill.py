@@ -1,0 +1,105 @@
+"""K3 prefill path (tcgen05 / TMEM / TMA grouped GEMM) vs the CPU oracle and vs the
+decode path (itself oracle-checked), at ragged per-expert row counts."""
+import ctypes as C
+
+import numpy as np
+import pytest
+
+import oracle as orc
+import paper_2509_23638_b200 as ps
+
+pytestmark = pytest.mark.gpu
+BF16_RTOL = 2e-2
+
+
+def _p(t):
+    return C.c_void_p(t.data_ptr()) if t is not None else None
+
+
+def _prefill_case(torch, H, F, E, k, B, seed, skew=None, check_oracle_rows=None, with_decode=True):
+    lib = ps.load()
+    s = C.c_void_p(torch.cuda.current_stream().cuda_stream)
+    rng = np.random.default_rng(seed)
+    ids = np.stack([rng.choice(E, k, replace=False) for _ in range(B)]).astype(np.int32)
+    if skew is not None:
+        ids[: B // 2, 0] = skew
+        for t in range(B // 2):
+            if skew in ids[t, 1:]:
+                ids[t, 1:] = [(skew + 1 + j) % E for j in range(k - 1)]
+    logits = rng.standard_normal((B, E))
+    gw = np.exp(logits - logits.max(1, keepdims=True))
+    gw /= gw.sum(1, keepdims=True)
+    x = orc.f32_to_bf16((rng.standard_normal((B, H)) / np.sqrt(H)).astype(np.float32))
+    slabs_d = []
+    for e in range(E):
+        t = torch.empty(3 * H * F, dtype=torch.int16, device="cuda")
+        ps.check(lib.ps_init_expert_slab(_p(t), H, F, seed, 0, e, s))
+        slabs_d.append(t)
+    rows = B * k
+    di = torch.as_tensor(ids, device="cuda")
+    dx = torch.as_tensor(x.view(np.int16), device="cuda")
+    off = torch.empty(E + 1, dtype=torch.int32, device="cuda")
+    src = torch.empty(rows, dtype=torch.int32, device="cuda")
+    inv = torch.empty(rows, dtype=torch.int32, device="cuda")
+    xp = torch.empty(rows, H, dtype=torch.int16, device="cuda")
+    ps.check(lib.ps_permute(_p(di), B, k, E, _p(off), _p(src), _p(inv), _p(dx), H, _p(xp), s))
+    counts = np.bincount(ids.ravel(), minlength=E).astype(np.int32)
+    offsets = off.cpu().numpy()
+    grp = ps.capi.ExpertGroup()
+    grp.n = E
+    for e in range(E):
+        grp.experts[e] = e
+        grp.slabs[e] = slabs_d[e].data_ptr()
+    h = torch.empty(rows, F, dtype=torch.int16, device="cuda")
+    yp = torch.full((rows, H), float("nan"), dtype=torch.float32, device="cuda")
+    ps.check(lib.ps_expert_ffn_prefill(C.byref(grp), counts.ctypes.data, offsets.ctypes.data, _p(xp), rows, H, F,
+                                       _p(h), _p(yp), s))
+    y = torch.empty(B, H, dtype=torch.float32, device="cuda")
+    dw = torch.as_tensor(gw.astype(np.float32), device="cuda")
+    ps.check(lib.ps_combine(_p(yp), 1, _p(inv), _p(di), _p(dw), B, k, E, H, _p(y), s))
+    y = y.cpu().numpy()
+    out = {"y": y}
+    if with_decode:  # decode path on the same inputs
+        h2 = torch.empty(rows, F, dtype=torch.int16, device="cuda")
+        yp2 = torch.empty(1, rows, H, dtype=torch.float32, device="cuda")
+        ps.check(lib.ps_expert_ffn(C.byref(grp), counts.ctypes.data, _p(off), _p(src), k, _p(dx), H, F, _p(h2),
+                                   _p(yp2), 1, rows, s))
+        y2 = torch.empty(B, H, dtype=torch.float32, device="cuda")
+        ps.check(lib.ps_combine(_p(yp2), 1, _p(inv), _p(di), _p(dw), B, k, E, H, _p(y2), s))
+        out["y_decode"] = y2.cpu().numpy()
+    if check_oracle_rows:
+        sel = np.arange(min(B, check_oracle_rows))
+        slabs_h = [t.cpu().numpy().view(np.uint16) if e in set(ids[sel].ravel()) else None
+                   for e, t in enumerate(slabs_d)]
+        out["y_oracle"] = orc.or_moe_layer(slabs_h, H, F, x[sel], ids[sel], gw[sel].astype(np.float32), True)
+        out["sel"] = sel
+    return out
+
+
+def _rel(a, b):
+    return np.linalg.norm(a - b) / np.linalg.norm(b)
+
+
+@pytest.mark.parametrize("H,F,E,k,B,skew", [(256, 512, 8, 2, 512, None), (256, 384, 8, 2, 300, 3),
+                                             (512, 1024, 16, 4, 160, None), (256, 256, 4, 1, 1, None)])
+def test_prefill_vs_oracle_small(torch_cuda, H, F, E, k, B, skew):
+    out = _prefill_case(torch_cuda, H, F, E, k, B, 7, skew, check_oracle_rows=B)
+    assert np.isfinite(out["y"]).all()
+    assert _rel(out["y"], out["y_oracle"]) < BF16_RTOL
+    assert _rel(out["y"], out["y_decode"]) < BF16_RTOL
+
+
+def test_prefill_deepseek_shape(torch_cuda):
+    """DeepSeek-V2-Lite expert shape (H=2048, F=1408), 64 experts top-6, 2k-token chunk."""
+    out = _prefill_case(torch_cuda, 2048, 1408, 64, 6, 2048, 3, check_oracle_rows=6)
+    assert _rel(out["y"], out["y_decode"]) < BF16_RTOL
+    sel = out["sel"]
+    assert _rel(out["y"][sel], out["y_oracle"]) < BF16_RTOL
+
+
+def test_prefill_mixtral_shape(torch_cuda):
+    """Mixtral expert shape (H=4096, F=14336), 8 experts top-2, 1k tokens (m_e ~ 256)."""
+    out = _prefill_case(torch_cuda, 4096, 14336, 8, 2, 1024, 5, check_oracle_rows=2)
+    assert _rel(out["y"], out["y_decode"]) < BF16_RTOL
+    sel = out["sel"]
+    assert _rel(out["y"][sel], out["y_oracle"]) < BF16_RTOL
