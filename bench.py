@@ -263,8 +263,10 @@ def run_ours(args):
 
     # Same steps with every expert resident (budget 100 %): the HBM-bound MoE layer.
     all_res = None
+    prefill = None
     if not args.no_all_resident:
-        e2 = eng.Engine(spec, gen, max_batch=B, weight_seed=args.weight_seed, gate=gate,
+        PT = args.prefill_tokens
+        e2 = eng.Engine(spec, gen, max_batch=max(B, PT), weight_seed=args.weight_seed, gate=gate,
                         budget_bytes=L * E * spec.expert_bytes, resident=[(l, x) for l in range(L) for x in range(E)],
                         policy=args.policy, predictor=predictor, device=local)
         for s in range(args.warmup):
@@ -275,6 +277,33 @@ def run_ours(args):
             e2.step_device(hid_d[s], fol_d[s], y_d)
         torch.cuda.synchronize()
         st2 = e2.stats()
+        if PT > 0:
+            # Prefill chunk of PT tokens through the same engine (tcgen05 path): random
+            # unit hidden states routed by the same gate matrices; inputs > L2.
+            g = torch.Generator(device="cuda").manual_seed(5)
+            ph = torch.randn(L, PT, H, device="cuda", generator=g)
+            ph /= ph.norm(dim=-1, keepdim=True)
+            pf = torch.zeros(L, PT, dtype=torch.uint8, device="cuda")
+            py = torch.empty(L, PT, H, dtype=torch.float32, device="cuda")
+            for _ in range(2):
+                e2.step_device(ph, pf, py)
+            torch.cuda.synchronize()
+            e2.reset_stats()
+            for _ in range(args.prefill_steps):
+                e2.step_device(ph, pf, py)
+            torch.cuda.synchronize()
+            st3 = e2.stats()
+            ms3 = st3["step_ms_total"] / max(1, st3["steps"])
+            peak_tf = json.loads((ROOT / "MEASURED_PEAKS.json").read_text()).get("bf16_tflops", 1590.0) \
+                if (ROOT / "MEASURED_PEAKS.json").exists() else 1590.0
+            tf = st3["ffn_flops_total"] / (st3["ffn_ms_total"] / 1e3) / 1e12 if st3["ffn_ms_total"] > 0 else 0.0
+            prefill = {"tokens_per_step": PT, "value": N_world(dist) * PT / (ms3 / 1e3), "unit": "tokens/s",
+                       "ms_per_step": ms3, "moe_layer_us": ms3 * 1e3 / L,
+                       "ffn_tflops": tf, "ffn_frac_of_bf16_peak": tf / peak_tf, "peak_tflops": peak_tf,
+                       "tc_launches": st3["tc_launches"],
+                       "route_phase_us_per_layer": st3["route_phase_ms_total"] * 1e3 / max(1, st3["layers"]),
+                       "data": "random unit hidden states, all experts resident"}
+            del ph, py
         e2.close()
         ms2 = st2["step_ms_total"] / max(1, st2["steps"])
         ach2 = st2["ffn_bytes_total"] / (st2["ffn_ms_total"] / 1e3) / 1e9 if st2["ffn_ms_total"] > 0 else 0.0
@@ -283,6 +312,8 @@ def run_ours(args):
                    "moe_layer_us": ms2 * 1e3 / L, "ffn_achieved_gbs": ach2,
                    "ffn_frac_of_hbm": ach2 / measured_peaks()[0],
                    "layer_frac_of_hbm": layer_bytes / (ms2 / 1e3 / L) / 1e9 / measured_peaks()[0],
+                   "route_phase_us_per_layer": st2["route_phase_ms_total"] * 1e3 / max(1, st2["layers"]),
+                   "combine_us_per_layer": st2["combine_ms_total"] * 1e3 / max(1, st2["layers"]),
                    "gpu_launches": st2["kernel_launches"]}
     lib.ps_llapor_free(predictor)
 
@@ -324,6 +355,7 @@ def run_ours(args):
         "cpu_baseline": ({"value": args.batch / cpu_step_s, "unit": "tokens/s", "cores": threads, "kind": "port",
                           "sample": cpu_desc} if cpu_step_s else None),
         "all_resident": all_res,
+        "prefill": prefill,
         "clocks": clk.summary(),
         "gpu_launches": st["kernel_launches"],
         "wall_s_timed": wall, "engine_create_s": t_create,
@@ -355,6 +387,8 @@ def main():
     ap.add_argument("--weight-seed", type=int, default=1)
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--no-all-resident", action="store_true")
+    ap.add_argument("--prefill-tokens", type=int, default=4096)
+    ap.add_argument("--prefill-steps", type=int, default=3)
     args = ap.parse_args()
     if args.impl == "reference":
         run_reference_arm(args)

@@ -256,6 +256,10 @@ ps_status ps_permute(const int32_t* ids, int B, int k, int E, int32_t* offsets,
                      int32_t* perm_src, int32_t* inv, const uint16_t* x, int H,
                      uint16_t* x_perm, void* stream);
 
+/* K2 — row gather: out[i, :] = x[idx[i] / div, :] (bf16 rows, H % 8 == 0). */
+ps_status ps_gather_rows(const uint16_t* x, const int32_t* idx, int n, int div, int H, uint16_t* out,
+                         void* stream);
+
 /* K2 — weighted combine: y[t] = sum_j weights[t, ids[t,j]] * sum_s y_part[s][inv[t*k+j]]
  * (full-softmax gate weights, workload.cpp:190-195; no top-k renormalisation).
  *   y_part [n_split, B*k, H] f32; y [B,H] f32. */
@@ -318,6 +322,37 @@ ps_status ps_llapor_forward(ps_llapor m, int layer, const float* hidden,
                             int B, int k, float* logits, int32_t* ids, int32_t* pred_counts,
                             void* scratch, void* stream);
 
+/* ---------------------------------------------------------- expert parallelism (EP)
+ * SURVEY.md §8e (a north_star extension; the reference has no multi-GPU code,
+ * SPEC.md:17): expert e of every layer is owned by rank e % world. Each rank routes its
+ * own tokens, permutes them owner-major (virtual id v = (e % G)*ceil(E/G) + e/G, so
+ * ps_permute over v yields destination-rank segments), exchanges per-(source, local
+ * expert) counts and then the rows (all-to-all dispatch), runs its local experts, and
+ * returns the per-row outputs (all-to-all combine) for the weighted sum at home. */
+typedef struct ps_ep_comm_s* ps_ep_comm;
+int ps_ep_local_experts(int E, int world, int rank);
+ps_status ps_ep_remap_ids(const int32_t* ids, int n, int E, int world, int32_t* vids, void* stream);
+/* Per-destination counts message [world][2*E_loc]: rows for each of the destination's
+ * local experts (from ps_permute offsets over virtual ids, [world*E_loc+1]) followed by
+ * this rank's predicted tokens for them (pred [E], nullable). */
+ps_status ps_ep_pack_counts(const int32_t* offsets_v, const int32_t* pred, int E, int world,
+                            int32_t* out, void* stream);
+/* Receiver plan from recv_counts [G][E_loc] (rows from source s for local expert j):
+ * offsets [E_loc+1] of the local expert-major order, perm_src [total] (permuted local
+ * row -> received row, nullable), recv_seg [G+1] row offsets of each source segment. */
+ps_status ps_ep_recv_plan(const int32_t* recv_counts, int world, int E_loc, int32_t* offsets,
+                          int32_t* perm_src, int32_t* recv_seg);
+/* NCCL transport (grouped ncclSend/ncclRecv over NVLink; NCCL loaded at run time). */
+ps_status ps_ep_unique_id(char* out, int cap); /* 128 bytes, broadcast by the caller */
+ps_status ps_ep_comm_create(const char* unique_id, int rank, int world, int device, ps_ep_comm* out);
+ps_status ps_ep_comm_destroy(ps_ep_comm c);
+int ps_ep_comm_rank(ps_ep_comm c);
+int ps_ep_comm_world(ps_ep_comm c);
+/* Segmented all-to-all: segment p of `send` (send_bytes[p]) goes to rank p, segment p
+ * of `recv` (recv_bytes[p]) comes from rank p; segments are contiguous and in rank order. */
+ps_status ps_ep_all_to_all(ps_ep_comm c, const void* send, const uint64_t* send_bytes, void* recv,
+                           const uint64_t* recv_bytes, void* stream);
+
 /* -------------------------------------------------------------------- decode engine
  * K5: the AsyncIO expert loader + HBM expert cache + per-layer decode driver.
  * Resident experts (plan_residency under budget_bytes) live in HBM; the others in
@@ -341,6 +376,9 @@ typedef struct {
   ps_llapor predictor;      /* nullable => perfect-prediction off; uses gate weights */
   int32_t device;
   int32_t host_pinned;      /* 1: non-resident experts in pinned host DRAM */
+  ps_ep_comm ep;            /* nullable: expert-parallel over this communicator; the
+                               engine then owns experts e % world == rank only, and
+                               `resident`/`budget_bytes` are this rank's */
 } ps_engine_config;
 
 ps_status ps_engine_create(const ps_engine_config* cfg, ps_engine* out);
@@ -367,6 +405,8 @@ typedef struct {
   double ffn_bytes_total;   /* algorithmic bytes of those launches: 3*H*F*2 per routed expert */
   double route_phase_ms_total; /* K1 + K4 + K2-index + counts D2H per layer (the scheduling point) */
   double combine_ms_total;     /* K2 combine */
+  double ffn_flops_total;      /* 6*m_e*H*F summed over FFN launches */
+  int64_t tc_launches;         /* K3 launches that took the tcgen05 (prefill) path */
   int64_t ffn_launches, kernel_launches;
   ps_cost_params cost;      /* calibrated costs in use */
 } ps_engine_stats;

@@ -113,7 +113,7 @@ class EngineConfig(C.Structure):
                 ("budget_bytes", C.c_uint64), ("resident", C.POINTER(C.c_int32)), ("n_resident", C.c_int32),
                 ("max_batch", C.c_int32), ("prefetch_slots", C.c_int32), ("policy", Policy),
                 ("cost", CostParams), ("predictor", C.c_void_p), ("device", C.c_int32),
-                ("host_pinned", C.c_int32)]
+                ("host_pinned", C.c_int32), ("ep", C.c_void_p)]
 
 
 class EngineStats(C.Structure):
@@ -122,7 +122,8 @@ class EngineStats(C.Structure):
                 ("prefetch_hits", C.c_int64), ("resident_hits", C.c_int64), ("h2d_bytes", C.c_double),
                 ("h2d_busy_ms", C.c_double), ("compute_wait_ms", C.c_double), ("step_ms_total", C.c_double),
                 ("ffn_ms_total", C.c_double), ("ffn_bytes_total", C.c_double),
-                ("route_phase_ms_total", C.c_double), ("combine_ms_total", C.c_double), ("ffn_launches", C.c_int64),
+                ("route_phase_ms_total", C.c_double), ("combine_ms_total", C.c_double),
+                ("ffn_flops_total", C.c_double), ("tc_launches", C.c_int64), ("ffn_launches", C.c_int64),
                 ("kernel_launches", C.c_int64),
                 ("cost", CostParams)]
 
@@ -179,6 +180,17 @@ _SIGS = {
     "ps_llapor_free": (C.c_int, [_P]),
     "ps_llapor_scratch_bytes": (C.c_size_t, [_P, C.c_int]),
     "ps_llapor_forward": (C.c_int, [_P, C.c_int, _P, _P, C.c_int, _P, C.c_int, C.c_int, _P, _P, _P, _P, _P]),
+    "ps_ep_local_experts": (C.c_int, [C.c_int, C.c_int, C.c_int]),
+    "ps_ep_remap_ids": (C.c_int, [_P, C.c_int, C.c_int, C.c_int, _P, _P]),
+    "ps_ep_recv_plan": (C.c_int, [_P, C.c_int, C.c_int, _P, _P, _P]),
+    "ps_ep_pack_counts": (C.c_int, [_P, _P, C.c_int, C.c_int, _P, _P]),
+    "ps_ep_unique_id": (C.c_int, [C.c_char_p, C.c_int]),
+    "ps_ep_comm_create": (C.c_int, [C.c_char_p, C.c_int, C.c_int, C.c_int, C.POINTER(C.c_void_p)]),
+    "ps_ep_comm_destroy": (C.c_int, [_P]),
+    "ps_ep_comm_rank": (C.c_int, [_P]),
+    "ps_ep_comm_world": (C.c_int, [_P]),
+    "ps_ep_all_to_all": (C.c_int, [_P, _P, _P, _P, _P, _P]),
+    "ps_gather_rows": (C.c_int, [_P, _P, C.c_int, C.c_int, C.c_int, _P, _P]),
     "ps_engine_create": (C.c_int, [C.POINTER(EngineConfig), C.POINTER(C.c_void_p)]),
     "ps_engine_destroy": (C.c_int, [_P]),
     "ps_engine_set_router": (C.c_int, [_P, _P]),

@@ -40,6 +40,7 @@ namespace ps {
 namespace {
 
 using Clock = std::chrono::steady_clock;
+constexpr int kDecodeMaxBatch = 64;  // larger batches (prefill chunks) take the tcgen05 path
 
 double now_us() {
   return std::chrono::duration<double, std::micro>(Clock::now().time_since_epoch()).count();
@@ -240,6 +241,8 @@ struct ps_engine_s {
   int32_t* pred_dev = nullptr;       // [E]
   int32_t* pinned_counts = nullptr;  // [2E] host pinned: counts | pred
   uint16_t* x_bf16 = nullptr;
+  uint16_t* x_perm = nullptr;        // [maxB*k, H] bf16 (prefill gather)
+  bool prefill_mode = false;         // B > kDecodeMaxBatch: tcgen05 path, exact-count launches
   int32_t *offsets = nullptr, *perm_src = nullptr, *inv = nullptr;
   uint16_t* hbuf = nullptr;
   float* y_part = nullptr;
@@ -249,6 +252,41 @@ struct ps_engine_s {
   float* out_y = nullptr;
   int32_t* out_ids = nullptr;
   cudaEvent_t ev_routed = nullptr, ev_step0 = nullptr, ev_step1 = nullptr;
+
+  // Where the FFN of the current layer reads its rows from (set per layer): the local
+  // routing (x_bf16 with k slots per token) or, under EP, the rows received from all
+  // ranks (k = 1). Offsets are indexed by GLOBAL expert id (zero-length for experts
+  // this rank does not own).
+  struct FfnSrc {
+    const int32_t* offsets_dev;
+    const int32_t* perm_dev;
+    int k;
+    const uint16_t* x;
+    int rows;
+    const int32_t* offsets_host;  // prefill tile scheduling
+  } src{};
+  int rows_max = 0;  // capacity of the per-row FFN buffers (G * maxB * k under EP)
+
+  // expert parallelism
+  ps_ep_comm ep = nullptr;
+  int G = 1, rank = 0, E_loc = 0;
+  int32_t* ep_vids = nullptr;      // [maxB*k] owner-major virtual ids
+  int32_t* ep_off_v = nullptr;     // [G*E_loc+1]
+  int32_t* ep_perm_v = nullptr;    // [maxB*k]
+  int32_t* ep_inv_v = nullptr;     // [maxB*k]
+  uint16_t* ep_send_x = nullptr;   // [maxB*k, H]
+  uint16_t* ep_recv_x = nullptr;   // [G*maxB*k, H]
+  float* ep_y_recv = nullptr;      // [G*maxB*k, H]
+  float* ep_y_back = nullptr;      // [maxB*k, H]
+  int32_t* ep_cnt_send = nullptr;  // [G][2*E_loc]
+  int32_t* ep_cnt_recv = nullptr;  // [G][2*E_loc]
+  int32_t* ep_plan_dev = nullptr;  // [E+1 | rows | rows]: offsets_glob, perm_loc, inv_loc
+  int32_t* ep_plan_host = nullptr; // pinned staging of the same
+  int32_t* ep_host = nullptr;      // pinned [G*E_loc+1 | G*2*E_loc]: own offsets_v, recv counts
+  float* ep_ones = nullptr;        // [rows_max] combine weights for the unpermute
+  int32_t* ep_zeros = nullptr;     // [rows_max]
+  std::vector<int32_t> ep_seg, ep_send_rows;  // per-layer receive segments / send rows
+  int ep_rows_recv = 0;
 
   // scheduler state across layers
   ps_hit_stats stats[3];
@@ -295,18 +333,37 @@ int group_of_layer(const ps_model_spec& s, int l) {
   return l < s.group_begin_middle ? PS_GROUP_INPUT : l < s.group_begin_output ? PS_GROUP_MIDDLE : PS_GROUP_OUTPUT;
 }
 
-void ffn(ps_engine_s& e, const ps_expert_group& g, const int32_t* counts_host, int B, bool timed) {
+void ffn(ps_engine_s& e, const ps_expert_group& g, const int32_t* counts_host, int B, bool timed,
+         bool exact_counts = true) {
   if (g.n == 0) return;
   cudaEvent_t a = nullptr, b = nullptr;
   if (timed) {
     a = take_event(e);
     PS_CUDA(cudaEventRecord(a, e.sc));
   }
-  ps_status s = ps_expert_ffn(&g, counts_host, e.offsets, e.perm_src, e.K, e.x_bf16, e.H, e.F, e.hbuf, e.y_part,
-                              e.n_split, B * e.K, e.sc);
+  // Path choice per launch: the tcgen05 grouped GEMM once an expert has a full 128-row
+  // M tile of tokens (prefill), the HBM-streaming GEMV otherwise (decode).
+  int max_m = 0;
+  double rows = 0;
+  for (int i = 0; i < g.n; ++i) {
+    max_m = std::max(max_m, counts_host[g.experts[i]]);
+    rows += counts_host[g.experts[i]];
+  }
+  ps_status s;
+  (void)B;
+  const auto& src = e.src;
+  if (e.prefill_mode && max_m >= 128 && e.H % 256 == 0 && e.F % 128 == 0) {
+    s = ps_expert_ffn_prefill(&g, counts_host, src.offsets_host, e.x_perm, src.rows, e.H, e.F, e.hbuf, e.y_part,
+                              e.sc);
+    e.st.tc_launches += 2;
+  } else {
+    s = ps_expert_ffn(&g, counts_host, src.offsets_dev, src.perm_dev, src.k, src.x, e.H, e.F, e.hbuf, e.y_part,
+                      e.n_split, src.rows, e.sc);
+  }
   if (s != PS_OK) fail(s, ps_last_error());
   e.st.ffn_launches += 2;
   e.st.kernel_launches += 2;
+  if (exact_counts) e.st.ffn_flops_total += 6.0 * rows * e.H * e.F;
   if (timed) {
     b = take_event(e);
     PS_CUDA(cudaEventRecord(b, e.sc));
@@ -368,9 +425,86 @@ double push_modelled(ps_engine_s& e) {  // channel busy-until model for alpha (R
   return e.io_free_us;
 }
 
+// EP dispatch, part 2 (after the counts exchange landed on the host): the receive plan
+// (local expert-major order over the received rows), the per-layer counts the loader
+// schedules with, and the row payload all-to-all.
+
+void ep_dispatch_rows(ps_engine_s& e, int B, std::vector<int32_t>& counts_l, std::vector<int32_t>& pred_l) {
+  const int G = e.G, El = e.E_loc, Ev = G * El, E = e.E, H = e.H;
+  const int32_t* off_v = e.ep_host;
+  const int32_t* rc = e.ep_host + Ev + 1;
+  std::vector<int32_t> rcnt(static_cast<size_t>(G) * El), off_loc(El + 1);
+  e.ep_seg.assign(G + 1, 0);
+  for (int s = 0; s < G; ++s)
+    for (int j = 0; j < El; ++j) rcnt[s * El + j] = rc[s * 2 * El + j];
+  int32_t* og = e.ep_plan_host;
+  int32_t* perm = og + (E + 1);
+  int32_t* inv = perm + e.rows_max;
+  ps_status st = ps_ep_recv_plan(rcnt.data(), G, El, off_loc.data(), nullptr, e.ep_seg.data());
+  if (st != PS_OK) fail(st, ps_last_error());
+  const int rows = e.ep_seg[G];
+  require(rows <= e.rows_max, "EP: received rows exceed capacity");
+  st = ps_ep_recv_plan(rcnt.data(), G, El, off_loc.data(), perm, e.ep_seg.data());
+  if (st != PS_OK) fail(st, ps_last_error());
+  for (int r = 0; r < rows; ++r) inv[perm[r]] = r;
+  int running = 0;
+  for (int ex = 0; ex < E; ++ex) {
+    og[ex] = running;
+    counts_l[ex] = pred_l[ex] = 0;
+    if (ex % G != e.rank) continue;
+    const int j = ex / G;
+    counts_l[ex] = off_loc[j + 1] - off_loc[j];
+    for (int s = 0; s < G; ++s) pred_l[ex] += rc[s * 2 * El + El + j];
+    running += counts_l[ex];
+  }
+  og[E] = running;
+  PS_CUDA(cudaMemcpyAsync(e.ep_plan_dev, e.ep_plan_host, sizeof(int32_t) * (E + 1 + 2 * static_cast<size_t>(e.rows_max)),
+                          cudaMemcpyHostToDevice, e.sc));
+  std::vector<uint64_t> sb(G), rb(G);
+  e.ep_send_rows.assign(G, 0);
+  for (int d = 0; d < G; ++d) {
+    e.ep_send_rows[d] = off_v[(d + 1) * El] - off_v[d * El];
+    sb[d] = static_cast<uint64_t>(e.ep_send_rows[d]) * H * sizeof(uint16_t);
+    rb[d] = static_cast<uint64_t>(e.ep_seg[d + 1] - e.ep_seg[d]) * H * sizeof(uint16_t);
+  }
+  st = ps_ep_all_to_all(e.ep, e.ep_send_x, sb.data(), e.ep_recv_x, rb.data(), e.sc);
+  if (st != PS_OK) fail(st, ps_last_error());
+  e.ep_rows_recv = rows;
+  const int32_t* plan = e.ep_plan_dev;
+  e.src = {plan, plan + (E + 1), 1, e.ep_recv_x, rows, og};
+  if (e.prefill_mode && rows > 0) {
+    st = ps_gather_rows(e.ep_recv_x, plan + (E + 1), rows, 1, H, e.x_perm, e.sc);
+    if (st != PS_OK) fail(st, ps_last_error());
+    e.st.kernel_launches += 1;
+  }
+  (void)B;
+}
+
+// EP combine: per-row outputs back to receive order, all-to-all back to the token
+// owners, weighted sum at home.
+ps_status ep_combine_rows(ps_engine_s& e, int B, const LayerDev& ld, float* y_l) {
+  const int G = e.G, H = e.H, E = e.E, K = e.K;
+  const int rows = e.ep_rows_recv;
+  ps_status st = PS_OK;
+  if (rows > 0)
+    st = ps_combine(e.y_part, e.n_split, e.ep_plan_dev + (E + 1) + e.rows_max, e.ep_zeros, e.ep_ones, rows, 1, 1, H,
+                    e.ep_y_recv, e.sc);
+  if (st != PS_OK) return st;
+  std::vector<uint64_t> sb(G), rb(G);
+  for (int p = 0; p < G; ++p) {
+    sb[p] = static_cast<uint64_t>(e.ep_seg[p + 1] - e.ep_seg[p]) * H * sizeof(float);
+    rb[p] = static_cast<uint64_t>(e.ep_send_rows[p]) * H * sizeof(float);
+  }
+  st = ps_ep_all_to_all(e.ep, e.ep_y_recv, sb.data(), e.ep_y_back, rb.data(), e.sc);
+  if (st != PS_OK) return st;
+  e.st.kernel_launches += 2;
+  return ps_combine(e.ep_y_back, 1, e.ep_inv_v, ld.ids, ld.weights, B, K, E, H, y_l, e.sc);
+}
+
 void decode_step(ps_engine_s& e, const float* hidden, const uint8_t* follow, int B, float* y, int32_t* ids_out) {
   const int L = e.L, E = e.E, K = e.K, H = e.H;
   require(B >= 1 && B <= e.maxB, "decode_step: batch out of range");
+  e.prefill_mode = B > kDecodeMaxBatch;
   e.jobs.clear();
   e.event_next = 0;
   e.job_event_next = 0;
@@ -406,18 +540,44 @@ void decode_step(ps_engine_s& e, const float* hidden, const uint8_t* follow, int
       e.st.kernel_launches += 2;
     }
     // --- K2 permute indices ------------------------------------------------------
-    s = ps_permute(ld.ids, B, K, E, e.offsets, e.perm_src, e.inv, nullptr, H, nullptr, e.sc);
-    if (s != PS_OK) fail(s, ps_last_error());
-    e.st.kernel_launches += 1;
-    PS_CUDA(cudaMemcpyAsync(e.pinned_counts, e.counts_dev, sizeof(int32_t) * E, cudaMemcpyDeviceToHost, e.sc));
-    if (predict)
-      PS_CUDA(cudaMemcpyAsync(e.pinned_counts + E, e.pred_dev, sizeof(int32_t) * E, cudaMemcpyDeviceToHost, e.sc));
+    // Prefill-sized batches gather x into contiguous permuted rows (TMA operand of the
+    // tcgen05 path) and need the offsets on the host for tile scheduling.
+    const int Ev = e.G * e.E_loc;  // owner-major virtual expert count under EP
+    if (!e.ep) {
+      s = ps_permute(ld.ids, B, K, E, e.offsets, e.perm_src, e.inv, e.prefill_mode ? e.x_bf16 : nullptr, H,
+                     e.prefill_mode ? e.x_perm : nullptr, e.sc);
+      if (s != PS_OK) fail(s, ps_last_error());
+      e.st.kernel_launches += e.prefill_mode ? 2 : 1;
+      PS_CUDA(cudaMemcpyAsync(e.pinned_counts, e.counts_dev, sizeof(int32_t) * E, cudaMemcpyDeviceToHost, e.sc));
+      if (predict)
+        PS_CUDA(cudaMemcpyAsync(e.pinned_counts + E, e.pred_dev, sizeof(int32_t) * E, cudaMemcpyDeviceToHost, e.sc));
+      if (e.prefill_mode)
+        PS_CUDA(cudaMemcpyAsync(e.pinned_counts + 2 * E, e.offsets, sizeof(int32_t) * (E + 1),
+                                cudaMemcpyDeviceToHost, e.sc));
+      e.src = {e.offsets, e.perm_src, K, e.x_bf16, B * K, e.pinned_counts + 2 * E};
+    } else {
+      // EP dispatch, part 1: owner-major permute + gather of this rank's routed rows,
+      // then the (rows, predicted tokens) counts exchange with every owner.
+      s = ps_ep_remap_ids(ld.ids, B * K, E, e.G, e.ep_vids, e.sc);
+      if (s == PS_OK)
+        s = ps_permute(e.ep_vids, B, K, Ev, e.ep_off_v, e.ep_perm_v, e.ep_inv_v, e.x_bf16, H, e.ep_send_x, e.sc);
+      if (s == PS_OK) s = ps_ep_pack_counts(e.ep_off_v, predict ? e.pred_dev : nullptr, E, e.G, e.ep_cnt_send, e.sc);
+      if (s != PS_OK) fail(s, ps_last_error());
+      e.st.kernel_launches += 4;
+      std::vector<uint64_t> cb(e.G, sizeof(int32_t) * 2 * e.E_loc);
+      s = ps_ep_all_to_all(e.ep, e.ep_cnt_send, cb.data(), e.ep_cnt_recv, cb.data(), e.sc);
+      if (s != PS_OK) fail(s, ps_last_error());
+      PS_CUDA(cudaMemcpyAsync(e.ep_host, e.ep_off_v, sizeof(int32_t) * (Ev + 1), cudaMemcpyDeviceToHost, e.sc));
+      PS_CUDA(cudaMemcpyAsync(e.ep_host + Ev + 1, e.ep_cnt_recv, sizeof(int32_t) * e.G * 2 * e.E_loc,
+                              cudaMemcpyDeviceToHost, e.sc));
+    }
     PS_CUDA(cudaEventRecord(e.ev_routed, e.sc));
     PS_CUDA(cudaEventRecord(ph.route1, e.sc));
 
-    // --- resident experts start now, before the host knows the counts (R6): the
-    // kernels read per-expert row counts from the device offsets, the grid is sized
+    // --- resident experts (R6). Decode: start now, before the host knows the counts —
+    // the kernels read per-expert row counts from the device offsets, the grid is sized
     // for the worst case m_e = B and warps of unrouted experts exit immediately.
+    // Prefill: launched after the host sync with exact counts (tile scheduling).
     ps_expert_group grp{};
     std::vector<int32_t> worst(E, B);
     for (int ex = 0; ex < E; ++ex)
@@ -427,7 +587,8 @@ void decode_step(ps_engine_s& e, const float* hidden, const uint8_t* follow, int
         ++grp.n;
       }
     const size_t resident_timing = e.ffn_t.size();
-    ffn(e, grp, worst.data(), B, true);
+    const bool early = !e.prefill_mode && !e.ep;
+    if (early) ffn(e, grp, worst.data(), B, true, false);
 
     // --- R2: resolve the previous layer's prefetch batch at this scheduling point
     {
@@ -448,14 +609,23 @@ void decode_step(ps_engine_s& e, const float* hidden, const uint8_t* follow, int
 
     // Wait for the routing result on the host (the only per-layer host sync).
     PS_CUDA(cudaEventSynchronize(e.ev_routed));
-    std::memcpy(counts_l.data(), e.pinned_counts, sizeof(int32_t) * E);
-    if (predict) std::memcpy(pred_l.data(), e.pinned_counts + E, sizeof(int32_t) * E);
-    else std::fill(pred_l.begin(), pred_l.end(), 0);
-    if (resident_timing < e.ffn_t.size()) {  // algorithmic bytes: routed experts only
-      double bytes = 0;
-      for (int i = 0; i < grp.n; ++i)
+    if (!e.ep) {
+      std::memcpy(counts_l.data(), e.pinned_counts, sizeof(int32_t) * E);
+      if (predict) std::memcpy(pred_l.data(), e.pinned_counts + E, sizeof(int32_t) * E);
+      else std::fill(pred_l.begin(), pred_l.end(), 0);
+    } else {
+      ep_dispatch_rows(e, B, counts_l, pred_l);
+    }
+    if (!early) {
+      ffn(e, grp, counts_l.data(), B, true, true);
+    } else if (resident_timing < e.ffn_t.size()) {  // algorithmic bytes/flops: routed experts only
+      double bytes = 0, rows = 0;
+      for (int i = 0; i < grp.n; ++i) {
         if (counts_l[grp.experts[i]] > 0) bytes += static_cast<double>(e.cfg.spec.expert_bytes);
+        rows += counts_l[grp.experts[i]];
+      }
       e.ffn_t[resident_timing].bytes = bytes;
+      e.st.ffn_flops_total += 6.0 * rows * e.H * e.F;
     }
     for (int i = 0; i < grp.n; ++i) e.st.resident_hits += counts_l[grp.experts[i]] > 0;
 
@@ -550,8 +720,12 @@ void decode_step(ps_engine_s& e, const float* hidden, const uint8_t* follow, int
 
     // --- combine -> y_l ------------------------------------------------------------
     PS_CUDA(cudaEventRecord(ph.comb0, e.sc));
-    s = ps_combine(e.y_part, e.n_split, e.inv, ld.ids, ld.weights, B, K, E, H, y + static_cast<size_t>(l) * B * H,
-                   e.sc);
+    if (!e.ep) {
+      s = ps_combine(e.y_part, e.n_split, e.inv, ld.ids, ld.weights, B, K, E, H, y + static_cast<size_t>(l) * B * H,
+                     e.sc);
+    } else {
+      s = ep_combine_rows(e, B, ld, y + static_cast<size_t>(l) * B * H);
+    }
     if (s != PS_OK) fail(s, ps_last_error());
     PS_CUDA(cudaEventRecord(ph.comb1, e.sc));
     e.phase_t.push_back(ph);
@@ -664,18 +838,30 @@ void create_engine(const ps_engine_config& cfg, ps_engine_s& e) {
   PS_CUDA(cudaStreamCreateWithFlags(&e.sc, cudaStreamNonBlocking));
   e.io = std::make_unique<IoChannel>(cfg.device, 2);
 
+  // Expert parallelism: this rank owns experts e % G == rank of every layer.
+  e.ep = cfg.ep;
+  if (e.ep) {
+    e.G = ps_ep_comm_world(e.ep);
+    e.rank = ps_ep_comm_rank(e.ep);
+    require(e.G >= 1 && e.rank >= 0 && e.rank < e.G && e.G <= e.E, "engine: bad EP communicator");
+  }
+  e.E_loc = (e.E + e.G - 1) / e.G;
+  auto owned = [&](int ex) { return ex % e.G == e.rank; };
+
   // Residency: explicit list or nothing (callers plan it with ps_plan_residency).
   const size_t LE = static_cast<size_t>(e.L) * e.E;
   e.resident.assign(LE, 0);
   for (int i = 0; i < cfg.n_resident; ++i) {
     int l = cfg.resident[2 * i], ex = cfg.resident[2 * i + 1];
     require(l >= 0 && l < e.L && ex >= 0 && ex < e.E, "engine: resident pair out of range");
+    require(owned(ex), "engine: resident expert not owned by this EP rank");
     e.resident[static_cast<size_t>(l) * e.E + ex] = 1;
   }
-  size_t n_res = 0;
+  size_t n_res = 0, n_owned = 0;
   for (uint8_t r : e.resident) n_res += r;
+  for (int ex = 0; ex < e.E; ++ex) n_owned += owned(ex) ? e.L : 0;
   require(n_res * sp.expert_bytes <= cfg.budget_bytes, "engine: resident set exceeds the HBM budget");
-  const size_t n_host = LE - n_res;
+  const size_t n_host = n_owned - n_res;
 
   e.dev_slab.assign(LE, nullptr);
   e.host_slab.assign(LE, nullptr);
@@ -689,6 +875,7 @@ void create_engine(const ps_engine_config& cfg, ps_engine_s& e) {
   for (int l = 0; l < e.L; ++l)
     for (int ex = 0; ex < e.E; ++ex) {
       const size_t idx = static_cast<size_t>(l) * e.E + ex;
+      if (!owned(ex)) continue;
       if (e.resident[idx]) {
         uint16_t* p = reinterpret_cast<uint16_t*>(static_cast<char*>(e.arena) + ri++ * sp.expert_bytes);
         if (ps_init_expert_slab(p, e.H, e.F, cfg.weight_seed, l, ex, e.sc) != PS_OK) fail(PS_ECUDA, ps_last_error());
@@ -723,6 +910,8 @@ void create_engine(const ps_engine_config& cfg, ps_engine_s& e) {
   PS_CUDA(cudaMemcpy(e.bias, bias.data(), sizeof(float) * bias.size(), cudaMemcpyHostToDevice));
 
   const size_t B = e.maxB, rows = B * e.K;
+  e.rows_max = static_cast<int>(e.G * rows);  // FFN rows: everything routed here by all ranks
+  const size_t frows = static_cast<size_t>(e.rows_max);
   e.layer.resize(e.L);
   for (auto& ld : e.layer) {
     PS_CUDA(cudaMalloc(&ld.weights, sizeof(float) * B * e.E));
@@ -730,13 +919,35 @@ void create_engine(const ps_engine_config& cfg, ps_engine_s& e) {
   }
   PS_CUDA(cudaMalloc(&e.counts_dev, sizeof(int32_t) * e.E));
   PS_CUDA(cudaMalloc(&e.pred_dev, sizeof(int32_t) * e.E));
-  PS_CUDA(cudaHostAlloc(&e.pinned_counts, sizeof(int32_t) * 2 * e.E, cudaHostAllocDefault));
+  PS_CUDA(cudaHostAlloc(&e.pinned_counts, sizeof(int32_t) * (3 * e.E + 1), cudaHostAllocDefault));
   PS_CUDA(cudaMalloc(&e.x_bf16, sizeof(uint16_t) * B * e.H));
+  PS_CUDA(cudaMalloc(&e.x_perm, sizeof(uint16_t) * frows * e.H));
   PS_CUDA(cudaMalloc(&e.offsets, sizeof(int32_t) * (e.E + 1)));
   PS_CUDA(cudaMalloc(&e.perm_src, sizeof(int32_t) * rows));
   PS_CUDA(cudaMalloc(&e.inv, sizeof(int32_t) * rows));
-  PS_CUDA(cudaMalloc(&e.hbuf, sizeof(uint16_t) * rows * e.F));
-  PS_CUDA(cudaMalloc(&e.y_part, sizeof(float) * e.n_split * rows * e.H));
+  PS_CUDA(cudaMalloc(&e.hbuf, sizeof(uint16_t) * frows * e.F));
+  PS_CUDA(cudaMalloc(&e.y_part, sizeof(float) * e.n_split * frows * e.H));
+  if (e.ep) {
+    const size_t Ev = static_cast<size_t>(e.G) * e.E_loc;
+    PS_CUDA(cudaMalloc(&e.ep_vids, sizeof(int32_t) * rows));
+    PS_CUDA(cudaMalloc(&e.ep_off_v, sizeof(int32_t) * (Ev + 1)));
+    PS_CUDA(cudaMalloc(&e.ep_perm_v, sizeof(int32_t) * rows));
+    PS_CUDA(cudaMalloc(&e.ep_inv_v, sizeof(int32_t) * rows));
+    PS_CUDA(cudaMalloc(&e.ep_send_x, sizeof(uint16_t) * rows * e.H));
+    PS_CUDA(cudaMalloc(&e.ep_recv_x, sizeof(uint16_t) * frows * e.H));
+    PS_CUDA(cudaMalloc(&e.ep_y_recv, sizeof(float) * frows * e.H));
+    PS_CUDA(cudaMalloc(&e.ep_y_back, sizeof(float) * rows * e.H));
+    PS_CUDA(cudaMalloc(&e.ep_cnt_send, sizeof(int32_t) * 2 * Ev));
+    PS_CUDA(cudaMalloc(&e.ep_cnt_recv, sizeof(int32_t) * 2 * Ev));
+    PS_CUDA(cudaMalloc(&e.ep_plan_dev, sizeof(int32_t) * (e.E + 1 + 2 * frows)));
+    PS_CUDA(cudaHostAlloc(&e.ep_plan_host, sizeof(int32_t) * (e.E + 1 + 2 * frows), cudaHostAllocDefault));
+    PS_CUDA(cudaHostAlloc(&e.ep_host, sizeof(int32_t) * (Ev + 1 + 2 * Ev), cudaHostAllocDefault));
+    PS_CUDA(cudaMalloc(&e.ep_ones, sizeof(float) * frows));
+    PS_CUDA(cudaMalloc(&e.ep_zeros, sizeof(int32_t) * frows));
+    std::vector<float> ones(frows, 1.0f);
+    PS_CUDA(cudaMemcpy(e.ep_ones, ones.data(), sizeof(float) * frows, cudaMemcpyHostToDevice));
+    PS_CUDA(cudaMemset(e.ep_zeros, 0, sizeof(int32_t) * frows));
+  }
   if (cfg.predictor) PS_CUDA(cudaMalloc(&e.llapor_scratch, ps_llapor_scratch_bytes(cfg.predictor, e.maxB)));
   PS_CUDA(cudaMalloc(&e.in_hidden, sizeof(float) * e.L * B * e.H));
   PS_CUDA(cudaMalloc(&e.in_follow, e.L * B));
@@ -757,10 +968,15 @@ void destroy_engine(ps_engine_s& e) {
     cudaFree(ld.ids);
   }
   for (void* p : {(void*)e.arena, (void*)e.gate, (void*)e.bias, (void*)e.counts_dev, (void*)e.pred_dev,
-                  (void*)e.x_bf16, (void*)e.offsets, (void*)e.perm_src, (void*)e.inv, (void*)e.hbuf,
+                  (void*)e.x_bf16, (void*)e.x_perm, (void*)e.offsets, (void*)e.perm_src, (void*)e.inv, (void*)e.hbuf,
                   (void*)e.y_part, e.llapor_scratch, (void*)e.in_hidden, (void*)e.in_follow, (void*)e.out_y,
-                  (void*)e.out_ids})
+                  (void*)e.out_ids, (void*)e.ep_vids, (void*)e.ep_off_v, (void*)e.ep_perm_v, (void*)e.ep_inv_v,
+                  (void*)e.ep_send_x, (void*)e.ep_recv_x, (void*)e.ep_y_recv, (void*)e.ep_y_back,
+                  (void*)e.ep_cnt_send, (void*)e.ep_cnt_recv, (void*)e.ep_plan_dev, (void*)e.ep_ones,
+                  (void*)e.ep_zeros})
     if (p) cudaFree(p);
+  if (e.ep_plan_host) cudaFreeHost(e.ep_plan_host);
+  if (e.ep_host) cudaFreeHost(e.ep_host);
   if (e.host_arena) cudaFreeHost(e.host_arena);
   if (e.pinned_counts) cudaFreeHost(e.pinned_counts);
   for (auto& s : e.od_slot) {

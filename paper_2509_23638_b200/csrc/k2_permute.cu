@@ -111,12 +111,62 @@ __global__ void combine_kernel(const float* __restrict__ y_part, int n_split, si
   *reinterpret_cast<float4*>(y + static_cast<size_t>(t) * H + h) = acc;
 }
 
+// Expert parallelism: owner-major virtual ids v = (e % G) * ceil(E/G) + e / G, so a
+// counting sort over v groups the routed rows by destination rank, then local expert.
+__global__ void ep_remap_kernel(const int32_t* __restrict__ ids, int n, int G, int e_loc, int32_t* __restrict__ v) {
+  const int i = blockIdx.x * blockDim.x + threadIdx.x;
+  if (i < n) {
+    const int e = ids[i];
+    v[i] = (e % G) * e_loc + e / G;
+  }
+}
+
+// out[d][j] = rows this rank sends to rank d for d's local expert j (from the owner-major
+// offsets); out[d][E_loc + j] = this rank's LLaPor-predicted tokens for that expert.
+__global__ void ep_pack_counts_kernel(const int32_t* __restrict__ offsets_v, const int32_t* __restrict__ pred,
+                                      int E, int G, int e_loc, int32_t* __restrict__ out) {
+  const int i = blockIdx.x * blockDim.x + threadIdx.x;
+  if (i >= G * e_loc) return;
+  const int d = i / e_loc, j = i % e_loc, e = j * G + d;
+  out[d * 2 * e_loc + j] = offsets_v[i + 1] - offsets_v[i];
+  out[d * 2 * e_loc + e_loc + j] = (pred && e < E) ? pred[e] : 0;
+}
+
 }  // namespace
 }  // namespace ps
 
 using namespace ps;
 
 extern "C" {
+
+ps_status ps_ep_pack_counts(const int32_t* offsets_v, const int32_t* pred, int E, int G, int32_t* out,
+                            void* stream) {
+  return guarded([&] {
+    require(offsets_v && out && E >= 1 && G >= 1, "ps_ep_pack_counts: bad arguments");
+    const int e_loc = (E + G - 1) / G;
+    ep_pack_counts_kernel<<<(G * e_loc + 127) / 128, 128, 0, as_stream(stream)>>>(offsets_v, pred, E, G, e_loc, out);
+    PS_LAUNCH_CHECK("ep_pack_counts_kernel");
+  });
+}
+
+ps_status ps_gather_rows(const uint16_t* x, const int32_t* idx, int n, int div, int H, uint16_t* out,
+                         void* stream) {
+  return guarded([&] {
+    require(n >= 0 && div >= 1 && H % 8 == 0 && x && idx && out, "ps_gather_rows: bad arguments");
+    if (n == 0) return;
+    gather_rows_kernel<<<(n * 32 + 255) / 256, 256, 0, as_stream(stream)>>>(x, idx, n, div, H, out);
+    PS_LAUNCH_CHECK("gather_rows_kernel");
+  });
+}
+
+ps_status ps_ep_remap_ids(const int32_t* ids, int n, int E, int G, int32_t* vids, void* stream) {
+  return guarded([&] {
+    require(n >= 0 && E >= 1 && G >= 1 && ids && vids, "ps_ep_remap_ids: bad arguments");
+    if (n == 0) return;
+    ep_remap_kernel<<<(n + 255) / 256, 256, 0, as_stream(stream)>>>(ids, n, G, (E + G - 1) / G, vids);
+    PS_LAUNCH_CHECK("ep_remap_kernel");
+  });
+}
 
 ps_status ps_permute(const int32_t* ids, int B, int k, int E, int32_t* offsets, int32_t* perm_src,
                      int32_t* inv, const uint16_t* x, int H, uint16_t* x_perm, void* stream) {

@@ -376,17 +376,29 @@ CUtensorMap make_map(const void* base, uint64_t rows, uint64_t cols, uint32_t bo
   return m;
 }
 
-struct MapBuffer {  // device + pinned staging for per-launch weight tensor maps
+// Ring of per-launch weight tensor-map slots (device array + pinned staging). A slot is
+// rewritten only after the event recorded behind its last kernels has completed, so no
+// launch ever waits on the host for the GPU (on-demand experts are launched while their
+// copies are still in flight).
+struct MapRing {
+  static constexpr int kSlots = 64;
+  static constexpr int kPerSlot = 2 * kMaxExperts;
   CUtensorMap* dev = nullptr;
   CUtensorMap* host = nullptr;
-  int cap = 0;
-  void ensure(int n) {
-    if (n <= cap) return;
-    if (dev) cudaFree(dev);
-    if (host) cudaFreeHost(host);
-    cap = std::max(n, 2 * kMaxExperts);
-    PS_CUDA(cudaMalloc(&dev, sizeof(CUtensorMap) * cap));
-    PS_CUDA(cudaHostAlloc(&host, sizeof(CUtensorMap) * cap, cudaHostAllocDefault));
+  cudaEvent_t ev[kSlots] = {};
+  bool used[kSlots] = {};
+  int next = 0;
+  int acquire() {
+    if (!dev) {
+      PS_CUDA(cudaMalloc(&dev, sizeof(CUtensorMap) * kSlots * kPerSlot));
+      PS_CUDA(cudaHostAlloc(&host, sizeof(CUtensorMap) * kSlots * kPerSlot, cudaHostAllocDefault));
+      for (auto& e : ev) PS_CUDA(cudaEventCreateWithFlags(&e, cudaEventDisableTiming));
+    }
+    const int s = next;
+    next = (next + 1) % kSlots;
+    if (used[s]) PS_CUDA(cudaEventSynchronize(ev[s]));
+    used[s] = true;
+    return s;
   }
 };
 
@@ -417,10 +429,12 @@ extern "C" ps_status ps_expert_ffn_prefill(const ps_expert_group* group, const i
             "ps_expert_ffn_prefill: needs H % 256 == 0 and F % 128 == 0");
     require(group->n <= kMaxExperts, "ps_expert_ffn_prefill: too many experts");
     cudaStream_t s = as_stream(stream);
-    static MapBuffer maps;  // reused across launches (stream-ordered: copy then kernel)
+    static MapRing ring;
     static std::mutex mu;
     std::lock_guard<std::mutex> lock(mu);
-    maps.ensure(2 * group->n);
+    const int slot = ring.acquire();
+    CUtensorMap* maps_host = ring.host + slot * MapRing::kPerSlot;
+    CUtensorMap* maps_dev = ring.dev + slot * MapRing::kPerSlot;
 
     PrefillParams gu{}, dn{};
     gu.mode = kSwiGLU;
@@ -437,8 +451,8 @@ extern "C" ps_status ps_expert_ffn_prefill(const ps_expert_group* group, const i
       const int m = counts_host[e];
       if (m == 0) continue;
       const uint16_t* slab = group->slabs[i];
-      maps.host[n] = make_map(slab, 2ull * F, H, kBN / 2);                                    // [Wg; Wu] [2F, H]
-      maps.host[group->n + n] = make_map(slab + 2ull * F * H, static_cast<uint64_t>(H), F, kBN / 2);  // Wd [H, F]
+      maps_host[n] = make_map(slab, 2ull * F, H, kBN / 2);                                           // [Wg; Wu]
+      maps_host[kMaxExperts + n] = make_map(slab + 2ull * F * H, static_cast<uint64_t>(H), F, kBN / 2);  // Wd
       const int mt = (m + kBM - 1) / kBM;
       for (PrefillParams* p : {&gu, &dn}) {
         p->m_tiles[n] = mt;
@@ -450,11 +464,9 @@ extern "C" ps_status ps_expert_ffn_prefill(const ps_expert_group* group, const i
     }
     if (n == 0) return;
     gu.n_experts = dn.n_experts = n;
-    PS_CUDA(cudaMemcpyAsync(maps.dev, maps.host, sizeof(CUtensorMap) * (group->n + n), cudaMemcpyHostToDevice, s));
-    // the staging buffer is reused by the next call only after this stream has consumed it
-    PS_CUDA(cudaStreamSynchronize(s));
-    gu.b_maps = maps.dev;
-    dn.b_maps = maps.dev + group->n;
+    PS_CUDA(cudaMemcpyAsync(maps_dev, maps_host, sizeof(CUtensorMap) * MapRing::kPerSlot, cudaMemcpyHostToDevice, s));
+    gu.b_maps = maps_dev;
+    dn.b_maps = maps_dev + kMaxExperts;
     gu.out = h_perm;
     gu.out_ld = F;
     dn.out = y_perm;
@@ -463,5 +475,6 @@ extern "C" ps_status ps_expert_ffn_prefill(const ps_expert_group* group, const i
     const CUtensorMap a_h = make_map(h_perm, static_cast<uint64_t>(total_rows), F, kBM);
     launch(a_x, gu, s);
     launch(a_h, dn, s);
+    PS_CUDA(cudaEventRecord(ring.ev[slot], s));
   });
 }

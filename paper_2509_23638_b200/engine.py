@@ -66,13 +66,39 @@ def hot_table(spec: capi.ModelSpec, gate: np.ndarray, hidden: np.ndarray, follow
     return freq
 
 
+class EpComm:
+    """NCCL communicator for expert parallelism (ps_ep_comm). `unique_id` (128 bytes)
+    comes from rank 0's EpComm.unique_id() and is broadcast by the caller (e.g. with
+    torch.distributed); world=1 needs no broadcast."""
+
+    @staticmethod
+    def unique_id() -> bytes:
+        buf = C.create_string_buffer(128)
+        check(load().ps_ep_unique_id(buf, 128))
+        return buf.raw
+
+    def __init__(self, rank: int = 0, world: int = 1, device: int = 0, unique_id: bytes | None = None):
+        uid = unique_id if unique_id is not None else EpComm.unique_id()
+        self.h = C.c_void_p()
+        check(load().ps_ep_comm_create(uid, rank, world, device, C.byref(self.h)))
+        self.rank, self.world = rank, world
+
+    def owned(self, E: int):
+        return [e for e in range(E) if e % self.world == self.rank]
+
+    def close(self):
+        if self.h:
+            check(load().ps_ep_comm_destroy(self.h))
+            self.h = None
+
+
 class Engine:
     """ps_engine handle. gate: [L,E,H] router matrices (from ps.trace_inputs)."""
 
     def __init__(self, spec: capi.ModelSpec, gen_cfg, *, max_batch: int, weight_seed: int = 0,
                  gate: np.ndarray, budget_fraction: float | None = None, budget_bytes: int | None = None,
                  resident=None, trace_hidden=None, trace_follow=None, policy: str = "presched",
-                 predictor=None, cost=None, prefetch_slots: int = 8, device: int = 0):
+                 predictor=None, cost=None, prefetch_slots: int = 8, device: int = 0, ep=None):
         from . import parse_policy, plan_residency, trace_inputs  # noqa: F401
         self.lib = load()
         self.spec = spec
@@ -105,6 +131,7 @@ class Engine:
         cfg.predictor = predictor
         cfg.device = device
         cfg.host_pinned = 1
+        cfg.ep = ep.h if isinstance(ep, EpComm) else ep
         h = C.c_void_p()
         check(self.lib.ps_engine_create(C.byref(cfg), C.byref(h)))
         self.h = h

@@ -75,6 +75,17 @@ def test_engine_qwen3_like_shape_with_llapor(torch_cuda):
     assert st["kernel_launches"] > 0
 
 
+@pytest.mark.parametrize("budget", [1.0, 0.5])
+def test_engine_prefill_chunk_uses_tcgen05_and_matches_oracle(torch_cuda, budget):
+    """B > 64 switches the engine to prefill mode: gathered x_perm, exact-count
+    launches, tcgen05 grouped GEMM for experts with >= 128 rows."""
+    spec = _small_spec(L=3, E=8, H=256, F=512)
+    y, y_ref, ids, st, _, agree = _run(spec, 512, budget, steps=1)
+    assert st["tc_launches"] > 0
+    assert agree >= 0.99
+    assert np.linalg.norm(y - y_ref) / np.linalg.norm(y_ref) < BF16_RTOL
+
+
 def test_engine_batch_one(torch_cuda):
     spec = _small_spec()
     y, y_ref, *_ = _run(spec, 1, 0.5)
