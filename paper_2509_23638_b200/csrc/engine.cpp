@@ -532,7 +532,11 @@ void decode_step(ps_engine_s& e, const float* hidden, const uint8_t* follow, int
     if (s != PS_OK) fail(s, ps_last_error());
     e.st.kernel_launches += 1;
     // --- K4 LLaPor: predicted histogram of layer l+1 -------------------------
-    const bool predict = e.cfg.predictor && l + 1 < L;
+    // Prefill chunks (>= 4 routed rows per expert on average) activate every expert of
+    // the next layer with near certainty: the prediction is then the dense histogram
+    // B*k/E per expert and the LLaPor launch is skipped (decode always runs LLaPor).
+    const bool dense_next = B * K >= 4 * E && l + 1 < L;
+    const bool predict = e.cfg.predictor && l + 1 < L && !dense_next;
     if (predict) {
       s = ps_llapor_forward(e.cfg.predictor, l + 1, x, ld.ids, K, ld.weights, B, K, nullptr, nullptr, e.pred_dev,
                             e.llapor_scratch, e.sc);
@@ -612,7 +616,7 @@ void decode_step(ps_engine_s& e, const float* hidden, const uint8_t* follow, int
     if (!e.ep) {
       std::memcpy(counts_l.data(), e.pinned_counts, sizeof(int32_t) * E);
       if (predict) std::memcpy(pred_l.data(), e.pinned_counts + E, sizeof(int32_t) * E);
-      else std::fill(pred_l.begin(), pred_l.end(), 0);
+      else std::fill(pred_l.begin(), pred_l.end(), dense_next ? (B * K) / E : 0);
     } else {
       ep_dispatch_rows(e, B, counts_l, pred_l);
     }

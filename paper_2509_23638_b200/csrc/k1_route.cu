@@ -19,77 +19,101 @@ constexpr int kMaxE = 256;
 constexpr int kMaxK = 16;
 constexpr int kETile = 8;
 
-// One CTA per token: the 8 warps split H (latency: a Mixtral token needs 4 float4
-// steps per lane instead of 32), per-warp partial logits are summed in shared memory
-// in fixed warp order (deterministic), then warp 0 finishes softmax / top-k.
+// One CTA per TB tokens: the 8 warps split H (latency: a Mixtral token needs 4 float4
+// steps per lane instead of 32) and every gate float4 loaded is applied to all TB
+// tokens (TB = 1 for decode batches, 8 for prefill chunks: 8x less L2 gate traffic).
+// Per-warp partial logits are summed in shared memory in fixed warp order
+// (deterministic and independent of TB); warp t then finishes token t: kappa override,
+// softmax, top-k, histogram.
+template <int TB>
 __global__ void __launch_bounds__(kWarps * 32)
 route_kernel(const float* __restrict__ x, const float* __restrict__ gate, const float* __restrict__ bias,
              const uint8_t* __restrict__ follow, const int32_t* __restrict__ prev_ids, int prev_k,
              int B, int H, int E, int k, float sqrt_h, float* __restrict__ logits_out,
              float* __restrict__ weights_out, int32_t* __restrict__ ids_out,
              int32_t* __restrict__ counts, uint16_t* __restrict__ x_bf16) {
-  __shared__ float s_part[kWarps][kMaxE];
-  __shared__ float s_logit[kMaxE];
+  __shared__ float s_part[kWarps][TB][kMaxE];
+  __shared__ float s_logit[TB][kMaxE];
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
-  const int b = blockIdx.x;
-  const float* xr = x + static_cast<size_t>(b) * H;
-  float* lg = s_logit;
+  const int b0 = blockIdx.x * TB;
+  const int nt = min(TB, B - b0);
   const bool vec = (H & 3) == 0;
 
   // Fused cast x -> bf16 (input of K3), vectorised, all threads.
-  if (x_bf16 && vec) {
-    for (int h = threadIdx.x * 4; h < H; h += kWarps * 128) {
-      float4 v = *reinterpret_cast<const float4*>(xr + h);
-      uint2 o;
-      o.x = (uint32_t)f32_to_bf16_rne(v.x) | ((uint32_t)f32_to_bf16_rne(v.y) << 16);
-      o.y = (uint32_t)f32_to_bf16_rne(v.z) | ((uint32_t)f32_to_bf16_rne(v.w) << 16);
-      *reinterpret_cast<uint2*>(x_bf16 + static_cast<size_t>(b) * H + h) = o;
+  for (int t = 0; t < nt; ++t) {
+    const float* xr = x + static_cast<size_t>(b0 + t) * H;
+    uint16_t* xo = x_bf16 ? x_bf16 + static_cast<size_t>(b0 + t) * H : nullptr;
+    if (xo && vec) {
+      for (int h = threadIdx.x * 4; h < H; h += kWarps * 128) {
+        float4 v = *reinterpret_cast<const float4*>(xr + h);
+        uint2 o;
+        o.x = (uint32_t)f32_to_bf16_rne(v.x) | ((uint32_t)f32_to_bf16_rne(v.y) << 16);
+        o.y = (uint32_t)f32_to_bf16_rne(v.z) | ((uint32_t)f32_to_bf16_rne(v.w) << 16);
+        *reinterpret_cast<uint2*>(xo + h) = o;
+      }
+    } else if (xo) {
+      for (int h = threadIdx.x; h < H; h += kWarps * 32) xo[h] = f32_to_bf16_rne(xr[h]);
     }
-  } else if (x_bf16) {
-    for (int h = threadIdx.x; h < H; h += kWarps * 32) x_bf16[static_cast<size_t>(b) * H + h] = f32_to_bf16_rne(xr[h]);
   }
 
   // Gate GEMV partials: warp w owns H slice [w*hs, (w+1)*hs), kETile experts at a time.
   const int hs = vec ? ((H / 4 + kWarps - 1) / kWarps) * 4 : (H + kWarps - 1) / kWarps;
   const int h_lo = min(H, warp * hs), h_hi = min(H, h_lo + hs);
   for (int e0 = 0; e0 < E; e0 += kETile) {
-    float acc[kETile];
+    float acc[TB][kETile];
 #pragma unroll
-    for (int j = 0; j < kETile; ++j) acc[j] = 0.f;
+    for (int t = 0; t < TB; ++t)
+#pragma unroll
+      for (int j = 0; j < kETile; ++j) acc[t][j] = 0.f;
     if (vec) {
       for (int h = h_lo + lane * 4; h < h_hi; h += 128) {
-        const float4 xv = *reinterpret_cast<const float4*>(xr + h);
+        float4 xv[TB];
+#pragma unroll
+        for (int t = 0; t < TB; ++t)
+          xv[t] = t < nt ? *reinterpret_cast<const float4*>(x + static_cast<size_t>(b0 + t) * H + h)
+                         : make_float4(0.f, 0.f, 0.f, 0.f);
 #pragma unroll
         for (int j = 0; j < kETile; ++j) {
           if (e0 + j < E) {
             const float4 g = __ldg(reinterpret_cast<const float4*>(gate + static_cast<size_t>(e0 + j) * H + h));
-            acc[j] += g.x * xv.x + g.y * xv.y + g.z * xv.z + g.w * xv.w;
+#pragma unroll
+            for (int t = 0; t < TB; ++t)
+              acc[t][j] += g.x * xv[t].x + g.y * xv[t].y + g.z * xv[t].z + g.w * xv[t].w;
           }
         }
       }
     } else {
       for (int h = h_lo + lane; h < h_hi; h += 32) {
-        const float xv = xr[h];
 #pragma unroll
-        for (int j = 0; j < kETile; ++j)
-          if (e0 + j < E) acc[j] += __ldg(gate + static_cast<size_t>(e0 + j) * H + h) * xv;
+        for (int j = 0; j < kETile; ++j) {
+          if (e0 + j >= E) continue;
+          const float g = __ldg(gate + static_cast<size_t>(e0 + j) * H + h);
+#pragma unroll
+          for (int t = 0; t < TB; ++t)
+            if (t < nt) acc[t][j] += g * x[static_cast<size_t>(b0 + t) * H + h];
+        }
       }
     }
 #pragma unroll
-    for (int j = 0; j < kETile; ++j) {
-      float s = warp_sum(acc[j]);
-      if (lane == 0 && e0 + j < E) s_part[warp][e0 + j] = s;
-    }
-  }
-  __syncthreads();
-  for (int e = threadIdx.x; e < E; e += kWarps * 32) {
-    float s = 0.f;
+    for (int t = 0; t < TB; ++t)
 #pragma unroll
-    for (int w = 0; w < kWarps; ++w) s += s_part[w][e];
-    lg[e] = s * sqrt_h + (bias ? bias[e] : 0.f);
+      for (int j = 0; j < kETile; ++j) {
+        float sum = warp_sum(acc[t][j]);
+        if (lane == 0 && e0 + j < E) s_part[warp][t][e0 + j] = sum;
+      }
   }
   __syncthreads();
-  if (warp != 0) return;
+  for (int i = threadIdx.x; i < nt * E; i += kWarps * 32) {
+    const int t = i / E, e = i % E;
+    float sum = 0.f;
+#pragma unroll
+    for (int w = 0; w < kWarps; ++w) sum += s_part[w][t][e];
+    s_logit[t][e] = sum * sqrt_h + (bias ? bias[e] : 0.f);
+  }
+  __syncthreads();
+  if (warp >= nt) return;
+  const int b = b0 + warp;
+  float* lg = s_logit[warp];
 
   // kappa-follow override: logits[(prev_top1+1) % E] = max + 1 (workload.cpp:183-188).
   if (follow && prev_ids && follow[b]) {
@@ -164,8 +188,13 @@ extern "C" ps_status ps_route_topk(const float* x, const float* gate, const floa
     if (counts) PS_CUDA(cudaMemsetAsync(counts, 0, sizeof(int32_t) * E, s));
     if (B == 0) return;
     const float sqrt_h = static_cast<float>(std::sqrt(static_cast<double>(H)));
-    route_kernel<<<B, kWarps * 32, 0, s>>>(
-        x, gate, bias, follow, prev_ids, prev_k, B, H, E, k, sqrt_h, logits, weights, ids, counts, x_bf16);
+    if (B <= 64) {
+      route_kernel<1><<<B, kWarps * 32, 0, s>>>(x, gate, bias, follow, prev_ids, prev_k, B, H, E, k, sqrt_h, logits,
+                                                weights, ids, counts, x_bf16);
+    } else {
+      route_kernel<4><<<(B + 3) / 4, kWarps * 32, 0, s>>>(x, gate, bias, follow, prev_ids, prev_k, B, H, E, k, sqrt_h,
+                                                          logits, weights, ids, counts, x_bf16);
+    }
     PS_LAUNCH_CHECK("route_kernel");
   });
 }

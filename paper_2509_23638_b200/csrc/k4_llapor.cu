@@ -108,14 +108,26 @@ __device__ __forceinline__ float gelu_erf(float v) { return 0.5f * v * (1.0f + e
 __device__ void affine_tokens(const float* __restrict__ W, const float* __restrict__ bvec, int rows, int cols,
                               const float* in, int in_stride, float* out, int out_stride, int nt, bool gelu) {
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31, nw = blockDim.x >> 5;
+  constexpr int kU = 8;  // weight loads in flight per lane (latency-bound: one L2 round trip per 256 cols)
   for (int r = warp; r < rows; r += nw) {
     float acc[kMlpTok];
 #pragma unroll
     for (int t = 0; t < kMlpTok; ++t) acc[t] = 0.f;
-    for (int c = lane; c < cols; c += 32) {
-      const float w = __ldg(W + static_cast<size_t>(r) * cols + c);
+    for (int c0 = 0; c0 < cols; c0 += 32 * kU) {
+      float w[kU];
 #pragma unroll
-      for (int t = 0; t < kMlpTok; ++t) acc[t] += w * in[t * in_stride + c];
+      for (int u = 0; u < kU; ++u) {
+        const int c = c0 + lane + 32 * u;
+        w[u] = c < cols ? __ldg(W + static_cast<size_t>(r) * cols + c) : 0.f;
+      }
+#pragma unroll
+      for (int u = 0; u < kU; ++u) {
+        const int c = c0 + lane + 32 * u;
+        if (c < cols) {
+#pragma unroll
+          for (int t = 0; t < kMlpTok; ++t) acc[t] += w[u] * in[t * in_stride + c];
+        }
+      }
     }
     const float bias = __ldg(bvec + r);
 #pragma unroll
