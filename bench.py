@@ -16,7 +16,9 @@ already in HBM. `e2e` = the same through the host-buffer C-ABI call
 blocking call. `roofline` = the decode FFN kernel (K3), the dominant kernel, vs the
 measured HBM copy bandwidth. `cpu_baseline` = the same step on the host cores: the
 oracle port of the SwiGLU FFN/combine + the reference's own scheduling code.
-N>1: independent decode replicas, one per GPU (no data-path collective).
+N>1: expert parallelism (torchrun, one rank per GPU): rank r owns experts e % N == r with the
+same budget fraction of its shard, decodes its own B tokens (weak scaling) and exchanges
+routed rows with NCCL all-to-all over NVLink.
 """
 from __future__ import annotations
 
@@ -170,7 +172,7 @@ def workload_config(args, spec):
                         f"({n_res}/{L * E} experts resident, hot-table residency from a warm-up trace), "
                         f"other experts in pinned host DRAM, policy {args.policy}",
             "model": f"{args.model}-8x7b-shape" if args.model == "mixtral" else args.model,
-            "global_batch": args.batch * args.gpus, "seq_len": 1, "parallelism": f"replicas{args.gpus}",
+            "global_batch": args.batch * args.gpus, "seq_len": 1, "parallelism": (f"ep{args.gpus}" if args.gpus > 1 else "single"),
             "budget_fraction": args.budget, "policy": args.policy,
             "l2": "inputs larger than L2 (each expert slab 336 MiB > 126 MB L2)"}
 
@@ -194,20 +196,40 @@ def run_ours(args):
     L, E, H, k = spec.num_layers, spec.experts_per_layer, spec.hidden_dim, spec.top_k
     B = args.batch
     S = args.warmup + args.steps
-    # routing inputs: one trace (fixed gate matrices), B*S tokens sliced into S decode steps
-    gate, hidden, follow, zipf = ps.trace_inputs(gen, spec, B * S, 1000 + rank)
+    # routing inputs: one trace (one set of gate matrices for all ranks), B*S tokens per
+    # rank sliced into S decode steps; rank r decodes its own tokens (weak scaling)
+    gate, hidden_all, follow_all, zipf = ps.trace_inputs(gen, spec, B * S * world, 1000)
+    hidden = hidden_all[rank * B * S:(rank + 1) * B * S]
+    follow = follow_all[rank * B * S:(rank + 1) * B * S]
     # hot table from a separate warm-up trace with the same gate matrices (perf mode)
-    _, warm_h, warm_f, _ = ps.trace_inputs(gen, spec, 64, 1000 + rank, want_gate=False)
+    _, warm_h, warm_f, _ = ps.trace_inputs(gen, spec, 64, 1000, want_gate=False)
     freq = eng.hot_table(spec, gate, warm_h, warm_f, zipf)
-    budget_bytes = int(round(args.budget * L * E)) * spec.expert_bytes
-    resident = ps.plan_residency(freq, budget_bytes, spec.expert_bytes)
+    ep = None
+    if world > 1:
+        # Expert parallelism: rank r owns experts e % world == r and the
+        # same budget fraction of its shard; tokens are exchanged with NCCL all-to-all.
+        uid = torch.zeros(128, dtype=torch.uint8, device="cuda")
+        if rank == 0:
+            uid.copy_(torch.frombuffer(bytearray(eng.EpComm.unique_id()), dtype=torch.uint8))
+        dist.broadcast(uid, 0)
+        ep = eng.EpComm(rank, world, local, bytes(uid.cpu().numpy().tobytes()))
+        freq = freq.copy()
+        for x in range(E):
+            if x % world != rank:
+                freq[:, x] = -1  # never resident here
+        n_owned = sum(1 for x in range(E) if x % world == rank) * L
+        budget_bytes = int(round(args.budget * n_owned)) * spec.expert_bytes
+    else:
+        budget_bytes = int(round(args.budget * L * E)) * spec.expert_bytes
+    resident = [(l, x) for (l, x) in ps.plan_residency(freq, budget_bytes, spec.expert_bytes)
+                if x % world == rank]
 
     lib = ps.load()
     predictor = C.c_void_p()
     ps.check(lib.ps_llapor_random(C.byref(spec), 256, 512, 32, 48, 3, C.byref(predictor)))
     t_create = time.perf_counter()
     e = eng.Engine(spec, gen, max_batch=B, weight_seed=args.weight_seed, gate=gate, budget_bytes=budget_bytes,
-                   resident=resident, policy=args.policy, predictor=predictor, device=local)
+                   resident=resident, policy=args.policy, predictor=predictor, device=local, ep=ep)
     t_create = time.perf_counter() - t_create
 
     # device-resident step inputs (layer-major), outputs
@@ -264,7 +286,7 @@ def run_ours(args):
     # Same steps with every expert resident (budget 100 %): the HBM-bound MoE layer.
     all_res = None
     prefill = None
-    if not args.no_all_resident:
+    if not args.no_all_resident and world == 1:
         PT = args.prefill_tokens
         e2 = eng.Engine(spec, gen, max_batch=max(B, PT), weight_seed=args.weight_seed, gate=gate,
                         budget_bytes=L * E * spec.expert_bytes, resident=[(l, x) for l in range(L) for x in range(E)],
@@ -316,6 +338,8 @@ def run_ours(args):
                    "combine_us_per_layer": st2["combine_ms_total"] * 1e3 / max(1, st2["layers"]),
                    "gpu_launches": st2["kernel_launches"]}
     lib.ps_llapor_free(predictor)
+    if ep is not None:
+        ep.close()
 
     if rank != 0:
         if dist:

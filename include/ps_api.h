@@ -217,6 +217,11 @@ ps_status ps_simulate_pipeline(const ps_pipeline_instance* inst, ps_policy polic
 ps_status ps_verify_timeline(const ps_timeline_event* events, int n_events,
                              const ps_pipeline_instance* inst, const ps_cost_params* params,
                              int* n_violations, char* msg_buf, int msg_cap);
+/* Same checks; measured != 0 for timelines recorded on the GPU (ps_engine_last_timeline):
+ * transfer durations are measured, so "atomic t_io interval" becomes "one interval". */
+ps_status ps_verify_timeline_ex(const ps_timeline_event* events, int n_events,
+                                const ps_pipeline_instance* inst, const ps_cost_params* params,
+                                int measured, int* n_violations, char* msg_buf, int msg_cap);
 /* compute_metrics (simulator.cpp:396-426). per_layer arrays nullable [L]. */
 typedef struct {
   int64_t makespan, decode_latency;
@@ -412,8 +417,20 @@ typedef struct {
 } ps_engine_stats;
 ps_status ps_engine_get_stats(ps_engine e, ps_engine_stats* out);
 ps_status ps_engine_reset_stats(ps_engine e);
-/* Measured timeline of the last step (events from CUDA events, us from step start). */
-ps_status ps_engine_last_timeline(ps_engine e, ps_timeline* out);
+/* Measured timeline of the last step, from the CUDA events the engine records (us from
+ * the step start): per layer an ATTENTION event for the scheduling-point phase
+ * (K1+K4+K2+counts D2H), GPU_EXPERT events for every routed expert's FFN launch, LOAD /
+ * PREFETCH events for every copy on the serial channel. truth_out [L*E] (nullable)
+ * receives the step's per-layer routed token counts and resident_out [L*E] (nullable)
+ * the resident flags, i.e. the PipelineInstance to check it against
+ * (ps_verify_timeline_ex, measured = 1). */
+ps_status ps_engine_last_timeline(ps_engine e, ps_timeline* out, int32_t* truth_out,
+                                  uint8_t* resident_out);
+/* Calibration (cost_model.cpp:45-72 fit + simulator cost semantics): replace the
+ * engine's PreSched costs with the means measured since the last stats reset —
+ * t_io = mean copy time per expert, t_g = mean FFN time per routed expert, t_attn =
+ * mean scheduling-point phase per layer (us). */
+ps_status ps_engine_calibrate(ps_engine e, ps_cost_params* out);
 
 #ifdef __cplusplus
 }

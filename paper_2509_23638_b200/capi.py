@@ -198,7 +198,10 @@ _SIGS = {
     "ps_engine_decode_step_host": (C.c_int, [_P, _P, _P, C.c_int, _P, _P]),
     "ps_engine_get_stats": (C.c_int, [_P, C.POINTER(EngineStats)]),
     "ps_engine_reset_stats": (C.c_int, [_P]),
-    "ps_engine_last_timeline": (C.c_int, [_P, C.POINTER(Timeline)]),
+    "ps_engine_last_timeline": (C.c_int, [_P, C.POINTER(Timeline), _P, _P]),
+    "ps_engine_calibrate": (C.c_int, [_P, C.POINTER(CostParams)]),
+    "ps_verify_timeline_ex": (C.c_int, [C.POINTER(TimelineEvent), C.c_int, C.POINTER(PipelineInstance),
+                                        C.POINTER(CostParams), C.c_int, C.POINTER(C.c_int), C.c_char_p, C.c_int]),
 }
 
 _lib = None

@@ -202,6 +202,8 @@ struct LayerDev {  // per-layer device outputs kept for the step
 struct FfnTiming {
   cudaEvent_t a, b;
   double bytes;
+  int layer;
+  std::vector<int> experts, tokens;  // routed experts of the launch (timeline export)
 };
 
 struct StallProbe {
@@ -288,6 +290,14 @@ struct ps_engine_s {
   std::vector<int32_t> ep_seg, ep_send_rows;  // per-layer receive segments / send rows
   int ep_rows_recv = 0;
 
+  // measured timeline of the last step (row f2 of SURVEY.md §8f)
+  int cur_layer = 0;
+  std::vector<int32_t> step_truth;             // [L*E] routed tokens per (layer, expert)
+  std::vector<ps_timeline_event> last_events;
+  std::vector<int64_t> last_layer_start, last_layer_end;
+  std::vector<int32_t> last_truth;
+  double copy_ms_total = 0, copies = 0, route_ms_total_cal = 0, ffn_expert_ms_total = 0, ffn_experts = 0;
+
   // scheduler state across layers
   ps_hit_stats stats[3];
   std::vector<std::unique_ptr<ps::IoJob>> jobs;  // owned for the step
@@ -367,10 +377,14 @@ void ffn(ps_engine_s& e, const ps_expert_group& g, const int32_t* counts_host, i
   if (timed) {
     b = take_event(e);
     PS_CUDA(cudaEventRecord(b, e.sc));
-    double bytes = 0;
+    FfnTiming t{a, b, 0.0, e.cur_layer, {}, {}};
     for (int i = 0; i < g.n; ++i)
-      if (counts_host[g.experts[i]] > 0) bytes += static_cast<double>(e.cfg.spec.expert_bytes);
-    e.ffn_t.push_back({a, b, bytes});
+      if (counts_host[g.experts[i]] > 0) {
+        t.bytes += static_cast<double>(e.cfg.spec.expert_bytes);
+        t.experts.push_back(g.experts[i]);
+        t.tokens.push_back(counts_host[g.experts[i]]);
+      }
+    e.ffn_t.push_back(std::move(t));
   }
 }
 
@@ -518,9 +532,11 @@ void decode_step(ps_engine_s& e, const float* hidden, const uint8_t* follow, int
 
   std::vector<ps_expert_load> cur, nxt, cpu_b(E), od_b(E), pf_b(E);
   std::vector<int32_t> counts_l(E), pred_l(E);
+  e.step_truth.assign(static_cast<size_t>(L) * E, 0);
 
   for (int l = 0; l < L; ++l) {
     const float* x = hidden + static_cast<size_t>(l) * B * H;
+    e.cur_layer = l;
     LayerDev& ld = e.layer[l];
     PhaseTiming ph{take_event(e), take_event(e), take_event(e), take_event(e)};
     PS_CUDA(cudaEventRecord(ph.route0, e.sc));
@@ -532,10 +548,10 @@ void decode_step(ps_engine_s& e, const float* hidden, const uint8_t* follow, int
     if (s != PS_OK) fail(s, ps_last_error());
     e.st.kernel_launches += 1;
     // --- K4 LLaPor: predicted histogram of layer l+1 -------------------------
-    // Prefill chunks (>= 4 routed rows per expert on average) activate every expert of
-    // the next layer with near certainty: the prediction is then the dense histogram
-    // B*k/E per expert and the LLaPor launch is skipped (decode always runs LLaPor).
-    const bool dense_next = B * K >= 4 * E && l + 1 < L;
+    // Prefill chunks (B > 64 and >= 16 routed rows per expert on average) activate every
+    // expert of the next layer with near certainty: the prediction is then the dense
+    // histogram B*k/E per expert and the LLaPor launch is skipped (decode always runs it).
+    const bool dense_next = e.prefill_mode && B * K >= 16 * E && l + 1 < L;
     const bool predict = e.cfg.predictor && l + 1 < L && !dense_next;
     if (predict) {
       s = ps_llapor_forward(e.cfg.predictor, l + 1, x, ld.ids, K, ld.weights, B, K, nullptr, nullptr, e.pred_dev,
@@ -623,14 +639,23 @@ void decode_step(ps_engine_s& e, const float* hidden, const uint8_t* follow, int
     if (!early) {
       ffn(e, grp, counts_l.data(), B, true, true);
     } else if (resident_timing < e.ffn_t.size()) {  // algorithmic bytes/flops: routed experts only
-      double bytes = 0, rows = 0;
+      FfnTiming& t = e.ffn_t[resident_timing];
+      double rows = 0;
+      t.bytes = 0;
+      t.experts.clear();
+      t.tokens.clear();
       for (int i = 0; i < grp.n; ++i) {
-        if (counts_l[grp.experts[i]] > 0) bytes += static_cast<double>(e.cfg.spec.expert_bytes);
-        rows += counts_l[grp.experts[i]];
+        const int m = counts_l[grp.experts[i]];
+        if (m > 0) {
+          t.bytes += static_cast<double>(e.cfg.spec.expert_bytes);
+          t.experts.push_back(grp.experts[i]);
+          t.tokens.push_back(m);
+        }
+        rows += m;
       }
-      e.ffn_t[resident_timing].bytes = bytes;
       e.st.ffn_flops_total += 6.0 * rows * e.H * e.F;
     }
+    std::copy(counts_l.begin(), counts_l.end(), e.step_truth.begin() + static_cast<size_t>(l) * E);
     for (int i = 0; i < grp.n; ++i) e.st.resident_hits += counts_l[grp.experts[i]] > 0;
 
     // Deferred HitStats for critical prefetches that targeted this layer (R2).
@@ -786,16 +811,39 @@ void decode_step(ps_engine_s& e, const float* hidden, const uint8_t* follow, int
 
   // --- measurement (CUDA events; no extra sync) ------------------------------------
   float ms = 0;
+  // Measured timeline (us from the step start) built from the same events.
+  auto at_us = [&](cudaEvent_t ev) {
+    float t = 0;
+    PS_CUDA(cudaEventElapsedTime(&t, e.ev_step0, ev));
+    return static_cast<int64_t>(std::llround(static_cast<double>(t) * 1000.0));
+  };
+  e.last_events.clear();
+  e.last_layer_start.assign(L, 0);
+  e.last_layer_end.assign(L, 0);
+  e.last_truth = e.step_truth;
   for (auto& t : e.ffn_t) {
     PS_CUDA(cudaEventElapsedTime(&ms, t.a, t.b));
     e.st.ffn_ms_total += ms;
     e.st.ffn_bytes_total += t.bytes;
+    if (!t.experts.empty()) {
+      e.ffn_expert_ms_total += ms;
+      e.ffn_experts += static_cast<double>(t.experts.size());
+    }
+    const int64_t a = at_us(t.a), b = at_us(t.b);
+    for (size_t i = 0; i < t.experts.size(); ++i)
+      e.last_events.push_back({a, b, PS_RES_GPU, PS_EV_GPU_EXPERT, t.layer, t.experts[i], t.tokens[i]});
   }
-  for (auto& p : e.phase_t) {
+  for (size_t l = 0; l < e.phase_t.size(); ++l) {
+    auto& p = e.phase_t[l];
     PS_CUDA(cudaEventElapsedTime(&ms, p.route0, p.route1));
     e.st.route_phase_ms_total += ms;
+    e.route_ms_total_cal += ms;
     PS_CUDA(cudaEventElapsedTime(&ms, p.comb0, p.comb1));
     e.st.combine_ms_total += ms;
+    e.last_layer_start[l] = at_us(p.route0);
+    e.last_layer_end[l] = at_us(p.comb1);
+    e.last_events.push_back({e.last_layer_start[l], at_us(p.route1), PS_RES_GPU, PS_EV_ATTENTION,
+                             static_cast<int32_t>(l), -1, 0});
   }
   for (auto& p : e.stall_t) {
     PS_CUDA(cudaEventElapsedTime(&ms, p.before, p.after));
@@ -805,7 +853,17 @@ void decode_step(ps_engine_s& e, const float* hidden, const uint8_t* follow, int
     if (j->state.load() != 1) continue;
     PS_CUDA(cudaEventElapsedTime(&ms, j->start_ev, j->done_ev));
     e.st.h2d_busy_ms += ms;
+    e.copy_ms_total += ms;
+    e.copies += 1;
+    e.last_events.push_back({at_us(j->start_ev), at_us(j->done_ev), PS_RES_IO,
+                             j->kind == kOnDemand ? PS_EV_LOAD : PS_EV_PREFETCH, j->layer, j->expert, j->tokens});
   }
+  std::stable_sort(e.last_events.begin(), e.last_events.end(),
+                   [](const ps_timeline_event& a, const ps_timeline_event& b) {
+                     if (a.resource != b.resource) return a.resource < b.resource;
+                     if (a.t_start != b.t_start) return a.t_start < b.t_start;
+                     return a.t_end < b.t_end;
+                   });
   PS_CUDA(cudaEventElapsedTime(&ms, e.ev_step0, e.ev_step1));
   e.st.step_ms_total += ms;
   e.st.steps += 1;
@@ -1065,8 +1123,34 @@ ps_status ps_engine_reset_stats(ps_engine e) {
   });
 }
 
-ps_status ps_engine_last_timeline(ps_engine e, ps_timeline* out) {
-  return guarded([&] { fail(PS_ERUNTIME, "ps_engine_last_timeline: not implemented yet"); });
+ps_status ps_engine_last_timeline(ps_engine e, ps_timeline* out, int32_t* truth_out, uint8_t* resident_out) {
+  return guarded([&] {
+    require(e && out, "ps_engine_last_timeline: null argument");
+    const int n = static_cast<int>(e->last_events.size());
+    if (n > out->cap_events) fail(PS_ERANGE, "ps_engine_last_timeline: event buffer too small (" + std::to_string(n) + ")");
+    std::copy(e->last_events.begin(), e->last_events.end(), out->events);
+    out->n_events = n;
+    out->makespan = 0;
+    for (const auto& ev : e->last_events) out->makespan = std::max(out->makespan, ev.t_end);
+    if (out->layer_start) std::copy(e->last_layer_start.begin(), e->last_layer_start.end(), out->layer_start);
+    if (out->layer_end) std::copy(e->last_layer_end.begin(), e->last_layer_end.end(), out->layer_end);
+    if (truth_out) std::copy(e->last_truth.begin(), e->last_truth.end(), truth_out);
+    if (resident_out) std::copy(e->resident.begin(), e->resident.end(), resident_out);
+  });
+}
+
+ps_status ps_engine_calibrate(ps_engine e, ps_cost_params* out) {
+  return guarded([&] {
+    ps_cost_params c = e->cfg.cost;
+    if (e->copies > 0) c.t_io = std::max<int64_t>(1, std::llround(1000.0 * e->copy_ms_total / e->copies));
+    if (e->ffn_experts > 0) c.t_g = std::max<int64_t>(0, std::llround(1000.0 * e->ffn_expert_ms_total / e->ffn_experts));
+    if (e->st.layers > 0) c.t_attn = std::llround(1000.0 * e->route_ms_total_cal / static_cast<double>(e->st.layers));
+    if (c.t_g >= c.t_io) c.t_g = c.t_io - 1;  // CostParams invariant t_g < t_io (cost_model.cpp:16)
+    if (ps_cost_params_validate(&c) != PS_OK) fail(PS_EINVAL, ps_last_error());
+    e->cfg.cost = c;
+    e->st.cost = c;
+    if (out) *out = c;
+  });
 }
 
 }  // extern "C"

@@ -251,8 +251,12 @@ void simulate(const ps_pipeline_instance& inst, ps_policy policy, ps_plan_fn pla
   out.n_events = static_cast<int32_t>(events.size());
 }
 
+// measured = true: a timeline recorded on the GPU (engine.cpp) — transfer durations
+// are measured, so the "atomic t_io interval" rule is replaced by "a transfer is one
+// interval" (it cannot be split: one cudaMemcpyAsync per expert), all other
+// invariants are the reference's.
 std::vector<std::string> verify(const ps_timeline_event* ev, int n, const ps_pipeline_instance& inst,
-                                const ps_cost_params& params) {
+                                const ps_cost_params& params, bool measured = false) {
   std::vector<std::string> v;
   const int L = inst.num_layers, E = inst.experts;
   auto truth = [&](int l, int e) { return inst.truth[static_cast<size_t>(l) * E + e]; };
@@ -266,7 +270,7 @@ std::vector<std::string> verify(const ps_timeline_event* ev, int n, const ps_pip
     if (io[i]->t_start < io[i - 1]->t_end)
       v.push_back("serial-io: overlapping transfers at t=" + std::to_string(io[i]->t_start));
   for (auto* e : io)
-    if (e->t_end - e->t_start != params.t_io)
+    if (measured ? e->t_end < e->t_start : e->t_end - e->t_start != params.t_io)
       v.push_back("non-interruptible: transfer of expert " + std::to_string(e->expert) +
                   " is not an atomic t_io interval");
 
@@ -346,8 +350,14 @@ ps_status ps_simulate_pipeline(const ps_pipeline_instance* inst, ps_policy polic
 
 ps_status ps_verify_timeline(const ps_timeline_event* events, int n_events, const ps_pipeline_instance* inst,
                              const ps_cost_params* params, int* n_violations, char* msg_buf, int msg_cap) {
+  return ps_verify_timeline_ex(events, n_events, inst, params, 0, n_violations, msg_buf, msg_cap);
+}
+
+ps_status ps_verify_timeline_ex(const ps_timeline_event* events, int n_events, const ps_pipeline_instance* inst,
+                                const ps_cost_params* params, int measured, int* n_violations, char* msg_buf,
+                                int msg_cap) {
   return guarded([&] {
-    std::vector<std::string> v = verify(events, n_events, *inst, *params);
+    std::vector<std::string> v = verify(events, n_events, *inst, *params, measured != 0);
     *n_violations = static_cast<int>(v.size());
     if (msg_buf && msg_cap > 0) {
       std::string all;
