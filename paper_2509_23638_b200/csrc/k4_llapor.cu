@@ -32,6 +32,7 @@ constexpr int kMaxE = 256;
 
 struct NetDev {  // device pointers into one allocation; kernel parameter
   int P, in_dim, width, E, n_blocks, n_res, valid;
+  int mlp_floats;  // contiguous MLP parameters from w[0] to the end of out_b (staged in smem)
   int dims[kMaxBlocks + 1];
   const float* mean;
   const float* comp;
@@ -118,7 +119,7 @@ __device__ void affine_tokens(const float* __restrict__ W, const float* __restri
 #pragma unroll
       for (int u = 0; u < kU; ++u) {
         const int c = c0 + lane + 32 * u;
-        w[u] = c < cols ? __ldg(W + static_cast<size_t>(r) * cols + c) : 0.f;
+        w[u] = c < cols ? W[static_cast<size_t>(r) * cols + c] : 0.f;
       }
 #pragma unroll
       for (int u = 0; u < kU; ++u) {
@@ -129,7 +130,7 @@ __device__ void affine_tokens(const float* __restrict__ W, const float* __restri
         }
       }
     }
-    const float bias = __ldg(bvec + r);
+    const float bias = bvec[r];
 #pragma unroll
     for (int t = 0; t < kMlpTok; ++t) {
       const float s = warp_sum(acc[t]) + bias;
@@ -144,7 +145,8 @@ __device__ void affine_tokens(const float* __restrict__ W, const float* __restri
 __global__ void __launch_bounds__(kMlpThreads)
 mlp_kernel(const __grid_constant__ NetDev net, const float* __restrict__ part, int n_part,
            const int32_t* __restrict__ prev_ids, int k_prev, const float* __restrict__ prev_w, int B, int k,
-           float* __restrict__ logits_out, int32_t* __restrict__ ids_out, int32_t* __restrict__ pred_counts) {
+           float* __restrict__ logits_out, int32_t* __restrict__ ids_out, int32_t* __restrict__ pred_counts,
+           int stage_w) {
   extern __shared__ float smem[];
   const int P = net.P, E = net.E, D = net.in_dim, Wd = net.width;
   const int t0 = blockIdx.x * kMlpTok, nt = min(kMlpTok, B - t0);
@@ -155,6 +157,22 @@ mlp_kernel(const __grid_constant__ NetDev net, const float* __restrict__ part, i
   float* h2 = h1 + kMlpTok * maxh;
   float* h3 = h2 + kMlpTok * maxh;
   float* lg = h3 + kMlpTok * maxh;      // [kMlpTok][E]
+  float* wsm = lg + kMlpTok * E;        // [mlp_floats] staged MLP parameters (if they fit)
+
+  // Stage every MLP parameter of the net (<= ~40K floats) with all threads at once: one
+  // L2 round trip instead of one per row chunk of every layer (latency-bound kernel).
+  NetDev n = net;
+  if (stage_w) {
+    const float4* src = reinterpret_cast<const float4*>(net.w[0]);
+    float4* dst = reinterpret_cast<float4*>(wsm);
+    for (int i = threadIdx.x; i < net.mlp_floats / 4; i += blockDim.x) dst[i] = __ldg(src + i);
+    auto tr = [&](const float* p) { return wsm + (p - net.w[0]); };
+    for (int j = 0; j < net.n_blocks; ++j) { n.w[j] = tr(net.w[j]); n.b[j] = tr(net.b[j]); }
+    for (int j = 0; j < net.n_res; ++j) { n.rw[j] = tr(net.rw[j]); n.rb[j] = tr(net.rb[j]); }
+    n.gate_w = tr(net.gate_w);
+    n.out_w = tr(net.out_w);
+    n.out_b = tr(net.out_b);
+  }
 
   for (int i = threadIdx.x; i < kMlpTok * D; i += blockDim.x) {
     const int t = i / D, c = i % D, tok = t0 + t;
@@ -180,7 +198,7 @@ mlp_kernel(const __grid_constant__ NetDev net, const float* __restrict__ part, i
   float* bufs[2] = {h1, h2};
   for (int j = 0; j < net.n_blocks; ++j) {
     float* o = bufs[j & 1];
-    affine_tokens(net.w[j], net.b[j], net.dims[j + 1], net.dims[j], cur, cur_stride, o, maxh, nt, true);
+    affine_tokens(n.w[j], n.b[j], net.dims[j + 1], net.dims[j], cur, cur_stride, o, maxh, nt, true);
     __syncthreads();
     cur = o;
     cur_stride = maxh;
@@ -192,7 +210,7 @@ mlp_kernel(const __grid_constant__ NetDev net, const float* __restrict__ part, i
     float* u = nullptr;
     for (int j = 0; j < net.n_res; ++j) {
       u = ubuf[j & 1];
-      affine_tokens(net.rw[j], net.rb[j], Wd, Wd, uin, maxh, u, maxh, nt, true);
+      affine_tokens(n.rw[j], n.rb[j], Wd, Wd, uin, maxh, u, maxh, nt, true);
       __syncthreads();
       uin = u;
     }
@@ -200,7 +218,7 @@ mlp_kernel(const __grid_constant__ NetDev net, const float* __restrict__ part, i
     const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
     for (int t = warp; t < nt; t += blockDim.x >> 5) {
       float d = 0.f;
-      for (int i = lane; i < P; i += 32) d += net.gate_w[i] * feat[t * D + i];
+      for (int i = lane; i < P; i += 32) d += n.gate_w[i] * feat[t * D + i];
       d = warp_sum(d);
       if (lane == 0) s_gate[t] = 1.0f / (1.0f + expf(-(d + net.gate_b)));
     }
@@ -212,7 +230,7 @@ mlp_kernel(const __grid_constant__ NetDev net, const float* __restrict__ part, i
     __syncthreads();
     cur = u;
   }
-  affine_tokens(net.out_w, net.out_b, E, Wd, cur, maxh, lg, E, nt, false);
+  affine_tokens(n.out_w, n.out_b, E, Wd, cur, maxh, lg, E, nt, false);
   __syncthreads();
   if (logits_out)
     for (int i = threadIdx.x; i < nt * E; i += blockDim.x) logits_out[static_cast<size_t>(t0) * E + i] = lg[i];
@@ -302,6 +320,7 @@ void upload(ps_llapor_s& m, int layer, const HostNet& hn) {
   d.gate_b = static_cast<float>(hn.gate_b);
   d.out_w = dev + o_ow;
   d.out_b = dev + o_ob;
+  d.mlp_floats = static_cast<int>(o_ob + ((hn.out.b.size() + 3) / 4) * 4 - o_w[0]);
   d.valid = 1;
   if (layer >= static_cast<int>(m.nets.size())) m.nets.resize(layer + 1);
   m.nets[layer] = d;
@@ -476,14 +495,16 @@ ps_status ps_llapor_forward(ps_llapor m, int layer, const float* hidden, const i
     PS_LAUNCH_CHECK("pca_partial_kernel");
     int maxh = net.width;
     for (int j = 1; j <= net.n_blocks; ++j) maxh = std::max(maxh, net.dims[j]);
-    const size_t smem = sizeof(float) * kMlpTok * (net.in_dim + 3 * maxh + net.E);
+    size_t smem = sizeof(float) * kMlpTok * (net.in_dim + 3 * maxh + net.E);
+    const int stage_w = smem + sizeof(float) * net.mlp_floats <= 200 * 1024 ? 1 : 0;
+    if (stage_w) smem += sizeof(float) * net.mlp_floats;
     static int smem_set = 0;
     if (static_cast<int>(smem) > smem_set) {
       PS_CUDA(cudaFuncSetAttribute(mlp_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(smem)));
       smem_set = static_cast<int>(smem);
     }
     mlp_kernel<<<(B + kMlpTok - 1) / kMlpTok, kMlpThreads, smem, s>>>(net, part, n_part, prev_ids, k_prev,
-                                                                      prev_weights, B, k, logits, ids, pred_counts);
+                                                                      prev_weights, B, k, logits, ids, pred_counts, stage_w);
     PS_LAUNCH_CHECK("mlp_kernel");
   });
 }

@@ -170,6 +170,44 @@ class Engine:
         d["cost"] = dict(t_io=c.t_io, t_g=c.t_g, t_attn=c.t_attn, beta=c.beta, startup=c.startup)
         return d
 
+    def last_timeline(self, cap: int = 1 << 16):
+        """Measured timeline of the last step: (events, truth [L,E], resident [L,E],
+        layer_start, layer_end) — events as (t_start, t_end, resource, kind, layer,
+        expert, tokens) in us from the step start."""
+        L, E = self.spec.num_layers, self.spec.experts_per_layer
+        ev = (capi.TimelineEvent * cap)()
+        ls, le = (C.c_int64 * L)(), (C.c_int64 * L)()
+        tl = capi.Timeline(ev, cap, 0, ls, le, 0, None)
+        truth = np.zeros((L, E), np.int32)
+        res = np.zeros((L, E), np.uint8)
+        check(self.lib.ps_engine_last_timeline(self.h, C.byref(tl), truth.ctypes.data_as(C.c_void_p),
+                                               res.ctypes.data_as(C.c_void_p)))
+        events = [(ev[i].t_start, ev[i].t_end, ev[i].resource, ev[i].kind, ev[i].layer, ev[i].expert, ev[i].tokens)
+                  for i in range(tl.n_events)]
+        return events, truth, res, list(ls), list(le)
+
+    def verify_last_step(self):
+        """verify_timeline (simulator.cpp:323-394) on the measured timeline of the last
+        step (measured mode: transfer durations are not the modelled t_io)."""
+        events, truth, res, _, _ = self.last_timeline()
+        from . import _instance
+        inst, keep = _instance(truth, np.zeros_like(truth), res)
+        arr = (capi.TimelineEvent * max(1, len(events)))(*[capi.TimelineEvent(*x) for x in events])
+        n = C.c_int()
+        buf = C.create_string_buffer(1 << 16)
+        st = self.stats()["cost"]
+        params = capi.CostParams(st["t_io"], st["t_g"], st["t_attn"], st["beta"], st["startup"], 0)
+        check(self.lib.ps_verify_timeline_ex(arr, len(events), C.byref(inst), C.byref(params), 1, C.byref(n), buf,
+                                             len(buf)))
+        del keep
+        return [m for m in buf.value.decode().split("\n") if m]
+
+    def calibrate(self):
+        """Replace PreSched costs with the measured means (ps_engine_calibrate)."""
+        c = capi.CostParams()
+        check(self.lib.ps_engine_calibrate(self.h, C.byref(c)))
+        return dict(t_io=c.t_io, t_g=c.t_g, t_attn=c.t_attn, beta=c.beta, startup=c.startup)
+
     def reset_stats(self):
         check(self.lib.ps_engine_reset_stats(self.h))
 

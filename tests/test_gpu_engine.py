@@ -86,6 +86,28 @@ def test_engine_prefill_chunk_uses_tcgen05_and_matches_oracle(torch_cuda, budget
     assert np.linalg.norm(y - y_ref) / np.linalg.norm(y_ref) < BF16_RTOL
 
 
+@pytest.mark.parametrize("budget,policy", [(0.5, "presched"), (0.25, "fixed:2"), (0.0, "ondemand")])
+def test_measured_timeline_satisfies_reference_invariants(torch_cuda, budget, policy):
+    """The GPU run's own timeline (CUDA events) passes verify_timeline: serial I/O,
+    one interval per transfer, every routed (layer, expert) computed exactly once,
+    causality (compute after its copy), dual on-demand buffer."""
+    spec = _small_spec(L=4, E=8, H=256, F=512)
+    cfg = ps.TraceGenConfig(*[ps.GROUP_DEFAULT_GEN[g] for g in ("input", "middle", "output")])
+    gate, hidden, follow, _ = ps.trace_inputs(cfg, spec, 8, 5)
+    with eng.Engine(spec, cfg, budget_fraction=budget, max_batch=8, weight_seed=1, gate=gate, trace_hidden=hidden,
+                    trace_follow=follow, policy=policy) as e:
+        e.step_host(hidden, follow)
+        events, truth, res, ls, le = e.last_timeline()
+        assert e.verify_last_step() == []
+        kinds = {ev[3] for ev in events}
+        assert 0 in kinds and 1 in kinds  # attention-phase and expert events
+        if budget < 1.0:
+            assert 3 in kinds  # on-demand loads
+        assert all(a <= b for a, b in zip(ls, le)) and all(le[i] <= ls[i + 1] for i in range(len(ls) - 1))
+        cost = e.calibrate()
+        assert cost["t_io"] > cost["t_g"] >= 0 and cost["t_attn"] > 0
+
+
 def test_engine_batch_one(torch_cuda):
     spec = _small_spec()
     y, y_ref, *_ = _run(spec, 1, 0.5)
