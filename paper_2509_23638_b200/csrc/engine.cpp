@@ -219,7 +219,7 @@ struct PhaseTiming {  // scheduling-point phase (K1+K4+K2+D2H) and combine, per 
 
 struct ps_engine_s {
   ps_engine_config cfg{};
-  int L = 0, E = 0, K = 0, H = 0, F = 0, maxB = 0, n_split = 1;
+  int L = 0, E = 0, K = 0, H = 0, F = 0, maxB = 0, n_split = 1, step_split = 1;
   uint64_t slab_elems = 0;
   cudaStream_t sc = nullptr;  // compute stream
   std::unique_ptr<ps::IoChannel> io;
@@ -368,7 +368,7 @@ void ffn(ps_engine_s& e, const ps_expert_group& g, const int32_t* counts_host, i
     e.st.tc_launches += 2;
   } else {
     s = ps_expert_ffn(&g, counts_host, src.offsets_dev, src.perm_dev, src.k, src.x, e.H, e.F, e.hbuf, e.y_part,
-                      e.n_split, src.rows, e.sc);
+                      e.step_split, src.rows, e.sc);
   }
   if (s != PS_OK) fail(s, ps_last_error());
   e.st.ffn_launches += 2;
@@ -501,7 +501,7 @@ ps_status ep_combine_rows(ps_engine_s& e, int B, const LayerDev& ld, float* y_l)
   const int rows = e.ep_rows_recv;
   ps_status st = PS_OK;
   if (rows > 0)
-    st = ps_combine(e.y_part, e.n_split, e.ep_plan_dev + (E + 1) + e.rows_max, e.ep_zeros, e.ep_ones, rows, 1, 1, H,
+    st = ps_combine(e.y_part, e.step_split, e.ep_plan_dev + (E + 1) + e.rows_max, e.ep_zeros, e.ep_ones, rows, 1, 1, H,
                     e.ep_y_recv, e.sc);
   if (st != PS_OK) return st;
   std::vector<uint64_t> sb(G), rb(G);
@@ -519,6 +519,9 @@ void decode_step(ps_engine_s& e, const float* hidden, const uint8_t* follow, int
   const int L = e.L, E = e.E, K = e.K, H = e.H;
   require(B >= 1 && B <= e.maxB, "decode_step: batch out of range");
   e.prefill_mode = B > kDecodeMaxBatch;
+  // Down-projection split-K of the decode GEMV (more CTAs for single-expert on-demand
+  // launches); the tcgen05 prefill path writes one split, so prefill steps use 1.
+  e.step_split = e.prefill_mode ? 1 : e.n_split;
   e.jobs.clear();
   e.event_next = 0;
   e.job_event_next = 0;
@@ -750,7 +753,7 @@ void decode_step(ps_engine_s& e, const float* hidden, const uint8_t* follow, int
     // --- combine -> y_l ------------------------------------------------------------
     PS_CUDA(cudaEventRecord(ph.comb0, e.sc));
     if (!e.ep) {
-      s = ps_combine(e.y_part, e.n_split, e.inv, ld.ids, ld.weights, B, K, E, H, y + static_cast<size_t>(l) * B * H,
+      s = ps_combine(e.y_part, e.step_split, e.inv, ld.ids, ld.weights, B, K, E, H, y + static_cast<size_t>(l) * B * H,
                      e.sc);
     } else {
       s = ep_combine_rows(e, B, ld, y + static_cast<size_t>(l) * B * H);

@@ -273,9 +273,11 @@ using namespace ps;
 extern "C" {
 
 int ps_ffn_down_splits(int H, int F) {
+  // K is split across the warps of each CTA; a long down projection (Mixtral F=14336)
+  // is additionally split in two across CTAs so a single on-demand expert still puts
+  // ~26 warps on every SM (the register-limited occupancy) instead of ~14.
   (void)H;
-  (void)F;
-  return 1;  // K is split across the warps of each CTA; no global partials needed
+  return F >= 8192 ? 2 : 1;
 }
 
 ps_status ps_expert_ffn(const ps_expert_group* group, const int32_t* counts_host, const int32_t* offsets,

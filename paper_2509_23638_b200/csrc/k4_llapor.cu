@@ -109,32 +109,43 @@ __device__ __forceinline__ float gelu_erf(float v) { return 0.5f * v * (1.0f + e
 __device__ void affine_tokens(const float* __restrict__ W, const float* __restrict__ bvec, int rows, int cols,
                               const float* in, int in_stride, float* out, int out_stride, int nt, bool gelu) {
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31, nw = blockDim.x >> 5;
-  constexpr int kU = 8;  // weight loads in flight per lane (latency-bound: one L2 round trip per 256 cols)
-  for (int r = warp; r < rows; r += nw) {
-    float acc[kMlpTok];
+  constexpr int kU = 4;  // weight loads in flight per lane and row
+  // Two rows per warp pass: every activation read from shared memory feeds two FMAs.
+  for (int r0 = 2 * warp; r0 < rows; r0 += 2 * nw) {
+    const bool two = r0 + 1 < rows;
+    float acc[2][kMlpTok];
 #pragma unroll
-    for (int t = 0; t < kMlpTok; ++t) acc[t] = 0.f;
+    for (int t = 0; t < kMlpTok; ++t) acc[0][t] = acc[1][t] = 0.f;
     for (int c0 = 0; c0 < cols; c0 += 32 * kU) {
-      float w[kU];
+      float w0[kU], w1[kU];
 #pragma unroll
       for (int u = 0; u < kU; ++u) {
         const int c = c0 + lane + 32 * u;
-        w[u] = c < cols ? W[static_cast<size_t>(r) * cols + c] : 0.f;
+        w0[u] = c < cols ? W[static_cast<size_t>(r0) * cols + c] : 0.f;
+        w1[u] = c < cols && two ? W[static_cast<size_t>(r0 + 1) * cols + c] : 0.f;
       }
 #pragma unroll
       for (int u = 0; u < kU; ++u) {
         const int c = c0 + lane + 32 * u;
         if (c < cols) {
 #pragma unroll
-          for (int t = 0; t < kMlpTok; ++t) acc[t] += w[u] * in[t * in_stride + c];
+          for (int t = 0; t < kMlpTok; ++t) {
+            const float a = in[t * in_stride + c];
+            acc[0][t] += w0[u] * a;
+            acc[1][t] += w1[u] * a;
+          }
         }
       }
     }
-    const float bias = bvec[r];
+    const float b0 = bvec[r0], b1 = two ? bvec[r0 + 1] : 0.f;
 #pragma unroll
     for (int t = 0; t < kMlpTok; ++t) {
-      const float s = warp_sum(acc[t]) + bias;
-      if (lane == 0 && t < nt) out[t * out_stride + r] = gelu ? gelu_erf(s) : s;
+      const float s0 = warp_sum(acc[0][t]) + b0;
+      const float s1 = warp_sum(acc[1][t]) + b1;
+      if (lane == 0 && t < nt) {
+        out[t * out_stride + r0] = gelu ? gelu_erf(s0) : s0;
+        if (two) out[t * out_stride + r0 + 1] = gelu ? gelu_erf(s1) : s1;
+      }
     }
   }
 }
@@ -174,17 +185,32 @@ mlp_kernel(const __grid_constant__ NetDev net, const float* __restrict__ part, i
     n.out_b = tr(net.out_b);
   }
 
-  for (int i = threadIdx.x; i < kMlpTok * D; i += blockDim.x) {
-    const int t = i / D, c = i % D, tok = t0 + t;
-    float v = 0.f;
-    if (t < nt) {
+  // PCA partial sums (fixed order) + features; 4 elements per thread per pass with all
+  // their partial loads issued together (latency-bound prologue).
+  constexpr int kMaxParts = 16;
+  for (int i0 = threadIdx.x; i0 < kMlpTok * D; i0 += 4 * blockDim.x) {
+    float v[4];
+#pragma unroll
+    for (int q = 0; q < 4; ++q) {
+      const int i = i0 + q * blockDim.x;
+      v[q] = 0.f;
+      if (i >= kMlpTok * D) continue;
+      const int t = i / D, c = i % D, tok = t0 + t;
+      if (t >= nt) continue;
       if (c < P) {
-        for (int s = 0; s < n_part; ++s) v += part[(static_cast<size_t>(s) * B + tok) * P + c];
+        float pv[kMaxParts];
+#pragma unroll
+        for (int s = 0; s < kMaxParts; ++s)
+          pv[s] = s < n_part ? part[(static_cast<size_t>(s) * B + tok) * P + c] : 0.f;
+#pragma unroll
+        for (int s = 0; s < kMaxParts; ++s) v[q] += pv[s];
       } else if (c >= P + E) {
-        v = prev_w[static_cast<size_t>(tok) * E + (c - P - E)];
+        v[q] = prev_w[static_cast<size_t>(tok) * E + (c - P - E)];
       }
     }
-    feat[i] = v;
+#pragma unroll
+    for (int q = 0; q < 4; ++q)
+      if (i0 + q * blockDim.x < kMlpTok * D) feat[i0 + q * blockDim.x] = v[q];
   }
   __syncthreads();
   for (int i = threadIdx.x; i < nt * k_prev; i += blockDim.x) {
@@ -484,6 +510,7 @@ ps_status ps_llapor_forward(ps_llapor m, int layer, const float* hidden, const i
       fail(PS_ERANGE, "llapor net for layer " + std::to_string(layer) + " is untrained/out of range");
     const NetDev& net = m->nets[layer];
     require(k >= 1 && k <= net.E && k_prev >= 1 && k_prev <= 32 && B >= 0, "ps_llapor_forward: bad k/B");
+    require(m->spec.hidden_dim <= 16 * kPcaChunk, "ps_llapor_forward: hidden_dim > 8192 unsupported");
     cudaStream_t s = as_stream(stream);
     if (pred_counts) PS_CUDA(cudaMemsetAsync(pred_counts, 0, sizeof(int32_t) * net.E, s));
     if (B == 0) return;
