@@ -354,6 +354,15 @@ def run_ours(args):
     # 3*H*F*2 (weights; activations are <0.1% at decode)
     ffn_bytes = ffn_bytes_total(st, spec)
     achieved = ffn_bytes / (ffn_ms / 1e3) / 1e9 if ffn_ms > 0 else 0.0
+    # DRAM traffic per launch from the committed ncu --set full capture of the same kernel
+    # (profiles/r01_ffn_decode_traffic.json): measured bytes / algorithmic bytes, applied
+    # to this run's algorithmic bytes per launch.
+    traffic, traffic_src = None, None
+    tpath = ROOT / "profiles" / "r01_ffn_decode_traffic.json"
+    if tpath.exists():
+        tj = json.loads(tpath.read_text())
+        traffic = tj["traffic_over_algorithmic"] * ffn_bytes / ffn_launches
+        traffic_src = f"{tj['source']}: traffic/algorithmic = {tj['traffic_over_algorithmic']:.4f}"
     h2d_gbs = st["h2d_bytes"] / (st["h2d_busy_ms"] / 1e3) / 1e9 if st["h2d_busy_ms"] > 0 else 0.0
     hidden_frac = 1.0 - st["compute_wait_ms"] / st["h2d_busy_ms"] if st["h2d_busy_ms"] > 0 else 1.0
     threads = os.cpu_count() or 1
@@ -368,7 +377,7 @@ def run_ours(args):
                 "d2h_bytes_per_step": d2h_out, "timing": "host wall-clock around ps_engine_decode_step_host"},
         "roofline": {"kernel": "K3 decode SwiGLU expert FFN (gate_up + down)", "bound": "hbm",
                      "achieved": achieved, "peak": peak_hbm, "peak_kind": peak_kind, "unit": "GB/s",
-                     "frac": achieved / peak_hbm, "traffic": None,
+                     "frac": achieved / peak_hbm, "traffic": traffic, "traffic_source": traffic_src,
                      "algorithmic_bytes_per_launch": ffn_bytes / ffn_launches,
                      "avg_launch_us": ffn_ms * 1e3 / ffn_launches},
         "h2d": {"achieved_gbs": h2d_gbs, "peak_gbs": PCIE_H2D_PEAK_GBS, "frac": h2d_gbs / PCIE_H2D_PEAK_GBS,
