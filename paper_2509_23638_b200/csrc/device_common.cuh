@@ -27,6 +27,28 @@ __device__ __forceinline__ float warp_max(float v) {
   return v;
 }
 
+// Reduce N per-lane partial sums across the warp at once (N a power of two <= 32):
+// a butterfly that halves the live values every step (N-1 shuffles + log2(32/N) more,
+// instead of 5N). On return v[0] of lane L holds the full sum of value index L % N.
+template <int N>
+__device__ __forceinline__ float warp_transpose_sum(float (&v)[N]) {
+  static_assert(N >= 1 && N <= 32 && (N & (N - 1)) == 0, "N must be a power of two <= 32");
+  const int lane = threadIdx.x & 31;
+#pragma unroll
+  for (int o = N / 2; o >= 1; o >>= 1) {
+    const bool upper = lane & o;
+#pragma unroll
+    for (int i = 0; i < o; ++i) {
+      const float send = upper ? v[i] : v[i + o];
+      const float keep = upper ? v[i + o] : v[i];
+      v[i] = keep + __shfl_xor_sync(0xffffffffu, send, o);
+    }
+  }
+#pragma unroll
+  for (int o = N; o < 32; o <<= 1) v[0] += __shfl_xor_sync(0xffffffffu, v[0], o);
+  return v[0];
+}
+
 // Warp arg-max with the reference's tie-break (value desc, lower index first,
 // workload.cpp:113-116). Invalid lanes pass idx = INT_MAX.
 __device__ __forceinline__ void warp_argmax(float& v, int& idx) {
@@ -53,6 +75,15 @@ __device__ __forceinline__ uint4 ldg_stream(const void* p) {
 __device__ __forceinline__ uint4 ldg_keep(const void* p) {
   return __ldg(reinterpret_cast<const uint4*>(p));
 }
+
+// Asynchronous 16-byte global -> shared copies (LDGSTS): a thread can have all of its
+// copies in flight at once, so staging N KiB costs one memory round trip instead of
+// one per loop iteration. Call cp_async_wait_all() + __syncthreads() before use.
+__device__ __forceinline__ void cp_async16(void* smem_dst, const void* gmem_src) {
+  const uint32_t d = static_cast<uint32_t>(__cvta_generic_to_shared(smem_dst));
+  asm volatile("cp.async.cg.shared.global [%0], [%1], 16;" ::"r"(d), "l"(gmem_src) : "memory");
+}
+__device__ __forceinline__ void cp_async_wait_all() { asm volatile("cp.async.wait_all;" ::: "memory"); }
 
 // Counter-based weight hash (splitmix64 finaliser).
 __host__ __device__ __forceinline__ uint64_t mix64(uint64_t x) {

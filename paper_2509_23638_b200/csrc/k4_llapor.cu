@@ -7,7 +7,7 @@
 //
 // Two launches per predicted layer:
 //  pca_partial_kernel — HBM-bound skinny GEMM over the [P, H] component matrix (the
-//               dominant bytes, 8 MiB at P=512, H=4096): grid (P/8, H/512), one row per
+//               dominant bytes, 8 MiB at P=512, H=4096): grid (P/16, H/512), two rows per
 //               warp, the centred x chunk staged once per CTA; partial sums per H chunk
 //               (deterministic, summed in fixed order by the MLP kernel).
 //  mlp_kernel — 16 tokens per CTA: feature concat [pca | onehot(prev top-k) | prev
@@ -44,6 +44,8 @@ struct NetDev {  // device pointers into one allocation; kernel parameter
   float gate_b;
   const float* out_w;
   const float* out_b;
+  // float offsets of the MLP parameters from w[0] (addresses into the smem-staged copy)
+  int o_w[kMaxBlocks], o_b[kMaxBlocks], o_rw[kMaxBlocks], o_rb[kMaxBlocks], o_gate, o_ow, o_ob;
 };
 
 }  // namespace ps
@@ -58,71 +60,119 @@ struct ps_llapor_s {
 namespace ps {
 namespace {
 
-constexpr int kPcaRows = 8;      // component rows per CTA (one warp each)
+constexpr int kPcaWarps = 8;     // warps per CTA (two component rows each)
 constexpr int kPcaChunk = 512;   // H elements per CTA (grid.y splits H)
 constexpr int kPcaTok = 16;      // tokens per pass
 constexpr int kMlpTok = 16;      // tokens per MLP CTA
 constexpr int kMlpThreads = 512;
 
 // Stage 1 of pca_apply: part[s][t][p] = sum_{h in chunk s} comp[p][h] * (x[t][h] - mean[h]).
-// grid = (ceil(P/8), ceil(H/512)): 512 CTAs at P=512, H=4096, so the 8 MiB component
-// matrix streams at HBM rate; the centred x chunk is staged once per CTA in smem.
-__global__ void __launch_bounds__(kPcaRows * 32)
+// grid = (ceil(P/16), ceil(H/512)): 256 CTAs at P=512, H=4096, so the 8 MiB component
+// matrix streams at HBM rate. The centred x chunk is staged once per CTA in smem; each
+// warp owns two component rows and each lane four consecutive columns per step, so one
+// 16-byte activation load from smem feeds eight FMAs. The 2 x 16 partial sums per lane
+// are reduced with one transpose-reduce (lane L owns row L / 16, token L % 16).
+__global__ void __launch_bounds__(kPcaWarps * 32)
 pca_partial_kernel(const float* __restrict__ comp, const float* __restrict__ mean, const float* __restrict__ x,
                    int B, int H, int P, float* __restrict__ part) {
+  static_assert(2 * kPcaTok == 32, "transpose-reduce maps (2 rows x kPcaTok tokens) onto the 32 lanes");
+  static_assert((kPcaWarps * 32) % (kPcaChunk / 4) == 0, "each thread stages one fixed column quad");
   __shared__ __align__(16) float s_x[kPcaTok][kPcaChunk];
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
-  const int p = blockIdx.x * kPcaRows + warp;
+  const int p0 = (blockIdx.x * kPcaWarps + warp) * 2;
   const int h0 = blockIdx.y * kPcaChunk;
   const int hn = min(kPcaChunk, H - h0);
+  const bool vec = (H & 3) == 0 && (hn & 3) == 0;
+  const int my_c4 = (threadIdx.x % (kPcaChunk / 4)) * 4;  // fixed column quad of this thread
+  const float4 my_mean = vec && my_c4 < hn ? __ldg(reinterpret_cast<const float4*>(mean + h0 + my_c4))
+                                            : make_float4(0.f, 0.f, 0.f, 0.f);
   for (int tb = 0; tb < B; tb += kPcaTok) {
     __syncthreads();
-    for (int i = threadIdx.x; i < kPcaTok * kPcaChunk; i += blockDim.x) {
-      const int t = i / kPcaChunk, c = i % kPcaChunk;
-      s_x[t][c] = (tb + t < B && c < hn) ? x[static_cast<size_t>(tb + t) * H + h0 + c] - mean[h0 + c] : 0.f;
+    // Stage the x chunk with asynchronous copies (all of a thread's copies in flight at
+    // once), then the copying thread centres its own elements in place.
+    if (vec) {
+      for (int t = threadIdx.x / (kPcaChunk / 4); t < kPcaTok; t += blockDim.x / (kPcaChunk / 4)) {
+        if (tb + t < B && my_c4 < hn) cp_async16(&s_x[t][my_c4], x + static_cast<size_t>(tb + t) * H + h0 + my_c4);
+        else *reinterpret_cast<float4*>(&s_x[t][my_c4]) = make_float4(0.f, 0.f, 0.f, 0.f);
+      }
+      cp_async_wait_all();
+      for (int t = threadIdx.x / (kPcaChunk / 4); t < kPcaTok; t += blockDim.x / (kPcaChunk / 4)) {
+        if (tb + t < B && my_c4 < hn) {
+          float4& v = *reinterpret_cast<float4*>(&s_x[t][my_c4]);
+          v.x -= my_mean.x; v.y -= my_mean.y; v.z -= my_mean.z; v.w -= my_mean.w;
+        }
+      }
+    } else {
+      for (int i = threadIdx.x; i < kPcaTok * kPcaChunk; i += blockDim.x) {
+        const int t = i / kPcaChunk, c = i % kPcaChunk;
+        s_x[t][c] = (tb + t < B && c < hn) ? x[static_cast<size_t>(tb + t) * H + h0 + c] - mean[h0 + c] : 0.f;
+      }
     }
     __syncthreads();
-    if (p >= P) continue;
-    float acc[kPcaTok];
+    if (p0 >= P) continue;
+    const bool two = p0 + 1 < P;
+    float acc[2 * kPcaTok];
 #pragma unroll
-    for (int t = 0; t < kPcaTok; ++t) acc[t] = 0.f;
-    const float* row = comp + static_cast<size_t>(p) * H + h0;
+    for (int i = 0; i < 2 * kPcaTok; ++i) acc[i] = 0.f;
+    const float* r0 = comp + static_cast<size_t>(p0) * H + h0;
+    const float* r1 = two ? r0 + H : r0;
+    if (vec) {
+      float4 c0[kPcaChunk / 128], c1[kPcaChunk / 128];
 #pragma unroll
-    for (int j = 0; j < kPcaChunk / 32; ++j) {
-      const int c = lane + 32 * j;
-      const float cv = c < hn ? __ldg(row + c) : 0.f;
+      for (int j = 0; j < kPcaChunk / 128; ++j) {
+        const int c = 4 * lane + 128 * j;
+        const bool ok = c < hn;
+        c0[j] = ok ? __ldg(reinterpret_cast<const float4*>(r0 + c)) : make_float4(0.f, 0.f, 0.f, 0.f);
+        c1[j] = ok && two ? __ldg(reinterpret_cast<const float4*>(r1 + c)) : make_float4(0.f, 0.f, 0.f, 0.f);
+      }
 #pragma unroll
-      for (int t = 0; t < kPcaTok; ++t) acc[t] += cv * s_x[t][c];
+      for (int j = 0; j < kPcaChunk / 128; ++j) {
+        const int c = 4 * lane + 128 * j;
+#pragma unroll
+        for (int t = 0; t < kPcaTok; ++t) {
+          const float4 a = *reinterpret_cast<const float4*>(&s_x[t][c]);
+          acc[t] += c0[j].x * a.x; acc[t] += c0[j].y * a.y; acc[t] += c0[j].z * a.z; acc[t] += c0[j].w * a.w;
+          acc[kPcaTok + t] += c1[j].x * a.x; acc[kPcaTok + t] += c1[j].y * a.y;
+          acc[kPcaTok + t] += c1[j].z * a.z; acc[kPcaTok + t] += c1[j].w * a.w;
+        }
+      }
+    } else {
+      for (int c = lane; c < hn; c += 32) {
+        const float v0 = r0[c], v1 = two ? r1[c] : 0.f;
+#pragma unroll
+        for (int t = 0; t < kPcaTok; ++t) { acc[t] += v0 * s_x[t][c]; acc[kPcaTok + t] += v1 * s_x[t][c]; }
+      }
     }
-#pragma unroll
-    for (int t = 0; t < kPcaTok; ++t) {
-      const float sum = warp_sum(acc[t]);
-      if (lane == 0 && tb + t < B) part[(static_cast<size_t>(blockIdx.y) * B + tb + t) * P + p] = sum;
-    }
+    const float sum = warp_transpose_sum(acc);
+    const int t = lane % kPcaTok, p = p0 + lane / kPcaTok;
+    if (tb + t < B && p < P) part[(static_cast<size_t>(blockIdx.y) * B + tb + t) * P + p] = sum;
   }
 }
 
 __device__ __forceinline__ float gelu_erf(float v) { return 0.5f * v * (1.0f + erff(v * 0.70710678118654752f)); }
 
-// out[t][r] = act(W[r,:] . in[t,:] + b[r]) for all tokens of the CTA: each weight row is
-// read once (lanes stride columns) and applied to every token from shared memory.
-__device__ void affine_tokens(const float* __restrict__ W, const float* __restrict__ bvec, int rows, int cols,
-                              const float* in, int in_stride, float* out, int out_stride, int nt, bool gelu) {
+// out[t][r] = act(W[r,:] . in[t,:] + b[r]) for all tokens of the CTA. A warp owns two rows;
+// lanes stride the columns so every activation read from shared memory feeds two FMAs, and
+// the 2 x kMlpTok partial sums are reduced with one transpose-reduce (lane L ends up owning
+// row r0 + L / kMlpTok, token L % kMlpTok and applies bias + activation itself).
+__device__ __forceinline__ void affine_tokens(const float* __restrict__ W, const float* __restrict__ bvec, int rows,
+                                              int cols, const float* in, int in_stride, float* out, int out_stride,
+                                              int nt, bool gelu) {
+  static_assert(2 * kMlpTok == 32, "transpose-reduce maps (2 rows x kMlpTok tokens) onto the 32 lanes");
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31, nw = blockDim.x >> 5;
   constexpr int kU = 4;  // weight loads in flight per lane and row
-  // Two rows per warp pass: every activation read from shared memory feeds two FMAs.
   for (int r0 = 2 * warp; r0 < rows; r0 += 2 * nw) {
     const bool two = r0 + 1 < rows;
-    float acc[2][kMlpTok];
+    float acc[2 * kMlpTok];
 #pragma unroll
-    for (int t = 0; t < kMlpTok; ++t) acc[0][t] = acc[1][t] = 0.f;
+    for (int i = 0; i < 2 * kMlpTok; ++i) acc[i] = 0.f;
     for (int c0 = 0; c0 < cols; c0 += 32 * kU) {
       float w0[kU], w1[kU];
 #pragma unroll
       for (int u = 0; u < kU; ++u) {
         const int c = c0 + lane + 32 * u;
-        w0[u] = c < cols ? W[static_cast<size_t>(r0) * cols + c] : 0.f;
-        w1[u] = c < cols && two ? W[static_cast<size_t>(r0 + 1) * cols + c] : 0.f;
+        w0[u] = c < cols ? W[r0 * cols + c] : 0.f;
+        w1[u] = c < cols && two ? W[(r0 + 1) * cols + c] : 0.f;
       }
 #pragma unroll
       for (int u = 0; u < kU; ++u) {
@@ -131,21 +181,17 @@ __device__ void affine_tokens(const float* __restrict__ W, const float* __restri
 #pragma unroll
           for (int t = 0; t < kMlpTok; ++t) {
             const float a = in[t * in_stride + c];
-            acc[0][t] += w0[u] * a;
-            acc[1][t] += w1[u] * a;
+            acc[t] += w0[u] * a;
+            acc[kMlpTok + t] += w1[u] * a;
           }
         }
       }
     }
-    const float b0 = bvec[r0], b1 = two ? bvec[r0 + 1] : 0.f;
-#pragma unroll
-    for (int t = 0; t < kMlpTok; ++t) {
-      const float s0 = warp_sum(acc[0][t]) + b0;
-      const float s1 = warp_sum(acc[1][t]) + b1;
-      if (lane == 0 && t < nt) {
-        out[t * out_stride + r0] = gelu ? gelu_erf(s0) : s0;
-        if (two) out[t * out_stride + r0 + 1] = gelu ? gelu_erf(s1) : s1;
-      }
+    const float s = warp_transpose_sum(acc);
+    const int t = lane % kMlpTok, r = r0 + lane / kMlpTok;
+    if (t < nt && r < rows) {
+      const float v = s + bvec[r];
+      out[t * out_stride + r] = gelu ? gelu_erf(v) : v;
     }
   }
 }
@@ -153,70 +199,75 @@ __device__ void affine_tokens(const float* __restrict__ W, const float* __restri
 // Feature concat [pca | onehot(prev top-k) | prev gate weights] (predictor.cpp:214-220),
 // GELU blocks, middle-group gated residual (229-240), logits (242-245), top-k on
 // logits (669-672), predicted histogram (experiment.cpp:104-112). kMlpTok tokens/CTA.
+// kStage: every MLP parameter is staged in shared memory first (one L2 round trip) and
+// addressed as smem + offset, so the layer loops issue LDS rather than generic loads.
+template <bool kStage>
 __global__ void __launch_bounds__(kMlpThreads)
 mlp_kernel(const __grid_constant__ NetDev net, const float* __restrict__ part, int n_part,
            const int32_t* __restrict__ prev_ids, int k_prev, const float* __restrict__ prev_w, int B, int k,
-           float* __restrict__ logits_out, int32_t* __restrict__ ids_out, int32_t* __restrict__ pred_counts,
-           int stage_w) {
-  extern __shared__ float smem[];
+           float* __restrict__ logits_out, int32_t* __restrict__ ids_out, int32_t* __restrict__ pred_counts) {
+  extern __shared__ __align__(16) float smem[];
   const int P = net.P, E = net.E, D = net.in_dim, Wd = net.width;
   const int t0 = blockIdx.x * kMlpTok, nt = min(kMlpTok, B - t0);
-  float* feat = smem;                   // [kMlpTok][D]
-  float* h1 = feat + kMlpTok * D;       // [kMlpTok][maxh]
   int maxh = Wd;
   for (int j = 1; j <= net.n_blocks; ++j) maxh = max(maxh, net.dims[j]);
+  float* wsm = smem;                                       // [mlp_floats] staged parameters
+  float* feat = smem + (kStage ? (net.mlp_floats + 3) / 4 * 4 : 0);  // [kMlpTok][D]
+  float* h1 = feat + kMlpTok * D;                          // [kMlpTok][maxh]
   float* h2 = h1 + kMlpTok * maxh;
   float* h3 = h2 + kMlpTok * maxh;
-  float* lg = h3 + kMlpTok * maxh;      // [kMlpTok][E]
-  float* wsm = lg + kMlpTok * E;        // [mlp_floats] staged MLP parameters (if they fit)
+  float* lg = h3 + kMlpTok * maxh;                         // [kMlpTok][E]
+  const float* base = kStage ? wsm : net.w[0];
 
-  // Stage every MLP parameter of the net (<= ~40K floats) with all threads at once: one
-  // L2 round trip instead of one per row chunk of every layer (latency-bound kernel).
-  NetDev n = net;
-  if (stage_w) {
+  if (kStage) {
     const float4* src = reinterpret_cast<const float4*>(net.w[0]);
     float4* dst = reinterpret_cast<float4*>(wsm);
-    for (int i = threadIdx.x; i < net.mlp_floats / 4; i += blockDim.x) dst[i] = __ldg(src + i);
-    auto tr = [&](const float* p) { return wsm + (p - net.w[0]); };
-    for (int j = 0; j < net.n_blocks; ++j) { n.w[j] = tr(net.w[j]); n.b[j] = tr(net.b[j]); }
-    for (int j = 0; j < net.n_res; ++j) { n.rw[j] = tr(net.rw[j]); n.rb[j] = tr(net.rb[j]); }
-    n.gate_w = tr(net.gate_w);
-    n.out_w = tr(net.out_w);
-    n.out_b = tr(net.out_b);
+    for (int i = threadIdx.x; i < net.mlp_floats / 4; i += blockDim.x) cp_async16(dst + i, src + i);
   }
 
-  // PCA partial sums (fixed order) + features; 4 elements per thread per pass with all
-  // their partial loads issued together (latency-bound prologue).
+  // PCA features: partial sums in fixed part order (0 + p0 + p1 + ...), all of a quad's
+  // partial loads in flight together.
   constexpr int kMaxParts = 16;
-  for (int i0 = threadIdx.x; i0 < kMlpTok * D; i0 += 4 * blockDim.x) {
-    float v[4];
+  const bool vecP = (P & 3) == 0;
+  const int Pq = vecP ? P / 4 : P;
+  for (int i = threadIdx.x; i < kMlpTok * Pq; i += blockDim.x) {
+    const int t = i / Pq, q = i % Pq;
+    if (vecP) {
+      float4 a = make_float4(0.f, 0.f, 0.f, 0.f);
+      if (t < nt) {
+        const float4* src = reinterpret_cast<const float4*>(part + static_cast<size_t>(t0 + t) * P) + q;
+        const size_t stride = static_cast<size_t>(B) * P / 4;
+        float4 pv[kMaxParts];
 #pragma unroll
-    for (int q = 0; q < 4; ++q) {
-      const int i = i0 + q * blockDim.x;
-      v[q] = 0.f;
-      if (i >= kMlpTok * D) continue;
-      const int t = i / D, c = i % D, tok = t0 + t;
-      if (t >= nt) continue;
-      if (c < P) {
-        float pv[kMaxParts];
+        for (int s = 0; s < kMaxParts; ++s) if (s < n_part) pv[s] = __ldg(src + s * stride);
 #pragma unroll
         for (int s = 0; s < kMaxParts; ++s)
-          pv[s] = s < n_part ? part[(static_cast<size_t>(s) * B + tok) * P + c] : 0.f;
-#pragma unroll
-        for (int s = 0; s < kMaxParts; ++s) v[q] += pv[s];
-      } else if (c >= P + E) {
-        v[q] = prev_w[static_cast<size_t>(tok) * E + (c - P - E)];
+          if (s < n_part) { a.x += pv[s].x; a.y += pv[s].y; a.z += pv[s].z; a.w += pv[s].w; }
+      }
+      float* f = feat + t * D + 4 * q;
+      f[0] = a.x; f[1] = a.y; f[2] = a.z; f[3] = a.w;
+    } else {
+      float a = 0.f;
+      if (t < nt)
+        for (int s = 0; s < n_part; ++s) a += part[(static_cast<size_t>(s) * B + t0 + t) * P + q];
+      feat[t * D + q] = a;
+    }
+  }
+  // onehot(prev top-k) | prev gate weights
+  for (int i = threadIdx.x; i < kMlpTok * 2 * E; i += blockDim.x) {
+    const int t = i / (2 * E), j = i % (2 * E);
+    float v = 0.f;
+    if (t < nt) {
+      if (j < E) {
+        for (int r = 0; r < k_prev; ++r)
+          if (prev_ids[static_cast<size_t>(t0 + t) * k_prev + r] == j) v = 1.0f;
+      } else {
+        v = prev_w[static_cast<size_t>(t0 + t) * E + (j - E)];
       }
     }
-#pragma unroll
-    for (int q = 0; q < 4; ++q)
-      if (i0 + q * blockDim.x < kMlpTok * D) feat[i0 + q * blockDim.x] = v[q];
+    feat[t * D + P + j] = v;
   }
-  __syncthreads();
-  for (int i = threadIdx.x; i < nt * k_prev; i += blockDim.x) {
-    const int t = i / k_prev;
-    feat[t * D + P + prev_ids[static_cast<size_t>(t0 + t) * k_prev + i % k_prev]] = 1.0f;
-  }
+  if (kStage) cp_async_wait_all();
   __syncthreads();
 
   const float* cur = feat;
@@ -224,7 +275,8 @@ mlp_kernel(const __grid_constant__ NetDev net, const float* __restrict__ part, i
   float* bufs[2] = {h1, h2};
   for (int j = 0; j < net.n_blocks; ++j) {
     float* o = bufs[j & 1];
-    affine_tokens(n.w[j], n.b[j], net.dims[j + 1], net.dims[j], cur, cur_stride, o, maxh, nt, true);
+    affine_tokens(base + net.o_w[j], base + net.o_b[j], net.dims[j + 1], net.dims[j], cur, cur_stride, o, maxh, nt,
+                  true);
     __syncthreads();
     cur = o;
     cur_stride = maxh;
@@ -236,15 +288,16 @@ mlp_kernel(const __grid_constant__ NetDev net, const float* __restrict__ part, i
     float* u = nullptr;
     for (int j = 0; j < net.n_res; ++j) {
       u = ubuf[j & 1];
-      affine_tokens(n.rw[j], n.rb[j], Wd, Wd, uin, maxh, u, maxh, nt, true);
+      affine_tokens(base + net.o_rw[j], base + net.o_rb[j], Wd, Wd, uin, maxh, u, maxh, nt, true);
       __syncthreads();
       uin = u;
     }
     __shared__ float s_gate[kMlpTok];
     const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+    const float* gw = base + net.o_gate;
     for (int t = warp; t < nt; t += blockDim.x >> 5) {
       float d = 0.f;
-      for (int i = lane; i < P; i += 32) d += n.gate_w[i] * feat[t * D + i];
+      for (int i = lane; i < P; i += 32) d += gw[i] * feat[t * D + i];
       d = warp_sum(d);
       if (lane == 0) s_gate[t] = 1.0f / (1.0f + expf(-(d + net.gate_b)));
     }
@@ -256,7 +309,7 @@ mlp_kernel(const __grid_constant__ NetDev net, const float* __restrict__ part, i
     __syncthreads();
     cur = u;
   }
-  affine_tokens(n.out_w, n.out_b, E, Wd, cur, maxh, lg, E, nt, false);
+  affine_tokens(base + net.o_ow, base + net.o_ob, E, Wd, cur, maxh, lg, E, nt, false);
   __syncthreads();
   if (logits_out)
     for (int i = threadIdx.x; i < nt * E; i += blockDim.x) logits_out[static_cast<size_t>(t0) * E + i] = lg[i];
@@ -347,6 +400,12 @@ void upload(ps_llapor_s& m, int layer, const HostNet& hn) {
   d.out_w = dev + o_ow;
   d.out_b = dev + o_ob;
   d.mlp_floats = static_cast<int>(o_ob + ((hn.out.b.size() + 3) / 4) * 4 - o_w[0]);
+  auto rel = [&](size_t o) { return static_cast<int>(o - o_w[0]); };
+  for (int j = 0; j < d.n_blocks; ++j) { d.o_w[j] = rel(o_w[j]); d.o_b[j] = rel(o_b[j]); }
+  for (int j = 0; j < d.n_res; ++j) { d.o_rw[j] = rel(o_rw[j]); d.o_rb[j] = rel(o_rb[j]); }
+  d.o_gate = rel(o_gate);
+  d.o_ow = rel(o_ow);
+  d.o_ob = rel(o_ob);
   d.valid = 1;
   if (layer >= static_cast<int>(m.nets.size())) m.nets.resize(layer + 1);
   m.nets[layer] = d;
@@ -517,21 +576,29 @@ ps_status ps_llapor_forward(ps_llapor m, int layer, const float* hidden, const i
     float* part = static_cast<float*>(scratch);
     const int H = m->spec.hidden_dim;
     const int n_part = (H + kPcaChunk - 1) / kPcaChunk;
-    dim3 grid((net.P + kPcaRows - 1) / kPcaRows, n_part);
-    pca_partial_kernel<<<grid, kPcaRows * 32, 0, s>>>(net.comp, net.mean, hidden, B, H, net.P, part);
+    dim3 grid((net.P + 2 * kPcaWarps - 1) / (2 * kPcaWarps), n_part);
+    pca_partial_kernel<<<grid, kPcaWarps * 32, 0, s>>>(net.comp, net.mean, hidden, B, H, net.P, part);
     PS_LAUNCH_CHECK("pca_partial_kernel");
     int maxh = net.width;
     for (int j = 1; j <= net.n_blocks; ++j) maxh = std::max(maxh, net.dims[j]);
-    size_t smem = sizeof(float) * kMlpTok * (net.in_dim + 3 * maxh + net.E);
-    const int stage_w = smem + sizeof(float) * net.mlp_floats <= 200 * 1024 ? 1 : 0;
-    if (stage_w) smem += sizeof(float) * net.mlp_floats;
-    static int smem_set = 0;
-    if (static_cast<int>(smem) > smem_set) {
-      PS_CUDA(cudaFuncSetAttribute(mlp_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(smem)));
-      smem_set = static_cast<int>(smem);
+    const size_t act = sizeof(float) * kMlpTok * (net.in_dim + 3 * maxh + net.E);
+    const size_t staged = act + sizeof(float) * ((net.mlp_floats + 3) / 4 * 4);
+    const bool stage_w = staged <= 200 * 1024;
+    const size_t smem = stage_w ? staged : act;
+    require(smem <= 227 * 1024, "ps_llapor_forward: predictor too wide for one CTA's shared memory");
+    static size_t smem_set[2] = {0, 0};
+    const void* fn = stage_w ? reinterpret_cast<const void*>(mlp_kernel<true>) : reinterpret_cast<const void*>(mlp_kernel<false>);
+    if (smem > smem_set[stage_w]) {
+      PS_CUDA(cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(smem)));
+      smem_set[stage_w] = smem;
     }
-    mlp_kernel<<<(B + kMlpTok - 1) / kMlpTok, kMlpThreads, smem, s>>>(net, part, n_part, prev_ids, k_prev,
-                                                                      prev_weights, B, k, logits, ids, pred_counts, stage_w);
+    const int grid_m = (B + kMlpTok - 1) / kMlpTok;
+    if (stage_w)
+      mlp_kernel<true><<<grid_m, kMlpThreads, smem, s>>>(net, part, n_part, prev_ids, k_prev, prev_weights, B, k, logits,
+                                                         ids, pred_counts);
+    else
+      mlp_kernel<false><<<grid_m, kMlpThreads, smem, s>>>(net, part, n_part, prev_ids, k_prev, prev_weights, B, k,
+                                                          logits, ids, pred_counts);
     PS_LAUNCH_CHECK("mlp_kernel");
   });
 }
