@@ -1,28 +1,45 @@
-// K3 (decode path) — grouped SwiGLU expert FFN as an HBM-streaming GEMV.
+// K3 (decode path) — grouped SwiGLU expert FFN as one persistent HBM-streaming kernel.
 //
 // No reference code exists for the expert FFN; the op is
 // y = W_down(SiLU(W_gate x) * (W_up x)) over the experts a
 // decode step activates, with per-expert token counts m_e <= 64 per pass.
 //
 // Design (HBM-bound: algorithmic bytes = sum_e 3*H*F*2):
-//  * CTA = one 16-row tile of one expert's weight matrix; its W warps split the K
-//    range of the tile and stream their slice once with 128-bit
-//    ld.global.nc.L1::no_allocate loads (16 loads per lane in flight); the W partial
-//    16xN accumulators are reduced through shared memory at the end. A single expert
-//    therefore spreads over (rows/16) x W warps (7168 warps for Mixtral gate_up) —
-//    enough memory-level parallelism for HBM even when one on-demand expert is
-//    launched alone.
-//  * m_e token vectors are the 8-wide N side of mma.sync.m16n8k16 (bf16 in, fp32
-//    accumulate). A dot product is invariant under a common permutation of K, so each
-//    lane feeds its A fragment straight from its own coalesced 16-byte load (rows g and
-//    g+8, elements 8t..8t+7 of a 32-wide K block) and loads the matching 16 bytes of x
-//    for its B fragment: no shared-memory staging, no swizzle, no descriptors.
-//  * gate_up: gate and up rows of the same F range in one CTA; epilogue
-//    h = SiLU(g) * u -> bf16 [perm_row, F].
-//    down:    16 H-rows of W_down; optional global split-K over F (n_split) into fp32
-//    partials y_part[split][perm_row][H], summed in fixed order by K2's combine.
-//  * Deterministic (no atomics). Rows beyond the matrix and K tails are zero-filled.
+//  * One launch does gate_up AND down. Work items are 32 weight rows x a K range:
+//    gate_up = (expert, 16-row F tile: 16 gate + 16 up rows, K = H); down = (expert,
+//    split of F, 32-row H tile). All gate_up items precede all down items; CTA b takes
+//    items b, b+G, b+2G, ... (G = one CTA per SM; cooperative launch, all resident).
+//  * Per CTA one producer lane streams the weight tiles through a 6-stage ring of
+//    32 KiB shared-memory stages with 2D TMA boxes (cp.async.bulk.tensor, {256 cols x 16
+//    or 32 rows} = 8-16 KiB per op, mbarrier complete_tx, out-of-bounds rows/cols
+//    zero-filled). Measured on B200 (scripts/probes): TMA ops of >= 8 KiB stream at the
+//    HBM roofline, 1-2 KiB ops are op-rate bound at 50-60% of it; >= 128 KiB must be in
+//    flight per SM. The ring keeps 192 KiB in flight and streams across item and phase
+//    boundaries.
+//  * 8 consumer warps split each stage's 16 K blocks (2 each). Tokens are the 8-wide N
+//    side of mma.sync.m16n8k16 (bf16 in, fp32 accumulate): a dot product is invariant
+//    under a common permutation of K, so a lane's A fragment is one 16-byte LDS (rows g
+//    and g+8, elements 8t..8t+7 of a 32-wide K block) and its B fragment the matching 16
+//    bytes of the activation row, loaded from L1/L2 one stage ahead. (Decode is
+//    HBM-bound at m_e <= 64: mma.sync keeps up with the stream; tcgen05 is used on the
+//    prefill path where the op is tensor-bound.)
+//  * Partials of the 8 warps are reduced through shared memory per item; epilogues:
+//    gate_up h = SiLU(g) * u -> bf16 [perm_row, F]; down -> fp32 y_part[split][row][H]
+//    (summed in fixed order by K2's combine). Deterministic (no float atomics).
+//  * gate_up -> down dependency without a second launch or a grid barrier: each gate_up
+//    item bumps a per-(expert, split) counter after its h stores (release); a down item
+//    waits (acquire) until every F tile of its split is done, then reads h from L2.
+//    Items run in increasing index order per CTA and every gate_up index is below every
+//    down index, so a wait never blocks a producer of h; the producer keeps prefetching
+//    down weights meanwhile. The last down item of a split resets its counters for the
+//    next launch (per-stream workspace).
+//  * Weight tensor maps are encoded on the host once per slab (cached) and passed in the
+//    kernel parameters (up to 64 experts per launch).
+#include <cuda.h>
+
 #include <algorithm>
+#include <mutex>
+#include <unordered_map>
 #include <vector>
 
 #include "device_common.cuh"
@@ -30,19 +47,104 @@
 namespace ps {
 namespace {
 
-constexpr int kMaxGroup = 120;
-// K blocks in flight per lane: 4 (16 x 16 B loads for gate_up) unless many token
-// groups make the x fragments the register bottleneck.
-template <int NT> constexpr int unroll_for() { return NT >= 4 ? 2 : 4; }
+constexpr int kMaxSplit = 8;
+constexpr int kSyncEntries = 64;                 // max entries per launch (sync workspace rows)
+constexpr int kCWarps = 8;                       // consumer warps
+constexpr int kThreads = (kCWarps + 1) * 32;     // + one producer warp
+constexpr int kBarBytes = 256;
+constexpr int kMaxTokens = 64;                   // tokens per expert per launch (8 * NT, NT <= 8)
+constexpr int kCols = 512;                       // K elements per stage
+constexpr int kHalf = 256;                       // TMA box width (cols)
+constexpr int kTileBytes = 16 * kHalf * 2;       // one (16-row m-tile, 256-col half) = 8 KiB
+constexpr int kStageBytes = 4 * kTileBytes;      // 2 m-tiles x 2 halves = 32 KiB
+static_assert(kCols / 32 == 2 * kCWarps, "two K blocks per consumer warp and stage");
 
-struct FfnLaunch {
-  int n;
-  int token_chunk;                 // tokens per work item (8 * NT)
-  int tile_start[kMaxGroup + 1];   // prefix of CTA work items per entry
-  int expert[kMaxGroup];
-  int tok_chunks[kMaxGroup];       // ceil(m_e / token_chunk)
-  const uint16_t* slab[kMaxGroup];
+template <int NT> struct Geo {
+  static constexpr int kStages = NT <= 4 ? 6 : 5;
+  static constexpr int kRedBytes = kCWarps * 2 * NT * 4 * 32 * 4;
+  static constexpr int kSmem = kBarBytes + kStages * kStageBytes + kRedBytes;
+  static_assert(kSmem <= 227 * 1024, "decode FFN smem budget");
 };
+
+template <int CAP>
+struct DecodeParams {
+  CUtensorMap gu_map[CAP];        // [Wg; Wu] as [2F, H], box {256, 16}
+  CUtensorMap dn_map[CAP];        // Wd as [H, F], box {256, 32}
+  int n;                          // entries (experts with m_e > tok_base)
+  int gu_start[CAP + 1];          // prefix of gate_up items per entry (F/16 each)
+  int dn_start[CAP + 1];          // prefix of down items per entry (n_split * H/32 each)
+  int expert[CAP];
+  int H, F, k, n_split, kchunk, dn_tiles, tok_base;
+  const int32_t* offsets;
+  const int32_t* perm_src;
+  const uint16_t* x;
+  uint16_t* h;
+  float* y_part;
+  size_t split_stride;
+  int* sync;                      // [2][kSyncEntries * kMaxSplit]: F tiles done, down items started
+};
+
+struct Item {
+  bool down;
+  int i, r0, split, kbeg, kend;
+};
+
+__device__ __forceinline__ int find_prefix(const int* start, int n, int w) {
+  int lo = 0, hi = n - 1;
+  while (lo < hi) {  // largest i with start[i] <= w
+    const int mid = (lo + hi + 1) >> 1;
+    if (start[mid] <= w) lo = mid;
+    else hi = mid - 1;
+  }
+  return lo;
+}
+
+template <class P>
+__device__ __forceinline__ Item item_at(const P& p, int idx) {
+  Item it;
+  const int gu_total = p.gu_start[p.n];
+  if (idx < gu_total) {
+    it.down = false;
+    it.i = find_prefix(p.gu_start, p.n, idx);
+    it.r0 = (idx - p.gu_start[it.i]) * 16;
+    it.split = it.r0 / p.kchunk;
+    it.kbeg = 0;
+    it.kend = p.H;
+  } else {
+    idx -= gu_total;
+    it.down = true;
+    it.i = find_prefix(p.dn_start, p.n, idx);
+    const int local = idx - p.dn_start[it.i];
+    it.split = local / p.dn_tiles;
+    it.r0 = (local % p.dn_tiles) * 32;
+    it.kbeg = min(p.F, it.split * p.kchunk);
+    it.kend = min(p.F, it.split * p.kchunk + p.kchunk);
+  }
+  return it;
+}
+
+// F tiles of split s (the down items of that split wait for all of them).
+template <class P>
+__device__ __forceinline__ int split_tiles(const P& p, int s) {
+  const int b = min(p.F, s * p.kchunk), e = min(p.F, s * p.kchunk + p.kchunk);
+  return (e - b + 15) / 16;
+}
+
+__device__ __forceinline__ void tma_2d(void* dst, const CUtensorMap* map, uint64_t* bar, int c0, int c1,
+                                       uint64_t policy) {
+  asm volatile(
+      "cp.async.bulk.tensor.2d.shared::cluster.global.mbarrier::complete_tx::bytes.L2::cache_hint [%0], [%1, {%2, "
+      "%3}], [%4], %5;" ::"r"(smem_u32(dst)),
+      "l"(map), "r"(c0), "r"(c1), "r"(smem_u32(bar)), "l"(policy)
+      : "memory");
+}
+
+// h is produced inside this launch by other SMs: read it from L2 (never a stale L1 line).
+__device__ __forceinline__ uint4 ld_cg(const void* p) {
+  uint4 r;
+  asm volatile("ld.global.cg.v4.u32 {%0,%1,%2,%3}, [%4];" : "=r"(r.x), "=r"(r.y), "=r"(r.z), "=r"(r.w) : "l"(p));
+  return r;
+}
 
 __device__ __forceinline__ void mma_bf16_16816(float (&c)[4], uint32_t a0, uint32_t a1, uint32_t a2,
                                                uint32_t a3, uint32_t b0, uint32_t b1) {
@@ -59,209 +161,361 @@ __device__ __forceinline__ void mma_block(float (&c)[4], const uint4& r0, const 
   mma_bf16_16816(c, r0.z, r8.z, r0.w, r8.w, xv.z, xv.w);
 }
 
-__device__ __forceinline__ int find_entry(const FfnLaunch& g, int w) {
-  int lo = 0, hi = g.n - 1;
-  while (lo < hi) {  // largest i with tile_start[i] <= w
-    int mid = (lo + hi + 1) >> 1;
-    if (g.tile_start[mid] <= w) lo = mid;
-    else hi = mid - 1;
-  }
-  return lo;
-}
-
 __device__ __forceinline__ uint4 zero4() { return make_uint4(0u, 0u, 0u, 0u); }
 
-// Streams rows (g, g+8) of NM matrices over this warp's K range [kbeg, kend),
-// accumulating NM x NT 16x8 tiles.
-template <int NT, int NM>
-__device__ __forceinline__ void stream_tile(const uint16_t* const (&row0)[NM], const uint16_t* const (&row8)[NM],
-                                            bool ok0, bool ok8, const uint16_t* const (&xr)[NT], int kbeg, int kend,
-                                            int tig, float (&acc)[NM][NT][4]) {
-  constexpr int kUnroll = unroll_for<NT>();
-  for (int kb = kbeg; kb < kend; kb += 32 * kUnroll) {
-    uint4 a0[kUnroll][NM], a8[kUnroll][NM], xv[kUnroll][NT];
+__device__ __forceinline__ uint4 lds128(const uint8_t* p) { return *reinterpret_cast<const uint4*>(p); }
+
+__device__ __forceinline__ int ld_acquire(const int* p) {
+  int v;
+  asm volatile("ld.acquire.gpu.global.b32 %0, [%1];" : "=r"(v) : "l"(p) : "memory");
+  return v;
+}
+
+__device__ __forceinline__ void consumer_sync() { asm volatile("bar.sync 1, %0;" ::"n"(kCWarps * 32) : "memory"); }
+
+// Activation fragments of this lane for one stage: 2 K blocks x NT token groups.
+template <int NT>
+__device__ __forceinline__ void load_act(uint4 (&xv)[2][NT], const uint16_t* const (&xr)[NT], bool down, int k0,
+                                         int kend, int warp, int tig) {
 #pragma unroll
-    for (int u = 0; u < kUnroll; ++u) {
-      const int off = kb + 32 * u + 8 * tig;
-      const bool kin = off < kend;
+  for (int u = 0; u < 2; ++u) {
+    const int kg = k0 + (2 * warp + u) * 32 + 8 * tig;
+    const bool kin = kg < kend;
 #pragma unroll
-      for (int mt = 0; mt < NM; ++mt) {
-        a0[u][mt] = kin && ok0 ? ldg_stream(row0[mt] + off) : zero4();
-        a8[u][mt] = kin && ok8 ? ldg_stream(row8[mt] + off) : zero4();
+    for (int j = 0; j < NT; ++j)
+      xv[u][j] = kin && xr[j] ? (down ? ld_cg(xr[j] + kg) : ldg_keep(xr[j] + kg)) : zero4();
+  }
+}
+
+template <int NT, int CAP>
+__global__ void __launch_bounds__(kThreads, 1) ffn_decode_kernel(const __grid_constant__ DecodeParams<CAP> p) {
+  using G = Geo<NT>;
+  extern __shared__ __align__(1024) uint8_t smem[];
+  uint64_t* full = reinterpret_cast<uint64_t*>(smem);
+  uint64_t* empty = full + G::kStages;
+  uint8_t* ring = smem + kBarBytes;
+  float* red = reinterpret_cast<float*>(ring + G::kStages * kStageBytes);  // [warp][mt][j][q][lane]
+
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const int total = p.gu_start[p.n] + p.dn_start[p.n];
+  const int n_slots = kSyncEntries * kMaxSplit;
+  if (threadIdx.x == 0) {
+    for (int s = 0; s < G::kStages; ++s) {
+      mbar_init(&full[s], 1);
+      mbar_init(&empty[s], kCWarps);
+    }
+    asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+  }
+  __syncthreads();
+
+  if (warp == kCWarps) {
+    // ---------------------------------------------------------------- producer lane
+    if (lane != 0) return;
+    const uint64_t pol = l2_evict_first_policy();
+    uint32_t n = 0;
+    for (int idx = blockIdx.x; idx < total; idx += gridDim.x) {
+      const Item it = item_at(p, idx);
+      const CUtensorMap* map = it.down ? &p.dn_map[it.i] : &p.gu_map[it.i];
+      for (int k0 = it.kbeg; k0 < it.kend; k0 += kCols, ++n) {
+        const int s = n % G::kStages;
+        mbar_wait(&empty[s], ((n / G::kStages) & 1) ^ 1);
+        uint8_t* dst = ring + s * kStageBytes;
+        mbar_expect_tx(&full[s], kStageBytes);
+        // smem tile (m-tile mt, half hf) at (hf * 2 + mt) * 8 KiB.
+        if (!it.down) {
+#pragma unroll
+          for (int hf = 0; hf < 2; ++hf) {
+            tma_2d(dst + (hf * 2 + 0) * kTileBytes, map, &full[s], k0 + hf * kHalf, it.r0, pol);        // gate rows
+            tma_2d(dst + (hf * 2 + 1) * kTileBytes, map, &full[s], k0 + hf * kHalf, p.F + it.r0, pol);  // up rows
+          }
+        } else {
+#pragma unroll
+          for (int hf = 0; hf < 2; ++hf) tma_2d(dst + hf * 2 * kTileBytes, map, &full[s], k0 + hf * kHalf, it.r0, pol);
+        }
       }
-#pragma unroll
-      for (int j = 0; j < NT; ++j) xv[u][j] = kin && xr[j] ? ldg_keep(xr[j] + off) : zero4();
     }
-#pragma unroll
-    for (int u = 0; u < kUnroll; ++u)
-#pragma unroll
-      for (int mt = 0; mt < NM; ++mt)
-#pragma unroll
-        for (int j = 0; j < NT; ++j) mma_block(acc[mt][j], a0[u][mt], a8[u][mt], xv[u][j]);
+    return;
   }
-}
 
-// Shared-memory reduction of the W warps' partial tiles, layout red[w][mt][j][q][lane].
-template <int NT, int NM>
-__device__ __forceinline__ void publish(float* red, const float (&acc)[NM][NT][4], int warp, int lane) {
+  // ------------------------------------------------------------------ consumer warps
+  const int gid = lane >> 2, tig = lane & 3;
+  const int hf = warp >> 2;                      // this warp's 256-col half of every stage
+  const int kl0 = ((2 * warp) & 7) * 32 + 8 * tig;  // element offset inside the half
+  uint32_t n = 0;
+  for (int idx = blockIdx.x; idx < total; idx += gridDim.x) {
+    const Item it = item_at(p, idx);
+    const int e = p.expert[it.i];
+    const int row0 = p.offsets[e] + p.tok_base;
+    const int m = min(8 * NT, p.offsets[e + 1] - row0);
+    const int slot = it.i * kMaxSplit + it.split;
+    if (it.down) {
+      if (threadIdx.x == 0) {
+        const int need = split_tiles(p, it.split);
+        while (ld_acquire(p.sync + slot) < need) __nanosleep(32);
+        __threadfence();
+        if (atomicAdd(p.sync + n_slots + slot, 1) == p.dn_tiles - 1) {  // last reader resets
+          p.sync[slot] = 0;
+          p.sync[n_slots + slot] = 0;
+        }
+      }
+      consumer_sync();
+    }
+    const uint16_t* xr[NT];
 #pragma unroll
-  for (int mt = 0; mt < NM; ++mt)
+    for (int j = 0; j < NT; ++j) {
+      const int t = 8 * j + gid;
+      xr[j] = t >= m ? nullptr
+              : it.down ? p.h + static_cast<size_t>(row0 + t) * p.F
+                        : p.x + static_cast<size_t>(p.perm_src[row0 + t] / p.k) * p.H;
+    }
+    float acc[2][NT][4];
 #pragma unroll
-    for (int j = 0; j < NT; ++j)
+    for (int mt = 0; mt < 2; ++mt)
 #pragma unroll
-      for (int q = 0; q < 4; ++q) red[(((warp * NM + mt) * NT + j) * 4 + q) * 32 + lane] = acc[mt][j][q];
-}
+      for (int j = 0; j < NT; ++j)
+#pragma unroll
+        for (int q = 0; q < 4; ++q) acc[mt][j][q] = 0.f;
 
-template <int NT, int NM, int W>
-__device__ __forceinline__ float reduced(const float* red, int mt, int j, int q, int lane) {
-  float s = 0.f;
+    uint4 xv[2][NT];
+    load_act<NT>(xv, xr, it.down, it.kbeg, it.kend, warp, tig);
+    for (int k0 = it.kbeg; k0 < it.kend; k0 += kCols, ++n) {
+      uint4 xn[2][NT];  // next stage's activations, in flight during this stage
+      if (NT <= 4 && k0 + kCols < it.kend) load_act<NT>(xn, xr, it.down, k0 + kCols, it.kend, warp, tig);
+      const int s = n % G::kStages;
+      mbar_wait(&full[s], (n / G::kStages) & 1);
+      const uint8_t* st = ring + s * kStageBytes + hf * 2 * kTileBytes;
 #pragma unroll
-  for (int w = 0; w < W; ++w) s += red[(((w * NM + mt) * NT + j) * 4 + q) * 32 + lane];
-  return s;
-}
+      for (int u = 0; u < 2; ++u) {
+        const int off = (kl0 + 32 * u) * 2;
+        const uint4 a00 = lds128(st + gid * (kHalf * 2) + off);
+        const uint4 a08 = lds128(st + (gid + 8) * (kHalf * 2) + off);
+        const uint4 a10 = lds128(st + kTileBytes + gid * (kHalf * 2) + off);
+        const uint4 a18 = lds128(st + kTileBytes + (gid + 8) * (kHalf * 2) + off);
+#pragma unroll
+        for (int j = 0; j < NT; ++j) {
+          mma_block(acc[0][j], a00, a08, xv[u][j]);
+          mma_block(acc[1][j], a10, a18, xv[u][j]);
+        }
+      }
+      __syncwarp();
+      if (lane == 0) mbar_arrive(&empty[s]);
+      if (k0 + kCols < it.kend) {
+        if (NT <= 4) {
+#pragma unroll
+          for (int u = 0; u < 2; ++u)
+#pragma unroll
+            for (int j = 0; j < NT; ++j) xv[u][j] = xn[u][j];
+        } else {
+          load_act<NT>(xv, xr, it.down, k0 + kCols, it.kend, warp, tig);
+        }
+      }
+    }
 
-template <int NT, int W>
-__global__ void __launch_bounds__(W * 32)
-ffn_gateup_kernel(const __grid_constant__ FfnLaunch g, const int32_t* __restrict__ offsets,
-                  const int32_t* __restrict__ perm_src, int k, const uint16_t* __restrict__ x, int H, int F,
-                  uint16_t* __restrict__ h_out) {
-  extern __shared__ float red[];
-  const int cta = blockIdx.x;
-  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31, gid = lane >> 2, tig = lane & 3;
-  const int i = find_entry(g, cta);
-  const int local = cta - g.tile_start[i];
-  const int chunk = local % g.tok_chunks[i];
-  const int f0 = (local / g.tok_chunks[i]) * 16;
-  const int e = g.expert[i];
-  const int row0 = offsets[e];
-  const int m = offsets[e + 1] - row0;
-  const int tb = chunk * g.token_chunk;
-  if (tb >= m) return;  // expert not routed this step (uniform across the CTA)
-
-  const uint16_t* wg = g.slab[i];
-  const bool ok0 = f0 + gid < F, ok8 = f0 + gid + 8 < F;
-  const size_t ra = ok0 ? f0 + gid : 0, rb = ok8 ? f0 + gid + 8 : 0;
-  const uint16_t* const r0[2] = {wg + ra * H, wg + (static_cast<size_t>(F) + ra) * H};
-  const uint16_t* const r8[2] = {wg + rb * H, wg + (static_cast<size_t>(F) + rb) * H};
-  const uint16_t* xr[NT];
+    // Cross-warp reduction through shared memory + epilogue.
 #pragma unroll
-  for (int j = 0; j < NT; ++j) {
-    const int t = tb + 8 * j + gid;
-    xr[j] = t < m ? x + static_cast<size_t>(perm_src[row0 + t] / k) * H : nullptr;
-  }
-  const int nblk = (H + 31) / 32, per = (nblk + W - 1) / W;
-  const int kbeg = min(H, warp * per * 32), kend = min(H, (warp + 1) * per * 32);
-
-  float acc[2][NT][4];
+    for (int mt = 0; mt < 2; ++mt)
 #pragma unroll
-  for (int mt = 0; mt < 2; ++mt)
+      for (int j = 0; j < NT; ++j)
 #pragma unroll
-    for (int j = 0; j < NT; ++j)
+        for (int q = 0; q < 4; ++q) red[(((warp * 2 + mt) * NT + j) * 4 + q) * 32 + lane] = acc[mt][j][q];
+    consumer_sync();
+    // Value v = (half, j, q, lane): c0,c1 -> row gid, tokens 2*tig+{0,1}; c2,c3 -> row gid+8.
+    const int n_out = (it.down ? 2 : 1) * NT * 4 * 32;
+    for (int v = threadIdx.x; v < n_out; v += kCWarps * 32) {
+      const int ln = v & 31, q = (v >> 5) & 3, j = (v >> 7) % NT, half = (v >> 7) / NT;
+      const int t = 8 * j + 2 * (ln & 3) + (q & 1);
+      const int r = (ln >> 2) + (q >> 1) * 8;
+      float s0 = 0.f, s1 = 0.f;
 #pragma unroll
-      for (int q = 0; q < 4; ++q) acc[mt][j][q] = 0.f;
-  stream_tile<NT, 2>(r0, r8, ok0, ok8, xr, kbeg, kend, tig, acc);
-  publish<NT, 2>(red, acc, warp, lane);
-  __syncthreads();
-
-  // Value v = (j, q, lane): c0,c1 -> row gid, tokens 2*tig+{0,1}; c2,c3 -> row gid+8.
-  for (int v = threadIdx.x; v < NT * 4 * 32; v += W * 32) {
-    const int ln = v & 31, q = (v >> 5) & 3, j = v >> 7;
-    const int t = tb + 8 * j + 2 * (ln & 3) + (q & 1);
-    const int f = f0 + (ln >> 2) + (q >> 1) * 8;
-    if (t < m && f < F) {
-      const float gv = reduced<NT, 2, W>(red, 0, j, q, ln), uv = reduced<NT, 2, W>(red, 1, j, q, ln);
-      const float hv = gv / (1.0f + expf(-gv)) * uv;
-      h_out[static_cast<size_t>(row0 + t) * F + f] = f32_to_bf16_rne(hv);
+      for (int w = 0; w < kCWarps; ++w) {
+        s0 += red[(((w * 2 + half) * NT + j) * 4 + q) * 32 + ln];
+        if (!it.down) s1 += red[(((w * 2 + 1) * NT + j) * 4 + q) * 32 + ln];
+      }
+      if (t < m) {
+        if (!it.down) {
+          const int f = it.r0 + r;
+          if (f < p.F) {
+            const float hv = s0 / (1.0f + expf(-s0)) * s1;
+            p.h[static_cast<size_t>(row0 + t) * p.F + f] = f32_to_bf16_rne(hv);
+          }
+        } else {
+          const int d = it.r0 + 16 * half + r;
+          if (d < p.H) p.y_part[it.split * p.split_stride + static_cast<size_t>(row0 + t) * p.H + d] = s0;
+        }
+      }
+    }
+    consumer_sync();  // red reusable; every h store of this item issued
+    if (!it.down && threadIdx.x == 0) {
+      __threadfence();
+      atomicAdd(p.sync + slot, 1);  // release this F tile to the down items of its split
     }
   }
 }
 
-template <int NT, int W>
-__global__ void __launch_bounds__(W * 32)
-ffn_down_kernel(const __grid_constant__ FfnLaunch g, const int32_t* __restrict__ offsets, int n_split,
-                int kchunk, int H, int F, const uint16_t* __restrict__ hin, float* __restrict__ y_part,
-                size_t split_stride) {
-  extern __shared__ float red[];
-  const int cta = blockIdx.x;
-  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31, gid = lane >> 2, tig = lane & 3;
-  const int i = find_entry(g, cta);
-  int local = cta - g.tile_start[i];
-  const int chunk = local % g.tok_chunks[i];
-  local /= g.tok_chunks[i];
-  const int split = local % n_split;
-  const int d0 = (local / n_split) * 16;
-  const int e = g.expert[i];
-  const int row0 = offsets[e];
-  const int m = offsets[e + 1] - row0;
-  const int tb = chunk * g.token_chunk;
-  if (tb >= m) return;
-  const int sbeg = split * kchunk, send = min(F, sbeg + kchunk);
+// ------------------------------------------------------------------ host side
+using EncodeFn = CUresult (*)(CUtensorMap*, CUtensorMapDataType, cuuint32_t, void*, const cuuint64_t*,
+                              const cuuint64_t*, const cuuint32_t*, const cuuint32_t*, CUtensorMapInterleave,
+                              CUtensorMapSwizzle, CUtensorMapL2promotion, CUtensorMapFloatOOBfill);
 
-  const uint16_t* wd = g.slab[i] + static_cast<size_t>(2) * F * H;
-  const bool ok0 = d0 + gid < H, ok8 = d0 + gid + 8 < H;
-  const uint16_t* const r0[1] = {wd + static_cast<size_t>(ok0 ? d0 + gid : 0) * F};
-  const uint16_t* const r8[1] = {wd + static_cast<size_t>(ok8 ? d0 + gid + 8 : 0) * F};
-  const uint16_t* xr[NT];
-#pragma unroll
-  for (int j = 0; j < NT; ++j) {
-    const int t = tb + 8 * j + gid;
-    xr[j] = t < m ? hin + static_cast<size_t>(row0 + t) * F : nullptr;
-  }
-  const int nblk = (send - sbeg + 31) / 32, per = (nblk + W - 1) / W;
-  const int kbeg = min(send, sbeg + warp * per * 32), kend = min(send, sbeg + (warp + 1) * per * 32);
-
-  float acc[1][NT][4];
-#pragma unroll
-  for (int j = 0; j < NT; ++j)
-#pragma unroll
-    for (int q = 0; q < 4; ++q) acc[0][j][q] = 0.f;
-  stream_tile<NT, 1>(r0, r8, ok0, ok8, xr, kbeg, kend, tig, acc);
-  publish<NT, 1>(red, acc, warp, lane);
-  __syncthreads();
-
-  float* out = y_part + split * split_stride;
-  for (int v = threadIdx.x; v < NT * 4 * 32; v += W * 32) {
-    const int ln = v & 31, q = (v >> 5) & 3, j = v >> 7;
-    const int t = tb + 8 * j + 2 * (ln & 3) + (q & 1);
-    const int d = d0 + (ln >> 2) + (q >> 1) * 8;
-    if (t < m && d < H) out[static_cast<size_t>(row0 + t) * H + d] = reduced<NT, 1, W>(red, 0, j, q, ln);
-  }
+EncodeFn encode_fn() {
+  static EncodeFn fn = nullptr;
+  static std::once_flag once;
+  std::call_once(once, [] {
+    void* ptr = nullptr;
+    cudaDriverEntryPointQueryResult q;
+    if (cudaGetDriverEntryPoint("cuTensorMapEncodeTiled", &ptr, cudaEnableDefault, &q) == cudaSuccess &&
+        q == cudaDriverEntryPointSuccess)
+      fn = reinterpret_cast<EncodeFn>(ptr);
+  });
+  if (!fn) fail(PS_ECUDA, "cuTensorMapEncodeTiled unavailable");
+  return fn;
 }
 
-template <int NT, int W>
-void launch_pair(const FfnLaunch& gu, const FfnLaunch& dn, const int32_t* offsets, const int32_t* perm_src,
-                 int k, const uint16_t* x, int H, int F, uint16_t* h, float* y_part, int n_split, int kchunk,
-                 size_t split_stride, cudaStream_t s) {
-  const int gu_ctas = gu.tile_start[gu.n], dn_ctas = dn.tile_start[dn.n];
-  const size_t smem_gu = sizeof(float) * W * 2 * NT * 4 * 32, smem_dn = sizeof(float) * W * NT * 4 * 32;
-  static bool attr_set = false;  // per template instance
-  if (!attr_set) {
-    PS_CUDA(cudaFuncSetAttribute(ffn_gateup_kernel<NT, W>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                 static_cast<int>(smem_gu)));
-    PS_CUDA(cudaFuncSetAttribute(ffn_down_kernel<NT, W>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                 static_cast<int>(smem_dn)));
-    attr_set = true;
-  }
-  if (gu_ctas > 0) {
-    ffn_gateup_kernel<NT, W><<<gu_ctas, W * 32, smem_gu, s>>>(gu, offsets, perm_src, k, x, H, F, h);
-    PS_LAUNCH_CHECK("ffn_gateup_kernel");
-  }
-  if (dn_ctas > 0) {
-    ffn_down_kernel<NT, W><<<dn_ctas, W * 32, smem_dn, s>>>(dn, offsets, n_split, kchunk, H, F, h, y_part,
-                                                           split_stride);
-    PS_LAUNCH_CHECK("ffn_down_kernel");
-  }
+// Row-major bf16 [rows, cols], box {256 cols, box_rows}, no swizzle, OOB -> zeros.
+CUtensorMap encode_rows(const void* base, uint64_t rows, uint64_t cols, uint32_t box_rows) {
+  CUtensorMap m;
+  cuuint64_t dims[2] = {cols, rows};
+  cuuint64_t strides[1] = {cols * 2};
+  cuuint32_t box[2] = {static_cast<cuuint32_t>(kHalf), box_rows};
+  cuuint32_t estr[2] = {1, 1};
+  CUresult r = encode_fn()(&m, CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, 2, const_cast<void*>(base), dims, strides, box, estr,
+                           CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_NONE,
+                           CU_TENSOR_MAP_L2_PROMOTION_L2_256B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+  if (r != CUDA_SUCCESS) fail(PS_ECUDA, "cuTensorMapEncodeTiled failed: " + std::to_string(static_cast<int>(r)));
+  return m;
 }
 
-template <int W>
-void launch_nt(int NT, const FfnLaunch& gu, const FfnLaunch& dn, const int32_t* offsets, const int32_t* perm_src,
-               int k, const uint16_t* x, int H, int F, uint16_t* h, float* y_part, int n_split, int kchunk,
-               size_t split_stride, cudaStream_t s) {
+struct SlabMaps {
+  CUtensorMap gu, dn;
+};
+
+// Maps depend only on (slab, H, F): encode once per slab (engine slabs are fixed pool slots).
+const SlabMaps& slab_maps(const uint16_t* slab, int H, int F) {
+  struct Key {
+    const void* p;
+    int H, F;
+    bool operator==(const Key& o) const { return p == o.p && H == o.H && F == o.F; }
+  };
+  struct Hash {
+    size_t operator()(const Key& k) const {
+      return std::hash<const void*>()(k.p) ^ (static_cast<size_t>(k.H) * 0x9e3779b97f4a7c15ull) ^ k.F;
+    }
+  };
+  static std::mutex mu;
+  static std::unordered_map<Key, SlabMaps, Hash> cache;
+  std::lock_guard<std::mutex> g(mu);
+  if (cache.size() > 8192) cache.clear();
+  auto it = cache.find(Key{slab, H, F});
+  if (it != cache.end()) return it->second;
+  SlabMaps m;
+  m.gu = encode_rows(slab, 2ull * F, static_cast<uint64_t>(H), 16);
+  m.dn = encode_rows(slab + 2ull * F * H, static_cast<uint64_t>(H), static_cast<uint64_t>(F), 32);
+  return cache.emplace(Key{slab, H, F}, m).first->second;
+}
+
+struct DeviceInfo {
+  int sms = 0;
+  std::unordered_map<const void*, int> blocks_per_sm;
+};
+
+DeviceInfo& device_info() {
+  static std::mutex mu;
+  static std::unordered_map<int, DeviceInfo> m;
+  int dev = 0;
+  PS_CUDA(cudaGetDevice(&dev));
+  std::lock_guard<std::mutex> g(mu);
+  DeviceInfo& d = m[dev];
+  if (d.sms == 0) PS_CUDA(cudaDeviceGetAttribute(&d.sms, cudaDevAttrMultiProcessorCount, dev));
+  return d;
+}
+
+// Counter workspace per (device, stream): launches on one stream are ordered, so they can
+// share it; the kernel leaves it zeroed.
+int* sync_workspace(cudaStream_t s) {
+  static std::mutex mu;
+  static std::unordered_map<uint64_t, int*> ws;
+  int dev = 0;
+  PS_CUDA(cudaGetDevice(&dev));
+  const uint64_t key = (static_cast<uint64_t>(dev) << 56) ^ reinterpret_cast<uint64_t>(s);
+  std::lock_guard<std::mutex> g(mu);
+  int*& ptr = ws[key];
+  if (!ptr) {
+    const size_t bytes = sizeof(int) * 2 * kSyncEntries * kMaxSplit;
+    PS_CUDA(cudaMalloc(&ptr, bytes));
+    PS_CUDA(cudaMemset(ptr, 0, bytes));
+  }
+  return ptr;
+}
+
+template <int NT, int CAP>
+void launch(const DecodeParams<CAP>& p, cudaStream_t s) {
+  DeviceInfo& d = device_info();
+  const size_t smem = Geo<NT>::kSmem;
+  const void* fn = reinterpret_cast<const void*>(ffn_decode_kernel<NT, CAP>);
+  int& bps = d.blocks_per_sm[fn];
+  if (bps == 0) {
+    PS_CUDA(cudaFuncSetAttribute(ffn_decode_kernel<NT, CAP>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                 static_cast<int>(smem)));
+    PS_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&bps, ffn_decode_kernel<NT, CAP>, kThreads, smem));
+    require(bps >= 1, "ffn_decode_kernel: does not fit on an SM");
+  }
+  const int total = p.gu_start[p.n] + p.dn_start[p.n];
+  const int grid = std::min(total, bps * d.sms);
+  cudaLaunchConfig_t cfg{};
+  cfg.gridDim = dim3(grid);
+  cfg.blockDim = dim3(kThreads);
+  cfg.dynamicSmemBytes = smem;
+  cfg.stream = s;
+  cudaLaunchAttribute attr[1];
+  attr[0].id = cudaLaunchAttributeCooperative;  // co-residency: the h dependency spins
+  attr[0].val.cooperative = 1;
+  cfg.attrs = attr;
+  cfg.numAttrs = 1;
+  PS_CUDA(cudaLaunchKernelEx(&cfg, ffn_decode_kernel<NT, CAP>, p));
+}
+
+struct Shape {
+  int H, F, k, n_split, kchunk, row_tiles_f, dn_tiles;
+};
+
+template <int CAP>
+void run_group(const ps_expert_group* group, int base, int count, const int32_t* counts_host, const Shape& sh,
+               int tok_base, int NT, const int32_t* offsets, const int32_t* perm_src, const uint16_t* x, uint16_t* h,
+               float* y_part, size_t split_stride, int* sync, cudaStream_t s) {
+  DecodeParams<CAP> p;
+  p.n = 0;
+  p.gu_start[0] = p.dn_start[0] = 0;
+  p.H = sh.H;
+  p.F = sh.F;
+  p.k = sh.k;
+  p.n_split = sh.n_split;
+  p.kchunk = sh.kchunk;
+  p.dn_tiles = sh.dn_tiles;
+  p.tok_base = tok_base;
+  p.offsets = offsets;
+  p.perm_src = perm_src;
+  p.x = x;
+  p.h = h;
+  p.y_part = y_part;
+  p.split_stride = split_stride;
+  p.sync = sync;
+  for (int i = base; i < base + count; ++i) {
+    const int e = group->experts[i];
+    if (counts_host[e] <= tok_base) continue;
+    const SlabMaps& m = slab_maps(group->slabs[i], sh.H, sh.F);
+    p.gu_map[p.n] = m.gu;
+    p.dn_map[p.n] = m.dn;
+    p.expert[p.n] = e;
+    p.gu_start[p.n + 1] = p.gu_start[p.n] + sh.row_tiles_f;
+    p.dn_start[p.n + 1] = p.dn_start[p.n] + sh.dn_tiles * sh.n_split;
+    ++p.n;
+  }
+  if (p.n == 0) return;
   switch (NT) {
-    case 1: launch_pair<1, W>(gu, dn, offsets, perm_src, k, x, H, F, h, y_part, n_split, kchunk, split_stride, s); break;
-    case 2: launch_pair<2, W>(gu, dn, offsets, perm_src, k, x, H, F, h, y_part, n_split, kchunk, split_stride, s); break;
-    case 4: launch_pair<4, W>(gu, dn, offsets, perm_src, k, x, H, F, h, y_part, n_split, kchunk, split_stride, s); break;
-    default: launch_pair<8, W>(gu, dn, offsets, perm_src, k, x, H, F, h, y_part, n_split, kchunk, split_stride, s); break;
+    case 1: launch<1, CAP>(p, s); break;
+    case 2: launch<2, CAP>(p, s); break;
+    case 4: launch<4, CAP>(p, s); break;
+    default: launch<8, CAP>(p, s); break;
   }
 }
 
@@ -273,11 +527,11 @@ using namespace ps;
 extern "C" {
 
 int ps_ffn_down_splits(int H, int F) {
-  // K is split across the warps of each CTA; a long down projection (Mixtral F=14336)
-  // is additionally split in two across CTAs so a single on-demand expert still puts
-  // ~26 warps on every SM (the register-limited occupancy) instead of ~14.
-  (void)H;
-  return F >= 8192 ? 2 : 1;
+  // Down items are (split of F) x (32 rows of H); splitting F into ~F/H parts keeps a
+  // down item about the size of a gate_up item (32 rows x H), which balances the
+  // persistent CTAs (Mixtral F=14336, H=4096: 4 splits of 3584 = 7 stages).
+  const int s = (F + H / 2) / std::max(H, 1);
+  return std::min(std::max(s, 1), kMaxSplit);
 }
 
 ps_status ps_expert_ffn(const ps_expert_group* group, const int32_t* counts_host, const int32_t* offsets,
@@ -286,7 +540,8 @@ ps_status ps_expert_ffn(const ps_expert_group* group, const int32_t* counts_host
   return guarded([&] {
     require(group && counts_host && offsets && perm_src && x && h && y_part, "ps_expert_ffn: null argument");
     require(H >= 8 && F >= 8 && H % 8 == 0 && F % 8 == 0, "ps_expert_ffn: H and F must be multiples of 8");
-    require(n_split >= 1 && group->n >= 0 && group->n <= PS_MAX_GROUP, "ps_expert_ffn: bad group/split");
+    require(n_split >= 1 && n_split <= kMaxSplit && group->n >= 0 && group->n <= PS_MAX_GROUP,
+            "ps_expert_ffn: bad group/split");
     cudaStream_t s = as_stream(stream);
     int max_m = 0;
     for (int i = 0; i < group->n; ++i) {
@@ -295,37 +550,25 @@ ps_status ps_expert_ffn(const ps_expert_group* group, const int32_t* counts_host
     }
     if (max_m == 0) return;
     require(total_rows >= max_m, "ps_expert_ffn: total_rows smaller than an expert's rows");
+    Shape sh{H, F, k, n_split, 0, (F + 15) / 16, (H + 31) / 32};
+    sh.kchunk = (F + n_split - 1) / n_split;
+    sh.kchunk = (sh.kchunk + 31) / 32 * 32;  // F tiles (16) never straddle a split
+    int* sync = sync_workspace(s);
     const size_t split_stride = static_cast<size_t>(total_rows) * H;
-    const int NT = max_m <= 8 ? 1 : max_m <= 16 ? 2 : max_m <= 32 ? 4 : 8;
-    const int token_chunk = 8 * NT;
-    int kchunk = (F + n_split - 1) / n_split;
-    kchunk = (kchunk + 31) / 32 * 32;
-    const int row_tiles_f = (F + 15) / 16, row_tiles_h = (H + 15) / 16;
 
-    for (int base = 0; base < group->n; base += kMaxGroup) {
-      FfnLaunch gu{}, dn{};
-      gu.token_chunk = dn.token_chunk = token_chunk;
-      for (int i = base; i < std::min(group->n, base + kMaxGroup); ++i) {
-        const int e = group->experts[i];
-        const int m = counts_host[e];
-        if (m == 0) continue;
-        const int tc = (m + token_chunk - 1) / token_chunk;
-        gu.expert[gu.n] = dn.expert[dn.n] = e;
-        gu.slab[gu.n] = dn.slab[dn.n] = group->slabs[i];
-        gu.tok_chunks[gu.n] = dn.tok_chunks[dn.n] = tc;
-        gu.tile_start[gu.n + 1] = gu.tile_start[gu.n] + row_tiles_f * tc;
-        dn.tile_start[dn.n + 1] = dn.tile_start[dn.n] + row_tiles_h * n_split * tc;
-        ++gu.n;
-        ++dn.n;
+    // Token passes of <= 64 rows per expert (decode has m_e <= 64: one pass).
+    for (int tok_base = 0; tok_base < max_m; tok_base += kMaxTokens) {
+      const int pass_m = std::min(kMaxTokens, max_m - tok_base);
+      const int NT = pass_m <= 8 ? 1 : pass_m <= 16 ? 2 : pass_m <= 32 ? 4 : 8;
+      for (int base = 0; base < group->n; base += kSyncEntries) {
+        const int count = std::min(kSyncEntries, group->n - base);
+        if (count <= 8)
+          run_group<8>(group, base, count, counts_host, sh, tok_base, NT, offsets, perm_src, x, h, y_part,
+                       split_stride, sync, s);
+        else
+          run_group<kSyncEntries>(group, base, count, counts_host, sh, tok_base, NT, offsets, perm_src, x, h, y_part,
+                                  split_stride, sync, s);
       }
-      if (gu.n == 0) continue;
-      // Warps per CTA: 8 while the launch is small (one or a few experts) so a single
-      // expert still fills every SM; 4 once there are >= 16 CTAs per SM anyway.
-      const int W = gu.tile_start[gu.n] >= 16 * kNumSMs ? 4 : 8;
-      if (W == 8)
-        launch_nt<8>(NT, gu, dn, offsets, perm_src, k, x, H, F, h, y_part, n_split, kchunk, split_stride, s);
-      else
-        launch_nt<4>(NT, gu, dn, offsets, perm_src, k, x, H, F, h, y_part, n_split, kchunk, split_stride, s);
     }
   });
 }
