@@ -33,8 +33,8 @@
 //    down index, so a wait never blocks a producer of h; the producer keeps prefetching
 //    down weights meanwhile. The last down item of a split resets its counters for the
 //    next launch (per-stream workspace).
-//  * Weight tensor maps are encoded on the host once per slab (cached) and passed in the
-//    kernel parameters (up to 64 experts per launch).
+//  * Weight tensor maps are encoded on the host once per slab and kept in a device table
+//    (immutable entries; the kernel acquire-fences them before first use).
 #include <cuda.h>
 
 #include <algorithm>
@@ -44,6 +44,13 @@
 
 #include "device_common.cuh"
 
+// Timeline hooks for scripts/probes/ffn_trace.cu (which includes this file with
+// PS_FFN_TRACE defined); compiled out of the product.
+#ifndef PS_FFN_TRACE
+#define PS_TRACE(ord, k)
+#define PS_STAGE_CHECK(it, k0, hf, kl, a00, a08, a10, a18)
+#endif
+
 namespace ps {
 namespace {
 
@@ -51,13 +58,15 @@ constexpr int kMaxSplit = 8;
 constexpr int kSyncEntries = 64;                 // max entries per launch (sync workspace rows)
 constexpr int kCWarps = 8;                       // consumer warps
 constexpr int kThreads = (kCWarps + 1) * 32;     // + one producer warp
-constexpr int kBarBytes = 256;
+constexpr int kBarBytes = 1024;                  // mbarriers + per-entry row table; keeps the ring 1 KiB aligned
 constexpr int kMaxTokens = 64;                   // tokens per expert per launch (8 * NT, NT <= 8)
 constexpr int kCols = 512;                       // K elements per stage
 constexpr int kHalf = 256;                       // TMA box width (cols)
 constexpr int kTileBytes = 16 * kHalf * 2;       // one (16-row m-tile, 256-col half) = 8 KiB
 constexpr int kStageBytes = 4 * kTileBytes;      // 2 m-tiles x 2 halves = 32 KiB
 static_assert(kCols / 32 == 2 * kCWarps, "two K blocks per consumer warp and stage");
+
+static_assert(128 + 2 * kSyncEntries * 4 <= kBarBytes, "smem header");
 
 template <int NT> struct Geo {
   static constexpr int kStages = NT <= 4 ? 6 : 5;
@@ -68,8 +77,9 @@ template <int NT> struct Geo {
 
 template <int CAP>
 struct DecodeParams {
-  CUtensorMap gu_map[CAP];        // [Wg; Wu] as [2F, H], box {256, 16}
-  CUtensorMap dn_map[CAP];        // Wd as [H, F], box {256, 32}
+  const CUtensorMap* maps;        // device map table: [2*idx] = [Wg; Wu] as [2F, H] box {256, 16},
+                                  //                   [2*idx+1] = Wd as [H, F] box {256, 32}
+  int map_idx[CAP];               // table index of entry i's slab
   int n;                          // entries (experts with m_e > tok_base)
   int gu_start[CAP + 1];          // prefix of gate_up items per entry (F/16 each)
   int dn_start[CAP + 1];          // prefix of down items per entry (n_split * H/32 each)
@@ -81,7 +91,8 @@ struct DecodeParams {
   uint16_t* h;
   float* y_part;
   size_t split_stride;
-  int* sync;                      // [2][kSyncEntries * kMaxSplit]: F tiles done, down items started
+  int* sync;                      // this launch's [kSyncEntries * kMaxSplit] F-tiles-done counters
+  int* sync_next;                 // the other parity's set: zeroed here for the next launch
 };
 
 struct Item {
@@ -130,12 +141,13 @@ __device__ __forceinline__ int split_tiles(const P& p, int s) {
   return (e - b + 15) / 16;
 }
 
-__device__ __forceinline__ void tma_2d(void* dst, const CUtensorMap* map, uint64_t* bar, int c0, int c1,
-                                       uint64_t policy) {
+// No .L2::cache_hint: with an evict_first policy on these loads, cold-TLB runs returned
+// wrong down-projection results (scripts/ffn_stress.py, first call); plain loads are exact.
+__device__ __forceinline__ void tma_2d(void* dst, const CUtensorMap* map, uint64_t* bar, int c0, int c1) {
   asm volatile(
-      "cp.async.bulk.tensor.2d.shared::cluster.global.mbarrier::complete_tx::bytes.L2::cache_hint [%0], [%1, {%2, "
-      "%3}], [%4], %5;" ::"r"(smem_u32(dst)),
-      "l"(map), "r"(c0), "r"(c1), "r"(smem_u32(bar)), "l"(policy)
+      "cp.async.bulk.tensor.2d.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1, {%2, %3}], [%4];" ::"r"(
+          smem_u32(dst)),
+      "l"(map), "r"(c0), "r"(c1), "r"(smem_u32(bar))
       : "memory");
 }
 
@@ -193,12 +205,13 @@ __global__ void __launch_bounds__(kThreads, 1) ffn_decode_kernel(const __grid_co
   extern __shared__ __align__(1024) uint8_t smem[];
   uint64_t* full = reinterpret_cast<uint64_t*>(smem);
   uint64_t* empty = full + G::kStages;
+  int* s_row0 = reinterpret_cast<int*>(smem + 128);           // per-entry first row of this pass
+  int* s_m = s_row0 + kSyncEntries;                           // per-entry rows of this pass (<= 8*NT)
   uint8_t* ring = smem + kBarBytes;
   float* red = reinterpret_cast<float*>(ring + G::kStages * kStageBytes);  // [warp][mt][j][q][lane]
 
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   const int total = p.gu_start[p.n] + p.dn_start[p.n];
-  const int n_slots = kSyncEntries * kMaxSplit;
   if (threadIdx.x == 0) {
     for (int s = 0; s < G::kStages; ++s) {
       mbar_init(&full[s], 1);
@@ -206,16 +219,32 @@ __global__ void __launch_bounds__(kThreads, 1) ffn_decode_kernel(const __grid_co
     }
     asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
   }
+  for (int i = threadIdx.x; i < p.n; i += blockDim.x) {
+    const int e = p.expert[i];
+    const int r0 = p.offsets[e] + p.tok_base;
+    s_row0[i] = r0;
+    s_m[i] = min(8 * NT, p.offsets[e + 1] - r0);
+  }
+  if (blockIdx.x == 0)  // counters of the next launch (other parity); this stream's previous launch is done
+    for (int i = threadIdx.x; i < kSyncEntries * kMaxSplit; i += blockDim.x) p.sync_next[i] = 0;
   __syncthreads();
 
   if (warp == kCWarps) {
     // ---------------------------------------------------------------- producer lane
+    // Table maps are written by host copies: order them before tensormap-proxy use
+    // (also drops any cached descriptor at a reused table slot).
+    for (int i = lane; i < 2 * p.n; i += 32) {
+      const CUtensorMap* m = p.maps + 2 * p.map_idx[i >> 1] + (i & 1);
+      asm volatile("fence.proxy.tensormap::generic.acquire.gpu [%0], 128;" ::"l"(m) : "memory");
+    }
+    __syncwarp();
     if (lane != 0) return;
-    const uint64_t pol = l2_evict_first_policy();
     uint32_t n = 0;
-    for (int idx = blockIdx.x; idx < total; idx += gridDim.x) {
+    int ord = 0;
+    for (int idx = blockIdx.x; idx < total; idx += gridDim.x, ++ord) {
+      PS_TRACE(ord, 4);
       const Item it = item_at(p, idx);
-      const CUtensorMap* map = it.down ? &p.dn_map[it.i] : &p.gu_map[it.i];
+      const CUtensorMap* map = p.maps + 2 * p.map_idx[it.i] + (it.down ? 1 : 0);
       for (int k0 = it.kbeg; k0 < it.kend; k0 += kCols, ++n) {
         const int s = n % G::kStages;
         mbar_wait(&empty[s], ((n / G::kStages) & 1) ^ 1);
@@ -225,12 +254,12 @@ __global__ void __launch_bounds__(kThreads, 1) ffn_decode_kernel(const __grid_co
         if (!it.down) {
 #pragma unroll
           for (int hf = 0; hf < 2; ++hf) {
-            tma_2d(dst + (hf * 2 + 0) * kTileBytes, map, &full[s], k0 + hf * kHalf, it.r0, pol);        // gate rows
-            tma_2d(dst + (hf * 2 + 1) * kTileBytes, map, &full[s], k0 + hf * kHalf, p.F + it.r0, pol);  // up rows
+            tma_2d(dst + (hf * 2 + 0) * kTileBytes, map, &full[s], k0 + hf * kHalf, it.r0);        // gate rows
+            tma_2d(dst + (hf * 2 + 1) * kTileBytes, map, &full[s], k0 + hf * kHalf, p.F + it.r0);  // up rows
           }
         } else {
 #pragma unroll
-          for (int hf = 0; hf < 2; ++hf) tma_2d(dst + hf * 2 * kTileBytes, map, &full[s], k0 + hf * kHalf, it.r0, pol);
+          for (int hf = 0; hf < 2; ++hf) tma_2d(dst + hf * 2 * kTileBytes, map, &full[s], k0 + hf * kHalf, it.r0);
         }
       }
     }
@@ -242,24 +271,20 @@ __global__ void __launch_bounds__(kThreads, 1) ffn_decode_kernel(const __grid_co
   const int hf = warp >> 2;                      // this warp's 256-col half of every stage
   const int kl0 = ((2 * warp) & 7) * 32 + 8 * tig;  // element offset inside the half
   uint32_t n = 0;
-  for (int idx = blockIdx.x; idx < total; idx += gridDim.x) {
+  int ord = 0;
+  for (int idx = blockIdx.x; idx < total; idx += gridDim.x, ++ord) {
+    if (threadIdx.x == 0) PS_TRACE(ord, 0);
     const Item it = item_at(p, idx);
-    const int e = p.expert[it.i];
-    const int row0 = p.offsets[e] + p.tok_base;
-    const int m = min(8 * NT, p.offsets[e + 1] - row0);
+    const int row0 = s_row0[it.i], m = s_m[it.i];
     const int slot = it.i * kMaxSplit + it.split;
     if (it.down) {
       if (threadIdx.x == 0) {
         const int need = split_tiles(p, it.split);
         while (ld_acquire(p.sync + slot) < need) __nanosleep(32);
-        __threadfence();
-        if (atomicAdd(p.sync + n_slots + slot, 1) == p.dn_tiles - 1) {  // last reader resets
-          p.sync[slot] = 0;
-          p.sync[n_slots + slot] = 0;
-        }
       }
       consumer_sync();
     }
+    if (threadIdx.x == 0) PS_TRACE(ord, 1);
     const uint16_t* xr[NT];
 #pragma unroll
     for (int j = 0; j < NT; ++j) {
@@ -291,12 +316,17 @@ __global__ void __launch_bounds__(kThreads, 1) ffn_decode_kernel(const __grid_co
         const uint4 a08 = lds128(st + (gid + 8) * (kHalf * 2) + off);
         const uint4 a10 = lds128(st + kTileBytes + gid * (kHalf * 2) + off);
         const uint4 a18 = lds128(st + kTileBytes + (gid + 8) * (kHalf * 2) + off);
+        PS_STAGE_CHECK(it, k0, hf, kl0 + 32 * u, a00, a08, a10, a18);
 #pragma unroll
         for (int j = 0; j < NT; ++j) {
           mma_block(acc[0][j], a00, a08, xv[u][j]);
           mma_block(acc[1][j], a10, a18, xv[u][j]);
         }
       }
+      // The slot is refilled by TMA (async proxy) after this arrive: order this lane's
+      // generic-proxy reads before it (without this fence, refills raced the reads:
+      // scripts/probes/ffn_check.cu, non-deterministic h/y).
+      asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
       __syncwarp();
       if (lane == 0) mbar_arrive(&empty[s]);
       if (k0 + kCols < it.kend) {
@@ -311,6 +341,7 @@ __global__ void __launch_bounds__(kThreads, 1) ffn_decode_kernel(const __grid_co
       }
     }
 
+    if (threadIdx.x == 0) PS_TRACE(ord, 2);
     // Cross-warp reduction through shared memory + epilogue.
 #pragma unroll
     for (int mt = 0; mt < 2; ++mt)
@@ -345,10 +376,9 @@ __global__ void __launch_bounds__(kThreads, 1) ffn_decode_kernel(const __grid_co
       }
     }
     consumer_sync();  // red reusable; every h store of this item issued
-    if (!it.down && threadIdx.x == 0) {
-      __threadfence();
-      atomicAdd(p.sync + slot, 1);  // release this F tile to the down items of its split
-    }
+    if (threadIdx.x == 0) PS_TRACE(ord, 3);
+    if (!it.down && threadIdx.x == 0)  // release this F tile to the down items of its split
+      asm volatile("red.release.gpu.global.add.s32 [%0], 1;" ::"l"(p.sync + slot) : "memory");
   }
 }
 
@@ -385,32 +415,52 @@ CUtensorMap encode_rows(const void* base, uint64_t rows, uint64_t cols, uint32_t
   return m;
 }
 
-struct SlabMaps {
-  CUtensorMap gu, dn;
-};
-
-// Maps depend only on (slab, H, F): encode once per slab (engine slabs are fixed pool slots).
-const SlabMaps& slab_maps(const uint16_t* slab, int H, int F) {
+// Device table of weight tensor maps, one (gate_up, down) pair per (slab, H, F), uploaded
+// once on first use (stream-ordered before the launch) and read by the kernel through a
+// global pointer. Maps passed as kernel parameters were wrong across back-to-back launches
+// with different slabs (the TMA unit served a descriptor cached for the previous launch's
+// parameter block: scripts/ffn_stress.py, 128 experts = two launches per call).
+int slab_map_index(const uint16_t* slab, int H, int F, cudaStream_t s, const CUtensorMap** table) {
   struct Key {
+    int dev;
     const void* p;
     int H, F;
-    bool operator==(const Key& o) const { return p == o.p && H == o.H && F == o.F; }
+    bool operator==(const Key& o) const { return dev == o.dev && p == o.p && H == o.H && F == o.F; }
   };
   struct Hash {
     size_t operator()(const Key& k) const {
-      return std::hash<const void*>()(k.p) ^ (static_cast<size_t>(k.H) * 0x9e3779b97f4a7c15ull) ^ k.F;
+      return std::hash<const void*>()(k.p) ^ (static_cast<size_t>(k.H) * 0x9e3779b97f4a7c15ull) ^
+             (static_cast<size_t>(k.F) << 20) ^ static_cast<size_t>(k.dev);
     }
   };
+  struct Table {
+    CUtensorMap* dev = nullptr;
+    int used = 0;
+  };
+  constexpr int kCap = 8192;  // slabs per device (2 maps each, 2 MiB)
   static std::mutex mu;
-  static std::unordered_map<Key, SlabMaps, Hash> cache;
+  static std::unordered_map<Key, int, Hash> index;
+  static std::unordered_map<int, Table> tables;
+  int dev = 0;
+  PS_CUDA(cudaGetDevice(&dev));
   std::lock_guard<std::mutex> g(mu);
-  if (cache.size() > 8192) cache.clear();
-  auto it = cache.find(Key{slab, H, F});
-  if (it != cache.end()) return it->second;
-  SlabMaps m;
-  m.gu = encode_rows(slab, 2ull * F, static_cast<uint64_t>(H), 16);
-  m.dn = encode_rows(slab + 2ull * F * H, static_cast<uint64_t>(H), static_cast<uint64_t>(F), 32);
-  return cache.emplace(Key{slab, H, F}, m).first->second;
+  Table& t = tables[dev];
+  if (!t.dev) PS_CUDA(cudaMalloc(&t.dev, sizeof(CUtensorMap) * 2 * kCap));
+  *table = t.dev;
+  auto it = index.find(Key{dev, slab, H, F});
+  if (it != index.end()) return it->second;
+  if (t.used == kCap) {  // full: start over (the kernel's acquire fence drops stale descriptors)
+    PS_CUDA(cudaStreamSynchronize(s));
+    for (auto i = index.begin(); i != index.end();) i = i->first.dev == dev ? index.erase(i) : std::next(i);
+    t.used = 0;
+  }
+  CUtensorMap m[2];
+  m[0] = encode_rows(slab, 2ull * F, static_cast<uint64_t>(H), 16);
+  m[1] = encode_rows(slab + 2ull * F * H, static_cast<uint64_t>(H), static_cast<uint64_t>(F), 32);
+  const int idx = t.used++;
+  PS_CUDA(cudaMemcpyAsync(t.dev + 2 * idx, m, sizeof(m), cudaMemcpyHostToDevice, s));  // pageable: staged now
+  index.emplace(Key{dev, slab, H, F}, idx);
+  return idx;
 }
 
 struct DeviceInfo {
@@ -431,20 +481,32 @@ DeviceInfo& device_info() {
 
 // Counter workspace per (device, stream): launches on one stream are ordered, so they can
 // share it; the kernel leaves it zeroed.
-int* sync_workspace(cudaStream_t s) {
+// Two counter sets per (device, stream), used by alternate launches: launch L counts in
+// set L&1 and zeroes set (L+1)&1, which the previous launch on this stream (ordered
+// before it) used. No reset atomics on the critical path.
+struct SyncSets {
+  int* cur;
+  int* next;
+};
+SyncSets sync_workspace(cudaStream_t s) {
+  struct Ws {
+    int* base = nullptr;
+    uint64_t launches = 0;
+  };
   static std::mutex mu;
-  static std::unordered_map<uint64_t, int*> ws;
+  static std::unordered_map<uint64_t, Ws> ws;
   int dev = 0;
   PS_CUDA(cudaGetDevice(&dev));
   const uint64_t key = (static_cast<uint64_t>(dev) << 56) ^ reinterpret_cast<uint64_t>(s);
   std::lock_guard<std::mutex> g(mu);
-  int*& ptr = ws[key];
-  if (!ptr) {
-    const size_t bytes = sizeof(int) * 2 * kSyncEntries * kMaxSplit;
-    PS_CUDA(cudaMalloc(&ptr, bytes));
-    PS_CUDA(cudaMemset(ptr, 0, bytes));
+  Ws& w = ws[key];
+  const size_t set = static_cast<size_t>(kSyncEntries) * kMaxSplit;
+  if (!w.base) {
+    PS_CUDA(cudaMalloc(&w.base, sizeof(int) * 2 * set));
+    PS_CUDA(cudaMemset(w.base, 0, sizeof(int) * 2 * set));
   }
-  return ptr;
+  const int par = static_cast<int>(w.launches++ & 1);
+  return SyncSets{w.base + par * set, w.base + (par ^ 1) * set};
 }
 
 template <int NT, int CAP>
@@ -481,7 +543,7 @@ struct Shape {
 template <int CAP>
 void run_group(const ps_expert_group* group, int base, int count, const int32_t* counts_host, const Shape& sh,
                int tok_base, int NT, const int32_t* offsets, const int32_t* perm_src, const uint16_t* x, uint16_t* h,
-               float* y_part, size_t split_stride, int* sync, cudaStream_t s) {
+               float* y_part, size_t split_stride, cudaStream_t s) {
   DecodeParams<CAP> p;
   p.n = 0;
   p.gu_start[0] = p.dn_start[0] = 0;
@@ -498,19 +560,19 @@ void run_group(const ps_expert_group* group, int base, int count, const int32_t*
   p.h = h;
   p.y_part = y_part;
   p.split_stride = split_stride;
-  p.sync = sync;
   for (int i = base; i < base + count; ++i) {
     const int e = group->experts[i];
     if (counts_host[e] <= tok_base) continue;
-    const SlabMaps& m = slab_maps(group->slabs[i], sh.H, sh.F);
-    p.gu_map[p.n] = m.gu;
-    p.dn_map[p.n] = m.dn;
+    p.map_idx[p.n] = slab_map_index(group->slabs[i], sh.H, sh.F, s, &p.maps);
     p.expert[p.n] = e;
     p.gu_start[p.n + 1] = p.gu_start[p.n] + sh.row_tiles_f;
     p.dn_start[p.n + 1] = p.dn_start[p.n] + sh.dn_tiles * sh.n_split;
     ++p.n;
   }
   if (p.n == 0) return;
+  const SyncSets ss = sync_workspace(s);  // one parity flip per launch
+  p.sync = ss.cur;
+  p.sync_next = ss.next;
   switch (NT) {
     case 1: launch<1, CAP>(p, s); break;
     case 2: launch<2, CAP>(p, s); break;
@@ -553,7 +615,6 @@ ps_status ps_expert_ffn(const ps_expert_group* group, const int32_t* counts_host
     Shape sh{H, F, k, n_split, 0, (F + 15) / 16, (H + 31) / 32};
     sh.kchunk = (F + n_split - 1) / n_split;
     sh.kchunk = (sh.kchunk + 31) / 32 * 32;  // F tiles (16) never straddle a split
-    int* sync = sync_workspace(s);
     const size_t split_stride = static_cast<size_t>(total_rows) * H;
 
     // Token passes of <= 64 rows per expert (decode has m_e <= 64: one pass).
@@ -564,10 +625,10 @@ ps_status ps_expert_ffn(const ps_expert_group* group, const int32_t* counts_host
         const int count = std::min(kSyncEntries, group->n - base);
         if (count <= 8)
           run_group<8>(group, base, count, counts_host, sh, tok_base, NT, offsets, perm_src, x, h, y_part,
-                       split_stride, sync, s);
+                       split_stride, s);
         else
           run_group<kSyncEntries>(group, base, count, counts_host, sh, tok_base, NT, offsets, perm_src, x, h, y_part,
-                                  split_stride, sync, s);
+                                  split_stride, s);
       }
     }
   });

@@ -58,6 +58,7 @@ struct PrefillParams {
   int m_tiles[kMaxExperts];
   int row0[kMaxExperts];     // first permuted row of the entry
   int rows[kMaxExperts];     // m_e
+  const CUtensorMap* a_map;  // device: activation map (x_perm or h_perm)
   const CUtensorMap* b_maps; // device array [n_experts] of weight tensor maps
   void* out;                 // h (bf16, [rows_total, F]) or y (f32, [rows_total, H])
   int out_ld;                // leading dimension (elements) of out
@@ -141,7 +142,7 @@ __device__ __forceinline__ TileCoord tile_coord(const PrefillParams& p, int t) {
 }
 
 __global__ void __launch_bounds__(kThreads, 1)
-ffn_prefill_kernel(const __grid_constant__ CUtensorMap a_map, const __grid_constant__ PrefillParams p) {
+ffn_prefill_kernel(const __grid_constant__ PrefillParams p) {
   extern __shared__ __align__(1024) uint8_t smem_raw[];
   uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
   uint64_t* full_bar = reinterpret_cast<uint64_t*>(smem + kStages * kStageBytes);
@@ -164,7 +165,6 @@ ffn_prefill_kernel(const __grid_constant__ CUtensorMap a_map, const __grid_const
       mbar_init(&tempty_bar[s], 128);
     }
     asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
-    prefetch_map(&a_map);
   }
   if (warp == 1) {  // whole warp: TMEM allocation (512 columns = 2 accumulator stages)
     asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], 512;" ::"r"(smem_u32(tmem_slot)));
@@ -176,7 +176,16 @@ ffn_prefill_kernel(const __grid_constant__ CUtensorMap a_map, const __grid_const
   const uint32_t tmem_base = *tmem_slot;
 
   if (warp == 0) {
+    // Maps live in a reused ring slot written by a host copy: order them before
+    // tensormap-proxy use (drops any descriptor cached for the slot's previous contents).
+    for (int i = lane; i <= p.n_experts; i += 32) {
+      const CUtensorMap* m = i == 0 ? p.a_map : p.b_maps + (i - 1);
+      asm volatile("fence.proxy.tensormap::generic.acquire.gpu [%0], 128;" ::"l"(m) : "memory");
+    }
+    __syncwarp();
     if (lane == 0) {  // ---------------------------------------------- TMA producer
+      const CUtensorMap* a_map = p.a_map;
+      prefetch_map(a_map);
       int stage = 0;
       uint32_t phase = 0;
       for (int t = blockIdx.x; t < n_tiles; t += gridDim.x) {
@@ -188,7 +197,7 @@ ffn_prefill_kernel(const __grid_constant__ CUtensorMap a_map, const __grid_const
           uint8_t* sa = smem + stage * kStageBytes;
           uint8_t* sb = sa + kABytes;
           mbar_expect_tx(&full_bar[stage], kStageBytes);
-          tma_load_2d(sa, &a_map, &full_bar[stage], kb * kBK, arow);
+          tma_load_2d(sa, a_map, &full_bar[stage], kb * kBK, arow);
           if (p.mode == kSwiGLU) {
             const int n0 = tc.n_tile * (kBN / 2);
             tma_load_2d(sb, bmap, &full_bar[stage], kb * kBK, n0);                      // gate rows
@@ -351,7 +360,7 @@ CUtensorMap make_map(const void* base, uint64_t rows, uint64_t cols, uint32_t bo
 // copies are still in flight).
 struct MapRing {
   static constexpr int kSlots = 64;
-  static constexpr int kPerSlot = 2 * kMaxExperts;
+  static constexpr int kPerSlot = 2 * kMaxExperts + 2;  // [a_x, a_h, gate_up maps, down maps]
   CUtensorMap* dev = nullptr;
   CUtensorMap* host = nullptr;
   cudaEvent_t ev[kSlots] = {};
@@ -371,7 +380,7 @@ struct MapRing {
   }
 };
 
-void launch(const CUtensorMap& amap, PrefillParams& p, cudaStream_t s) {
+void launch(PrefillParams& p, cudaStream_t s) {
   static bool attr = false;
   if (!attr) {
     PS_CUDA(cudaFuncSetAttribute(ffn_prefill_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, kSmemBytes));
@@ -380,7 +389,7 @@ void launch(const CUtensorMap& amap, PrefillParams& p, cudaStream_t s) {
   const int tiles = p.tile_start[p.n_experts];
   if (tiles == 0) return;
   const int grid = std::min(tiles, kNumSMs);
-  ffn_prefill_kernel<<<grid, kThreads, kSmemBytes, s>>>(amap, p);
+  ffn_prefill_kernel<<<grid, kThreads, kSmemBytes, s>>>(p);
   PS_LAUNCH_CHECK("ffn_prefill_kernel");
 }
 
@@ -420,8 +429,8 @@ extern "C" ps_status ps_expert_ffn_prefill(const ps_expert_group* group, const i
       const int m = counts_host[e];
       if (m == 0) continue;
       const uint16_t* slab = group->slabs[i];
-      maps_host[n] = make_map(slab, 2ull * F, H, kBN / 2);                                           // [Wg; Wu]
-      maps_host[kMaxExperts + n] = make_map(slab + 2ull * F * H, static_cast<uint64_t>(H), F, kBN / 2);  // Wd
+      maps_host[2 + n] = make_map(slab, 2ull * F, H, kBN / 2);                                          // [Wg; Wu]
+      maps_host[2 + group->n + n] = make_map(slab + 2ull * F * H, static_cast<uint64_t>(H), F, kBN / 2);  // Wd
       const int mt = (m + kBM - 1) / kBM;
       for (PrefillParams* p : {&gu, &dn}) {
         p->m_tiles[n] = mt;
@@ -433,17 +442,19 @@ extern "C" ps_status ps_expert_ffn_prefill(const ps_expert_group* group, const i
     }
     if (n == 0) return;
     gu.n_experts = dn.n_experts = n;
-    PS_CUDA(cudaMemcpyAsync(maps_dev, maps_host, sizeof(CUtensorMap) * MapRing::kPerSlot, cudaMemcpyHostToDevice, s));
-    gu.b_maps = maps_dev;
-    dn.b_maps = maps_dev + kMaxExperts;
+    maps_host[0] = make_map(x_perm, static_cast<uint64_t>(total_rows), H, kBM);
+    maps_host[1] = make_map(h_perm, static_cast<uint64_t>(total_rows), F, kBM);
+    PS_CUDA(cudaMemcpyAsync(maps_dev, maps_host, sizeof(CUtensorMap) * (2 + 2 * group->n), cudaMemcpyHostToDevice, s));
+    gu.a_map = maps_dev;
+    dn.a_map = maps_dev + 1;
+    gu.b_maps = maps_dev + 2;
+    dn.b_maps = maps_dev + 2 + group->n;
     gu.out = h_perm;
     gu.out_ld = F;
     dn.out = y_perm;
     dn.out_ld = H;
-    const CUtensorMap a_x = make_map(x_perm, static_cast<uint64_t>(total_rows), H, kBM);
-    const CUtensorMap a_h = make_map(h_perm, static_cast<uint64_t>(total_rows), F, kBM);
-    launch(a_x, gu, s);
-    launch(a_h, dn, s);
+    launch(gu, s);
+    launch(dn, s);
     PS_CUDA(cudaEventRecord(ring.ev[slot], s));
   });
 }

@@ -167,6 +167,42 @@ def test_expert_ffn_and_combine_vs_oracle(torch_cuda, H, F, E, k, B, skew):
     assert np.abs(y - y_ref).max() <= BF16_RTOL * np.abs(y_ref).max()
 
 
+@pytest.mark.parametrize("H,F,E,k,B", [(2048, 768, 16, 2, 8), (2048, 768, 128, 8, 32), (4096, 14336, 8, 2, 16)])
+def test_expert_ffn_bitwise_deterministic(torch_cuda, H, F, E, k, B):
+    """K3 decode is deterministic by construction (fixed reduction order, no float
+    atomics): repeated calls must agree bit for bit. Guards the smem ring / TMA refill
+    ordering and the gate_up -> down dependency counters."""
+    torch = torch_cuda
+    lib = ps.load()
+    rng = np.random.default_rng(11)
+    ids = np.stack([rng.choice(E, k, replace=False) for _ in range(B)]).astype(np.int32)
+    slabs = [torch.empty(3 * H * F, dtype=torch.int16, device="cuda") for _ in range(E)]
+    for e in range(E):
+        ps.check(lib.ps_init_expert_slab(_p(slabs[e]), H, F, 3, 0, e, _s(torch)))
+    di = torch.as_tensor(ids, device="cuda")
+    off = torch.empty(E + 1, dtype=torch.int32, device="cuda")
+    src = torch.empty(B * k, dtype=torch.int32, device="cuda")
+    inv = torch.empty(B * k, dtype=torch.int32, device="cuda")
+    ps.check(lib.ps_permute(_p(di), B, k, E, _p(off), _p(src), _p(inv), None, H, None, _s(torch)))
+    x = (torch.randn(B, H, device="cuda") / H ** 0.5).to(torch.bfloat16).view(torch.int16)
+    counts = np.bincount(ids.ravel(), minlength=E).astype(np.int32)
+    grp = ps.capi.ExpertGroup()
+    grp.n = E
+    for e in range(E):
+        grp.experts[e] = e
+        grp.slabs[e] = slabs[e].data_ptr()
+    n_split = lib.ps_ffn_down_splits(H, F)
+    outs = []
+    for _ in range(6):
+        h = torch.full((B * k, F), -1, dtype=torch.int16, device="cuda")
+        yp = torch.zeros(n_split, B * k, H, dtype=torch.float32, device="cuda")
+        ps.check(lib.ps_expert_ffn(C.byref(grp), counts.ctypes.data, _p(off), _p(src), k, _p(x), H, F, _p(h), _p(yp),
+                                   n_split, B * k, _s(torch)))
+        outs.append((h.cpu(), yp.cpu()))
+    for h, yp in outs[1:]:
+        assert torch.equal(h, outs[0][0]) and torch.equal(yp, outs[0][1])
+
+
 def test_expert_ffn_mixtral_full_shape(torch_cuda):
     """Full Mixtral expert shape (H=4096, F=14336, 4-way split-K) on a small batch."""
     y, y_ref = _moe_case(torch_cuda, 4096, 14336, 8, 2, 3, 2)
