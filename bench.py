@@ -349,7 +349,7 @@ def run_ours(args):
     value = N * B / (dev_ms / 1e3)
     peak_hbm, peak_kind = measured_peaks()
     ffn_ms = st["ffn_ms_total"]
-    ffn_launches = max(1, st["ffn_launches"] // 2)
+    ffn_launches = max(1, st["ffn_launches"])  # one persistent K3 kernel (gate_up + down) per launch
     # algorithmic bytes of the FFN launches = sum over launched experts with m_e > 0 of
     # 3*H*F*2 (weights; activations are <0.1% at decode)
     ffn_bytes = ffn_bytes_total(st, spec)

@@ -366,13 +366,22 @@ void ffn(ps_engine_s& e, const ps_expert_group& g, const int32_t* counts_host, i
     s = ps_expert_ffn_prefill(&g, counts_host, src.offsets_host, e.x_perm, src.rows, e.H, e.F, e.hbuf, e.y_part,
                               e.sc);
     e.st.tc_launches += 2;
+    e.st.ffn_launches += 2;  // gate_up + down
+    e.st.kernel_launches += 2;
   } else {
     s = ps_expert_ffn(&g, counts_host, src.offsets_dev, src.perm_dev, src.k, src.x, e.H, e.F, e.hbuf, e.y_part,
                       e.step_split, src.rows, e.sc);
+    // One persistent kernel per pass of <= 64 tokens per expert and <= 64 experts.
+    int launches = 0;
+    for (int base = 0; base < max_m; base += 64) {
+      int n = 0;
+      for (int i = 0; i < g.n; ++i) n += counts_host[g.experts[i]] > base;
+      launches += (n + 63) / 64;
+    }
+    e.st.ffn_launches += launches;
+    e.st.kernel_launches += launches;
   }
   if (s != PS_OK) fail(s, ps_last_error());
-  e.st.ffn_launches += 2;
-  e.st.kernel_launches += 2;
   if (exact_counts) e.st.ffn_flops_total += 6.0 * rows * e.H * e.F;
   if (timed) {
     b = take_event(e);
