@@ -48,7 +48,7 @@
 // PS_FFN_TRACE defined); compiled out of the product.
 #ifndef PS_FFN_TRACE
 #define PS_TRACE(ord, k)
-#define PS_STAGE_CHECK(it, k0, hf, kl, a00, a08, a10, a18)
+#define PS_STAGE_CHECK(it, k0, hf, kl, mt, a0, a8)
 #endif
 
 namespace ps {
@@ -60,29 +60,39 @@ constexpr int kCWarps = 8;                       // consumer warps
 constexpr int kThreads = (kCWarps + 1) * 32;     // + one producer warp
 constexpr int kBarBytes = 1024;                  // mbarriers + per-entry row table; keeps the ring 1 KiB aligned
 constexpr int kMaxTokens = 64;                   // tokens per expert per launch (8 * NT, NT <= 8)
-constexpr int kCols = 512;                       // K elements per stage
 constexpr int kHalf = 256;                       // TMA box width (cols)
 constexpr int kTileBytes = 16 * kHalf * 2;       // one (16-row m-tile, 256-col half) = 8 KiB
-constexpr int kStageBytes = 4 * kTileBytes;      // 2 m-tiles x 2 halves = 32 KiB
-static_assert(kCols / 32 == 2 * kCWarps, "two K blocks per consumer warp and stage");
+constexpr int kStageBytes = 4 * kTileBytes;      // 32 KiB: MT m-tiles x (4 / MT) halves
+constexpr int kMaps = 3;                         // per slab: gate_up {256,16}, gate_up {256,32}, down {256,32}
 
 static_assert(128 + 2 * kSyncEntries * 4 <= kBarBytes, "smem header");
 
-template <int NT> struct Geo {
-  static constexpr int kStages = NT <= 4 ? 6 : 5;
-  static constexpr int kRedBytes = kCWarps * 2 * NT * 4 * 32 * 4;
+// NT = 8-token groups per expert, MT = 16-row m-tiles per stage (and per item). A stage
+// is always 32 KiB: MT = 2 -> 32 rows x 512 cols, MT = 4 -> 64 rows x 256 cols. Activation
+// bytes per stage scale with tokens / rows, so more tokens use taller items (MT = 4): the
+// activations are re-read from L2 once per item and would otherwise approach the L2
+// bandwidth at 16+ tokens per expert.
+template <int NT, int MT> struct Geo {
+  static constexpr int kCols = 2 * 512 / MT;          // K elements per stage
+  static constexpr int kKb = 2;                       // K blocks per consumer warp and stage
+  static constexpr int kWarpsPerStage = kCols / 64;   // 8 (MT = 2) or 4 (MT = 4)
+  static constexpr int kGroups = kCWarps / kWarpsPerStage;  // warp groups taking alternate stages
+  static constexpr int kRows = 16 * MT;               // weight rows per item and stage
+  static constexpr int kRedBytes = kCWarps * MT * NT * 4 * 32 * 4;
+  static constexpr int kStages = (227 * 1024 - kBarBytes - kRedBytes) / kStageBytes > 6
+                                     ? 6 : (227 * 1024 - kBarBytes - kRedBytes) / kStageBytes;
   static constexpr int kSmem = kBarBytes + kStages * kStageBytes + kRedBytes;
-  static_assert(kSmem <= 227 * 1024, "decode FFN smem budget");
+  static_assert(kStages >= 3 && kSmem <= 227 * 1024, "decode FFN smem budget");
 };
 
 template <int CAP>
 struct DecodeParams {
-  const CUtensorMap* maps;        // device map table: [2*idx] = [Wg; Wu] as [2F, H] box {256, 16},
-                                  //                   [2*idx+1] = Wd as [H, F] box {256, 32}
+  const CUtensorMap* maps;        // device map table, kMaps per slab: [Wg; Wu] as [2F, H] box {256, 16}
+                                  //   and box {256, 32}; Wd as [H, F] box {256, 32}
   int map_idx[CAP];               // table index of entry i's slab
   int n;                          // entries (experts with m_e > tok_base)
-  int gu_start[CAP + 1];          // prefix of gate_up items per entry (F/16 each)
-  int dn_start[CAP + 1];          // prefix of down items per entry (n_split * H/32 each)
+  int gu_start[CAP + 1];          // prefix of gate_up items per entry (F / (8 MT) each)
+  int dn_start[CAP + 1];          // prefix of down items per entry (n_split * H / (16 MT) each)
   int expert[CAP];
   int H, F, k, n_split, kchunk, dn_tiles, tok_base;
   const int32_t* offsets;
@@ -91,7 +101,7 @@ struct DecodeParams {
   uint16_t* h;
   float* y_part;
   size_t split_stride;
-  int* sync;                      // this launch's [kSyncEntries * kMaxSplit] F-tiles-done counters
+  int* sync;                      // this launch's [kSyncEntries * kMaxSplit] gate_up-items-done counters
   int* sync_next;                 // the other parity's set: zeroed here for the next launch
 };
 
@@ -110,14 +120,16 @@ __device__ __forceinline__ int find_prefix(const int* start, int n, int w) {
   return lo;
 }
 
-template <class P>
+// gate_up items: 8*MT F rows (8*MT gate + 8*MT up weight rows) x all of H; down items:
+// 16*MT H rows x one split of F.
+template <int MT, class P>
 __device__ __forceinline__ Item item_at(const P& p, int idx) {
   Item it;
   const int gu_total = p.gu_start[p.n];
   if (idx < gu_total) {
     it.down = false;
     it.i = find_prefix(p.gu_start, p.n, idx);
-    it.r0 = (idx - p.gu_start[it.i]) * 16;
+    it.r0 = (idx - p.gu_start[it.i]) * 8 * MT;
     it.split = it.r0 / p.kchunk;
     it.kbeg = 0;
     it.kend = p.H;
@@ -127,22 +139,20 @@ __device__ __forceinline__ Item item_at(const P& p, int idx) {
     it.i = find_prefix(p.dn_start, p.n, idx);
     const int local = idx - p.dn_start[it.i];
     it.split = local / p.dn_tiles;
-    it.r0 = (local % p.dn_tiles) * 32;
+    it.r0 = (local % p.dn_tiles) * 16 * MT;
     it.kbeg = min(p.F, it.split * p.kchunk);
     it.kend = min(p.F, it.split * p.kchunk + p.kchunk);
   }
   return it;
 }
 
-// F tiles of split s (the down items of that split wait for all of them).
-template <class P>
-__device__ __forceinline__ int split_tiles(const P& p, int s) {
+// gate_up items of split s (the down items of that split wait for all of them).
+template <int MT, class P>
+__device__ __forceinline__ int split_items(const P& p, int s) {
   const int b = min(p.F, s * p.kchunk), e = min(p.F, s * p.kchunk + p.kchunk);
-  return (e - b + 15) / 16;
+  return (e - b + 8 * MT - 1) / (8 * MT);
 }
 
-// No .L2::cache_hint: with an evict_first policy on these loads, cold-TLB runs returned
-// wrong down-projection results (scripts/ffn_stress.py, first call); plain loads are exact.
 __device__ __forceinline__ void tma_2d(void* dst, const CUtensorMap* map, uint64_t* bar, int c0, int c1) {
   asm volatile(
       "cp.async.bulk.tensor.2d.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1, {%2, %3}], [%4];" ::"r"(
@@ -185,13 +195,14 @@ __device__ __forceinline__ int ld_acquire(const int* p) {
 
 __device__ __forceinline__ void consumer_sync() { asm volatile("bar.sync 1, %0;" ::"n"(kCWarps * 32) : "memory"); }
 
-// Activation fragments of this lane for one stage: 2 K blocks x NT token groups.
-template <int NT>
-__device__ __forceinline__ void load_act(uint4 (&xv)[2][NT], const uint16_t* const (&xr)[NT], bool down, int k0,
-                                         int kend, int warp, int tig) {
+// Activation fragments of this lane for one stage: KB K blocks x NT token groups.
+// kw = the warp's first column in this stage.
+template <int NT, int KB>
+__device__ __forceinline__ void load_act(uint4 (&xv)[KB][NT], const uint16_t* const (&xr)[NT], bool down, int kw,
+                                         int kend, int, int tig) {
 #pragma unroll
-  for (int u = 0; u < 2; ++u) {
-    const int kg = k0 + (2 * warp + u) * 32 + 8 * tig;
+  for (int u = 0; u < KB; ++u) {
+    const int kg = kw + u * 32 + 8 * tig;
     const bool kin = kg < kend;
 #pragma unroll
     for (int j = 0; j < NT; ++j)
@@ -199,9 +210,11 @@ __device__ __forceinline__ void load_act(uint4 (&xv)[2][NT], const uint16_t* con
   }
 }
 
-template <int NT, int CAP>
+template <int NT, int MT, int CAP>
 __global__ void __launch_bounds__(kThreads, 1) ffn_decode_kernel(const __grid_constant__ DecodeParams<CAP> p) {
-  using G = Geo<NT>;
+  using G = Geo<NT, MT>;
+  constexpr int KB = G::kKb;
+  constexpr int kHalves = 4 / MT;  // 256-col halves per stage
   extern __shared__ __align__(1024) uint8_t smem[];
   uint64_t* full = reinterpret_cast<uint64_t*>(smem);
   uint64_t* empty = full + G::kStages;
@@ -215,7 +228,7 @@ __global__ void __launch_bounds__(kThreads, 1) ffn_decode_kernel(const __grid_co
   if (threadIdx.x == 0) {
     for (int s = 0; s < G::kStages; ++s) {
       mbar_init(&full[s], 1);
-      mbar_init(&empty[s], kCWarps);
+      mbar_init(&empty[s], G::kWarpsPerStage);
     }
     asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
   }
@@ -233,8 +246,8 @@ __global__ void __launch_bounds__(kThreads, 1) ffn_decode_kernel(const __grid_co
     // ---------------------------------------------------------------- producer lane
     // Table maps are written by host copies: order them before tensormap-proxy use
     // (also drops any cached descriptor at a reused table slot).
-    for (int i = lane; i < 2 * p.n; i += 32) {
-      const CUtensorMap* m = p.maps + 2 * p.map_idx[i >> 1] + (i & 1);
+    for (int i = lane; i < kMaps * p.n; i += 32) {
+      const CUtensorMap* m = p.maps + kMaps * p.map_idx[i / kMaps] + i % kMaps;
       asm volatile("fence.proxy.tensormap::generic.acquire.gpu [%0], 128;" ::"l"(m) : "memory");
     }
     __syncwarp();
@@ -243,23 +256,27 @@ __global__ void __launch_bounds__(kThreads, 1) ffn_decode_kernel(const __grid_co
     int ord = 0;
     for (int idx = blockIdx.x; idx < total; idx += gridDim.x, ++ord) {
       PS_TRACE(ord, 4);
-      const Item it = item_at(p, idx);
-      const CUtensorMap* map = p.maps + 2 * p.map_idx[it.i] + (it.down ? 1 : 0);
-      for (int k0 = it.kbeg; k0 < it.kend; k0 += kCols, ++n) {
+      const Item it = item_at<MT>(p, idx);
+      const CUtensorMap* maps = p.maps + kMaps * p.map_idx[it.i];
+      for (int k0 = it.kbeg; k0 < it.kend; k0 += G::kCols, ++n) {
         const int s = n % G::kStages;
         mbar_wait(&empty[s], ((n / G::kStages) & 1) ^ 1);
         uint8_t* dst = ring + s * kStageBytes;
         mbar_expect_tx(&full[s], kStageBytes);
-        // smem tile (m-tile mt, half hf) at (hf * 2 + mt) * 8 KiB.
-        if (!it.down) {
+        // smem tile (m-tile mt, half hf) at (hf * MT + mt) * 8 KiB; a box of 16*b rows
+        // fills b consecutive m-tiles.
 #pragma unroll
-          for (int hf = 0; hf < 2; ++hf) {
-            tma_2d(dst + (hf * 2 + 0) * kTileBytes, map, &full[s], k0 + hf * kHalf, it.r0);        // gate rows
-            tma_2d(dst + (hf * 2 + 1) * kTileBytes, map, &full[s], k0 + hf * kHalf, p.F + it.r0);  // up rows
+        for (int hf = 0; hf < kHalves; ++hf) {
+          uint8_t* d = dst + hf * MT * kTileBytes;
+          const int c = k0 + hf * kHalf;
+          if (!it.down) {  // m-tiles [0, MT/2): gate rows; [MT/2, MT): up rows
+            const CUtensorMap* gm = MT == 2 ? &maps[0] : &maps[1];
+            tma_2d(d, gm, &full[s], c, it.r0);
+            tma_2d(d + (MT / 2) * kTileBytes, gm, &full[s], c, p.F + it.r0);
+          } else {         // MT m-tiles of W_down rows, boxes of 32 rows
+#pragma unroll
+            for (int b = 0; b < MT / 2; ++b) tma_2d(d + 2 * b * kTileBytes, &maps[2], &full[s], c, it.r0 + 32 * b);
           }
-        } else {
-#pragma unroll
-          for (int hf = 0; hf < 2; ++hf) tma_2d(dst + hf * 2 * kTileBytes, map, &full[s], k0 + hf * kHalf, it.r0);
         }
       }
     }
@@ -267,19 +284,25 @@ __global__ void __launch_bounds__(kThreads, 1) ffn_decode_kernel(const __grid_co
   }
 
   // ------------------------------------------------------------------ consumer warps
+  // Warp w always covers K columns [512 s + 64 w, +64) of every 512-wide window s: with
+  // MT = 4 (256-col stages) warp group w/4 takes alternate stages. The per-warp partial
+  // sums, and so the results, are bitwise independent of MT (i.e. of the launch's token
+  // counts) and of the split of experts into launches.
   const int gid = lane >> 2, tig = lane & 3;
-  const int hf = warp >> 2;                      // this warp's 256-col half of every stage
-  const int kl0 = ((2 * warp) & 7) * 32 + 8 * tig;  // element offset inside the half
+  const int grp = warp / G::kWarpsPerStage;                      // stages st with st % kGroups == grp
+  const int wcol = 64 * (warp % G::kWarpsPerStage);              // this warp's columns inside its stage
+  const int hf = wcol / kHalf;                                   // its 256-col half
+  const int kl0 = wcol % kHalf + 8 * tig;                        // element offset inside the half
   uint32_t n = 0;
   int ord = 0;
   for (int idx = blockIdx.x; idx < total; idx += gridDim.x, ++ord) {
     if (threadIdx.x == 0) PS_TRACE(ord, 0);
-    const Item it = item_at(p, idx);
+    const Item it = item_at<MT>(p, idx);
     const int row0 = s_row0[it.i], m = s_m[it.i];
     const int slot = it.i * kMaxSplit + it.split;
     if (it.down) {
       if (threadIdx.x == 0) {
-        const int need = split_tiles(p, it.split);
+        const int need = split_items<MT>(p, it.split);
         while (ld_acquire(p.sync + slot) < need) __nanosleep(32);
       }
       consumer_sync();
@@ -293,34 +316,33 @@ __global__ void __launch_bounds__(kThreads, 1) ffn_decode_kernel(const __grid_co
               : it.down ? p.h + static_cast<size_t>(row0 + t) * p.F
                         : p.x + static_cast<size_t>(p.perm_src[row0 + t] / p.k) * p.H;
     }
-    float acc[2][NT][4];
+    float acc[MT][NT][4];
 #pragma unroll
-    for (int mt = 0; mt < 2; ++mt)
+    for (int mt = 0; mt < MT; ++mt)
 #pragma unroll
       for (int j = 0; j < NT; ++j)
 #pragma unroll
         for (int q = 0; q < 4; ++q) acc[mt][j][q] = 0.f;
 
-    uint4 xv[2][NT];
-    load_act<NT>(xv, xr, it.down, it.kbeg, it.kend, warp, tig);
-    for (int k0 = it.kbeg; k0 < it.kend; k0 += kCols, ++n) {
-      uint4 xn[2][NT];  // next stage's activations, in flight during this stage
-      if (NT <= 4 && k0 + kCols < it.kend) load_act<NT>(xn, xr, it.down, k0 + kCols, it.kend, warp, tig);
-      const int s = n % G::kStages;
-      mbar_wait(&full[s], (n / G::kStages) & 1);
-      const uint8_t* st = ring + s * kStageBytes + hf * 2 * kTileBytes;
+    const int nst = (it.kend - it.kbeg + G::kCols - 1) / G::kCols;
+    const int kcol0 = it.kbeg + wcol;  // this warp's first column of stage 0
+    // One ring stage st of this item: wait for the TMA fill, 2 K blocks x (MT m-tiles x NT)
+    // MMAs, release.
+    auto consume = [&](int st, const uint4 (&xv)[KB][NT]) {
+      const uint32_t q = n + st;
+      const int s = q % G::kStages;
+      mbar_wait(&full[s], (q / G::kStages) & 1);
+      const uint8_t* sp = ring + s * kStageBytes + hf * MT * kTileBytes;
 #pragma unroll
-      for (int u = 0; u < 2; ++u) {
+      for (int u = 0; u < KB; ++u) {
         const int off = (kl0 + 32 * u) * 2;
-        const uint4 a00 = lds128(st + gid * (kHalf * 2) + off);
-        const uint4 a08 = lds128(st + (gid + 8) * (kHalf * 2) + off);
-        const uint4 a10 = lds128(st + kTileBytes + gid * (kHalf * 2) + off);
-        const uint4 a18 = lds128(st + kTileBytes + (gid + 8) * (kHalf * 2) + off);
-        PS_STAGE_CHECK(it, k0, hf, kl0 + 32 * u, a00, a08, a10, a18);
 #pragma unroll
-        for (int j = 0; j < NT; ++j) {
-          mma_block(acc[0][j], a00, a08, xv[u][j]);
-          mma_block(acc[1][j], a10, a18, xv[u][j]);
+        for (int mt = 0; mt < MT; ++mt) {
+          const uint4 a0 = lds128(sp + mt * kTileBytes + gid * (kHalf * 2) + off);
+          const uint4 a8 = lds128(sp + mt * kTileBytes + (gid + 8) * (kHalf * 2) + off);
+          PS_STAGE_CHECK(it, it.kbeg + st * G::kCols, hf, kl0 + 32 * u, mt, a0, a8);
+#pragma unroll
+          for (int j = 0; j < NT; ++j) mma_block(acc[mt][j], a0, a8, xv[u][j]);
         }
       }
       // The slot is refilled by TMA (async proxy) after this arrive: order this lane's
@@ -329,38 +351,53 @@ __global__ void __launch_bounds__(kThreads, 1) ffn_decode_kernel(const __grid_co
       asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
       __syncwarp();
       if (lane == 0) mbar_arrive(&empty[s]);
-      if (k0 + kCols < it.kend) {
-        if (NT <= 4) {
-#pragma unroll
-          for (int u = 0; u < 2; ++u)
-#pragma unroll
-            for (int j = 0; j < NT; ++j) xv[u][j] = xn[u][j];
-        } else {
-          load_act<NT>(xv, xr, it.down, k0 + kCols, it.kend, warp, tig);
-        }
+    };
+    auto load = [&](uint4 (&xv)[KB][NT], int st) {
+      load_act<NT, KB>(xv, xr, it.down, kcol0 + st * G::kCols, it.kend, 0, tig);
+    };
+    constexpr int GS = G::kGroups;
+    if constexpr (NT >= 8) {  // 64 tokens: no registers for a second activation buffer
+      uint4 xa[KB][NT];
+      for (int st = grp; st < nst; st += GS) {
+        load(xa, st);
+        consume(st, xa);
+      }
+    } else {
+      // Activations for this warp's next stage are loaded during the current one (L1/L2
+      // latency overlaps the weight stream).
+      uint4 xa[KB][NT], xb[KB][NT];
+      if (grp < nst) load(xa, grp);
+      for (int st = grp; st < nst; st += 2 * GS) {
+        if (st + GS < nst) load(xb, st + GS);
+        consume(st, xa);
+        if (st + GS >= nst) break;
+        if (st + 2 * GS < nst) load(xa, st + 2 * GS);
+        consume(st + GS, xb);
       }
     }
+    n += nst;
 
     if (threadIdx.x == 0) PS_TRACE(ord, 2);
     // Cross-warp reduction through shared memory + epilogue.
 #pragma unroll
-    for (int mt = 0; mt < 2; ++mt)
+    for (int mt = 0; mt < MT; ++mt)
 #pragma unroll
       for (int j = 0; j < NT; ++j)
 #pragma unroll
-        for (int q = 0; q < 4; ++q) red[(((warp * 2 + mt) * NT + j) * 4 + q) * 32 + lane] = acc[mt][j][q];
+        for (int q = 0; q < 4; ++q) red[(((warp * MT + mt) * NT + j) * 4 + q) * 32 + lane] = acc[mt][j][q];
     consumer_sync();
-    // Value v = (half, j, q, lane): c0,c1 -> row gid, tokens 2*tig+{0,1}; c2,c3 -> row gid+8.
-    const int n_out = (it.down ? 2 : 1) * NT * 4 * 32;
-    for (int v = threadIdx.x; v < n_out; v += kCWarps * 32) {
-      const int ln = v & 31, q = (v >> 5) & 3, j = (v >> 7) % NT, half = (v >> 7) / NT;
+    // Value v = (mt, j, q, lane): c0,c1 -> row gid, tokens 2*tig+{0,1}; c2,c3 -> row gid+8.
+    // gate_up pairs gate m-tile mt with up m-tile mt + MT/2.
+    const int n_mt = it.down ? MT : MT / 2;
+    for (int v = threadIdx.x; v < n_mt * NT * 4 * 32; v += kCWarps * 32) {
+      const int ln = v & 31, q = (v >> 5) & 3, j = (v >> 7) % NT, mt = (v >> 7) / NT;
       const int t = 8 * j + 2 * (ln & 3) + (q & 1);
-      const int r = (ln >> 2) + (q >> 1) * 8;
+      const int r = 16 * mt + (ln >> 2) + (q >> 1) * 8;
       float s0 = 0.f, s1 = 0.f;
 #pragma unroll
       for (int w = 0; w < kCWarps; ++w) {
-        s0 += red[(((w * 2 + half) * NT + j) * 4 + q) * 32 + ln];
-        if (!it.down) s1 += red[(((w * 2 + 1) * NT + j) * 4 + q) * 32 + ln];
+        s0 += red[(((w * MT + mt) * NT + j) * 4 + q) * 32 + ln];
+        if (!it.down) s1 += red[(((w * MT + mt + MT / 2) * NT + j) * 4 + q) * 32 + ln];
       }
       if (t < m) {
         if (!it.down) {
@@ -370,7 +407,7 @@ __global__ void __launch_bounds__(kThreads, 1) ffn_decode_kernel(const __grid_co
             p.h[static_cast<size_t>(row0 + t) * p.F + f] = f32_to_bf16_rne(hv);
           }
         } else {
-          const int d = it.r0 + 16 * half + r;
+          const int d = it.r0 + r;
           if (d < p.H) p.y_part[it.split * p.split_stride + static_cast<size_t>(row0 + t) * p.H + d] = s0;
         }
       }
@@ -415,11 +452,10 @@ CUtensorMap encode_rows(const void* base, uint64_t rows, uint64_t cols, uint32_t
   return m;
 }
 
-// Device table of weight tensor maps, one (gate_up, down) pair per (slab, H, F), uploaded
-// once on first use (stream-ordered before the launch) and read by the kernel through a
-// global pointer. Maps passed as kernel parameters were wrong across back-to-back launches
-// with different slabs (the TMA unit served a descriptor cached for the previous launch's
-// parameter block: scripts/ffn_stress.py, 128 experts = two launches per call).
+// Device table of weight tensor maps, kMaps per (slab, H, F), uploaded once on first use
+// (stream-ordered before the launch) and read by the kernel through a global pointer:
+// keeps the launch parameter block small (64 experts x 3 maps would be 24 KiB) and
+// costs no host encode or copy in steady state (engine slabs are fixed pool slots).
 int slab_map_index(const uint16_t* slab, int H, int F, cudaStream_t s, const CUtensorMap** table) {
   struct Key {
     int dev;
@@ -437,7 +473,7 @@ int slab_map_index(const uint16_t* slab, int H, int F, cudaStream_t s, const CUt
     CUtensorMap* dev = nullptr;
     int used = 0;
   };
-  constexpr int kCap = 8192;  // slabs per device (2 maps each, 2 MiB)
+  constexpr int kCap = 8192;  // slabs per device (kMaps maps each, 3 MiB)
   static std::mutex mu;
   static std::unordered_map<Key, int, Hash> index;
   static std::unordered_map<int, Table> tables;
@@ -445,7 +481,7 @@ int slab_map_index(const uint16_t* slab, int H, int F, cudaStream_t s, const CUt
   PS_CUDA(cudaGetDevice(&dev));
   std::lock_guard<std::mutex> g(mu);
   Table& t = tables[dev];
-  if (!t.dev) PS_CUDA(cudaMalloc(&t.dev, sizeof(CUtensorMap) * 2 * kCap));
+  if (!t.dev) PS_CUDA(cudaMalloc(&t.dev, sizeof(CUtensorMap) * kMaps * kCap));
   *table = t.dev;
   auto it = index.find(Key{dev, slab, H, F});
   if (it != index.end()) return it->second;
@@ -454,11 +490,12 @@ int slab_map_index(const uint16_t* slab, int H, int F, cudaStream_t s, const CUt
     for (auto i = index.begin(); i != index.end();) i = i->first.dev == dev ? index.erase(i) : std::next(i);
     t.used = 0;
   }
-  CUtensorMap m[2];
+  CUtensorMap m[kMaps];
   m[0] = encode_rows(slab, 2ull * F, static_cast<uint64_t>(H), 16);
-  m[1] = encode_rows(slab + 2ull * F * H, static_cast<uint64_t>(H), static_cast<uint64_t>(F), 32);
+  m[1] = encode_rows(slab, 2ull * F, static_cast<uint64_t>(H), 32);
+  m[2] = encode_rows(slab + 2ull * F * H, static_cast<uint64_t>(H), static_cast<uint64_t>(F), 32);
   const int idx = t.used++;
-  PS_CUDA(cudaMemcpyAsync(t.dev + 2 * idx, m, sizeof(m), cudaMemcpyHostToDevice, s));  // pageable: staged now
+  PS_CUDA(cudaMemcpyAsync(t.dev + kMaps * idx, m, sizeof(m), cudaMemcpyHostToDevice, s));  // pageable: staged now
   index.emplace(Key{dev, slab, H, F}, idx);
   return idx;
 }
@@ -479,8 +516,6 @@ DeviceInfo& device_info() {
   return d;
 }
 
-// Counter workspace per (device, stream): launches on one stream are ordered, so they can
-// share it; the kernel leaves it zeroed.
 // Two counter sets per (device, stream), used by alternate launches: launch L counts in
 // set L&1 and zeroes set (L+1)&1, which the previous launch on this stream (ordered
 // before it) used. No reset atomics on the critical path.
@@ -509,16 +544,16 @@ SyncSets sync_workspace(cudaStream_t s) {
   return SyncSets{w.base + par * set, w.base + (par ^ 1) * set};
 }
 
-template <int NT, int CAP>
+template <int NT, int MT, int CAP>
 void launch(const DecodeParams<CAP>& p, cudaStream_t s) {
   DeviceInfo& d = device_info();
-  const size_t smem = Geo<NT>::kSmem;
-  const void* fn = reinterpret_cast<const void*>(ffn_decode_kernel<NT, CAP>);
+  const size_t smem = Geo<NT, MT>::kSmem;
+  const void* fn = reinterpret_cast<const void*>(ffn_decode_kernel<NT, MT, CAP>);
   int& bps = d.blocks_per_sm[fn];
   if (bps == 0) {
-    PS_CUDA(cudaFuncSetAttribute(ffn_decode_kernel<NT, CAP>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+    PS_CUDA(cudaFuncSetAttribute(ffn_decode_kernel<NT, MT, CAP>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                  static_cast<int>(smem)));
-    PS_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&bps, ffn_decode_kernel<NT, CAP>, kThreads, smem));
+    PS_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&bps, ffn_decode_kernel<NT, MT, CAP>, kThreads, smem));
     require(bps >= 1, "ffn_decode_kernel: does not fit on an SM");
   }
   const int total = p.gu_start[p.n] + p.dn_start[p.n];
@@ -533,12 +568,15 @@ void launch(const DecodeParams<CAP>& p, cudaStream_t s) {
   attr[0].val.cooperative = 1;
   cfg.attrs = attr;
   cfg.numAttrs = 1;
-  PS_CUDA(cudaLaunchKernelEx(&cfg, ffn_decode_kernel<NT, CAP>, p));
+  PS_CUDA(cudaLaunchKernelEx(&cfg, ffn_decode_kernel<NT, MT, CAP>, p));
 }
 
 struct Shape {
-  int H, F, k, n_split, kchunk, row_tiles_f, dn_tiles;
+  int H, F, k, n_split, kchunk;
 };
+
+// Items per entry for m-tiles-per-item MT: gate_up F/(8 MT), down n_split * H/(16 MT).
+constexpr int mt_for(int NT) { return NT == 1 || NT == 8 ? 2 : 4; }
 
 template <int CAP>
 void run_group(const ps_expert_group* group, int base, int count, const int32_t* counts_host, const Shape& sh,
@@ -552,7 +590,9 @@ void run_group(const ps_expert_group* group, int base, int count, const int32_t*
   p.k = sh.k;
   p.n_split = sh.n_split;
   p.kchunk = sh.kchunk;
-  p.dn_tiles = sh.dn_tiles;
+  const int MT = mt_for(NT);
+  const int gu_items = (sh.F + 8 * MT - 1) / (8 * MT);
+  p.dn_tiles = (sh.H + 16 * MT - 1) / (16 * MT);
   p.tok_base = tok_base;
   p.offsets = offsets;
   p.perm_src = perm_src;
@@ -565,8 +605,8 @@ void run_group(const ps_expert_group* group, int base, int count, const int32_t*
     if (counts_host[e] <= tok_base) continue;
     p.map_idx[p.n] = slab_map_index(group->slabs[i], sh.H, sh.F, s, &p.maps);
     p.expert[p.n] = e;
-    p.gu_start[p.n + 1] = p.gu_start[p.n] + sh.row_tiles_f;
-    p.dn_start[p.n + 1] = p.dn_start[p.n] + sh.dn_tiles * sh.n_split;
+    p.gu_start[p.n + 1] = p.gu_start[p.n] + gu_items;
+    p.dn_start[p.n + 1] = p.dn_start[p.n] + p.dn_tiles * sh.n_split;
     ++p.n;
   }
   if (p.n == 0) return;
@@ -574,10 +614,10 @@ void run_group(const ps_expert_group* group, int base, int count, const int32_t*
   p.sync = ss.cur;
   p.sync_next = ss.next;
   switch (NT) {
-    case 1: launch<1, CAP>(p, s); break;
-    case 2: launch<2, CAP>(p, s); break;
-    case 4: launch<4, CAP>(p, s); break;
-    default: launch<8, CAP>(p, s); break;
+    case 1: launch<1, mt_for(1), CAP>(p, s); break;
+    case 2: launch<2, mt_for(2), CAP>(p, s); break;
+    case 4: launch<4, mt_for(4), CAP>(p, s); break;
+    default: launch<8, mt_for(8), CAP>(p, s); break;
   }
 }
 
@@ -589,9 +629,9 @@ using namespace ps;
 extern "C" {
 
 int ps_ffn_down_splits(int H, int F) {
-  // Down items are (split of F) x (32 rows of H); splitting F into ~F/H parts keeps a
-  // down item about the size of a gate_up item (32 rows x H), which balances the
-  // persistent CTAs (Mixtral F=14336, H=4096: 4 splits of 3584 = 7 stages).
+  // Down items are (split of F) x (16*MT rows of H), gate_up items (16*MT weight rows) x
+  // H; splitting F into ~F/H parts keeps both item kinds about the same size, which
+  // balances the persistent CTAs (Mixtral F=14336, H=4096: 4 splits of 3584).
   const int s = (F + H / 2) / std::max(H, 1);
   return std::min(std::max(s, 1), kMaxSplit);
 }
@@ -612,9 +652,9 @@ ps_status ps_expert_ffn(const ps_expert_group* group, const int32_t* counts_host
     }
     if (max_m == 0) return;
     require(total_rows >= max_m, "ps_expert_ffn: total_rows smaller than an expert's rows");
-    Shape sh{H, F, k, n_split, 0, (F + 15) / 16, (H + 31) / 32};
+    Shape sh{H, F, k, n_split, 0};
     sh.kchunk = (F + n_split - 1) / n_split;
-    sh.kchunk = (sh.kchunk + 31) / 32 * 32;  // F tiles (16) never straddle a split
+    sh.kchunk = (sh.kchunk + 31) / 32 * 32;  // gate_up items (8*MT <= 32 F rows) never straddle a split
     const size_t split_stride = static_cast<size_t>(total_rows) * H;
 
     // Token passes of <= 64 rows per expert (decode has m_e <= 64: one pass).

@@ -12,30 +12,33 @@ __device__ int g_first[8];
 #define PS_FFN_TRACE 1
 #define PS_TRACE(ord, k)
 #ifdef NOCHECK
-#define PS_STAGE_CHECK(it, k0, hf, kl, a00, a08, a10, a18)
+#define PS_STAGE_CHECK(it, k0, hf, kl, mt, a0, a8)
 #else
-#define PS_STAGE_CHECK(it, k0, hf, kl, a00, a08, a10, a18)                                              \
+#define PS_STAGE_CHECK(it, k0, hf, kl, mt, a0, a8)                                                      \
   do {                                                                                                    \
-    const uint16_t* sl = g_slab[p.expert[it.i]];                                                                    \
+    const uint16_t* sl = g_slab[p.expert[it.i]];                                                          \
     const int col = k0 + hf * 256 + kl;                                                                   \
     if (col < it.kend) {                                                                                  \
-      const uint16_t* r[4];                                                                               \
-      if (!it.down) {                                                                                     \
-        r[0] = sl + (size_t)(it.r0 + gid) * p.H; r[1] = sl + (size_t)(it.r0 + gid + 8) * p.H;             \
-        r[2] = sl + (size_t)(p.F + it.r0 + gid) * p.H; r[3] = sl + (size_t)(p.F + it.r0 + gid + 8) * p.H; \
-      } else {                                                                                            \
-        const uint16_t* wd = sl + 2ull * p.F * p.H;                                                       \
-        for (int q_ = 0; q_ < 4; ++q_) r[q_] = wd + (size_t)(it.r0 + gid + 8 * q_) * p.F;                 \
-      }                                                                                                   \
-      const uint4 got[4] = {a00, a08, a10, a18};                                                          \
-      for (int q_ = 0; q_ < 4; ++q_) {                                                                    \
-        const bool rowok = !it.down ? (it.r0 + gid + 8 * (q_ & 1) < p.F) : (it.r0 + gid + 8 * q_ < p.H);  \
-        if (!rowok) continue;                                                                             \
-        const uint4 want = *reinterpret_cast<const uint4*>(r[q_] + col);                                 \
-        if (want.x != got[q_].x || want.y != got[q_].y || want.z != got[q_].z || want.w != got[q_].w) {   \
+      for (int h_ = 0; h_ < 2; ++h_) {                                                                    \
+        const int rr = 16 * mt + gid + 8 * h_; /* row inside the item */                                 \
+        const uint16_t* row;                                                                              \
+        bool ok;                                                                                          \
+        if (!it.down) {                                                                                   \
+          const int half = 8 * MT; /* gate rows [0, half), up rows [half, 2 half) */                     \
+          const int f = it.r0 + (rr % half);                                                              \
+          ok = f < p.F;                                                                                   \
+          row = sl + (size_t)((rr < half ? 0 : p.F) + f) * p.H;                                           \
+        } else {                                                                                          \
+          ok = it.r0 + rr < p.H;                                                                          \
+          row = sl + 2ull * p.F * p.H + (size_t)(it.r0 + rr) * p.F;                                       \
+        }                                                                                                 \
+        if (!ok) continue;                                                                                \
+        const uint4 want = *reinterpret_cast<const uint4*>(row + col);                                    \
+        const uint4 got = h_ ? a8 : a0;                                                                   \
+        if (want.x != got.x || want.y != got.y || want.z != got.z || want.w != got.w) {                   \
           if (atomicAdd(&g_bad, 1u) == 0) {                                                               \
             g_first[0] = blockIdx.x; g_first[1] = it.i; g_first[2] = it.down; g_first[3] = it.r0;         \
-            g_first[4] = col; g_first[5] = q_; g_first[6] = (int)n; g_first[7] = warp;                     \
+            g_first[4] = col; g_first[5] = rr; g_first[6] = (int)n; g_first[7] = warp;                    \
           }                                                                                               \
         }                                                                                                 \
       }                                                                                                   \
