@@ -39,24 +39,11 @@ route_kernel(const float* __restrict__ x, const float* __restrict__ gate, const 
   const int nt = min(TB, B - b0);
   const bool vec = (H & 3) == 0;
 
-  // Fused cast x -> bf16 (input of K3), vectorised, all threads.
-  for (int t = 0; t < nt; ++t) {
-    const float* xr = x + static_cast<size_t>(b0 + t) * H;
-    uint16_t* xo = x_bf16 ? x_bf16 + static_cast<size_t>(b0 + t) * H : nullptr;
-    if (xo && vec) {
-      for (int h = threadIdx.x * 4; h < H; h += kWarps * 128) {
-        float4 v = *reinterpret_cast<const float4*>(xr + h);
-        uint2 o;
-        o.x = (uint32_t)f32_to_bf16_rne(v.x) | ((uint32_t)f32_to_bf16_rne(v.y) << 16);
-        o.y = (uint32_t)f32_to_bf16_rne(v.z) | ((uint32_t)f32_to_bf16_rne(v.w) << 16);
-        *reinterpret_cast<uint2*>(xo + h) = o;
-      }
-    } else if (xo) {
-      for (int h = threadIdx.x; h < H; h += kWarps * 32) xo[h] = f32_to_bf16_rne(xr[h]);
-    }
-  }
-
   // Gate GEMV partials: warp w owns H slice [w*hs, (w+1)*hs), kETile experts at a time.
+  // Vector path: kU float4 steps per lane in flight together (latency-bound at decode),
+  // and the x values loaded for the first expert tile are also written out as bf16
+  // (fused cast for K3).
+  constexpr int kU = 2;
   const int hs = vec ? ((H / 4 + kWarps - 1) / kWarps) * 4 : (H + kWarps - 1) / kWarps;
   const int h_lo = min(H, warp * hs), h_hi = min(H, h_lo + hs);
   for (int e0 = 0; e0 < E; e0 += kETile) {
@@ -66,23 +53,47 @@ route_kernel(const float* __restrict__ x, const float* __restrict__ gate, const 
 #pragma unroll
       for (int j = 0; j < kETile; ++j) acc[t][j] = 0.f;
     if (vec) {
-      for (int h = h_lo + lane * 4; h < h_hi; h += 128) {
-        float4 xv[TB];
+      for (int hb = h_lo + lane * 4; hb < h_hi; hb += 128 * kU) {
+        float4 xv[kU][TB], g[kU][kETile];
 #pragma unroll
-        for (int t = 0; t < TB; ++t)
-          xv[t] = t < nt ? *reinterpret_cast<const float4*>(x + static_cast<size_t>(b0 + t) * H + h)
-                         : make_float4(0.f, 0.f, 0.f, 0.f);
+        for (int u = 0; u < kU; ++u) {
+          const int h = hb + 128 * u;
+          const bool hin = h < h_hi;
 #pragma unroll
-        for (int j = 0; j < kETile; ++j) {
-          if (e0 + j < E) {
-            const float4 g = __ldg(reinterpret_cast<const float4*>(gate + static_cast<size_t>(e0 + j) * H + h));
+          for (int t = 0; t < TB; ++t)
+            xv[u][t] = hin && t < nt ? *reinterpret_cast<const float4*>(x + static_cast<size_t>(b0 + t) * H + h)
+                                     : make_float4(0.f, 0.f, 0.f, 0.f);
+#pragma unroll
+          for (int j = 0; j < kETile; ++j)
+            g[u][j] = hin && e0 + j < E ? __ldg(reinterpret_cast<const float4*>(gate + static_cast<size_t>(e0 + j) * H + h))
+                                        : make_float4(0.f, 0.f, 0.f, 0.f);
+        }
+#pragma unroll
+        for (int u = 0; u < kU; ++u) {
+#pragma unroll
+          for (int j = 0; j < kETile; ++j)
 #pragma unroll
             for (int t = 0; t < TB; ++t)
-              acc[t][j] += g.x * xv[t].x + g.y * xv[t].y + g.z * xv[t].z + g.w * xv[t].w;
+              acc[t][j] += g[u][j].x * xv[u][t].x + g[u][j].y * xv[u][t].y + g[u][j].z * xv[u][t].z +
+                           g[u][j].w * xv[u][t].w;
+          const int h = hb + 128 * u;
+          if (x_bf16 && e0 == 0 && h < h_hi) {
+#pragma unroll
+            for (int t = 0; t < TB; ++t)
+              if (t < nt) {
+                uint2 o;
+                o.x = (uint32_t)f32_to_bf16_rne(xv[u][t].x) | ((uint32_t)f32_to_bf16_rne(xv[u][t].y) << 16);
+                o.y = (uint32_t)f32_to_bf16_rne(xv[u][t].z) | ((uint32_t)f32_to_bf16_rne(xv[u][t].w) << 16);
+                *reinterpret_cast<uint2*>(x_bf16 + static_cast<size_t>(b0 + t) * H + h) = o;
+              }
           }
         }
       }
     } else {
+      if (x_bf16 && e0 == 0)
+        for (int t = 0; t < nt; ++t)
+          for (int h = h_lo + lane; h < h_hi; h += 32)
+            x_bf16[static_cast<size_t>(b0 + t) * H + h] = f32_to_bf16_rne(x[static_cast<size_t>(b0 + t) * H + h]);
       for (int h = h_lo + lane; h < h_hi; h += 32) {
 #pragma unroll
         for (int j = 0; j < kETile; ++j) {

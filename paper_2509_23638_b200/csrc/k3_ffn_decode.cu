@@ -57,7 +57,8 @@ namespace {
 constexpr int kMaxSplit = 8;
 constexpr int kSyncEntries = 64;                 // max entries per launch (sync workspace rows)
 constexpr int kCWarps = 8;                       // consumer warps
-constexpr int kThreads = (kCWarps + 1) * 32;     // + one producer warp
+constexpr int kThreads = (kCWarps + 2) * 32;     // + TMA producer warp + release signaler warp
+constexpr int kMailbox = 8;                      // consumer -> signaler queue of finished gate_up items
 constexpr int kBarBytes = 1024;                  // mbarriers + per-entry row table; keeps the ring 1 KiB aligned
 constexpr int kMaxTokens = 64;                   // tokens per expert per launch (8 * NT, NT <= 8)
 constexpr int kHalf = 256;                       // TMA box width (cols)
@@ -65,7 +66,8 @@ constexpr int kTileBytes = 16 * kHalf * 2;       // one (16-row m-tile, 256-col 
 constexpr int kStageBytes = 4 * kTileBytes;      // 32 KiB: MT m-tiles x (4 / MT) halves
 constexpr int kMaps = 3;                         // per slab: gate_up {256,16}, gate_up {256,32}, down {256,32}
 
-static_assert(128 + 2 * kSyncEntries * 4 <= kBarBytes, "smem header");
+// smem header: full[8] | empty[8] | posted[kMailbox] | freed[kMailbox] | row0[64] | m[64] | mailbox slots
+static_assert(256 + 2 * kSyncEntries * 4 + kMailbox * 4 <= kBarBytes, "smem header");
 
 // NT = 8-token groups per expert, MT = 16-row m-tiles per stage (and per item). A stage
 // is always 32 KiB: MT = 2 -> 32 rows x 512 cols, MT = 4 -> 64 rows x 256 cols. Activation
@@ -217,9 +219,12 @@ __global__ void __launch_bounds__(kThreads, 1) ffn_decode_kernel(const __grid_co
   constexpr int kHalves = 4 / MT;  // 256-col halves per stage
   extern __shared__ __align__(1024) uint8_t smem[];
   uint64_t* full = reinterpret_cast<uint64_t*>(smem);
-  uint64_t* empty = full + G::kStages;
-  int* s_row0 = reinterpret_cast<int*>(smem + 128);           // per-entry first row of this pass
+  uint64_t* empty = full + 8;
+  uint64_t* posted = full + 16;                               // gate_up item done (consumer -> signaler)
+  uint64_t* freed = full + 16 + kMailbox;                     // mailbox entry free (signaler -> consumer)
+  int* s_row0 = reinterpret_cast<int*>(smem + 256);           // per-entry first row of this pass
   int* s_m = s_row0 + kSyncEntries;                           // per-entry rows of this pass (<= 8*NT)
+  int* s_mb = s_m + kSyncEntries;                             // mailbox: counter slot of the finished item
   uint8_t* ring = smem + kBarBytes;
   float* red = reinterpret_cast<float*>(ring + G::kStages * kStageBytes);  // [warp][mt][j][q][lane]
 
@@ -229,6 +234,10 @@ __global__ void __launch_bounds__(kThreads, 1) ffn_decode_kernel(const __grid_co
     for (int s = 0; s < G::kStages; ++s) {
       mbar_init(&full[s], 1);
       mbar_init(&empty[s], G::kWarpsPerStage);
+    }
+    for (int b = 0; b < kMailbox; ++b) {
+      mbar_init(&posted[b], 1);
+      mbar_init(&freed[b], 1);
     }
     asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
   }
@@ -241,6 +250,27 @@ __global__ void __launch_bounds__(kThreads, 1) ffn_decode_kernel(const __grid_co
   if (blockIdx.x == 0)  // counters of the next launch (other parity); this stream's previous launch is done
     for (int i = threadIdx.x; i < kSyncEntries * kMaxSplit; i += blockDim.x) p.sync_next[i] = 0;
   __syncthreads();
+
+  if (warp == kCWarps + 1) {
+    // ---------------------------------------------------------------- signaler lane
+    // Publishes finished gate_up items to the down items of their split: acquire the
+    // consumers' mailbox post (which follows their h stores and a CTA barrier), then a
+    // gpu-scope fence + counter increment. The fence stalls only this lane, not the
+    // consumer warps that feed the ring.
+    if (lane != 0) return;
+    const int gu_total = p.gu_start[p.n];
+    const int mine = gu_total > static_cast<int>(blockIdx.x)
+                         ? (gu_total - static_cast<int>(blockIdx.x) + gridDim.x - 1) / gridDim.x : 0;
+    for (int q = 0; q < mine; ++q) {
+      const int b = q % kMailbox;
+      mbar_wait(&posted[b], (q / kMailbox) & 1);
+      const int slot = s_mb[b];
+      __threadfence();
+      atomicAdd(p.sync + slot, 1);
+      mbar_arrive(&freed[b]);
+    }
+    return;
+  }
 
   if (warp == kCWarps) {
     // ---------------------------------------------------------------- producer lane
@@ -294,7 +324,7 @@ __global__ void __launch_bounds__(kThreads, 1) ffn_decode_kernel(const __grid_co
   const int hf = wcol / kHalf;                                   // its 256-col half
   const int kl0 = wcol % kHalf + 8 * tig;                        // element offset inside the half
   uint32_t n = 0;
-  int ord = 0;
+  int ord = 0, gu_done = 0;
   for (int idx = blockIdx.x; idx < total; idx += gridDim.x, ++ord) {
     if (threadIdx.x == 0) PS_TRACE(ord, 0);
     const Item it = item_at<MT>(p, idx);
@@ -414,8 +444,15 @@ __global__ void __launch_bounds__(kThreads, 1) ffn_decode_kernel(const __grid_co
     }
     consumer_sync();  // red reusable; every h store of this item issued
     if (threadIdx.x == 0) PS_TRACE(ord, 3);
-    if (!it.down && threadIdx.x == 0)  // release this F tile to the down items of its split
-      asm volatile("red.release.gpu.global.add.s32 [%0], 1;" ::"l"(p.sync + slot) : "memory");
+    if (!it.down) {  // hand this F tile to the signaler (mbarrier arrive = release.cta)
+      if (threadIdx.x == 0) {
+        const int b = gu_done % kMailbox;
+        mbar_wait(&freed[b], ((gu_done / kMailbox) & 1) ^ 1);
+        s_mb[b] = slot;
+        mbar_arrive(&posted[b]);
+      }
+      ++gu_done;
+    }
   }
 }
 

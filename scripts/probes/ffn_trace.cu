@@ -15,6 +15,7 @@ __device__ __forceinline__ unsigned long long gtime() {
   return t;
 }
 #define PS_FFN_TRACE 1
+#define PS_STAGE_CHECK(it, k0, hf, kl, mt, a0, a8)
 #define PS_TRACE(ord, k) \
   do { if ((ord) < 96 && blockIdx.x < 148) g_trace[blockIdx.x][(ord)][(k)] = gtime(); } while (0)
 #include "k3_ffn_decode.cu"
