@@ -604,7 +604,7 @@ void launch(const DecodeParams<CAP>& p, cudaStream_t s) {
   attr[0].id = cudaLaunchAttributeCooperative;  // co-residency: the h dependency spins
   attr[0].val.cooperative = 1;
   cfg.attrs = attr;
-  cfg.numAttrs = 1;
+  cfg.numAttrs = 1;  // measured cost of the attribute: ~1.5 us per launch
   PS_CUDA(cudaLaunchKernelEx(&cfg, ffn_decode_kernel<NT, MT, CAP>, p));
 }
 
