@@ -80,6 +80,29 @@ ps_status ps_trace_inputs(const ps_trace_gen_config* cfg, const ps_model_spec* s
                           uint64_t seed, double* gate, double* hidden, uint8_t* follow,
                           double* zipf_per_layer);
 
+/* ------------------------------------------------------------------- trace files
+ * write_trace / read_trace (workload.cpp:290-436), format v1: one JSON header line
+ * {"batch_size","checksum" (FNV-1a 64 of the body),"format_version":1,"seed","spec"},
+ * then one TSV line per (token, layer) step in (token, layer) order:
+ *   layer \t hidden[H] \t gate_weights[E] \t active[k] \t e:m e:m ...  (doubles %.17g).
+ * Errors: PS_ERUNTIME "TraceFormatError: ..." / "TraceChecksumError: ..."
+ * (workload.hpp:106-111) or I/O failure; PS_EINVAL for an invalid spec. */
+typedef struct ps_trace_s* ps_trace;
+uint64_t ps_fnv1a64(const void* data, size_t n);                 /* workload.cpp:290-297 */
+ps_status ps_trace_read(const char* path, ps_trace* out);        /* read_trace, workload.cpp:409-436 */
+ps_status ps_trace_shape(ps_trace t, ps_model_spec* spec, int32_t* batch, uint64_t* seed,
+                         uint64_t* checksum);
+/* Dense copies, index (token*L + layer): hidden [B*L*H] f64, gate_weights [B*L*E] f64,
+ * active [B*L*k] i32 (weight-desc), tokens [B*L*E] i32 (tokens_per_expert, 0 = absent).
+ * Each output nullable. */
+ps_status ps_trace_arrays(ps_trace t, double* hidden, double* gate_weights, int32_t* active,
+                          int32_t* tokens);
+ps_status ps_trace_free(ps_trace t);
+/* write_trace (workload.cpp:391-407): byte-identical to the reference for the same trace. */
+ps_status ps_trace_write(const char* path, const ps_model_spec* spec, int batch, uint64_t seed,
+                         const double* hidden, const double* gate_weights, const int32_t* active,
+                         const int32_t* tokens);
+
 /* --------------------------------------------------------------------- cost model
  * prescope::CostParams / ExpertLoad / HitStats (cost_model.hpp:13-62). Ticks = us. */
 typedef struct {
@@ -271,6 +294,14 @@ ps_status ps_gather_rows(const uint16_t* x, const int32_t* idx, int n, int div, 
 ps_status ps_combine(const float* y_part, int n_split, const int32_t* inv, const int32_t* ids,
                      const float* weights, int B, int k, int E, int H, float* y, void* stream);
 
+/* Shared experts (BASELINE config 3, DeepSeek-V2-Lite: 2 always-active experts with gate
+ * weight 1; a north_star extension — the reference's ModelSpec has none): appends
+ * virtual experts E..E+S-1 to every token so K2/K3/combine run them with the routed ones.
+ *   ids [B,k] -> ids_ext [B,k+S]; weights [B,E] -> weights_ext [B,E+S] (1.0 for shared);
+ *   counts [E+S] (nullable): entries E..E+S-1 set to B (K1 wrote 0..E-1). */
+ps_status ps_append_shared(const int32_t* ids, const float* weights, int B, int k, int E, int S,
+                           int32_t* ids_ext, float* weights_ext, int32_t* counts, void* stream);
+
 /* K3 — grouped SwiGLU expert FFN over a set of experts whose slabs are on device.
  * Slab layout [Wg (F*H) | Wu (F*H) | Wd (H*F)] bf16 row-major = expert_bytes.
  * Rows of expert experts[i] are permuted rows [offsets[e], offsets[e+1]) (K2), token
@@ -384,6 +415,8 @@ typedef struct {
   ps_ep_comm ep;            /* nullable: expert-parallel over this communicator; the
                                engine then owns experts e % world == rank only, and
                                `resident`/`budget_bytes` are this rank's */
+  int32_t n_shared;         /* always-active shared experts per layer (DeepSeek: 2),
+                               HBM-resident outside the routed-expert budget; 0 = none */
 } ps_engine_config;
 
 ps_status ps_engine_create(const ps_engine_config* cfg, ps_engine* out);

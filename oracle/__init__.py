@@ -446,16 +446,23 @@ def or_init_slab(H, F, seed, layer, expert):
     return out
 
 
-def or_engine_reference(spec, F, weight_seed, hidden, ids, weights, threads=16):
+def or_engine_reference(spec, F, weight_seed, hidden, ids, weights, threads=16, n_shared=0):
     """Per-layer MoE outputs the decode engine must produce: hidden [B,L,H] f64 (trace
     order), ids [L,B,k] (routing to evaluate), weights [L,B,E] (full-softmax gate
-    weights). x is the bf16 rounding of hidden (the FFN input). Returns y [L,B,H]."""
+    weights). x is the bf16 rounding of hidden (the FFN input). Returns y [L,B,H].
+    n_shared > 0: DeepSeek-style shared experts (hash-keyed as experts E..E+S-1, gate
+    weight 1, every token) are added to each token's output."""
     B, L, H = hidden.shape
     E = spec.experts_per_layer
+    S = n_shared
     y = np.empty((L, B, H), np.float32)
     for l in range(L):
-        used = sorted(set(int(e) for e in np.unique(ids[l])))
-        slabs = [or_init_slab(H, F, weight_seed, l, e) if e in used else None for e in range(E)]
+        used = set(int(e) for e in np.unique(ids[l])) | set(range(E, E + S))
+        slabs = [or_init_slab(H, F, weight_seed, l, e) if e in used else None for e in range(E + S)]
         x = f32_to_bf16(hidden[:, l, :].astype(np.float32))
-        y[l] = or_moe_layer(slabs, H, F, x, ids[l], weights[l].astype(np.float32), True, threads)
+        ids_l, w_l = ids[l], weights[l].astype(np.float32)
+        if S:
+            ids_l = np.concatenate([ids_l, np.broadcast_to(np.arange(E, E + S, dtype=np.int32), (B, S))], 1)
+            w_l = np.concatenate([w_l, np.ones((B, S), np.float32)], 1)
+        y[l] = or_moe_layer(slabs, H, F, x, ids_l, w_l, True, threads)
     return y

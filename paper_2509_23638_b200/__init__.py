@@ -17,7 +17,7 @@ from .capi import check, load
 
 __all__ = ["capi", "load", "check", "spec_preset", "desk_scale", "ffn_dim", "trace_inputs", "plan_layer",
            "parse_policy", "simulate", "verify_timeline", "plan_residency", "Plan", "TraceGenConfig",
-           "GROUP_DEFAULT_GEN"]
+           "GROUP_DEFAULT_GEN", "Trace", "read_trace", "write_trace"]
 
 # Default generator knobs of the benchmark workloads:
 # input/output {rho .9, kappa .5, zipf .5}; middle {rho .95, kappa .6, zipf 1.0}; noise 1.
@@ -67,6 +67,49 @@ def trace_inputs(cfg, spec: capi.ModelSpec, batch: int, seed: int, want_gate=Tru
     check(load().ps_trace_inputs(C.byref(cfg), C.byref(spec), batch, seed, ptr(gate), ptr(hidden), ptr(follow),
                                  ptr(zipf)))
     return gate, hidden, follow, zipf
+
+
+@dataclass
+class Trace:
+    """prescope::Trace (workload.hpp:47-66) as dense arrays, index [token, layer]:
+    hidden [B,L,H] f64, gate_weights [B,L,E] f64, active [B,L,k] i32 (weight-desc),
+    tokens [B,L,E] i32 (tokens_per_expert; 0 = absent)."""
+    spec: capi.ModelSpec
+    batch_size: int
+    seed: int
+    hidden: np.ndarray
+    gate_weights: np.ndarray
+    active: np.ndarray
+    tokens: np.ndarray
+    checksum: int = 0
+
+
+def read_trace(path) -> Trace:
+    """read_trace (workload.cpp:409-436): raises RuntimeError on TraceFormatError /
+    TraceChecksumError / I/O failure, ValueError on an invalid spec."""
+    lib = load()
+    h = C.c_void_p()
+    check(lib.ps_trace_read(str(path).encode(), C.byref(h)))
+    try:
+        spec, b, seed, cs = capi.ModelSpec(), C.c_int32(), C.c_uint64(), C.c_uint64()
+        check(lib.ps_trace_shape(h, C.byref(spec), C.byref(b), C.byref(seed), C.byref(cs)))
+        B, L, E, H, k = b.value, spec.num_layers, spec.experts_per_layer, spec.hidden_dim, spec.top_k
+        hid = np.empty((B, L, H), np.float64)
+        gw = np.empty((B, L, E), np.float64)
+        act = np.empty((B, L, k), np.int32)
+        tok = np.empty((B, L, E), np.int32)
+        check(lib.ps_trace_arrays(h, *(a.ctypes.data_as(C.c_void_p) for a in (hid, gw, act, tok))))
+    finally:
+        lib.ps_trace_free(h)
+    return Trace(spec, B, seed.value, hid, gw, act, tok, cs.value)
+
+
+def write_trace(trace: Trace, path) -> None:
+    """write_trace (workload.cpp:391-407), byte-identical to the reference's writer."""
+    arrs = [np.ascontiguousarray(trace.hidden, np.float64), np.ascontiguousarray(trace.gate_weights, np.float64),
+            np.ascontiguousarray(trace.active, np.int32), np.ascontiguousarray(trace.tokens, np.int32)]
+    check(load().ps_trace_write(str(path).encode(), C.byref(trace.spec), trace.batch_size, trace.seed,
+                                *(a.ctypes.data_as(C.c_void_p) for a in arrs)))
 
 
 def parse_policy(text: str) -> capi.Policy:

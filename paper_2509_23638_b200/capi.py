@@ -113,7 +113,7 @@ class EngineConfig(C.Structure):
                 ("budget_bytes", C.c_uint64), ("resident", C.POINTER(C.c_int32)), ("n_resident", C.c_int32),
                 ("max_batch", C.c_int32), ("prefetch_slots", C.c_int32), ("policy", Policy),
                 ("cost", CostParams), ("predictor", C.c_void_p), ("device", C.c_int32),
-                ("host_pinned", C.c_int32), ("ep", C.c_void_p)]
+                ("host_pinned", C.c_int32), ("ep", C.c_void_p), ("n_shared", C.c_int32)]
 
 
 class EngineStats(C.Structure):
@@ -167,6 +167,14 @@ _SIGS = {
                                 _P, _P, _P, _P, _P, _P]),
     "ps_permute": (C.c_int, [_P, C.c_int, C.c_int, C.c_int, _P, _P, _P, _P, C.c_int, _P, _P]),
     "ps_combine": (C.c_int, [_P, C.c_int, _P, _P, _P, C.c_int, C.c_int, C.c_int, C.c_int, _P, _P]),
+    "ps_fnv1a64": (C.c_uint64, [_P, C.c_size_t]),
+    "ps_trace_read": (C.c_int, [C.c_char_p, C.POINTER(C.c_void_p)]),
+    "ps_trace_shape": (C.c_int, [_P, C.POINTER(ModelSpec), C.POINTER(C.c_int32), C.POINTER(C.c_uint64),
+                                 C.POINTER(C.c_uint64)]),
+    "ps_trace_arrays": (C.c_int, [_P, _P, _P, _P, _P]),
+    "ps_trace_free": (C.c_int, [_P]),
+    "ps_trace_write": (C.c_int, [C.c_char_p, C.POINTER(ModelSpec), C.c_int, C.c_uint64, _P, _P, _P, _P]),
+    "ps_append_shared": (C.c_int, [_P, _P, C.c_int, C.c_int, C.c_int, C.c_int, _P, _P, _P, _P]),
     "ps_expert_ffn": (C.c_int, [C.POINTER(ExpertGroup), _P, _P, _P, C.c_int, _P, C.c_int, C.c_int, _P, _P,
                                 C.c_int, C.c_int, _P]),
     "ps_ffn_down_splits": (C.c_int, [C.c_int, C.c_int]),

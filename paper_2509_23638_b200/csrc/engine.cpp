@@ -220,6 +220,13 @@ struct PhaseTiming {  // scheduling-point phase (K1+K4+K2+D2H) and combine, per 
 struct ps_engine_s {
   ps_engine_config cfg{};
   int L = 0, E = 0, K = 0, H = 0, F = 0, maxB = 0, n_split = 1, step_split = 1;
+  // Shared experts (cfg.n_shared): virtual experts E..E+S-1 of every token; Et/Kt are the
+  // expert count / assignments per token that K2, K3 and the combine see.
+  int S = 0, Et = 0, Kt = 0;
+  void* shared_arena = nullptr;               // [L*S] slabs, HBM, outside the routed budget
+  std::vector<const uint16_t*> shared_slab;   // [L*S]
+  int32_t* ids_ext = nullptr;                 // [maxB, Kt]
+  float* w_ext = nullptr;                     // [maxB, Et]
   uint64_t slab_elems = 0;
   cudaStream_t sc = nullptr;  // compute stream
   std::unique_ptr<ps::IoChannel> io;
@@ -239,9 +246,9 @@ struct ps_engine_s {
 
   // step buffers
   std::vector<ps::LayerDev> layer;
-  int32_t* counts_dev = nullptr;     // [E]
+  int32_t* counts_dev = nullptr;     // [Et]
   int32_t* pred_dev = nullptr;       // [E]
-  int32_t* pinned_counts = nullptr;  // [2E] host pinned: counts | pred
+  int32_t* pinned_counts = nullptr;  // [3Et+1] host pinned: counts | pred | offsets
   uint16_t* x_bf16 = nullptr;
   uint16_t* x_perm = nullptr;        // [maxB*k, H] bf16 (prefill gather)
   bool prefill_mode = false;         // B > kDecodeMaxBatch: tcgen05 path, exact-count launches
@@ -543,7 +550,8 @@ void decode_step(ps_engine_s& e, const float* hidden, const uint8_t* follow, int
   const auto host_t0 = Clock::now();
 
   std::vector<ps_expert_load> cur, nxt, cpu_b(E), od_b(E), pf_b(E);
-  std::vector<int32_t> counts_l(E), pred_l(E);
+  const int Et = e.Et, Kt = e.Kt;
+  std::vector<int32_t> counts_l(Et), pred_l(E);
   e.step_truth.assign(static_cast<size_t>(L) * E, 0);
 
   for (int l = 0; l < L; ++l) {
@@ -576,17 +584,22 @@ void decode_step(ps_engine_s& e, const float* hidden, const uint8_t* follow, int
     // tcgen05 path) and need the offsets on the host for tile scheduling.
     const int Ev = e.G * e.E_loc;  // owner-major virtual expert count under EP
     if (!e.ep) {
-      s = ps_permute(ld.ids, B, K, E, e.offsets, e.perm_src, e.inv, e.prefill_mode ? e.x_bf16 : nullptr, H,
-                     e.prefill_mode ? e.x_perm : nullptr, e.sc);
+      if (e.S) {
+        s = ps_append_shared(ld.ids, ld.weights, B, K, E, e.S, e.ids_ext, e.w_ext, e.counts_dev, e.sc);
+        if (s != PS_OK) fail(s, ps_last_error());
+        e.st.kernel_launches += 1;
+      }
+      s = ps_permute(e.S ? e.ids_ext : ld.ids, B, Kt, Et, e.offsets, e.perm_src, e.inv,
+                     e.prefill_mode ? e.x_bf16 : nullptr, H, e.prefill_mode ? e.x_perm : nullptr, e.sc);
       if (s != PS_OK) fail(s, ps_last_error());
       e.st.kernel_launches += e.prefill_mode ? 2 : 1;
-      PS_CUDA(cudaMemcpyAsync(e.pinned_counts, e.counts_dev, sizeof(int32_t) * E, cudaMemcpyDeviceToHost, e.sc));
+      PS_CUDA(cudaMemcpyAsync(e.pinned_counts, e.counts_dev, sizeof(int32_t) * Et, cudaMemcpyDeviceToHost, e.sc));
       if (predict)
-        PS_CUDA(cudaMemcpyAsync(e.pinned_counts + E, e.pred_dev, sizeof(int32_t) * E, cudaMemcpyDeviceToHost, e.sc));
+        PS_CUDA(cudaMemcpyAsync(e.pinned_counts + Et, e.pred_dev, sizeof(int32_t) * E, cudaMemcpyDeviceToHost, e.sc));
       if (e.prefill_mode)
-        PS_CUDA(cudaMemcpyAsync(e.pinned_counts + 2 * E, e.offsets, sizeof(int32_t) * (E + 1),
+        PS_CUDA(cudaMemcpyAsync(e.pinned_counts + 2 * Et, e.offsets, sizeof(int32_t) * (Et + 1),
                                 cudaMemcpyDeviceToHost, e.sc));
-      e.src = {e.offsets, e.perm_src, K, e.x_bf16, B * K, e.pinned_counts + 2 * E};
+      e.src = {e.offsets, e.perm_src, Kt, e.x_bf16, B * Kt, e.pinned_counts + 2 * Et};
     } else {
       // EP dispatch, part 1: owner-major permute + gather of this rank's routed rows,
       // then the (rows, predicted tokens) counts exchange with every owner.
@@ -611,13 +624,18 @@ void decode_step(ps_engine_s& e, const float* hidden, const uint8_t* follow, int
     // for the worst case m_e = B and warps of unrouted experts exit immediately.
     // Prefill: launched after the host sync with exact counts (tile scheduling).
     ps_expert_group grp{};
-    std::vector<int32_t> worst(E, B);
+    std::vector<int32_t> worst(Et, B);
     for (int ex = 0; ex < E; ++ex)
       if (e.resident[static_cast<size_t>(l) * E + ex]) {
         grp.experts[grp.n] = ex;
         grp.slabs[grp.n] = e.dev_slab[static_cast<size_t>(l) * E + ex];
         ++grp.n;
       }
+    for (int j = 0; j < e.S; ++j) {  // shared experts run with the resident group
+      grp.experts[grp.n] = E + j;
+      grp.slabs[grp.n] = e.shared_slab[static_cast<size_t>(l) * e.S + j];
+      ++grp.n;
+    }
     const size_t resident_timing = e.ffn_t.size();
     const bool early = !e.prefill_mode && !e.ep;
     if (early) ffn(e, grp, worst.data(), B, true, false);
@@ -642,8 +660,8 @@ void decode_step(ps_engine_s& e, const float* hidden, const uint8_t* follow, int
     // Wait for the routing result on the host (the only per-layer host sync).
     PS_CUDA(cudaEventSynchronize(e.ev_routed));
     if (!e.ep) {
-      std::memcpy(counts_l.data(), e.pinned_counts, sizeof(int32_t) * E);
-      if (predict) std::memcpy(pred_l.data(), e.pinned_counts + E, sizeof(int32_t) * E);
+      std::memcpy(counts_l.data(), e.pinned_counts, sizeof(int32_t) * Et);
+      if (predict) std::memcpy(pred_l.data(), e.pinned_counts + Et, sizeof(int32_t) * E);
       else std::fill(pred_l.begin(), pred_l.end(), dense_next ? (B * K) / E : 0);
     } else {
       ep_dispatch_rows(e, B, counts_l, pred_l);
@@ -667,8 +685,8 @@ void decode_step(ps_engine_s& e, const float* hidden, const uint8_t* follow, int
       }
       e.st.ffn_flops_total += 6.0 * rows * e.H * e.F;
     }
-    std::copy(counts_l.begin(), counts_l.end(), e.step_truth.begin() + static_cast<size_t>(l) * E);
-    for (int i = 0; i < grp.n; ++i) e.st.resident_hits += counts_l[grp.experts[i]] > 0;
+    std::copy(counts_l.begin(), counts_l.begin() + E, e.step_truth.begin() + static_cast<size_t>(l) * E);
+    for (int i = 0; i < grp.n; ++i) e.st.resident_hits += grp.experts[i] < E && counts_l[grp.experts[i]] > 0;
 
     // Deferred HitStats for critical prefetches that targeted this layer (R2).
     for (auto it = e.hit_checks.begin(); it != e.hit_checks.end();) {
@@ -762,8 +780,8 @@ void decode_step(ps_engine_s& e, const float* hidden, const uint8_t* follow, int
     // --- combine -> y_l ------------------------------------------------------------
     PS_CUDA(cudaEventRecord(ph.comb0, e.sc));
     if (!e.ep) {
-      s = ps_combine(e.y_part, e.step_split, e.inv, ld.ids, ld.weights, B, K, E, H, y + static_cast<size_t>(l) * B * H,
-                     e.sc);
+      s = ps_combine(e.y_part, e.step_split, e.inv, e.S ? e.ids_ext : ld.ids, e.S ? e.w_ext : ld.weights, B, Kt, Et, H,
+                     y + static_cast<size_t>(l) * B * H, e.sc);
     } else {
       s = ep_combine_rows(e, B, ld, y + static_cast<size_t>(l) * B * H);
     }
@@ -842,8 +860,9 @@ void decode_step(ps_engine_s& e, const float* hidden, const uint8_t* follow, int
       e.ffn_experts += static_cast<double>(t.experts.size());
     }
     const int64_t a = at_us(t.a), b = at_us(t.b);
-    for (size_t i = 0; i < t.experts.size(); ++i)
-      e.last_events.push_back({a, b, PS_RES_GPU, PS_EV_GPU_EXPERT, t.layer, t.experts[i], t.tokens[i]});
+    for (size_t i = 0; i < t.experts.size(); ++i)  // shared experts are not part of the routed timeline
+      if (t.experts[i] < E)
+        e.last_events.push_back({a, b, PS_RES_GPU, PS_EV_GPU_EXPERT, t.layer, t.experts[i], t.tokens[i]});
   }
   for (size_t l = 0; l < e.phase_t.size(); ++l) {
     auto& p = e.phase_t[l];
@@ -894,7 +913,12 @@ void create_engine(const ps_engine_config& cfg, ps_engine_s& e) {
   e.K = sp.top_k;
   e.H = sp.hidden_dim;
   e.maxB = cfg.max_batch;
-  require(e.maxB >= 1 && e.E <= 256 && e.H % 8 == 0 && e.F % 8 == 0, "engine: unsupported shape");
+  e.S = cfg.n_shared;
+  e.Et = e.E + e.S;
+  e.Kt = e.K + e.S;
+  require(e.maxB >= 1 && e.Et <= 256 && e.H % 8 == 0 && e.F % 8 == 0, "engine: unsupported shape");
+  require(e.S >= 0 && e.S <= 32, "engine: n_shared out of range [0, 32]");
+  require(e.S == 0 || !cfg.ep, "engine: shared experts are not supported with expert parallelism");
   if (e.cfg.prefetch_slots <= 0) e.cfg.prefetch_slots = 8;
   e.n_split = ps_ffn_down_splits(e.H, e.F);
   e.slab_elems = sp.expert_bytes / 2;
@@ -962,6 +986,20 @@ void create_engine(const ps_engine_config& cfg, ps_engine_s& e) {
         e.host_slab[idx] = hp;
       }
     }
+  // Shared experts: dense weights of every layer, always in HBM (not part of the routed
+  // budget PreScope manages); hash-keyed as experts E..E+S-1.
+  e.shared_slab.assign(static_cast<size_t>(e.L) * e.S, nullptr);
+  if (e.S) {
+    PS_CUDA(cudaMalloc(&e.shared_arena, static_cast<size_t>(e.L) * e.S * sp.expert_bytes));
+    for (int l = 0; l < e.L; ++l)
+      for (int j = 0; j < e.S; ++j) {
+        const size_t idx = static_cast<size_t>(l) * e.S + j;
+        uint16_t* p = reinterpret_cast<uint16_t*>(static_cast<char*>(e.shared_arena) + idx * sp.expert_bytes);
+        if (ps_init_expert_slab(p, e.H, e.F, cfg.weight_seed, l, e.E + j, e.sc) != PS_OK)
+          fail(PS_ECUDA, ps_last_error());
+        e.shared_slab[idx] = p;
+      }
+  }
   PS_CUDA(cudaStreamSynchronize(e.sc));
   if (stage) cudaFree(stage);
 
@@ -983,22 +1021,26 @@ void create_engine(const ps_engine_config& cfg, ps_engine_s& e) {
   PS_CUDA(cudaMalloc(&e.bias, sizeof(float) * bias.size()));
   PS_CUDA(cudaMemcpy(e.bias, bias.data(), sizeof(float) * bias.size(), cudaMemcpyHostToDevice));
 
-  const size_t B = e.maxB, rows = B * e.K;
-  e.rows_max = static_cast<int>(e.G * rows);  // FFN rows: everything routed here by all ranks
+  const size_t B = e.maxB, rows = B * e.K, rows_t = B * e.Kt;
+  e.rows_max = static_cast<int>(e.G * rows_t);  // FFN rows: everything routed here by all ranks
   const size_t frows = static_cast<size_t>(e.rows_max);
   e.layer.resize(e.L);
   for (auto& ld : e.layer) {
     PS_CUDA(cudaMalloc(&ld.weights, sizeof(float) * B * e.E));
     PS_CUDA(cudaMalloc(&ld.ids, sizeof(int32_t) * rows));
   }
-  PS_CUDA(cudaMalloc(&e.counts_dev, sizeof(int32_t) * e.E));
+  PS_CUDA(cudaMalloc(&e.counts_dev, sizeof(int32_t) * e.Et));
   PS_CUDA(cudaMalloc(&e.pred_dev, sizeof(int32_t) * e.E));
-  PS_CUDA(cudaHostAlloc(&e.pinned_counts, sizeof(int32_t) * (3 * e.E + 1), cudaHostAllocDefault));
+  PS_CUDA(cudaHostAlloc(&e.pinned_counts, sizeof(int32_t) * (3 * e.Et + 1), cudaHostAllocDefault));
+  if (e.S) {
+    PS_CUDA(cudaMalloc(&e.ids_ext, sizeof(int32_t) * rows_t));
+    PS_CUDA(cudaMalloc(&e.w_ext, sizeof(float) * B * e.Et));
+  }
   PS_CUDA(cudaMalloc(&e.x_bf16, sizeof(uint16_t) * B * e.H));
   PS_CUDA(cudaMalloc(&e.x_perm, sizeof(uint16_t) * frows * e.H));
-  PS_CUDA(cudaMalloc(&e.offsets, sizeof(int32_t) * (e.E + 1)));
-  PS_CUDA(cudaMalloc(&e.perm_src, sizeof(int32_t) * rows));
-  PS_CUDA(cudaMalloc(&e.inv, sizeof(int32_t) * rows));
+  PS_CUDA(cudaMalloc(&e.offsets, sizeof(int32_t) * (e.Et + 1)));
+  PS_CUDA(cudaMalloc(&e.perm_src, sizeof(int32_t) * rows_t));
+  PS_CUDA(cudaMalloc(&e.inv, sizeof(int32_t) * rows_t));
   PS_CUDA(cudaMalloc(&e.hbuf, sizeof(uint16_t) * frows * e.F));
   PS_CUDA(cudaMalloc(&e.y_part, sizeof(float) * e.n_split * frows * e.H));
   if (e.ep) {
@@ -1047,7 +1089,7 @@ void destroy_engine(ps_engine_s& e) {
                   (void*)e.out_ids, (void*)e.ep_vids, (void*)e.ep_off_v, (void*)e.ep_perm_v, (void*)e.ep_inv_v,
                   (void*)e.ep_send_x, (void*)e.ep_recv_x, (void*)e.ep_y_recv, (void*)e.ep_y_back,
                   (void*)e.ep_cnt_send, (void*)e.ep_cnt_recv, (void*)e.ep_plan_dev, (void*)e.ep_ones,
-                  (void*)e.ep_zeros})
+                  (void*)e.ep_zeros, e.shared_arena, (void*)e.ids_ext, (void*)e.w_ext})
     if (p) cudaFree(p);
   if (e.ep_plan_host) cudaFreeHost(e.ep_plan_host);
   if (e.ep_host) cudaFreeHost(e.ep_host);

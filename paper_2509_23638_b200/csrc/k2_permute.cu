@@ -132,6 +132,20 @@ __global__ void ep_pack_counts_kernel(const int32_t* __restrict__ offsets_v, con
   out[d * 2 * e_loc + e_loc + j] = (pred && e < E) ? pred[e] : 0;
 }
 
+// Shared experts (DeepSeek-style, always active, gate weight 1): appended as virtual
+// experts E..E+S-1 so permute / FFN / combine treat them like routed ones.
+__global__ void append_shared_kernel(const int32_t* __restrict__ ids, const float* __restrict__ w, int B, int k,
+                                     int E, int S, int32_t* __restrict__ ids_ext, float* __restrict__ w_ext,
+                                     int32_t* __restrict__ counts) {
+  const int kt = k + S, et = E + S;
+  for (int i = blockIdx.x * blockDim.x + threadIdx.x; i < B * et; i += gridDim.x * blockDim.x) {
+    const int t = i / et, c = i % et;
+    w_ext[i] = c < E ? w[static_cast<size_t>(t) * E + c] : 1.0f;
+    if (c < kt) ids_ext[static_cast<size_t>(t) * kt + c] = c < k ? ids[static_cast<size_t>(t) * k + c] : E + (c - k);
+  }
+  if (counts && blockIdx.x == 0 && threadIdx.x < S) counts[E + threadIdx.x] = B;
+}
+
 }  // namespace
 }  // namespace ps
 
@@ -146,6 +160,18 @@ ps_status ps_ep_pack_counts(const int32_t* offsets_v, const int32_t* pred, int E
     const int e_loc = (E + G - 1) / G;
     ep_pack_counts_kernel<<<(G * e_loc + 127) / 128, 128, 0, as_stream(stream)>>>(offsets_v, pred, E, G, e_loc, out);
     PS_LAUNCH_CHECK("ep_pack_counts_kernel");
+  });
+}
+
+ps_status ps_append_shared(const int32_t* ids, const float* weights, int B, int k, int E, int S,
+                           int32_t* ids_ext, float* weights_ext, int32_t* counts, void* stream) {
+  return guarded([&] {
+    require(B >= 0 && k >= 1 && E >= 1 && S >= 1 && S <= 32 && ids && weights && ids_ext && weights_ext,
+            "ps_append_shared: bad arguments");
+    const int n = B * (E + S);
+    append_shared_kernel<<<std::max(1, std::min((n + 255) / 256, 148)), 256, 0, as_stream(stream)>>>(
+        ids, weights, B, k, E, S, ids_ext, weights_ext, counts);
+    PS_LAUNCH_CHECK("append_shared_kernel");
   });
 }
 

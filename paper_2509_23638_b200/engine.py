@@ -98,7 +98,8 @@ class Engine:
     def __init__(self, spec: capi.ModelSpec, gen_cfg, *, max_batch: int, weight_seed: int = 0,
                  gate: np.ndarray, budget_fraction: float | None = None, budget_bytes: int | None = None,
                  resident=None, trace_hidden=None, trace_follow=None, policy: str = "presched",
-                 predictor=None, cost=None, prefetch_slots: int = 8, device: int = 0, ep=None):
+                 predictor=None, cost=None, prefetch_slots: int = 8, device: int = 0, ep=None,
+                 n_shared: int = 0):
         from . import parse_policy, plan_residency, trace_inputs  # noqa: F401
         self.lib = load()
         self.spec = spec
@@ -132,6 +133,7 @@ class Engine:
         cfg.device = device
         cfg.host_pinned = 1
         cfg.ep = ep.h if isinstance(ep, EpComm) else ep
+        cfg.n_shared = n_shared
         h = C.c_void_p()
         check(self.lib.ps_engine_create(C.byref(cfg), C.byref(h)))
         self.h = h

@@ -19,6 +19,9 @@ Outputs (all small, committed):
   llapor_desk.llpc        LLaPor trained by the reference on config[0]-shaped traces
                           (make_llapor + train + save_checkpoint).
   llapor_desk_expected.npz reference pca/logits/top-k for 64 (token, layer) features.
+  ref_trace_desk.tsv      a trace file written by the reference's write_trace
+                          (workload.cpp:391-407): desk_scale(mixtral,4,8,16), B=3, seed 17,
+                          knobs (rho .9, kappa .3, zipf .5) — read/re-write parity.
 """
 from __future__ import annotations
 
@@ -172,6 +175,13 @@ def llapor():
                         topk=np.array(tops), predicted_loads=loads, hidden=hidden, gate_weights=gw, active=act)
 
 
+def ref_trace_file():
+    spec = desk_spec("mixtral", 4, 8, 16)
+    gen = orc.ref_gen((0.9, 0.3, 0.5), (0.9, 0.3, 0.5), (0.9, 0.3, 0.5))
+    orc.ref_check(orc.ref_lib().ref_write_trace(C.byref(gen), C.byref(spec), 3, 17,
+                                                str(OUT / "ref_trace_desk.tsv").encode()))
+
+
 def main():
     orc.ref_check(orc.ref_lib().ref_dump_golden(str(OUT / "golden_scenarios.json").encode()))
     (OUT / "trace_fingerprints.json").write_text(json.dumps(fingerprints(), indent=1))
@@ -179,6 +189,7 @@ def main():
     (OUT / "presched_cases.json").write_text(json.dumps(presched_cases()))
     (OUT / "sim_cases.json").write_text(json.dumps(sim_cases()))
     llapor()
+    ref_trace_file()
     print("golden fixtures written to", OUT)
 
 

@@ -20,19 +20,20 @@ def _small_spec(L=4, E=8, H=256, F=512, preset="mixtral"):
     return spec
 
 
-def _run(spec, B, budget, policy="presched", seed=3, steps=2, predictor=None):
+def _run(spec, B, budget, policy="presched", seed=3, steps=2, predictor=None, n_shared=0):
     cfg = ps.TraceGenConfig(*[ps.GROUP_DEFAULT_GEN[g] for g in ("input", "middle", "output")])
     gate, hidden, follow, zipf = ps.trace_inputs(cfg, spec, B, seed)
     F = ps.ffn_dim(spec)
     with eng.Engine(spec, cfg, budget_fraction=budget, max_batch=B, weight_seed=9, gate=gate,
-                    trace_hidden=hidden, trace_follow=follow, policy=policy, predictor=predictor) as e:
+                    trace_hidden=hidden, trace_follow=follow, policy=policy, predictor=predictor,
+                    n_shared=n_shared) as e:
         for _ in range(steps):
             y, ids = e.step_host(hidden, follow)
         st = e.stats()
         resident = set(e.resident)
     _, ref_w, ref_ids = orc.or_route_trace(gate, hidden, follow, zipf, spec.top_k)
     agree = (np.sort(ids, -1) == np.sort(ref_ids.transpose(1, 0, 2), -1)).all(-1).mean()
-    y_ref = orc.or_engine_reference(spec, F, 9, hidden, ids, ref_w.transpose(1, 0, 2))
+    y_ref = orc.or_engine_reference(spec, F, 9, hidden, ids, ref_w.transpose(1, 0, 2), n_shared=n_shared)
     return y, y_ref, ids, st, resident, agree
 
 
@@ -112,3 +113,20 @@ def test_engine_batch_one(torch_cuda):
     spec = _small_spec()
     y, y_ref, *_ = _run(spec, 1, 0.5)
     assert np.linalg.norm(y - y_ref) / np.linalg.norm(y_ref) < BF16_RTOL
+
+
+@pytest.mark.parametrize("B,budget", [(8, 0.5), (16, 0.0), (512, 0.5)])
+def test_engine_shared_experts_deepseek_shape(torch_cuda, B, budget):
+    """BASELINE config 3 (DeepSeek-V2-Lite: 64 routed top-6 + 2 shared experts): the
+    shared experts run with the resident group on every token (gate weight 1), both on
+    the decode GEMV path and, for a 512-token chunk, on the tcgen05 prefill path."""
+    spec = _small_spec(L=3, E=64, H=256, F=256, preset="deepseek")
+    y, y_ref, ids, st, resident, agree = _run(spec, B, budget, n_shared=2, steps=1)
+    assert agree >= 0.98
+    assert np.linalg.norm(y - y_ref) / np.linalg.norm(y_ref) < BF16_RTOL
+    if B >= 128:
+        assert st["tc_launches"] > 0
+    # shared experts are outside the routed budget: never loaded over PCIe
+    needed = sum(1 for l in range(spec.num_layers) for e in set(ids[l].ravel().tolist()) if (l, e) not in resident)
+    assert st["ondemand_loads"] + st["prefetches_committed"] >= needed
+    assert st["ondemand_loads"] <= needed
