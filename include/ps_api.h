@@ -339,6 +339,20 @@ ps_status ps_init_expert_slab(uint16_t* slab, int H, int F, uint64_t seed, int l
 ps_status ps_init_expert_slab_host(uint16_t* slab, int H, int F, uint64_t seed, int layer,
                                    int expert);
 
+/* Host expert lane (Resource::Cpu of the reference, simulator.cpp:139-146; cpu_cost
+ * cost_model.cpp:34-37): SwiGLU expert FFN on the host cores (AVX512-BF16 GEMV, a thread
+ * pool, fp32 accumulation, h rounded to bf16 like K3) reading the expert's slab where it
+ * lies in (pinned) host DRAM. Opt-in lane of the engine (ps_engine_config.host_threads);
+ * PS_ERUNTIME if the CPU lacks AVX512_BF16. A lane is single-owner.
+ *   slab [Wg|Wu|Wd] bf16 (host), x [m,H] bf16 (host), y [m,H] f32 (host). H,F % 32 == 0. */
+typedef struct ps_host_lane_s* ps_host_lane;
+ps_status ps_host_lane_create(int threads, ps_host_lane* out);
+ps_status ps_host_lane_destroy(ps_host_lane lane);
+int ps_host_lane_threads(ps_host_lane lane);
+int ps_host_lane_isa(ps_host_lane lane); /* 2 = AMX-BF16 tiles, 1 = AVX512-BF16 GEMV */
+ps_status ps_host_expert_ffn(ps_host_lane lane, const uint16_t* slab, int H, int F, const uint16_t* x,
+                             int m, float* y);
+
 /* K4 — LLaPor predictor (predictor.cpp:116-124, 166-247, 344-352, 669-672). */
 typedef struct ps_llapor_s* ps_llapor;
 /* load_checkpoint (predictor.cpp:866-929): LLPC v1 file -> device-resident nets. */
@@ -417,6 +431,10 @@ typedef struct {
                                `resident`/`budget_bytes` are this rank's */
   int32_t n_shared;         /* always-active shared experts per layer (DeepSeek: 2),
                                HBM-resident outside the routed-expert budget; 0 = none */
+  int32_t host_threads;     /* > 0: host expert lane (ps_host_expert_ffn) with this many
+                               threads runs PreSched's cpu_set from pinned host DRAM,
+                               concurrently with the PCIe loads; beta/startup are then
+                               measured at create (unless cost.t_io > 0). 0 = GPU only. */
 } ps_engine_config;
 
 ps_status ps_engine_create(const ps_engine_config* cfg, ps_engine* out);
@@ -447,6 +465,9 @@ typedef struct {
   int64_t tc_launches;         /* K3 launches that took the tcgen05 (prefill) path */
   int64_t ffn_launches, kernel_launches;
   ps_cost_params cost;      /* calibrated costs in use */
+  int64_t cpu_experts;      /* experts run on the host lane */
+  double cpu_ms_total;      /* host-lane busy time (wall clock) */
+  double cpu_bytes_total;   /* expert bytes the host lane streamed */
 } ps_engine_stats;
 ps_status ps_engine_get_stats(ps_engine e, ps_engine_stats* out);
 ps_status ps_engine_reset_stats(ps_engine e);

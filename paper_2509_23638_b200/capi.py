@@ -113,7 +113,8 @@ class EngineConfig(C.Structure):
                 ("budget_bytes", C.c_uint64), ("resident", C.POINTER(C.c_int32)), ("n_resident", C.c_int32),
                 ("max_batch", C.c_int32), ("prefetch_slots", C.c_int32), ("policy", Policy),
                 ("cost", CostParams), ("predictor", C.c_void_p), ("device", C.c_int32),
-                ("host_pinned", C.c_int32), ("ep", C.c_void_p), ("n_shared", C.c_int32)]
+                ("host_pinned", C.c_int32), ("ep", C.c_void_p), ("n_shared", C.c_int32),
+                ("host_threads", C.c_int32)]
 
 
 class EngineStats(C.Structure):
@@ -125,7 +126,8 @@ class EngineStats(C.Structure):
                 ("route_phase_ms_total", C.c_double), ("combine_ms_total", C.c_double),
                 ("ffn_flops_total", C.c_double), ("tc_launches", C.c_int64), ("ffn_launches", C.c_int64),
                 ("kernel_launches", C.c_int64),
-                ("cost", CostParams)]
+                ("cost", CostParams), ("cpu_experts", C.c_int64), ("cpu_ms_total", C.c_double),
+                ("cpu_bytes_total", C.c_double)]
 
 
 PLAN_FN = C.CFUNCTYPE(C.c_int, C.c_void_p, C.POINTER(LayerInputs), C.c_int, C.POINTER(LayerPlan))
@@ -174,6 +176,11 @@ _SIGS = {
     "ps_trace_arrays": (C.c_int, [_P, _P, _P, _P, _P]),
     "ps_trace_free": (C.c_int, [_P]),
     "ps_trace_write": (C.c_int, [C.c_char_p, C.POINTER(ModelSpec), C.c_int, C.c_uint64, _P, _P, _P, _P]),
+    "ps_host_lane_create": (C.c_int, [C.c_int, C.POINTER(C.c_void_p)]),
+    "ps_host_lane_destroy": (C.c_int, [_P]),
+    "ps_host_lane_threads": (C.c_int, [_P]),
+    "ps_host_lane_isa": (C.c_int, [_P]),
+    "ps_host_expert_ffn": (C.c_int, [_P, _P, C.c_int, C.c_int, _P, C.c_int, _P]),
     "ps_append_shared": (C.c_int, [_P, _P, C.c_int, C.c_int, C.c_int, C.c_int, _P, _P, _P, _P]),
     "ps_expert_ffn": (C.c_int, [C.POINTER(ExpertGroup), _P, _P, _P, C.c_int, _P, C.c_int, C.c_int, _P, _P,
                                 C.c_int, C.c_int, _P]),

@@ -199,6 +199,81 @@ struct LayerDev {  // per-layer device outputs kept for the step
   int32_t* ids;    // [B,k]
 };
 
+// Host expert lane (Resource::Cpu, simulator.cpp:139-146; R5): one driver thread runs a
+// layer's cpu_set sequentially on the lane's pool (the driver is pool worker 0) while
+// the engine thread keeps issuing the layer's PCIe loads and GPU FFNs. The engine
+// submits after the scheduling point and waits before the layer's combine.
+struct CpuJob {
+  int layer, expert, m, row0;
+  const uint16_t* slab;
+  double t0_us = 0, t1_us = 0;  // host clock, filled by the driver
+};
+
+class LaneDriver {
+ public:
+  LaneDriver(ps_host_lane lane, int H, int F) : lane_(lane), H_(H), F_(F), thread_([this] { loop(); }) {}
+  ~LaneDriver() {
+    {
+      std::lock_guard<std::mutex> g(mu_);
+      stop_ = true;
+    }
+    cv_.notify_all();
+    thread_.join();
+  }
+  // xrows / yrows: [rows, H] bf16 / f32, job j reads/writes rows [row0, row0 + m).
+  void submit(std::vector<CpuJob>* jobs, const uint16_t* xrows, float* yrows) {
+    std::lock_guard<std::mutex> g(mu_);
+    jobs_ = jobs;
+    x_ = xrows;
+    y_ = yrows;
+    done_ = false;
+    cv_.notify_all();
+  }
+  void wait() {
+    std::unique_lock<std::mutex> g(mu_);
+    cv_.wait(g, [&] { return done_; });
+    if (!err_.empty()) {
+      std::string m = err_;
+      err_.clear();
+      fail(PS_ERUNTIME, "host lane: " + m);
+    }
+  }
+
+ private:
+  void loop() {
+    std::unique_lock<std::mutex> g(mu_);
+    while (true) {
+      cv_.wait(g, [&] { return stop_ || jobs_ != nullptr; });
+      if (stop_) return;
+      std::vector<CpuJob>* jobs = jobs_;
+      g.unlock();
+      std::string err;
+      for (CpuJob& j : *jobs) {
+        j.t0_us = now_us();
+        if (ps_host_expert_ffn(lane_, j.slab, H_, F_, x_ + static_cast<size_t>(j.row0) * H_, j.m,
+                               y_ + static_cast<size_t>(j.row0) * H_) != PS_OK && err.empty())
+          err = ps_last_error();
+        j.t1_us = now_us();
+      }
+      g.lock();
+      jobs_ = nullptr;
+      err_ = err;
+      done_ = true;
+      cv_.notify_all();
+    }
+  }
+  ps_host_lane lane_;
+  int H_, F_;
+  std::mutex mu_;
+  std::condition_variable cv_;
+  std::vector<CpuJob>* jobs_ = nullptr;
+  const uint16_t* x_ = nullptr;
+  float* y_ = nullptr;
+  bool stop_ = false, done_ = true;
+  std::string err_;
+  std::thread thread_;  // last: starts after the members it uses
+};
+
 struct FfnTiming {
   cudaEvent_t a, b;
   double bytes;
@@ -227,6 +302,19 @@ struct ps_engine_s {
   std::vector<const uint16_t*> shared_slab;   // [L*S]
   int32_t* ids_ext = nullptr;                 // [maxB, Kt]
   float* w_ext = nullptr;                     // [maxB, Et]
+
+  // host expert lane (cfg.host_threads > 0)
+  ps_host_lane lane = nullptr;
+  std::unique_ptr<ps::LaneDriver> lane_drv;
+  uint16_t* lane_x = nullptr;    // pinned: [maxB, H] bf16 x (D2H at the scheduling point)
+  int32_t* lane_idx = nullptr;   // pinned: perm_src [maxB*Kt] | offsets [Et+1]
+  uint16_t* lane_xrows = nullptr;  // pinned: [maxB*Kt, H] bf16 gathered rows of CPU experts
+  float* lane_yrows = nullptr;     // pinned: [maxB*Kt, H] f32 their outputs
+  std::vector<ps::CpuJob> cpu_jobs;      // current layer
+  std::vector<ps::CpuJob> cpu_done;      // this step (timeline)
+  double cpu_ms_cal = 0, cpu_tokens_cal = 0;  // calibration samples
+  std::vector<int32_t> cal_m;
+  std::vector<int64_t> cal_us;
   uint64_t slab_elems = 0;
   cudaStream_t sc = nullptr;  // compute stream
   std::unique_ptr<ps::IoChannel> io;
@@ -548,6 +636,8 @@ void decode_step(ps_engine_s& e, const float* hidden, const uint8_t* follow, int
   e.pending_pf.clear();
   PS_CUDA(cudaEventRecord(e.ev_step0, e.sc));
   const auto host_t0 = Clock::now();
+  const double host_t0_us = now_us();
+  e.cpu_done.clear();
 
   std::vector<ps_expert_load> cur, nxt, cpu_b(E), od_b(E), pf_b(E);
   const int Et = e.Et, Kt = e.Kt;
@@ -600,6 +690,12 @@ void decode_step(ps_engine_s& e, const float* hidden, const uint8_t* follow, int
         PS_CUDA(cudaMemcpyAsync(e.pinned_counts + 2 * Et, e.offsets, sizeof(int32_t) * (Et + 1),
                                 cudaMemcpyDeviceToHost, e.sc));
       e.src = {e.offsets, e.perm_src, Kt, e.x_bf16, B * Kt, e.pinned_counts + 2 * Et};
+      if (e.lane) {  // the host lane needs x and the permutation for its rows
+        PS_CUDA(cudaMemcpyAsync(e.lane_x, e.x_bf16, sizeof(uint16_t) * B * H, cudaMemcpyDeviceToHost, e.sc));
+        PS_CUDA(cudaMemcpyAsync(e.lane_idx, e.perm_src, sizeof(int32_t) * B * Kt, cudaMemcpyDeviceToHost, e.sc));
+        PS_CUDA(cudaMemcpyAsync(e.lane_idx + static_cast<size_t>(e.maxB) * Kt, e.offsets, sizeof(int32_t) * (Et + 1),
+                                cudaMemcpyDeviceToHost, e.sc));
+      }
     } else {
       // EP dispatch, part 1: owner-major permute + gather of this rank's routed rows,
       // then the (rows, predicted tokens) counts exchange with every owner.
@@ -747,7 +843,26 @@ void decode_step(ps_engine_s& e, const float* hidden, const uint8_t* follow, int
 
     // --- R7: on-demand loads through the dual buffer, FFN per landed expert --------
     std::vector<ps_expert_load> loads(plan.ondemand_seq, plan.ondemand_seq + plan.n_ondemand);
-    loads.insert(loads.end(), plan.cpu_set, plan.cpu_set + plan.n_cpu);  // no CPU lane
+    // R5: cpu_set on the host lane (concurrent with the loads below); without a lane the
+    // GPU-only executor loads them after ondemand_seq.
+    e.cpu_jobs.clear();
+    if (e.lane && plan.n_cpu > 0) {
+      const int32_t* perm = e.lane_idx;
+      const int32_t* off = e.lane_idx + static_cast<size_t>(e.maxB) * Kt;
+      for (int i = 0; i < plan.n_cpu; ++i) {
+        const int ex = plan.cpu_set[i].expert;
+        const uint16_t* slab = e.host_slab[static_cast<size_t>(l) * E + ex];
+        require(slab != nullptr, "host lane: cpu_set expert has no host copy");
+        CpuJob j{l, ex, off[ex + 1] - off[ex], off[ex], slab};
+        for (int r = j.row0; r < j.row0 + j.m; ++r)
+          std::memcpy(e.lane_xrows + static_cast<size_t>(r) * H, e.lane_x + static_cast<size_t>(perm[r] / Kt) * H,
+                      sizeof(uint16_t) * H);
+        e.cpu_jobs.push_back(j);
+      }
+      e.lane_drv->submit(&e.cpu_jobs, e.lane_xrows, e.lane_yrows);
+    } else {
+      loads.insert(loads.end(), plan.cpu_set, plan.cpu_set + plan.n_cpu);
+    }
     std::vector<IoJob*> od_jobs;
     for (size_t j = 0; j < loads.size(); ++j) {
       Slot* slot = &e.od_slot[j % 2];
@@ -775,6 +890,28 @@ void decode_step(ps_engine_s& e, const float* hidden, const uint8_t* follow, int
       release_slot_after_compute(e, job->slot);
       e.st.ondemand_loads++;
       e.st.h2d_bytes += static_cast<double>(job->bytes);
+    }
+
+    // Host-lane results (R5) -> y_part rows (split 0; other splits zero), then combine.
+    if (!e.cpu_jobs.empty()) {
+      e.lane_drv->wait();
+      const size_t total_rows = static_cast<size_t>(e.src.rows);
+      for (CpuJob& j : e.cpu_jobs) {
+        const size_t bytes = sizeof(float) * static_cast<size_t>(j.m) * H;
+        PS_CUDA(cudaMemcpyAsync(e.y_part + static_cast<size_t>(j.row0) * H, e.lane_yrows + static_cast<size_t>(j.row0) * H,
+                                bytes, cudaMemcpyHostToDevice, e.sc));
+        for (int sp = 1; sp < e.step_split; ++sp)
+          PS_CUDA(cudaMemsetAsync(e.y_part + (sp * total_rows + j.row0) * H, 0, bytes, e.sc));
+        e.st.cpu_experts += 1;
+        e.st.cpu_ms_total += (j.t1_us - j.t0_us) / 1e3;
+        e.st.cpu_bytes_total += static_cast<double>(e.cfg.spec.expert_bytes);
+        e.cal_m.push_back(j.m);
+        e.cal_us.push_back(ps_to_ticks(j.t1_us - j.t0_us));
+        j.t0_us -= host_t0_us;
+        j.t1_us -= host_t0_us;
+        e.cpu_done.push_back(j);
+      }
+      e.cpu_jobs.clear();
     }
 
     // --- combine -> y_l ------------------------------------------------------------
@@ -876,6 +1013,9 @@ void decode_step(ps_engine_s& e, const float* hidden, const uint8_t* follow, int
     e.last_events.push_back({e.last_layer_start[l], at_us(p.route1), PS_RES_GPU, PS_EV_ATTENTION,
                              static_cast<int32_t>(l), -1, 0});
   }
+  for (const CpuJob& j : e.cpu_done)  // host clock from the step start (~ev_step0)
+    e.last_events.push_back({static_cast<int64_t>(std::llround(j.t0_us)), static_cast<int64_t>(std::llround(j.t1_us)),
+                             PS_RES_CPU, PS_EV_CPU_EXPERT, j.layer, j.expert, j.m});
   for (auto& p : e.stall_t) {
     PS_CUDA(cudaEventElapsedTime(&ms, p.before, p.after));
     e.st.compute_wait_ms += ms;
@@ -923,7 +1063,8 @@ void create_engine(const ps_engine_config& cfg, ps_engine_s& e) {
   e.n_split = ps_ffn_down_splits(e.H, e.F);
   e.slab_elems = sp.expert_bytes / 2;
   for (auto& h : e.stats) h = {1.0, 0.0, 32};
-  if (e.cfg.cost.t_io <= 0) {  // provisional costs: PCIe Gen5 ~55 GB/s, HBM ~6.5 TB/s
+  const bool auto_cost = e.cfg.cost.t_io <= 0;
+  if (auto_cost) {  // provisional costs: PCIe Gen5 ~55 GB/s, HBM ~6.5 TB/s
     e.cfg.cost.t_io = std::max<int64_t>(2, static_cast<int64_t>(sp.expert_bytes / 55e3));
     e.cfg.cost.t_g = std::max<int64_t>(1, std::min<int64_t>(e.cfg.cost.t_io - 1,
                                                              static_cast<int64_t>(sp.expert_bytes / 6.5e6) + 5));
@@ -1072,12 +1213,52 @@ void create_engine(const ps_engine_config& cfg, ps_engine_s& e) {
   PS_CUDA(cudaEventCreateWithFlags(&e.ev_routed, cudaEventDisableTiming));
   PS_CUDA(cudaEventCreate(&e.ev_step0));
   PS_CUDA(cudaEventCreate(&e.ev_step1));
+
+  if (cfg.host_threads > 0) {
+    require(!e.ep, "engine: the host expert lane is not supported with expert parallelism");
+    if (ps_host_lane_create(cfg.host_threads, &e.lane) != PS_OK) fail(PS_ERUNTIME, ps_last_error());
+    PS_CUDA(cudaHostAlloc(&e.lane_x, sizeof(uint16_t) * B * e.H, cudaHostAllocDefault));
+    PS_CUDA(cudaHostAlloc(&e.lane_idx, sizeof(int32_t) * (rows_t + e.Et + 1), cudaHostAllocDefault));
+    PS_CUDA(cudaHostAlloc(&e.lane_xrows, sizeof(uint16_t) * rows_t * e.H, cudaHostAllocDefault));
+    PS_CUDA(cudaHostAlloc(&e.lane_yrows, sizeof(float) * rows_t * e.H, cudaHostAllocDefault));
+    e.lane_drv = std::make_unique<LaneDriver>(e.lane, e.H, e.F);
+    // cpu_cost = beta*m + C (cost_model.cpp:34-37) measured on this host: the lane on a
+    // host-resident expert slab at m = 1 and m = min(16, maxB), best of 3 each.
+    const uint16_t* probe = nullptr;
+    for (const uint16_t* p : e.host_slab)
+      if (p) {
+        probe = p;
+        break;
+      }
+    if (auto_cost && probe) {
+      std::memset(e.lane_xrows, 0, sizeof(uint16_t) * rows_t * e.H);
+      auto best = [&](int m) {
+        double t = 1e30;
+        for (int r = 0; r < 3; ++r) {
+          const double a = now_us();
+          if (ps_host_expert_ffn(e.lane, probe, e.H, e.F, e.lane_xrows, m, e.lane_yrows) != PS_OK)
+            fail(PS_ERUNTIME, ps_last_error());
+          t = std::min(t, now_us() - a);
+        }
+        return t;
+      };
+      const int m2 = std::min<int>(16, static_cast<int>(rows_t));
+      const double t1 = best(1), t2 = m2 > 1 ? best(m2) : t1;
+      const double beta = m2 > 1 ? std::max(0.0, (t2 - t1) / (m2 - 1)) : 0.0;
+      e.cfg.cost.beta = std::max(beta, 1e-3);
+      e.cfg.cost.startup = std::max<int64_t>(0, ps_to_ticks(t1 - beta));
+    }
+  }
   e.st.cost = e.cfg.cost;
 }
 
 void destroy_engine(ps_engine_s& e) {
   if (e.io) e.io->drain();
   e.io.reset();
+  e.lane_drv.reset();
+  if (e.lane) ps_host_lane_destroy(e.lane);
+  for (void* p : {(void*)e.lane_x, (void*)e.lane_idx, (void*)e.lane_xrows, (void*)e.lane_yrows})
+    if (p) cudaFreeHost(p);
   if (e.sc) cudaStreamSynchronize(e.sc);
   for (auto& ld : e.layer) {
     cudaFree(ld.weights);
@@ -1200,6 +1381,21 @@ ps_status ps_engine_calibrate(ps_engine e, ps_cost_params* out) {
     if (e->ffn_experts > 0) c.t_g = std::max<int64_t>(0, std::llround(1000.0 * e->ffn_expert_ms_total / e->ffn_experts));
     if (e->st.layers > 0) c.t_attn = std::llround(1000.0 * e->route_ms_total_cal / static_cast<double>(e->st.layers));
     if (c.t_g >= c.t_io) c.t_g = c.t_io - 1;  // CostParams invariant t_g < t_io (cost_model.cpp:16)
+    // Host lane: cpu_cost = beta*m + C from the measured (tokens, us) samples
+    // (fit_cost_params, cost_model.cpp:45-72) when they span >= 2 token counts.
+    if (!e->cal_m.empty()) {
+      const bool spread = std::any_of(e->cal_m.begin(), e->cal_m.end(), [&](int m) { return m != e->cal_m[0]; });
+      double beta = c.beta, startup = 0, r2 = 0;
+      if (spread && ps_fit_cost_params(e->cal_m.data(), e->cal_us.data(), static_cast<int>(e->cal_m.size()), &beta,
+                                       &startup, &r2) == PS_OK && beta > 0) {
+        c.beta = beta;
+        c.startup = std::max<int64_t>(0, ps_to_ticks(startup));
+      } else {
+        double mean = 0;
+        for (size_t i = 0; i < e->cal_m.size(); ++i) mean += e->cal_us[i] - c.beta * e->cal_m[i];
+        c.startup = std::max<int64_t>(0, ps_to_ticks(mean / e->cal_m.size()));
+      }
+    }
     if (ps_cost_params_validate(&c) != PS_OK) fail(PS_EINVAL, ps_last_error());
     e->cfg.cost = c;
     e->st.cost = c;

@@ -20,16 +20,18 @@ def _small_spec(L=4, E=8, H=256, F=512, preset="mixtral"):
     return spec
 
 
-def _run(spec, B, budget, policy="presched", seed=3, steps=2, predictor=None, n_shared=0):
+def _run(spec, B, budget, policy="presched", seed=3, steps=2, predictor=None, n_shared=0, **kw):
     cfg = ps.TraceGenConfig(*[ps.GROUP_DEFAULT_GEN[g] for g in ("input", "middle", "output")])
     gate, hidden, follow, zipf = ps.trace_inputs(cfg, spec, B, seed)
     F = ps.ffn_dim(spec)
     with eng.Engine(spec, cfg, budget_fraction=budget, max_batch=B, weight_seed=9, gate=gate,
                     trace_hidden=hidden, trace_follow=follow, policy=policy, predictor=predictor,
-                    n_shared=n_shared) as e:
+                    n_shared=n_shared, **kw) as e:
         for _ in range(steps):
             y, ids = e.step_host(hidden, follow)
         st = e.stats()
+        if kw.get("host_threads"):
+            assert e.verify_last_step() == []
         resident = set(e.resident)
     _, ref_w, ref_ids = orc.or_route_trace(gate, hidden, follow, zipf, spec.top_k)
     agree = (np.sort(ids, -1) == np.sort(ref_ids.transpose(1, 0, 2), -1)).all(-1).mean()
@@ -130,3 +132,21 @@ def test_engine_shared_experts_deepseek_shape(torch_cuda, B, budget):
     needed = sum(1 for l in range(spec.num_layers) for e in set(ids[l].ravel().tolist()) if (l, e) not in resident)
     assert st["ondemand_loads"] + st["prefetches_committed"] >= needed
     assert st["ondemand_loads"] <= needed
+
+
+@pytest.mark.parametrize("B,budget,n_shared", [(8, 0.25, 0), (16, 0.0, 0), (8, 0.5, 2)])
+def test_engine_host_lane_runs_cpu_set_and_matches_oracle(torch_cuda, B, budget, n_shared):
+    """Host expert lane (R5): with PCIe priced far above the host's cpu_cost, PreSched
+    puts the coldest experts in cpu_set; the lane computes them from pinned host DRAM
+    while the remaining loads run; outputs still match the oracle, every routed
+    non-resident expert is either computed on the host or crosses PCIe, and the measured
+    timeline (CPU_EXPERT events included) passes verify_timeline."""
+    spec = _small_spec() if not n_shared else _small_spec(L=3, E=64, H=256, F=256, preset="deepseek")
+    cost = (1000, 5, 10, 1.0, 1, 0)  # t_io, t_g, t_attn, beta, startup, alpha (us)
+    y, y_ref, ids, st, resident, agree = _run(spec, B, budget, host_threads=4, cost=cost, n_shared=n_shared)
+    assert agree >= 0.98
+    assert np.linalg.norm(y - y_ref) / np.linalg.norm(y_ref) < BF16_RTOL
+    assert st["cpu_experts"] > 0 and st["cpu_ms_total"] > 0
+    needed = sum(1 for l in range(spec.num_layers) for e in set(ids[l].ravel().tolist()) if (l, e) not in resident)
+    assert st["cpu_experts"] + st["ondemand_loads"] + st["prefetches_committed"] >= needed * st["steps"]
+    assert st["cpu_experts"] + st["ondemand_loads"] <= needed * st["steps"]

@@ -1,0 +1,105 @@
+"""Host expert lane (Resource::Cpu of the reference, simulator.cpp:139-146): the
+AVX512-BF16 / AMX-BF16 SwiGLU of ps_host_expert_ffn vs the f64 CPU oracle
+(or_expert_ffn, h rounded to bf16 like K3) at the bf16 tolerance. CPU-only tests: the
+lane runs on the host, no GPU involved."""
+import ctypes as C
+import os
+
+import numpy as np
+import pytest
+
+import oracle as orc
+import paper_2509_23638_b200 as ps
+
+BF16_RTOL = 2e-2
+
+
+def _has(flag):
+    try:
+        return flag in open("/proc/cpuinfo").read()
+    except OSError:
+        return False
+
+
+needs_bf16 = pytest.mark.skipif(not _has("avx512_bf16"), reason="host CPU lacks AVX512_BF16")
+
+
+def _lane(threads, isa):
+    old = os.environ.get("PS_HOST_LANE_ISA")
+    if isa == "avx512":
+        os.environ["PS_HOST_LANE_ISA"] = "avx512"
+    try:
+        h = C.c_void_p()
+        ps.check(ps.load().ps_host_lane_create(threads, C.byref(h)))
+    finally:
+        if old is None:
+            os.environ.pop("PS_HOST_LANE_ISA", None)
+        else:
+            os.environ["PS_HOST_LANE_ISA"] = old
+    return h
+
+
+ISAS = ["avx512"] + (["amx"] if _has("amx_bf16") else [])
+
+
+@needs_bf16
+@pytest.mark.parametrize("isa", ISAS)
+@pytest.mark.parametrize("H,F,m", [(256, 512, 1), (256, 512, 5), (256, 512, 16), (256, 512, 17),
+                                   (512, 768, 33), (2048, 1408, 3)])
+def test_host_expert_ffn_matches_oracle(isa, H, F, m):
+    lib = ps.load()
+    lane = _lane(3, isa)
+    try:
+        want = 2 if isa == "amx" else 1
+        assert lib.ps_host_lane_isa(lane) == want
+        slab = orc.or_init_slab(H, F, 5, 1, 2)
+        rng = np.random.default_rng(H + m)
+        x = orc.f32_to_bf16(rng.standard_normal((m, H)).astype(np.float32))
+        y = np.full((m, H), np.nan, np.float32)
+        ps.check(lib.ps_host_expert_ffn(lane, slab.ctypes.data, H, F, x.ctypes.data, m, y.ctypes.data))
+        yr = np.empty((m, H), np.float32)
+        orc.oracle_lib().or_expert_ffn(slab.ctypes.data, H, F, m, x.ctypes.data, yr.ctypes.data, 1)
+        assert np.isfinite(y).all()
+        for t in range(m):  # per token: padding rows of a 16-token AMX group must not leak
+            assert np.linalg.norm(y[t] - yr[t]) / np.linalg.norm(yr[t]) < BF16_RTOL
+    finally:
+        lib.ps_host_lane_destroy(lane)
+
+
+@needs_bf16
+def test_host_lane_isas_agree_and_threads_invariant():
+    """Row partitioning over threads does not change any value (each output element is
+    one thread's fixed-order sum); the two ISAs agree at the bf16 tolerance."""
+    lib = ps.load()
+    H, F, m = 512, 1024, 9
+    slab = orc.or_init_slab(H, F, 1, 0, 0)
+    x = orc.f32_to_bf16(np.random.default_rng(0).standard_normal((m, H)).astype(np.float32))
+    outs = {}
+    for isa in ISAS:
+        for threads in (1, 4):
+            lane = _lane(threads, isa)
+            y = np.empty((m, H), np.float32)
+            ps.check(lib.ps_host_expert_ffn(lane, slab.ctypes.data, H, F, x.ctypes.data, m, y.ctypes.data))
+            lib.ps_host_lane_destroy(lane)
+            outs[(isa, threads)] = y
+    for isa in ISAS:
+        np.testing.assert_array_equal(outs[(isa, 1)], outs[(isa, 4)])
+    a, b = outs[(ISAS[0], 1)], outs[(ISAS[-1], 1)]
+    assert np.linalg.norm(a - b) / np.linalg.norm(b) < BF16_RTOL
+
+
+@needs_bf16
+def test_host_lane_argument_errors():
+    lib = ps.load()
+    lane = _lane(1, "avx512")
+    try:
+        y = np.empty(64, np.float32)
+        x = np.zeros(64, np.uint16)
+        slab = np.zeros(3 * 48 * 64, np.uint16)
+        assert lib.ps_host_expert_ffn(lane, slab.ctypes.data, 48, 64, x.ctypes.data, 1, y.ctypes.data) == ps.capi.PS_EINVAL
+        assert lib.ps_host_expert_ffn(lane, slab.ctypes.data, 64, 64, x.ctypes.data, 0, y.ctypes.data) == ps.capi.PS_OK
+        assert lib.ps_host_expert_ffn(lane, None, 64, 64, x.ctypes.data, 1, y.ctypes.data) == ps.capi.PS_EINVAL
+    finally:
+        lib.ps_host_lane_destroy(lane)
+    h = C.c_void_p()
+    assert lib.ps_host_lane_create(0, C.byref(h)) == ps.capi.PS_EINVAL
