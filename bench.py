@@ -163,14 +163,16 @@ def run_reference_arm(args):
     print(json.dumps(line))
 
 
-def workload_config(args, spec):
+def workload_config(args, spec, executor="gpu_only"):
     import paper_2509_23638_b200 as ps
     L, E = spec.num_layers, spec.experts_per_layer
     n_res = int(round(args.budget * L * E))
     return {"workload": f"{args.model}-shape MoE decode: {L} layers, {E} experts top-{spec.top_k}, H={spec.hidden_dim}, "
                         f"F={ps.ffn_dim(spec)}, batch {args.batch}, HBM expert budget {args.budget:.0%} "
                         f"({n_res}/{L * E} experts resident, hot-table residency from a warm-up trace), "
-                        f"other experts in pinned host DRAM, policy {args.policy}",
+                        f"other experts in pinned host DRAM, policy {args.policy}"
+                        + (", PreSched cpu_set on the host expert lane (AMX-BF16)" if executor == "host_lane" else
+                           ", GPU-only executor"),
             "model": f"{args.model}-8x7b-shape" if args.model == "mixtral" else args.model,
             "global_batch": args.batch * args.gpus, "seq_len": 1, "parallelism": (f"ep{args.gpus}" if args.gpus > 1 else "single"),
             "budget_fraction": args.budget, "policy": args.policy,
@@ -227,10 +229,13 @@ def run_ours(args):
     lib = ps.load()
     predictor = C.c_void_p()
     ps.check(lib.ps_llapor_random(C.byref(spec), 256, 512, 32, 48, 3, C.byref(predictor)))
+    host_threads = args.host_threads if args.host_threads >= 0 else default_host_threads()
     t_create = time.perf_counter()
     e = eng.Engine(spec, gen, max_batch=B, weight_seed=args.weight_seed, gate=gate, budget_bytes=budget_bytes,
-                   resident=resident, policy=args.policy, predictor=predictor, device=local, ep=ep)
+                   resident=resident, policy=args.policy, predictor=predictor, device=local, ep=ep,
+                   host_threads=host_threads if world == 1 else 0)
     t_create = time.perf_counter() - t_create
+    measured_cost = e.stats()["cost"]
 
     # device-resident step inputs (layer-major), outputs
     hid_d = [torch.as_tensor(np.ascontiguousarray(hidden[s * B:(s + 1) * B].transpose(1, 0, 2), np.float32),
@@ -238,28 +243,42 @@ def run_ours(args):
     fol_d = [torch.as_tensor(np.ascontiguousarray(follow[s * B:(s + 1) * B].T), device="cuda") for s in range(S)]
     y_d = torch.empty(L, B, H, dtype=torch.float32, device="cuda")
 
-    for s in range(args.warmup):
-        e.step_device(hid_d[s], fol_d[s], y_d)
-    torch.cuda.synchronize()
-    e.reset_stats()
-    if dist:
-        dist.barrier()
-    torch.cuda.synchronize()
-    with ClockSampler(local) as clk:
-        t0 = time.perf_counter()
-        for s in range(args.warmup, S):
+    def decode_leg(calibrate=False):
+        for s in range(args.warmup):
             e.step_device(hid_d[s], fol_d[s], y_d)
         torch.cuda.synchronize()
-        wall = time.perf_counter() - t0
-    st = e.stats()
-    dev_ms = st["step_ms_total"] / max(1, st["steps"])
-    if dist:
-        t = torch.tensor([dev_ms], device="cuda")
-        dist.all_reduce(t, op=dist.ReduceOp.MAX)
-        dev_ms = float(t.item())
-        dist.barrier()
+        if calibrate:
+            e.calibrate()  # measured t_io / t_g / t_attn / host-lane beta, C (fit_cost_params)
+        e.reset_stats()
+        if dist:
+            dist.barrier()
+        torch.cuda.synchronize()
+        with ClockSampler(local) as clk:
+            t0 = time.perf_counter()
+            for s in range(args.warmup, S):
+                e.step_device(hid_d[s], fol_d[s], y_d)
+            torch.cuda.synchronize()
+            wall = time.perf_counter() - t0
+        st = e.stats()
+        dev_ms = st["step_ms_total"] / max(1, st["steps"])
+        if dist:
+            t = torch.tensor([dev_ms], device="cuda")
+            dist.all_reduce(t, op=dist.ReduceOp.MAX)
+            dev_ms = float(t.item())
+            dist.barrier()
+        return st, dev_ms, wall, clk.summary()
 
-    # end-to-end through the host-buffer C-ABI entry point (pinned host buffers)
+    # GPU-only executor: PreSched with beta = 1e9 (cpu_set always empty).
+    e.set_cost(measured_cost["t_io"], measured_cost["t_g"], measured_cost["t_attn"], 1e9, 0)
+    legs = {"gpu_only": decode_leg()}
+    if e.host_threads:
+        # Host expert lane: PreSched with the host's measured cpu_cost (beta*m + C).
+        e.set_cost(**measured_cost)
+        legs["host_lane"] = decode_leg(calibrate=True)
+    head = "host_lane" if "host_lane" in legs else "gpu_only"
+    st, dev_ms, wall, clocks = legs[head]
+
+    # end-to-end through the host-buffer C-ABI entry point (pinned host buffers), same executor
     hid_h = [torch.from_numpy(np.ascontiguousarray(hidden[s * B:(s + 1) * B], np.float32)).pin_memory()
              for s in range(S)]
     fol_h = [torch.from_numpy(np.ascontiguousarray(follow[s * B:(s + 1) * B])).pin_memory() for s in range(S)]
@@ -363,15 +382,16 @@ def run_ours(args):
         tj = json.loads(tpath.read_text())
         traffic = tj["traffic_over_algorithmic"] * ffn_bytes / ffn_launches
         traffic_src = f"{tj['source']}: traffic/algorithmic = {tj['traffic_over_algorithmic']:.4f}"
-    h2d_gbs = st["h2d_bytes"] / (st["h2d_busy_ms"] / 1e3) / 1e9 if st["h2d_busy_ms"] > 0 else 0.0
-    hidden_frac = 1.0 - st["compute_wait_ms"] / st["h2d_busy_ms"] if st["h2d_busy_ms"] > 0 else 1.0
+    leg_summary = {name: decode_summary(lst, lms, N, B, L) for name, (lst, lms, _, _) in legs.items()}
+    if "cpu_lane" in leg_summary.get("host_lane", {}):
+        leg_summary["host_lane"]["cpu_lane"]["threads"] = host_threads
     threads = os.cpu_count() or 1
     cpu_step_s, cpu_desc = cpu_sample(args, spec, gen, threads) if not args.no_cpu_baseline else (None, "skipped")
     line = {
         "metric": METRIC, "value": value, "unit": "tokens/s", "n_gpus": N, "steps": args.steps,
         "warmup": args.warmup, "ms_per_step": dev_ms, "higher_is_better": True, "scaling": "weak",
         "vs_baseline": None, "dtype": "bf16", "data": "synthetic (reference trace generator, hash-init bf16 weights)",
-        "config": workload_config(args, spec),
+        "config": workload_config(args, spec, head),
         "moe_layer_us": dev_ms * 1e3 / L,
         "e2e": {"value": N * B / e2e_s, "unit": "tokens/s", "h2d_bytes_per_step": h2d_in,
                 "d2h_bytes_per_step": d2h_out, "timing": "host wall-clock around ps_engine_decode_step_host"},
@@ -380,16 +400,15 @@ def run_ours(args):
                      "frac": achieved / peak_hbm, "traffic": traffic, "traffic_source": traffic_src,
                      "algorithmic_bytes_per_launch": ffn_bytes / ffn_launches,
                      "avg_launch_us": ffn_ms * 1e3 / ffn_launches},
-        "h2d": {"achieved_gbs": h2d_gbs, "peak_gbs": PCIE_H2D_PEAK_GBS, "frac": h2d_gbs / PCIE_H2D_PEAK_GBS,
-                "bytes_per_step": st["h2d_bytes"] / max(1, st["steps"]),
-                "ondemand_loads_per_step": st["ondemand_loads"] / max(1, st["steps"]),
-                "prefetches_per_step": st["prefetches_committed"] / max(1, st["steps"]),
-                "hidden_fraction": hidden_frac},
+        "h2d": leg_summary[head]["h2d"],
+        "executor": head,
+        "host_lane": leg_summary.get("host_lane"),
+        "gpu_only": leg_summary["gpu_only"],
         "cpu_baseline": ({"value": args.batch / cpu_step_s, "unit": "tokens/s", "cores": threads, "kind": "port",
                           "sample": cpu_desc} if cpu_step_s else None),
         "all_resident": all_res,
         "prefill": prefill,
-        "clocks": clk.summary(),
+        "clocks": clocks,
         "gpu_launches": st["kernel_launches"],
         "wall_s_timed": wall, "engine_create_s": t_create,
         "cost_params_us": st["cost"],
@@ -397,6 +416,41 @@ def run_ours(args):
     print(json.dumps(line))
     if dist:
         dist.destroy_process_group()
+
+
+def default_host_threads():
+    """Host expert lane threads: all cores but 4 (engine thread, I/O thread, bench), at
+    most 12 (12 threads stream 120-165 GB/s on the B200 box's 16-core host; more
+    oversubscribe, profiles/r01_host_lane_micro.jsonl); 0 without AVX512_BF16."""
+    try:
+        if "avx512_bf16" not in open("/proc/cpuinfo").read():
+            return 0
+    except OSError:
+        return 0
+    return max(0, min(12, (os.cpu_count() or 1) - 4))
+
+
+def decode_summary(st, dev_ms, N, B, L):
+    """Per-executor decode numbers: throughput, PCIe, hidden fraction, host lane."""
+    steps = max(1, st["steps"])
+    h2d_gbs = st["h2d_bytes"] / (st["h2d_busy_ms"] / 1e3) / 1e9 if st["h2d_busy_ms"] > 0 else 0.0
+    out = {"value": N * B / (dev_ms / 1e3), "unit": "tokens/s", "ms_per_step": dev_ms,
+           "moe_layer_us": dev_ms * 1e3 / L,
+           "h2d": {"achieved_gbs": h2d_gbs, "peak_gbs": PCIE_H2D_PEAK_GBS, "frac": h2d_gbs / PCIE_H2D_PEAK_GBS,
+                   "bytes_per_step": st["h2d_bytes"] / steps,
+                   "ondemand_loads_per_step": st["ondemand_loads"] / steps,
+                   "prefetches_per_step": st["prefetches_committed"] / steps,
+                   "prefetch_hits_per_step": st["prefetch_hits"] / steps,
+                   # 1 - (compute-stream stall on copy events) / (copy-engine busy time)
+                   "hidden_fraction": (1.0 - st["compute_wait_ms"] / st["h2d_busy_ms"]) if st["h2d_busy_ms"] > 0
+                   else 1.0},
+           "cost_params_us": st["cost"]}
+    if st["cpu_experts"]:
+        out["cpu_lane"] = {"experts_per_step": st["cpu_experts"] / steps,
+                           "busy_ms_per_step": st["cpu_ms_total"] / steps,
+                           "achieved_gbs": st["cpu_bytes_total"] / (st["cpu_ms_total"] / 1e3) / 1e9,
+                           "threads": None}
+    return out
 
 
 def N_world(dist):
@@ -422,6 +476,8 @@ def main():
     ap.add_argument("--no-all-resident", action="store_true")
     ap.add_argument("--prefill-tokens", type=int, default=4096)
     ap.add_argument("--prefill-steps", type=int, default=3)
+    ap.add_argument("--host-threads", type=int, default=-1,
+                    help="host expert lane threads (-1 auto, 0 = GPU-only executor)")
     args = ap.parse_args()
     if args.impl == "reference":
         run_reference_arm(args)

@@ -480,6 +480,9 @@ ps_status ps_engine_reset_stats(ps_engine e);
  * (ps_verify_timeline_ex, measured = 1). */
 ps_status ps_engine_last_timeline(ps_engine e, ps_timeline* out, int32_t* truth_out,
                                   uint8_t* resident_out);
+/* Replace the cost parameters PreSched plans with (e.g. beta = 1e9 disables the host
+ * lane's cpu_set for a GPU-only comparison on the same engine). */
+ps_status ps_engine_set_cost(ps_engine e, const ps_cost_params* cost);
 /* Calibration (cost_model.cpp:45-72 fit + simulator cost semantics): replace the
  * engine's PreSched costs with the means measured since the last stats reset —
  * t_io = mean copy time per expert, t_g = mean FFN time per routed expert, t_attn =

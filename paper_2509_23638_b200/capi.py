@@ -215,6 +215,7 @@ _SIGS = {
     "ps_engine_reset_stats": (C.c_int, [_P]),
     "ps_engine_last_timeline": (C.c_int, [_P, C.POINTER(Timeline), _P, _P]),
     "ps_engine_calibrate": (C.c_int, [_P, C.POINTER(CostParams)]),
+    "ps_engine_set_cost": (C.c_int, [_P, C.POINTER(CostParams)]),
     "ps_verify_timeline_ex": (C.c_int, [C.POINTER(TimelineEvent), C.c_int, C.POINTER(PipelineInstance),
                                         C.POINTER(CostParams), C.c_int, C.POINTER(C.c_int), C.c_char_p, C.c_int]),
 }

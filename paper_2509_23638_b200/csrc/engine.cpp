@@ -889,7 +889,6 @@ void decode_step(ps_engine_s& e, const float* hidden, const uint8_t* follow, int
       ffn(e, one, counts_l.data(), B, true);
       release_slot_after_compute(e, job->slot);
       e.st.ondemand_loads++;
-      e.st.h2d_bytes += static_cast<double>(job->bytes);
     }
 
     // Host-lane results (R5) -> y_part rows (split 0; other splits zero), then combine.
@@ -960,7 +959,6 @@ void decode_step(ps_engine_s& e, const float* hidden, const uint8_t* follow, int
         e.pending_pf.push_back(job);
         push_modelled(e);
         e.io->push(job);
-        e.st.h2d_bytes += static_cast<double>(job->bytes);
       }
     }
   }
@@ -1024,6 +1022,7 @@ void decode_step(ps_engine_s& e, const float* hidden, const uint8_t* follow, int
     if (j->state.load() != 1) continue;
     PS_CUDA(cudaEventElapsedTime(&ms, j->start_ev, j->done_ev));
     e.st.h2d_busy_ms += ms;
+    e.st.h2d_bytes += static_cast<double>(j->bytes);  // issued copies only (cancelled prefetches moved nothing)
     e.copy_ms_total += ms;
     e.copies += 1;
     e.last_events.push_back({at_us(j->start_ev), at_us(j->done_ev), PS_RES_IO,
@@ -1371,6 +1370,15 @@ ps_status ps_engine_last_timeline(ps_engine e, ps_timeline* out, int32_t* truth_
     if (out->layer_end) std::copy(e->last_layer_end.begin(), e->last_layer_end.end(), out->layer_end);
     if (truth_out) std::copy(e->last_truth.begin(), e->last_truth.end(), truth_out);
     if (resident_out) std::copy(e->resident.begin(), e->resident.end(), resident_out);
+  });
+}
+
+ps_status ps_engine_set_cost(ps_engine e, const ps_cost_params* cost) {
+  return guarded([&] {
+    require(e && cost, "ps_engine_set_cost: null argument");
+    if (ps_cost_params_validate(cost) != PS_OK) fail(PS_EINVAL, ps_last_error());
+    e->cfg.cost = *cost;
+    e->st.cost = *cost;
   });
 }
 

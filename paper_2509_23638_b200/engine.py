@@ -135,6 +135,7 @@ class Engine:
         cfg.ep = ep.h if isinstance(ep, EpComm) else ep
         cfg.n_shared = n_shared
         cfg.host_threads = host_threads
+        self.host_threads = host_threads
         h = C.c_void_p()
         check(self.lib.ps_engine_create(C.byref(cfg), C.byref(h)))
         self.h = h
@@ -210,6 +211,10 @@ class Engine:
         c = capi.CostParams()
         check(self.lib.ps_engine_calibrate(self.h, C.byref(c)))
         return dict(t_io=c.t_io, t_g=c.t_g, t_attn=c.t_attn, beta=c.beta, startup=c.startup)
+
+    def set_cost(self, t_io, t_g, t_attn, beta, startup):
+        """Replace the PreSched cost parameters (ps_engine_set_cost)."""
+        check(self.lib.ps_engine_set_cost(self.h, C.byref(capi.CostParams(t_io, t_g, t_attn, beta, startup, 0))))
 
     def reset_stats(self):
         check(self.lib.ps_engine_reset_stats(self.h))

@@ -134,7 +134,7 @@ def test_engine_shared_experts_deepseek_shape(torch_cuda, B, budget):
     assert st["ondemand_loads"] <= needed
 
 
-@pytest.mark.parametrize("B,budget,n_shared", [(8, 0.25, 0), (16, 0.0, 0), (8, 0.5, 2)])
+@pytest.mark.parametrize("B,budget,n_shared", [(8, 0.25, 0), (16, 0.0, 0), (8, 0.2, 2)])
 def test_engine_host_lane_runs_cpu_set_and_matches_oracle(torch_cuda, B, budget, n_shared):
     """Host expert lane (R5): with PCIe priced far above the host's cpu_cost, PreSched
     puts the coldest experts in cpu_set; the lane computes them from pinned host DRAM
