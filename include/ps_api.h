@@ -352,6 +352,11 @@ int ps_host_lane_threads(ps_host_lane lane);
 int ps_host_lane_isa(ps_host_lane lane); /* 2 = AMX-BF16 tiles, 1 = AVX512-BF16 GEMV */
 ps_status ps_host_expert_ffn(ps_host_lane lane, const uint16_t* slab, int H, int F, const uint16_t* x,
                              int m, float* y);
+/* A layer's cpu_set in one call: expert j reads x rows [row0[j], row0[j] + m[j]) and
+ * writes the same rows of y (both [*, H], host). Same numerics per expert. */
+ps_status ps_host_expert_ffn_batch(ps_host_lane lane, int n, const uint16_t* const* slabs,
+                                   const int32_t* m, const int32_t* row0, int H, int F,
+                                   const uint16_t* x, float* y);
 
 /* K4 — LLaPor predictor (predictor.cpp:116-124, 166-247, 344-352, 669-672). */
 typedef struct ps_llapor_s* ps_llapor;

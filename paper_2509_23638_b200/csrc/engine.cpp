@@ -247,13 +247,25 @@ class LaneDriver {
       if (stop_) return;
       std::vector<CpuJob>* jobs = jobs_;
       g.unlock();
+      // One batch call per layer (both pool passes span all experts of the set); every
+      // expert of the set is reported with the batch's interval.
       std::string err;
+      slabs_.clear();
+      m_.clear();
+      row0_.clear();
+      for (const CpuJob& j : *jobs) {
+        slabs_.push_back(j.slab);
+        m_.push_back(j.m);
+        row0_.push_back(j.row0);
+      }
+      const double t0 = now_us();
+      if (ps_host_expert_ffn_batch(lane_, static_cast<int>(jobs->size()), slabs_.data(), m_.data(), row0_.data(), H_,
+                                   F_, x_, y_) != PS_OK)
+        err = ps_last_error();
+      const double t1 = now_us();
       for (CpuJob& j : *jobs) {
-        j.t0_us = now_us();
-        if (ps_host_expert_ffn(lane_, j.slab, H_, F_, x_ + static_cast<size_t>(j.row0) * H_, j.m,
-                               y_ + static_cast<size_t>(j.row0) * H_) != PS_OK && err.empty())
-          err = ps_last_error();
-        j.t1_us = now_us();
+        j.t0_us = t0;
+        j.t1_us = t1;
       }
       g.lock();
       jobs_ = nullptr;
@@ -271,6 +283,8 @@ class LaneDriver {
   float* y_ = nullptr;
   bool stop_ = false, done_ = true;
   std::string err_;
+  std::vector<const uint16_t*> slabs_;
+  std::vector<int32_t> m_, row0_;
   std::thread thread_;  // last: starts after the members it uses
 };
 
@@ -307,7 +321,6 @@ struct ps_engine_s {
   ps_host_lane lane = nullptr;
   std::unique_ptr<ps::LaneDriver> lane_drv;
   uint16_t* lane_x = nullptr;    // pinned: [maxB, H] bf16 x (D2H at the scheduling point)
-  int32_t* lane_idx = nullptr;   // pinned: perm_src [maxB*Kt] | offsets [Et+1]
   uint16_t* lane_xrows = nullptr;  // pinned: [maxB*Kt, H] bf16 gathered rows of CPU experts
   float* lane_yrows = nullptr;     // pinned: [maxB*Kt, H] f32 their outputs
   std::vector<ps::CpuJob> cpu_jobs;      // current layer
@@ -336,7 +349,10 @@ struct ps_engine_s {
   std::vector<ps::LayerDev> layer;
   int32_t* counts_dev = nullptr;     // [Et]
   int32_t* pred_dev = nullptr;       // [E]
-  int32_t* pinned_counts = nullptr;  // [3Et+1] host pinned: counts | pred | offsets
+  // Scheduling-point block, one device allocation mirrored in pinned host memory so the
+  // per-layer D2H is ONE copy: counts [Et] | pred [Et] | offsets [Et+1] | perm_src [maxB*Kt]
+  int32_t* sched_dev = nullptr;
+  int32_t* pinned_counts = nullptr;  // host mirror of sched_dev
   uint16_t* x_bf16 = nullptr;
   uint16_t* x_perm = nullptr;        // [maxB*k, H] bf16 (prefill gather)
   bool prefill_mode = false;         // B > kDecodeMaxBatch: tcgen05 path, exact-count launches
@@ -683,19 +699,12 @@ void decode_step(ps_engine_s& e, const float* hidden, const uint8_t* follow, int
                      e.prefill_mode ? e.x_bf16 : nullptr, H, e.prefill_mode ? e.x_perm : nullptr, e.sc);
       if (s != PS_OK) fail(s, ps_last_error());
       e.st.kernel_launches += e.prefill_mode ? 2 : 1;
-      PS_CUDA(cudaMemcpyAsync(e.pinned_counts, e.counts_dev, sizeof(int32_t) * Et, cudaMemcpyDeviceToHost, e.sc));
-      if (predict)
-        PS_CUDA(cudaMemcpyAsync(e.pinned_counts + Et, e.pred_dev, sizeof(int32_t) * E, cudaMemcpyDeviceToHost, e.sc));
-      if (e.prefill_mode)
-        PS_CUDA(cudaMemcpyAsync(e.pinned_counts + 2 * Et, e.offsets, sizeof(int32_t) * (Et + 1),
-                                cudaMemcpyDeviceToHost, e.sc));
+      // counts | pred | offsets (| perm_src for the host lane) in one copy
+      const size_t n_sched = 3 * static_cast<size_t>(Et) + 1 + (e.lane ? static_cast<size_t>(B) * Kt : 0);
+      PS_CUDA(cudaMemcpyAsync(e.pinned_counts, e.sched_dev, sizeof(int32_t) * n_sched, cudaMemcpyDeviceToHost, e.sc));
       e.src = {e.offsets, e.perm_src, Kt, e.x_bf16, B * Kt, e.pinned_counts + 2 * Et};
-      if (e.lane) {  // the host lane needs x and the permutation for its rows
+      if (e.lane)  // the host lane gathers its rows from x
         PS_CUDA(cudaMemcpyAsync(e.lane_x, e.x_bf16, sizeof(uint16_t) * B * H, cudaMemcpyDeviceToHost, e.sc));
-        PS_CUDA(cudaMemcpyAsync(e.lane_idx, e.perm_src, sizeof(int32_t) * B * Kt, cudaMemcpyDeviceToHost, e.sc));
-        PS_CUDA(cudaMemcpyAsync(e.lane_idx + static_cast<size_t>(e.maxB) * Kt, e.offsets, sizeof(int32_t) * (Et + 1),
-                                cudaMemcpyDeviceToHost, e.sc));
-      }
     } else {
       // EP dispatch, part 1: owner-major permute + gather of this rank's routed rows,
       // then the (rows, predicted tokens) counts exchange with every owner.
@@ -847,8 +856,8 @@ void decode_step(ps_engine_s& e, const float* hidden, const uint8_t* follow, int
     // GPU-only executor loads them after ondemand_seq.
     e.cpu_jobs.clear();
     if (e.lane && plan.n_cpu > 0) {
-      const int32_t* perm = e.lane_idx;
-      const int32_t* off = e.lane_idx + static_cast<size_t>(e.maxB) * Kt;
+      const int32_t* off = e.pinned_counts + 2 * Et;
+      const int32_t* perm = e.pinned_counts + 3 * Et + 1;
       for (int i = 0; i < plan.n_cpu; ++i) {
         const int ex = plan.cpu_set[i].expert;
         const uint16_t* slab = e.host_slab[static_cast<size_t>(l) * E + ex];
@@ -895,6 +904,16 @@ void decode_step(ps_engine_s& e, const float* hidden, const uint8_t* follow, int
     if (!e.cpu_jobs.empty()) {
       e.lane_drv->wait();
       const size_t total_rows = static_cast<size_t>(e.src.rows);
+      {  // one batch per layer: T = beta*sum(m) + n*C, so (mean tokens, mean time) per
+         // expert is one sample of cpu_cost(m) = beta*m + C for fit_cost_params
+        const double us = e.cpu_jobs[0].t1_us - e.cpu_jobs[0].t0_us;
+        const double n = static_cast<double>(e.cpu_jobs.size());
+        double tok = 0;
+        for (const CpuJob& j : e.cpu_jobs) tok += j.m;
+        e.st.cpu_ms_total += us / 1e3;
+        e.cal_m.push_back(static_cast<int32_t>(std::lround(tok / n)));
+        e.cal_us.push_back(ps_to_ticks(us / n));
+      }
       for (CpuJob& j : e.cpu_jobs) {
         const size_t bytes = sizeof(float) * static_cast<size_t>(j.m) * H;
         PS_CUDA(cudaMemcpyAsync(e.y_part + static_cast<size_t>(j.row0) * H, e.lane_yrows + static_cast<size_t>(j.row0) * H,
@@ -902,10 +921,7 @@ void decode_step(ps_engine_s& e, const float* hidden, const uint8_t* follow, int
         for (int sp = 1; sp < e.step_split; ++sp)
           PS_CUDA(cudaMemsetAsync(e.y_part + (sp * total_rows + j.row0) * H, 0, bytes, e.sc));
         e.st.cpu_experts += 1;
-        e.st.cpu_ms_total += (j.t1_us - j.t0_us) / 1e3;
         e.st.cpu_bytes_total += static_cast<double>(e.cfg.spec.expert_bytes);
-        e.cal_m.push_back(j.m);
-        e.cal_us.push_back(ps_to_ticks(j.t1_us - j.t0_us));
         j.t0_us -= host_t0_us;
         j.t1_us -= host_t0_us;
         e.cpu_done.push_back(j);
@@ -1169,17 +1185,20 @@ void create_engine(const ps_engine_config& cfg, ps_engine_s& e) {
     PS_CUDA(cudaMalloc(&ld.weights, sizeof(float) * B * e.E));
     PS_CUDA(cudaMalloc(&ld.ids, sizeof(int32_t) * rows));
   }
-  PS_CUDA(cudaMalloc(&e.counts_dev, sizeof(int32_t) * e.Et));
-  PS_CUDA(cudaMalloc(&e.pred_dev, sizeof(int32_t) * e.E));
-  PS_CUDA(cudaHostAlloc(&e.pinned_counts, sizeof(int32_t) * (3 * e.Et + 1), cudaHostAllocDefault));
+  const size_t n_sched = 3 * static_cast<size_t>(e.Et) + 1 + rows_t;
+  PS_CUDA(cudaMalloc(&e.sched_dev, sizeof(int32_t) * n_sched));
+  PS_CUDA(cudaMemset(e.sched_dev, 0, sizeof(int32_t) * n_sched));
+  PS_CUDA(cudaHostAlloc(&e.pinned_counts, sizeof(int32_t) * n_sched, cudaHostAllocDefault));
+  e.counts_dev = e.sched_dev;
+  e.pred_dev = e.sched_dev + e.Et;
+  e.offsets = e.sched_dev + 2 * e.Et;
+  e.perm_src = e.sched_dev + 3 * e.Et + 1;
   if (e.S) {
     PS_CUDA(cudaMalloc(&e.ids_ext, sizeof(int32_t) * rows_t));
     PS_CUDA(cudaMalloc(&e.w_ext, sizeof(float) * B * e.Et));
   }
   PS_CUDA(cudaMalloc(&e.x_bf16, sizeof(uint16_t) * B * e.H));
   PS_CUDA(cudaMalloc(&e.x_perm, sizeof(uint16_t) * frows * e.H));
-  PS_CUDA(cudaMalloc(&e.offsets, sizeof(int32_t) * (e.Et + 1)));
-  PS_CUDA(cudaMalloc(&e.perm_src, sizeof(int32_t) * rows_t));
   PS_CUDA(cudaMalloc(&e.inv, sizeof(int32_t) * rows_t));
   PS_CUDA(cudaMalloc(&e.hbuf, sizeof(uint16_t) * frows * e.F));
   PS_CUDA(cudaMalloc(&e.y_part, sizeof(float) * e.n_split * frows * e.H));
@@ -1217,7 +1236,6 @@ void create_engine(const ps_engine_config& cfg, ps_engine_s& e) {
     require(!e.ep, "engine: the host expert lane is not supported with expert parallelism");
     if (ps_host_lane_create(cfg.host_threads, &e.lane) != PS_OK) fail(PS_ERUNTIME, ps_last_error());
     PS_CUDA(cudaHostAlloc(&e.lane_x, sizeof(uint16_t) * B * e.H, cudaHostAllocDefault));
-    PS_CUDA(cudaHostAlloc(&e.lane_idx, sizeof(int32_t) * (rows_t + e.Et + 1), cudaHostAllocDefault));
     PS_CUDA(cudaHostAlloc(&e.lane_xrows, sizeof(uint16_t) * rows_t * e.H, cudaHostAllocDefault));
     PS_CUDA(cudaHostAlloc(&e.lane_yrows, sizeof(float) * rows_t * e.H, cudaHostAllocDefault));
     e.lane_drv = std::make_unique<LaneDriver>(e.lane, e.H, e.F);
@@ -1256,15 +1274,15 @@ void destroy_engine(ps_engine_s& e) {
   e.io.reset();
   e.lane_drv.reset();
   if (e.lane) ps_host_lane_destroy(e.lane);
-  for (void* p : {(void*)e.lane_x, (void*)e.lane_idx, (void*)e.lane_xrows, (void*)e.lane_yrows})
+  for (void* p : {(void*)e.lane_x, (void*)e.lane_xrows, (void*)e.lane_yrows})
     if (p) cudaFreeHost(p);
   if (e.sc) cudaStreamSynchronize(e.sc);
   for (auto& ld : e.layer) {
     cudaFree(ld.weights);
     cudaFree(ld.ids);
   }
-  for (void* p : {(void*)e.arena, (void*)e.gate, (void*)e.bias, (void*)e.counts_dev, (void*)e.pred_dev,
-                  (void*)e.x_bf16, (void*)e.x_perm, (void*)e.offsets, (void*)e.perm_src, (void*)e.inv, (void*)e.hbuf,
+  for (void* p : {(void*)e.arena, (void*)e.gate, (void*)e.bias, (void*)e.sched_dev,
+                  (void*)e.x_bf16, (void*)e.x_perm, (void*)e.inv, (void*)e.hbuf,
                   (void*)e.y_part, e.llapor_scratch, (void*)e.in_hidden, (void*)e.in_follow, (void*)e.out_y,
                   (void*)e.out_ids, (void*)e.ep_vids, (void*)e.ep_off_v, (void*)e.ep_perm_v, (void*)e.ep_inv_v,
                   (void*)e.ep_send_x, (void*)e.ep_recv_x, (void*)e.ep_y_recv, (void*)e.ep_y_back,

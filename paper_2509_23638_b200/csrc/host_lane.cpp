@@ -276,70 +276,122 @@ int ps_host_lane_threads(ps_host_lane l) { return l ? l->pool->size() : 0; }
 
 int ps_host_lane_isa(ps_host_lane l) { return l ? (l->amx ? 2 : 1) : 0; }
 
-ps_status ps_host_expert_ffn(ps_host_lane l, const uint16_t* slab, int H, int F, const uint16_t* x, int m, float* y) {
+// A batch of experts (PreSched's cpu_set of one layer) in two pool passes: phase 1 over
+// all (expert, 16-row block of W_gate/W_up) units, phase 2 over all (expert, 16-row
+// block of W_down) units; each thread streams a contiguous range of units. One pass pair
+// per layer instead of per expert keeps small experts (Qwen3: 9 MiB) off the pool's
+// wake-up latency.
+ps_status ps_host_expert_ffn_batch(ps_host_lane l, int n, const uint16_t* const* slabs, const int32_t* m,
+                                   const int32_t* row0, int H, int F, const uint16_t* x, float* y) {
   return guarded([&] {
-    require(l && slab && x && y, "ps_host_expert_ffn: null argument");
+    require(l && n >= 0 && (n == 0 || (slabs && m && row0 && x && y)), "ps_host_expert_ffn_batch: null argument");
     require(H > 0 && F > 0 && H % 32 == 0 && F % 32 == 0, "ps_host_expert_ffn: H and F must be multiples of 32");
-    require(m >= 0 && m <= 4096, "ps_host_expert_ffn: m out of range");
-    if (m == 0) return;
-    const uint16_t* wg = slab;
-    const uint16_t* wu = slab + static_cast<size_t>(F) * H;
-    const uint16_t* wd = slab + static_cast<size_t>(2) * F * H;
-    if (l->h.size() < static_cast<size_t>(m) * F) l->h.resize(static_cast<size_t>(m) * F);
-    uint16_t* h = l->h.data();
+    for (int j = 0; j < n; ++j) {
+      require(slabs[j] != nullptr, "ps_host_expert_ffn: null slab");
+      require(m[j] >= 0 && m[j] <= 4096 && row0[j] >= 0, "ps_host_expert_ffn: m out of range");
+    }
     const int T = l->pool->size();
+    const int nb1 = F / 16, nb2 = H / 16;
+    const int64_t U1 = static_cast<int64_t>(n) * nb1, U2 = static_cast<int64_t>(n) * nb2;
+    auto range = [&](int64_t U, int tid, int64_t& u0, int64_t& u1) {
+      u0 = U * tid / T;
+      u1 = U * (tid + 1) / T;
+    };
     if (l->amx) {
-      // AMX path: token groups of 16 (zero-padded), x packed into the VNNI pair layout.
-      const int G = (m + kTok - 1) / kTok;
-      if (l->xb.size() < static_cast<size_t>(G) * H * kTok) l->xb.resize(static_cast<size_t>(G) * H * kTok);
-      if (l->hb.size() < static_cast<size_t>(G) * F * kTok) l->hb.resize(static_cast<size_t>(G) * F * kTok);
+      // AMX path: per expert, token groups of 16 (zero-padded), x packed into the VNNI
+      // pair layout; h written by phase 1 in the same layout.
+      std::vector<size_t> xo(n + 1, 0), ho(n + 1, 0);
+      for (int j = 0; j < n; ++j) {
+        const size_t G = (m[j] + kTok - 1) / kTok;
+        xo[j + 1] = xo[j] + G * H * kTok;
+        ho[j + 1] = ho[j] + G * F * kTok;
+      }
+      if (l->xb.size() < xo[n]) l->xb.resize(xo[n]);
+      if (l->hb.size() < ho[n]) l->hb.resize(ho[n]);
       uint16_t* xb = l->xb.data();
       uint16_t* hb = l->hb.data();
-      std::memset(xb, 0, sizeof(uint16_t) * G * H * kTok);
-      for (int t = 0; t < m; ++t)
-        for (int k = 0; k < H; ++k)
-          xb[static_cast<size_t>(t / kTok) * H * kTok + (static_cast<size_t>(k >> 1) * kTok + t % kTok) * 2 + (k & 1)] =
-              x[static_cast<size_t>(t) * H + k];
-      const int nb1 = F / 16, nb2 = H / 16;
+      std::memset(xb, 0, sizeof(uint16_t) * xo[n]);
+      for (int j = 0; j < n; ++j)
+        for (int t = 0; t < m[j]; ++t) {
+          const uint16_t* xr = x + static_cast<size_t>(row0[j] + t) * H;
+          uint16_t* d = xb + xo[j] + static_cast<size_t>(t / kTok) * H * kTok + (t % kTok) * 2;
+          for (int k = 0; k < H; k += 2) {
+            d[static_cast<size_t>(k >> 1) * kTok * 2] = xr[k];
+            d[static_cast<size_t>(k >> 1) * kTok * 2 + 1] = xr[k + 1];
+          }
+        }
       l->pool->run([&](int tid) {
+        int64_t u0, u1;
+        range(U1, tid, u0, u1);
+        if (u0 == u1) return;
         amx_config();
-        for (int blk = nb1 * tid / T; blk < nb1 * (tid + 1) / T; ++blk)
-          for (int g = 0; g < G; ++g)
-            amx_gate_up_block(wg, wu, xb + static_cast<size_t>(g) * H * kTok, H, blk * 16,
-                              hb + static_cast<size_t>(g) * F * kTok);
+        for (int64_t u = u0; u < u1; ++u) {
+          const int j = static_cast<int>(u / nb1), blk = static_cast<int>(u % nb1);
+          const uint16_t* wg = slabs[j];
+          const uint16_t* wu = wg + static_cast<size_t>(F) * H;
+          for (int g = 0; g * kTok < m[j]; ++g)
+            amx_gate_up_block(wg, wu, xb + xo[j] + static_cast<size_t>(g) * H * kTok, H, blk * 16,
+                              hb + ho[j] + static_cast<size_t>(g) * F * kTok);
+        }
         amx_release();
       });
       l->pool->run([&](int tid) {
+        int64_t u0, u1;
+        range(U2, tid, u0, u1);
+        if (u0 == u1) return;
         amx_config();
-        for (int blk = nb2 * tid / T; blk < nb2 * (tid + 1) / T; ++blk)
-          for (int g = 0; g < G; ++g)
-            amx_down_block(wd, hb + static_cast<size_t>(g) * F * kTok, H, F, blk * 16, std::min(kTok, m - g * kTok),
-                           y + static_cast<size_t>(g) * kTok * H);
+        for (int64_t u = u0; u < u1; ++u) {
+          const int j = static_cast<int>(u / nb2), blk = static_cast<int>(u % nb2);
+          const uint16_t* wd = slabs[j] + static_cast<size_t>(2) * F * H;
+          for (int g = 0; g * kTok < m[j]; ++g)
+            amx_down_block(wd, hb + ho[j] + static_cast<size_t>(g) * F * kTok, H, F, blk * 16,
+                           std::min(kTok, m[j] - g * kTok), y + static_cast<size_t>(row0[j] + g * kTok) * H);
+        }
         amx_release();
       });
       return;
     }
-    // Rows outer, token chunks inner: a weight row (8 KiB at H = 4096) is read from DRAM
-    // once and re-read from L1 by the next chunk of 8 tokens.
+    // AVX512-BF16 GEMV path. Rows outer, token chunks inner: a weight row (8 KiB at
+    // H = 4096) is read from DRAM once and re-read from L1 by the next chunk of 8 tokens.
+    std::vector<size_t> hoff(n + 1, 0);
+    for (int j = 0; j < n; ++j) hoff[j + 1] = hoff[j] + static_cast<size_t>(m[j]) * F;
+    if (l->h.size() < hoff[n]) l->h.resize(hoff[n]);
+    uint16_t* h = l->h.data();
     l->pool->run([&](int tid) {
-      const int r0 = static_cast<int>(static_cast<int64_t>(F) * tid / T);
-      const int r1 = static_cast<int>(static_cast<int64_t>(F) * (tid + 1) / T);
-      for (int r = r0; r < r1; ++r)
-        by_token_chunks(m, [&](auto mt, int t0) {
-          gate_up_row<decltype(mt)::value>(wg + static_cast<size_t>(r) * H, wu + static_cast<size_t>(r) * H,
-                                           x + static_cast<size_t>(t0) * H, H, F, h + static_cast<size_t>(t0) * F + r);
-        });
+      int64_t u0, u1;
+      range(U1, tid, u0, u1);
+      for (int64_t u = u0; u < u1; ++u) {
+        const int j = static_cast<int>(u / nb1), blk = static_cast<int>(u % nb1);
+        const uint16_t* wg = slabs[j];
+        const uint16_t* wu = wg + static_cast<size_t>(F) * H;
+        const uint16_t* xj = x + static_cast<size_t>(row0[j]) * H;
+        for (int r = blk * 16; r < blk * 16 + 16; ++r)
+          by_token_chunks(m[j], [&](auto mt, int t0) {
+            gate_up_row<decltype(mt)::value>(wg + static_cast<size_t>(r) * H, wu + static_cast<size_t>(r) * H,
+                                             xj + static_cast<size_t>(t0) * H, H, F,
+                                             h + hoff[j] + static_cast<size_t>(t0) * F + r);
+          });
+      }
     });
     l->pool->run([&](int tid) {
-      const int r0 = static_cast<int>(static_cast<int64_t>(H) * tid / T);
-      const int r1 = static_cast<int>(static_cast<int64_t>(H) * (tid + 1) / T);
-      for (int r = r0; r < r1; ++r)
-        by_token_chunks(m, [&](auto mt, int t0) {
-          down_row<decltype(mt)::value>(wd + static_cast<size_t>(r) * F, h + static_cast<size_t>(t0) * F, H, F,
-                                        y + static_cast<size_t>(t0) * H + r);
-        });
+      int64_t u0, u1;
+      range(U2, tid, u0, u1);
+      for (int64_t u = u0; u < u1; ++u) {
+        const int j = static_cast<int>(u / nb2), blk = static_cast<int>(u % nb2);
+        const uint16_t* wd = slabs[j] + static_cast<size_t>(2) * F * H;
+        for (int r = blk * 16; r < blk * 16 + 16; ++r)
+          by_token_chunks(m[j], [&](auto mt, int t0) {
+            down_row<decltype(mt)::value>(wd + static_cast<size_t>(r) * F, h + hoff[j] + static_cast<size_t>(t0) * F,
+                                          H, F, y + static_cast<size_t>(row0[j] + t0) * H + r);
+          });
+      }
     });
   });
+}
+
+ps_status ps_host_expert_ffn(ps_host_lane l, const uint16_t* slab, int H, int F, const uint16_t* x, int m, float* y) {
+  const int32_t zero = 0;
+  return ps_host_expert_ffn_batch(l, 1, &slab, &m, &zero, H, F, x, y);
 }
 
 }  // extern "C"

@@ -59,15 +59,16 @@ constexpr int kSyncEntries = 64;                 // max entries per launch (sync
 constexpr int kCWarps = 8;                       // consumer warps
 constexpr int kThreads = (kCWarps + 2) * 32;     // + TMA producer warp + release signaler warp
 constexpr int kMailbox = 8;                      // consumer -> signaler queue of finished gate_up items
-constexpr int kBarBytes = 1024;                  // mbarriers + per-entry row table; keeps the ring 1 KiB aligned
+constexpr int kBarBytes = 2048;                  // mbarriers + per-entry tables; keeps the ring 1 KiB aligned
 constexpr int kMaxTokens = 64;                   // tokens per expert per launch (8 * NT, NT <= 8)
 constexpr int kHalf = 256;                       // TMA box width (cols)
 constexpr int kTileBytes = 16 * kHalf * 2;       // one (16-row m-tile, 256-col half) = 8 KiB
 constexpr int kStageBytes = 4 * kTileBytes;      // 32 KiB: MT m-tiles x (4 / MT) halves
 constexpr int kMaps = 3;                         // per slab: gate_up {256,16}, gate_up {256,32}, down {256,32}
 
-// smem header: full[8] | empty[8] | posted[kMailbox] | freed[kMailbox] | row0[64] | m[64] | mailbox slots
-static_assert(256 + 2 * kSyncEntries * 4 + kMailbox * 4 <= kBarBytes, "smem header");
+// smem header: full[8] | empty[8] | posted[kMailbox] | freed[kMailbox] | row0[64] | m[64] | mailbox slots |
+// active entries[64] | n_active
+static_assert(256 + 3 * kSyncEntries * 4 + kMailbox * 4 + 4 <= kBarBytes, "smem header");
 
 // NT = 8-token groups per expert, MT = 16-row m-tiles per stage (and per item). A stage
 // is always 32 KiB: MT = 2 -> 32 rows x 512 cols, MT = 4 -> 64 rows x 256 cols. Activation
@@ -92,9 +93,12 @@ struct DecodeParams {
   const CUtensorMap* maps;        // device map table, kMaps per slab: [Wg; Wu] as [2F, H] box {256, 16}
                                   //   and box {256, 32}; Wd as [H, F] box {256, 32}
   int map_idx[CAP];               // table index of entry i's slab
-  int n;                          // entries (experts with m_e > tok_base)
-  int gu_start[CAP + 1];          // prefix of gate_up items per entry (F / (8 MT) each)
-  int dn_start[CAP + 1];          // prefix of down items per entry (n_split * H / (16 MT) each)
+  int n;                          // entries (experts with host-side m_e > tok_base; the
+                                  // resident group is launched before the host knows the
+                                  // counts, so entries with device-side m_e = 0 are dropped
+                                  // in the kernel prologue: only active entries get items)
+  int gu_per;                     // gate_up items per entry (F / (8 MT))
+  int dn_per;                     // down items per entry (n_split * H / (16 MT))
   int expert[CAP];
   int H, F, k, n_split, kchunk, dn_tiles, tok_base;
   const int32_t* offsets;
@@ -112,34 +116,26 @@ struct Item {
   int i, r0, split, kbeg, kend;
 };
 
-__device__ __forceinline__ int find_prefix(const int* start, int n, int w) {
-  int lo = 0, hi = n - 1;
-  while (lo < hi) {  // largest i with start[i] <= w
-    const int mid = (lo + hi + 1) >> 1;
-    if (start[mid] <= w) lo = mid;
-    else hi = mid - 1;
-  }
-  return lo;
-}
-
 // gate_up items: 8*MT F rows (8*MT gate + 8*MT up weight rows) x all of H; down items:
-// 16*MT H rows x one split of F.
+// 16*MT H rows x one split of F. Items enumerate the ACTIVE entries act[0..n_act).
 template <int MT, class P>
-__device__ __forceinline__ Item item_at(const P& p, int idx) {
+__device__ __forceinline__ Item item_at(const P& p, const int* act, int n_act, int idx) {
   Item it;
-  const int gu_total = p.gu_start[p.n];
+  const int gu_total = n_act * p.gu_per;
   if (idx < gu_total) {
     it.down = false;
-    it.i = find_prefix(p.gu_start, p.n, idx);
-    it.r0 = (idx - p.gu_start[it.i]) * 8 * MT;
+    const int j = idx / p.gu_per;
+    it.i = act[j];
+    it.r0 = (idx - j * p.gu_per) * 8 * MT;
     it.split = it.r0 / p.kchunk;
     it.kbeg = 0;
     it.kend = p.H;
   } else {
     idx -= gu_total;
     it.down = true;
-    it.i = find_prefix(p.dn_start, p.n, idx);
-    const int local = idx - p.dn_start[it.i];
+    const int j = idx / p.dn_per;
+    it.i = act[j];
+    const int local = idx - j * p.dn_per;
     it.split = local / p.dn_tiles;
     it.r0 = (local % p.dn_tiles) * 16 * MT;
     it.kbeg = min(p.F, it.split * p.kchunk);
@@ -225,11 +221,12 @@ __global__ void __launch_bounds__(kThreads, 1) ffn_decode_kernel(const __grid_co
   int* s_row0 = reinterpret_cast<int*>(smem + 256);           // per-entry first row of this pass
   int* s_m = s_row0 + kSyncEntries;                           // per-entry rows of this pass (<= 8*NT)
   int* s_mb = s_m + kSyncEntries;                             // mailbox: counter slot of the finished item
+  int* s_act = s_mb + kMailbox;                               // active entries (device m_e > 0), in order
+  int* s_nact = s_act + kSyncEntries;
   uint8_t* ring = smem + kBarBytes;
   float* red = reinterpret_cast<float*>(ring + G::kStages * kStageBytes);  // [warp][mt][j][q][lane]
 
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
-  const int total = p.gu_start[p.n] + p.dn_start[p.n];
   if (threadIdx.x == 0) {
     for (int s = 0; s < G::kStages; ++s) {
       mbar_init(&full[s], 1);
@@ -250,6 +247,20 @@ __global__ void __launch_bounds__(kThreads, 1) ffn_decode_kernel(const __grid_co
   if (blockIdx.x == 0)  // counters of the next launch (other parity); this stream's previous launch is done
     for (int i = threadIdx.x; i < kSyncEntries * kMaxSplit; i += blockDim.x) p.sync_next[i] = 0;
   __syncthreads();
+  if (warp == 0) {  // compact the active entries (ballot + popc, order preserved)
+    int na = 0;
+    for (int i0 = 0; i0 < p.n; i0 += 32) {
+      const int i = i0 + lane;
+      const bool on = i < p.n && s_m[i] > 0;
+      const unsigned mask = __ballot_sync(0xffffffffu, on);
+      if (on) s_act[na + __popc(mask & ((1u << lane) - 1u))] = i;
+      na += __popc(mask);
+    }
+    if (lane == 0) *s_nact = na;
+  }
+  __syncthreads();
+  const int n_act = *s_nact;
+  const int total = n_act * (p.gu_per + p.dn_per);
 
   if (warp == kCWarps + 1) {
     // ---------------------------------------------------------------- signaler lane
@@ -258,7 +269,7 @@ __global__ void __launch_bounds__(kThreads, 1) ffn_decode_kernel(const __grid_co
     // gpu-scope fence + counter increment. The fence stalls only this lane, not the
     // consumer warps that feed the ring.
     if (lane != 0) return;
-    const int gu_total = p.gu_start[p.n];
+    const int gu_total = n_act * p.gu_per;
     const int mine = gu_total > static_cast<int>(blockIdx.x)
                          ? (gu_total - static_cast<int>(blockIdx.x) + gridDim.x - 1) / gridDim.x : 0;
     for (int q = 0; q < mine; ++q) {
@@ -286,7 +297,7 @@ __global__ void __launch_bounds__(kThreads, 1) ffn_decode_kernel(const __grid_co
     int ord = 0;
     for (int idx = blockIdx.x; idx < total; idx += gridDim.x, ++ord) {
       PS_TRACE(ord, 4);
-      const Item it = item_at<MT>(p, idx);
+      const Item it = item_at<MT>(p, s_act, n_act, idx);
       const CUtensorMap* maps = p.maps + kMaps * p.map_idx[it.i];
       for (int k0 = it.kbeg; k0 < it.kend; k0 += G::kCols, ++n) {
         const int s = n % G::kStages;
@@ -327,7 +338,7 @@ __global__ void __launch_bounds__(kThreads, 1) ffn_decode_kernel(const __grid_co
   int ord = 0, gu_done = 0;
   for (int idx = blockIdx.x; idx < total; idx += gridDim.x, ++ord) {
     if (threadIdx.x == 0) PS_TRACE(ord, 0);
-    const Item it = item_at<MT>(p, idx);
+    const Item it = item_at<MT>(p, s_act, n_act, idx);
     const int row0 = s_row0[it.i], m = s_m[it.i];
     const int slot = it.i * kMaxSplit + it.split;
     if (it.down) {
@@ -593,7 +604,7 @@ void launch(const DecodeParams<CAP>& p, cudaStream_t s) {
     PS_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&bps, ffn_decode_kernel<NT, MT, CAP>, kThreads, smem));
     require(bps >= 1, "ffn_decode_kernel: does not fit on an SM");
   }
-  const int total = p.gu_start[p.n] + p.dn_start[p.n];
+  const int total = p.n * (p.gu_per + p.dn_per);  // upper bound (entries with m_e = 0 are dropped on device)
   const int grid = std::min(total, bps * d.sms);
   cudaLaunchConfig_t cfg{};
   cfg.gridDim = dim3(grid);
@@ -621,15 +632,15 @@ void run_group(const ps_expert_group* group, int base, int count, const int32_t*
                float* y_part, size_t split_stride, cudaStream_t s) {
   DecodeParams<CAP> p;
   p.n = 0;
-  p.gu_start[0] = p.dn_start[0] = 0;
   p.H = sh.H;
   p.F = sh.F;
   p.k = sh.k;
   p.n_split = sh.n_split;
   p.kchunk = sh.kchunk;
   const int MT = mt_for(NT);
-  const int gu_items = (sh.F + 8 * MT - 1) / (8 * MT);
+  p.gu_per = (sh.F + 8 * MT - 1) / (8 * MT);
   p.dn_tiles = (sh.H + 16 * MT - 1) / (16 * MT);
+  p.dn_per = p.dn_tiles * sh.n_split;
   p.tok_base = tok_base;
   p.offsets = offsets;
   p.perm_src = perm_src;
@@ -642,8 +653,6 @@ void run_group(const ps_expert_group* group, int base, int count, const int32_t*
     if (counts_host[e] <= tok_base) continue;
     p.map_idx[p.n] = slab_map_index(group->slabs[i], sh.H, sh.F, s, &p.maps);
     p.expert[p.n] = e;
-    p.gu_start[p.n + 1] = p.gu_start[p.n] + gu_items;
-    p.dn_start[p.n + 1] = p.dn_start[p.n] + p.dn_tiles * sh.n_split;
     ++p.n;
   }
   if (p.n == 0) return;

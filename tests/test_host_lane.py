@@ -103,3 +103,31 @@ def test_host_lane_argument_errors():
         lib.ps_host_lane_destroy(lane)
     h = C.c_void_p()
     assert lib.ps_host_lane_create(0, C.byref(h)) == ps.capi.PS_EINVAL
+
+
+@needs_bf16
+@pytest.mark.parametrize("isa", ISAS)
+def test_host_expert_ffn_batch_equals_single_calls(isa):
+    """A layer's cpu_set in one batch call (rows [row0, row0+m) of shared x/y buffers)
+    gives bitwise the per-expert results."""
+    lib = ps.load()
+    H, F = 256, 384
+    ms, row0 = [3, 0, 17, 1], [0, 3, 3, 20]
+    slabs = [orc.or_init_slab(H, F, 2, 0, e) for e in range(4)]
+    x = orc.f32_to_bf16(np.random.default_rng(7).standard_normal((21, H)).astype(np.float32))
+    lane = _lane(4, isa)
+    try:
+        y = np.full((21, H), np.nan, np.float32)
+        arr = (C.c_void_p * 4)(*[s.ctypes.data for s in slabs])
+        m_a, r_a = np.array(ms, np.int32), np.array(row0, np.int32)
+        ps.check(lib.ps_host_expert_ffn_batch(lane, 4, arr, m_a.ctypes.data, r_a.ctypes.data, H, F, x.ctypes.data,
+                                              y.ctypes.data))
+        for j in range(4):
+            if ms[j] == 0:
+                continue
+            yj = np.empty((ms[j], H), np.float32)
+            ps.check(lib.ps_host_expert_ffn(lane, slabs[j].ctypes.data, H, F, x[row0[j]:].ctypes.data, ms[j],
+                                            yj.ctypes.data))
+            np.testing.assert_array_equal(y[row0[j]:row0[j] + ms[j]], yj)
+    finally:
+        lib.ps_host_lane_destroy(lane)
