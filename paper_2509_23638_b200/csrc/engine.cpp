@@ -330,12 +330,15 @@ struct ps_engine_s {
   std::vector<int64_t> cal_us;
   uint64_t slab_elems = 0;
   cudaStream_t sc = nullptr;  // compute stream
+  cudaStream_t s_d2h = nullptr;  // scheduling-point D2H (off the compute stream's critical path)
+  cudaEvent_t last_ffn_end = nullptr;  // end event of the last FFN enqueued (reused as a start mark)
   std::unique_ptr<ps::IoChannel> io;
 
   // expert placement
   std::vector<const uint16_t*> dev_slab;  // [L*E] resident pointer or null
   std::vector<const uint16_t*> host_slab; // [L*E] pinned host pointer or null
   std::vector<uint8_t> resident;          // [L*E]
+  std::vector<uint8_t> has_host;          // [L]: layer has an owned non-resident expert
   void* arena = nullptr;                  // resident HBM arena
   void* host_arena = nullptr;             // pinned host arena
   ps::Slot od_slot[2];
@@ -444,7 +447,9 @@ cudaEvent_t take_event(ps_engine_s& e) {
 cudaEvent_t take_job_event(ps_engine_s& e) {
   if (e.job_event_next == e.job_event_pool.size()) {
     cudaEvent_t ev;
-    PS_CUDA(cudaEventCreate(&ev));
+    // The I/O thread waits milliseconds on these (one expert copy): blocking sync, so it
+    // sleeps instead of spinning on a core the host expert lane could use.
+    PS_CUDA(cudaEventCreateWithFlags(&ev, cudaEventBlockingSync));
     e.job_event_pool.push_back(ev);
   }
   return e.job_event_pool[e.job_event_next++];
@@ -454,13 +459,20 @@ int group_of_layer(const ps_model_spec& s, int l) {
   return l < s.group_begin_middle ? PS_GROUP_INPUT : l < s.group_begin_output ? PS_GROUP_MIDDLE : PS_GROUP_OUTPUT;
 }
 
+// Timing events with timestamps serialise the stream front end (~3 us per record between
+// two kernels on B200, scripts/engine_timeline.py): callers pass the event that already
+// marks the launch point (`start`) instead of recording a new one, and the last FFN's end
+// event is reused as the combine's start.
 void ffn(ps_engine_s& e, const ps_expert_group& g, const int32_t* counts_host, int B, bool timed,
-         bool exact_counts = true) {
+         bool exact_counts = true, cudaEvent_t start = nullptr) {
   if (g.n == 0) return;
   cudaEvent_t a = nullptr, b = nullptr;
   if (timed) {
-    a = take_event(e);
-    PS_CUDA(cudaEventRecord(a, e.sc));
+    a = start;
+    if (!a) {
+      a = take_event(e);
+      PS_CUDA(cudaEventRecord(a, e.sc));
+    }
   }
   // Path choice per launch: the tcgen05 grouped GEMM once an expert has a full 128-row
   // M tile of tokens (prefill), the HBM-streaming GEMV otherwise (decode).
@@ -497,6 +509,7 @@ void ffn(ps_engine_s& e, const ps_expert_group& g, const int32_t* counts_host, i
   if (timed) {
     b = take_event(e);
     PS_CUDA(cudaEventRecord(b, e.sc));
+    e.last_ffn_end = b;
     FfnTiming t{a, b, 0.0, e.cur_layer, {}, {}};
     for (int i = 0; i < g.n; ++i)
       if (counts_host[g.experts[i]] > 0) {
@@ -664,21 +677,25 @@ void decode_step(ps_engine_s& e, const float* hidden, const uint8_t* follow, int
     const float* x = hidden + static_cast<size_t>(l) * B * H;
     e.cur_layer = l;
     LayerDev& ld = e.layer[l];
-    PhaseTiming ph{take_event(e), take_event(e), take_event(e), take_event(e)};
-    PS_CUDA(cudaEventRecord(ph.route0, e.sc));
+    // Layer start = the previous layer's combine end (nothing timed runs in between).
+    PhaseTiming ph{l > 0 ? e.phase_t.back().comb1 : take_event(e), nullptr, nullptr, nullptr};
+    if (l == 0) PS_CUDA(cudaEventRecord(ph.route0, e.sc));
+    e.last_ffn_end = nullptr;
     // --- K1 route (+fused bf16 cast, histogram) -------------------------------
     ps_status s = ps_route_topk(x, e.gate + static_cast<size_t>(l) * E * H, e.bias + static_cast<size_t>(l) * E,
                                 follow ? follow + static_cast<size_t>(l) * B : nullptr,
                                 l > 0 ? e.layer[l - 1].ids : nullptr, K, B, H, E, K, nullptr, ld.weights, ld.ids,
-                                e.counts_dev, e.x_bf16, e.sc);
+                                nullptr, e.x_bf16, e.sc);  // histogram: from K2's offsets on the host
     if (s != PS_OK) fail(s, ps_last_error());
     e.st.kernel_launches += 1;
     // --- K4 LLaPor: predicted histogram of layer l+1 -------------------------
     // Prefill chunks (B > 64 and >= 16 routed rows per expert on average) activate every
     // expert of the next layer with near certainty: the prediction is then the dense
     // histogram B*k/E per expert and the LLaPor launch is skipped (decode always runs it).
+    // The prediction only feeds e_next (non-resident experts of l+1): a fully resident
+    // next layer has no prefetch candidates whatever LLaPor says, so K4 is skipped there.
     const bool dense_next = e.prefill_mode && B * K >= 16 * E && l + 1 < L;
-    const bool predict = e.cfg.predictor && l + 1 < L && !dense_next;
+    const bool predict = e.cfg.predictor && l + 1 < L && !dense_next && e.has_host[l + 1];
     if (predict) {
       s = ps_llapor_forward(e.cfg.predictor, l + 1, x, ld.ids, K, ld.weights, B, K, nullptr, nullptr, e.pred_dev,
                             e.llapor_scratch, e.sc);
@@ -691,7 +708,7 @@ void decode_step(ps_engine_s& e, const float* hidden, const uint8_t* follow, int
     const int Ev = e.G * e.E_loc;  // owner-major virtual expert count under EP
     if (!e.ep) {
       if (e.S) {
-        s = ps_append_shared(ld.ids, ld.weights, B, K, E, e.S, e.ids_ext, e.w_ext, e.counts_dev, e.sc);
+        s = ps_append_shared(ld.ids, ld.weights, B, K, E, e.S, e.ids_ext, e.w_ext, nullptr, e.sc);
         if (s != PS_OK) fail(s, ps_last_error());
         e.st.kernel_launches += 1;
       }
@@ -699,12 +716,19 @@ void decode_step(ps_engine_s& e, const float* hidden, const uint8_t* follow, int
                      e.prefill_mode ? e.x_bf16 : nullptr, H, e.prefill_mode ? e.x_perm : nullptr, e.sc);
       if (s != PS_OK) fail(s, ps_last_error());
       e.st.kernel_launches += e.prefill_mode ? 2 : 1;
-      // counts | pred | offsets (| perm_src for the host lane) in one copy
+      // counts | pred | offsets (| perm_src for the host lane) in one copy, on the side
+      // stream: the compute stream goes straight on to the resident FFN while the copy
+      // engine brings the scheduling inputs to the host.
       const size_t n_sched = 3 * static_cast<size_t>(Et) + 1 + (e.lane ? static_cast<size_t>(B) * Kt : 0);
-      PS_CUDA(cudaMemcpyAsync(e.pinned_counts, e.sched_dev, sizeof(int32_t) * n_sched, cudaMemcpyDeviceToHost, e.sc));
+      ph.route1 = take_event(e);  // end of the scheduling-point kernels = start of the early FFN
+      PS_CUDA(cudaEventRecord(ph.route1, e.sc));
+      PS_CUDA(cudaStreamWaitEvent(e.s_d2h, ph.route1, 0));
+      PS_CUDA(cudaMemcpyAsync(e.pinned_counts, e.sched_dev, sizeof(int32_t) * n_sched, cudaMemcpyDeviceToHost,
+                              e.s_d2h));
       e.src = {e.offsets, e.perm_src, Kt, e.x_bf16, B * Kt, e.pinned_counts + 2 * Et};
       if (e.lane)  // the host lane gathers its rows from x
-        PS_CUDA(cudaMemcpyAsync(e.lane_x, e.x_bf16, sizeof(uint16_t) * B * H, cudaMemcpyDeviceToHost, e.sc));
+        PS_CUDA(cudaMemcpyAsync(e.lane_x, e.x_bf16, sizeof(uint16_t) * B * H, cudaMemcpyDeviceToHost, e.s_d2h));
+      PS_CUDA(cudaEventRecord(e.ev_routed, e.s_d2h));
     } else {
       // EP dispatch, part 1: owner-major permute + gather of this rank's routed rows,
       // then the (rows, predicted tokens) counts exchange with every owner.
@@ -721,8 +745,11 @@ void decode_step(ps_engine_s& e, const float* hidden, const uint8_t* follow, int
       PS_CUDA(cudaMemcpyAsync(e.ep_host + Ev + 1, e.ep_cnt_recv, sizeof(int32_t) * e.G * 2 * e.E_loc,
                               cudaMemcpyDeviceToHost, e.sc));
     }
-    PS_CUDA(cudaEventRecord(e.ev_routed, e.sc));
-    PS_CUDA(cudaEventRecord(ph.route1, e.sc));
+    if (e.ep) PS_CUDA(cudaEventRecord(e.ev_routed, e.sc));
+    if (!ph.route1) {
+      ph.route1 = take_event(e);
+      PS_CUDA(cudaEventRecord(ph.route1, e.sc));
+    }
 
     // --- resident experts (R6). Decode: start now, before the host knows the counts —
     // the kernels read per-expert row counts from the device offsets, the grid is sized
@@ -743,7 +770,7 @@ void decode_step(ps_engine_s& e, const float* hidden, const uint8_t* follow, int
     }
     const size_t resident_timing = e.ffn_t.size();
     const bool early = !e.prefill_mode && !e.ep;
-    if (early) ffn(e, grp, worst.data(), B, true, false);
+    if (early) ffn(e, grp, worst.data(), B, true, false, ph.route1);
 
     // --- R2: resolve the previous layer's prefetch batch at this scheduling point
     {
@@ -765,7 +792,8 @@ void decode_step(ps_engine_s& e, const float* hidden, const uint8_t* follow, int
     // Wait for the routing result on the host (the only per-layer host sync).
     PS_CUDA(cudaEventSynchronize(e.ev_routed));
     if (!e.ep) {
-      std::memcpy(counts_l.data(), e.pinned_counts, sizeof(int32_t) * Et);
+      const int32_t* off_h = e.pinned_counts + 2 * Et;  // aggregate_layer_loads = diff of K2's offsets
+      for (int ex = 0; ex < Et; ++ex) counts_l[ex] = off_h[ex + 1] - off_h[ex];
       if (predict) std::memcpy(pred_l.data(), e.pinned_counts + Et, sizeof(int32_t) * E);
       else std::fill(pred_l.begin(), pred_l.end(), dense_next ? (B * K) / E : 0);
     } else {
@@ -895,7 +923,7 @@ void decode_step(ps_engine_s& e, const float* hidden, const uint8_t* follow, int
       one.n = 1;
       one.experts[0] = job->expert;
       one.slabs[0] = static_cast<const uint16_t*>(job->dst);
-      ffn(e, one, counts_l.data(), B, true);
+      ffn(e, one, counts_l.data(), B, true, true, p.after);
       release_slot_after_compute(e, job->slot);
       e.st.ondemand_loads++;
     }
@@ -903,6 +931,7 @@ void decode_step(ps_engine_s& e, const float* hidden, const uint8_t* follow, int
     // Host-lane results (R5) -> y_part rows (split 0; other splits zero), then combine.
     if (!e.cpu_jobs.empty()) {
       e.lane_drv->wait();
+      e.last_ffn_end = nullptr;  // copies follow the last FFN
       const size_t total_rows = static_cast<size_t>(e.src.rows);
       {  // one batch per layer: T = beta*sum(m) + n*C, so (mean tokens, mean time) per
          // expert is one sample of cpu_cost(m) = beta*m + C for fit_cost_params
@@ -930,7 +959,11 @@ void decode_step(ps_engine_s& e, const float* hidden, const uint8_t* follow, int
     }
 
     // --- combine -> y_l ------------------------------------------------------------
-    PS_CUDA(cudaEventRecord(ph.comb0, e.sc));
+    ph.comb0 = e.last_ffn_end;  // nothing enqueued since the last FFN ended (else a new mark)
+    if (!ph.comb0) {
+      ph.comb0 = take_event(e);
+      PS_CUDA(cudaEventRecord(ph.comb0, e.sc));
+    }
     if (!e.ep) {
       s = ps_combine(e.y_part, e.step_split, e.inv, e.S ? e.ids_ext : ld.ids, e.S ? e.w_ext : ld.weights, B, Kt, Et, H,
                      y + static_cast<size_t>(l) * B * H, e.sc);
@@ -938,6 +971,7 @@ void decode_step(ps_engine_s& e, const float* hidden, const uint8_t* follow, int
       s = ep_combine_rows(e, B, ld, y + static_cast<size_t>(l) * B * H);
     }
     if (s != PS_OK) fail(s, ps_last_error());
+    ph.comb1 = take_event(e);
     PS_CUDA(cudaEventRecord(ph.comb1, e.sc));
     e.phase_t.push_back(ph);
     e.st.kernel_launches += 1;
@@ -1090,6 +1124,7 @@ void create_engine(const ps_engine_config& cfg, ps_engine_s& e) {
   if (ps_cost_params_validate(&e.cfg.cost) != PS_OK) fail(PS_EINVAL, ps_last_error());
 
   PS_CUDA(cudaStreamCreateWithFlags(&e.sc, cudaStreamNonBlocking));
+  PS_CUDA(cudaStreamCreateWithFlags(&e.s_d2h, cudaStreamNonBlocking));
   e.io = std::make_unique<IoChannel>(cfg.device, 2);
 
   // Expert parallelism: this rank owns experts e % G == rank of every layer.
@@ -1116,6 +1151,11 @@ void create_engine(const ps_engine_config& cfg, ps_engine_s& e) {
   for (int ex = 0; ex < e.E; ++ex) n_owned += owned(ex) ? e.L : 0;
   require(n_res * sp.expert_bytes <= cfg.budget_bytes, "engine: resident set exceeds the HBM budget");
   const size_t n_host = n_owned - n_res;
+  e.has_host.assign(e.L, 0);
+  for (int l = 0; l < e.L; ++l)
+    for (int ex = 0; ex < e.E; ++ex)
+      // under EP every rank's prediction feeds every owner's plan (counts exchange)
+      if (e.ep || (owned(ex) && !e.resident[static_cast<size_t>(l) * e.E + ex])) e.has_host[l] = 1;
 
   e.dev_slab.assign(LE, nullptr);
   e.host_slab.assign(LE, nullptr);
@@ -1277,6 +1317,7 @@ void destroy_engine(ps_engine_s& e) {
   for (void* p : {(void*)e.lane_x, (void*)e.lane_xrows, (void*)e.lane_yrows})
     if (p) cudaFreeHost(p);
   if (e.sc) cudaStreamSynchronize(e.sc);
+  if (e.s_d2h) cudaStreamSynchronize(e.s_d2h);
   for (auto& ld : e.layer) {
     cudaFree(ld.weights);
     cudaFree(ld.ids);
@@ -1306,6 +1347,7 @@ void destroy_engine(ps_engine_s& e) {
   for (cudaEvent_t ev : {e.ev_routed, e.ev_step0, e.ev_step1})
     if (ev) cudaEventDestroy(ev);
   if (e.sc) cudaStreamDestroy(e.sc);
+  if (e.s_d2h) cudaStreamDestroy(e.s_d2h);
 }
 
 }  // namespace

@@ -151,11 +151,21 @@ __device__ __forceinline__ int split_items(const P& p, int s) {
   return (e - b + 8 * MT - 1) / (8 * MT);
 }
 
-__device__ __forceinline__ void tma_2d(void* dst, const CUtensorMap* map, uint64_t* bar, int c0, int c1) {
+// Weights are streamed exactly once per launch: load them with an L2 evict-first policy
+// so they do not push the small per-layer tensors (router gate, hidden states, ids,
+// LLaPor components) out of L2 between layers.
+__device__ __forceinline__ uint64_t evict_first_policy() {
+  uint64_t pol;
+  asm volatile("createpolicy.fractional.L2::evict_first.b64 %0, 1.0;" : "=l"(pol));
+  return pol;
+}
+
+__device__ __forceinline__ void tma_2d(void* dst, const CUtensorMap* map, uint64_t* bar, int c0, int c1,
+                                       uint64_t policy) {
   asm volatile(
-      "cp.async.bulk.tensor.2d.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1, {%2, %3}], [%4];" ::"r"(
-          smem_u32(dst)),
-      "l"(map), "r"(c0), "r"(c1), "r"(smem_u32(bar))
+      "cp.async.bulk.tensor.2d.shared::cluster.global.mbarrier::complete_tx::bytes.L2::cache_hint [%0], [%1, {%2, "
+      "%3}], [%4], %5;" ::"r"(smem_u32(dst)),
+      "l"(map), "r"(c0), "r"(c1), "r"(smem_u32(bar)), "l"(policy)
       : "memory");
 }
 
@@ -293,6 +303,7 @@ __global__ void __launch_bounds__(kThreads, 1) ffn_decode_kernel(const __grid_co
     }
     __syncwarp();
     if (lane != 0) return;
+    const uint64_t pol = evict_first_policy();
     uint32_t n = 0;
     int ord = 0;
     for (int idx = blockIdx.x; idx < total; idx += gridDim.x, ++ord) {
@@ -312,11 +323,11 @@ __global__ void __launch_bounds__(kThreads, 1) ffn_decode_kernel(const __grid_co
           const int c = k0 + hf * kHalf;
           if (!it.down) {  // m-tiles [0, MT/2): gate rows; [MT/2, MT): up rows
             const CUtensorMap* gm = MT == 2 ? &maps[0] : &maps[1];
-            tma_2d(d, gm, &full[s], c, it.r0);
-            tma_2d(d + (MT / 2) * kTileBytes, gm, &full[s], c, p.F + it.r0);
+            tma_2d(d, gm, &full[s], c, it.r0, pol);
+            tma_2d(d + (MT / 2) * kTileBytes, gm, &full[s], c, p.F + it.r0, pol);
           } else {         // MT m-tiles of W_down rows, boxes of 32 rows
 #pragma unroll
-            for (int b = 0; b < MT / 2; ++b) tma_2d(d + 2 * b * kTileBytes, &maps[2], &full[s], c, it.r0 + 32 * b);
+            for (int b = 0; b < MT / 2; ++b) tma_2d(d + 2 * b * kTileBytes, &maps[2], &full[s], c, it.r0 + 32 * b, pol);
           }
         }
       }

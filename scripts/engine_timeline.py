@@ -23,6 +23,8 @@ def main():
     ap.add_argument("--model", default="mixtral")
     ap.add_argument("--batch", type=int, default=16)
     ap.add_argument("--layers", type=int, default=6)
+    ap.add_argument("--host-experts", type=int, default=0,
+                    help="last N experts of every layer live in pinned host DRAM (K4 + loads active)")
     args = ap.parse_args()
     spec = ps.spec_preset(args.model)
     spec = ps.desk_scale(spec, args.layers, spec.experts_per_layer, spec.hidden_dim)
@@ -34,7 +36,7 @@ def main():
     pred = C.c_void_p()
     ps.check(lib.ps_llapor_random(C.byref(spec), 256, 512, 32, 48, 3, C.byref(pred)))
     e = eng.Engine(spec, gen, max_batch=B, weight_seed=1, gate=gate, budget_bytes=L * E * spec.expert_bytes,
-                   resident=[(l, x) for l in range(L) for x in range(E)], predictor=pred)
+                   resident=[(l, x) for l in range(L) for x in range(E - args.host_experts)], predictor=pred)
     g = torch.Generator(device="cuda").manual_seed(1)
     h = torch.randn(L, B, H, device="cuda", generator=g)
     h /= h.norm(dim=-1, keepdim=True)
