@@ -277,6 +277,17 @@ ps_status ps_route_topk(const float* x, const float* gate, const float* bias,
                         int H, int E, int k, float* logits, float* weights, int32_t* ids,
                         int32_t* counts, uint16_t* x_bf16, void* stream);
 
+/* K1 + K2 index pass in ONE launch for decode batches (1 <= B <= 64): the route CTAs as
+ * in ps_route_topk (no histogram: counts = diff of offsets), then the last CTA to finish
+ * runs the counting-sort permute of ps_permute over all B*k ids (bit-identical outputs).
+ * workspace: one int32 on the device, zero before the first call (the kernel leaves it
+ * zero); one workspace per stream. */
+ps_status ps_route_permute(const float* x, const float* gate, const float* bias,
+                           const uint8_t* follow, const int32_t* prev_ids, int prev_k, int B,
+                           int H, int E, int k, float* weights, int32_t* ids, uint16_t* x_bf16,
+                           int32_t* offsets, int32_t* perm_src, int32_t* inv, int32_t* workspace,
+                           void* stream);
+
 /* K2 — counting-sort permute: rows ordered (expert asc, token asc, slot asc).
  *   offsets [E+1], perm_src [B*k] (= token*k+slot), inv [B*k].
  *   x [B,H] bf16 + x_perm [B*k,H] bf16: optional gather (both nullable). */

@@ -167,6 +167,8 @@ _SIGS = {
     "ps_plan_residency": (C.c_int, [_P, C.c_int, C.c_int, C.c_uint64, C.c_uint64, _P, C.POINTER(C.c_int)]),
     "ps_route_topk": (C.c_int, [_P, _P, _P, _P, _P, C.c_int, C.c_int, C.c_int, C.c_int, C.c_int,
                                 _P, _P, _P, _P, _P, _P]),
+    "ps_route_permute": (C.c_int, [_P, _P, _P, _P, _P, C.c_int, C.c_int, C.c_int, C.c_int, C.c_int,
+                                   _P, _P, _P, _P, _P, _P, _P, _P]),
     "ps_permute": (C.c_int, [_P, C.c_int, C.c_int, C.c_int, _P, _P, _P, _P, C.c_int, _P, _P]),
     "ps_combine": (C.c_int, [_P, C.c_int, _P, _P, _P, C.c_int, C.c_int, C.c_int, C.c_int, _P, _P]),
     "ps_fnv1a64": (C.c_uint64, [_P, C.c_size_t]),

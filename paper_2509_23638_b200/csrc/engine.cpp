@@ -355,6 +355,7 @@ struct ps_engine_s {
   // Scheduling-point block, one device allocation mirrored in pinned host memory so the
   // per-layer D2H is ONE copy: counts [Et] | pred [Et] | offsets [Et+1] | perm_src [maxB*Kt]
   int32_t* sched_dev = nullptr;
+  int32_t* route_ws = nullptr;       // ticket counter of the fused route+permute launch
   int32_t* pinned_counts = nullptr;  // host mirror of sched_dev
   uint16_t* x_bf16 = nullptr;
   uint16_t* x_perm = nullptr;        // [maxB*k, H] bf16 (prefill gather)
@@ -677,15 +678,25 @@ void decode_step(ps_engine_s& e, const float* hidden, const uint8_t* follow, int
     const float* x = hidden + static_cast<size_t>(l) * B * H;
     e.cur_layer = l;
     LayerDev& ld = e.layer[l];
-    // Layer start = the previous layer's combine end (nothing timed runs in between).
-    PhaseTiming ph{l > 0 ? e.phase_t.back().comb1 : take_event(e), nullptr, nullptr, nullptr};
-    if (l == 0) PS_CUDA(cudaEventRecord(ph.route0, e.sc));
+    // Layer start: a fresh mark (the previous combine's end would also count the host's
+    // inter-layer latency, which must not leak into the calibrated t_attn).
+    PhaseTiming ph{take_event(e), nullptr, nullptr, nullptr};
+    PS_CUDA(cudaEventRecord(ph.route0, e.sc));
     e.last_ffn_end = nullptr;
-    // --- K1 route (+fused bf16 cast, histogram) -------------------------------
-    ps_status s = ps_route_topk(x, e.gate + static_cast<size_t>(l) * E * H, e.bias + static_cast<size_t>(l) * E,
-                                follow ? follow + static_cast<size_t>(l) * B : nullptr,
-                                l > 0 ? e.layer[l - 1].ids : nullptr, K, B, H, E, K, nullptr, ld.weights, ld.ids,
-                                nullptr, e.x_bf16, e.sc);  // histogram: from K2's offsets on the host
+    // --- K1 route (+fused bf16 cast) ------------------------------------------------
+    // Decode without shared experts / EP: K1 and K2's index pass in one launch (the last
+    // route CTA permutes). Otherwise K1 here and K2 below. Histogram: diff of K2 offsets.
+    const bool fused_perm = !e.ep && e.S == 0 && !e.prefill_mode;
+    ps_status s;
+    if (fused_perm)
+      s = ps_route_permute(x, e.gate + static_cast<size_t>(l) * E * H, e.bias + static_cast<size_t>(l) * E,
+                           follow ? follow + static_cast<size_t>(l) * B : nullptr, l > 0 ? e.layer[l - 1].ids : nullptr,
+                           K, B, H, E, K, ld.weights, ld.ids, e.x_bf16, e.offsets, e.perm_src, e.inv, e.route_ws,
+                           e.sc);
+    else
+      s = ps_route_topk(x, e.gate + static_cast<size_t>(l) * E * H, e.bias + static_cast<size_t>(l) * E,
+                        follow ? follow + static_cast<size_t>(l) * B : nullptr, l > 0 ? e.layer[l - 1].ids : nullptr, K,
+                        B, H, E, K, nullptr, ld.weights, ld.ids, nullptr, e.x_bf16, e.sc);
     if (s != PS_OK) fail(s, ps_last_error());
     e.st.kernel_launches += 1;
     // --- K4 LLaPor: predicted histogram of layer l+1 -------------------------
@@ -712,10 +723,12 @@ void decode_step(ps_engine_s& e, const float* hidden, const uint8_t* follow, int
         if (s != PS_OK) fail(s, ps_last_error());
         e.st.kernel_launches += 1;
       }
-      s = ps_permute(e.S ? e.ids_ext : ld.ids, B, Kt, Et, e.offsets, e.perm_src, e.inv,
-                     e.prefill_mode ? e.x_bf16 : nullptr, H, e.prefill_mode ? e.x_perm : nullptr, e.sc);
-      if (s != PS_OK) fail(s, ps_last_error());
-      e.st.kernel_launches += e.prefill_mode ? 2 : 1;
+      if (!fused_perm) {
+        s = ps_permute(e.S ? e.ids_ext : ld.ids, B, Kt, Et, e.offsets, e.perm_src, e.inv,
+                       e.prefill_mode ? e.x_bf16 : nullptr, H, e.prefill_mode ? e.x_perm : nullptr, e.sc);
+        if (s != PS_OK) fail(s, ps_last_error());
+        e.st.kernel_launches += e.prefill_mode ? 2 : 1;
+      }
       // counts | pred | offsets (| perm_src for the host lane) in one copy, on the side
       // stream: the compute stream goes straight on to the resident FFN while the copy
       // engine brings the scheduling inputs to the host.
@@ -1203,6 +1216,14 @@ void create_engine(const ps_engine_config& cfg, ps_engine_s& e) {
     PS_CUDA(cudaMalloc(&s.dev, sp.expert_bytes));
     PS_CUDA(cudaEventCreateWithFlags(&s.free_ev, cudaEventDisableTiming));
   }
+  // Prefetch slots for two live target layers (R8 cap per layer) up front: a cudaMalloc
+  // of an expert-sized buffer inside a step costs milliseconds of host time.
+  for (size_t i = 0; i < std::min<size_t>(2 * static_cast<size_t>(e.cfg.prefetch_slots), n_host); ++i) {
+    auto s = std::make_unique<Slot>();
+    PS_CUDA(cudaMalloc(&s->dev, sp.expert_bytes));
+    PS_CUDA(cudaEventCreateWithFlags(&s->free_ev, cudaEventDisableTiming));
+    e.pf_pool.push_back(std::move(s));
+  }
 
   // Router bias: -zipf_g * ln(e+1) per layer (workload.cpp:180-181).
   PS_CUDA(cudaMalloc(&e.gate, sizeof(float) * e.L * e.E * e.H));
@@ -1227,9 +1248,11 @@ void create_engine(const ps_engine_config& cfg, ps_engine_s& e) {
   }
   const size_t n_sched = 3 * static_cast<size_t>(e.Et) + 1 + rows_t;
   PS_CUDA(cudaMalloc(&e.sched_dev, sizeof(int32_t) * n_sched));
-  PS_CUDA(cudaMemset(e.sched_dev, 0, sizeof(int32_t) * n_sched));
+  PS_CUDA(cudaMemsetAsync(e.sched_dev, 0, sizeof(int32_t) * n_sched, e.sc));
   PS_CUDA(cudaHostAlloc(&e.pinned_counts, sizeof(int32_t) * n_sched, cudaHostAllocDefault));
   e.counts_dev = e.sched_dev;
+  PS_CUDA(cudaMalloc(&e.route_ws, sizeof(int32_t)));
+  PS_CUDA(cudaMemsetAsync(e.route_ws, 0, sizeof(int32_t), e.sc));
   e.pred_dev = e.sched_dev + e.Et;
   e.offsets = e.sched_dev + 2 * e.Et;
   e.perm_src = e.sched_dev + 3 * e.Et + 1;
@@ -1280,7 +1303,7 @@ void create_engine(const ps_engine_config& cfg, ps_engine_s& e) {
     PS_CUDA(cudaHostAlloc(&e.lane_yrows, sizeof(float) * rows_t * e.H, cudaHostAllocDefault));
     e.lane_drv = std::make_unique<LaneDriver>(e.lane, e.H, e.F);
     // cpu_cost = beta*m + C (cost_model.cpp:34-37) measured on this host: the lane on a
-    // host-resident expert slab at m = 1 and m = min(16, maxB), best of 3 each.
+    // host-resident expert slab at m = 1 and m = m2, best of 3 each.
     const uint16_t* probe = nullptr;
     for (const uint16_t* p : e.host_slab)
       if (p) {
@@ -1299,7 +1322,9 @@ void create_engine(const ps_engine_config& cfg, ps_engine_s& e) {
         }
         return t;
       };
-      const int m2 = std::min<int>(16, static_cast<int>(rows_t));
+      // m2 up to 64 tokens: prefill-sized engines see the lane leave its DRAM-bound
+      // regime (AMX compute grows with ceil(m/16)) and price large m_e accordingly.
+      const int m2 = std::min<int>(std::max(16, std::min(64, e.maxB)), static_cast<int>(rows_t));
       const double t1 = best(1), t2 = m2 > 1 ? best(m2) : t1;
       const double beta = m2 > 1 ? std::max(0.0, (t2 - t1) / (m2 - 1)) : 0.0;
       e.cfg.cost.beta = std::max(beta, 1e-3);
@@ -1322,7 +1347,7 @@ void destroy_engine(ps_engine_s& e) {
     cudaFree(ld.weights);
     cudaFree(ld.ids);
   }
-  for (void* p : {(void*)e.arena, (void*)e.gate, (void*)e.bias, (void*)e.sched_dev,
+  for (void* p : {(void*)e.arena, (void*)e.gate, (void*)e.bias, (void*)e.sched_dev, (void*)e.route_ws,
                   (void*)e.x_bf16, (void*)e.x_perm, (void*)e.inv, (void*)e.hbuf,
                   (void*)e.y_part, e.llapor_scratch, (void*)e.in_hidden, (void*)e.in_follow, (void*)e.out_y,
                   (void*)e.out_ids, (void*)e.ep_vids, (void*)e.ep_off_v, (void*)e.ep_perm_v, (void*)e.ep_inv_v,
@@ -1414,6 +1439,10 @@ ps_status ps_engine_reset_stats(ps_engine e) {
   return guarded([&] {
     e->st = ps_engine_stats{};
     e->st.cost = e->cfg.cost;
+    // calibration samples are "since the last stats reset" (ps_engine_calibrate)
+    e->copy_ms_total = e->copies = e->route_ms_total_cal = e->ffn_expert_ms_total = e->ffn_experts = 0;
+    e->cal_m.clear();
+    e->cal_us.clear();
   });
 }
 
@@ -1449,20 +1478,15 @@ ps_status ps_engine_calibrate(ps_engine e, ps_cost_params* out) {
     if (e->ffn_experts > 0) c.t_g = std::max<int64_t>(0, std::llround(1000.0 * e->ffn_expert_ms_total / e->ffn_experts));
     if (e->st.layers > 0) c.t_attn = std::llround(1000.0 * e->route_ms_total_cal / static_cast<double>(e->st.layers));
     if (c.t_g >= c.t_io) c.t_g = c.t_io - 1;  // CostParams invariant t_g < t_io (cost_model.cpp:16)
-    // Host lane: cpu_cost = beta*m + C from the measured (tokens, us) samples
-    // (fit_cost_params, cost_model.cpp:45-72) when they span >= 2 token counts.
+    // Host lane: cpu_cost = beta*m + C. The lane is DRAM-bound, so the in-step samples
+    // (per-layer batches, mean tokens vs mean time per expert, under PCIe contention)
+    // span too few token counts for a stable slope: beta stays the create-time probe's
+    // (m = 1 vs 16 in isolation) and C is refit as the median residual of the samples.
     if (!e->cal_m.empty()) {
-      const bool spread = std::any_of(e->cal_m.begin(), e->cal_m.end(), [&](int m) { return m != e->cal_m[0]; });
-      double beta = c.beta, startup = 0, r2 = 0;
-      if (spread && ps_fit_cost_params(e->cal_m.data(), e->cal_us.data(), static_cast<int>(e->cal_m.size()), &beta,
-                                       &startup, &r2) == PS_OK && beta > 0) {
-        c.beta = beta;
-        c.startup = std::max<int64_t>(0, ps_to_ticks(startup));
-      } else {
-        double mean = 0;
-        for (size_t i = 0; i < e->cal_m.size(); ++i) mean += e->cal_us[i] - c.beta * e->cal_m[i];
-        c.startup = std::max<int64_t>(0, ps_to_ticks(mean / e->cal_m.size()));
-      }
+      std::vector<double> res;
+      for (size_t i = 0; i < e->cal_m.size(); ++i) res.push_back(e->cal_us[i] - c.beta * e->cal_m[i]);
+      std::nth_element(res.begin(), res.begin() + res.size() / 2, res.end());
+      c.startup = std::max<int64_t>(0, ps_to_ticks(res[res.size() / 2]));
     }
     if (ps_cost_params_validate(&c) != PS_OK) fail(PS_EINVAL, ps_last_error());
     e->cfg.cost = c;

@@ -10,6 +10,7 @@
 // lower index first), exactly what topk_indices does on the same numbers, so the
 // returned ids are bit-exact against topk_indices(weights) (tests/test_gpu_route.py).
 #include "device_common.cuh"
+#include "permute_device.cuh"
 
 namespace ps {
 namespace {
@@ -19,19 +20,87 @@ constexpr int kMaxE = 256;
 constexpr int kMaxK = 16;
 constexpr int kETile = 8;
 
+// Per-token tail of the router (one warp): kappa override, softmax, top-k, histogram.
+__device__ __forceinline__ void finish_token_impl(int warp, int b0, float* lg, const uint8_t* __restrict__ follow,
+                                                  const int32_t* __restrict__ prev_ids, int prev_k, int E, int k,
+                                                  float* __restrict__ logits_out, float* __restrict__ weights_out,
+                                                  int32_t* __restrict__ ids_out, int32_t* __restrict__ counts) {
+  const int lane = threadIdx.x & 31;
+  const int b = b0 + warp;
+
+  // kappa-follow override: logits[(prev_top1+1) % E] = max + 1 (workload.cpp:183-188).
+  if (follow && prev_ids && follow[b]) {
+    float m = -INFINITY;
+    for (int e = lane; e < E; e += 32) m = fmaxf(m, lg[e]);
+    m = warp_max(m);
+    const int target = (prev_ids[static_cast<size_t>(b) * prev_k] + 1) % E;
+    __syncwarp();
+    if (lane == 0) lg[target] = m + 1.0f;
+    __syncwarp();
+  }
+
+  // Softmax (workload.cpp:190-195).
+  float m = -INFINITY;
+  for (int e = lane; e < E; e += 32) m = fmaxf(m, lg[e]);
+  m = warp_max(m);
+  float z = 0.f;
+  for (int e = lane; e < E; e += 32) z += expf(lg[e] - m);
+  z = warp_sum(z);
+  const float inv_z = 1.0f / z;
+  float w_local[kMaxE / 32];
+#pragma unroll
+  for (int i = 0; i < kMaxE / 32; ++i) {
+    const int e = lane + 32 * i;
+    w_local[i] = e < E ? expf(lg[e] - m) * inv_z : -INFINITY;
+    if (e < E) {
+      if (logits_out) logits_out[static_cast<size_t>(b) * E + e] = lg[e];
+      if (weights_out) weights_out[static_cast<size_t>(b) * E + e] = w_local[i];
+    }
+  }
+
+  // Top-k over the weights: k rounds of warp arg-max (ties -> lower index).
+  for (int r = 0; r < k; ++r) {
+    float bv = -INFINITY;
+    int bi = 0x7fffffff;
+#pragma unroll
+    for (int i = 0; i < kMaxE / 32; ++i) {
+      const int e = lane + 32 * i;
+      if (e < E && (w_local[i] > bv || (w_local[i] == bv && e < bi))) {
+        bv = w_local[i];
+        bi = e;
+      }
+    }
+    warp_argmax(bv, bi);
+    if (lane == 0) {
+      ids_out[static_cast<size_t>(b) * k + r] = bi;
+      if (counts) atomicAdd(counts + bi, 1);
+    }
+#pragma unroll
+    for (int i = 0; i < kMaxE / 32; ++i)
+      if (lane + 32 * i == bi) w_local[i] = -INFINITY;  // remove from later rounds
+  }
+}
+
 // One CTA per TB tokens: the 8 warps split H (latency: a Mixtral token needs 4 float4
 // steps per lane instead of 32) and every gate float4 loaded is applied to all TB
 // tokens (TB = 1 for decode batches, 8 for prefill chunks: 8x less L2 gate traffic).
 // Per-warp partial logits are summed in shared memory in fixed warp order
 // (deterministic and independent of TB); warp t then finishes token t: kappa override,
-// softmax, top-k, histogram.
-template <int TB>
+// softmax, top-k, histogram. kFused: the last CTA also runs the K2 index pass.
+struct FusedPermute {  // K2 index pass run by the last CTA of a decode route launch
+  int32_t* offsets;
+  int32_t* perm_src;
+  int32_t* inv;
+  int* done;  // launch ticket counter (zero between launches; the last CTA resets it)
+};
+
+template <int TB, bool kFused>
 __global__ void __launch_bounds__(kWarps * 32)
 route_kernel(const float* __restrict__ x, const float* __restrict__ gate, const float* __restrict__ bias,
              const uint8_t* __restrict__ follow, const int32_t* __restrict__ prev_ids, int prev_k,
              int B, int H, int E, int k, float sqrt_h, float* __restrict__ logits_out,
              float* __restrict__ weights_out, int32_t* __restrict__ ids_out,
-             int32_t* __restrict__ counts, uint16_t* __restrict__ x_bf16) {
+             int32_t* __restrict__ counts, uint16_t* __restrict__ x_bf16, FusedPermute fp) {
   __shared__ float s_part[kWarps][TB][kMaxE];
   __shared__ float s_logit[TB][kMaxE];
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
@@ -122,60 +191,22 @@ route_kernel(const float* __restrict__ x, const float* __restrict__ gate, const 
     s_logit[t][e] = sum * sqrt_h + (bias ? bias[e] : 0.f);
   }
   __syncthreads();
-  if (warp >= nt) return;
-  const int b = b0 + warp;
-  float* lg = s_logit[warp];
-
-  // kappa-follow override: logits[(prev_top1+1) % E] = max + 1 (workload.cpp:183-188).
-  if (follow && prev_ids && follow[b]) {
-    float m = -INFINITY;
-    for (int e = lane; e < E; e += 32) m = fmaxf(m, lg[e]);
-    m = warp_max(m);
-    const int target = (prev_ids[static_cast<size_t>(b) * prev_k] + 1) % E;
-    __syncwarp();
-    if (lane == 0) lg[target] = m + 1.0f;
-    __syncwarp();
-  }
-
-  // Softmax (workload.cpp:190-195).
-  float m = -INFINITY;
-  for (int e = lane; e < E; e += 32) m = fmaxf(m, lg[e]);
-  m = warp_max(m);
-  float z = 0.f;
-  for (int e = lane; e < E; e += 32) z += expf(lg[e] - m);
-  z = warp_sum(z);
-  const float inv_z = 1.0f / z;
-  float w_local[kMaxE / 32];
-#pragma unroll
-  for (int i = 0; i < kMaxE / 32; ++i) {
-    const int e = lane + 32 * i;
-    w_local[i] = e < E ? expf(lg[e] - m) * inv_z : -INFINITY;
-    if (e < E) {
-      if (logits_out) logits_out[static_cast<size_t>(b) * E + e] = lg[e];
-      if (weights_out) weights_out[static_cast<size_t>(b) * E + e] = w_local[i];
-    }
-  }
-
-  // Top-k over the weights: k rounds of warp arg-max (ties -> lower index).
-  for (int r = 0; r < k; ++r) {
-    float bv = -INFINITY;
-    int bi = 0x7fffffff;
-#pragma unroll
-    for (int i = 0; i < kMaxE / 32; ++i) {
-      const int e = lane + 32 * i;
-      if (e < E && (w_local[i] > bv || (w_local[i] == bv && e < bi))) {
-        bv = w_local[i];
-        bi = e;
-      }
-    }
-    warp_argmax(bv, bi);
-    if (lane == 0) {
-      ids_out[static_cast<size_t>(b) * k + r] = bi;
-      if (counts) atomicAdd(counts + bi, 1);
-    }
-#pragma unroll
-    for (int i = 0; i < kMaxE / 32; ++i)
-      if (lane + 32 * i == bi) w_local[i] = -INFINITY;  // remove from later rounds
+  if (warp < nt) finish_token_impl(warp, b0, s_logit[warp], follow, prev_ids, prev_k, E, k, logits_out, weights_out,
+                                   ids_out, counts);
+  if constexpr (kFused) {
+    // Last CTA to finish runs the K2 index pass over all B*k ids (one launch instead of
+    // two on the decode critical path). Release: ids stores -> fence -> ticket.
+    __shared__ int s_last;
+    __shared__ int s_base[kPermMaxE + 1];
+    __shared__ int s_warp_cnt[kWarps][kPermMaxE];
+    __threadfence();
+    __syncthreads();
+    if (threadIdx.x == 0) s_last = atomicAdd(fp.done, 1) == static_cast<int>(gridDim.x) - 1;
+    __syncthreads();
+    if (!s_last) return;
+    __threadfence();  // acquire side: every CTA's ids are visible (read through L2)
+    permute_block<kWarps * 32, true>(ids_out, B * k, E, fp.offsets, fp.perm_src, fp.inv, s_base, s_warp_cnt);
+    if (threadIdx.x == 0) *fp.done = 0;
   }
 }
 
@@ -200,12 +231,32 @@ extern "C" ps_status ps_route_topk(const float* x, const float* gate, const floa
     if (B == 0) return;
     const float sqrt_h = static_cast<float>(std::sqrt(static_cast<double>(H)));
     if (B <= 64) {
-      route_kernel<1><<<B, kWarps * 32, 0, s>>>(x, gate, bias, follow, prev_ids, prev_k, B, H, E, k, sqrt_h, logits,
-                                                weights, ids, counts, x_bf16);
+      route_kernel<1, false><<<B, kWarps * 32, 0, s>>>(x, gate, bias, follow, prev_ids, prev_k, B, H, E, k, sqrt_h,
+                                                       logits, weights, ids, counts, x_bf16, FusedPermute{});
     } else {
-      route_kernel<4><<<(B + 3) / 4, kWarps * 32, 0, s>>>(x, gate, bias, follow, prev_ids, prev_k, B, H, E, k, sqrt_h,
-                                                          logits, weights, ids, counts, x_bf16);
+      route_kernel<4, false><<<(B + 3) / 4, kWarps * 32, 0, s>>>(x, gate, bias, follow, prev_ids, prev_k, B, H, E, k,
+                                                                 sqrt_h, logits, weights, ids, counts, x_bf16,
+                                                                 FusedPermute{});
     }
     PS_LAUNCH_CHECK("route_kernel");
+  });
+}
+
+extern "C" ps_status ps_route_permute(const float* x, const float* gate, const float* bias, const uint8_t* follow,
+                                      const int32_t* prev_ids, int prev_k, int B, int H, int E, int k,
+                                      float* weights, int32_t* ids, uint16_t* x_bf16, int32_t* offsets,
+                                      int32_t* perm_src, int32_t* inv, int32_t* workspace, void* stream) {
+  return guarded([&] {
+    require(B >= 1 && B <= 64 && H >= 1 && E >= 1 && E <= kMaxE && k >= 1 && k <= E && k <= kMaxK,
+            "ps_route_permute: decode shapes only (1 <= B <= 64, E <= 256, 1 <= k <= min(E,16))");
+    require(x && gate && ids && offsets && perm_src && inv && workspace, "ps_route_permute: null argument");
+    require(!(follow && prev_ids) || prev_k >= 1, "ps_route_permute: prev_k must be >= 1");
+    require((reinterpret_cast<uintptr_t>(x) & 15) == 0 && (reinterpret_cast<uintptr_t>(gate) & 15) == 0,
+            "ps_route_permute: x and gate must be 16-byte aligned");
+    const float sqrt_h = static_cast<float>(std::sqrt(static_cast<double>(H)));
+    route_kernel<1, true><<<B, kWarps * 32, 0, as_stream(stream)>>>(
+        x, gate, bias, follow, prev_ids, prev_k, B, H, E, k, sqrt_h, nullptr, weights, ids, nullptr, x_bf16,
+        FusedPermute{offsets, perm_src, inv, workspace});
+    PS_LAUNCH_CHECK("route_kernel<fused permute>");
   });
 }

@@ -11,6 +11,7 @@
 // shared table, so positions are deterministic without global atomics.
 // Gather/combine passes: HBM-bound, 16-byte vectorised, one CTA row-slab each.
 #include "device_common.cuh"
+#include "permute_device.cuh"
 
 namespace ps {
 namespace {
@@ -24,57 +25,7 @@ permute_index_kernel(const int32_t* __restrict__ ids, int n, int E, int32_t* __r
                      int32_t* __restrict__ perm_src, int32_t* __restrict__ inv) {
   __shared__ int s_base[kMaxE + 1];
   __shared__ int s_warp_cnt[kPermWarps][kMaxE];
-  const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
-
-  // Histogram -> exclusive scan -> offsets.
-  for (int e = tid; e <= E; e += kPermThreads) s_base[e] = 0;
-  __syncthreads();
-  for (int i = tid; i < n; i += kPermThreads) atomicAdd(&s_base[ids[i] + 1], 1);
-  __syncthreads();
-  if (warp == 0) {  // warp-level inclusive scan over E+1 entries, 32 at a time
-    int carry = 0;
-    for (int e0 = 0; e0 <= E; e0 += 32) {
-      int v = e0 + lane <= E ? s_base[e0 + lane] : 0;
-#pragma unroll
-      for (int o = 1; o < 32; o <<= 1) {
-        int t = __shfl_up_sync(0xffffffffu, v, o);
-        if (lane >= o) v += t;
-      }
-      v += carry;
-      if (e0 + lane <= E) s_base[e0 + lane] = v;
-      carry = __shfl_sync(0xffffffffu, v, 31);
-    }
-  }
-  __syncthreads();
-  for (int e = tid; e <= E; e += kPermThreads) offsets[e] = s_base[e];
-  // s_base[e] now holds the running insertion base of expert e.
-
-  const unsigned lt_mask = (1u << lane) - 1u;
-  for (int c0 = 0; c0 < n; c0 += kPermThreads) {
-    for (int i = tid; i < kPermWarps * E; i += kPermThreads) s_warp_cnt[i / E][i % E] = 0;
-    __syncthreads();
-    const int i = c0 + tid;
-    const bool valid = i < n;
-    const int e = valid ? ids[i] : -1 - lane;  // invalid lanes never match anyone
-    const unsigned peers = __match_any_sync(0xffffffffu, e);
-    const int rank = __popc(peers & lt_mask);
-    if (valid && rank == 0) s_warp_cnt[warp][e] = __popc(peers);
-    __syncthreads();
-    if (valid) {
-      int before = 0;
-      for (int w = 0; w < warp; ++w) before += s_warp_cnt[w][e];
-      const int pos = s_base[e] + before + rank;
-      perm_src[pos] = i;
-      inv[i] = pos;
-    }
-    __syncthreads();
-    for (int ee = tid; ee < E; ee += kPermThreads) {
-      int tot = 0;
-      for (int w = 0; w < kPermWarps; ++w) tot += s_warp_cnt[w][ee];
-      s_base[ee] += tot;
-    }
-    __syncthreads();
-  }
+  permute_block<kPermThreads, false>(ids, n, E, offsets, perm_src, inv, s_base, s_warp_cnt);
 }
 
 // x_perm[pos] = x[perm_src[pos] / k]; one warp per row, 16 B per lane per step.

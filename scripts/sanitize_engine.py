@@ -1,0 +1,39 @@
+"""Small engine run for compute-sanitizer (memcheck / racecheck / synccheck): every
+kernel and copy path of the decode engine once — resident group, on-demand loads,
+prefetch, host expert lane, shared experts, prefill chunk (tcgen05) — at desk shapes.
+
+  compute-sanitizer --tool memcheck python scripts/sanitize_engine.py
+"""
+import pathlib
+import sys
+
+import torch  # noqa: F401  (CUDA context + pinned allocator parity with the tests)
+
+sys.path.insert(0, str(pathlib.Path(__file__).resolve().parents[1]))
+import paper_2509_23638_b200 as ps  # noqa: E402
+from paper_2509_23638_b200 import engine as eng  # noqa: E402
+
+
+def run(preset, L, E, H, F, B, budget, **kw):
+    spec = ps.desk_scale(preset, L, E, H)
+    spec.expert_bytes = 6 * H * F
+    gen = ps.TraceGenConfig(*[ps.GROUP_DEFAULT_GEN[g] for g in ("input", "middle", "output")])
+    gate, hidden, follow, _ = ps.trace_inputs(gen, spec, B, 3)
+    with eng.Engine(spec, gen, budget_fraction=budget, max_batch=B, weight_seed=9, gate=gate, trace_hidden=hidden,
+                    trace_follow=follow, **kw) as e:
+        for _ in range(2):
+            e.step_host(hidden, follow)
+        print(preset, B, budget, kw, e.stats()["ondemand_loads"], e.stats()["cpu_experts"])
+
+
+def main():
+    cost = (1000, 5, 10, 1.0, 1, 0)
+    run("mixtral", 3, 8, 256, 512, 8, 0.25)
+    run("mixtral", 3, 8, 256, 512, 8, 0.25, host_threads=2, cost=cost)
+    run("deepseek", 3, 64, 256, 256, 8, 0.2, n_shared=2, host_threads=2, cost=cost)
+    run("mixtral", 2, 8, 256, 512, 256, 0.5)
+    print("sanitize run done")
+
+
+if __name__ == "__main__":
+    main()

@@ -116,6 +116,51 @@ def test_permute_bit_exact(torch_cuda, B, k, E):
     assert np.array_equal(xp.cpu().numpy().view(np.uint16), x[o_src // k])
 
 
+@pytest.mark.parametrize("preset,E,H,B", [("mixtral", 8, 4096, 1), ("mixtral", 8, 4096, 16), ("deepseek", 64, 2048, 37),
+                                          ("qwen3", 128, 2048, 64)])
+def test_route_permute_fused_equals_separate(torch_cuda, preset, E, H, B):
+    """ps_route_permute (K1 + K2 index pass in one launch, the last CTA permutes) gives
+    bitwise the weights/ids/x_bf16 of ps_route_topk and the offsets/perm/inv of
+    ps_permute (= the oracle permutation), over several layers reusing the workspace."""
+    torch = torch_cuda
+    lib = ps.load()
+    spec = ps.desk_scale(preset, 3, E, H)
+    k = spec.top_k
+    cfg = ps.TraceGenConfig(*[ps.GROUP_DEFAULT_GEN[g] for g in ("input", "middle", "output")])
+    gate, hidden, follow, zipf = ps.trace_inputs(cfg, spec, B, 5)
+    g = torch.as_tensor(gate.astype(np.float32), device="cuda")
+    ws = torch.zeros(1, dtype=torch.int32, device="cuda")
+    prev = None
+    for l in range(3):
+        x = torch.as_tensor(np.ascontiguousarray(hidden[:, l], np.float32), device="cuda")
+        fol = torch.as_tensor(np.ascontiguousarray(follow[:, l]), device="cuda")
+        bias = torch.as_tensor(np.array([-zipf[l] * np.log(e + 1.0) for e in range(E)], np.float32), device="cuda")
+        outs = []
+        for fused in (False, True):
+            w = torch.empty(B, E, device="cuda")
+            ids = torch.empty(B, k, dtype=torch.int32, device="cuda")
+            xb = torch.empty(B, H, dtype=torch.int16, device="cuda")
+            off = torch.empty(E + 1, dtype=torch.int32, device="cuda")
+            src = torch.empty(B * k, dtype=torch.int32, device="cuda")
+            inv = torch.empty(B * k, dtype=torch.int32, device="cuda")
+            if fused:
+                ps.check(lib.ps_route_permute(_p(x), _p(g[l]), _p(bias), _p(fol), _p(prev), k, B, H, E, k, _p(w),
+                                              _p(ids), _p(xb), _p(off), _p(src), _p(inv), _p(ws), _s(torch)))
+            else:
+                ps.check(lib.ps_route_topk(_p(x), _p(g[l]), _p(bias), _p(fol), _p(prev), k, B, H, E, k, None, _p(w),
+                                           _p(ids), None, _p(xb), _s(torch)))
+                ps.check(lib.ps_permute(_p(ids), B, k, E, _p(off), _p(src), _p(inv), None, H, None, _s(torch)))
+            torch.cuda.synchronize()
+            outs.append([t.cpu().numpy() for t in (w, ids, xb, off, src, inv)])
+        for a, b in zip(*outs):
+            np.testing.assert_array_equal(a, b)
+        o_off, o_src, o_inv = orc.or_permute(outs[1][1], E)
+        np.testing.assert_array_equal(outs[1][3], o_off)
+        np.testing.assert_array_equal(outs[1][4], o_src)
+        assert int(ws.item()) == 0  # the last CTA reset the ticket
+        prev = torch.as_tensor(outs[1][1], device="cuda")
+
+
 def _moe_case(torch, H, F, E, k, B, seed, skew=None, split=None):
     lib = ps.load()
     rng = np.random.default_rng(seed)
