@@ -31,7 +31,7 @@ def main():
     run("mixtral", 3, 8, 256, 512, 8, 0.25)
     run("mixtral", 3, 8, 256, 512, 8, 0.25, host_threads=2, cost=cost)
     run("deepseek", 3, 64, 256, 256, 8, 0.2, n_shared=2, host_threads=2, cost=cost)
-    run("mixtral", 2, 8, 256, 512, 256, 0.5)
+    run("mixtral", 3, 8, 256, 512, 256, 0.5)
     print("sanitize run done")
 
 
