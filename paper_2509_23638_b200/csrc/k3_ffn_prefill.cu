@@ -26,6 +26,7 @@
 #include <cuda.h>
 
 #include <algorithm>
+#include <cstdlib>
 #include <cstring>
 #include <mutex>
 #include <vector>
@@ -321,6 +322,244 @@ ffn_prefill_kernel(const __grid_constant__ PrefillParams p) {
   }
 }
 
+// ------------------------------------------------------------------ CTA-pair variant
+// tcgen05.mma.cta_group::2: a cluster of 2 CTAs on the two SMs of a TPC computes one
+// 256 x 256 tile (M = 256 = 128 rows per CTA, N = 256). Each CTA stages only its half
+// of the operands — A: its 128 token rows; B: 128 of the 256 weight rows (SwiGLU: CTA 0
+// the gate rows, CTA 1 the up rows; down: consecutive halves) — so a 64-wide K stage is
+// 32 KiB per CTA instead of 48 KiB: 1.5x less L2->SM traffic per flop and 6 stages in
+// flight instead of 4. The leader (rank 0) issues the MMAs for the pair; both CTAs' TMA
+// loads complete on the leader's full barrier; tcgen05.commit multicasts the stage-free
+// and accumulator-ready signals to both CTAs; both CTAs' epilogues arrive on the
+// leader's accumulator-empty barrier. Each CTA's TMEM holds its 128 rows x 256 columns.
+constexpr int kPairStages = 6;
+constexpr int kPairStageBytes = kABytes + kBBytes / 2;  // 32 KiB
+constexpr int kPairSmemBytes = kPairStages * kPairStageBytes + 1024 + 256;
+constexpr uint32_t kIdescPair = (1u << 4) | (1u << 7) | (1u << 10) | (static_cast<uint32_t>(kBN >> 3) << 17) |
+                                (static_cast<uint32_t>((2 * kBM) >> 4) << 24);
+
+__device__ __forceinline__ uint32_t cluster_rank() {
+  uint32_t r;
+  asm volatile("mov.u32 %0, %%cluster_ctarank;" : "=r"(r));
+  return r;
+}
+__device__ __forceinline__ void cluster_sync_all() {
+  asm volatile("barrier.cluster.arrive.release.aligned;\nbarrier.cluster.wait.acquire.aligned;" ::: "memory");
+}
+// shared::cluster address of the same shared variable in CTA `rank` of the cluster.
+__device__ __forceinline__ uint32_t mapa_shared(uint32_t addr, uint32_t rank) {
+  uint32_t r;
+  asm volatile("mapa.shared::cluster.u32 %0, %1, %2;" : "=r"(r) : "r"(addr), "r"(rank));
+  return r;
+}
+__device__ __forceinline__ void tma_load_2d_pair(void* dst, const CUtensorMap* map, uint32_t leader_bar, int c0, int c1) {
+  asm volatile(
+      "cp.async.bulk.tensor.2d.cta_group::2.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1, {%2, %3}], "
+      "[%4];" ::"r"(smem_u32(dst)),
+      "l"(map), "r"(c0), "r"(c1), "r"(leader_bar)
+      : "memory");
+}
+__device__ __forceinline__ void umma_f16_pair(uint32_t tmem_d, uint64_t adesc, uint64_t bdesc, uint32_t accumulate) {
+  asm volatile(
+      "{\n"
+      ".reg .pred p;\n"
+      "setp.ne.b32 p, %4, 0;\n"
+      "tcgen05.mma.cta_group::2.kind::f16 [%0], %1, %2, %3, p;\n"
+      "}\n" ::"r"(tmem_d),
+      "l"(adesc), "l"(bdesc), "r"(kIdescPair), "r"(accumulate));
+}
+__device__ __forceinline__ void umma_commit_pair(uint64_t* bar) {  // arrive on `bar` in both CTAs
+  asm volatile(
+      "tcgen05.commit.cta_group::2.mbarrier::arrive::one.shared::cluster.multicast::cluster.b64 [%0], %1;" ::"r"(
+          smem_u32(bar)),
+      "h"(static_cast<uint16_t>(3))
+      : "memory");
+}
+__device__ __forceinline__ void mbar_arrive_cluster(uint32_t cluster_addr) {
+  asm volatile("mbarrier.arrive.release.cluster.shared::cluster.b64 _, [%0];" ::"r"(cluster_addr) : "memory");
+}
+
+// Pair tiles: (entry, 256-row block, n tile), m fastest; m_tiles[] count 256-row blocks.
+__global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads, 1)
+ffn_prefill_pair_kernel(const __grid_constant__ PrefillParams p) {
+  extern __shared__ __align__(1024) uint8_t smem_raw[];
+  uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
+  uint64_t* full_bar = reinterpret_cast<uint64_t*>(smem + kPairStages * kPairStageBytes);
+  uint64_t* empty_bar = full_bar + kPairStages;
+  uint64_t* tfull_bar = empty_bar + kPairStages;
+  uint64_t* tempty_bar = tfull_bar + 2;
+  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(tempty_bar + 2);
+
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const uint32_t rank = cluster_rank();
+  const bool leader = rank == 0;
+  const int pair = blockIdx.x >> 1, n_pairs = gridDim.x >> 1;
+  const int n_tiles = p.tile_start[p.n_experts];
+  const int k_blocks = (p.K + kBK - 1) / kBK;
+
+  if (warp == 0 && lane == 0) {
+    for (int s = 0; s < kPairStages; ++s) {
+      mbar_init(&full_bar[s], 1);   // leader: its producer's arrive.expect_tx (both CTAs' bytes)
+      mbar_init(&empty_bar[s], 1);  // one multicast commit per stage use
+    }
+    for (int s = 0; s < 2; ++s) {
+      mbar_init(&tfull_bar[s], 1);
+      mbar_init(&tempty_bar[s], 2 * 128);  // leader: the epilogue threads of both CTAs
+    }
+    asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+  }
+  if (warp == 1) {  // TMEM: 2 accumulator stages x 256 columns, allocated for the pair
+    asm volatile("tcgen05.alloc.cta_group::2.sync.aligned.shared::cta.b32 [%0], 512;" ::"r"(smem_u32(tmem_slot)));
+    asm volatile("tcgen05.relinquish_alloc_permit.cta_group::2.sync.aligned;");
+  }
+  tc_fence_before();
+  __syncthreads();
+  cluster_sync_all();  // peer barriers initialised before any remote arrive / complete_tx
+  tc_fence_after();
+  const uint32_t tmem_base = *tmem_slot;
+
+  if (warp == 0) {
+    for (int i = lane; i <= p.n_experts; i += 32) {
+      const CUtensorMap* m = i == 0 ? p.a_map : p.b_maps + (i - 1);
+      asm volatile("fence.proxy.tensormap::generic.acquire.gpu [%0], 128;" ::"l"(m) : "memory");
+    }
+    __syncwarp();
+    if (lane == 0) {  // ---------------------------------------------- TMA producer (both CTAs)
+      const CUtensorMap* a_map = p.a_map;
+      prefetch_map(a_map);
+      int stage = 0;
+      uint32_t phase = 0;
+      for (int t = pair; t < n_tiles; t += n_pairs) {
+        const TileCoord tc = tile_coord(p, t);
+        const CUtensorMap* bmap = p.b_maps + tc.entry;
+        const int arow = p.row0[tc.entry] + tc.m_tile * (2 * kBM) + static_cast<int>(rank) * kBM;
+        int brow;
+        if (p.mode == kSwiGLU) brow = (rank ? p.F : 0) + tc.n_tile * (kBN / 2);  // gate | up rows
+        else brow = tc.n_tile * kBN + static_cast<int>(rank) * (kBN / 2);
+        for (int kb = 0; kb < k_blocks; ++kb) {
+          mbar_wait(&empty_bar[stage], phase ^ 1);
+          uint8_t* sa = smem + stage * kPairStageBytes;
+          uint8_t* sb = sa + kABytes;
+          const uint32_t lbar = mapa_shared(smem_u32(&full_bar[stage]), 0);
+          if (leader) mbar_expect_tx(&full_bar[stage], 2 * kPairStageBytes);
+          tma_load_2d_pair(sa, a_map, lbar, kb * kBK, arow);
+          tma_load_2d_pair(sb, bmap, lbar, kb * kBK, brow);
+          if (++stage == kPairStages) {
+            stage = 0;
+            phase ^= 1;
+          }
+        }
+      }
+    }
+  } else if (warp == 1) {
+    if (leader && lane == 0) {  // ------------------------------------ MMA issuer (leader only)
+      int stage = 0;
+      uint32_t phase = 0;
+      int as = 0;
+      uint32_t aphase = 0;
+      for (int t = pair; t < n_tiles; t += n_pairs) {
+        mbar_wait(&tempty_bar[as], aphase ^ 1);
+        tc_fence_after();
+        const uint32_t d = tmem_base + static_cast<uint32_t>(as * kBN);
+        for (int kb = 0; kb < k_blocks; ++kb) {
+          mbar_wait(&full_bar[stage], phase);
+          tc_fence_after();
+          const uint32_t sa = smem_u32(smem + stage * kPairStageBytes);
+          const uint32_t sb = sa + kABytes;
+#pragma unroll
+          for (int kk = 0; kk < kBK / 16; ++kk)
+            umma_f16_pair(d, make_desc(sa + kk * 32), make_desc(sb + kk * 32), (kb | kk) != 0 ? 1u : 0u);
+          umma_commit_pair(&empty_bar[stage]);
+          if (++stage == kPairStages) {
+            stage = 0;
+            phase ^= 1;
+          }
+        }
+        umma_commit_pair(&tfull_bar[as]);
+        as ^= 1;
+        if (as == 0) aphase ^= 1;
+      }
+    }
+  } else {  // ------------------------------------------------------- epilogue (4 warps, both CTAs)
+    const int quarter = warp & 3;
+    const int r = quarter * 32 + lane;
+    const uint32_t tempty_leader[2] = {mapa_shared(smem_u32(&tempty_bar[0]), 0), mapa_shared(smem_u32(&tempty_bar[1]), 0)};
+    int as = 0;
+    uint32_t aphase = 0;
+    for (int t = pair; t < n_tiles; t += n_pairs) {
+      const TileCoord tc = tile_coord(p, t);
+      mbar_wait(&tfull_bar[as], aphase);
+      tc_fence_after();
+      const uint32_t tbase = tmem_base + static_cast<uint32_t>(as * kBN) + (static_cast<uint32_t>(quarter * 32) << 16);
+      const int row_in_expert = tc.m_tile * (2 * kBM) + static_cast<int>(rank) * kBM + r;
+      const bool valid = row_in_expert < p.rows[tc.entry];
+      const size_t out_row = static_cast<size_t>(p.row0[tc.entry] + row_in_expert);
+      if (p.mode == kSwiGLU) {
+        const int n0 = tc.n_tile * (kBN / 2);
+        uint16_t* out = static_cast<uint16_t*>(p.out) + out_row * p.out_ld + n0;
+#pragma unroll 1
+        for (int c = 0; c < kBN / 2; c += 32) {
+          uint32_t g[32], u[32];
+          tmem_ld32(tbase + c, g);
+          tmem_ld32(tbase + kBN / 2 + c, u);
+          tmem_ld_wait();
+          if (valid) {
+            uint32_t packed[16];
+#pragma unroll
+            for (int j = 0; j < 32; j += 2) {
+              const float g0 = __uint_as_float(g[j]), g1 = __uint_as_float(g[j + 1]);
+              const float h0 = g0 / (1.0f + expf(-g0)) * __uint_as_float(u[j]);
+              const float h1 = g1 / (1.0f + expf(-g1)) * __uint_as_float(u[j + 1]);
+              packed[j / 2] = static_cast<uint32_t>(f32_to_bf16_rne(h0)) |
+                              (static_cast<uint32_t>(f32_to_bf16_rne(h1)) << 16);
+            }
+            if (n0 + c + 32 <= p.F) {
+              uint4* dst = reinterpret_cast<uint4*>(out + c);
+#pragma unroll
+              for (int q = 0; q < 4; ++q)
+                dst[q] = make_uint4(packed[4 * q], packed[4 * q + 1], packed[4 * q + 2], packed[4 * q + 3]);
+            } else {
+              for (int j = 0; j < 32 && n0 + c + j < p.F; ++j)
+                out[c + j] = static_cast<uint16_t>(packed[j / 2] >> (16 * (j & 1)));
+            }
+          }
+        }
+      } else {
+        const int n0 = tc.n_tile * kBN;
+        float* out = static_cast<float*>(p.out) + out_row * p.out_ld + n0;
+#pragma unroll 1
+        for (int c = 0; c < kBN; c += 32) {
+          uint32_t v[32];
+          tmem_ld32(tbase + c, v);
+          tmem_ld_wait();
+          if (valid) {
+            if (n0 + c + 32 <= p.H) {
+              float4* dst = reinterpret_cast<float4*>(out + c);
+#pragma unroll
+              for (int q = 0; q < 8; ++q)
+                dst[q] = make_float4(__uint_as_float(v[4 * q]), __uint_as_float(v[4 * q + 1]),
+                                     __uint_as_float(v[4 * q + 2]), __uint_as_float(v[4 * q + 3]));
+            } else {
+              for (int j = 0; j < 32 && n0 + c + j < p.H; ++j) out[c + j] = __uint_as_float(v[j]);
+            }
+          }
+        }
+      }
+      tc_fence_before();
+      mbar_arrive_cluster(tempty_leader[as]);
+      as ^= 1;
+      if (as == 0) aphase ^= 1;
+    }
+  }
+  tc_fence_before();
+  __syncthreads();
+  cluster_sync_all();  // the peer is done with every TMEM / barrier access of the pair
+  if (warp == 1) {
+    tc_fence_after();
+    asm volatile("tcgen05.dealloc.cta_group::2.sync.aligned.b32 %0, 512;" ::"r"(tmem_base));
+  }
+}
+
 // ------------------------------------------------------------------ host helpers
 using EncodeFn = CUresult (*)(CUtensorMap*, CUtensorMapDataType, cuuint32_t, void*, const cuuint64_t*,
                               const cuuint64_t*, const cuuint32_t*, const cuuint32_t*, CUtensorMapInterleave,
@@ -380,6 +619,28 @@ struct MapRing {
   }
 };
 
+void launch_pair(PrefillParams& p, cudaStream_t s) {
+  static bool attr = false;
+  if (!attr) {
+    PS_CUDA(cudaFuncSetAttribute(ffn_prefill_pair_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                 kPairSmemBytes));
+    attr = true;
+  }
+  const int tiles = p.tile_start[p.n_experts];
+  if (tiles == 0) return;
+  const int grid = 2 * std::min(tiles, kNumSMs / 2);  // one CTA pair per TPC, persistent
+  ffn_prefill_pair_kernel<<<grid, kThreads, kPairSmemBytes, s>>>(p);
+  PS_LAUNCH_CHECK("ffn_prefill_pair_kernel");
+}
+
+bool use_pair() {  // PS_PREFILL_PAIR=0 selects the single-CTA kernel (A/B comparison)
+  static const bool on = [] {
+    const char* v = std::getenv("PS_PREFILL_PAIR");
+    return !(v && v[0] == '0');
+  }();
+  return on;
+}
+
 void launch(PrefillParams& p, cudaStream_t s) {
   static bool attr = false;
   if (!attr) {
@@ -431,7 +692,7 @@ extern "C" ps_status ps_expert_ffn_prefill(const ps_expert_group* group, const i
       const uint16_t* slab = group->slabs[i];
       maps_host[2 + n] = make_map(slab, 2ull * F, H, kBN / 2);                                          // [Wg; Wu]
       maps_host[2 + group->n + n] = make_map(slab + 2ull * F * H, static_cast<uint64_t>(H), F, kBN / 2);  // Wd
-      const int mt = (m + kBM - 1) / kBM;
+      const int mt = use_pair() ? (m + 2 * kBM - 1) / (2 * kBM) : (m + kBM - 1) / kBM;
       for (PrefillParams* p : {&gu, &dn}) {
         p->m_tiles[n] = mt;
         p->row0[n] = offsets_host[e];
@@ -453,8 +714,13 @@ extern "C" ps_status ps_expert_ffn_prefill(const ps_expert_group* group, const i
     gu.out_ld = F;
     dn.out = y_perm;
     dn.out_ld = H;
-    launch(gu, s);
-    launch(dn, s);
+    if (use_pair()) {
+      launch_pair(gu, s);
+      launch_pair(dn, s);
+    } else {
+      launch(gu, s);
+      launch(dn, s);
+    }
     PS_CUDA(cudaEventRecord(ring.ev[slot], s));
   });
 }

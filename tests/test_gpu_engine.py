@@ -150,3 +150,25 @@ def test_engine_host_lane_runs_cpu_set_and_matches_oracle(torch_cuda, B, budget,
     needed = sum(1 for l in range(spec.num_layers) for e in set(ids[l].ravel().tolist()) if (l, e) not in resident)
     assert st["cpu_experts"] + st["ondemand_loads"] + st["prefetches_committed"] >= needed * st["steps"]
     assert st["cpu_experts"] + st["ondemand_loads"] <= needed * st["steps"]
+
+
+def test_engine_set_cost_and_calibrate_semantics(torch_cuda):
+    """ps_engine_set_cost validates like CostParams::validate (t_g < t_io, ...); beta = 1e9
+    keeps cpu_set empty (GPU-only executor) on a host-lane engine; calibrate refits from
+    the samples since the last stats reset."""
+    spec = _small_spec()
+    cfg = ps.TraceGenConfig(*[ps.GROUP_DEFAULT_GEN[g] for g in ("input", "middle", "output")])
+    gate, hidden, follow, _ = ps.trace_inputs(cfg, spec, 8, 3)
+    with eng.Engine(spec, cfg, budget_fraction=0.25, max_batch=8, weight_seed=9, gate=gate, trace_hidden=hidden,
+                    trace_follow=follow, host_threads=2, cost=(1000, 5, 10, 1.0, 1, 0)) as e:
+        with pytest.raises(ps.capi.PsError):
+            e.set_cost(10, 20, 1, 1.0, 0)  # t_g >= t_io
+        e.set_cost(1000, 5, 10, 1e9, 0)
+        e.step_host(hidden, follow)
+        assert e.stats()["cpu_experts"] == 0 and e.stats()["ondemand_loads"] > 0
+        e.set_cost(1000, 5, 10, 1.0, 1)
+        e.reset_stats()
+        e.step_host(hidden, follow)
+        assert e.stats()["cpu_experts"] > 0
+        c = e.calibrate()
+        assert c["beta"] == 1.0 and c["startup"] >= 0 and c["t_io"] > c["t_g"]
