@@ -305,6 +305,9 @@ ps_status ps_gather_rows(const uint16_t* x, const int32_t* idx, int n, int div, 
 ps_status ps_combine(const float* y_part, int n_split, const int32_t* inv, const int32_t* ids,
                      const float* weights, int B, int k, int E, int H, float* y, void* stream);
 
+/* x [n] f32 -> bf16 (round to nearest even), the FFN input cast K1 otherwise fuses. */
+ps_status ps_cast_bf16(const float* x, int64_t n, uint16_t* out, void* stream);
+
 /* Shared experts (BASELINE config 3, DeepSeek-V2-Lite: 2 always-active experts with gate
  * weight 1; a north_star extension — the reference's ModelSpec has none): appends
  * virtual experts E..E+S-1 to every token so K2/K3/combine run them with the routed ones.
@@ -339,6 +342,10 @@ ps_status ps_expert_ffn(const ps_expert_group* group, const int32_t* counts_host
 ps_status ps_expert_ffn_prefill(const ps_expert_group* group, const int32_t* counts_host,
                                 const int32_t* offsets_host, const uint16_t* x_perm, int total_rows,
                                 int H, int F, uint16_t* h_perm, float* y_perm, void* stream);
+/* Prefill kernel choice (process-wide): 0 = single-CTA M=128 tiles, 1 = CTA pairs
+ * (cta_group::2, M=256), 2 = auto (default: pairs unless their extra padding of the
+ * experts' last M tiles exceeds 3 % of the routed rows). */
+ps_status ps_set_prefill_kernel(int mode);
 /* Split-K factor ps_expert_ffn expects for the down projection at this shape. */
 int ps_ffn_down_splits(int H, int F);
 
@@ -463,6 +470,12 @@ ps_status ps_engine_set_router(ps_engine e, const float* gate_host);
  * Blocks the host until the step's GPU work is complete. */
 ps_status ps_engine_decode_step(ps_engine e, const float* hidden, const uint8_t* follow, int B,
                                 float* y, int32_t* ids);
+/* One decode step with the routing GIVEN instead of computed by K1 — the gating truth of
+ * a prescope::Trace (active experts [L,B,k] i32 and full-softmax gate_weights [L,B,E] f32,
+ * device buffers, e.g. from ps_trace_read) replayed through the real executor (K2 ->
+ * loader/PreSched -> K3 -> combine) with x = hidden [L,B,H] f32. */
+ps_status ps_engine_decode_step_routed(ps_engine e, const float* hidden, const int32_t* ids,
+                                       const float* weights, int B, float* y);
 /* Same, from HOST buffers (pinned or pageable): copies in, step, copies out. */
 ps_status ps_engine_decode_step_host(ps_engine e, const float* hidden_host,
                                      const uint8_t* follow_host, int B, float* y_host,

@@ -184,10 +184,13 @@ _SIGS = {
     "ps_host_lane_isa": (C.c_int, [_P]),
     "ps_host_expert_ffn": (C.c_int, [_P, _P, C.c_int, C.c_int, _P, C.c_int, _P]),
     "ps_host_expert_ffn_batch": (C.c_int, [_P, C.c_int, _P, _P, _P, C.c_int, C.c_int, _P, _P]),
+    "ps_cast_bf16": (C.c_int, [_P, C.c_int64, _P, _P]),
+    "ps_engine_decode_step_routed": (C.c_int, [_P, _P, _P, _P, C.c_int, _P]),
     "ps_append_shared": (C.c_int, [_P, _P, C.c_int, C.c_int, C.c_int, C.c_int, _P, _P, _P, _P]),
     "ps_expert_ffn": (C.c_int, [C.POINTER(ExpertGroup), _P, _P, _P, C.c_int, _P, C.c_int, C.c_int, _P, _P,
                                 C.c_int, C.c_int, _P]),
     "ps_ffn_down_splits": (C.c_int, [C.c_int, C.c_int]),
+    "ps_set_prefill_kernel": (C.c_int, [C.c_int]),
     "ps_expert_ffn_prefill": (C.c_int, [C.POINTER(ExpertGroup), _P, _P, _P, C.c_int, C.c_int, C.c_int, _P, _P,
                                         _P]),
     "ps_init_expert_slab": (C.c_int, [_P, C.c_int, C.c_int, C.c_uint64, C.c_int, C.c_int, _P]),

@@ -649,7 +649,10 @@ ps_status ep_combine_rows(ps_engine_s& e, int B, const LayerDev& ld, float* y_l)
   return ps_combine(e.ep_y_back, 1, e.ep_inv_v, ld.ids, ld.weights, B, K, E, H, y_l, e.sc);
 }
 
-void decode_step(ps_engine_s& e, const float* hidden, const uint8_t* follow, int B, float* y, int32_t* ids_out) {
+// routed_ids / routed_w (nullable, device, [L,B,k] / [L,B,E]): the routing is given (a
+// reference trace's gating truth) and replaces K1; everything downstream is unchanged.
+void decode_step(ps_engine_s& e, const float* hidden, const uint8_t* follow, int B, float* y, int32_t* ids_out,
+                 const int32_t* routed_ids = nullptr, const float* routed_w = nullptr) {
   const int L = e.L, E = e.E, K = e.K, H = e.H;
   require(B >= 1 && B <= e.maxB, "decode_step: batch out of range");
   e.prefill_mode = B > kDecodeMaxBatch;
@@ -686,9 +689,15 @@ void decode_step(ps_engine_s& e, const float* hidden, const uint8_t* follow, int
     // --- K1 route (+fused bf16 cast) ------------------------------------------------
     // Decode without shared experts / EP: K1 and K2's index pass in one launch (the last
     // route CTA permutes). Otherwise K1 here and K2 below. Histogram: diff of K2 offsets.
-    const bool fused_perm = !e.ep && e.S == 0 && !e.prefill_mode;
+    const bool fused_perm = !e.ep && e.S == 0 && !e.prefill_mode && !routed_ids;
     ps_status s;
-    if (fused_perm)
+    if (routed_ids) {
+      PS_CUDA(cudaMemcpyAsync(ld.ids, routed_ids + static_cast<size_t>(l) * B * K, sizeof(int32_t) * B * K,
+                              cudaMemcpyDeviceToDevice, e.sc));
+      PS_CUDA(cudaMemcpyAsync(ld.weights, routed_w + static_cast<size_t>(l) * B * E, sizeof(float) * B * E,
+                              cudaMemcpyDeviceToDevice, e.sc));
+      s = ps_cast_bf16(x, static_cast<int64_t>(B) * H, e.x_bf16, e.sc);
+    } else if (fused_perm)
       s = ps_route_permute(x, e.gate + static_cast<size_t>(l) * E * H, e.bias + static_cast<size_t>(l) * E,
                            follow ? follow + static_cast<size_t>(l) * B : nullptr, l > 0 ? e.layer[l - 1].ids : nullptr,
                            K, B, H, E, K, ld.weights, ld.ids, e.x_bf16, e.offsets, e.perm_src, e.inv, e.route_ws,
@@ -1410,6 +1419,14 @@ ps_status ps_engine_set_router(ps_engine e, const float* gate_host) {
 ps_status ps_engine_decode_step(ps_engine e, const float* hidden, const uint8_t* follow, int B, float* y,
                                 int32_t* ids) {
   return guarded([&] { decode_step(*e, hidden, follow, B, y, ids); });
+}
+
+ps_status ps_engine_decode_step_routed(ps_engine e, const float* hidden, const int32_t* ids, const float* weights, int B,
+                                       float* y) {
+  return guarded([&] {
+    require(e && hidden && ids && weights && y, "decode_step_routed: null argument");
+    decode_step(*e, hidden, nullptr, B, y, nullptr, ids, weights);
+  });
 }
 
 ps_status ps_engine_decode_step_host(ps_engine e, const float* hidden_host, const uint8_t* follow_host, int B,

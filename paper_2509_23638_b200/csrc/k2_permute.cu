@@ -83,6 +83,12 @@ __global__ void ep_pack_counts_kernel(const int32_t* __restrict__ offsets_v, con
   out[d * 2 * e_loc + e_loc + j] = (pred && e < E) ? pred[e] : 0;
 }
 
+__global__ void cast_bf16_kernel(const float* __restrict__ x, int64_t n, uint16_t* __restrict__ out) {
+  for (int64_t i = blockIdx.x * static_cast<int64_t>(blockDim.x) + threadIdx.x; i < n;
+       i += static_cast<int64_t>(gridDim.x) * blockDim.x)
+    out[i] = f32_to_bf16_rne(x[i]);
+}
+
 // Shared experts (DeepSeek-style, always active, gate weight 1): appended as virtual
 // experts E..E+S-1 so permute / FFN / combine treat them like routed ones.
 __global__ void append_shared_kernel(const int32_t* __restrict__ ids, const float* __restrict__ w, int B, int k,
@@ -111,6 +117,16 @@ ps_status ps_ep_pack_counts(const int32_t* offsets_v, const int32_t* pred, int E
     const int e_loc = (E + G - 1) / G;
     ep_pack_counts_kernel<<<(G * e_loc + 127) / 128, 128, 0, as_stream(stream)>>>(offsets_v, pred, E, G, e_loc, out);
     PS_LAUNCH_CHECK("ep_pack_counts_kernel");
+  });
+}
+
+ps_status ps_cast_bf16(const float* x, int64_t n, uint16_t* out, void* stream) {
+  return guarded([&] {
+    require(n >= 0 && (n == 0 || (x && out)), "ps_cast_bf16: bad arguments");
+    if (n == 0) return;
+    const int grid = static_cast<int>(std::min<int64_t>((n + 255) / 256, 4 * 148));
+    cast_bf16_kernel<<<grid, 256, 0, as_stream(stream)>>>(x, n, out);
+    PS_LAUNCH_CHECK("cast_bf16_kernel");
   });
 }
 

@@ -26,6 +26,7 @@
 #include <cuda.h>
 
 #include <algorithm>
+#include <atomic>
 #include <cstdlib>
 #include <cstring>
 #include <mutex>
@@ -633,12 +634,14 @@ void launch_pair(PrefillParams& p, cudaStream_t s) {
   PS_LAUNCH_CHECK("ffn_prefill_pair_kernel");
 }
 
-bool use_pair() {  // PS_PREFILL_PAIR=0 selects the single-CTA kernel (A/B comparison)
-  static const bool on = [] {
+// Kernel choice: 0 = single-CTA, 1 = CTA pairs, 2 = auto (pairs unless padding costs
+// more than they gain). Initial value from PS_PREFILL_PAIR, else auto.
+std::atomic<int>& prefill_mode() {
+  static std::atomic<int> mode{[] {
     const char* v = std::getenv("PS_PREFILL_PAIR");
-    return !(v && v[0] == '0');
-  }();
-  return on;
+    return v && (v[0] == '0' || v[0] == '1') ? v[0] - '0' : 2;
+  }()};
+  return mode;
 }
 
 void launch(PrefillParams& p, cudaStream_t s) {
@@ -675,6 +678,21 @@ extern "C" ps_status ps_expert_ffn_prefill(const ps_expert_group* group, const i
     CUtensorMap* maps_host = ring.host + slot * MapRing::kPerSlot;
     CUtensorMap* maps_dev = ring.dev + slot * MapRing::kPerSlot;
 
+    // CTA pairs compute 256-row M tiles: 1.03-1.05x the single-CTA throughput on full
+    // tiles (scripts/prefill_micro.py), but an expert's last tile pads up to 255 rows
+    // instead of 127. Pairs unless their extra padding exceeds 3 % of the routed rows.
+    const int mode = prefill_mode().load();
+    bool pair = mode != 0;
+    if (mode == 2) {
+      int64_t rows = 0, pad1 = 0, pad2 = 0;
+      for (int i = 0; i < group->n; ++i) {
+        const int64_t m = counts_host[group->experts[i]];
+        rows += m;
+        pad1 += (m + kBM - 1) / kBM * kBM - m;
+        pad2 += (m + 2 * kBM - 1) / (2 * kBM) * (2 * kBM) - m;
+      }
+      if (pad2 - pad1 > rows * 3 / 100) pair = false;
+    }
     PrefillParams gu{}, dn{};
     gu.mode = kSwiGLU;
     dn.mode = kStoreF32;
@@ -692,7 +710,7 @@ extern "C" ps_status ps_expert_ffn_prefill(const ps_expert_group* group, const i
       const uint16_t* slab = group->slabs[i];
       maps_host[2 + n] = make_map(slab, 2ull * F, H, kBN / 2);                                          // [Wg; Wu]
       maps_host[2 + group->n + n] = make_map(slab + 2ull * F * H, static_cast<uint64_t>(H), F, kBN / 2);  // Wd
-      const int mt = use_pair() ? (m + 2 * kBM - 1) / (2 * kBM) : (m + kBM - 1) / kBM;
+      const int mt = pair ? (m + 2 * kBM - 1) / (2 * kBM) : (m + kBM - 1) / kBM;
       for (PrefillParams* p : {&gu, &dn}) {
         p->m_tiles[n] = mt;
         p->row0[n] = offsets_host[e];
@@ -714,7 +732,7 @@ extern "C" ps_status ps_expert_ffn_prefill(const ps_expert_group* group, const i
     gu.out_ld = F;
     dn.out = y_perm;
     dn.out_ld = H;
-    if (use_pair()) {
+    if (pair) {
       launch_pair(gu, s);
       launch_pair(dn, s);
     } else {
@@ -722,5 +740,12 @@ extern "C" ps_status ps_expert_ffn_prefill(const ps_expert_group* group, const i
       launch(dn, s);
     }
     PS_CUDA(cudaEventRecord(ring.ev[slot], s));
+  });
+}
+
+extern "C" ps_status ps_set_prefill_kernel(int mode) {
+  return guarded([&] {
+    require(mode >= 0 && mode <= 2, "ps_set_prefill_kernel: mode 0 (single CTA), 1 (CTA pairs) or 2 (auto)");
+    prefill_mode().store(mode);
   });
 }

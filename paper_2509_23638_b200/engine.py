@@ -160,6 +160,19 @@ class Engine:
                                                    y.ctypes.data_as(C.c_void_p), ids.ctypes.data_as(C.c_void_p)))
         return y, ids
 
+    def step_routed(self, hidden, active, gate_weights):
+        """Replay a trace's routing (prescope::Trace arrays, [B,L,...] trace order): hidden
+        [B,L,H], active [B,L,k], gate_weights [B,L,E]. Returns y [L,B,H] f32."""
+        torch = _torch()
+        B, L, H = hidden.shape
+        hid = torch.as_tensor(np.ascontiguousarray(hidden.transpose(1, 0, 2), np.float32), device="cuda")
+        ids = torch.as_tensor(np.ascontiguousarray(active.transpose(1, 0, 2), np.int32), device="cuda")
+        w = torch.as_tensor(np.ascontiguousarray(gate_weights.transpose(1, 0, 2), np.float32), device="cuda")
+        y = torch.empty(L, B, H, dtype=torch.float32, device="cuda")
+        check(self.lib.ps_engine_decode_step_routed(self.h, _ptr(hid), _ptr(ids), _ptr(w), B, _ptr(y)))
+        torch.cuda.synchronize()
+        return y.cpu().numpy()
+
     def step_device(self, hidden_lbh, follow_lb, y_lbh, ids_lbk=None):
         """One decode step on device tensors (layer-major)."""
         B = hidden_lbh.shape[1]

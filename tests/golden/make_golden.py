@@ -22,6 +22,9 @@ Outputs (all small, committed):
   ref_trace_desk.tsv      a trace file written by the reference's write_trace
                           (workload.cpp:391-407): desk_scale(mixtral,4,8,16), B=3, seed 17,
                           knobs (rho .9, kappa .3, zipf .5) — read/re-write parity.
+  ref_trace_h256.tsv      reference trace desk_scale(mixtral,4,8,256), B=8, seed 23,
+                          benchmark knobs — replayed through the GPU executor
+                          (ps_engine_decode_step_routed, tests/test_gpu_engine.py).
 """
 from __future__ import annotations
 
@@ -182,6 +185,13 @@ def ref_trace_file():
                                                 str(OUT / "ref_trace_desk.tsv").encode()))
 
 
+def ref_trace_h256():
+    spec = desk_spec("mixtral", 4, 8, 256)
+    gen = orc.ref_gen(DEFAULT["input"], DEFAULT["middle"], DEFAULT["output"])
+    orc.ref_check(orc.ref_lib().ref_write_trace(C.byref(gen), C.byref(spec), 8, 23,
+                                                str(OUT / "ref_trace_h256.tsv").encode()))
+
+
 def main():
     orc.ref_check(orc.ref_lib().ref_dump_golden(str(OUT / "golden_scenarios.json").encode()))
     (OUT / "trace_fingerprints.json").write_text(json.dumps(fingerprints(), indent=1))
@@ -190,6 +200,7 @@ def main():
     (OUT / "sim_cases.json").write_text(json.dumps(sim_cases()))
     llapor()
     ref_trace_file()
+    ref_trace_h256()
     print("golden fixtures written to", OUT)
 
 

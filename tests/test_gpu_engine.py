@@ -8,6 +8,7 @@ import pytest
 import oracle as orc
 import paper_2509_23638_b200 as ps
 from paper_2509_23638_b200 import engine as eng
+from conftest import GOLDEN as GOLD
 
 pytestmark = pytest.mark.gpu
 
@@ -172,3 +173,33 @@ def test_engine_set_cost_and_calibrate_semantics(torch_cuda):
         assert e.stats()["cpu_experts"] > 0
         c = e.calibrate()
         assert c["beta"] == 1.0 and c["startup"] >= 0 and c["t_io"] > c["t_g"]
+
+
+@pytest.mark.parametrize("budget,host_threads", [(0.5, 0), (0.25, 2)])
+def test_engine_replays_reference_trace_file(torch_cuda, budget, host_threads):
+    """a trace written by the reference (write_trace) is read with
+    ps_trace_read and its gating truth replayed through the real executor
+    (ps_engine_decode_step_routed): outputs match the oracle MoE layer on the trace's own
+    routing, and every (layer, expert) the trace activates is computed (loaded, host lane
+    or resident) exactly as the trace's aggregate_layer_loads says."""
+    t = ps.read_trace(GOLD / "ref_trace_h256.tsv")
+    spec = t.spec
+    H, F = spec.hidden_dim, 512
+    spec.expert_bytes = 6 * H * F
+    cfg = ps.TraceGenConfig(*[ps.GROUP_DEFAULT_GEN[g] for g in ("input", "middle", "output")])
+    gate, _, _, _ = ps.trace_inputs(cfg, spec, 1, t.seed)
+    kw = dict(host_threads=host_threads, cost=(1000, 5, 10, 1.0, 1, 0)) if host_threads else {}
+    with eng.Engine(spec, cfg, budget_fraction=budget, max_batch=t.batch_size, weight_seed=4, gate=gate,
+                    trace_hidden=t.hidden, trace_follow=np.zeros(t.hidden.shape[:2], np.uint8), **kw) as e:
+        y = e.step_routed(t.hidden, t.active, t.gate_weights)
+        st = e.stats()
+        assert e.verify_last_step() == []
+        events, truth, res, _, _ = e.last_timeline()
+        L, E = spec.num_layers, spec.experts_per_layer
+        want = t.tokens.sum(0)  # [L,E] aggregate_layer_loads of the trace
+        assert np.array_equal(np.asarray(truth).reshape(L, E), want)
+    ids = np.ascontiguousarray(t.active.transpose(1, 0, 2))
+    y_ref = orc.or_engine_reference(spec, F, 4, t.hidden, ids, t.gate_weights.transpose(1, 0, 2))
+    assert np.linalg.norm(y - y_ref) / np.linalg.norm(y_ref) < BF16_RTOL
+    if host_threads:
+        assert st["cpu_experts"] > 0

@@ -80,16 +80,25 @@ def _rel(a, b):
     return np.linalg.norm(a - b) / np.linalg.norm(b)
 
 
+@pytest.fixture(params=[0, 1], ids=["single_cta", "cta_pair"])
+def prefill_kernel(request):
+    """Both tcgen05 kernels explicitly (ps_set_prefill_kernel), auto mode restored after."""
+    lib = ps.load()
+    ps.check(lib.ps_set_prefill_kernel(request.param))
+    yield request.param
+    ps.check(lib.ps_set_prefill_kernel(2))
+
+
 @pytest.mark.parametrize("H,F,E,k,B,skew", [(256, 512, 8, 2, 512, None), (256, 384, 8, 2, 300, 3),
                                              (512, 1024, 16, 4, 160, None), (256, 256, 4, 1, 1, None)])
-def test_prefill_vs_oracle_small(torch_cuda, H, F, E, k, B, skew):
+def test_prefill_vs_oracle_small(torch_cuda, prefill_kernel, H, F, E, k, B, skew):
     out = _prefill_case(torch_cuda, H, F, E, k, B, 7, skew, check_oracle_rows=B)
     assert np.isfinite(out["y"]).all()
     assert _rel(out["y"], out["y_oracle"]) < BF16_RTOL
     assert _rel(out["y"], out["y_decode"]) < BF16_RTOL
 
 
-def test_prefill_deepseek_shape(torch_cuda):
+def test_prefill_deepseek_shape(torch_cuda, prefill_kernel):
     """DeepSeek-V2-Lite expert shape (H=2048, F=1408), 64 experts top-6, 2k-token chunk."""
     out = _prefill_case(torch_cuda, 2048, 1408, 64, 6, 2048, 3, check_oracle_rows=6)
     assert _rel(out["y"], out["y_decode"]) < BF16_RTOL
@@ -97,7 +106,7 @@ def test_prefill_deepseek_shape(torch_cuda):
     assert _rel(out["y"][sel], out["y_oracle"]) < BF16_RTOL
 
 
-def test_prefill_mixtral_shape(torch_cuda):
+def test_prefill_mixtral_shape(torch_cuda, prefill_kernel):
     """Mixtral expert shape (H=4096, F=14336), 8 experts top-2, 1k tokens (m_e ~ 256)."""
     out = _prefill_case(torch_cuda, 4096, 14336, 8, 2, 1024, 5, check_oracle_rows=2)
     assert _rel(out["y"], out["y_decode"]) < BF16_RTOL
