@@ -344,7 +344,7 @@ ps_status ps_expert_ffn_prefill(const ps_expert_group* group, const int32_t* cou
                                 int H, int F, uint16_t* h_perm, float* y_perm, void* stream);
 /* Prefill kernel choice (process-wide): 0 = single-CTA M=128 tiles, 1 = CTA pairs
  * (cta_group::2, M=256), 2 = auto (default: pairs unless their extra padding of the
- * experts' last M tiles exceeds 3 % of the routed rows). */
+ * experts' last M tiles exceeds 8 % of the routed rows). */
 ps_status ps_set_prefill_kernel(int mode);
 /* Split-K factor ps_expert_ffn expects for the down projection at this shape. */
 int ps_ffn_down_splits(int H, int F);
@@ -368,6 +368,10 @@ ps_status ps_host_lane_create(int threads, ps_host_lane* out);
 ps_status ps_host_lane_destroy(ps_host_lane lane);
 int ps_host_lane_threads(ps_host_lane lane);
 int ps_host_lane_isa(ps_host_lane lane); /* 2 = AMX-BF16 tiles, 1 = AVX512-BF16 GEMV */
+/* Pin the calling thread (the one that will call ps_host_expert_ffn*: pool worker 0) to
+ * the lane's first CPU. The pool's workers are pinned to the last `threads` CPUs of the
+ * process affinity set unless PS_HOST_LANE_PIN=0. */
+ps_status ps_host_lane_bind_caller(ps_host_lane lane);
 ps_status ps_host_expert_ffn(ps_host_lane lane, const uint16_t* slab, int H, int F, const uint16_t* x,
                              int m, float* y);
 /* A layer's cpu_set in one call: expert j reads x rows [row0[j], row0[j] + m[j]) and

@@ -182,6 +182,7 @@ _SIGS = {
     "ps_host_lane_destroy": (C.c_int, [_P]),
     "ps_host_lane_threads": (C.c_int, [_P]),
     "ps_host_lane_isa": (C.c_int, [_P]),
+    "ps_host_lane_bind_caller": (C.c_int, [_P]),
     "ps_host_expert_ffn": (C.c_int, [_P, _P, C.c_int, C.c_int, _P, C.c_int, _P]),
     "ps_host_expert_ffn_batch": (C.c_int, [_P, C.c_int, _P, _P, _P, C.c_int, C.c_int, _P, _P]),
     "ps_cast_bf16": (C.c_int, [_P, C.c_int64, _P, _P]),

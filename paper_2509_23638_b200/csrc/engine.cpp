@@ -241,6 +241,7 @@ class LaneDriver {
 
  private:
   void loop() {
+    ps_host_lane_bind_caller(lane_);  // the driver is the lane pool's worker 0
     std::unique_lock<std::mutex> g(mu_);
     while (true) {
       cv_.wait(g, [&] { return stop_ || jobs_ != nullptr; });

@@ -25,6 +25,8 @@
 #include <thread>
 #include <vector>
 
+#include <pthread.h>
+#include <sched.h>
 #include <sys/syscall.h>
 #include <unistd.h>
 
@@ -33,12 +35,43 @@
 namespace ps {
 namespace {
 
+// CPUs for the lane: the LAST `n` CPUs of the process's affinity set, so the engine and
+// I/O threads (and the Python caller) keep the first ones. Empty = no pinning
+// (PS_HOST_LANE_PIN=0 or fewer CPUs than threads).
+std::vector<int> lane_cpus(int n) {
+  const char* v = std::getenv("PS_HOST_LANE_PIN");
+  if (v && v[0] == '0') return {};
+  cpu_set_t set;
+  CPU_ZERO(&set);
+  if (sched_getaffinity(0, sizeof(set), &set) != 0) return {};
+  std::vector<int> cpus;
+  for (int c = 0; c < CPU_SETSIZE; ++c)
+    if (CPU_ISSET(c, &set)) cpus.push_back(c);
+  if (static_cast<int>(cpus.size()) < n + 2) return {};
+  return std::vector<int>(cpus.end() - n, cpus.end());
+}
+
+void pin_self(int cpu) {
+  cpu_set_t set;
+  CPU_ZERO(&set);
+  CPU_SET(cpu, &set);
+  pthread_setaffinity_np(pthread_self(), sizeof(set), &set);
+}
+
 // Persistent pool: the caller is worker 0; workers wait on a generation counter
-// (C++20 atomic wait = futex), run their share, count down.
+// (C++20 atomic wait = futex), run their share, count down. Workers are pinned to
+// lane_cpus() (one CPU each); the caller pins itself with pin_caller().
 class Pool {
  public:
-  explicit Pool(int threads) : n_(std::max(1, threads)) {
-    for (int i = 1; i < n_; ++i) workers_.emplace_back([this, i] { loop(i); });
+  explicit Pool(int threads) : n_(std::max(1, threads)), cpus_(lane_cpus(n_)) {
+    for (int i = 1; i < n_; ++i)
+      workers_.emplace_back([this, i] {
+        if (!cpus_.empty()) pin_self(cpus_[i]);
+        loop(i);
+      });
+  }
+  void pin_caller() const {
+    if (!cpus_.empty()) pin_self(cpus_[0]);
   }
   ~Pool() {
     stop_ = true;
@@ -70,6 +103,7 @@ class Pool {
     }
   }
   int n_;
+  std::vector<int> cpus_;
   std::vector<std::thread> workers_;
   std::atomic<uint64_t> gen_{0};
   std::atomic<int> remaining_{0};
@@ -275,6 +309,13 @@ ps_status ps_host_lane_destroy(ps_host_lane l) {
 int ps_host_lane_threads(ps_host_lane l) { return l ? l->pool->size() : 0; }
 
 int ps_host_lane_isa(ps_host_lane l) { return l ? (l->amx ? 2 : 1) : 0; }
+
+ps_status ps_host_lane_bind_caller(ps_host_lane l) {
+  return guarded([&] {
+    require(l != nullptr, "ps_host_lane_bind_caller: null lane");
+    l->pool->pin_caller();
+  });
+}
 
 // A batch of experts (PreSched's cpu_set of one layer) in two pool passes: phase 1 over
 // all (expert, 16-row block of W_gate/W_up) units, phase 2 over all (expert, 16-row
