@@ -277,6 +277,20 @@ int ref_write_trace(const ref_gen* gen, const ref_spec* spec, int batch, uint64_
   return guarded([&] { write_trace(generate_trace(to_gen(*gen), to_spec(*spec), batch, seed), path); });
 }
 
+// read_trace (workload.cpp:409-436) of a file written by anyone: batch, seed, checksum
+// and the flattened routing (active [B*L*k]) as the reference parses them.
+int ref_read_trace(const char* path, int* batch, uint64_t* seed, int32_t* active, int cap) {
+  return guarded([&] {
+    Trace t = read_trace(path);
+    *batch = t.batch_size;
+    *seed = t.seed;
+    int n = 0;
+    for (const TraceStep& s : t.steps)
+      for (int e : s.active_experts)
+        if (n < cap) active[n++] = e;
+  });
+}
+
 int ref_topk(const double* w, int n, int k, int32_t* out, int* n_out) {
   return guarded([&] {
     std::vector<int> r = topk_indices(std::vector<double>(w, w + n), k);

@@ -109,3 +109,20 @@ def test_reference_traces_roundtrip_and_fingerprints(tmp_path):
         q = tmp_path / "ours.tsv"
         ps.write_trace(t, q)
         assert q.read_bytes() == p.read_bytes()
+
+
+@pytest.mark.skipif(not orc.ref_available(), reason="oracle/_ref not built")
+def test_reference_reads_our_trace(tmp_path):
+    """The other direction: a file written by ps_trace_write (here from modified arrays,
+    so it is not a byte copy of a reference file) is accepted by the reference's
+    read_trace (checksum, header) and parses to the same routing."""
+    t = ps.read_trace(GOLD / "ref_trace_desk.tsv")
+    t.seed = 99
+    t.active = t.active[:, :, ::-1].copy()  # any routing: the reader does not re-derive it
+    p = tmp_path / "ours.tsv"
+    ps.write_trace(t, p)
+    b, seed = C.c_int(), C.c_uint64()
+    act = np.zeros(t.active.size, np.int32)
+    orc.ref_check(orc.ref_lib().ref_read_trace(str(p).encode(), C.byref(b), C.byref(seed), act.ctypes.data, act.size))
+    assert (b.value, seed.value) == (t.batch_size, 99)
+    np.testing.assert_array_equal(act, t.active.ravel())
