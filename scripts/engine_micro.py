@@ -57,7 +57,8 @@ def main():
                       "combine_us": st["combine_ms_total"] * 1e3 / n,
                       "ffn_gbs": st["ffn_bytes_total"] / max(1e-9, st["ffn_ms_total"] / 1e3) / 1e9,
                       "ffn_tflops": st["ffn_flops_total"] / max(1e-9, st["ffn_ms_total"] / 1e3) / 1e12,
-                      "tc_launches": st["tc_launches"]}))
+                      "tc_launches": st["tc_launches"],
+                      "m_e": e.last_timeline()[1].tolist()}))
     e.close()
     lib.ps_llapor_free(pred)
 
