@@ -7,6 +7,7 @@
 // Link with libprescope_b200.so.
 #pragma once
 
+#include <algorithm>
 #include <cstdint>
 #include <functional>
 #include <map>
@@ -79,6 +80,112 @@ inline std::vector<int> topk_indices(const std::vector<double>& weights, int k) 
   std::vector<int32_t> out(std::max(0, std::min<int>(k, static_cast<int>(weights.size()))));
   int n = ps_topk_indices(weights.data(), static_cast<int>(weights.size()), k, out.data());
   return std::vector<int>(out.begin(), out.begin() + n);
+}
+
+// ---------------------------------------------------------------- trace files
+// TraceStep / Trace (workload.hpp:47-66), TraceFormatError / TraceChecksumError
+// (workload.hpp:106-111), write_trace / read_trace / fnv1a64 (workload.cpp:290-436),
+// aggregate_layer_loads (workload.cpp:283-288).
+struct TraceStep {
+  int layer = 0;
+  std::vector<double> hidden;
+  std::vector<double> gate_weights;
+  std::vector<int> active_experts;
+  std::map<int, int> tokens_per_expert;
+  bool operator==(const TraceStep&) const = default;
+};
+
+struct Trace {
+  ModelSpec spec;
+  int batch_size = 0;
+  std::uint64_t seed = 0;
+  std::vector<TraceStep> steps;  // ordered by (token, layer)
+  bool operator==(const Trace&) const = default;
+  const TraceStep& step(int token, int layer) const {
+    const size_t i = static_cast<size_t>(token) * spec.num_layers + layer;
+    if (token < 0 || layer < 0 || layer >= spec.num_layers || i >= steps.size())
+      throw std::out_of_range("Trace::step: index out of range");
+    return steps[i];
+  }
+};
+
+struct TraceFormatError : std::runtime_error {
+  using std::runtime_error::runtime_error;
+};
+struct TraceChecksumError : std::runtime_error {
+  using std::runtime_error::runtime_error;
+};
+
+namespace detail {
+inline void trace_throw_if(ps_status s) {
+  if (s == PS_OK) return;
+  const std::string msg = ps_last_error();
+  if (s == PS_ERUNTIME && msg.rfind("TraceChecksumError", 0) == 0) throw TraceChecksumError(msg);
+  if (s == PS_ERUNTIME && msg.rfind("TraceFormatError", 0) == 0) throw TraceFormatError(msg);
+  ps_throw_if(s);
+}
+}  // namespace detail
+
+inline std::uint64_t fnv1a64(const std::string& data) { return ps_fnv1a64(data.data(), data.size()); }
+
+inline Trace read_trace(const std::string& path) {
+  ps_trace h = nullptr;
+  detail::trace_throw_if(ps_trace_read(path.c_str(), &h));
+  ps_model_spec s{};
+  int32_t b = 0;
+  uint64_t seed = 0;
+  ps_trace_shape(h, &s, &b, &seed, nullptr);
+  const int L = s.num_layers, E = s.experts_per_layer, K = s.top_k, H = s.hidden_dim;
+  const size_t n = static_cast<size_t>(b) * L;
+  std::vector<double> hid(n * H), gw(n * E);
+  std::vector<int32_t> act(n * K), tok(n * E);
+  ps_trace_arrays(h, hid.data(), gw.data(), act.data(), tok.data());
+  ps_trace_free(h);
+  Trace t;
+  t.spec = ModelSpec::from(s);
+  t.batch_size = b;
+  t.seed = seed;
+  t.steps.resize(n);
+  for (size_t i = 0; i < n; ++i) {
+    TraceStep& st = t.steps[i];
+    st.layer = static_cast<int>(i % L);
+    st.hidden.assign(hid.begin() + i * H, hid.begin() + (i + 1) * H);
+    st.gate_weights.assign(gw.begin() + i * E, gw.begin() + (i + 1) * E);
+    st.active_experts.assign(act.begin() + i * K, act.begin() + (i + 1) * K);
+    for (int e = 0; e < E; ++e)
+      if (tok[i * E + e]) st.tokens_per_expert[e] = tok[i * E + e];
+  }
+  return t;
+}
+
+inline void write_trace(const Trace& t, const std::string& path) {
+  const ModelSpec& s = t.spec;
+  const int E = s.experts_per_layer, K = s.top_k, H = s.hidden_dim;
+  const size_t n = t.steps.size();
+  if (n != static_cast<size_t>(t.batch_size) * s.num_layers)
+    throw std::invalid_argument("write_trace: steps != batch_size * num_layers");
+  std::vector<double> hid(n * H), gw(n * E);
+  std::vector<int32_t> act(n * K), tok(n * E, 0);
+  for (size_t i = 0; i < n; ++i) {
+    const TraceStep& st = t.steps[i];
+    if (st.hidden.size() != static_cast<size_t>(H) || st.gate_weights.size() != static_cast<size_t>(E) ||
+        st.active_experts.size() != static_cast<size_t>(K))
+      throw std::invalid_argument("write_trace: step vector sizes do not match the spec");
+    std::copy(st.hidden.begin(), st.hidden.end(), hid.begin() + i * H);
+    std::copy(st.gate_weights.begin(), st.gate_weights.end(), gw.begin() + i * E);
+    std::copy(st.active_experts.begin(), st.active_experts.end(), act.begin() + i * K);
+    for (auto [e, m] : st.tokens_per_expert) tok[i * E + e] = m;
+  }
+  const ps_model_spec cs = s.c();
+  detail::trace_throw_if(
+      ps_trace_write(path.c_str(), &cs, t.batch_size, t.seed, hid.data(), gw.data(), act.data(), tok.data()));
+}
+
+inline std::map<int, int> aggregate_layer_loads(const Trace& trace, int layer) {
+  std::map<int, int> loads;
+  for (int tok = 0; tok < trace.batch_size; ++tok)
+    for (auto [e, m] : trace.step(tok, layer).tokens_per_expert) loads[e] += m;
+  return loads;
 }
 inline int routing_map(const ModelSpec& spec, int expert) {
   ps_model_spec s = spec.c();

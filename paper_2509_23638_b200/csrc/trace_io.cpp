@@ -124,9 +124,11 @@ std::vector<std::string> split(const std::string& line, char sep) {
   return out;
 }
 
-// Whitespace-separated doubles / ints of one field; count must match.
+// Whitespace-separated doubles / ints of one field into out[0..want). Returns "" or the
+// problem (unparsable value or a count other than `want`); the caller decides whether it
+// is fatal now (syntax the reference parser also rejects) or after the checksum check.
 template <typename T>
-void parse_list(const std::string& f, size_t want, T* out, const char* what) {
+std::string parse_list(const std::string& f, size_t want, T* out, const char* what) {
   const char* c = f.c_str();
   size_t n = 0;
   while (true) {
@@ -137,13 +139,13 @@ void parse_list(const std::string& f, size_t want, T* out, const char* what) {
     T v;
     if constexpr (std::is_same_v<T, double>) v = std::strtod(c, &end);
     else v = static_cast<T>(std::strtol(c, &end, 10));
-    if (end == c || errno == ERANGE || (*end && *end != ' '))
-      format_error(std::string("trace body line: bad ") + what);
-    if (n >= want) format_error(std::string("trace body line: too many ") + what);
+    if (end == c || errno == ERANGE || (*end && *end != ' ')) return std::string("trace body line: bad ") + what;
+    if (n >= want) return std::string("trace body line: too many ") + what;
     out[n++] = v;
     c = end;
   }
-  if (n != want) format_error(std::string("trace body line: wrong number of ") + what);
+  if (n != want) return std::string("trace body line: wrong number of ") + what;
+  return {};
 }
 
 std::string header_line(const ps_model_spec& s, int batch, uint64_t seed, uint64_t checksum) {
@@ -197,6 +199,14 @@ void read_trace(const char* path, ps_trace_s& t) {
   t.gate_weights.assign(n_steps * E, 0.0);
   t.active.assign(n_steps * K, 0);
   t.tokens.assign(n_steps * E, 0);
+  // Syntax errors the reference's parse_step also throws on (field count, token map
+  // without ':') are raised at once; anything the reference would accept silently but a
+  // dense trace cannot hold (vector sizes, expert ids, step order/count) is deferred until
+  // after the checksum, so a corrupted file reports TraceChecksumError like the reference.
+  std::string deferred;
+  auto note = [&](const std::string& m) {
+    if (deferred.empty()) deferred = m;
+  };
   uint64_t h = 0xcbf29ce484222325ull;
   size_t i = 0;
   while (std::getline(in, line)) {
@@ -208,26 +218,31 @@ void read_trace(const char* path, ps_trace_s& t) {
     h *= 0x100000001b3ull;
     auto f = split(line, '\t');
     if (f.size() != 5) format_error("trace body line: expected 5 fields");
-    if (i >= n_steps) format_error("read_trace: more steps than batch_size * num_layers");
-    int32_t layer = 0;
-    parse_list(f[0], 1, &layer, "layer");
-    if (layer != static_cast<int32_t>(i % L)) format_error("read_trace: steps not in (token, layer) order");
-    parse_list(f[1], H, t.hidden.data() + i * H, "hidden");
-    parse_list(f[2], E, t.gate_weights.data() + i * E, "gate weights");
-    parse_list(f[3], K, t.active.data() + i * K, "active experts");
-    for (const std::string& pr : split(f[4], ' ')) {
-      if (pr.empty()) continue;
-      const size_t colon = pr.find(':');
-      if (colon == std::string::npos) format_error("trace body line: bad token map");
-      int32_t e = 0, m = 0;
-      parse_list(pr.substr(0, colon), 1, &e, "token map expert");
-      parse_list(pr.substr(colon + 1), 1, &m, "token map count");
-      if (e < 0 || e >= E) format_error("trace body line: token map expert out of range");
-      t.tokens[i * E + e] = m;
+    for (const std::string& pr : split(f[4], ' '))
+      if (!pr.empty() && pr.find(':') == std::string::npos) format_error("trace body line: bad token map");
+    if (i >= n_steps) note("read_trace: more steps than batch_size * num_layers");
+    if (deferred.empty()) {
+      int32_t layer = 0;
+      std::string err = parse_list(f[0], 1, &layer, "layer");
+      if (err.empty() && layer != static_cast<int32_t>(i % L)) err = "read_trace: steps not in (token, layer) order";
+      if (err.empty()) err = parse_list(f[1], H, t.hidden.data() + i * H, "hidden");
+      if (err.empty()) err = parse_list(f[2], E, t.gate_weights.data() + i * E, "gate weights");
+      if (err.empty()) err = parse_list(f[3], K, t.active.data() + i * K, "active experts");
+      for (const std::string& pr : split(f[4], ' ')) {
+        if (pr.empty() || !err.empty()) continue;
+        const size_t colon = pr.find(':');
+        int32_t e = 0, m = 0;
+        err = parse_list(pr.substr(0, colon), 1, &e, "token map expert");
+        if (err.empty()) err = parse_list(pr.substr(colon + 1), 1, &m, "token map count");
+        if (err.empty() && (e < 0 || e >= E)) err = "trace body line: token map expert out of range";
+        if (err.empty()) t.tokens[i * E + e] = m;
+      }
+      if (!err.empty()) note(err);
     }
     ++i;
   }
   if (h != t.checksum) fail(PS_ERUNTIME, std::string("TraceChecksumError: read_trace: checksum mismatch in ") + path);
+  if (!deferred.empty()) format_error(deferred);
   if (i != n_steps) format_error("read_trace: fewer steps than batch_size * num_layers");
 }
 

@@ -92,6 +92,32 @@ int main() {
   Timeline bad = r.timeline;
   bad.events.push_back({100, 102, Resource::Gpu, EventKind::GpuExpert, 0, 7, 1});
   CHECK(!verify_timeline(bad, inst, p).empty());
+  // trace files (test_workload.cpp round-trip + checksum): a reference-written file reads
+  // into prescope::Trace, re-writes byte-identically, and a corrupted copy throws
+  // TraceChecksumError (PRESCOPE_GOLDEN_TRACE points at tests/golden/ref_trace_desk.tsv).
+  if (const char* gold = std::getenv("PRESCOPE_GOLDEN_TRACE")) {
+    Trace t = read_trace(gold);
+    CHECK(t.batch_size == 3 && t.seed == 17 && t.spec.num_layers == 4 && t.steps.size() == 12);
+    CHECK(t.step(2, 3).layer == 3 && t.step(0, 0).active_experts.size() == 2);
+    CHECK(topk_indices(t.step(1, 2).gate_weights, 2) == t.step(1, 2).active_experts);
+    int total = 0;
+    for (auto [e, m] : aggregate_layer_loads(t, 1)) total += m;
+    CHECK(total == 3 * 2);
+    const std::string out = std::string(gold) + ".shim_rt.tsv";
+    write_trace(t, out);
+    CHECK(read_trace(out) == t);
+    {
+      std::FILE* f = std::fopen(out.c_str(), "r+b");
+      CHECK(f != nullptr);
+      std::fseek(f, -5, SEEK_END);
+      std::fputc('9', f);
+      std::fclose(f);
+    }
+    CHECK(throws<TraceChecksumError>([&] { read_trace(out); }));
+    CHECK(throws<std::out_of_range>([&] { t.step(3, 0); }));
+    std::remove(out.c_str());
+  }
+
   std::printf("shim ok\n");
   return 0;
 }

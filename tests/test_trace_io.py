@@ -126,3 +126,25 @@ def test_reference_reads_our_trace(tmp_path):
     orc.ref_check(orc.ref_lib().ref_read_trace(str(p).encode(), C.byref(b), C.byref(seed), act.ctypes.data, act.size))
     assert (b.value, seed.value) == (t.batch_size, 99)
     np.testing.assert_array_equal(act, t.active.ravel())
+
+
+def test_semantic_errors_after_checksum(tmp_path):
+    """Files the reference would parse but a dense trace cannot hold (extra hidden value,
+    expert id >= E) raise TraceFormatError when their checksum is valid, and
+    TraceChecksumError when it is not (the reference checks the checksum after parsing)."""
+    lib = ps.load()
+    raw = (GOLD / "ref_trace_desk.tsv").read_bytes()
+    head, body = raw.split(b"\n", 1)
+    lines = body.split(b"\n")
+    f = lines[0].split(b"\t")
+    f[1] = f[1] + b" 0.5"
+    lines[0] = b"\t".join(f)
+    nb = b"\n".join(lines)
+    hdr = json.loads(head)
+    hdr["checksum"] = lib.ps_fnv1a64(nb, len(nb))
+    good_head = json.dumps(hdr, separators=(",", ":"), sort_keys=True).encode()
+    p = tmp_path / "sem.tsv"
+    p.write_bytes(good_head + b"\n" + nb)
+    _expect_error(p, "too many hidden")
+    p.write_bytes(head + b"\n" + nb)  # stale checksum
+    _expect_error(p, "TraceChecksumError")
