@@ -172,7 +172,9 @@ def workload_config(args, spec, executor="gpu_only"):
                         f"({n_res}/{L * E} experts resident, hot-table residency from a warm-up trace), "
                         f"other experts in pinned host DRAM, policy {args.policy}"
                         + (", PreSched cpu_set on the host expert lane (AMX-BF16)" if executor == "host_lane" else
-                           ", GPU-only executor"),
+                           ", GPU-only executor")
+                        + (", loads as lossless 12-bit z-slabs decoded on the GPU" if getattr(args, "compress", 0)
+                           else ""),
             "model": f"{args.model}-8x7b-shape" if args.model == "mixtral" else args.model,
             "global_batch": args.batch * args.gpus, "seq_len": 1, "parallelism": (f"ep{args.gpus}" if args.gpus > 1 else "single"),
             "budget_fraction": args.budget, "policy": args.policy,
@@ -233,7 +235,7 @@ def run_ours(args):
     t_create = time.perf_counter()
     e = eng.Engine(spec, gen, max_batch=B, weight_seed=args.weight_seed, gate=gate, budget_bytes=budget_bytes,
                    resident=resident, policy=args.policy, predictor=predictor, device=local, ep=ep,
-                   host_threads=host_threads if world == 1 else 0)
+                   host_threads=host_threads if world == 1 else 0, compress_host=bool(args.compress))
     t_create = time.perf_counter() - t_create
     measured_cost = e.stats()["cost"]
 
@@ -438,6 +440,10 @@ def decode_summary(st, dev_ms, N, B, L):
            "moe_layer_us": dev_ms * 1e3 / L,
            "h2d": {"achieved_gbs": h2d_gbs, "peak_gbs": PCIE_H2D_PEAK_GBS, "frac": h2d_gbs / PCIE_H2D_PEAK_GBS,
                    "bytes_per_step": st["h2d_bytes"] / steps,
+                   # expert bytes delivered per second of copy time (z-slabs: > the link rate)
+                   "expert_gbs": st["h2d_expert_bytes"] / (st["h2d_busy_ms"] / 1e3) / 1e9 if st["h2d_busy_ms"] > 0
+                   else 0.0,
+                   "z_ratio": st["h2d_bytes"] / st["h2d_expert_bytes"] if st["h2d_expert_bytes"] > 0 else None,
                    "ondemand_loads_per_step": st["ondemand_loads"] / steps,
                    "prefetches_per_step": st["prefetches_committed"] / steps,
                    "prefetch_hits_per_step": st["prefetch_hits"] / steps,
@@ -476,6 +482,8 @@ def main():
     ap.add_argument("--no-all-resident", action="store_true")
     ap.add_argument("--prefill-tokens", type=int, default=4096)
     ap.add_argument("--prefill-steps", type=int, default=3)
+    ap.add_argument("--compress", type=int, default=1,
+                    help="1: non-resident experts cross PCIe as lossless z-slabs (decoded on the GPU)")
     ap.add_argument("--host-threads", type=int, default=-1,
                     help="host expert lane threads (-1 auto, 0 = GPU-only executor)")
     args = ap.parse_args()

@@ -380,6 +380,18 @@ ps_status ps_host_expert_ffn_batch(ps_host_lane lane, int n, const uint16_t* con
                                    const int32_t* m, const int32_t* row0, int H, int F,
                                    const uint16_t* x, float* y);
 
+/* z-slabs: lossless transfer format of a host-resident expert slab (csrc/zexpert.cu):
+ * verbatim sign+mantissa bytes, 4-bit exponent codes relative to a per-slab base, escapes
+ * for the rest (~12 bits per bf16 value), so PCIe moves ~75 % of the bytes. Decoding is
+ * bit-exact. Encode on the host (at engine create), decode on the GPU after the copy. */
+uint64_t ps_zslab_bound(uint64_t n);  /* worst-case z-slab bytes for n bf16 values */
+ps_status ps_zslab_encode(const uint16_t* slab, uint64_t n, uint8_t* out, uint64_t cap,
+                          uint64_t* out_bytes, int threads);
+ps_status ps_zslab_info(const uint8_t* z_host, uint64_t* n, uint64_t* bytes, uint64_t* n_escapes);
+/* z_dev: device copy of the z-slab; z_host_header: the host z-slab (header read on the host). */
+ps_status ps_zslab_decode(const uint8_t* z_dev, const uint8_t* z_host_header, uint16_t* out,
+                          void* stream);
+
 /* K4 — LLaPor predictor (predictor.cpp:116-124, 166-247, 344-352, 669-672). */
 typedef struct ps_llapor_s* ps_llapor;
 /* load_checkpoint (predictor.cpp:866-929): LLPC v1 file -> device-resident nets. */
@@ -462,6 +474,8 @@ typedef struct {
                                threads runs PreSched's cpu_set from pinned host DRAM,
                                concurrently with the PCIe loads; beta/startup are then
                                measured at create (unless cost.t_io > 0). 0 = GPU only. */
+  int32_t compress_host;    /* 1: host slabs also kept as z-slabs (ps_zslab_encode at create);
+                               loads move the z-slab over PCIe and decode it on the GPU */
 } ps_engine_config;
 
 ps_status ps_engine_create(const ps_engine_config* cfg, ps_engine* out);
@@ -501,6 +515,9 @@ typedef struct {
   int64_t cpu_experts;      /* experts run on the host lane */
   double cpu_ms_total;      /* host-lane busy time (wall clock) */
   double cpu_bytes_total;   /* expert bytes the host lane streamed */
+  int64_t z_decodes;        /* z-slab decodes (compressed loads landed) */
+  double h2d_expert_bytes;  /* expert bytes the issued copies delivered (= h2d_bytes
+                               without compression) */
 } ps_engine_stats;
 ps_status ps_engine_get_stats(ps_engine e, ps_engine_stats* out);
 ps_status ps_engine_reset_stats(ps_engine e);

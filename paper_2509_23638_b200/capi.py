@@ -114,7 +114,7 @@ class EngineConfig(C.Structure):
                 ("max_batch", C.c_int32), ("prefetch_slots", C.c_int32), ("policy", Policy),
                 ("cost", CostParams), ("predictor", C.c_void_p), ("device", C.c_int32),
                 ("host_pinned", C.c_int32), ("ep", C.c_void_p), ("n_shared", C.c_int32),
-                ("host_threads", C.c_int32)]
+                ("host_threads", C.c_int32), ("compress_host", C.c_int32)]
 
 
 class EngineStats(C.Structure):
@@ -127,7 +127,7 @@ class EngineStats(C.Structure):
                 ("ffn_flops_total", C.c_double), ("tc_launches", C.c_int64), ("ffn_launches", C.c_int64),
                 ("kernel_launches", C.c_int64),
                 ("cost", CostParams), ("cpu_experts", C.c_int64), ("cpu_ms_total", C.c_double),
-                ("cpu_bytes_total", C.c_double)]
+                ("cpu_bytes_total", C.c_double), ("z_decodes", C.c_int64), ("h2d_expert_bytes", C.c_double)]
 
 
 PLAN_FN = C.CFUNCTYPE(C.c_int, C.c_void_p, C.POINTER(LayerInputs), C.c_int, C.POINTER(LayerPlan))
@@ -187,6 +187,10 @@ _SIGS = {
     "ps_host_expert_ffn_batch": (C.c_int, [_P, C.c_int, _P, _P, _P, C.c_int, C.c_int, _P, _P]),
     "ps_cast_bf16": (C.c_int, [_P, C.c_int64, _P, _P]),
     "ps_engine_decode_step_routed": (C.c_int, [_P, _P, _P, _P, C.c_int, _P]),
+    "ps_zslab_bound": (C.c_uint64, [C.c_uint64]),
+    "ps_zslab_encode": (C.c_int, [_P, C.c_uint64, _P, C.c_uint64, C.POINTER(C.c_uint64), C.c_int]),
+    "ps_zslab_info": (C.c_int, [_P, C.POINTER(C.c_uint64), C.POINTER(C.c_uint64), C.POINTER(C.c_uint64)]),
+    "ps_zslab_decode": (C.c_int, [_P, _P, _P, _P]),
     "ps_append_shared": (C.c_int, [_P, _P, C.c_int, C.c_int, C.c_int, C.c_int, _P, _P, _P, _P]),
     "ps_expert_ffn": (C.c_int, [C.POINTER(ExpertGroup), _P, _P, _P, C.c_int, _P, C.c_int, C.c_int, _P, _P,
                                 C.c_int, C.c_int, _P]),

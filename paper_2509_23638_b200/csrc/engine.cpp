@@ -48,6 +48,7 @@ double now_us() {
 
 struct Slot {
   void* dev = nullptr;
+  void* zdev = nullptr;            // landing buffer of a z-slab copy (decoded into dev)
   cudaEvent_t free_ev = nullptr;   // recorded on the compute stream after the last reader
   std::atomic<int64_t> recorded_gen{0};
   int64_t next_gen = 0;            // generation a new copy must wait for
@@ -69,6 +70,7 @@ struct IoJob {
   std::atomic<int> state{0};   // 0 queued, 1 issued, 2 cancelled
   bool critical = false;
   int issue_group = 1;
+  const uint8_t* zhost = nullptr;  // z-slab source (header read on the host), null = raw copy
 };
 
 // The serial I/O channel: one copy stream, one host thread, FIFO with cancel.
@@ -342,6 +344,12 @@ struct ps_engine_s {
   std::vector<uint8_t> has_host;          // [L]: layer has an owned non-resident expert
   void* arena = nullptr;                  // resident HBM arena
   void* host_arena = nullptr;             // pinned host arena
+  // z-slabs (cfg.compress_host): lossless ~12-bit copies of the host slabs that PCIe
+  // carries instead (decoded on the GPU); the raw arena stays for the host lane.
+  void* z_arena = nullptr;
+  size_t z_cap = 0;                        // bytes per z-slab slot
+  std::vector<const uint8_t*> host_z;      // [L*E] or empty
+  std::vector<uint64_t> host_z_bytes;      // [L*E]
   ps::Slot od_slot[2];
   std::vector<std::unique_ptr<ps::Slot>> pf_pool;
 
@@ -535,6 +543,7 @@ Slot* take_prefetch_slot(ps_engine_s& e, int target) {
     }
   auto s = std::make_unique<Slot>();
   PS_CUDA(cudaMalloc(&s->dev, e.cfg.spec.expert_bytes));
+  if (e.z_cap) PS_CUDA(cudaMalloc(&s->zdev, e.z_cap));
   PS_CUDA(cudaEventCreateWithFlags(&s->free_ev, cudaEventDisableTiming));
   s->in_use = true;
   s->target_layer = target;
@@ -557,15 +566,35 @@ IoJob* new_job(ps_engine_s& e, int kind, int layer, int expert, int tokens, Slot
   j->expert = expert;
   j->tokens = tokens;
   j->slot = slot;
+  const size_t idx = static_cast<size_t>(layer) * e.E + expert;
   j->dst = slot->dev;
-  j->src = e.host_slab[static_cast<size_t>(layer) * e.E + expert];
+  j->src = e.host_slab[idx];
   if (!j->src) fail(PS_ERUNTIME, "engine: expert has no host copy");
   j->bytes = e.cfg.spec.expert_bytes;
+  if (!e.host_z.empty() && e.host_z[idx]) {  // z-slab: PCIe moves ~75 %, decoded on the GPU
+    j->zhost = e.host_z[idx];
+    j->src = e.host_z[idx];
+    j->dst = slot->zdev;
+    j->bytes = e.host_z_bytes[idx];
+  }
   j->wait_gen = slot->next_gen;  // the slot's latest reader must be done
   j->start_ev = take_job_event(e);
   j->done_ev = take_job_event(e);
   e.jobs.push_back(std::move(j));
   return e.jobs.back().get();
+}
+
+// Make a landed copy usable by the FFN: after the copy event, decode a z-slab into the
+// slot's bf16 buffer (no-op for raw copies). Compute stream.
+void land(ps_engine_s& e, IoJob* j) {
+  PS_CUDA(cudaStreamWaitEvent(e.sc, j->done_ev, 0));
+  if (j->zhost) {
+    if (ps_zslab_decode(static_cast<const uint8_t*>(j->dst), j->zhost, static_cast<uint16_t*>(j->slot->dev), e.sc) !=
+        PS_OK)
+      fail(PS_ECUDA, ps_last_error());
+    e.st.kernel_launches += 1;
+    e.st.z_decodes += 1;
+  }
 }
 
 double push_modelled(ps_engine_s& e) {  // channel busy-until model for alpha (R4)
@@ -863,7 +892,7 @@ void decode_step(ps_engine_s& e, const float* hidden, const uint8_t* follow, int
     };
     for (auto& r : e.ready) {
       if (r.layer != l || counts_l[r.expert] == 0) continue;
-      PS_CUDA(cudaStreamWaitEvent(e.sc, r.job->done_ev, 0));
+      land(e, r.job);
       ps_expert_group one{};
       one.n = 1;
       one.experts[0] = r.expert;
@@ -941,12 +970,13 @@ void decode_step(ps_engine_s& e, const float* hidden, const uint8_t* follow, int
       PS_CUDA(cudaEventRecord(p.before, e.sc));
       PS_CUDA(cudaStreamWaitEvent(e.sc, job->done_ev, 0));
       PS_CUDA(cudaEventRecord(p.after, e.sc));
+      land(e, job);
       e.stall_t.push_back(p);
       ps_expert_group one{};
       one.n = 1;
       one.experts[0] = job->expert;
-      one.slabs[0] = static_cast<const uint16_t*>(job->dst);
-      ffn(e, one, counts_l.data(), B, true, true, p.after);
+      one.slabs[0] = static_cast<const uint16_t*>(job->slot->dev);
+      ffn(e, one, counts_l.data(), B, true, true, job->zhost ? nullptr : p.after);
       release_slot_after_compute(e, job->slot);
       e.st.ondemand_loads++;
     }
@@ -1096,6 +1126,7 @@ void decode_step(ps_engine_s& e, const float* hidden, const uint8_t* follow, int
     PS_CUDA(cudaEventElapsedTime(&ms, j->start_ev, j->done_ev));
     e.st.h2d_busy_ms += ms;
     e.st.h2d_bytes += static_cast<double>(j->bytes);  // issued copies only (cancelled prefetches moved nothing)
+    e.st.h2d_expert_bytes += static_cast<double>(e.cfg.spec.expert_bytes);
     e.copy_ms_total += ms;
     e.copies += 1;
     e.last_events.push_back({at_us(j->start_ev), at_us(j->done_ev), PS_RES_IO,
@@ -1222,8 +1253,36 @@ void create_engine(const ps_engine_config& cfg, ps_engine_s& e) {
   PS_CUDA(cudaStreamSynchronize(e.sc));
   if (stage) cudaFree(stage);
 
+  // z-slabs: encode every host slab once (all host cores), keep raw ones that do not fit.
+  if (cfg.compress_host && n_host) {
+    const uint64_t n = sp.expert_bytes / 2, nb = (n + 1023) / 1024, n_pad = nb * 1024;
+    e.z_cap = ((64 + n_pad + n_pad / 2 + 4 * (nb + 1) + n / 64) + 4095) / 4096 * 4096;
+    PS_CUDA(cudaHostAlloc(&e.z_arena, n_host * e.z_cap, cudaHostAllocPortable));
+    e.host_z.assign(LE, nullptr);
+    e.host_z_bytes.assign(LE, 0);
+    size_t zi = 0;
+    for (size_t idx = 0; idx < LE; ++idx) {
+      if (!e.host_slab[idx]) continue;
+      uint8_t* z = static_cast<uint8_t*>(e.z_arena) + zi++ * e.z_cap;
+      uint64_t bytes = 0;
+      if (ps_zslab_encode(e.host_slab[idx], n, z, e.z_cap, &bytes, 0) == PS_OK) {
+        e.host_z[idx] = z;
+        e.host_z_bytes[idx] = bytes;
+      }
+    }
+  }
+  if (auto_cost && e.z_cap) {  // provisional t_io from the mean z-slab size
+    double zb = 0, cnt = 0;
+    for (uint64_t b : e.host_z_bytes)
+      if (b) {
+        zb += static_cast<double>(b);
+        cnt += 1;
+      }
+    if (cnt > 0) e.cfg.cost.t_io = std::max<int64_t>(e.cfg.cost.t_g + 1, static_cast<int64_t>(zb / cnt / 55e3));
+  }
   for (auto& s : e.od_slot) {
     PS_CUDA(cudaMalloc(&s.dev, sp.expert_bytes));
+    if (e.z_cap) PS_CUDA(cudaMalloc(&s.zdev, e.z_cap));
     PS_CUDA(cudaEventCreateWithFlags(&s.free_ev, cudaEventDisableTiming));
   }
   // Prefetch slots for two live target layers (R8 cap per layer) up front: a cudaMalloc
@@ -1231,6 +1290,7 @@ void create_engine(const ps_engine_config& cfg, ps_engine_s& e) {
   for (size_t i = 0; i < std::min<size_t>(2 * static_cast<size_t>(e.cfg.prefetch_slots), n_host); ++i) {
     auto s = std::make_unique<Slot>();
     PS_CUDA(cudaMalloc(&s->dev, sp.expert_bytes));
+    if (e.z_cap) PS_CUDA(cudaMalloc(&s->zdev, e.z_cap));
     PS_CUDA(cudaEventCreateWithFlags(&s->free_ev, cudaEventDisableTiming));
     e.pf_pool.push_back(std::move(s));
   }
@@ -1368,13 +1428,16 @@ void destroy_engine(ps_engine_s& e) {
   if (e.ep_plan_host) cudaFreeHost(e.ep_plan_host);
   if (e.ep_host) cudaFreeHost(e.ep_host);
   if (e.host_arena) cudaFreeHost(e.host_arena);
+  if (e.z_arena) cudaFreeHost(e.z_arena);
   if (e.pinned_counts) cudaFreeHost(e.pinned_counts);
   for (auto& s : e.od_slot) {
     if (s.dev) cudaFree(s.dev);
+    if (s.zdev) cudaFree(s.zdev);
     if (s.free_ev) cudaEventDestroy(s.free_ev);
   }
   for (auto& s : e.pf_pool) {
     cudaFree(s->dev);
+    if (s->zdev) cudaFree(s->zdev);
     cudaEventDestroy(s->free_ev);
   }
   for (cudaEvent_t ev : e.event_pool) cudaEventDestroy(ev);

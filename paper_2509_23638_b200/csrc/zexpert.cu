@@ -1,0 +1,227 @@
+// Lossless transfer format for host-resident expert slabs ("z-slabs").
+//
+// The non-resident experts cross PCIe (55 GB/s) while the GPU streams HBM at 6.5 TB/s,
+// so every byte not sent over PCIe is worth ~100x its decode cost. bf16 weights of a
+// trained (or, here, synthetic Gaussian) matrix use only a narrow band of the 8-bit
+// exponent field: a slab is stored as
+//   lo    [n]        u8   sign << 7 | 7-bit mantissa        (verbatim)
+//   codes [n/2]      u8   two 4-bit exponent codes per byte: code c < 15 means
+//                         exponent = base + c; c = 15 is an escape
+//   esc_off [nb + 1] u32  prefix of escapes per 1024-value block
+//   esc   [n_esc]    u8   raw exponents of the escaped values, in value order
+// i.e. 12 bits per value + 1 byte per escape (~75 % of bf16). Decoding is bit-exact
+// (tests/test_gpu_zexpert.py), so every downstream result is identical to loading the
+// raw slab. Encoder: host C++ (at engine create, multithreaded over blocks); decoder:
+// one warp per 1024-value block, 32 values per lane, escape ranks by a warp scan,
+// 16-byte loads/stores (HBM-bound: 1.5 B read + 2 B written per value).
+#include <algorithm>
+#include <cstring>
+#include <thread>
+#include <vector>
+
+#include "device_common.cuh"
+
+namespace ps {
+namespace {
+
+constexpr int kZBlock = 1024;   // values per block
+constexpr int kZEscape = 15;
+
+struct ZHeader {  // at the start of every z-slab (64 bytes, keeps the streams 16-B aligned)
+  uint64_t magic;   // "PSZSLAB1"
+  uint64_t n;       // values (bf16 count)
+  uint32_t base;    // exponent of code 0
+  uint32_t nb;      // blocks
+  uint64_t n_esc;   // escaped values
+  uint64_t bytes;   // total z-slab bytes
+  uint64_t pad[3];
+};
+static_assert(sizeof(ZHeader) == 64, "z header");
+constexpr uint64_t kZMagic = 0x31424c534c5a5350ull;  // "PSZSLAB1"
+
+__host__ __device__ inline size_t z_lo_off() { return sizeof(ZHeader); }
+__host__ __device__ inline size_t z_codes_off(uint64_t n_pad) { return z_lo_off() + n_pad; }
+__host__ __device__ inline size_t z_escoff_off(uint64_t n_pad) { return z_codes_off(n_pad) + n_pad / 2; }
+__host__ __device__ inline size_t z_esc_off(uint64_t n_pad, uint32_t nb) { return z_escoff_off(n_pad) + 4ull * (nb + 1); }
+
+__global__ void z_decode_kernel(const uint8_t* __restrict__ z, uint64_t n, uint32_t base, uint32_t nb,
+                                uint16_t* __restrict__ out) {
+  const uint64_t n_pad = static_cast<uint64_t>(nb) * kZBlock;
+  const uint8_t* lo = z + z_lo_off();
+  const uint8_t* codes = z + z_codes_off(n_pad);
+  const uint32_t* esc_off = reinterpret_cast<const uint32_t*>(z + z_escoff_off(n_pad));
+  const uint8_t* esc = z + z_esc_off(n_pad, nb);
+  const int lane = threadIdx.x & 31;
+  const uint32_t warps = (gridDim.x * blockDim.x) >> 5;
+  for (uint32_t b = (blockIdx.x * blockDim.x + threadIdx.x) >> 5; b < nb; b += warps) {
+    const uint64_t v0 = static_cast<uint64_t>(b) * kZBlock + lane * 32;  // this lane's 32 values
+    const uint4 l0 = *reinterpret_cast<const uint4*>(lo + v0);
+    const uint4 l1 = *reinterpret_cast<const uint4*>(lo + v0 + 16);
+    const uint4 cw = *reinterpret_cast<const uint4*>(codes + v0 / 2);
+    const uint32_t lw[8] = {l0.x, l0.y, l0.z, l0.w, l1.x, l1.y, l1.z, l1.w};
+    const uint32_t cv[4] = {cw.x, cw.y, cw.z, cw.w};
+    int n_e = 0;
+#pragma unroll
+    for (int q = 0; q < 4; ++q)
+#pragma unroll
+      for (int j = 0; j < 8; ++j) n_e += ((cv[q] >> (4 * j)) & 15u) == kZEscape;
+    int incl = n_e;  // warp inclusive scan of escape counts
+#pragma unroll
+    for (int o = 1; o < 32; o <<= 1) {
+      const int t = __shfl_up_sync(0xffffffffu, incl, o);
+      if (lane >= o) incl += t;
+    }
+    uint32_t e_at = esc_off[b] + static_cast<uint32_t>(incl - n_e);
+    uint32_t packed[16];
+#pragma unroll
+    for (int i = 0; i < 32; ++i) {
+      const uint32_t c = (cv[i >> 3] >> (4 * (i & 7))) & 15u;
+      const uint32_t l = (lw[i >> 2] >> (8 * (i & 3))) & 0xffu;
+      const uint32_t ex = c == kZEscape ? esc[e_at++] : base + c;
+      const uint32_t v = ((l & 0x80u) << 8) | (ex << 7) | (l & 0x7fu);
+      if (i & 1) packed[i >> 1] |= v << 16;
+      else packed[i >> 1] = v;
+    }
+    if (v0 + 32 <= n) {
+      uint4* dst = reinterpret_cast<uint4*>(out + v0);
+#pragma unroll
+      for (int q = 0; q < 4; ++q)
+        dst[q] = make_uint4(packed[4 * q], packed[4 * q + 1], packed[4 * q + 2], packed[4 * q + 3]);
+    } else {
+      for (int i = 0; i < 32 && v0 + i < n; ++i)
+        out[v0 + i] = static_cast<uint16_t>(packed[i >> 1] >> (16 * (i & 1)));
+    }
+  }
+}
+
+template <typename F>
+void parallel_blocks(uint32_t nb, int threads, F&& f) {
+  threads = std::max(1, std::min<int>(threads, static_cast<int>(nb)));
+  std::vector<std::thread> ts;
+  for (int t = 0; t < threads; ++t)
+    ts.emplace_back([&, t] {
+      for (uint32_t b = static_cast<uint32_t>(static_cast<uint64_t>(nb) * t / threads);
+           b < static_cast<uint64_t>(nb) * (t + 1) / threads; ++b)
+        f(b);
+    });
+  for (auto& th : ts) th.join();
+}
+
+}  // namespace
+}  // namespace ps
+
+using namespace ps;
+
+extern "C" {
+
+uint64_t ps_zslab_bound(uint64_t n) {
+  const uint64_t nb = (n + kZBlock - 1) / kZBlock, n_pad = nb * kZBlock;
+  return z_esc_off(n_pad, static_cast<uint32_t>(nb)) + n_pad;  // worst case: every value escaped
+}
+
+ps_status ps_zslab_encode(const uint16_t* slab, uint64_t n, uint8_t* out, uint64_t cap, uint64_t* out_bytes,
+                          int threads) {
+  return guarded([&] {
+    require(slab && out && out_bytes && n > 0, "ps_zslab_encode: bad arguments");
+    const uint32_t nb = static_cast<uint32_t>((n + kZBlock - 1) / kZBlock);
+    const uint64_t n_pad = static_cast<uint64_t>(nb) * kZBlock;
+    require(cap >= z_esc_off(n_pad, nb), "ps_zslab_encode: output too small");
+    threads = threads > 0 ? threads : static_cast<int>(std::max(1u, std::thread::hardware_concurrency()));
+    // exponent histogram (sampled every 7th value) -> the 15-wide window with most mass
+    std::vector<uint64_t> hist(256, 0);
+    for (uint64_t i = 0; i < n; i += 7) hist[(slab[i] >> 7) & 0xff]++;
+    uint32_t base = 0;
+    uint64_t best = 0;
+    for (uint32_t b = 0; b + 15 <= 256; ++b) {
+      uint64_t s = 0;
+      for (uint32_t j = 0; j < 15; ++j) s += hist[b + j];
+      if (s > best) {
+        best = s;
+        base = b;
+      }
+    }
+    uint8_t* lo = out + z_lo_off();
+    uint8_t* codes = out + z_codes_off(n_pad);
+    uint32_t* esc_off = reinterpret_cast<uint32_t*>(out + z_escoff_off(n_pad));
+    auto exp_of = [&](uint64_t i) { return i < n ? static_cast<uint32_t>((slab[i] >> 7) & 0xff) : base; };
+    auto escaped = [&](uint32_t e) { return e < base || e >= base + kZEscape; };
+    // pass 1: lo bytes, codes, escape count per block (branch-free inner loop over
+    // full blocks; the ragged tail is padded with code-0 values)
+    std::vector<uint32_t> cnt(nb);
+    parallel_blocks(nb, threads, [&](uint32_t b) {
+      const uint64_t i0 = static_cast<uint64_t>(b) * kZBlock;
+      uint16_t tmp[kZBlock];
+      const uint16_t* src = slab + i0;
+      if (i0 + kZBlock > n) {
+        for (int k = 0; k < kZBlock; ++k) tmp[k] = i0 + k < n ? slab[i0 + k] : static_cast<uint16_t>(base << 7);
+        src = tmp;
+      }
+      uint32_t c = 0;
+      uint8_t* lo_b = lo + i0;
+      uint8_t* co_b = codes + i0 / 2;
+      for (int k = 0; k < kZBlock; k += 2) {
+        const uint32_t v0 = src[k], v1 = src[k + 1];
+        lo_b[k] = static_cast<uint8_t>(((v0 >> 8) & 0x80u) | (v0 & 0x7fu));
+        lo_b[k + 1] = static_cast<uint8_t>(((v1 >> 8) & 0x80u) | (v1 & 0x7fu));
+        const uint32_t d0 = ((v0 >> 7) & 0xffu) - base, d1 = ((v1 >> 7) & 0xffu) - base;  // wraps if below base
+        const uint32_t c0 = d0 < kZEscape ? d0 : kZEscape, c1 = d1 < kZEscape ? d1 : kZEscape;
+        c += (c0 == kZEscape) + (c1 == kZEscape);
+        co_b[k / 2] = static_cast<uint8_t>(c0 | (c1 << 4));
+      }
+      cnt[b] = c;
+    });
+    esc_off[0] = 0;
+    for (uint32_t b = 0; b < nb; ++b) esc_off[b + 1] = esc_off[b] + cnt[b];
+    const uint64_t n_esc = esc_off[nb];
+    const uint64_t bytes = (z_esc_off(n_pad, nb) + n_esc + 15) / 16 * 16;
+    require(cap >= bytes, "ps_zslab_encode: output too small for the escapes");
+    uint8_t* esc = out + z_esc_off(n_pad, nb);
+    // pass 2: escaped exponents in value order
+    parallel_blocks(nb, threads, [&](uint32_t b) {
+      uint32_t at = esc_off[b];
+      for (uint64_t i = static_cast<uint64_t>(b) * kZBlock; i < static_cast<uint64_t>(b + 1) * kZBlock; ++i) {
+        const uint32_t e = exp_of(i);
+        if (escaped(e)) esc[at++] = static_cast<uint8_t>(e);
+      }
+    });
+    ZHeader h{};
+    h.magic = kZMagic;
+    h.n = n;
+    h.base = base;
+    h.nb = nb;
+    h.n_esc = n_esc;
+    h.bytes = bytes;
+    std::memcpy(out, &h, sizeof(h));
+    *out_bytes = bytes;
+  });
+}
+
+ps_status ps_zslab_info(const uint8_t* z_host, uint64_t* n, uint64_t* bytes, uint64_t* n_esc) {
+  return guarded([&] {
+    require(z_host != nullptr, "ps_zslab_info: null");
+    ZHeader h;
+    std::memcpy(&h, z_host, sizeof(h));
+    require(h.magic == kZMagic, "ps_zslab_info: not a z-slab");
+    if (n) *n = h.n;
+    if (bytes) *bytes = h.bytes;
+    if (n_esc) *n_esc = h.n_esc;
+  });
+}
+
+// Device decode: z (device copy of the z-slab) -> out [n] bf16. The header fields are
+// passed from the host (the caller keeps the host z-slab), so no device read-back.
+ps_status ps_zslab_decode(const uint8_t* z_dev, const uint8_t* z_host_header, uint16_t* out, void* stream) {
+  return guarded([&] {
+    require(z_dev && z_host_header && out, "ps_zslab_decode: null argument");
+    ZHeader h;
+    std::memcpy(&h, z_host_header, sizeof(h));
+    require(h.magic == kZMagic, "ps_zslab_decode: not a z-slab");
+    const int threads = 256;
+    const int grid = static_cast<int>(std::min<uint64_t>((static_cast<uint64_t>(h.nb) * 32 + threads - 1) / threads,
+                                                         8 * 148));
+    z_decode_kernel<<<grid, threads, 0, as_stream(stream)>>>(z_dev, h.n, h.base, h.nb, out);
+    PS_LAUNCH_CHECK("z_decode_kernel");
+  });
+}
+
+}  // extern "C"

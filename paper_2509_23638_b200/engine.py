@@ -99,7 +99,7 @@ class Engine:
                  gate: np.ndarray, budget_fraction: float | None = None, budget_bytes: int | None = None,
                  resident=None, trace_hidden=None, trace_follow=None, policy: str = "presched",
                  predictor=None, cost=None, prefetch_slots: int = 8, device: int = 0, ep=None,
-                 n_shared: int = 0, host_threads: int = 0):
+                 n_shared: int = 0, host_threads: int = 0, compress_host: bool = False):
         from . import parse_policy, plan_residency, trace_inputs  # noqa: F401
         self.lib = load()
         self.spec = spec
@@ -135,6 +135,7 @@ class Engine:
         cfg.ep = ep.h if isinstance(ep, EpComm) else ep
         cfg.n_shared = n_shared
         cfg.host_threads = host_threads
+        cfg.compress_host = int(bool(compress_host))
         self.host_threads = host_threads
         h = C.c_void_p()
         check(self.lib.ps_engine_create(C.byref(cfg), C.byref(h)))

@@ -33,12 +33,16 @@ import paper_2509_23638_b200 as ps  # noqa: E402
 from paper_2509_23638_b200 import engine as eng  # noqa: E402
 
 
+COMPRESS = True
+
+
 def make_engine(spec, gen, gate, freq, budget, B, predictor, host_threads, n_shared=0):
     L, E = spec.num_layers, spec.experts_per_layer
     budget_bytes = int(round(budget * L * E)) * spec.expert_bytes
     resident = ps.plan_residency(freq, budget_bytes, spec.expert_bytes)
     return eng.Engine(spec, gen, max_batch=B, weight_seed=1, gate=gate, budget_bytes=budget_bytes, resident=resident,
-                      policy="presched", predictor=predictor, host_threads=host_threads, n_shared=n_shared)
+                      policy="presched", predictor=predictor, host_threads=host_threads, n_shared=n_shared,
+                      compress_host=COMPRESS)
 
 
 def timed_steps(torch, e, hid, fol, y, warmup, steps, calibrate=False):
@@ -171,10 +175,13 @@ def main():
     ap.add_argument("--steps", type=int, default=3)
     ap.add_argument("--warmup", type=int, default=2)
     ap.add_argument("--host-threads", type=int, default=-1)
+    ap.add_argument("--compress", type=int, default=1)
     args = ap.parse_args()
     import torch
     torch.cuda.set_device(0)
     ht = args.host_threads if args.host_threads >= 0 else bench.default_host_threads()
+    global COMPRESS
+    COMPRESS = bool(args.compress)
     runs = {"qwen3": run_qwen3, "deepseek": run_deepseek, "mixtral-sweep": run_mixtral_sweep}
     for c in args.configs.split(","):
         t0 = time.perf_counter()
