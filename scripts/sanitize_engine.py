@@ -32,6 +32,8 @@ def main():
     run("mixtral", 3, 8, 256, 512, 8, 0.25, host_threads=2, cost=cost)
     run("deepseek", 3, 64, 256, 256, 8, 0.2, n_shared=2, host_threads=2, cost=cost)
     run("mixtral", 3, 8, 256, 512, 256, 0.5)
+    run("mixtral", 3, 8, 256, 512, 8, 0.25, compress_host=True)
+    run("mixtral", 3, 8, 256, 512, 256, 0.5, compress_host=True)
     print("sanitize run done")
 
 

@@ -50,7 +50,7 @@ def test_zslab_roundtrip_bit_exact(torch_cuda, case):
     np.testing.assert_array_equal(out.cpu().numpy().view(np.uint16), slab)
 
 
-@pytest.mark.parametrize("host_threads", [0, 2])
+@pytest.mark.parametrize("host_threads", [0, 2])  # 2: host lane + z-slabs in one engine
 def test_engine_zslab_loads_bitwise_equal(torch_cuda, host_threads):
     spec = ps.desk_scale("mixtral", 4, 8, 256)
     spec.expert_bytes = 6 * 256 * 512
@@ -68,6 +68,9 @@ def test_engine_zslab_loads_bitwise_equal(torch_cuda, host_threads):
             assert e.verify_last_step() == []
     np.testing.assert_array_equal(outs[0], outs[1])
     raw, zz = stats
+    if host_threads:  # PCIe priced high: the lane takes the set, outputs still identical
+        assert zz["cpu_experts"] > 0 and zz["cpu_experts"] == raw["cpu_experts"]
+        return
     loads = zz["ondemand_loads"] + zz["prefetches_committed"]
     assert zz["z_decodes"] >= zz["ondemand_loads"] and loads > 0
     assert zz["h2d_bytes"] < 0.77 * zz["h2d_expert_bytes"]
