@@ -374,6 +374,12 @@ int ps_host_lane_isa(ps_host_lane lane); /* 2 = AMX-BF16 tiles, 1 = AVX512-BF16 
 ps_status ps_host_lane_bind_caller(ps_host_lane lane);
 ps_status ps_host_expert_ffn(ps_host_lane lane, const uint16_t* slab, int H, int F, const uint16_t* x,
                              int m, float* y);
+/* Same, weights read from z-slabs (ps_zslab_encode of the slabs): 1.5 instead of 2 bytes
+ * of host DRAM per weight, decoded tile by tile in registers/L1 (AMX-BF16 lanes only,
+ * PS_ERUNTIME otherwise). Bitwise the results of the raw-slab call. */
+ps_status ps_host_expert_ffn_batch_z(ps_host_lane lane, int n, const uint8_t* const* zslabs,
+                                     const int32_t* m, const int32_t* row0, int H, int F,
+                                     const uint16_t* x, float* y);
 /* A layer's cpu_set in one call: expert j reads x rows [row0[j], row0[j] + m[j]) and
  * writes the same rows of y (both [*, H], host). Same numerics per expert. */
 ps_status ps_host_expert_ffn_batch(ps_host_lane lane, int n, const uint16_t* const* slabs,

@@ -23,6 +23,7 @@
 #include <chrono>
 #include <cmath>
 #include <condition_variable>
+#include <cstdlib>
 #include <cstring>
 #include <deque>
 #include <memory>
@@ -208,8 +209,21 @@ struct LayerDev {  // per-layer device outputs kept for the step
 struct CpuJob {
   int layer, expert, m, row0;
   const uint16_t* slab;
+  const uint8_t* z = nullptr;   // z-slab of the expert (lane reads 1.5 B/weight), null = raw
   double t0_us = 0, t1_us = 0;  // host clock, filled by the driver
 };
+
+// The lane can read z-slabs (1.5 instead of 2 B of host DRAM per weight) but decoding
+// them tile by tile costs more CPU than the bytes save on the 16-core B200 host (75-79
+// vs 88-135 GB/s of expert weights, profiles/r01_host_lane_micro_z.jsonl): raw bf16 by
+// default, PS_HOST_LANE_Z=1 opts in.
+bool lane_z_enabled() {
+  static const bool on = [] {
+    const char* v = std::getenv("PS_HOST_LANE_Z");
+    return v && v[0] == '1';
+  }();
+  return on;
+}
 
 class LaneDriver {
  public:
@@ -254,17 +268,24 @@ class LaneDriver {
       // expert of the set is reported with the batch's interval.
       std::string err;
       slabs_.clear();
+      zs_.clear();
       m_.clear();
       row0_.clear();
+      bool all_z = lane_z_enabled() && ps_host_lane_isa(lane_) == 2;
       for (const CpuJob& j : *jobs) {
         slabs_.push_back(j.slab);
+        zs_.push_back(j.z);
+        all_z = all_z && j.z;
         m_.push_back(j.m);
         row0_.push_back(j.row0);
       }
       const double t0 = now_us();
-      if (ps_host_expert_ffn_batch(lane_, static_cast<int>(jobs->size()), slabs_.data(), m_.data(), row0_.data(), H_,
-                                   F_, x_, y_) != PS_OK)
-        err = ps_last_error();
+      const int n = static_cast<int>(jobs->size());
+      const ps_status st = all_z ? ps_host_expert_ffn_batch_z(lane_, n, zs_.data(), m_.data(), row0_.data(), H_, F_,
+                                                              x_, y_)
+                                 : ps_host_expert_ffn_batch(lane_, n, slabs_.data(), m_.data(), row0_.data(), H_, F_,
+                                                            x_, y_);
+      if (st != PS_OK) err = ps_last_error();
       const double t1 = now_us();
       for (CpuJob& j : *jobs) {
         j.t0_us = t0;
@@ -287,6 +308,7 @@ class LaneDriver {
   bool stop_ = false, done_ = true;
   std::string err_;
   std::vector<const uint16_t*> slabs_;
+  std::vector<const uint8_t*> zs_;
   std::vector<int32_t> m_, row0_;
   std::thread thread_;  // last: starts after the members it uses
 };
@@ -943,6 +965,7 @@ void decode_step(ps_engine_s& e, const float* hidden, const uint8_t* follow, int
         const uint16_t* slab = e.host_slab[static_cast<size_t>(l) * E + ex];
         require(slab != nullptr, "host lane: cpu_set expert has no host copy");
         CpuJob j{l, ex, off[ex + 1] - off[ex], off[ex], slab};
+        if (!e.host_z.empty()) j.z = e.host_z[static_cast<size_t>(l) * E + ex];
         for (int r = j.row0; r < j.row0 + j.m; ++r)
           std::memcpy(e.lane_xrows + static_cast<size_t>(r) * H, e.lane_x + static_cast<size_t>(perm[r] / Kt) * H,
                       sizeof(uint16_t) * H);
@@ -1375,9 +1398,11 @@ void create_engine(const ps_engine_config& cfg, ps_engine_s& e) {
     // cpu_cost = beta*m + C (cost_model.cpp:34-37) measured on this host: the lane on a
     // host-resident expert slab at m = 1 and m = m2, best of 3 each.
     const uint16_t* probe = nullptr;
-    for (const uint16_t* p : e.host_slab)
-      if (p) {
-        probe = p;
+    const uint8_t* probe_z = nullptr;  // the lane reads z-slabs when they exist (AMX)
+    for (size_t i = 0; i < e.host_slab.size(); ++i)
+      if (e.host_slab[i]) {
+        probe = e.host_slab[i];
+        if (!e.host_z.empty() && lane_z_enabled() && ps_host_lane_isa(e.lane) == 2) probe_z = e.host_z[i];
         break;
       }
     if (auto_cost && probe) {
@@ -1386,8 +1411,11 @@ void create_engine(const ps_engine_config& cfg, ps_engine_s& e) {
         double t = 1e30;
         for (int r = 0; r < 3; ++r) {
           const double a = now_us();
-          if (ps_host_expert_ffn(e.lane, probe, e.H, e.F, e.lane_xrows, m, e.lane_yrows) != PS_OK)
-            fail(PS_ERUNTIME, ps_last_error());
+          const int32_t row0 = 0;
+          const ps_status st = probe_z ? ps_host_expert_ffn_batch_z(e.lane, 1, &probe_z, &m, &row0, e.H, e.F,
+                                                                    e.lane_xrows, e.lane_yrows)
+                                       : ps_host_expert_ffn(e.lane, probe, e.H, e.F, e.lane_xrows, m, e.lane_yrows);
+          if (st != PS_OK) fail(PS_ERUNTIME, ps_last_error());
           t = std::min(t, now_us() - a);
         }
         return t;

@@ -31,6 +31,7 @@
 #include <unistd.h>
 
 #include "common.hpp"
+#include "zslab_format.hpp"
 
 namespace ps {
 namespace {
@@ -256,6 +257,107 @@ void amx_down_block(const uint16_t* wd, const uint16_t* hb, int H, int F, int r,
 }
 
 __attribute__((target("amx-tile"))) void amx_release() { _tile_release(); }
+// ---- z-slab path: the lane reads the 12-bit transfer format instead of bf16 --------
+// Host DRAM is the lane's bound, so reading 1.5 B instead of 2 B per weight is worth a
+// few vector ops: each 16-row x 32-column A tile is decoded from the z-slab into a 1 KiB
+// scratch (AVX-512: sign/mantissa bytes widened to 16 bit, 4-bit exponent codes unpacked
+// and rebased, escapes patched from the block's escape list) and loaded from there.
+
+// Escaped exponents of the 32-value segment at value index v (v % 32 == 0, so the
+// segment lies in one 1024-value block): rank of the first one = escapes in the block
+// before v.
+inline void z_patch_escapes(const ZView& z, uint64_t v, uint16_t* seg) {
+  const uint64_t b = v / kZBlock;
+  uint32_t rank = 0;
+  for (uint64_t u = b * kZBlock; u < v; u += 2) {
+    const uint8_t c = z.codes[u / 2];
+    rank += (c & 15) == kZEscape;
+    rank += (c >> 4) == kZEscape;
+  }
+  const uint8_t* e = z.esc + z.esc_off[b] + rank;
+  for (int i = 0; i < 32; ++i) {
+    const uint8_t c = (z.codes[(v + i) / 2] >> (4 * ((v + i) & 1))) & 15;
+    if (c == kZEscape) seg[i] = static_cast<uint16_t>((seg[i] & 0x807fu) | (static_cast<uint32_t>(*e++) << 7));
+  }
+}
+
+// 32 values at v -> seg[32] bf16.
+__attribute__((target("avx512f,avx512bw,avx512vl")))
+inline void z_decode32(const ZView& z, uint64_t v, uint16_t* seg) {
+  const __m512i lo16 = _mm512_cvtepu8_epi16(_mm256_loadu_si256(reinterpret_cast<const __m256i*>(z.lo + v)));
+  const __m128i cb = _mm_loadu_si128(reinterpret_cast<const __m128i*>(z.codes + v / 2));
+  const __m128i nib = _mm_set1_epi8(0x0f);
+  const __m128i ev = _mm_and_si128(cb, nib), od = _mm_and_si128(_mm_srli_epi16(cb, 4), nib);
+  const __m256i codes8 = _mm256_set_m128i(_mm_unpackhi_epi8(ev, od), _mm_unpacklo_epi8(ev, od));
+  const __m512i code16 = _mm512_cvtepu8_epi16(codes8);
+  const __m512i exp16 = _mm512_add_epi16(code16, _mm512_set1_epi16(static_cast<short>(z.base)));
+  const __m512i val = _mm512_or_si512(
+      _mm512_or_si512(_mm512_slli_epi16(_mm512_and_si512(lo16, _mm512_set1_epi16(0x80)), 8),
+                      _mm512_slli_epi16(exp16, 7)),
+      _mm512_and_si512(lo16, _mm512_set1_epi16(0x7f)));
+  _mm512_storeu_si512(seg, val);
+  if (_mm512_cmpeq_epi16_mask(code16, _mm512_set1_epi16(kZEscape))) z_patch_escapes(z, v, seg);
+}
+
+// A tile (16 rows x 32 cols) of the row-major matrix whose row r starts at value `rowv`,
+// row length `ld` values, column k -> scratch [16][32]. The 16 rows are 32 streams (sign/
+// mantissa bytes and codes) — too many for the hardware prefetchers — so every row's
+// lines are prefetched 1 KiB of values ahead.
+__attribute__((target("avx512f,avx512bw,avx512vl")))
+inline void z_tile(const ZView& z, uint64_t rowv, uint64_t ld, int k, int kend, uint16_t* scratch) {
+  const int kp = k + 1024;
+  if (kp < kend)
+    for (int i = 0; i < 16; ++i) {
+      const uint64_t v = rowv + static_cast<uint64_t>(i) * ld + kp;
+      if ((k & 63) == 0) _mm_prefetch(reinterpret_cast<const char*>(z.lo + v), _MM_HINT_T0);
+      if ((k & 127) == 0) _mm_prefetch(reinterpret_cast<const char*>(z.codes + v / 2), _MM_HINT_T0);
+    }
+  for (int i = 0; i < 16; ++i) z_decode32(z, rowv + static_cast<uint64_t>(i) * ld + k, scratch + i * 32);
+}
+
+__attribute__((target("amx-tile,amx-bf16,avx512f,avx512bw,avx512vl")))
+void amx_gate_up_block_z(const ZView& z, int H, int F, const uint16_t* xb, int r, uint16_t* hb) {
+  alignas(64) float cg[16 * 16], cu[16 * 16];
+  alignas(64) uint16_t sg[16 * 32], su[16 * 32];
+  const uint64_t gv = static_cast<uint64_t>(r) * H, uv = (static_cast<uint64_t>(F) + r) * H;
+  _tile_zero(0);
+  _tile_zero(1);
+  for (int k = 0; k < H; k += 32) {
+    z_tile(z, gv, H, k, H, sg);
+    z_tile(z, uv, H, k, H, su);
+    _tile_loadd(2, sg, 64);
+    _tile_loadd(3, su, 64);
+    _tile_loadd(4, xb + static_cast<size_t>(k) * kTok, 64);
+    _tile_dpbf16ps(0, 2, 4);
+    _tile_dpbf16ps(1, 3, 4);
+  }
+  _tile_stored(0, cg, 64);
+  _tile_stored(1, cu, 64);
+  for (int i = 0; i < 16; ++i)
+    for (int t = 0; t < kTok; ++t) {
+      const float g = cg[i * 16 + t], u = cu[i * 16 + t];
+      hb[(static_cast<size_t>((r + i) >> 1) * kTok + t) * 2 + ((r + i) & 1)] = f32_to_bf16_rn(g / (1.0f + std::exp(-g)) * u);
+    }
+}
+
+__attribute__((target("amx-tile,amx-bf16,avx512f,avx512bw,avx512vl")))
+void amx_down_block_z(const ZView& z, const uint16_t* hb, int H, int F, int r, int m, float* y) {
+  alignas(64) float c[16 * 16];
+  alignas(64) uint16_t sd[16 * 32];
+  const uint64_t dv = 2ull * F * H + static_cast<uint64_t>(r) * F;
+  _tile_zero(0);
+  for (int k = 0; k < F; k += 32) {
+    z_tile(z, dv, F, k, F, sd);
+    _tile_loadd(2, sd, 64);
+    _tile_loadd(4, hb + static_cast<size_t>(k) * kTok, 64);
+    _tile_dpbf16ps(0, 2, 4);
+  }
+  _tile_stored(0, c, 64);
+  for (int t = 0; t < m; ++t)
+    for (int i = 0; i < 16; ++i) y[static_cast<size_t>(t) * H + r + i] = c[i * 16 + t];
+}
+
+
 
 template <typename Fn>
 void by_token_chunks(int m, Fn&& fn) {  // fn(template MT, t0)
@@ -426,6 +528,70 @@ ps_status ps_host_expert_ffn_batch(ps_host_lane l, int n, const uint16_t* const*
                                           H, F, y + static_cast<size_t>(row0[j] + t0) * H + r);
           });
       }
+    });
+  });
+}
+
+// Same as ps_host_expert_ffn_batch, weights read from z-slabs (AMX path only).
+ps_status ps_host_expert_ffn_batch_z(ps_host_lane l, int n, const uint8_t* const* zslabs, const int32_t* m,
+                                     const int32_t* row0, int H, int F, const uint16_t* x, float* y) {
+  return guarded([&] {
+    require(l && n >= 0 && (n == 0 || (zslabs && m && row0 && x && y)), "ps_host_expert_ffn_batch_z: null argument");
+    require(H > 0 && F > 0 && H % 32 == 0 && F % 32 == 0, "ps_host_expert_ffn_batch_z: H, F % 32 == 0");
+    if (!l->amx) fail(PS_ERUNTIME, "ps_host_expert_ffn_batch_z: needs AMX-BF16 (use the raw slabs)");
+    std::vector<ZView> zv;
+    for (int j = 0; j < n; ++j) {
+      require(zslabs[j] != nullptr && m[j] >= 0 && m[j] <= 4096 && row0[j] >= 0, "ps_host_expert_ffn_batch_z: bad job");
+      const ZHeader* h = reinterpret_cast<const ZHeader*>(zslabs[j]);
+      require(h->magic == kZMagic && h->n == 3ull * H * F, "ps_host_expert_ffn_batch_z: not a z-slab of this shape");
+      zv.emplace_back(zslabs[j]);
+    }
+    const int T = l->pool->size();
+    const int nb1 = F / 16, nb2 = H / 16;
+    const int64_t U1 = static_cast<int64_t>(n) * nb1, U2 = static_cast<int64_t>(n) * nb2;
+    std::vector<size_t> xo(n + 1, 0), ho(n + 1, 0);
+    for (int j = 0; j < n; ++j) {
+      const size_t G = (m[j] + kTok - 1) / kTok;
+      xo[j + 1] = xo[j] + G * H * kTok;
+      ho[j + 1] = ho[j] + G * F * kTok;
+    }
+    if (l->xb.size() < xo[n]) l->xb.resize(xo[n]);
+    if (l->hb.size() < ho[n]) l->hb.resize(ho[n]);
+    uint16_t* xb = l->xb.data();
+    uint16_t* hb = l->hb.data();
+    std::memset(xb, 0, sizeof(uint16_t) * xo[n]);
+    for (int j = 0; j < n; ++j)
+      for (int t = 0; t < m[j]; ++t) {
+        const uint16_t* xr = x + static_cast<size_t>(row0[j] + t) * H;
+        uint16_t* d = xb + xo[j] + static_cast<size_t>(t / kTok) * H * kTok + (t % kTok) * 2;
+        for (int k = 0; k < H; k += 2) {
+          d[static_cast<size_t>(k >> 1) * kTok * 2] = xr[k];
+          d[static_cast<size_t>(k >> 1) * kTok * 2 + 1] = xr[k + 1];
+        }
+      }
+    l->pool->run([&](int tid) {
+      const int64_t u0 = U1 * tid / T, u1 = U1 * (tid + 1) / T;
+      if (u0 == u1) return;
+      amx_config();
+      for (int64_t u = u0; u < u1; ++u) {
+        const int j = static_cast<int>(u / nb1), blk = static_cast<int>(u % nb1);
+        for (int g = 0; g * kTok < m[j]; ++g)
+          amx_gate_up_block_z(zv[j], H, F, xb + xo[j] + static_cast<size_t>(g) * H * kTok, blk * 16,
+                              hb + ho[j] + static_cast<size_t>(g) * F * kTok);
+      }
+      amx_release();
+    });
+    l->pool->run([&](int tid) {
+      const int64_t u0 = U2 * tid / T, u1 = U2 * (tid + 1) / T;
+      if (u0 == u1) return;
+      amx_config();
+      for (int64_t u = u0; u < u1; ++u) {
+        const int j = static_cast<int>(u / nb2), blk = static_cast<int>(u % nb2);
+        for (int g = 0; g * kTok < m[j]; ++g)
+          amx_down_block_z(zv[j], hb + ho[j] + static_cast<size_t>(g) * F * kTok, H, F, blk * 16,
+                           std::min(kTok, m[j] - g * kTok), y + static_cast<size_t>(row0[j] + g * kTok) * H);
+      }
+      amx_release();
     });
   });
 }

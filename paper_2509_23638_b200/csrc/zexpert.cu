@@ -20,29 +20,10 @@
 #include <vector>
 
 #include "device_common.cuh"
+#include "zslab_format.hpp"
 
 namespace ps {
 namespace {
-
-constexpr int kZBlock = 1024;   // values per block
-constexpr int kZEscape = 15;
-
-struct ZHeader {  // at the start of every z-slab (64 bytes, keeps the streams 16-B aligned)
-  uint64_t magic;   // "PSZSLAB1"
-  uint64_t n;       // values (bf16 count)
-  uint32_t base;    // exponent of code 0
-  uint32_t nb;      // blocks
-  uint64_t n_esc;   // escaped values
-  uint64_t bytes;   // total z-slab bytes
-  uint64_t pad[3];
-};
-static_assert(sizeof(ZHeader) == 64, "z header");
-constexpr uint64_t kZMagic = 0x31424c534c5a5350ull;  // "PSZSLAB1"
-
-__host__ __device__ inline size_t z_lo_off() { return sizeof(ZHeader); }
-__host__ __device__ inline size_t z_codes_off(uint64_t n_pad) { return z_lo_off() + n_pad; }
-__host__ __device__ inline size_t z_escoff_off(uint64_t n_pad) { return z_codes_off(n_pad) + n_pad / 2; }
-__host__ __device__ inline size_t z_esc_off(uint64_t n_pad, uint32_t nb) { return z_escoff_off(n_pad) + 4ull * (nb + 1); }
 
 __global__ void z_decode_kernel(const uint8_t* __restrict__ z, uint64_t n, uint32_t base, uint32_t nb,
                                 uint16_t* __restrict__ out) {

@@ -1,0 +1,53 @@
+// z-slab layout (lossless 12-bit transfer format of an expert slab; see zexpert.cu),
+// shared by the CUDA decoder and the host expert lane's AMX z-path.
+#pragma once
+#include <cstddef>
+#include <cstdint>
+
+#ifdef __CUDACC__
+#define PS_HD __host__ __device__
+#else
+#define PS_HD
+#endif
+
+namespace ps {
+
+constexpr int kZBlock = 1024;  // values per block (escape prefix granularity)
+constexpr int kZEscape = 15;   // 4-bit code of an escaped exponent
+
+struct ZHeader {  // at the start of every z-slab (64 bytes, keeps the streams 16-B aligned)
+  uint64_t magic;  // "PSZSLAB1"
+  uint64_t n;      // values (bf16 count)
+  uint32_t base;   // exponent of code 0
+  uint32_t nb;     // blocks
+  uint64_t n_esc;  // escaped values
+  uint64_t bytes;  // total z-slab bytes
+  uint64_t pad[3];
+};
+static_assert(sizeof(ZHeader) == 64, "z header");
+constexpr uint64_t kZMagic = 0x31424c534c5a5350ull;  // "PSZSLAB1"
+
+PS_HD inline size_t z_lo_off() { return sizeof(ZHeader); }
+PS_HD inline size_t z_codes_off(uint64_t n_pad) { return z_lo_off() + n_pad; }
+PS_HD inline size_t z_escoff_off(uint64_t n_pad) { return z_codes_off(n_pad) + n_pad / 2; }
+PS_HD inline size_t z_esc_off(uint64_t n_pad, uint32_t nb) { return z_escoff_off(n_pad) + 4ull * (nb + 1); }
+
+// Pointers into a z-slab (host view).
+struct ZView {
+  const uint8_t* lo;
+  const uint8_t* codes;
+  const uint32_t* esc_off;
+  const uint8_t* esc;
+  uint32_t base;
+  explicit ZView(const uint8_t* z) {
+    const ZHeader* h = reinterpret_cast<const ZHeader*>(z);
+    const uint64_t n_pad = static_cast<uint64_t>(h->nb) * kZBlock;
+    lo = z + z_lo_off();
+    codes = z + z_codes_off(n_pad);
+    esc_off = reinterpret_cast<const uint32_t*>(z + z_escoff_off(n_pad));
+    esc = z + z_esc_off(n_pad, h->nb);
+    base = h->base;
+  }
+};
+
+}  // namespace ps

@@ -26,6 +26,7 @@ def main():
     ap.add_argument("--slabs", type=int, default=4)
     ap.add_argument("--reps", type=int, default=8)
     ap.add_argument("--isa", default="")
+    ap.add_argument("--z", type=int, default=0, help="1: read z-slabs (ps_host_expert_ffn_batch_z)")
     args = ap.parse_args()
     import os
     if args.isa:
@@ -37,6 +38,15 @@ def main():
     slabs = [torch.empty(nbytes // 2, dtype=torch.int16).pin_memory() for _ in range(args.slabs)]
     for i, s in enumerate(slabs):
         ps.check(lib.ps_init_expert_slab_host(C.c_void_p(s.data_ptr()), H, F, 1, 0, i))
+    zs = []
+    if args.z:
+        for sl in slabs:
+            cap = lib.ps_zslab_bound(nbytes // 2)
+            z = torch.empty(cap, dtype=torch.uint8).pin_memory()
+            nb = C.c_uint64()
+            ps.check(lib.ps_zslab_encode(C.c_void_p(sl.data_ptr()), nbytes // 2, C.c_void_p(z.data_ptr()), cap,
+                                         C.byref(nb), 0))
+            zs.append(z)
     x = np.zeros((64, H), np.uint16)
     y = np.zeros((64, H), np.float32)
 
@@ -73,8 +83,14 @@ def main():
                 for r in range(args.reps):
                     s = slabs[r % len(slabs)]
                     t0 = time.perf_counter()
-                    ps.check(lib.ps_host_expert_ffn(lane, C.c_void_p(s.data_ptr()), H, F, x.ctypes.data, m,
-                                                    y.ctypes.data))
+                    if args.z:
+                        zp = (C.c_void_p * 1)(zs[r % len(zs)].data_ptr())
+                        mm, r0 = (C.c_int32 * 1)(m), (C.c_int32 * 1)(0)
+                        ps.check(lib.ps_host_expert_ffn_batch_z(lane, 1, zp, mm, r0, H, F, x.ctypes.data,
+                                                                y.ctypes.data))
+                    else:
+                        ps.check(lib.ps_host_expert_ffn(lane, C.c_void_p(s.data_ptr()), H, F, x.ctypes.data, m,
+                                                        y.ctypes.data))
                     ts.append(time.perf_counter() - t0)
                 dma_gbs = None
                 if th:
@@ -82,7 +98,7 @@ def main():
                     th.join()
                     dma_gbs = dma_bytes[0] / dma_bytes[1] / 1e9
                 ts.sort()
-                print(json.dumps({"threads": threads, "isa": isa, "tokens": m, "concurrent_h2d": concurrent,
+                print(json.dumps({"threads": threads, "isa": isa, "z": bool(args.z), "tokens": m, "concurrent_h2d": concurrent,
                                   "ms_median": ts[len(ts) // 2] * 1e3, "gbs_median": nbytes / ts[len(ts) // 2] / 1e9,
                                   "gbs_best": nbytes / ts[0] / 1e9, "h2d_gbs_during": dma_gbs}), flush=True)
         lib.ps_host_lane_destroy(lane)

@@ -131,3 +131,41 @@ def test_host_expert_ffn_batch_equals_single_calls(isa):
             np.testing.assert_array_equal(y[row0[j]:row0[j] + ms[j]], yj)
     finally:
         lib.ps_host_lane_destroy(lane)
+
+
+@needs_bf16
+@pytest.mark.skipif(not _has("amx_bf16"), reason="z-slab lane path needs AMX-BF16")
+@pytest.mark.parametrize("escapes", [False, True])
+def test_host_lane_reads_zslabs_bitwise(escapes):
+    """The lane's z-slab path (12-bit transfer format decoded per tile) gives bitwise the
+    raw-slab results, escapes included."""
+    lib = ps.load()
+    H, F = 256, 384
+    ms, row0 = [3, 17, 1], [0, 3, 20]
+    slabs, zs = [], []
+    rng = np.random.default_rng(11)
+    for e in range(3):
+        s = orc.or_init_slab(H, F, 2, 1, e)
+        if escapes:
+            idx = rng.choice(s.size, 3000, replace=False)
+            s[idx] = (rng.integers(0, 2, idx.size) << 15 | rng.integers(1, 200, idx.size) << 7 |
+                      rng.integers(0, 128, idx.size)).astype(np.uint16)  # finite, wide exponents
+        slabs.append(s)
+        cap = lib.ps_zslab_bound(s.size)
+        z = np.zeros(cap, np.uint8)
+        nb = C.c_uint64()
+        ps.check(lib.ps_zslab_encode(s.ctypes.data, s.size, z.ctypes.data, cap, C.byref(nb), 2))
+        zs.append(z)
+    x = orc.f32_to_bf16(rng.standard_normal((21, H)).astype(np.float32))
+    lane = _lane(3, "amx")
+    try:
+        m_a, r_a = np.array(ms, np.int32), np.array(row0, np.int32)
+        y_raw = np.full((21, H), np.nan, np.float32)
+        y_z = np.full((21, H), np.nan, np.float32)
+        ps.check(lib.ps_host_expert_ffn_batch(lane, 3, (C.c_void_p * 3)(*[s.ctypes.data for s in slabs]),
+                                              m_a.ctypes.data, r_a.ctypes.data, H, F, x.ctypes.data, y_raw.ctypes.data))
+        ps.check(lib.ps_host_expert_ffn_batch_z(lane, 3, (C.c_void_p * 3)(*[z.ctypes.data for z in zs]),
+                                                m_a.ctypes.data, r_a.ctypes.data, H, F, x.ctypes.data, y_z.ctypes.data))
+        np.testing.assert_array_equal(y_raw, y_z)
+    finally:
+        lib.ps_host_lane_destroy(lane)
