@@ -245,6 +245,11 @@ ps_status ps_verify_timeline(const ps_timeline_event* events, int n_events,
 ps_status ps_verify_timeline_ex(const ps_timeline_event* events, int n_events,
                                 const ps_pipeline_instance* inst, const ps_cost_params* params,
                                 int measured, int* n_violations, char* msg_buf, int msg_cap);
+/* export_timeline (simulator.cpp:428-436): "# tick_unit=us makespan=M" then one
+ * "t_start t_end resource kind layer expert tokens" line per event (same text as the
+ * reference). *needed = bytes incl. NUL; buf (nullable) receives at most cap-1 chars. */
+ps_status ps_export_timeline(const ps_timeline_event* events, int n, int64_t makespan, char* buf,
+                             int cap, int* needed);
 /* compute_metrics (simulator.cpp:396-426). per_layer arrays nullable [L]. */
 typedef struct {
   int64_t makespan, decode_latency;

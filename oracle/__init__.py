@@ -128,6 +128,8 @@ def ref_lib() -> C.CDLL:
         _ref.ref_generate_trace.argtypes = [C.POINTER(RefGen), C.POINTER(RefSpec), C.c_int, C.c_uint64,
                                             C.c_void_p, C.c_void_p, C.c_void_p]
         _ref.ref_write_trace.argtypes = [C.POINTER(RefGen), C.POINTER(RefSpec), C.c_int, C.c_uint64, C.c_char_p]
+        _ref.ref_export_timeline.argtypes = [C.c_void_p, C.c_int, C.c_int64, C.c_char_p, C.c_int,
+                                             C.POINTER(C.c_int)]
         _ref.ref_read_trace.argtypes = [C.c_char_p, C.POINTER(C.c_int), C.POINTER(C.c_uint64), C.c_void_p, C.c_int]
         _ref.ref_residency.argtypes = [C.POINTER(RefGen), C.POINTER(RefSpec), C.c_int, C.c_uint64, C.c_uint64,
                                        C.c_void_p, C.POINTER(C.c_int)]

@@ -398,6 +398,26 @@ int ref_verify_timeline(int L, const int32_t* truth, int n_truth, const int32_t*
   });
 }
 
+// export_timeline (simulator.cpp:428-436) of a caller-supplied event list.
+int ref_export_timeline(const ref_event* events, int n_events, int64_t makespan, char* buf, int cap, int* needed) {
+  return guarded([&] {
+    Timeline t;
+    t.makespan = makespan;
+    for (int i = 0; i < n_events; ++i) {
+      const ref_event& e = events[i];
+      t.events.push_back({e.t_start, e.t_end, static_cast<Resource>(e.resource), static_cast<EventKind>(e.kind),
+                          e.layer, e.expert, e.tokens});
+    }
+    const std::string s = export_timeline(t);
+    *needed = static_cast<int>(s.size()) + 1;
+    if (buf && cap > 0) {
+      const size_t n = std::min<size_t>(s.size(), static_cast<size_t>(cap - 1));
+      std::memcpy(buf, s.data(), n);
+      buf[n] = 0;
+    }
+  });
+}
+
 // Dumps the six golden scenarios (golden.cpp:61-234) with their hand-derived
 // timelines, plus the reference PreSched plans/timeline on each instance.
 int ref_dump_golden(const char* path) {

@@ -192,6 +192,7 @@ _SIGS = {
     "ps_zslab_encode": (C.c_int, [_P, C.c_uint64, _P, C.c_uint64, C.POINTER(C.c_uint64), C.c_int]),
     "ps_zslab_info": (C.c_int, [_P, C.POINTER(C.c_uint64), C.POINTER(C.c_uint64), C.POINTER(C.c_uint64)]),
     "ps_zslab_decode": (C.c_int, [_P, _P, _P, _P]),
+    "ps_export_timeline": (C.c_int, [_P, C.c_int, C.c_int64, C.c_char_p, C.c_int, C.POINTER(C.c_int)]),
     "ps_append_shared": (C.c_int, [_P, _P, C.c_int, C.c_int, C.c_int, C.c_int, _P, _P, _P, _P]),
     "ps_expert_ffn": (C.c_int, [C.POINTER(ExpertGroup), _P, _P, _P, C.c_int, _P, C.c_int, C.c_int, _P, _P,
                                 C.c_int, C.c_int, _P]),

@@ -31,6 +31,8 @@
 #include <thread>
 #include <vector>
 
+#include <nvtx3/nvToolsExt.h>
+
 #include "cuda_host.hpp"
 
 namespace ps {
@@ -703,8 +705,16 @@ ps_status ep_combine_rows(ps_engine_s& e, int B, const LayerDev& ld, float* y_l)
 
 // routed_ids / routed_w (nullable, device, [L,B,k] / [L,B,E]): the routing is given (a
 // reference trace's gating truth) and replaces K1; everything downstream is unchanged.
+// NVTX ranges (header-only nvtx3; no-ops unless a profiler is attached): the step and,
+// per layer, the scheduling point, the host plan, the loads and the combine.
+struct NvtxRange {
+  explicit NvtxRange(const char* name) { nvtxRangePushA(name); }
+  ~NvtxRange() { nvtxRangePop(); }
+};
+
 void decode_step(ps_engine_s& e, const float* hidden, const uint8_t* follow, int B, float* y, int32_t* ids_out,
                  const int32_t* routed_ids = nullptr, const float* routed_w = nullptr) {
+  NvtxRange step_range("ps.decode_step");
   const int L = e.L, E = e.E, K = e.K, H = e.H;
   require(B >= 1 && B <= e.maxB, "decode_step: batch out of range");
   e.prefill_mode = B > kDecodeMaxBatch;
@@ -738,6 +748,7 @@ void decode_step(ps_engine_s& e, const float* hidden, const uint8_t* follow, int
     PhaseTiming ph{take_event(e), nullptr, nullptr, nullptr};
     PS_CUDA(cudaEventRecord(ph.route0, e.sc));
     e.last_ffn_end = nullptr;
+    nvtxRangePushA("ps.layer.route");
     // --- K1 route (+fused bf16 cast) ------------------------------------------------
     // Decode without shared experts / EP: K1 and K2's index pass in one launch (the last
     // route CTA permutes). Otherwise K1 here and K2 below. Histogram: diff of K2 offsets.
@@ -863,6 +874,8 @@ void decode_step(ps_engine_s& e, const float* hidden, const uint8_t* follow, int
       e.pending_pf.clear();
     }
 
+    nvtxRangePop();
+    nvtxRangePushA("ps.layer.plan");
     // Wait for the routing result on the host (the only per-layer host sync).
     PS_CUDA(cudaEventSynchronize(e.ev_routed));
     if (!e.ep) {
@@ -952,6 +965,8 @@ void decode_step(ps_engine_s& e, const float* hidden, const uint8_t* follow, int
     plan.prefetch_seq = pf_b.data();
     plan_layer(in, e.cfg.policy, plan);
 
+    nvtxRangePop();
+    NvtxRange loads_range("ps.layer.loads_ffn_combine");
     // --- R7: on-demand loads through the dual buffer, FFN per landed expert --------
     std::vector<ps_expert_load> loads(plan.ondemand_seq, plan.ondemand_seq + plan.n_ondemand);
     // R5: cpu_set on the host lane (concurrent with the loads below); without a lane the

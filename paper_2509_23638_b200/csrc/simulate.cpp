@@ -369,6 +369,29 @@ ps_status ps_verify_timeline_ex(const ps_timeline_event* events, int n_events, c
   });
 }
 
+ps_status ps_export_timeline(const ps_timeline_event* events, int n, int64_t makespan, char* buf, int cap,
+                             int* needed) {
+  return guarded([&] {
+    require(n >= 0 && (n == 0 || events) && needed, "ps_export_timeline: bad arguments");
+    static const char* kRes[] = {"gpu", "cpu", "io"};
+    static const char* kKind[] = {"attention", "gpu_expert", "cpu_expert", "load", "prefetch", "idle"};
+    std::string out = "# tick_unit=us makespan=" + std::to_string(makespan) + "\n";
+    for (int i = 0; i < n; ++i) {
+      const ps_timeline_event& e = events[i];
+      const char* r = e.resource >= 0 && e.resource < 3 ? kRes[e.resource] : "?";
+      const char* k = e.kind >= 0 && e.kind < 6 ? kKind[e.kind] : "?";
+      out += std::to_string(e.t_start) + ' ' + std::to_string(e.t_end) + ' ' + r + ' ' + k + ' ' +
+             std::to_string(e.layer) + ' ' + std::to_string(e.expert) + ' ' + std::to_string(e.tokens) + '\n';
+    }
+    *needed = static_cast<int>(out.size()) + 1;
+    if (buf && cap > 0) {
+      const size_t m = std::min<size_t>(out.size(), static_cast<size_t>(cap - 1));
+      std::memcpy(buf, out.data(), m);
+      buf[m] = 0;
+    }
+  });
+}
+
 ps_status ps_compute_metrics(const ps_timeline_event* events, int n, const int64_t* layer_start,
                              const int64_t* layer_end, int L, int output_tokens, ps_metrics* m,
                              int64_t* per_layer_latency, int64_t* cpu_gpu_gap) {

@@ -238,3 +238,29 @@ def test_cost_model_kats():
     b, c, r2 = C.c_double(), C.c_double(), C.c_double()
     ps.check(lib.ps_fit_cost_params(tok.ctypes.data, tk.ctypes.data, 50, C.byref(b), C.byref(c), C.byref(r2)))
     assert b.value == pytest.approx(3.0) and c.value == pytest.approx(5.0) and r2.value == pytest.approx(1.0)
+
+
+def test_export_timeline_text_matches_reference():
+    """export_timeline (simulator.cpp:428-436): same text as the reference for every
+    golden timeline (and the GPU engine's measured timelines use the same call)."""
+    import ctypes as C
+    import oracle as orc
+    lib = ps.load()
+    scen = json.loads((GOLDEN / "golden_scenarios.json").read_text())
+    for s in scen:
+        ev = s["presched_timeline"]["events"]
+        mk = s["presched_timeline"].get("makespan", max(e[1] for e in ev))
+        arr = (ps.capi.TimelineEvent * len(ev))(*[ps.capi.TimelineEvent(*e) for e in ev])
+        need = C.c_int()
+        ps.check(lib.ps_export_timeline(arr, len(ev), mk, None, 0, C.byref(need)))
+        buf = C.create_string_buffer(need.value)
+        ps.check(lib.ps_export_timeline(arr, len(ev), mk, buf, need.value, C.byref(need)))
+        text = buf.value.decode()
+        assert text.startswith(f"# tick_unit=us makespan={mk}\n") and text.count("\n") == len(ev) + 1
+        if orc.ref_available():
+            rarr = (orc.RefEvent * len(ev))(*[orc.RefEvent(*e) for e in ev])
+            rneed = C.c_int()
+            orc.ref_check(orc.ref_lib().ref_export_timeline(rarr, len(ev), mk, None, 0, C.byref(rneed)))
+            rbuf = C.create_string_buffer(rneed.value)
+            orc.ref_check(orc.ref_lib().ref_export_timeline(rarr, len(ev), mk, rbuf, rneed.value, C.byref(rneed)))
+            assert rbuf.value.decode() == text
