@@ -49,16 +49,18 @@ def main():
         att = [x for x in ev if x[3] == 0]
         cpu = [x for x in ev if x[3] == 2]
         ld = [x for x in ev if x[3] == 3]
+        pf = [x for x in events if x[3] == 4 and x[4] == l + 1]
         gpu = [x for x in ev if x[3] == 1]
         rows.append({"layer": l, "start": ls[l], "end": le[l], "sched_end": att[0][1] if att else None,
                      "cpu_start": cpu[0][0] if cpu else None, "cpu_end": cpu[0][1] if cpu else None,
-                     "n_cpu": len(cpu), "n_load": len(ld), "load_end": max((x[1] for x in ld), default=None),
+                     "n_cpu": len(cpu), "n_load": len(ld), "n_prefetch_next": len(pf),
+                     "load_us": [x[1] - x[0] for x in ld + pf], "load_end": max((x[1] for x in ld), default=None),
                      "gpu_end": max((x[1] for x in gpu), default=None)})
     tot = le[-1] - ls[0]
     cpu_busy = sum(r["cpu_end"] - r["cpu_start"] for r in rows if r["cpu_start"] is not None)
     gaps = [(r["cpu_start"] - r["start"]) for r in rows if r["cpu_start"] is not None]
     tails = [(r["end"] - r["cpu_end"]) for r in rows if r["cpu_end"] is not None]
-    print(json.dumps({"step_us": tot, "cpu_busy_us": cpu_busy, "layer_start_to_lane_start_us_mean": float(np.mean(gaps)),
+    print(json.dumps({"cost": e.stats()["cost"], "step_us": tot, "cpu_busy_us": cpu_busy, "layer_start_to_lane_start_us_mean": float(np.mean(gaps)),
                       "lane_end_to_layer_end_us_mean": float(np.mean(tails)), "layers": rows}))
     e.close()
 

@@ -23,7 +23,8 @@ def _p(t):
     return C.c_void_p(t.data_ptr()) if t is not None else None
 
 
-def test_engine_ep_world1_matches_engine(torch_cuda):
+@pytest.mark.parametrize("compress", [False, True])
+def test_engine_ep_world1_matches_engine(torch_cuda, compress):
     spec = ps.desk_scale("mixtral", 4, 8, 256)
     spec.expert_bytes = 6 * 256 * 512
     cfg = ps.TraceGenConfig(*[ps.GROUP_DEFAULT_GEN[g] for g in ("input", "middle", "output")])
@@ -34,7 +35,7 @@ def test_engine_ep_world1_matches_engine(torch_cuda):
         comm = eng.EpComm() if use_ep else None
         try:
             with eng.Engine(spec, cfg, budget_fraction=0.5, max_batch=B, weight_seed=3, gate=gate,
-                            trace_hidden=hidden, trace_follow=follow, ep=comm) as e:
+                            trace_hidden=hidden, trace_follow=follow, ep=comm, compress_host=compress) as e:
                 outs.append(e.step_host(hidden, follow))
         finally:
             if comm:
