@@ -1411,7 +1411,7 @@ void create_engine(const ps_engine_config& cfg, ps_engine_s& e) {
     PS_CUDA(cudaHostAlloc(&e.lane_yrows, sizeof(float) * rows_t * e.H, cudaHostAllocDefault));
     e.lane_drv = std::make_unique<LaneDriver>(e.lane, e.H, e.F);
     // cpu_cost = beta*m + C (cost_model.cpp:34-37) measured on this host: the lane on a
-    // host-resident expert slab at m = 1 and m = m2, best of 3 each.
+    // host-resident expert slab at two token counts (below), best of 3 each.
     const uint16_t* probe = nullptr;
     const uint8_t* probe_z = nullptr;  // the lane reads z-slabs when they exist (AMX)
     for (size_t i = 0; i < e.host_slab.size(); ++i)
@@ -1435,13 +1435,17 @@ void create_engine(const ps_engine_config& cfg, ps_engine_s& e) {
         }
         return t;
       };
-      // m2 up to 64 tokens: prefill-sized engines see the lane leave its DRAM-bound
-      // regime (AMX compute grows with ceil(m/16)) and price large m_e accordingly.
-      const int m2 = std::min<int>(std::max(16, std::min(64, e.maxB)), static_cast<int>(rows_t));
-      const double t1 = best(1), t2 = m2 > 1 ? best(m2) : t1;
-      const double beta = m2 > 1 ? std::max(0.0, (t2 - t1) / (m2 - 1)) : 0.0;
+      // Decode engines (maxB <= 64): the line through m = 1 and m = min(16, maxB), the
+      // DRAM-bound regime decode experts live in. Prefill-capable engines: the line
+      // through m = 16 and 128, where the AMX lane is compute-bound (cost grows with
+      // ceil(m/16)), so 100+-token experts are not under-priced against PCIe.
+      const bool prefill = e.maxB > 64;
+      const int m1 = prefill ? 16 : 1;
+      const int m2 = std::min<int>(prefill ? 128 : std::max(1, std::min(16, e.maxB)), static_cast<int>(rows_t));
+      const double t1 = best(m1), t2 = m2 > m1 ? best(m2) : t1;
+      const double beta = m2 > m1 ? std::max(0.0, (t2 - t1) / (m2 - m1)) : 0.0;
       e.cfg.cost.beta = std::max(beta, 1e-3);
-      e.cfg.cost.startup = std::max<int64_t>(0, ps_to_ticks(t1 - beta));
+      e.cfg.cost.startup = std::max<int64_t>(0, ps_to_ticks(t1 - beta * m1));
     }
   }
   e.st.cost = e.cfg.cost;
