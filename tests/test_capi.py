@@ -41,3 +41,20 @@ def test_product_does_not_import_oracle():
     for p in (ROOT / "paper_2509_23638_b200").rglob("*.py"):
         text = p.read_text()
         assert "import oracle" not in text and "from oracle" not in text, p
+
+
+def test_argument_validation_before_any_launch():
+    """Entry points reject bad shapes with PS_EINVAL before touching the GPU (CPU safe)."""
+    lib = ps.load()
+    assert lib.ps_set_prefill_kernel(3) == ps.capi.PS_EINVAL
+    assert lib.ps_set_prefill_kernel(2) == ps.capi.PS_OK
+    # fused route+permute is a decode-only launch: B <= 64
+    p = C.c_void_p(16)
+    assert lib.ps_route_permute(p, p, None, None, None, 2, 65, 64, 8, 2, p, p, p, p, p, p, p, None) == ps.capi.PS_EINVAL
+    assert b"decode shapes only" in lib.ps_last_error()
+    # z-slab codec: null / empty arguments
+    nb = C.c_uint64()
+    assert lib.ps_zslab_encode(None, 0, None, 0, C.byref(nb), 1) == ps.capi.PS_EINVAL
+    assert lib.ps_zslab_bound(1024) > 1024
+    # shared-expert append: S out of range
+    assert lib.ps_append_shared(p, p, 4, 2, 8, 0, p, p, None, None) == ps.capi.PS_EINVAL
