@@ -191,8 +191,10 @@ def workload_config(args, spec, executor="gpu_only"):
                            ", GPU-only executor")
                         + (", loads as lossless 12-bit z-slabs decoded on the GPU" if getattr(args, "compress", 0)
                            else ""),
-            "model": f"{args.model}-8x7b-shape" if args.model == "mixtral" else args.model,
-            "global_batch": args.batch * args.gpus, "seq_len": 1, "parallelism": (f"ep{args.gpus}" if args.gpus > 1 else "single"),
+            "expert_shape": f"{args.model}-8x7b" if args.model == "mixtral" else args.model,
+            "decode_batch": args.batch, "global_batch": args.batch * args.gpus,
+            "parallelism": (f"ep{args.gpus}" if args.gpus > 1 else "single"),
+            "executor": executor,
             "budget_fraction": args.budget, "policy": args.policy,
             "l2": "inputs larger than L2 (each expert slab 336 MiB > 126 MB L2)"}
 
