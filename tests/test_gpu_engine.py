@@ -203,3 +203,17 @@ def test_engine_replays_reference_trace_file(torch_cuda, budget, host_threads):
     assert np.linalg.norm(y - y_ref) / np.linalg.norm(y_ref) < BF16_RTOL
     if host_threads:
         assert st["cpu_experts"] > 0
+
+
+@pytest.mark.parametrize("compress", [False, True])
+def test_engine_prefill_chunk_with_host_lane(torch_cuda, compress):
+    """A prefill-sized chunk (B > 64: gathered rows, exact-count tcgen05 launches) with the
+    host lane taking PreSched's cpu_set (m_e in the tens of tokens per expert) and z-slab
+    loads for the rest: outputs match the oracle."""
+    spec = _small_spec(L=3, E=8, H=256, F=512)
+    cost = (1000, 5, 10, 0.5, 1, 0)
+    y, y_ref, ids, st, resident, agree = _run(spec, 256, 0.25, steps=1, host_threads=3, cost=cost,
+                                              compress_host=compress)
+    assert agree >= 0.99
+    assert np.linalg.norm(y - y_ref) / np.linalg.norm(y_ref) < BF16_RTOL
+    assert st["cpu_experts"] > 0
