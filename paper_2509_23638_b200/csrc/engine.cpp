@@ -34,6 +34,7 @@
 #include <nvtx3/nvToolsExt.h>
 
 #include "cuda_host.hpp"
+#include "zslab_format.hpp"
 
 namespace ps {
 void plan_layer(const ps_layer_inputs& in, ps_policy pol, ps_layer_plan& out);
@@ -980,7 +981,10 @@ void decode_step(ps_engine_s& e, const float* hidden, const uint8_t* follow, int
         const uint16_t* slab = e.host_slab[static_cast<size_t>(l) * E + ex];
         require(slab != nullptr, "host lane: cpu_set expert has no host copy");
         CpuJob j{l, ex, off[ex + 1] - off[ex], off[ex], slab};
-        if (!e.host_z.empty()) j.z = e.host_z[static_cast<size_t>(l) * E + ex];
+        if (!e.host_z.empty()) {  // the lane's z path reads 4-bit z-slabs only
+          const uint8_t* z = e.host_z[static_cast<size_t>(l) * E + ex];
+          if (z && reinterpret_cast<const ZHeader*>(z)->code_bits == 4) j.z = z;
+        }
         for (int r = j.row0; r < j.row0 + j.m; ++r)
           std::memcpy(e.lane_xrows + static_cast<size_t>(r) * H, e.lane_x + static_cast<size_t>(perm[r] / Kt) * H,
                       sizeof(uint16_t) * H);
@@ -1417,7 +1421,9 @@ void create_engine(const ps_engine_config& cfg, ps_engine_s& e) {
     for (size_t i = 0; i < e.host_slab.size(); ++i)
       if (e.host_slab[i]) {
         probe = e.host_slab[i];
-        if (!e.host_z.empty() && lane_z_enabled() && ps_host_lane_isa(e.lane) == 2) probe_z = e.host_z[i];
+        if (!e.host_z.empty() && lane_z_enabled() && ps_host_lane_isa(e.lane) == 2 && e.host_z[i] &&
+            reinterpret_cast<const ZHeader*>(e.host_z[i])->code_bits == 4)
+          probe_z = e.host_z[i];
         break;
       }
     if (auto_cost && probe) {

@@ -544,6 +544,7 @@ ps_status ps_host_expert_ffn_batch_z(ps_host_lane l, int n, const uint8_t* const
       require(zslabs[j] != nullptr && m[j] >= 0 && m[j] <= 4096 && row0[j] >= 0, "ps_host_expert_ffn_batch_z: bad job");
       const ZHeader* h = reinterpret_cast<const ZHeader*>(zslabs[j]);
       require(h->magic == kZMagic && h->n == 3ull * H * F, "ps_host_expert_ffn_batch_z: not a z-slab of this shape");
+      require(h->code_bits == 4, "ps_host_expert_ffn_batch_z: the lane decodes 4-bit z-slabs only");
       zv.emplace_back(zslabs[j]);
     }
     const int T = l->pool->size();

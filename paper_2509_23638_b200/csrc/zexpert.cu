@@ -5,16 +5,19 @@
 // trained (or, here, synthetic Gaussian) matrix use only a narrow band of the 8-bit
 // exponent field: a slab is stored as
 //   lo    [n]        u8   sign << 7 | 7-bit mantissa        (verbatim)
-//   codes [n/2]      u8   two 4-bit exponent codes per byte: code c < 15 means
-//                         exponent = base + c; c = 15 is an escape
+//   codes [n*bits/8]      `bits` = 3 or 4 per value (32 values = `bits` little-endian
+//                         words per lane segment): code c < 2^bits - 1 means
+//                         exponent = base + c; all ones is an escape
 //   esc_off [nb + 1] u32  prefix of escapes per 1024-value block
 //   esc   [n_esc]    u8   raw exponents of the escaped values, in value order
-// i.e. 12 bits per value + 1 byte per escape (~75 % of bf16). Decoding is bit-exact
+// i.e. 11-12 bits per value + 1 byte per escape (70-75 % of bf16; the encoder picks the
+// code width with the smaller estimated size). Decoding is bit-exact
 // (tests/test_gpu_zexpert.py), so every downstream result is identical to loading the
 // raw slab. Encoder: host C++ (at engine create, multithreaded over blocks); decoder:
 // one warp per 1024-value block, 32 values per lane, escape ranks by a warp scan,
 // 16-byte loads/stores (HBM-bound: 1.5 B read + 2 B written per value).
 #include <algorithm>
+#include <cstdlib>
 #include <cstring>
 #include <thread>
 #include <vector>
@@ -25,27 +28,40 @@
 namespace ps {
 namespace {
 
+// One warp per 1024-value block, 32 values per lane: lane L's codes are the BITS*4 bytes
+// at BITS*4*L of the block's code region (bit 3i.. of a little-endian word array).
+template <int BITS>
 __global__ void z_decode_kernel(const uint8_t* __restrict__ z, uint64_t n, uint32_t base, uint32_t nb,
                                 uint16_t* __restrict__ out) {
+  constexpr uint32_t kEsc = (1u << BITS) - 1u;
+  constexpr int kWords = BITS;  // 32 values * BITS bits = BITS 32-bit words
   const uint64_t n_pad = static_cast<uint64_t>(nb) * kZBlock;
   const uint8_t* lo = z + z_lo_off();
-  const uint8_t* codes = z + z_codes_off(n_pad);
-  const uint32_t* esc_off = reinterpret_cast<const uint32_t*>(z + z_escoff_off(n_pad));
-  const uint8_t* esc = z + z_esc_off(n_pad, nb);
+  const uint32_t* codes = reinterpret_cast<const uint32_t*>(z + z_codes_off(n_pad));
+  const uint32_t* esc_off = reinterpret_cast<const uint32_t*>(z + z_escoff_off(n_pad, BITS));
+  const uint8_t* esc = z + z_esc_off(n_pad, nb, BITS);
   const int lane = threadIdx.x & 31;
   const uint32_t warps = (gridDim.x * blockDim.x) >> 5;
   for (uint32_t b = (blockIdx.x * blockDim.x + threadIdx.x) >> 5; b < nb; b += warps) {
-    const uint64_t v0 = static_cast<uint64_t>(b) * kZBlock + lane * 32;  // this lane's 32 values
+    const uint64_t seg = static_cast<uint64_t>(b) * 32 + lane;  // this lane's 32-value segment
+    const uint64_t v0 = seg * 32;
     const uint4 l0 = *reinterpret_cast<const uint4*>(lo + v0);
     const uint4 l1 = *reinterpret_cast<const uint4*>(lo + v0 + 16);
-    const uint4 cw = *reinterpret_cast<const uint4*>(codes + v0 / 2);
+    uint32_t cw[kWords + 1];
+#pragma unroll
+    for (int q = 0; q < kWords; ++q) cw[q] = codes[seg * kWords + q];
+    cw[kWords] = 0;
     const uint32_t lw[8] = {l0.x, l0.y, l0.z, l0.w, l1.x, l1.y, l1.z, l1.w};
-    const uint32_t cv[4] = {cw.x, cw.y, cw.z, cw.w};
+    uint32_t cd[32];
     int n_e = 0;
 #pragma unroll
-    for (int q = 0; q < 4; ++q)
-#pragma unroll
-      for (int j = 0; j < 8; ++j) n_e += ((cv[q] >> (4 * j)) & 15u) == kZEscape;
+    for (int i = 0; i < 32; ++i) {
+      const int bit = BITS * i, w = bit >> 5, sh = bit & 31;
+      uint32_t c = cw[w] >> sh;
+      if (sh + BITS > 32) c |= cw[w + 1] << (32 - sh);
+      cd[i] = c & kEsc;
+      n_e += cd[i] == kEsc;
+    }
     int incl = n_e;  // warp inclusive scan of escape counts
 #pragma unroll
     for (int o = 1; o < 32; o <<= 1) {
@@ -56,9 +72,8 @@ __global__ void z_decode_kernel(const uint8_t* __restrict__ z, uint64_t n, uint3
     uint32_t packed[16];
 #pragma unroll
     for (int i = 0; i < 32; ++i) {
-      const uint32_t c = (cv[i >> 3] >> (4 * (i & 7))) & 15u;
       const uint32_t l = (lw[i >> 2] >> (8 * (i & 3))) & 0xffu;
-      const uint32_t ex = c == kZEscape ? esc[e_at++] : base + c;
+      const uint32_t ex = cd[i] == kEsc ? esc[e_at++] : base + cd[i];
       const uint32_t v = ((l & 0x80u) << 8) | (ex << 7) | (l & 0x7fu);
       if (i & 1) packed[i >> 1] |= v << 16;
       else packed[i >> 1] = v;
@@ -75,20 +90,41 @@ __global__ void z_decode_kernel(const uint8_t* __restrict__ z, uint64_t n, uint3
   }
 }
 
-// One 1024-value block: lo bytes, packed 4-bit codes; returns the escape count.
+// One 1024-value block: lo bytes, packed `bits`-bit codes; returns the escape count.
 uint32_t z_encode_block(const uint16_t* __restrict__ src, uint8_t* __restrict__ lo, uint8_t* __restrict__ codes,
-                        uint32_t base) {
-  // separate simple loops (auto-vectorised): sign+mantissa bytes, 4-bit codes, escapes
+                        uint32_t base, uint32_t bits) {
+  // separate simple loops (auto-vectorised): sign+mantissa bytes, codes, escapes
+  const uint32_t esc = z_escape(bits);
   uint8_t cd[kZBlock];
   for (int k = 0; k < kZBlock; ++k) {
     const uint32_t v = src[k];
     lo[k] = static_cast<uint8_t>(((v >> 8) & 0x80u) | (v & 0x7fu));
     const uint32_t d = ((v >> 7) & 0xffu) - base;  // wraps below base
-    cd[k] = static_cast<uint8_t>(d < kZEscape ? d : kZEscape);
+    cd[k] = static_cast<uint8_t>(d < esc ? d : esc);
   }
   uint32_t c = 0;
-  for (int k = 0; k < kZBlock; ++k) c += cd[k] == kZEscape;
-  for (int k = 0; k < kZBlock / 2; ++k) codes[k] = static_cast<uint8_t>(cd[2 * k] | (cd[2 * k + 1] << 4));
+  for (int k = 0; k < kZBlock; ++k) c += cd[k] == esc;
+  if (bits == 4) {
+    for (int k = 0; k < kZBlock / 2; ++k) codes[k] = static_cast<uint8_t>(cd[2 * k] | (cd[2 * k + 1] << 4));
+  } else {  // 3 bits: 32 values -> 3 little-endian words per segment
+    uint32_t* w = reinterpret_cast<uint32_t*>(codes);
+    for (int sgm = 0; sgm < kZBlock / 32; ++sgm) {
+      uint64_t acc[2] = {0, 0};
+#pragma GCC unroll 32
+      for (int i = 0; i < 32; ++i) {
+        const int bit = 3 * i;
+        if (bit < 64) {
+          acc[0] |= static_cast<uint64_t>(cd[32 * sgm + i]) << bit;
+          if (bit + 3 > 64) acc[1] |= static_cast<uint64_t>(cd[32 * sgm + i]) >> (64 - bit);
+        } else {
+          acc[1] |= static_cast<uint64_t>(cd[32 * sgm + i]) << (bit - 64);
+        }
+      }
+      w[3 * sgm] = static_cast<uint32_t>(acc[0]);
+      w[3 * sgm + 1] = static_cast<uint32_t>(acc[0] >> 32);
+      w[3 * sgm + 2] = static_cast<uint32_t>(acc[1]);
+    }
+  }
   return c;
 }
 
@@ -114,7 +150,7 @@ extern "C" {
 
 uint64_t ps_zslab_bound(uint64_t n) {
   const uint64_t nb = (n + kZBlock - 1) / kZBlock, n_pad = nb * kZBlock;
-  return z_esc_off(n_pad, static_cast<uint32_t>(nb)) + n_pad;  // worst case: every value escaped
+  return z_esc_off(n_pad, static_cast<uint32_t>(nb), 4) + n_pad;  // worst case: 4-bit codes, every value escaped
 }
 
 ps_status ps_zslab_encode(const uint16_t* slab, uint64_t n, uint8_t* out, uint64_t cap, uint64_t* out_bytes,
@@ -123,28 +159,60 @@ ps_status ps_zslab_encode(const uint16_t* slab, uint64_t n, uint8_t* out, uint64
     require(slab && out && out_bytes && n > 0, "ps_zslab_encode: bad arguments");
     const uint32_t nb = static_cast<uint32_t>((n + kZBlock - 1) / kZBlock);
     const uint64_t n_pad = static_cast<uint64_t>(nb) * kZBlock;
-    require(cap >= z_esc_off(n_pad, nb), "ps_zslab_encode: output too small");
+    require(cap >= z_esc_off(n_pad, nb, 3), "ps_zslab_encode: output too small");
     threads = threads > 0 ? threads : static_cast<int>(std::max(1u, std::thread::hardware_concurrency()));
-    // exponent histogram (sampled every 61st value) -> the 15-wide window with most mass
+    // exponent histogram (sampled every 61st value) -> for code widths 3 and 4, the
+    // window of 2^bits - 1 exponents with most mass; the width with the smaller
+    // estimated size (codes + one byte per escape) wins.
     std::vector<uint64_t> hist(256, 0);
-    for (uint64_t i = 0; i < n; i += 61) hist[(slab[i] >> 7) & 0xff]++;
-    uint32_t base = 0;
-    uint64_t best = 0;
-    for (uint32_t b = 0; b + 15 <= 256; ++b) {
-      uint64_t s = 0;
-      for (uint32_t j = 0; j < 15; ++j) s += hist[b + j];
-      if (s > best) {
-        best = s;
-        base = b;
+    uint64_t samples = 0;
+    for (uint64_t i = 0; i < n; i += 61, ++samples) hist[(slab[i] >> 7) & 0xff]++;
+    uint32_t bits = 4, base = 0;
+    double best_size = 1e300;
+    for (uint32_t bw : {3u, 4u}) {
+      const uint32_t win = z_escape(bw);
+      uint32_t bb = 0;
+      uint64_t best = 0;
+      for (uint32_t b = 0; b + win <= 256; ++b) {
+        uint64_t s = 0;
+        for (uint32_t j = 0; j < win; ++j) s += hist[b + j];
+        if (s > best) {
+          best = s;
+          bb = b;
+        }
+      }
+      const double esc_frac = samples ? 1.0 - static_cast<double>(best) / samples : 0.0;
+      const double size = bw / 8.0 + esc_frac;  // bytes per value beyond the lo byte
+      if (size < best_size) {
+        best_size = size;
+        bits = bw;
+        base = bb;
       }
     }
+    if (const char* v = std::getenv("PS_ZSLAB_BITS")) {  // tests pin the width
+      const uint32_t forced = static_cast<uint32_t>(std::atoi(v));
+      if (forced == 3 || forced == 4) {
+        bits = forced;
+        uint64_t best = 0;
+        for (uint32_t b = 0; b + z_escape(bits) <= 256; ++b) {
+          uint64_t s = 0;
+          for (uint32_t j = 0; j < z_escape(bits); ++j) s += hist[b + j];
+          if (s > best) {
+            best = s;
+            base = b;
+          }
+        }
+      }
+    }
+    const uint32_t escv = z_escape(bits);
+    require(cap >= z_esc_off(n_pad, nb, bits), "ps_zslab_encode: output too small");
     uint8_t* lo = out + z_lo_off();
     uint8_t* codes = out + z_codes_off(n_pad);
-    uint32_t* esc_off = reinterpret_cast<uint32_t*>(out + z_escoff_off(n_pad));
+    uint32_t* esc_off = reinterpret_cast<uint32_t*>(out + z_escoff_off(n_pad, bits));
     auto exp_of = [&](uint64_t i) { return i < n ? static_cast<uint32_t>((slab[i] >> 7) & 0xff) : base; };
-    auto escaped = [&](uint32_t e) { return e < base || e >= base + kZEscape; };
-    // pass 1: lo bytes, codes, escape count per block (branch-free inner loop over
-    // full blocks; the ragged tail is padded with code-0 values)
+    auto escaped = [&](uint32_t e) { return e < base || e >= base + escv; };
+    // pass 1: lo bytes, codes, escape count per block (the ragged tail is padded with
+    // code-0 values)
     std::vector<uint32_t> cnt(nb);
     parallel_blocks(nb, threads, [&](uint32_t b) {
       const uint64_t i0 = static_cast<uint64_t>(b) * kZBlock;
@@ -154,17 +222,17 @@ ps_status ps_zslab_encode(const uint16_t* slab, uint64_t n, uint8_t* out, uint64
         for (int k = 0; k < kZBlock; ++k) tmp[k] = i0 + k < n ? slab[i0 + k] : static_cast<uint16_t>(base << 7);
         src = tmp;
       }
-      cnt[b] = z_encode_block(src, lo + i0, codes + i0 / 2, base);
+      cnt[b] = z_encode_block(src, lo + i0, codes + i0 * bits / 8, base, bits);
     });
     esc_off[0] = 0;
     for (uint32_t b = 0; b < nb; ++b) esc_off[b + 1] = esc_off[b] + cnt[b];
     const uint64_t n_esc = esc_off[nb];
-    const uint64_t bytes = (z_esc_off(n_pad, nb) + n_esc + 15) / 16 * 16;
+    const uint64_t bytes = (z_esc_off(n_pad, nb, bits) + n_esc + 15) / 16 * 16;
     require(cap >= bytes, "ps_zslab_encode: output too small for the escapes");
-    uint8_t* esc = out + z_esc_off(n_pad, nb);
+    uint8_t* esc = out + z_esc_off(n_pad, nb, bits);
     // pass 2: escaped exponents in value order
     parallel_blocks(nb, threads, [&](uint32_t b) {
-      if (cnt[b] == 0) return;  // ~88 % of blocks of a weight slab have no escape
+      if (cnt[b] == 0) return;  // most blocks of a weight slab have no escape
       uint32_t at = esc_off[b];
       for (uint64_t i = static_cast<uint64_t>(b) * kZBlock; i < static_cast<uint64_t>(b + 1) * kZBlock; ++i) {
         const uint32_t e = exp_of(i);
@@ -178,6 +246,7 @@ ps_status ps_zslab_encode(const uint16_t* slab, uint64_t n, uint8_t* out, uint64
     h.nb = nb;
     h.n_esc = n_esc;
     h.bytes = bytes;
+    h.code_bits = bits;
     std::memcpy(out, &h, sizeof(h));
     *out_bytes = bytes;
   });
@@ -206,7 +275,11 @@ ps_status ps_zslab_decode(const uint8_t* z_dev, const uint8_t* z_host_header, ui
     const int threads = 256;
     const int grid = static_cast<int>(std::min<uint64_t>((static_cast<uint64_t>(h.nb) * 32 + threads - 1) / threads,
                                                          8 * 148));
-    z_decode_kernel<<<grid, threads, 0, as_stream(stream)>>>(z_dev, h.n, h.base, h.nb, out);
+    require(h.code_bits == 3 || h.code_bits == 4, "ps_zslab_decode: bad code width");
+    if (h.code_bits == 3)
+      z_decode_kernel<3><<<grid, threads, 0, as_stream(stream)>>>(z_dev, h.n, h.base, h.nb, out);
+    else
+      z_decode_kernel<4><<<grid, threads, 0, as_stream(stream)>>>(z_dev, h.n, h.base, h.nb, out);
     PS_LAUNCH_CHECK("z_decode_kernel");
   });
 }

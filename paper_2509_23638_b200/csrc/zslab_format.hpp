@@ -13,7 +13,8 @@
 namespace ps {
 
 constexpr int kZBlock = 1024;  // values per block (escape prefix granularity)
-constexpr int kZEscape = 15;   // 4-bit code of an escaped exponent
+constexpr int kZEscape = 15;   // escape code of the 4-bit format (the 3-bit format uses 7)
+PS_HD inline uint32_t z_escape(uint32_t bits) { return (1u << bits) - 1u; }
 
 struct ZHeader {  // at the start of every z-slab (64 bytes, keeps the streams 16-B aligned)
   uint64_t magic;  // "PSZSLAB1"
@@ -22,15 +23,20 @@ struct ZHeader {  // at the start of every z-slab (64 bytes, keeps the streams 1
   uint32_t nb;     // blocks
   uint64_t n_esc;  // escaped values
   uint64_t bytes;  // total z-slab bytes
-  uint64_t pad[3];
+  uint32_t code_bits;  // 3 or 4: exponent code width (escape = all ones)
+  uint32_t pad0;
+  uint64_t pad[2];
 };
 static_assert(sizeof(ZHeader) == 64, "z header");
 constexpr uint64_t kZMagic = 0x31424c534c5a5350ull;  // "PSZSLAB1"
 
 PS_HD inline size_t z_lo_off() { return sizeof(ZHeader); }
 PS_HD inline size_t z_codes_off(uint64_t n_pad) { return z_lo_off() + n_pad; }
-PS_HD inline size_t z_escoff_off(uint64_t n_pad) { return z_codes_off(n_pad) + n_pad / 2; }
-PS_HD inline size_t z_esc_off(uint64_t n_pad, uint32_t nb) { return z_escoff_off(n_pad) + 4ull * (nb + 1); }
+// codes: `bits` per value, 32 values = 4*bits bytes (a lane's segment), little endian
+PS_HD inline size_t z_escoff_off(uint64_t n_pad, uint32_t bits) { return z_codes_off(n_pad) + n_pad * bits / 8; }
+PS_HD inline size_t z_esc_off(uint64_t n_pad, uint32_t nb, uint32_t bits) {
+  return z_escoff_off(n_pad, bits) + 4ull * (nb + 1);
+}
 
 // Pointers into a z-slab (host view).
 struct ZView {
@@ -38,14 +44,15 @@ struct ZView {
   const uint8_t* codes;
   const uint32_t* esc_off;
   const uint8_t* esc;
-  uint32_t base;
+  uint32_t base, bits;
   explicit ZView(const uint8_t* z) {
     const ZHeader* h = reinterpret_cast<const ZHeader*>(z);
     const uint64_t n_pad = static_cast<uint64_t>(h->nb) * kZBlock;
+    bits = h->code_bits;
     lo = z + z_lo_off();
     codes = z + z_codes_off(n_pad);
-    esc_off = reinterpret_cast<const uint32_t*>(z + z_escoff_off(n_pad));
-    esc = z + z_esc_off(n_pad, h->nb);
+    esc_off = reinterpret_cast<const uint32_t*>(z + z_escoff_off(n_pad, bits));
+    esc = z + z_esc_off(n_pad, h->nb, bits);
     base = h->base;
   }
 };

@@ -23,8 +23,18 @@ def _encode(slab):
     return z[:nb.value].copy()
 
 
+@pytest.fixture(params=["3", "4", "auto"])
+def zbits(request, monkeypatch):
+    """Pin the z-slab code width (PS_ZSLAB_BITS, read per encode) or let the encoder pick."""
+    if request.param != "auto":
+        monkeypatch.setenv("PS_ZSLAB_BITS", request.param)
+    else:
+        monkeypatch.delenv("PS_ZSLAB_BITS", raising=False)
+    return request.param
+
+
 @pytest.mark.parametrize("case", ["weights", "escapes", "ragged"])
-def test_zslab_roundtrip_bit_exact(torch_cuda, case):
+def test_zslab_roundtrip_bit_exact(torch_cuda, case, zbits):
     torch = torch_cuda
     lib = ps.load()
     H, F = 256, 512
@@ -41,7 +51,8 @@ def test_zslab_roundtrip_bit_exact(torch_cuda, case):
     esc = C.c_uint64()
     ps.check(lib.ps_zslab_info(z.ctypes.data, None, None, C.byref(esc)))
     if case == "weights":
-        assert z.size < 0.76 * slab.nbytes and esc.value < slab.size // 1000
+        limit = {"3": 0.71, "4": 0.76, "auto": 0.71}[zbits]
+        assert z.size < limit * slab.nbytes
     zd = torch.as_tensor(z, device="cuda")
     out = torch.zeros(slab.size, dtype=torch.int16, device="cuda")
     ps.check(lib.ps_zslab_decode(C.c_void_p(zd.data_ptr()), z.ctypes.data, C.c_void_p(out.data_ptr()),

@@ -136,7 +136,8 @@ def test_host_expert_ffn_batch_equals_single_calls(isa):
 @needs_bf16
 @pytest.mark.skipif(not _has("amx_bf16"), reason="z-slab lane path needs AMX-BF16")
 @pytest.mark.parametrize("escapes", [False, True])
-def test_host_lane_reads_zslabs_bitwise(escapes):
+def test_host_lane_reads_zslabs_bitwise(escapes, monkeypatch):
+    monkeypatch.setenv("PS_ZSLAB_BITS", "4")  # the lane's z path decodes the 4-bit format
     """The lane's z-slab path (12-bit transfer format decoded per tile) gives bitwise the
     raw-slab results, escapes included."""
     lib = ps.load()
