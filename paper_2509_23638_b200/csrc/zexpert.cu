@@ -31,10 +31,21 @@ namespace {
 // One warp per 1024-value block, 32 values per lane: lane L's codes are the BITS*4 bytes
 // at BITS*4*L of the block's code region (bit 3i.. of a little-endian word array).
 template <int BITS>
-__global__ void z_decode_kernel(const uint8_t* __restrict__ z, uint64_t n, uint32_t base, uint32_t nb,
-                                uint16_t* __restrict__ out) {
+__device__ __forceinline__ uint32_t z_code(const uint32_t (&cw)[BITS + 1], int i) {
+  const int bit = BITS * i, w = bit >> 5, sh = bit & 31;
+  uint32_t c = cw[w] >> sh;
+  if (sh + BITS > 32) c |= cw[w + 1] << (32 - sh);
+  return c & ((1u << BITS) - 1u);
+}
+
+// One warp per 1024-value block, 32 values per lane: lane L's codes are the BITS 32-bit
+// words at BITS*L of the block's code region (bit BITS*i.. of a little-endian array).
+// Codes are extracted twice (escape count for the warp scan, then the values) instead of
+// kept in registers: <= 64 registers, 4 CTAs of 256 threads per SM for latency hiding.
+template <int BITS>
+__global__ void __launch_bounds__(256, 4)
+z_decode_kernel(const uint8_t* __restrict__ z, uint64_t n, uint32_t base, uint32_t nb, uint16_t* __restrict__ out) {
   constexpr uint32_t kEsc = (1u << BITS) - 1u;
-  constexpr int kWords = BITS;  // 32 values * BITS bits = BITS 32-bit words
   const uint64_t n_pad = static_cast<uint64_t>(nb) * kZBlock;
   const uint8_t* lo = z + z_lo_off();
   const uint32_t* codes = reinterpret_cast<const uint32_t*>(z + z_codes_off(n_pad));
@@ -47,45 +58,42 @@ __global__ void z_decode_kernel(const uint8_t* __restrict__ z, uint64_t n, uint3
     const uint64_t v0 = seg * 32;
     const uint4 l0 = *reinterpret_cast<const uint4*>(lo + v0);
     const uint4 l1 = *reinterpret_cast<const uint4*>(lo + v0 + 16);
-    uint32_t cw[kWords + 1];
+    uint32_t cw[BITS + 1];
 #pragma unroll
-    for (int q = 0; q < kWords; ++q) cw[q] = codes[seg * kWords + q];
-    cw[kWords] = 0;
-    const uint32_t lw[8] = {l0.x, l0.y, l0.z, l0.w, l1.x, l1.y, l1.z, l1.w};
-    uint32_t cd[32];
+    for (int q = 0; q < BITS; ++q) cw[q] = codes[seg * BITS + q];
+    cw[BITS] = 0;
+    const uint32_t eoff = esc_off[b];
     int n_e = 0;
 #pragma unroll
-    for (int i = 0; i < 32; ++i) {
-      const int bit = BITS * i, w = bit >> 5, sh = bit & 31;
-      uint32_t c = cw[w] >> sh;
-      if (sh + BITS > 32) c |= cw[w + 1] << (32 - sh);
-      cd[i] = c & kEsc;
-      n_e += cd[i] == kEsc;
-    }
+    for (int i = 0; i < 32; ++i) n_e += z_code<BITS>(cw, i) == kEsc;
     int incl = n_e;  // warp inclusive scan of escape counts
 #pragma unroll
     for (int o = 1; o < 32; o <<= 1) {
       const int t = __shfl_up_sync(0xffffffffu, incl, o);
       if (lane >= o) incl += t;
     }
-    uint32_t e_at = esc_off[b] + static_cast<uint32_t>(incl - n_e);
-    uint32_t packed[16];
+    uint32_t e_at = eoff + static_cast<uint32_t>(incl - n_e);
+    const uint32_t lw[8] = {l0.x, l0.y, l0.z, l0.w, l1.x, l1.y, l1.z, l1.w};
+    const bool full = v0 + 32 <= n;
 #pragma unroll
-    for (int i = 0; i < 32; ++i) {
-      const uint32_t l = (lw[i >> 2] >> (8 * (i & 3))) & 0xffu;
-      const uint32_t ex = cd[i] == kEsc ? esc[e_at++] : base + cd[i];
-      const uint32_t v = ((l & 0x80u) << 8) | (ex << 7) | (l & 0x7fu);
-      if (i & 1) packed[i >> 1] |= v << 16;
-      else packed[i >> 1] = v;
-    }
-    if (v0 + 32 <= n) {
-      uint4* dst = reinterpret_cast<uint4*>(out + v0);
+    for (int q = 0; q < 4; ++q) {  // 8 values -> one 16-byte store
+      uint32_t pk[4];
 #pragma unroll
-      for (int q = 0; q < 4; ++q)
-        dst[q] = make_uint4(packed[4 * q], packed[4 * q + 1], packed[4 * q + 2], packed[4 * q + 3]);
-    } else {
-      for (int i = 0; i < 32 && v0 + i < n; ++i)
-        out[v0 + i] = static_cast<uint16_t>(packed[i >> 1] >> (16 * (i & 1)));
+      for (int j = 0; j < 8; ++j) {
+        const int i = 8 * q + j;
+        const uint32_t c = z_code<BITS>(cw, i);
+        const uint32_t l = (lw[i >> 2] >> (8 * (i & 3))) & 0xffu;
+        const uint32_t ex = c == kEsc ? esc[e_at++] : base + c;
+        const uint32_t v = ((l & 0x80u) << 8) | (ex << 7) | (l & 0x7fu);
+        if (j & 1) pk[j >> 1] |= v << 16;
+        else pk[j >> 1] = v;
+      }
+      if (full) {
+        reinterpret_cast<uint4*>(out + v0)[q] = make_uint4(pk[0], pk[1], pk[2], pk[3]);
+      } else {
+        for (int j = 0; j < 8 && v0 + 8 * q + j < n; ++j)
+          out[v0 + 8 * q + j] = static_cast<uint16_t>(pk[j >> 1] >> (16 * (j & 1)));
+      }
     }
   }
 }
@@ -274,7 +282,7 @@ ps_status ps_zslab_decode(const uint8_t* z_dev, const uint8_t* z_host_header, ui
     require(h.magic == kZMagic, "ps_zslab_decode: not a z-slab");
     const int threads = 256;
     const int grid = static_cast<int>(std::min<uint64_t>((static_cast<uint64_t>(h.nb) * 32 + threads - 1) / threads,
-                                                         8 * 148));
+                                                         4 * 148));
     require(h.code_bits == 3 || h.code_bits == 4, "ps_zslab_decode: bad code width");
     if (h.code_bits == 3)
       z_decode_kernel<3><<<grid, threads, 0, as_stream(stream)>>>(z_dev, h.n, h.base, h.nb, out);
