@@ -28,6 +28,22 @@
 namespace ps {
 namespace {
 
+// Escapes (all-ones codes) among a lane's 32 codes with word-level bit tricks.
+template <int BITS>
+__device__ __forceinline__ int z_count_esc(const uint32_t (&cw)[BITS + 1]) {
+  if constexpr (BITS == 4) {
+    int c = 0;
+#pragma unroll
+    for (int q = 0; q < 4; ++q) c += __popc(cw[q] & (cw[q] >> 1) & (cw[q] >> 2) & (cw[q] >> 3) & 0x11111111u);
+    return c;
+  } else {  // 96 bits: codes 0..20 in the low 64 bits, codes 21..31 from bit 63 on
+    const uint64_t lo = static_cast<uint64_t>(cw[0]) | (static_cast<uint64_t>(cw[1]) << 32);
+    const uint64_t hi = (static_cast<uint64_t>(cw[1]) >> 31) | (static_cast<uint64_t>(cw[2]) << 1);
+    return __popcll(lo & (lo >> 1) & (lo >> 2) & 0x1249249249249249ull) +
+           __popcll(hi & (hi >> 1) & (hi >> 2) & 0x49249249ull);
+  }
+}
+
 // One warp per 1024-value block, 32 values per lane: lane L's codes are the BITS*4 bytes
 // at BITS*4*L of the block's code region (bit 3i.. of a little-endian word array).
 template <int BITS>
@@ -42,10 +58,16 @@ __device__ __forceinline__ uint32_t z_code(const uint32_t (&cw)[BITS + 1], int i
 // words at BITS*L of the block's code region (bit BITS*i.. of a little-endian array).
 // Codes are extracted twice (escape count for the warp scan, then the values) instead of
 // kept in registers: <= 64 registers, 4 CTAs of 256 threads per SM for latency hiding.
+// The block's escape bytes (contiguous, ~30 at 3-bit codes) are staged in shared memory
+// by one coalesced warp load, so a lane's escapes cost a shared-memory read instead of a
+// dependent global load after the scan.
+constexpr int kZEscStage = 256;  // staged escapes per block (more: read from global)
+
 template <int BITS>
 __global__ void __launch_bounds__(256, 4)
 z_decode_kernel(const uint8_t* __restrict__ z, uint64_t n, uint32_t base, uint32_t nb, uint16_t* __restrict__ out) {
   constexpr uint32_t kEsc = (1u << BITS) - 1u;
+  __shared__ uint8_t s_esc[8][kZEscStage];
   const uint64_t n_pad = static_cast<uint64_t>(nb) * kZBlock;
   const uint8_t* lo = z + z_lo_off();
   const uint32_t* codes = reinterpret_cast<const uint32_t*>(z + z_codes_off(n_pad));
@@ -62,10 +84,12 @@ z_decode_kernel(const uint8_t* __restrict__ z, uint64_t n, uint32_t base, uint32
 #pragma unroll
     for (int q = 0; q < BITS; ++q) cw[q] = codes[seg * BITS + q];
     cw[BITS] = 0;
-    const uint32_t eoff = esc_off[b];
-    int n_e = 0;
-#pragma unroll
-    for (int i = 0; i < 32; ++i) n_e += z_code<BITS>(cw, i) == kEsc;
+    const uint32_t eoff = esc_off[b], eend = esc_off[b + 1];
+    uint8_t* se = s_esc[threadIdx.x >> 5];
+    const uint32_t n_stage = min(eend - eoff, static_cast<uint32_t>(kZEscStage));
+    for (uint32_t k = lane; k < n_stage; k += 32) se[k] = esc[eoff + k];
+    __syncwarp();
+    const int n_e = z_count_esc<BITS>(cw);
     int incl = n_e;  // warp inclusive scan of escape counts
 #pragma unroll
     for (int o = 1; o < 32; o <<= 1) {
@@ -83,7 +107,12 @@ z_decode_kernel(const uint8_t* __restrict__ z, uint64_t n, uint32_t base, uint32
         const int i = 8 * q + j;
         const uint32_t c = z_code<BITS>(cw, i);
         const uint32_t l = (lw[i >> 2] >> (8 * (i & 3))) & 0xffu;
-        const uint32_t ex = c == kEsc ? esc[e_at++] : base + c;
+        uint32_t ex = base + c;
+        if (c == kEsc) {
+          const uint32_t r = e_at - eoff;
+          ex = r < static_cast<uint32_t>(kZEscStage) ? se[r] : esc[e_at];
+          ++e_at;
+        }
         const uint32_t v = ((l & 0x80u) << 8) | (ex << 7) | (l & 0x7fu);
         if (j & 1) pk[j >> 1] |= v << 16;
         else pk[j >> 1] = v;
@@ -95,6 +124,7 @@ z_decode_kernel(const uint8_t* __restrict__ z, uint64_t n, uint32_t base, uint32
           out[v0 + 8 * q + j] = static_cast<uint16_t>(pk[j >> 1] >> (16 * (j & 1)));
       }
     }
+    __syncwarp();  // every lane done with s_esc before the next block restages it
   }
 }
 
