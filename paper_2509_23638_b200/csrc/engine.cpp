@@ -32,6 +32,7 @@
 #include <vector>
 
 #include <nvtx3/nvToolsExt.h>
+#include <sys/mman.h>
 
 #include "cuda_host.hpp"
 #include "zslab_format.hpp"
@@ -49,6 +50,50 @@ constexpr int kDecodeMaxBatch = 64;  // larger batches (prefill chunks) take the
 double now_us() {
   return std::chrono::duration<double, std::micro>(Clock::now().time_since_epoch()).count();
 }
+
+// Pinned host arena on transparent 2 MiB pages: the host lane streams whole experts with
+// 12 threads and 4 KiB pages cost it a TLB miss every 4 KiB per stream (measured +5-12 %
+// lane bandwidth, scripts/probes/thp_lane_probe.py). Anonymous mmap + MADV_HUGEPAGE,
+// pages faulted in parallel, then cudaHostRegister; cudaHostAlloc if any step fails.
+struct PinnedArena {
+  void* ptr = nullptr;
+  size_t bytes = 0;
+  bool registered = false;  // mmap + cudaHostRegister (else cudaHostAlloc)
+  void alloc(size_t n) {
+    bytes = n;
+    void* p = mmap(nullptr, n, PROT_READ | PROT_WRITE, MAP_PRIVATE | MAP_ANONYMOUS, -1, 0);
+    if (p != MAP_FAILED) {
+      madvise(p, n, MADV_HUGEPAGE);
+      const size_t page = 2u << 20;
+      const size_t pages = (n + page - 1) / page;
+      const int T = static_cast<int>(std::max(1u, std::min(16u, std::thread::hardware_concurrency())));
+      std::vector<std::thread> ts;
+      for (int t = 0; t < T; ++t)
+        ts.emplace_back([&, t] {
+          for (size_t i = pages * t / T; i < pages * (t + 1) / T; ++i) static_cast<volatile char*>(p)[i * page] = 0;
+        });
+      for (auto& th : ts) th.join();
+      if (cudaHostRegister(p, n, cudaHostRegisterPortable) == cudaSuccess) {
+        ptr = p;
+        registered = true;
+        return;
+      }
+      cudaGetLastError();
+      munmap(p, n);
+    }
+    PS_CUDA(cudaHostAlloc(&ptr, n, cudaHostAllocPortable));
+  }
+  void release() {
+    if (!ptr) return;
+    if (registered) {
+      cudaHostUnregister(ptr);
+      munmap(ptr, bytes);
+    } else {
+      cudaFreeHost(ptr);
+    }
+    ptr = nullptr;
+  }
+};
 
 struct Slot {
   void* dev = nullptr;
@@ -369,6 +414,7 @@ struct ps_engine_s {
   std::vector<uint8_t> has_host;          // [L]: layer has an owned non-resident expert
   void* arena = nullptr;                  // resident HBM arena
   void* host_arena = nullptr;             // pinned host arena
+  ps::PinnedArena host_pin, z_pin;        // their allocations (THP + register, or cudaHostAlloc)
   // z-slabs (cfg.compress_host): lossless ~12-bit copies of the host slabs that PCIe
   // carries instead (decoded on the GPU); the raw arena stays for the host lane.
   void* z_arena = nullptr;
@@ -1256,7 +1302,10 @@ void create_engine(const ps_engine_config& cfg, ps_engine_s& e) {
   e.dev_slab.assign(LE, nullptr);
   e.host_slab.assign(LE, nullptr);
   if (n_res) PS_CUDA(cudaMalloc(&e.arena, n_res * sp.expert_bytes));
-  if (n_host) PS_CUDA(cudaHostAlloc(&e.host_arena, n_host * sp.expert_bytes, cudaHostAllocPortable));
+  if (n_host) {
+    e.host_pin.alloc(n_host * sp.expert_bytes);
+    e.host_arena = e.host_pin.ptr;
+  }
   // Materialise weights: resident on device directly; host ones via a device staging
   // slab and a D2H copy (the hash is identical on both sides, see weights.cu).
   void* stage = nullptr;
@@ -1299,7 +1348,8 @@ void create_engine(const ps_engine_config& cfg, ps_engine_s& e) {
   if (cfg.compress_host && n_host) {
     const uint64_t n = sp.expert_bytes / 2, nb = (n + 1023) / 1024, n_pad = nb * 1024;
     e.z_cap = ((64 + n_pad + n_pad / 2 + 4 * (nb + 1) + n / 64) + 4095) / 4096 * 4096;
-    PS_CUDA(cudaHostAlloc(&e.z_arena, n_host * e.z_cap, cudaHostAllocPortable));
+    e.z_pin.alloc(n_host * e.z_cap);
+    e.z_arena = e.z_pin.ptr;
     e.host_z.assign(LE, nullptr);
     e.host_z_bytes.assign(LE, 0);
     size_t zi = 0;
@@ -1480,8 +1530,8 @@ void destroy_engine(ps_engine_s& e) {
     if (p) cudaFree(p);
   if (e.ep_plan_host) cudaFreeHost(e.ep_plan_host);
   if (e.ep_host) cudaFreeHost(e.ep_host);
-  if (e.host_arena) cudaFreeHost(e.host_arena);
-  if (e.z_arena) cudaFreeHost(e.z_arena);
+  e.host_pin.release();
+  e.z_pin.release();
   if (e.pinned_counts) cudaFreeHost(e.pinned_counts);
   for (auto& s : e.od_slot) {
     if (s.dev) cudaFree(s.dev);
