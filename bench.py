@@ -440,15 +440,16 @@ def run_ours(args):
 
 
 def default_host_threads():
-    """Host expert lane threads: all cores but 4 (engine thread, I/O thread, bench), at
-    most 12 (12 threads stream 120-165 GB/s on the B200 box's 16-core host; more
-    oversubscribe, profiles/r01_host_lane_micro.jsonl); 0 without AVX512_BF16."""
+    """Host expert lane threads: all cores but 2 (the engine and I/O threads mostly sleep
+    on futexes; the lane is pinned to the last CPUs), at most 14: on the B200 box's
+    16-core host 14 threads stream 153-159 GB/s vs 144-146 with 12 in the engine
+    (profiles/r01_bench_threads.jsonl); 0 without AVX512_BF16."""
     try:
         if "avx512_bf16" not in open("/proc/cpuinfo").read():
             return 0
     except OSError:
         return 0
-    return max(0, min(12, (os.cpu_count() or 1) - 4))
+    return max(0, min(14, (os.cpu_count() or 1) - 2))
 
 
 def decode_summary(st, dev_ms, N, B, L):
