@@ -293,6 +293,13 @@ class LaneDriver {
     done_ = false;
     cv_.notify_all();
   }
+  // Blocks until no batch is running, dropping any error (used at step entry so a step
+  // that failed mid-layer cannot leave the driver reading the next step's job list).
+  void drain() {
+    std::unique_lock<std::mutex> g(mu_);
+    cv_.wait(g, [&] { return done_; });
+    err_.clear();
+  }
   void wait() {
     std::unique_lock<std::mutex> g(mu_);
     cv_.wait(g, [&] { return done_; });
@@ -412,6 +419,7 @@ struct ps_engine_s {
   std::vector<const uint16_t*> host_slab; // [L*E] pinned host pointer or null
   std::vector<uint8_t> resident;          // [L*E]
   std::vector<uint8_t> has_host;          // [L]: layer has an owned non-resident expert
+  size_t host_slab_count = 0;             // owned non-resident experts (0 = fully resident)
   void* arena = nullptr;                  // resident HBM arena
   void* host_arena = nullptr;             // pinned host arena
   ps::PinnedArena host_pin, z_pin;        // their allocations (THP + register, or cudaHostAlloc)
@@ -780,6 +788,7 @@ void decode_step(ps_engine_s& e, const float* hidden, const uint8_t* follow, int
   const auto host_t0 = Clock::now();
   const double host_t0_us = now_us();
   e.cpu_done.clear();
+  if (e.lane_drv) e.lane_drv->drain();
 
   std::vector<ps_expert_load> cur, nxt, cpu_b(E), od_b(E), pf_b(E);
   const int Et = e.Et, Kt = e.Kt;
@@ -791,9 +800,12 @@ void decode_step(ps_engine_s& e, const float* hidden, const uint8_t* follow, int
     e.cur_layer = l;
     LayerDev& ld = e.layer[l];
     // Layer start: a fresh mark (the previous combine's end would also count the host's
-    // inter-layer latency, which must not leak into the calibrated t_attn).
-    PhaseTiming ph{take_event(e), nullptr, nullptr, nullptr};
-    PS_CUDA(cudaEventRecord(ph.route0, e.sc));
+    // inter-layer latency, which must not leak into the calibrated t_attn) — except on a
+    // fully resident engine, where nothing is planned or calibrated from it and the
+    // previous layer's combine end marks the same stream position one record earlier.
+    const bool reuse_mark = l > 0 && e.host_slab_count == 0 && !e.ep;
+    PhaseTiming ph{reuse_mark ? e.phase_t.back().comb1 : take_event(e), nullptr, nullptr, nullptr};
+    if (!reuse_mark) PS_CUDA(cudaEventRecord(ph.route0, e.sc));
     e.last_ffn_end = nullptr;
     nvtxRangePushA("ps.layer.route");
     // --- K1 route (+fused bf16 cast) ------------------------------------------------
@@ -1293,6 +1305,7 @@ void create_engine(const ps_engine_config& cfg, ps_engine_s& e) {
   for (int ex = 0; ex < e.E; ++ex) n_owned += owned(ex) ? e.L : 0;
   require(n_res * sp.expert_bytes <= cfg.budget_bytes, "engine: resident set exceeds the HBM budget");
   const size_t n_host = n_owned - n_res;
+  e.host_slab_count = n_host;
   e.has_host.assign(e.L, 0);
   for (int l = 0; l < e.L; ++l)
     for (int ex = 0; ex < e.E; ++ex)
