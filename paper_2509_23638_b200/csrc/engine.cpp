@@ -169,6 +169,14 @@ class IoChannel {
     }
     return out;
   }
+  // Step entry after a failed step: forget every job still queued (their FFNs were never
+  // launched, so slot generations they wait for would never come).
+  void abandon_queued() {
+    std::lock_guard<std::mutex> g(mu_);
+    for (IoJob* j : queue_) j->state = 2;
+    queue_.clear();
+    cv_.notify_all();
+  }
   void drain() {  // wait until the queue is empty and every issued copy completed
     std::unique_lock<std::mutex> g(mu_);
     cv_.wait(g, [&] { return (queue_.empty() && !busy_) || error_; });
@@ -773,6 +781,11 @@ void decode_step(ps_engine_s& e, const float* hidden, const uint8_t* follow, int
   const int L = e.L, E = e.E, K = e.K, H = e.H;
   require(B >= 1 && B <= e.maxB, "decode_step: batch out of range");
   e.prefill_mode = B > kDecodeMaxBatch;
+  // A step that threw mid-layer may have left jobs queued / a lane batch running: settle
+  // both before this step recycles the job list (no-ops after a normal step).
+  e.io->abandon_queued();
+  e.io->drain();
+  for (auto& sl : e.pf_pool) sl->in_use = false;
   // Down-projection split-K of the decode GEMV (more CTAs for single-expert on-demand
   // launches); the tcgen05 prefill path writes one split, so prefill steps use 1.
   e.step_split = e.prefill_mode ? 1 : e.n_split;
