@@ -462,6 +462,20 @@ ps_status ps_ep_all_to_all(ps_ep_comm c, const void* send, const uint64_t* send_
  * the compute stream. */
 typedef struct ps_engine_s* ps_engine;
 
+/* The reference's predictor menu (PredictorChoice, experiment.cpp:60-99) for the
+ * next-layer load prediction PreSched consumes (predict_loads, experiment.cpp:104-112):
+ *   LLAPOR   ps_llapor_forward on the GPU (K4);
+ *   GATE     gate_reuse_predict (predictor.cpp:688-690): top-k of layer l's gate weights,
+ *            i.e. layer l's own routing histogram;
+ *   STATS    stats_predict (predictor.cpp:674-686): the hot table's top-k of layer l+1
+ *            for every token;
+ *   PERFECT  the true routing of layer l+1 (K1 run one layer early on its inputs);
+ *   NONE     no prediction (no prefetch candidates). */
+typedef enum {
+  PS_PRED_AUTO = 0, PS_PRED_LLAPOR = 1, PS_PRED_GATE = 2, PS_PRED_STATS = 3,
+  PS_PRED_PERFECT = 4, PS_PRED_NONE = 5
+} ps_predictor_kind;
+
 typedef struct {
   ps_model_spec spec;
   ps_trace_gen_config gen;  /* zipf per group for the router bias */
@@ -487,6 +501,10 @@ typedef struct {
                                measured at create (unless cost.t_io > 0). 0 = GPU only. */
   int32_t compress_host;    /* 1: host slabs also kept as z-slabs (ps_zslab_encode at create);
                                loads move the z-slab over PCIe and decode it on the GPU */
+  int32_t predictor_kind;   /* ps_predictor_kind: which PredictFn (experiment.cpp:60-99)
+                               feeds PreSched's e_next (0 = LLaPor when `predictor` is set) */
+  const int32_t* stats_ranking; /* PS_PRED_STATS: [L*E] experts of each layer in hot-table
+                               order (build_hot_table ranking, predictor.cpp:405-424) */
 } ps_engine_config;
 
 ps_status ps_engine_create(const ps_engine_config* cfg, ps_engine* out);
@@ -541,6 +559,9 @@ ps_status ps_engine_reset_stats(ps_engine e);
  * (ps_verify_timeline_ex, measured = 1). */
 ps_status ps_engine_last_timeline(ps_engine e, ps_timeline* out, int32_t* truth_out,
                                   uint8_t* resident_out);
+/* Predicted per-expert token counts of the last step, [L*E] (row l = the prediction
+ * made at layer l-1 for layer l; row 0 = 0). */
+ps_status ps_engine_last_predictions(ps_engine e, int32_t* out);
 /* Replace the cost parameters PreSched plans with (e.g. beta = 1e9 disables the host
  * lane's cpu_set for a GPU-only comparison on the same engine). */
 ps_status ps_engine_set_cost(ps_engine e, const ps_cost_params* cost);

@@ -114,7 +114,8 @@ class EngineConfig(C.Structure):
                 ("max_batch", C.c_int32), ("prefetch_slots", C.c_int32), ("policy", Policy),
                 ("cost", CostParams), ("predictor", C.c_void_p), ("device", C.c_int32),
                 ("host_pinned", C.c_int32), ("ep", C.c_void_p), ("n_shared", C.c_int32),
-                ("host_threads", C.c_int32), ("compress_host", C.c_int32)]
+                ("host_threads", C.c_int32), ("compress_host", C.c_int32), ("predictor_kind", C.c_int32),
+                ("stats_ranking", C.POINTER(C.c_int32))]
 
 
 class EngineStats(C.Structure):
@@ -229,6 +230,7 @@ _SIGS = {
     "ps_engine_last_timeline": (C.c_int, [_P, C.POINTER(Timeline), _P, _P]),
     "ps_engine_calibrate": (C.c_int, [_P, C.POINTER(CostParams)]),
     "ps_engine_set_cost": (C.c_int, [_P, C.POINTER(CostParams)]),
+    "ps_engine_last_predictions": (C.c_int, [_P, _P]),
     "ps_verify_timeline_ex": (C.c_int, [C.POINTER(TimelineEvent), C.c_int, C.POINTER(PipelineInstance),
                                         C.POINTER(CostParams), C.c_int, C.POINTER(C.c_int), C.c_char_p, C.c_int]),
 }

@@ -428,6 +428,11 @@ struct ps_engine_s {
   std::vector<uint8_t> resident;          // [L*E]
   std::vector<uint8_t> has_host;          // [L]: layer has an owned non-resident expert
   size_t host_slab_count = 0;             // owned non-resident experts (0 = fully resident)
+  int pred_kind = PS_PRED_NONE;           // resolved ps_predictor_kind
+  std::vector<int32_t> stats_rank;        // [L*E] PS_PRED_STATS ranking
+  std::vector<int32_t> last_pred;         // [L*E] predictions of the last step
+  int32_t* pp_ids = nullptr;              // PS_PRED_PERFECT scratch: [maxB, k] ids
+  float* pp_w = nullptr;                  //                          [maxB, E] weights
   void* arena = nullptr;                  // resident HBM arena
   void* host_arena = nullptr;             // pinned host arena
   ps::PinnedArena host_pin, z_pin;        // their allocations (THP + register, or cudaHostAlloc)
@@ -807,6 +812,7 @@ void decode_step(ps_engine_s& e, const float* hidden, const uint8_t* follow, int
   const int Et = e.Et, Kt = e.Kt;
   std::vector<int32_t> counts_l(Et), pred_l(E);
   e.step_truth.assign(static_cast<size_t>(L) * E, 0);
+  e.last_pred.assign(static_cast<size_t>(L) * E, 0);
 
   for (int l = 0; l < L; ++l) {
     const float* x = hidden + static_cast<size_t>(l) * B * H;
@@ -850,12 +856,20 @@ void decode_step(ps_engine_s& e, const float* hidden, const uint8_t* follow, int
     // The prediction only feeds e_next (non-resident experts of l+1): a fully resident
     // next layer has no prefetch candidates whatever LLaPor says, so K4 is skipped there.
     const bool dense_next = e.prefill_mode && B * K >= 16 * E && l + 1 < L;
-    const bool predict = e.cfg.predictor && l + 1 < L && !dense_next && e.has_host[l + 1];
-    if (predict) {
+    const bool want_pred = l + 1 < L && !dense_next && e.has_host[l + 1];
+    const bool predict = want_pred && (e.pred_kind == PS_PRED_LLAPOR || e.pred_kind == PS_PRED_PERFECT);
+    if (predict && e.pred_kind == PS_PRED_LLAPOR) {
       s = ps_llapor_forward(e.cfg.predictor, l + 1, x, ld.ids, K, ld.weights, B, K, nullptr, nullptr, e.pred_dev,
                             e.llapor_scratch, e.sc);
       if (s != PS_OK) fail(s, ps_last_error());
       e.st.kernel_launches += 2;
+    } else if (predict) {  // PERFECT: layer l+1's true routing, K1 one layer early
+      const float* xn = hidden + static_cast<size_t>(l + 1) * B * H;
+      s = ps_route_topk(xn, e.gate + static_cast<size_t>(l + 1) * E * H, e.bias + static_cast<size_t>(l + 1) * E,
+                        follow ? follow + static_cast<size_t>(l + 1) * B : nullptr, ld.ids, K, B, H, E, K, nullptr,
+                        e.pp_w, e.pp_ids, e.pred_dev, nullptr, e.sc);
+      if (s != PS_OK) fail(s, ps_last_error());
+      e.st.kernel_launches += 1;
     }
     // --- K2 permute indices ------------------------------------------------------
     // Prefill-sized batches gather x into contiguous permuted rows (TMA operand of the
@@ -953,8 +967,16 @@ void decode_step(ps_engine_s& e, const float* hidden, const uint8_t* follow, int
     if (!e.ep) {
       const int32_t* off_h = e.pinned_counts + 2 * Et;  // aggregate_layer_loads = diff of K2's offsets
       for (int ex = 0; ex < Et; ++ex) counts_l[ex] = off_h[ex + 1] - off_h[ex];
-      if (predict) std::memcpy(pred_l.data(), e.pinned_counts + Et, sizeof(int32_t) * E);
-      else std::fill(pred_l.begin(), pred_l.end(), dense_next ? (B * K) / E : 0);
+      if (predict) {
+        std::memcpy(pred_l.data(), e.pinned_counts + Et, sizeof(int32_t) * E);
+      } else if (want_pred && e.pred_kind == PS_PRED_GATE) {  // top-k of layer l's gate weights
+        std::copy(counts_l.begin(), counts_l.begin() + E, pred_l.begin());
+      } else if (want_pred && e.pred_kind == PS_PRED_STATS) {  // hot table's top-k of l+1, every token
+        std::fill(pred_l.begin(), pred_l.end(), 0);
+        for (int j = 0; j < K; ++j) pred_l[e.stats_rank[static_cast<size_t>(l + 1) * E + j]] = B;
+      } else {
+        std::fill(pred_l.begin(), pred_l.end(), dense_next ? (B * K) / E : 0);
+      }
     } else {
       ep_dispatch_rows(e, B, counts_l, pred_l);
     }
@@ -978,6 +1000,7 @@ void decode_step(ps_engine_s& e, const float* hidden, const uint8_t* follow, int
       e.st.ffn_flops_total += 6.0 * rows * e.H * e.F;
     }
     std::copy(counts_l.begin(), counts_l.begin() + E, e.step_truth.begin() + static_cast<size_t>(l) * E);
+    if (l + 1 < L) std::copy(pred_l.begin(), pred_l.end(), e.last_pred.begin() + static_cast<size_t>(l + 1) * E);
     for (int i = 0; i < grp.n; ++i) e.st.resident_hits += grp.experts[i] < E && counts_l[grp.experts[i]] > 0;
 
     // Deferred HitStats for critical prefetches that targeted this layer (R2).
@@ -1319,6 +1342,16 @@ void create_engine(const ps_engine_config& cfg, ps_engine_s& e) {
   require(n_res * sp.expert_bytes <= cfg.budget_bytes, "engine: resident set exceeds the HBM budget");
   const size_t n_host = n_owned - n_res;
   e.host_slab_count = n_host;
+  e.pred_kind = cfg.predictor_kind == PS_PRED_AUTO ? (cfg.predictor ? PS_PRED_LLAPOR : PS_PRED_NONE)
+                                                   : cfg.predictor_kind;
+  require(e.pred_kind >= PS_PRED_LLAPOR && e.pred_kind <= PS_PRED_NONE, "engine: bad predictor_kind");
+  require(e.pred_kind != PS_PRED_LLAPOR || cfg.predictor, "engine: PS_PRED_LLAPOR needs a predictor");
+  require(!(cfg.ep && (e.pred_kind == PS_PRED_GATE || e.pred_kind == PS_PRED_STATS)),
+          "engine: host-side predictors (gate, stats) are not supported with expert parallelism");
+  if (e.pred_kind == PS_PRED_STATS) {
+    require(cfg.stats_ranking != nullptr, "engine: PS_PRED_STATS needs stats_ranking [L*E]");
+    e.stats_rank.assign(cfg.stats_ranking, cfg.stats_ranking + static_cast<size_t>(e.L) * e.E);
+  }
   e.has_host.assign(e.L, 0);
   for (int l = 0; l < e.L; ++l)
     for (int ex = 0; ex < e.E; ++ex)
@@ -1475,6 +1508,10 @@ void create_engine(const ps_engine_config& cfg, ps_engine_s& e) {
     PS_CUDA(cudaMemset(e.ep_zeros, 0, sizeof(int32_t) * frows));
   }
   if (cfg.predictor) PS_CUDA(cudaMalloc(&e.llapor_scratch, ps_llapor_scratch_bytes(cfg.predictor, e.maxB)));
+  if (e.pred_kind == PS_PRED_PERFECT) {
+    PS_CUDA(cudaMalloc(&e.pp_ids, sizeof(int32_t) * B * e.K));
+    PS_CUDA(cudaMalloc(&e.pp_w, sizeof(float) * B * e.E));
+  }
   PS_CUDA(cudaMalloc(&e.in_hidden, sizeof(float) * e.L * B * e.H));
   PS_CUDA(cudaMalloc(&e.in_follow, e.L * B));
   PS_CUDA(cudaMalloc(&e.out_y, sizeof(float) * e.L * B * e.H));
@@ -1546,7 +1583,7 @@ void destroy_engine(ps_engine_s& e) {
     cudaFree(ld.weights);
     cudaFree(ld.ids);
   }
-  for (void* p : {(void*)e.arena, (void*)e.gate, (void*)e.bias, (void*)e.sched_dev, (void*)e.route_ws,
+  for (void* p : {(void*)e.arena, (void*)e.gate, (void*)e.bias, (void*)e.sched_dev, (void*)e.route_ws, (void*)e.pp_ids, (void*)e.pp_w,
                   (void*)e.x_bf16, (void*)e.x_perm, (void*)e.inv, (void*)e.hbuf,
                   (void*)e.y_part, e.llapor_scratch, (void*)e.in_hidden, (void*)e.in_follow, (void*)e.out_y,
                   (void*)e.out_ids, (void*)e.ep_vids, (void*)e.ep_off_v, (void*)e.ep_perm_v, (void*)e.ep_inv_v,
@@ -1618,6 +1655,7 @@ ps_status ps_engine_decode_step_routed(ps_engine e, const float* hidden, const i
                                        float* y) {
   return guarded([&] {
     require(e && hidden && ids && weights && y, "decode_step_routed: null argument");
+    require(e->pred_kind != PS_PRED_PERFECT, "decode_step_routed: PS_PRED_PERFECT routes from the trace inputs");
     decode_step(*e, hidden, nullptr, B, y, nullptr, ids, weights);
   });
 }
@@ -1669,6 +1707,13 @@ ps_status ps_engine_last_timeline(ps_engine e, ps_timeline* out, int32_t* truth_
     if (out->layer_end) std::copy(e->last_layer_end.begin(), e->last_layer_end.end(), out->layer_end);
     if (truth_out) std::copy(e->last_truth.begin(), e->last_truth.end(), truth_out);
     if (resident_out) std::copy(e->resident.begin(), e->resident.end(), resident_out);
+  });
+}
+
+ps_status ps_engine_last_predictions(ps_engine e, int32_t* out) {
+  return guarded([&] {
+    require(e && out, "ps_engine_last_predictions: null argument");
+    std::copy(e->last_pred.begin(), e->last_pred.end(), out);
   });
 }
 

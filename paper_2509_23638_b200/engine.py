@@ -99,7 +99,8 @@ class Engine:
                  gate: np.ndarray, budget_fraction: float | None = None, budget_bytes: int | None = None,
                  resident=None, trace_hidden=None, trace_follow=None, policy: str = "presched",
                  predictor=None, cost=None, prefetch_slots: int = 8, device: int = 0, ep=None,
-                 n_shared: int = 0, host_threads: int = 0, compress_host: bool = False):
+                 n_shared: int = 0, host_threads: int = 0, compress_host: bool = False,
+                 predictor_kind: str = "auto", stats_ranking=None):
         from . import parse_policy, plan_residency, trace_inputs  # noqa: F401
         self.lib = load()
         self.spec = spec
@@ -136,6 +137,11 @@ class Engine:
         cfg.n_shared = n_shared
         cfg.host_threads = host_threads
         cfg.compress_host = int(bool(compress_host))
+        kinds = {"auto": 0, "llapor": 1, "gate": 2, "stats": 3, "perfect": 4, "none": 5}
+        cfg.predictor_kind = kinds[predictor_kind]
+        if stats_ranking is not None:
+            self._rank = np.ascontiguousarray(stats_ranking, np.int32).reshape(-1)
+            cfg.stats_ranking = self._rank.ctypes.data_as(C.POINTER(C.c_int32))
         self.host_threads = host_threads
         h = C.c_void_p()
         check(self.lib.ps_engine_create(C.byref(cfg), C.byref(h)))
@@ -225,6 +231,12 @@ class Engine:
         c = capi.CostParams()
         check(self.lib.ps_engine_calibrate(self.h, C.byref(c)))
         return dict(t_io=c.t_io, t_g=c.t_g, t_attn=c.t_attn, beta=c.beta, startup=c.startup)
+
+    def last_predictions(self):
+        """[L,E] predicted token counts of the last step (row l: predicted at layer l-1)."""
+        out = np.zeros((self.spec.num_layers, self.spec.experts_per_layer), np.int32)
+        check(self.lib.ps_engine_last_predictions(self.h, out.ctypes.data_as(C.c_void_p)))
+        return out
 
     def set_cost(self, t_io, t_g, t_attn, beta, startup):
         """Replace the PreSched cost parameters (ps_engine_set_cost)."""

@@ -217,3 +217,39 @@ def test_engine_prefill_chunk_with_host_lane(torch_cuda, compress):
     assert agree >= 0.99
     assert np.linalg.norm(y - y_ref) / np.linalg.norm(y_ref) < BF16_RTOL
     assert st["cpu_experts"] > 0
+
+
+def test_engine_predictor_menu_matches_reference_predict_loads(torch_cuda):
+    """The reference's PredictFn menu (experiment.cpp:60-99) on the executor: the loads
+    PreSched sees for layer l+1 equal predict_loads of that predictor — PERFECT = the true
+    histogram of l+1, GATE = gate_reuse_predict = layer l's own histogram, STATS = the hot
+    table's top-k of l+1 for every token — and the MoE outputs do not depend on it."""
+    spec = _small_spec()
+    cfg = ps.TraceGenConfig(*[ps.GROUP_DEFAULT_GEN[g] for g in ("input", "middle", "output")])
+    B = 8
+    gate, hidden, follow, zipf = ps.trace_inputs(cfg, spec, B, 3)
+    L, E, k = spec.num_layers, spec.experts_per_layer, spec.top_k
+    freq = eng.hot_table(spec, gate, hidden, follow, zipf)
+    rank = np.argsort(-freq, axis=1, kind="stable").astype(np.int32)  # ties -> lower expert
+    outs = {}
+    for kind in ("perfect", "gate", "stats", "none"):
+        with eng.Engine(spec, cfg, budget_fraction=0.0, max_batch=B, weight_seed=9, gate=gate, trace_hidden=hidden,
+                        trace_follow=follow, predictor_kind=kind, stats_ranking=rank) as e:
+            y, ids = e.step_host(hidden, follow)
+            pred = e.last_predictions()
+            _, truth, _, _, _ = e.last_timeline()
+        truth = np.asarray(truth).reshape(L, E)
+        outs[kind] = y
+        for l in range(1, L):
+            if kind == "perfect":
+                np.testing.assert_array_equal(pred[l], truth[l])
+            elif kind == "gate":
+                np.testing.assert_array_equal(pred[l], truth[l - 1])
+            elif kind == "stats":
+                want = np.zeros(E, np.int32)
+                want[rank[l, :k]] = B
+                np.testing.assert_array_equal(pred[l], want)
+            else:
+                assert not pred[l].any()
+    for kind in ("gate", "stats", "none"):
+        np.testing.assert_array_equal(outs[kind], outs["perfect"])
