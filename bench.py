@@ -189,8 +189,10 @@ def workload_config(args, spec, executor="gpu_only"):
                         f"other experts in pinned host DRAM, policy {args.policy}"
                         + (", PreSched cpu_set on the host expert lane (AMX-BF16)" if executor == "host_lane" else
                            ", GPU-only executor")
-                        + (", loads as lossless 12-bit z-slabs decoded on the GPU" if getattr(args, "compress", 0)
-                           else ""),
+                        + (", loads as lossless z-slabs decoded on the GPU" if getattr(args, "compress", 0)
+                           else "")
+                        + f", predictor {getattr(args, 'predictor', 'llapor')}"
+                        + (" (random-init at full shape)" if getattr(args, "predictor", "llapor") == "llapor" else ""),
             "expert_shape": f"{args.model}-8x7b" if args.model == "mixtral" else args.model,
             "decode_batch": args.batch, "global_batch": args.batch * args.gpus,
             "parallelism": (f"ep{args.gpus}" if args.gpus > 1 else "single"),
@@ -253,7 +255,8 @@ def run_ours(args):
     t_create = time.perf_counter()
     e = eng.Engine(spec, gen, max_batch=B, weight_seed=args.weight_seed, gate=gate, budget_bytes=budget_bytes,
                    resident=resident, policy=args.policy, predictor=predictor, device=local, ep=ep,
-                   host_threads=host_threads if world == 1 else 0, compress_host=bool(args.compress))
+                   host_threads=host_threads if world == 1 else 0, compress_host=bool(args.compress),
+                   predictor_kind=args.predictor)
     t_create = time.perf_counter() - t_create
     measured_cost = e.stats()["cost"]
 
@@ -502,6 +505,8 @@ def main():
     ap.add_argument("--no-all-resident", action="store_true")
     ap.add_argument("--prefill-tokens", type=int, default=4096)
     ap.add_argument("--prefill-steps", type=int, default=5)
+    ap.add_argument("--predictor", default="llapor", choices=["llapor", "gate", "perfect", "none"],
+                    help="next-layer load predictor feeding PreSched (the reference's PredictFn menu)")
     ap.add_argument("--compress", type=int, default=1,
                     help="1: non-resident experts cross PCIe as lossless z-slabs (decoded on the GPU)")
     ap.add_argument("--host-threads", type=int, default=-1,
