@@ -373,6 +373,8 @@ ps_status ps_host_lane_create(int threads, ps_host_lane* out);
 ps_status ps_host_lane_destroy(ps_host_lane lane);
 int ps_host_lane_threads(ps_host_lane lane);
 int ps_host_lane_isa(ps_host_lane lane); /* 2 = AMX-BF16 tiles, 1 = AVX512-BF16 GEMV */
+/* 1 if ps_host_expert_ffn_batch_z runs on this host (AMX-BF16 + AVX-512 VBMI2) */
+int ps_host_lane_reads_z(ps_host_lane lane);
 /* Pin the calling thread (the one that will call ps_host_expert_ffn*: pool worker 0) to
  * the lane's first CPU. The pool's workers are pinned to the last `threads` CPUs of the
  * process affinity set unless PS_HOST_LANE_PIN=0. */
@@ -390,6 +392,16 @@ ps_status ps_host_expert_ffn_batch_z(ps_host_lane lane, int n, const uint8_t* co
 ps_status ps_host_expert_ffn_batch(ps_host_lane lane, int n, const uint16_t* const* slabs,
                                    const int32_t* m, const int32_t* row0, int H, int F,
                                    const uint16_t* x, float* y);
+/* The lane's tile layout: ps_host_slab_tile re-lays a slab in place so that every 16-row
+ * block of W_gate/W_up [F][H] and W_down [H][F] is a run of 16x32 tiles of 1 KiB (the
+ * block keeps its byte range); ps_host_expert_ffn_batch_tiled reads slabs in that layout
+ * (AMX-BF16 lanes only) with two sequential streams per block instead of 32 row streams.
+ * Bitwise the results of ps_host_expert_ffn_batch on the row-major slabs. */
+ps_status ps_host_slab_tile(uint16_t* slab, int H, int F);
+ps_status ps_host_slab_untile(uint16_t* slab, int H, int F); /* inverse of ps_host_slab_tile */
+ps_status ps_host_expert_ffn_batch_tiled(ps_host_lane lane, int n, const uint16_t* const* slabs,
+                                         const int32_t* m, const int32_t* row0, int H, int F,
+                                         const uint16_t* x, float* y);
 
 /* z-slabs: lossless transfer format of a host-resident expert slab (csrc/zexpert.cu):
  * verbatim sign+mantissa bytes, 4-bit exponent codes relative to a per-slab base, escapes
@@ -399,6 +411,11 @@ uint64_t ps_zslab_bound(uint64_t n);  /* worst-case z-slab bytes for n bf16 valu
 ps_status ps_zslab_encode(const uint16_t* slab, uint64_t n, uint8_t* out, uint64_t cap,
                           uint64_t* out_bytes, int threads);
 ps_status ps_zslab_info(const uint8_t* z_host, uint64_t* n, uint64_t* bytes, uint64_t* n_escapes);
+/* z-slab of a slab in the lane's tile layout (after ps_host_slab_tile): header marked
+ * tiled, so ps_zslab_decode still writes the row-major slab and the lane's z path reads
+ * every 16-row block as two sequential streams. */
+ps_status ps_zslab_encode_tiled(const uint16_t* slab_tiled, int H, int F, uint8_t* out, uint64_t cap,
+                                uint64_t* out_bytes, int threads);
 /* z_dev: device copy of the z-slab; z_host_header: the host z-slab (header read on the host). */
 ps_status ps_zslab_decode(const uint8_t* z_dev, const uint8_t* z_host_header, uint16_t* out,
                           void* stream);

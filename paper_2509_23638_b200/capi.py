@@ -183,9 +183,14 @@ _SIGS = {
     "ps_host_lane_destroy": (C.c_int, [_P]),
     "ps_host_lane_threads": (C.c_int, [_P]),
     "ps_host_lane_isa": (C.c_int, [_P]),
+    "ps_host_lane_reads_z": (C.c_int, [_P]),
     "ps_host_lane_bind_caller": (C.c_int, [_P]),
     "ps_host_expert_ffn": (C.c_int, [_P, _P, C.c_int, C.c_int, _P, C.c_int, _P]),
     "ps_host_expert_ffn_batch": (C.c_int, [_P, C.c_int, _P, _P, _P, C.c_int, C.c_int, _P, _P]),
+    "ps_host_expert_ffn_batch_tiled": (C.c_int, [_P, C.c_int, _P, _P, _P, C.c_int, C.c_int, _P, _P]),
+    "ps_host_slab_tile": (C.c_int, [_P, C.c_int, C.c_int]),
+    "ps_host_slab_untile": (C.c_int, [_P, C.c_int, C.c_int]),
+    "ps_zslab_encode_tiled": (C.c_int, [_P, C.c_int, C.c_int, _P, C.c_uint64, C.POINTER(C.c_uint64), C.c_int]),
     "ps_host_expert_ffn_batch_z": (C.c_int, [_P, C.c_int, _P, _P, _P, C.c_int, C.c_int, _P, _P]),
     "ps_cast_bf16": (C.c_int, [_P, C.c_int64, _P, _P]),
     "ps_engine_decode_step_routed": (C.c_int, [_P, _P, _P, _P, C.c_int, _P]),

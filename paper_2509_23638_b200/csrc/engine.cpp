@@ -20,6 +20,7 @@
 // SURVEY.md §7 hard part 1) is loaded on demand after ondemand_seq.
 #include <algorithm>
 #include <atomic>
+#include <functional>
 #include <chrono>
 #include <cmath>
 #include <condition_variable>
@@ -273,6 +274,14 @@ struct CpuJob {
 // them tile by tile costs more CPU than the bytes save on the 16-core B200 host (75-79
 // vs 88-135 GB/s of expert weights, profiles/r01_host_lane_micro_z.jsonl): raw bf16 by
 // default, PS_HOST_LANE_Z=1 opts in.
+bool lane_tiles_enabled() {  // PS_HOST_LANE_TILED=0 keeps the row-major host slabs
+  static const bool on = [] {
+    const char* v = std::getenv("PS_HOST_LANE_TILED");
+    return !(v && v[0] == '0');
+  }();
+  return on;
+}
+
 bool lane_z_enabled() {
   static const bool on = [] {
     const char* v = std::getenv("PS_HOST_LANE_Z");
@@ -284,6 +293,7 @@ bool lane_z_enabled() {
 class LaneDriver {
  public:
   LaneDriver(ps_host_lane lane, int H, int F) : lane_(lane), H_(H), F_(F), thread_([this] { loop(); }) {}
+  std::atomic<bool> tiled{false};  // raw host slabs are in the lane's tile layout (set before any submit)
   ~LaneDriver() {
     {
       std::lock_guard<std::mutex> g(mu_);
@@ -334,7 +344,7 @@ class LaneDriver {
       zs_.clear();
       m_.clear();
       row0_.clear();
-      bool all_z = lane_z_enabled() && ps_host_lane_isa(lane_) == 2;
+      bool all_z = lane_z_enabled() && ps_host_lane_reads_z(lane_);
       for (const CpuJob& j : *jobs) {
         slabs_.push_back(j.slab);
         zs_.push_back(j.z);
@@ -346,8 +356,8 @@ class LaneDriver {
       const int n = static_cast<int>(jobs->size());
       const ps_status st = all_z ? ps_host_expert_ffn_batch_z(lane_, n, zs_.data(), m_.data(), row0_.data(), H_, F_,
                                                               x_, y_)
-                                 : ps_host_expert_ffn_batch(lane_, n, slabs_.data(), m_.data(), row0_.data(), H_, F_,
-                                                            x_, y_);
+                                 : (tiled.load() ? ps_host_expert_ffn_batch_tiled : ps_host_expert_ffn_batch)(
+                                       lane_, n, slabs_.data(), m_.data(), row0_.data(), H_, F_, x_, y_);
       if (st != PS_OK) err = ps_last_error();
       const double t1 = now_us();
       for (CpuJob& j : *jobs) {
@@ -442,6 +452,7 @@ struct ps_engine_s {
   size_t z_cap = 0;                        // bytes per z-slab slot
   std::vector<const uint8_t*> host_z;      // [L*E] or empty
   std::vector<uint64_t> host_z_bytes;      // [L*E]
+  bool host_tiled = false;                 // host_slab in the lane's tile layout (lane-only; PCIe reads host_z)
   ps::Slot od_slot[2];
   std::vector<std::unique_ptr<ps::Slot>> pf_pool;
 
@@ -1411,16 +1422,55 @@ void create_engine(const ps_engine_config& cfg, ps_engine_s& e) {
     e.z_arena = e.z_pin.ptr;
     e.host_z.assign(LE, nullptr);
     e.host_z_bytes.assign(LE, 0);
-    size_t zi = 0;
-    for (size_t idx = 0; idx < LE; ++idx) {
-      if (!e.host_slab[idx]) continue;
-      uint8_t* z = static_cast<uint8_t*>(e.z_arena) + zi++ * e.z_cap;
-      uint64_t bytes = 0;
-      if (ps_zslab_encode(e.host_slab[idx], n, z, e.z_cap, &bytes, 0) == PS_OK) {
-        e.host_z[idx] = z;
-        e.host_z_bytes[idx] = bytes;
+    // With an AMX host lane, the raw slabs only feed the lane (PCIe reads the z-slabs):
+    // re-lay them into the lane's tile layout first and encode the tiled values, so both
+    // the lane's raw and z paths read sequential streams (ps_zslab_decode un-tiles on the
+    // GPU). If any slab does not fit a z-slab, everything goes back to row-major.
+    bool tiled = false;
+    if (cfg.host_threads > 0 && lane_tiles_enabled()) {
+      ps_host_lane probe_lane = nullptr;
+      if (ps_host_lane_create(1, &probe_lane) == PS_OK) {
+        tiled = ps_host_lane_isa(probe_lane) == 2;
+        ps_host_lane_destroy(probe_lane);
       }
     }
+    std::vector<uint16_t*> hosts;
+    for (size_t idx = 0; idx < LE; ++idx)
+      if (e.host_slab[idx]) hosts.push_back(const_cast<uint16_t*>(e.host_slab[idx]));
+    auto parallel_slabs = [&](const std::function<bool(uint16_t*)>& fn) {
+      std::atomic<size_t> next{0};
+      std::atomic<bool> ok{true};
+      std::vector<std::thread> th;
+      const unsigned nt = std::max(1u, std::min<unsigned>(std::thread::hardware_concurrency(), 32));
+      for (unsigned t = 0; t < nt; ++t)
+        th.emplace_back([&] {
+          for (size_t i; (i = next.fetch_add(1)) < hosts.size();)
+            if (!fn(hosts[i])) ok = false;
+        });
+      for (auto& t : th) t.join();
+      return ok.load();
+    };
+    if (tiled && !parallel_slabs([&](uint16_t* p) { return ps_host_slab_tile(p, e.H, e.F) == PS_OK; }))
+      fail(PS_ERUNTIME, "engine: host slab re-layout failed");
+    for (int pass = 0; pass < 2; ++pass) {
+      size_t zi = 0;
+      bool all = true;
+      for (size_t idx = 0; idx < LE; ++idx) {
+        if (!e.host_slab[idx]) continue;
+        uint8_t* z = static_cast<uint8_t*>(e.z_arena) + zi++ * e.z_cap;
+        uint64_t bytes = 0;
+        const ps_status st = tiled ? ps_zslab_encode_tiled(e.host_slab[idx], e.H, e.F, z, e.z_cap, &bytes, 0)
+                                   : ps_zslab_encode(e.host_slab[idx], n, z, e.z_cap, &bytes, 0);
+        e.host_z[idx] = st == PS_OK ? z : nullptr;
+        e.host_z_bytes[idx] = st == PS_OK ? bytes : 0;
+        all = all && st == PS_OK;
+      }
+      if (all || !tiled) break;
+      if (!parallel_slabs([&](uint16_t* p) { return ps_host_slab_untile(p, e.H, e.F) == PS_OK; }))
+        fail(PS_ERUNTIME, "engine: host slab re-layout failed");
+      tiled = false;
+    }
+    e.host_tiled = tiled;
   }
   if (auto_cost && e.z_cap) {  // provisional t_io from the mean z-slab size
     double zb = 0, cnt = 0;
@@ -1527,6 +1577,7 @@ void create_engine(const ps_engine_config& cfg, ps_engine_s& e) {
     PS_CUDA(cudaHostAlloc(&e.lane_xrows, sizeof(uint16_t) * rows_t * e.H, cudaHostAllocDefault));
     PS_CUDA(cudaHostAlloc(&e.lane_yrows, sizeof(float) * rows_t * e.H, cudaHostAllocDefault));
     e.lane_drv = std::make_unique<LaneDriver>(e.lane, e.H, e.F);
+    e.lane_drv->tiled = e.host_tiled;
     // cpu_cost = beta*m + C (cost_model.cpp:34-37) measured on this host: the lane on a
     // host-resident expert slab at two token counts (below), best of 3 each.
     const uint16_t* probe = nullptr;
@@ -1534,8 +1585,7 @@ void create_engine(const ps_engine_config& cfg, ps_engine_s& e) {
     for (size_t i = 0; i < e.host_slab.size(); ++i)
       if (e.host_slab[i]) {
         probe = e.host_slab[i];
-        if (!e.host_z.empty() && lane_z_enabled() && ps_host_lane_isa(e.lane) == 2 && e.host_z[i] &&
-            reinterpret_cast<const ZHeader*>(e.host_z[i])->code_bits == 4)
+        if (!e.host_z.empty() && lane_z_enabled() && ps_host_lane_reads_z(e.lane) && e.host_z[i])
           probe_z = e.host_z[i];
         break;
       }
@@ -1548,7 +1598,8 @@ void create_engine(const ps_engine_config& cfg, ps_engine_s& e) {
           const int32_t row0 = 0;
           const ps_status st = probe_z ? ps_host_expert_ffn_batch_z(e.lane, 1, &probe_z, &m, &row0, e.H, e.F,
                                                                     e.lane_xrows, e.lane_yrows)
-                                       : ps_host_expert_ffn(e.lane, probe, e.H, e.F, e.lane_xrows, m, e.lane_yrows);
+                                       : (e.host_tiled ? ps_host_expert_ffn_batch_tiled : ps_host_expert_ffn_batch)(
+                                             e.lane, 1, &probe, &m, &row0, e.H, e.F, e.lane_xrows, e.lane_yrows);
           if (st != PS_OK) fail(PS_ERUNTIME, ps_last_error());
           t = std::min(t, now_us() - a);
         }

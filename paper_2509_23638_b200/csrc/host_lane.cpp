@@ -204,23 +204,35 @@ void amx_config() {
 
 // Phase 1 on 16 rows [r, r+16) of W_gate/W_up and one group of 16 tokens:
 // xb = packed x of the group [H/2][16][2]; writes h (VNNI layout hb [F/2][16][2]) for
-// those rows.
+// those rows. kTiled: the slab is in the lane's tile layout (ps_host_slab_tile): the 16-row
+// block occupies the same bytes as in row-major order, but as consecutive 16x32 tiles of
+// 1 KiB (column tile kb at + kb*512 values), so a block is two sequential streams instead
+// of 32 row streams — the hardware prefetchers keep far more lines in flight per core.
+template <bool kTiled>
 __attribute__((target("amx-tile,amx-bf16,avx512f")))
 void amx_gate_up_block(const uint16_t* wg, const uint16_t* wu, const uint16_t* xb, int H, int r, uint16_t* hb) {
   alignas(64) float cg[16 * 16], cu[16 * 16];
-  const size_t pitch = static_cast<size_t>(H) * 2;
+  const size_t pitch = kTiled ? 64 : static_cast<size_t>(H) * 2;
   const uint16_t* ag = wg + static_cast<size_t>(r) * H;
   const uint16_t* au = wu + static_cast<size_t>(r) * H;
   _tile_zero(0);
   _tile_zero(1);
   for (int k = 0; k < H; k += 32) {
-    if (k + 512 < H)
+    const size_t o = kTiled ? static_cast<size_t>(k) * 16 : static_cast<size_t>(k);
+    if (kTiled) {
+      if (k + 256 < H)
+        for (int q = 0; q < 16; ++q) {
+          _mm_prefetch(reinterpret_cast<const char*>(ag + o + 8 * 512) + 64 * q, _MM_HINT_T0);
+          _mm_prefetch(reinterpret_cast<const char*>(au + o + 8 * 512) + 64 * q, _MM_HINT_T0);
+        }
+    } else if (k + 512 < H) {
       for (int i = 0; i < 16; ++i) {
         _mm_prefetch(reinterpret_cast<const char*>(ag + static_cast<size_t>(i) * H + k + 512), _MM_HINT_T0);
         _mm_prefetch(reinterpret_cast<const char*>(au + static_cast<size_t>(i) * H + k + 512), _MM_HINT_T0);
       }
-    _tile_loadd(2, ag + k, pitch);
-    _tile_loadd(3, au + k, pitch);
+    }
+    _tile_loadd(2, ag + o, pitch);
+    _tile_loadd(3, au + o, pitch);
     _tile_loadd(4, xb + static_cast<size_t>(k) * kTok, 64);
     _tile_dpbf16ps(0, 2, 4);
     _tile_dpbf16ps(1, 3, 4);
@@ -237,17 +249,23 @@ void amx_gate_up_block(const uint16_t* wg, const uint16_t* wu, const uint16_t* x
 
 // Phase 2 on 16 rows [r, r+16) of W_down against hb (VNNI [F/2][16][2]); y[t*H + r+i]
 // for the first m tokens of the group.
+template <bool kTiled>
 __attribute__((target("amx-tile,amx-bf16,avx512f")))
 void amx_down_block(const uint16_t* wd, const uint16_t* hb, int H, int F, int r, int m, float* y) {
   alignas(64) float c[16 * 16];
-  const size_t pitch = static_cast<size_t>(F) * 2;
+  const size_t pitch = kTiled ? 64 : static_cast<size_t>(F) * 2;
   const uint16_t* a = wd + static_cast<size_t>(r) * F;
   _tile_zero(0);
   for (int k = 0; k < F; k += 32) {
-    if (k + 512 < F)
+    const size_t o = kTiled ? static_cast<size_t>(k) * 16 : static_cast<size_t>(k);
+    if (kTiled) {
+      if (k + 256 < F)
+        for (int q = 0; q < 16; ++q) _mm_prefetch(reinterpret_cast<const char*>(a + o + 8 * 512) + 64 * q, _MM_HINT_T0);
+    } else if (k + 512 < F) {
       for (int i = 0; i < 16; ++i)
         _mm_prefetch(reinterpret_cast<const char*>(a + static_cast<size_t>(i) * F + k + 512), _MM_HINT_T0);
-    _tile_loadd(2, a + k, pitch);
+    }
+    _tile_loadd(2, a + o, pitch);
     _tile_loadd(4, hb + static_cast<size_t>(k) * kTok, 64);
     _tile_dpbf16ps(0, 2, 4);
   }
@@ -256,80 +274,190 @@ void amx_down_block(const uint16_t* wd, const uint16_t* hb, int H, int F, int r,
     for (int i = 0; i < 16; ++i) y[static_cast<size_t>(t) * H + r + i] = c[i * 16 + t];
 }
 
+void untile_matrix_inplace(uint16_t* w, int R, int K, std::vector<uint16_t>& tmp) {
+  tmp.resize(static_cast<size_t>(16) * K);
+  for (int rb = 0; rb < R / 16; ++rb) {
+    uint16_t* blk = w + static_cast<size_t>(rb) * 16 * K;
+    std::memcpy(tmp.data(), blk, sizeof(uint16_t) * 16 * K);
+    for (int kb = 0; kb < K / 32; ++kb)
+      for (int i = 0; i < 16; ++i)
+        std::memcpy(blk + static_cast<size_t>(i) * K + kb * 32, tmp.data() + static_cast<size_t>(kb) * 512 + i * 32, 64);
+  }
+}
+
+// In-place re-layout of one [R][K] matrix into 16x32 tiles, block by block (a 16-row block
+// keeps its byte range).
+void tile_matrix_inplace(uint16_t* w, int R, int K, std::vector<uint16_t>& tmp) {
+  tmp.resize(static_cast<size_t>(16) * K);
+  for (int rb = 0; rb < R / 16; ++rb) {
+    uint16_t* blk = w + static_cast<size_t>(rb) * 16 * K;
+    std::memcpy(tmp.data(), blk, sizeof(uint16_t) * 16 * K);
+    for (int kb = 0; kb < K / 32; ++kb)
+      for (int i = 0; i < 16; ++i)
+        std::memcpy(blk + static_cast<size_t>(kb) * 512 + i * 32, tmp.data() + static_cast<size_t>(i) * K + kb * 32, 64);
+  }
+}
+
 __attribute__((target("amx-tile"))) void amx_release() { _tile_release(); }
-// ---- z-slab path: the lane reads the 12-bit transfer format instead of bf16 --------
-// Host DRAM is the lane's bound, so reading 1.5 B instead of 2 B per weight is worth a
+// ---- z-slab path: the lane reads the transfer format instead of bf16 -----------------
+// Host DRAM is the lane's bound, so reading 1.41-1.5 B instead of 2 B per weight is worth a
 // few vector ops: each 16-row x 32-column A tile is decoded from the z-slab into a 1 KiB
-// scratch (AVX-512: sign/mantissa bytes widened to 16 bit, 4-bit exponent codes unpacked
-// and rebased, escapes patched from the block's escape list) and loaded from there.
+// scratch and loaded from there. Per 32-value row segment (AVX-512 VBMI/VBMI2, branch-free):
+// sign/mantissa bytes widened to 16 bit; the 3- or 4-bit exponent codes (a little-endian
+// bit stream) pulled into 16-bit lanes with one byte permute + variable shift and rebased;
+// escaped lanes patched with an expand-load from the block's escape list. Each row keeps a
+// running escape pointer, so no per-segment rank scan.
 
-// Escaped exponents of the 32-value segment at value index v (v % 32 == 0, so the
-// segment lies in one 1024-value block): rank of the first one = escapes in the block
-// before v.
-inline void z_patch_escapes(const ZView& z, uint64_t v, uint16_t* seg) {
+bool z_isa_ok() {
+  static const bool ok = [] {
+    __builtin_cpu_init();
+    return __builtin_cpu_supports("avx512vbmi") && __builtin_cpu_supports("avx512vbmi2") &&
+           __builtin_cpu_supports("avx512bw") && __builtin_cpu_supports("avx512vl");
+  }();
+  return ok;
+}
+
+inline uint32_t z_code_at(const ZView& z, uint64_t u) {  // scalar code of value u
+  const uint64_t bit = u * z.bits;
+  const uint32_t w = z.codes[bit >> 3] | (static_cast<uint32_t>(z.codes[(bit >> 3) + 1]) << 8);
+  return (w >> (bit & 7)) & z_escape(z.bits);
+}
+
+// Escape-list position of value v: the block's first escape + escapes in the block before v.
+inline const uint8_t* z_esc_ptr(const ZView& z, uint64_t v) {
   const uint64_t b = v / kZBlock;
+  const uint32_t esc = z_escape(z.bits);
   uint32_t rank = 0;
-  for (uint64_t u = b * kZBlock; u < v; u += 2) {
-    const uint8_t c = z.codes[u / 2];
-    rank += (c & 15) == kZEscape;
-    rank += (c >> 4) == kZEscape;
-  }
-  const uint8_t* e = z.esc + z.esc_off[b] + rank;
-  for (int i = 0; i < 32; ++i) {
-    const uint8_t c = (z.codes[(v + i) / 2] >> (4 * ((v + i) & 1))) & 15;
-    if (c == kZEscape) seg[i] = static_cast<uint16_t>((seg[i] & 0x807fu) | (static_cast<uint32_t>(*e++) << 7));
-  }
+  for (uint64_t u = b * kZBlock; u < v; ++u) rank += z_code_at(z, u) == esc;
+  return z.esc + z.esc_off[b] + rank;
 }
 
-// 32 values at v -> seg[32] bf16.
-__attribute__((target("avx512f,avx512bw,avx512vl")))
-inline void z_decode32(const ZView& z, uint64_t v, uint16_t* seg) {
-  const __m512i lo16 = _mm512_cvtepu8_epi16(_mm256_loadu_si256(reinterpret_cast<const __m256i*>(z.lo + v)));
-  const __m128i cb = _mm_loadu_si128(reinterpret_cast<const __m128i*>(z.codes + v / 2));
-  const __m128i nib = _mm_set1_epi8(0x0f);
-  const __m128i ev = _mm_and_si128(cb, nib), od = _mm_and_si128(_mm_srli_epi16(cb, 4), nib);
-  const __m256i codes8 = _mm256_set_m128i(_mm_unpackhi_epi8(ev, od), _mm_unpacklo_epi8(ev, od));
-  const __m512i code16 = _mm512_cvtepu8_epi16(codes8);
-  const __m512i exp16 = _mm512_add_epi16(code16, _mm512_set1_epi16(static_cast<short>(z.base)));
-  const __m512i val = _mm512_or_si512(
-      _mm512_or_si512(_mm512_slli_epi16(_mm512_and_si512(lo16, _mm512_set1_epi16(0x80)), 8),
-                      _mm512_slli_epi16(exp16, 7)),
-      _mm512_and_si512(lo16, _mm512_set1_epi16(0x7f)));
-  _mm512_storeu_si512(seg, val);
-  if (_mm512_cmpeq_epi16_mask(code16, _mm512_set1_epi16(kZEscape))) z_patch_escapes(z, v, seg);
+struct alignas(64) ZDec {  // per-slab constants of the vector decoder (plain data)
+  uint8_t perm[64];   // byte permute: qword q (values 8q..8q+7) <- code bytes q*bits .. q*bits+7
+  uint8_t shift[64];  // multishift: byte j of each qword <- bits j*bits .. j*bits+7 of it
+  uint8_t cmask, base;
+  uint32_t seg_bytes;  // code bytes per 64-value segment
+};
+
+ZDec z_dec(const ZView& z) {
+  ZDec d{};
+  for (int q = 0; q < 8; ++q)
+    for (int b = 0; b < 8; ++b) {
+      d.perm[8 * q + b] = static_cast<uint8_t>(q * static_cast<int>(z.bits) + b);
+      d.shift[8 * q + b] = static_cast<uint8_t>(b * static_cast<int>(z.bits));
+    }
+  d.cmask = static_cast<uint8_t>(z_escape(z.bits));
+  d.base = static_cast<uint8_t>(z.base);
+  d.seg_bytes = 8 * z.bits;
+  return d;
 }
 
-// A tile (16 rows x 32 cols) of the row-major matrix whose row r starts at value `rowv`,
-// row length `ld` values, column k -> scratch [16][32]. The 16 rows are 32 streams (sign/
-// mantissa bytes and codes) — too many for the hardware prefetchers — so every row's
-// lines are prefetched 1 KiB of values ahead.
-__attribute__((target("avx512f,avx512bw,avx512vl")))
-inline void z_tile(const ZView& z, uint64_t rowv, uint64_t ld, int k, int kend, uint16_t* scratch) {
-  const int kp = k + 1024;
+struct ZRegs {
+  __m512i perm, shift, cmask, base, m80, lo_idx, hi_idx;
+};
+
+__attribute__((target("avx512f,avx512bw,avx512vl,avx512vbmi")))
+inline ZRegs z_regs(const ZDec& d) {
+  // bf16 values 0-31 / 32-63 from the in-lane byte interleaves u0 = unpacklo(lo, hi)
+  // (values 0-7 | 16-23 | 32-39 | 48-55) and u1 = unpackhi (8-15 | 24-31 | ...)
+  return {_mm512_loadu_si512(d.perm), _mm512_loadu_si512(d.shift), _mm512_set1_epi8(static_cast<char>(d.cmask)),
+          _mm512_set1_epi8(static_cast<char>(d.base)), _mm512_set1_epi8(static_cast<char>(0x80)),
+          _mm512_set_epi64(11, 10, 3, 2, 9, 8, 1, 0), _mm512_set_epi64(15, 14, 7, 6, 13, 12, 5, 4)};
+}
+
+// 64 values at v (v % 64 == 0) -> seg[0..31], seg[512..543] (the same row of two
+// consecutive 16x32 tiles); ep = this row's escape pointer. Byte-wide throughout (64
+// values per op; 512-bit ALU work has two ports): codes pulled out of the bit stream with
+// one byte permute + multishift, escapes merged by an expand-load, then the two bf16
+// bytes (sign|exp>>1, exp<<7|mantissa) built with bit-selects and interleaved.
+__attribute__((target("avx512f,avx512bw,avx512vl,avx512vbmi,avx512vbmi2")))
+inline void z_decode64(const ZView& z, const ZRegs& r, uint32_t seg_bytes, uint64_t v, const uint8_t*& ep,
+                       uint16_t* seg, uint16_t* seg2) {
+  const __m512i L = _mm512_loadu_si512(z.lo + v);
+  const __m512i cb = _mm512_zextsi256_si512(
+      _mm256_loadu_si256(reinterpret_cast<const __m256i*>(z.codes + (v / 64) * seg_bytes)));
+  const __m512i code = _mm512_and_si512(_mm512_multishift_epi64_epi8(r.shift, _mm512_permutexvar_epi8(r.perm, cb)),
+                                        r.cmask);
+  const __mmask64 em = _mm512_cmpeq_epi8_mask(code, r.cmask);
+  const __m512i ex = _mm512_mask_expandloadu_epi8(_mm512_add_epi8(code, r.base), em, ep);
+  ep += _mm_popcnt_u64(em);
+  // hi byte: sign (bit 7 of L) | exp >> 1 ; lo byte: exp bit 0 -> bit 7 | mantissa (L & 0x7f)
+  const __m512i hi = _mm512_ternarylogic_epi32(r.m80, L, _mm512_srli_epi16(ex, 1), 0xCA);
+  const __m512i lo = _mm512_ternarylogic_epi32(r.m80, _mm512_slli_epi16(ex, 7), L, 0xCA);
+  const __m512i u0 = _mm512_unpacklo_epi8(lo, hi), u1 = _mm512_unpackhi_epi8(lo, hi);
+  _mm512_storeu_si512(seg, _mm512_permutex2var_epi64(u0, r.lo_idx, u1));
+  _mm512_storeu_si512(seg2, _mm512_permutex2var_epi64(u0, r.hi_idx, u1));
+}
+
+// Tiled z-slab: the 1024 values at v (one z block, v % 1024 == 0) are two consecutive
+// 16x32 A tiles in order -> out[1024]. Two sequential streams (lo bytes, codes),
+// prefetched 4 blocks ahead.
+__attribute__((target("avx512f,avx512bw,avx512vl,avx512vbmi,avx512vbmi2")))
+inline void z_run1024(const ZView& z, const ZRegs& r, uint32_t seg_bytes, uint64_t v, uint64_t vend, uint16_t* out) {
+  if (v + 4096 < vend) {
+    const char* pl = reinterpret_cast<const char*>(z.lo + v + 4096);
+    for (int q = 0; q < 16; ++q) _mm_prefetch(pl + 64 * q, _MM_HINT_T0);
+    const char* pc = reinterpret_cast<const char*>(z.codes + (v + 4096) / 64 * seg_bytes);
+    for (uint32_t q = 0; q < seg_bytes / 4; ++q) _mm_prefetch(pc + 64 * q, _MM_HINT_T0);  // 16 x seg_bytes
+  }
+  const uint8_t* ep = z.esc + z.esc_off[v / kZBlock];
+  for (int g = 0; g < 16; ++g) z_decode64(z, r, seg_bytes, v + 64 * g, ep, out + 64 * g, out + 64 * g + 32);
+}
+
+// Two consecutive A tiles (16 rows x 64 cols) of the row-major matrix whose row r starts at
+// value `rowv`, row length `ld` values, columns [k, k+64) -> scratch [2][16][32]. The 16
+// rows are 32 streams (sign/mantissa bytes and codes) — too many for the hardware
+// prefetchers — so every row's lines are prefetched 1 KiB of values ahead. ep[16]: the
+// rows' escape pointers, set at k == 0 and at every block start.
+__attribute__((target("avx512f,avx512bw,avx512vl,avx512vbmi,avx512vbmi2")))
+inline void z_tile2(const ZView& z, const ZRegs& r, uint32_t seg_bytes, uint64_t rowv, uint64_t ld, int k, int kend,
+                    const uint8_t** ep, uint16_t* scratch) {
+  const int kp = k + 512;
   if (kp < kend)
     for (int i = 0; i < 16; ++i) {
       const uint64_t v = rowv + static_cast<uint64_t>(i) * ld + kp;
-      if ((k & 63) == 0) _mm_prefetch(reinterpret_cast<const char*>(z.lo + v), _MM_HINT_T0);
-      if ((k & 127) == 0) _mm_prefetch(reinterpret_cast<const char*>(z.codes + v / 2), _MM_HINT_T0);
+      _mm_prefetch(reinterpret_cast<const char*>(z.lo + v), _MM_HINT_T1);
+      if ((k & 127) == 0) _mm_prefetch(reinterpret_cast<const char*>(z.codes + (v / 64) * seg_bytes), _MM_HINT_T1);
     }
-  for (int i = 0; i < 16; ++i) z_decode32(z, rowv + static_cast<uint64_t>(i) * ld + k, scratch + i * 32);
+  for (int i = 0; i < 16; ++i) {
+    const uint64_t v = rowv + static_cast<uint64_t>(i) * ld + k;
+    if (k == 0)
+      ep[i] = z_esc_ptr(z, v);
+    else if (v % kZBlock == 0)
+      ep[i] = z.esc + z.esc_off[v / kZBlock];
+    z_decode64(z, r, seg_bytes, v, ep[i], scratch + i * 32, scratch + 512 + i * 32);
+  }
 }
 
-__attribute__((target("amx-tile,amx-bf16,avx512f,avx512bw,avx512vl")))
-void amx_gate_up_block_z(const ZView& z, int H, int F, const uint16_t* xb, int r, uint16_t* hb) {
+__attribute__((target("amx-tile,amx-bf16,avx512f,avx512bw,avx512vl,avx512vbmi,avx512vbmi2")))
+void amx_gate_up_block_z(const ZView& z, const ZDec& d, int H, int F, const uint16_t* xb, int r, uint16_t* hb) {
   alignas(64) float cg[16 * 16], cu[16 * 16];
-  alignas(64) uint16_t sg[16 * 32], su[16 * 32];
+  // two scratch sets, alternated per step: the next step's decode stores do not wait for
+  // this step's tile loads (write-after-read on one buffer serialises decode and AMX)
+  alignas(64) uint16_t sgb[2][2 * 16 * 32], sub[2][2 * 16 * 32];
+  const uint8_t* eg[16];
+  const uint8_t* eu[16];
+  const ZRegs R = z_regs(d);
   const uint64_t gv = static_cast<uint64_t>(r) * H, uv = (static_cast<uint64_t>(F) + r) * H;
   _tile_zero(0);
   _tile_zero(1);
-  for (int k = 0; k < H; k += 32) {
-    z_tile(z, gv, H, k, H, sg);
-    z_tile(z, uv, H, k, H, su);
-    _tile_loadd(2, sg, 64);
-    _tile_loadd(3, su, 64);
-    _tile_loadd(4, xb + static_cast<size_t>(k) * kTok, 64);
-    _tile_dpbf16ps(0, 2, 4);
-    _tile_dpbf16ps(1, 3, 4);
+  for (int k = 0; k < H; k += 64) {
+    uint16_t* sg = sgb[(k >> 6) & 1];
+    uint16_t* su = sub[(k >> 6) & 1];
+    if (z.tiled) {  // block rows [r, r+16), tiles k/32 and k/32+1: 1024 contiguous values
+      z_run1024(z, R, d.seg_bytes, gv + static_cast<uint64_t>(k) * 16, gv + 16ull * H, sg);
+      z_run1024(z, R, d.seg_bytes, uv + static_cast<uint64_t>(k) * 16, uv + 16ull * H, su);
+    } else {
+      z_tile2(z, R, d.seg_bytes, gv, H, k, H, eg, sg);
+      z_tile2(z, R, d.seg_bytes, uv, H, k, H, eu, su);
+    }
+    for (int h = 0; h < 2; ++h) {
+      _tile_loadd(2, sg + h * 512, 64);
+      _tile_loadd(3, su + h * 512, 64);
+      _tile_loadd(4, xb + static_cast<size_t>(k + 32 * h) * kTok, 64);
+      _tile_dpbf16ps(0, 2, 4);
+      _tile_dpbf16ps(1, 3, 4);
+    }
   }
   _tile_stored(0, cg, 64);
   _tile_stored(1, cu, 64);
@@ -340,24 +468,30 @@ void amx_gate_up_block_z(const ZView& z, int H, int F, const uint16_t* xb, int r
     }
 }
 
-__attribute__((target("amx-tile,amx-bf16,avx512f,avx512bw,avx512vl")))
-void amx_down_block_z(const ZView& z, const uint16_t* hb, int H, int F, int r, int m, float* y) {
+__attribute__((target("amx-tile,amx-bf16,avx512f,avx512bw,avx512vl,avx512vbmi,avx512vbmi2")))
+void amx_down_block_z(const ZView& z, const ZDec& d, const uint16_t* hb, int H, int F, int r, int m, float* y) {
   alignas(64) float c[16 * 16];
-  alignas(64) uint16_t sd[16 * 32];
+  alignas(64) uint16_t sdb[2][2 * 16 * 32];
+  const uint8_t* ed[16];
+  const ZRegs R = z_regs(d);
   const uint64_t dv = 2ull * F * H + static_cast<uint64_t>(r) * F;
   _tile_zero(0);
-  for (int k = 0; k < F; k += 32) {
-    z_tile(z, dv, F, k, F, sd);
-    _tile_loadd(2, sd, 64);
-    _tile_loadd(4, hb + static_cast<size_t>(k) * kTok, 64);
-    _tile_dpbf16ps(0, 2, 4);
+  for (int k = 0; k < F; k += 64) {
+    uint16_t* sd = sdb[(k >> 6) & 1];
+    if (z.tiled)
+      z_run1024(z, R, d.seg_bytes, dv + static_cast<uint64_t>(k) * 16, dv + 16ull * F, sd);
+    else
+      z_tile2(z, R, d.seg_bytes, dv, F, k, F, ed, sd);
+    for (int h = 0; h < 2; ++h) {
+      _tile_loadd(2, sd + h * 512, 64);
+      _tile_loadd(4, hb + static_cast<size_t>(k + 32 * h) * kTok, 64);
+      _tile_dpbf16ps(0, 2, 4);
+    }
   }
   _tile_stored(0, c, 64);
   for (int t = 0; t < m; ++t)
     for (int i = 0; i < 16; ++i) y[static_cast<size_t>(t) * H + r + i] = c[i * 16 + t];
 }
-
-
 
 template <typename Fn>
 void by_token_chunks(int m, Fn&& fn) {  // fn(template MT, t0)
@@ -411,6 +545,7 @@ ps_status ps_host_lane_destroy(ps_host_lane l) {
 int ps_host_lane_threads(ps_host_lane l) { return l ? l->pool->size() : 0; }
 
 int ps_host_lane_isa(ps_host_lane l) { return l ? (l->amx ? 2 : 1) : 0; }
+int ps_host_lane_reads_z(ps_host_lane l) { return l && l->amx && z_isa_ok() ? 1 : 0; }
 
 ps_status ps_host_lane_bind_caller(ps_host_lane l) {
   return guarded([&] {
@@ -424,9 +559,12 @@ ps_status ps_host_lane_bind_caller(ps_host_lane l) {
 // block of W_down) units; each thread streams a contiguous range of units. One pass pair
 // per layer instead of per expert keeps small experts (Qwen3: 9 MiB) off the pool's
 // wake-up latency.
-ps_status ps_host_expert_ffn_batch(ps_host_lane l, int n, const uint16_t* const* slabs, const int32_t* m,
-                                   const int32_t* row0, int H, int F, const uint16_t* x, float* y) {
+namespace ps {
+namespace {
+ps_status expert_ffn_batch(ps_host_lane l, int n, const uint16_t* const* slabs, const int32_t* m, const int32_t* row0,
+                           int H, int F, const uint16_t* x, float* y, bool tiled) {
   return guarded([&] {
+    if (tiled && !(l && l->amx)) fail(PS_ERUNTIME, "ps_host_expert_ffn_batch_tiled: needs AMX-BF16");
     require(l && n >= 0 && (n == 0 || (slabs && m && row0 && x && y)), "ps_host_expert_ffn_batch: null argument");
     require(H > 0 && F > 0 && H % 32 == 0 && F % 32 == 0, "ps_host_expert_ffn: H and F must be multiples of 32");
     for (int j = 0; j < n; ++j) {
@@ -473,8 +611,9 @@ ps_status ps_host_expert_ffn_batch(ps_host_lane l, int n, const uint16_t* const*
           const uint16_t* wg = slabs[j];
           const uint16_t* wu = wg + static_cast<size_t>(F) * H;
           for (int g = 0; g * kTok < m[j]; ++g)
-            amx_gate_up_block(wg, wu, xb + xo[j] + static_cast<size_t>(g) * H * kTok, H, blk * 16,
-                              hb + ho[j] + static_cast<size_t>(g) * F * kTok);
+            (tiled ? amx_gate_up_block<true> : amx_gate_up_block<false>)(
+                wg, wu, xb + xo[j] + static_cast<size_t>(g) * H * kTok, H, blk * 16,
+                hb + ho[j] + static_cast<size_t>(g) * F * kTok);
         }
         amx_release();
       });
@@ -487,8 +626,9 @@ ps_status ps_host_expert_ffn_batch(ps_host_lane l, int n, const uint16_t* const*
           const int j = static_cast<int>(u / nb2), blk = static_cast<int>(u % nb2);
           const uint16_t* wd = slabs[j] + static_cast<size_t>(2) * F * H;
           for (int g = 0; g * kTok < m[j]; ++g)
-            amx_down_block(wd, hb + ho[j] + static_cast<size_t>(g) * F * kTok, H, F, blk * 16,
-                           std::min(kTok, m[j] - g * kTok), y + static_cast<size_t>(row0[j] + g * kTok) * H);
+            (tiled ? amx_down_block<true> : amx_down_block<false>)(
+                wd, hb + ho[j] + static_cast<size_t>(g) * F * kTok, H, F, blk * 16, std::min(kTok, m[j] - g * kTok),
+                y + static_cast<size_t>(row0[j] + g * kTok) * H);
         }
         amx_release();
       });
@@ -531,21 +671,58 @@ ps_status ps_host_expert_ffn_batch(ps_host_lane l, int n, const uint16_t* const*
     });
   });
 }
+}  // namespace
+}  // namespace ps
+
+ps_status ps_host_expert_ffn_batch(ps_host_lane l, int n, const uint16_t* const* slabs, const int32_t* m,
+                                   const int32_t* row0, int H, int F, const uint16_t* x, float* y) {
+  return ps::expert_ffn_batch(l, n, slabs, m, row0, H, F, x, y, false);
+}
+
+ps_status ps_host_expert_ffn_batch_tiled(ps_host_lane l, int n, const uint16_t* const* slabs, const int32_t* m,
+                                         const int32_t* row0, int H, int F, const uint16_t* x, float* y) {
+  return ps::expert_ffn_batch(l, n, slabs, m, row0, H, F, x, y, true);
+}
+
+ps_status ps_host_slab_untile(uint16_t* slab, int H, int F) {
+  return guarded([&] {
+    require(slab && H > 0 && F > 0 && H % 32 == 0 && F % 32 == 0, "ps_host_slab_untile: bad argument");
+    std::vector<uint16_t> tmp;
+    untile_matrix_inplace(slab, F, H, tmp);
+    untile_matrix_inplace(slab + static_cast<size_t>(F) * H, F, H, tmp);
+    untile_matrix_inplace(slab + static_cast<size_t>(2) * F * H, H, F, tmp);
+  });
+}
+
+ps_status ps_host_slab_tile(uint16_t* slab, int H, int F) {
+  return guarded([&] {
+    require(slab && H > 0 && F > 0 && H % 32 == 0 && F % 32 == 0, "ps_host_slab_tile: bad argument");
+    std::vector<uint16_t> tmp;
+    tile_matrix_inplace(slab, F, H, tmp);                                      // W_gate [F][H]
+    tile_matrix_inplace(slab + static_cast<size_t>(F) * H, F, H, tmp);         // W_up   [F][H]
+    tile_matrix_inplace(slab + static_cast<size_t>(2) * F * H, H, F, tmp);     // W_down [H][F]
+  });
+}
 
 // Same as ps_host_expert_ffn_batch, weights read from z-slabs (AMX path only).
 ps_status ps_host_expert_ffn_batch_z(ps_host_lane l, int n, const uint8_t* const* zslabs, const int32_t* m,
                                      const int32_t* row0, int H, int F, const uint16_t* x, float* y) {
   return guarded([&] {
     require(l && n >= 0 && (n == 0 || (zslabs && m && row0 && x && y)), "ps_host_expert_ffn_batch_z: null argument");
-    require(H > 0 && F > 0 && H % 32 == 0 && F % 32 == 0, "ps_host_expert_ffn_batch_z: H, F % 32 == 0");
-    if (!l->amx) fail(PS_ERUNTIME, "ps_host_expert_ffn_batch_z: needs AMX-BF16 (use the raw slabs)");
+    require(H > 0 && F > 0 && H % 64 == 0 && F % 64 == 0, "ps_host_expert_ffn_batch_z: H, F % 64 == 0");
+    if (!l->amx || !z_isa_ok())
+      fail(PS_ERUNTIME, "ps_host_expert_ffn_batch_z: needs AMX-BF16 and AVX-512 VBMI2 (use the raw slabs)");
     std::vector<ZView> zv;
+    std::vector<ZDec> zd;
     for (int j = 0; j < n; ++j) {
       require(zslabs[j] != nullptr && m[j] >= 0 && m[j] <= 4096 && row0[j] >= 0, "ps_host_expert_ffn_batch_z: bad job");
       const ZHeader* h = reinterpret_cast<const ZHeader*>(zslabs[j]);
       require(h->magic == kZMagic && h->n == 3ull * H * F, "ps_host_expert_ffn_batch_z: not a z-slab of this shape");
-      require(h->code_bits == 4, "ps_host_expert_ffn_batch_z: the lane decodes 4-bit z-slabs only");
+      require(h->code_bits == 3 || h->code_bits == 4, "ps_host_expert_ffn_batch_z: bad code width");
+      require(!h->tiled || (h->tile_h == static_cast<uint32_t>(H) && h->tile_f == static_cast<uint32_t>(F)),
+              "ps_host_expert_ffn_batch_z: tiled z-slab of another shape");
       zv.emplace_back(zslabs[j]);
+      zd.push_back(z_dec(zv.back()));
     }
     const int T = l->pool->size();
     const int nb1 = F / 16, nb2 = H / 16;
@@ -577,7 +754,7 @@ ps_status ps_host_expert_ffn_batch_z(ps_host_lane l, int n, const uint8_t* const
       for (int64_t u = u0; u < u1; ++u) {
         const int j = static_cast<int>(u / nb1), blk = static_cast<int>(u % nb1);
         for (int g = 0; g * kTok < m[j]; ++g)
-          amx_gate_up_block_z(zv[j], H, F, xb + xo[j] + static_cast<size_t>(g) * H * kTok, blk * 16,
+          amx_gate_up_block_z(zv[j], zd[j], H, F, xb + xo[j] + static_cast<size_t>(g) * H * kTok, blk * 16,
                               hb + ho[j] + static_cast<size_t>(g) * F * kTok);
       }
       amx_release();
@@ -589,7 +766,7 @@ ps_status ps_host_expert_ffn_batch_z(ps_host_lane l, int n, const uint8_t* const
       for (int64_t u = u0; u < u1; ++u) {
         const int j = static_cast<int>(u / nb2), blk = static_cast<int>(u % nb2);
         for (int g = 0; g * kTok < m[j]; ++g)
-          amx_down_block_z(zv[j], hb + ho[j] + static_cast<size_t>(g) * F * kTok, H, F, blk * 16,
+          amx_down_block_z(zv[j], zd[j], hb + ho[j] + static_cast<size_t>(g) * F * kTok, H, F, blk * 16,
                            std::min(kTok, m[j] - g * kTok), y + static_cast<size_t>(row0[j] + g * kTok) * H);
       }
       amx_release();

@@ -65,7 +65,8 @@ constexpr int kZEscStage = 256;  // staged escapes per block (more: read from gl
 
 template <int BITS>
 __global__ void __launch_bounds__(256, 4)
-z_decode_kernel(const uint8_t* __restrict__ z, uint64_t n, uint32_t base, uint32_t nb, uint16_t* __restrict__ out) {
+z_decode_kernel(const uint8_t* __restrict__ z, uint64_t n, uint32_t base, uint32_t nb, uint32_t tile_h,
+                uint32_t tile_f, uint16_t* __restrict__ out) {
   constexpr uint32_t kEsc = (1u << BITS) - 1u;
   __shared__ uint8_t s_esc[8][kZEscStage];
   const uint64_t n_pad = static_cast<uint64_t>(nb) * kZBlock;
@@ -99,6 +100,9 @@ z_decode_kernel(const uint8_t* __restrict__ z, uint64_t n, uint32_t base, uint32
     uint32_t e_at = eoff + static_cast<uint32_t>(incl - n_e);
     const uint32_t lw[8] = {l0.x, l0.y, l0.z, l0.w, l1.x, l1.y, l1.z, l1.w};
     const bool full = v0 + 32 <= n;
+    // tiled slabs (n = 3HF, a multiple of 1024, so always full): a lane's segment is one
+    // 32-value tile row, 64 contiguous bytes of the row-major output
+    uint16_t* dst = tile_h ? out + z_untile(v0, tile_h, tile_f) : out + v0;
 #pragma unroll
     for (int q = 0; q < 4; ++q) {  // 8 values -> one 16-byte store
       uint32_t pk[4];
@@ -118,7 +122,7 @@ z_decode_kernel(const uint8_t* __restrict__ z, uint64_t n, uint32_t base, uint32
         else pk[j >> 1] = v;
       }
       if (full) {
-        reinterpret_cast<uint4*>(out + v0)[q] = make_uint4(pk[0], pk[1], pk[2], pk[3]);
+        reinterpret_cast<uint4*>(dst)[q] = make_uint4(pk[0], pk[1], pk[2], pk[3]);
       } else {
         for (int j = 0; j < 8 && v0 + 8 * q + j < n; ++j)
           out[v0 + 8 * q + j] = static_cast<uint16_t>(pk[j >> 1] >> (16 * (j & 1)));
@@ -302,6 +306,27 @@ ps_status ps_zslab_info(const uint8_t* z_host, uint64_t* n, uint64_t* bytes, uin
   });
 }
 
+// z-slab of an expert slab in the host lane's tile layout (ps_host_slab_tile): the same
+// encoding of the tiled values, header marked so ps_zslab_decode emits row-major order and
+// the lane's z path reads tiles as sequential streams.
+ps_status ps_zslab_encode_tiled(const uint16_t* slab_tiled, int H, int F, uint8_t* out, uint64_t cap,
+                                uint64_t* out_bytes, int threads) {
+  const uint64_t n = 3ull * static_cast<uint64_t>(H) * static_cast<uint64_t>(F);
+  if (!(H > 0 && F > 0 && H % 32 == 0 && F % 32 == 0)) {
+    set_last_error("ps_zslab_encode_tiled: H, F must be positive multiples of 32");
+    return PS_EINVAL;
+  }
+  const ps_status st = ps_zslab_encode(slab_tiled, n, out, cap, out_bytes, threads);
+  if (st != PS_OK) return st;
+  ZHeader h;
+  std::memcpy(&h, out, sizeof(h));
+  h.tiled = 1;
+  h.tile_h = static_cast<uint32_t>(H);
+  h.tile_f = static_cast<uint32_t>(F);
+  std::memcpy(out, &h, sizeof(h));
+  return PS_OK;
+}
+
 // Device decode: z (device copy of the z-slab) -> out [n] bf16. The header fields are
 // passed from the host (the caller keeps the host z-slab), so no device read-back.
 ps_status ps_zslab_decode(const uint8_t* z_dev, const uint8_t* z_host_header, uint16_t* out, void* stream) {
@@ -314,10 +339,13 @@ ps_status ps_zslab_decode(const uint8_t* z_dev, const uint8_t* z_host_header, ui
     const int grid = static_cast<int>(std::min<uint64_t>((static_cast<uint64_t>(h.nb) * 32 + threads - 1) / threads,
                                                          4 * 148));
     require(h.code_bits == 3 || h.code_bits == 4, "ps_zslab_decode: bad code width");
+    const uint32_t th = h.tiled ? h.tile_h : 0, tf = h.tiled ? h.tile_f : 0;
+    require(!h.tiled || (th % 32 == 0 && tf % 32 == 0 && th && tf && h.n == 3ull * th * tf),
+            "ps_zslab_decode: bad tiled header");
     if (h.code_bits == 3)
-      z_decode_kernel<3><<<grid, threads, 0, as_stream(stream)>>>(z_dev, h.n, h.base, h.nb, out);
+      z_decode_kernel<3><<<grid, threads, 0, as_stream(stream)>>>(z_dev, h.n, h.base, h.nb, th, tf, out);
     else
-      z_decode_kernel<4><<<grid, threads, 0, as_stream(stream)>>>(z_dev, h.n, h.base, h.nb, out);
+      z_decode_kernel<4><<<grid, threads, 0, as_stream(stream)>>>(z_dev, h.n, h.base, h.nb, th, tf, out);
     PS_LAUNCH_CHECK("z_decode_kernel");
   });
 }

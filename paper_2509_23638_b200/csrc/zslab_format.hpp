@@ -24,8 +24,9 @@ struct ZHeader {  // at the start of every z-slab (64 bytes, keeps the streams 1
   uint64_t n_esc;  // escaped values
   uint64_t bytes;  // total z-slab bytes
   uint32_t code_bits;  // 3 or 4: exponent code width (escape = all ones)
-  uint32_t pad0;
-  uint64_t pad[2];
+  uint32_t tiled;      // 1: the values are an expert slab in the host lane's tile layout
+  uint32_t tile_h, tile_f;  // H, F of that slab (tiled == 1); decoders emit row-major
+  uint64_t pad;
 };
 static_assert(sizeof(ZHeader) == 64, "z header");
 constexpr uint64_t kZMagic = 0x31424c534c5a5350ull;  // "PSZSLAB1"
@@ -44,9 +45,10 @@ struct ZView {
   const uint8_t* codes;
   const uint32_t* esc_off;
   const uint8_t* esc;
-  uint32_t base, bits;
+  uint32_t base, bits, tiled;
   explicit ZView(const uint8_t* z) {
     const ZHeader* h = reinterpret_cast<const ZHeader*>(z);
+    tiled = h->tiled;
     const uint64_t n_pad = static_cast<uint64_t>(h->nb) * kZBlock;
     bits = h->code_bits;
     lo = z + z_lo_off();
@@ -56,5 +58,18 @@ struct ZView {
     base = h->base;
   }
 };
+
+// Lane tile layout (ps_host_slab_tile): W_gate [F][H], W_up [F][H], W_down [H][F], each
+// 16-row block stored as consecutive 16x32 tiles (1 KiB, row-major inside). Row-major index
+// of the 32-value tile row that starts at tiled index v (v % 32 == 0).
+PS_HD inline uint64_t z_untile(uint64_t v, uint32_t H, uint32_t F) {
+  const uint64_t fh = static_cast<uint64_t>(F) * H;
+  const uint64_t base = v < fh ? 0 : (v < 2 * fh ? fh : 2 * fh);
+  const uint32_t K = v < 2 * fh ? H : F;
+  const uint64_t t = v - base, tile = t >> 9;
+  const uint32_t i = static_cast<uint32_t>(t >> 5) & 15u, nkb = K / 32;
+  const uint64_t rb = tile / nkb, kb = tile - rb * nkb;
+  return base + (rb * 16 + i) * K + kb * 32;
+}
 
 }  // namespace ps

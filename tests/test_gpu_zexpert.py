@@ -61,6 +61,36 @@ def test_zslab_roundtrip_bit_exact(torch_cuda, case, zbits):
     np.testing.assert_array_equal(out.cpu().numpy().view(np.uint16), slab)
 
 
+@pytest.mark.parametrize("escapes", [False, True])
+def test_tiled_zslab_decodes_to_row_major(torch_cuda, zbits, escapes):
+    """A z-slab of a slab in the lane's tile layout (ps_host_slab_tile +
+    ps_zslab_encode_tiled) decodes on the GPU to the ORIGINAL row-major slab, bit for bit."""
+    torch = torch_cuda
+    lib = ps.load()
+    H, F = 256, 384
+    slab = np.empty(3 * H * F, np.uint16)
+    ps.check(lib.ps_init_expert_slab_host(slab.ctypes.data, H, F, 5, 2, 1))
+    if escapes:
+        rng = np.random.default_rng(2)
+        idx = rng.choice(slab.size, 20000, replace=False)
+        slab[idx] = rng.integers(0, 65536, idx.size, dtype=np.uint16)
+    tiled = slab.copy()
+    ps.check(lib.ps_host_slab_tile(tiled.ctypes.data, H, F))
+    back = tiled.copy()
+    ps.check(lib.ps_host_slab_untile(back.ctypes.data, H, F))
+    np.testing.assert_array_equal(back, slab)
+    cap = lib.ps_zslab_bound(slab.size)
+    z = np.zeros(cap, np.uint8)
+    nb = C.c_uint64()
+    ps.check(lib.ps_zslab_encode_tiled(tiled.ctypes.data, H, F, z.ctypes.data, cap, C.byref(nb), 2))
+    zd = torch.as_tensor(z[:nb.value].copy(), device="cuda")
+    out = torch.zeros(slab.size, dtype=torch.int16, device="cuda")
+    ps.check(lib.ps_zslab_decode(C.c_void_p(zd.data_ptr()), z.ctypes.data, C.c_void_p(out.data_ptr()),
+                                 C.c_void_p(torch.cuda.current_stream().cuda_stream)))
+    torch.cuda.synchronize()
+    np.testing.assert_array_equal(out.cpu().numpy().view(np.uint16), slab)
+
+
 @pytest.mark.parametrize("host_threads", [0, 2])  # 2: host lane + z-slabs in one engine
 def test_engine_zslab_loads_bitwise_equal(torch_cuda, host_threads):
     spec = ps.desk_scale("mixtral", 4, 8, 256)

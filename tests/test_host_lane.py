@@ -134,12 +134,14 @@ def test_host_expert_ffn_batch_equals_single_calls(isa):
 
 
 @needs_bf16
-@pytest.mark.skipif(not _has("amx_bf16"), reason="z-slab lane path needs AMX-BF16")
-@pytest.mark.parametrize("escapes", [False, True])
-def test_host_lane_reads_zslabs_bitwise(escapes, monkeypatch):
-    monkeypatch.setenv("PS_ZSLAB_BITS", "4")  # the lane's z path decodes the 4-bit format
-    """The lane's z-slab path (12-bit transfer format decoded per tile) gives bitwise the
-    raw-slab results, escapes included."""
+@pytest.mark.skipif(not (_has("amx_bf16") and _has("avx512_vbmi2")), reason="z-slab lane path needs AMX-BF16 + VBMI2")
+@pytest.mark.parametrize("bits", [3, 4])
+@pytest.mark.parametrize("escapes", [0, 3000, 90000])
+def test_host_lane_reads_zslabs_bitwise(bits, escapes, monkeypatch):
+    """The lane's z-slab path (3- or 4-bit exponent codes decoded per tile, rows starting
+    mid-block) gives bitwise the raw-slab results, escapes included (up to ~30 % of the
+    values, so segments with many escapes and blocks with long escape lists)."""
+    monkeypatch.setenv("PS_ZSLAB_BITS", str(bits))
     lib = ps.load()
     H, F = 256, 384
     ms, row0 = [3, 17, 1], [0, 3, 20]
@@ -148,7 +150,7 @@ def test_host_lane_reads_zslabs_bitwise(escapes, monkeypatch):
     for e in range(3):
         s = orc.or_init_slab(H, F, 2, 1, e)
         if escapes:
-            idx = rng.choice(s.size, 3000, replace=False)
+            idx = rng.choice(s.size, escapes, replace=False)
             s[idx] = (rng.integers(0, 2, idx.size) << 15 | rng.integers(1, 200, idx.size) << 7 |
                       rng.integers(0, 128, idx.size)).astype(np.uint16)  # finite, wide exponents
         slabs.append(s)
@@ -156,6 +158,7 @@ def test_host_lane_reads_zslabs_bitwise(escapes, monkeypatch):
         z = np.zeros(cap, np.uint8)
         nb = C.c_uint64()
         ps.check(lib.ps_zslab_encode(s.ctypes.data, s.size, z.ctypes.data, cap, C.byref(nb), 2))
+        assert z[40:44].view(np.uint32)[0] == bits  # ZHeader.code_bits
         zs.append(z)
     x = orc.f32_to_bf16(rng.standard_normal((21, H)).astype(np.float32))
     lane = _lane(3, "amx")
@@ -163,6 +166,80 @@ def test_host_lane_reads_zslabs_bitwise(escapes, monkeypatch):
         m_a, r_a = np.array(ms, np.int32), np.array(row0, np.int32)
         y_raw = np.full((21, H), np.nan, np.float32)
         y_z = np.full((21, H), np.nan, np.float32)
+        ps.check(lib.ps_host_expert_ffn_batch(lane, 3, (C.c_void_p * 3)(*[s.ctypes.data for s in slabs]),
+                                              m_a.ctypes.data, r_a.ctypes.data, H, F, x.ctypes.data, y_raw.ctypes.data))
+        ps.check(lib.ps_host_expert_ffn_batch_z(lane, 3, (C.c_void_p * 3)(*[z.ctypes.data for z in zs]),
+                                                m_a.ctypes.data, r_a.ctypes.data, H, F, x.ctypes.data, y_z.ctypes.data))
+        np.testing.assert_array_equal(y_raw, y_z)
+    finally:
+        lib.ps_host_lane_destroy(lane)
+
+
+@needs_bf16
+@pytest.mark.skipif(not _has("amx_bf16"), reason="tile layout path needs AMX-BF16")
+def test_host_lane_tile_layout_bitwise():
+    """ps_host_slab_tile + ps_host_expert_ffn_batch_tiled give bitwise the row-major
+    batch results (same tile ops in the same order), token groups of 1..17 included."""
+    lib = ps.load()
+    H, F = 256, 384
+    ms, row0 = [1, 17, 0, 5], [0, 1, 18, 18]
+    slabs = [orc.or_init_slab(H, F, 3, 2, e) for e in range(4)]
+    tiled = [s.copy() for s in slabs]
+    for t in tiled:
+        ps.check(lib.ps_host_slab_tile(t.ctypes.data, H, F))
+    assert not np.array_equal(tiled[0], slabs[0])  # the layout did change
+    rng = np.random.default_rng(3)
+    x = orc.f32_to_bf16(rng.standard_normal((23, H)).astype(np.float32))
+    lane = _lane(3, "amx")
+    try:
+        m_a, r_a = np.array(ms, np.int32), np.array(row0, np.int32)
+        y_raw = np.full((23, H), np.nan, np.float32)
+        y_t = np.full((23, H), np.nan, np.float32)
+        ps.check(lib.ps_host_expert_ffn_batch(lane, 4, (C.c_void_p * 4)(*[s.ctypes.data for s in slabs]),
+                                              m_a.ctypes.data, r_a.ctypes.data, H, F, x.ctypes.data, y_raw.ctypes.data))
+        ps.check(lib.ps_host_expert_ffn_batch_tiled(lane, 4, (C.c_void_p * 4)(*[s.ctypes.data for s in tiled]),
+                                                    m_a.ctypes.data, r_a.ctypes.data, H, F, x.ctypes.data,
+                                                    y_t.ctypes.data))
+        np.testing.assert_array_equal(y_raw, y_t)
+    finally:
+        lib.ps_host_lane_destroy(lane)
+
+
+@needs_bf16
+@pytest.mark.skipif(not (_has("amx_bf16") and _has("avx512_vbmi2")), reason="z-slab lane path needs AMX-BF16 + VBMI2")
+@pytest.mark.parametrize("bits", [3, 4])
+def test_host_lane_reads_tiled_zslabs_bitwise(bits, monkeypatch):
+    """z-slabs of tile-layout slabs (ps_zslab_encode_tiled): the lane's sequential z path
+    gives bitwise the row-major raw results; the slab round-trips through untile."""
+    monkeypatch.setenv("PS_ZSLAB_BITS", str(bits))
+    lib = ps.load()
+    H, F = 256, 384
+    ms, row0 = [2, 16, 1], [0, 2, 18]
+    rng = np.random.default_rng(5)
+    slabs, zs = [], []
+    for e in range(3):
+        s = orc.or_init_slab(H, F, 4, 0, e)
+        idx = rng.choice(s.size, 20000, replace=False)
+        s[idx] = (rng.integers(0, 2, idx.size) << 15 | rng.integers(1, 255, idx.size) << 7 |
+                  rng.integers(0, 128, idx.size)).astype(np.uint16)
+        slabs.append(s)
+        t = s.copy()
+        ps.check(lib.ps_host_slab_tile(t.ctypes.data, H, F))
+        back = t.copy()
+        ps.check(lib.ps_host_slab_untile(back.ctypes.data, H, F))
+        np.testing.assert_array_equal(back, s)
+        cap = lib.ps_zslab_bound(s.size)
+        z = np.zeros(cap, np.uint8)
+        nb = C.c_uint64()
+        ps.check(lib.ps_zslab_encode_tiled(t.ctypes.data, H, F, z.ctypes.data, cap, C.byref(nb), 2))
+        assert z[40:44].view(np.uint32)[0] == bits and z[44:48].view(np.uint32)[0] == 1
+        zs.append(z)
+    x = orc.f32_to_bf16(rng.standard_normal((19, H)).astype(np.float32))
+    lane = _lane(3, "amx")
+    try:
+        m_a, r_a = np.array(ms, np.int32), np.array(row0, np.int32)
+        y_raw = np.full((19, H), np.nan, np.float32)
+        y_z = np.full((19, H), np.nan, np.float32)
         ps.check(lib.ps_host_expert_ffn_batch(lane, 3, (C.c_void_p * 3)(*[s.ctypes.data for s in slabs]),
                                               m_a.ctypes.data, r_a.ctypes.data, H, F, x.ctypes.data, y_raw.ctypes.data))
         ps.check(lib.ps_host_expert_ffn_batch_z(lane, 3, (C.c_void_p * 3)(*[z.ctypes.data for z in zs]),
