@@ -312,6 +312,10 @@ ps_status ps_combine(const float* y_part, int n_split, const int32_t* inv, const
 
 /* x [n] f32 -> bf16 (round to nearest even), the FFN input cast K1 otherwise fuses. */
 ps_status ps_cast_bf16(const float* x, int64_t n, uint16_t* out, void* stream);
+/* dst[0, n) = host_src[0, n) read by the SMs from mapped pinned host memory (no copy
+ * engine), and dst[z*zero_stride, +n) = 0 for z = 1..zero_copies. n, zero_stride % 4 == 0. */
+ps_status ps_rows_from_host(const float* host_src, int64_t n, float* dst, int zero_copies, int64_t zero_stride,
+                            void* stream);
 
 /* Shared experts (BASELINE config 3, DeepSeek-V2-Lite: 2 always-active experts with gate
  * weight 1; a north_star extension — the reference's ModelSpec has none): appends

@@ -1145,10 +1145,14 @@ void decode_step(ps_engine_s& e, const float* hidden, const uint8_t* follow, int
       }
       for (CpuJob& j : e.cpu_jobs) {
         const size_t bytes = sizeof(float) * static_cast<size_t>(j.m) * H;
-        PS_CUDA(cudaMemcpyAsync(e.y_part + static_cast<size_t>(j.row0) * H, e.lane_yrows + static_cast<size_t>(j.row0) * H,
-                                bytes, cudaMemcpyHostToDevice, e.sc));
-        for (int sp = 1; sp < e.step_split; ++sp)
-          PS_CUDA(cudaMemsetAsync(e.y_part + (sp * total_rows + j.row0) * H, 0, bytes, e.sc));
+        (void)bytes;
+        // SM-driven read of the mapped pinned rows: a copy-engine H2D here would queue
+        // behind an in-flight expert load on the same engine (up to ~4.5 ms)
+        const ps_status cs = ps_rows_from_host(e.lane_yrows + static_cast<size_t>(j.row0) * H,
+                                               static_cast<int64_t>(j.m) * H, e.y_part + static_cast<size_t>(j.row0) * H,
+                                               e.step_split - 1, static_cast<int64_t>(total_rows) * H, e.sc);
+        if (cs != PS_OK) fail(cs, ps_last_error());
+        e.st.kernel_launches += 1;
         e.st.cpu_experts += 1;
         e.st.cpu_bytes_total += static_cast<double>(e.cfg.spec.expert_bytes);
         j.t0_us -= host_t0_us;
@@ -1575,7 +1579,7 @@ void create_engine(const ps_engine_config& cfg, ps_engine_s& e) {
     if (ps_host_lane_create(cfg.host_threads, &e.lane) != PS_OK) fail(PS_ERUNTIME, ps_last_error());
     PS_CUDA(cudaHostAlloc(&e.lane_x, sizeof(uint16_t) * B * e.H, cudaHostAllocDefault));
     PS_CUDA(cudaHostAlloc(&e.lane_xrows, sizeof(uint16_t) * rows_t * e.H, cudaHostAllocDefault));
-    PS_CUDA(cudaHostAlloc(&e.lane_yrows, sizeof(float) * rows_t * e.H, cudaHostAllocDefault));
+    PS_CUDA(cudaHostAlloc(&e.lane_yrows, sizeof(float) * rows_t * e.H, cudaHostAllocMapped));
     e.lane_drv = std::make_unique<LaneDriver>(e.lane, e.H, e.F);
     e.lane_drv->tiled = e.host_tiled;
     // cpu_cost = beta*m + C (cost_model.cpp:34-37) measured on this host: the lane on a

@@ -89,6 +89,19 @@ __global__ void cast_bf16_kernel(const float* __restrict__ x, int64_t n, uint16_
     out[i] = f32_to_bf16_rne(x[i]);
 }
 
+// SM-driven copy of f32 rows from mapped pinned host memory (zero-copy over PCIe) into
+// device memory, with `zero_copies` further zero-filled copies at a stride: the host
+// lane's outputs reach y_part without a copy-engine transfer, which would queue behind
+// the serial channel's multi-ms expert loads on the same copy engine.
+__global__ void rows_from_host_kernel(const float4* __restrict__ src, int64_t n4, float4* __restrict__ dst,
+                                      int zero_copies, int64_t zero_stride4) {
+  for (int64_t i = blockIdx.x * static_cast<int64_t>(blockDim.x) + threadIdx.x; i < n4;
+       i += static_cast<int64_t>(gridDim.x) * blockDim.x) {
+    dst[i] = src[i];
+    for (int z = 1; z <= zero_copies; ++z) dst[i + z * zero_stride4] = make_float4(0.f, 0.f, 0.f, 0.f);
+  }
+}
+
 // Shared experts (DeepSeek-style, always active, gate weight 1): appended as virtual
 // experts E..E+S-1 so permute / FFN / combine treat them like routed ones.
 __global__ void append_shared_kernel(const int32_t* __restrict__ ids, const float* __restrict__ w, int B, int k,
@@ -127,6 +140,25 @@ ps_status ps_cast_bf16(const float* x, int64_t n, uint16_t* out, void* stream) {
     const int grid = static_cast<int>(std::min<int64_t>((n + 255) / 256, 4 * 148));
     cast_bf16_kernel<<<grid, 256, 0, as_stream(stream)>>>(x, n, out);
     PS_LAUNCH_CHECK("cast_bf16_kernel");
+  });
+}
+
+ps_status ps_rows_from_host(const float* host_src, int64_t n, float* dst, int zero_copies, int64_t zero_stride,
+                            void* stream) {
+  return guarded([&] {
+    require(n >= 0 && zero_copies >= 0 && n % 4 == 0 && zero_stride % 4 == 0 && (n == 0 || (host_src && dst)),
+            "ps_rows_from_host: bad arguments");
+    if (n == 0) return;
+    void* dev_src = nullptr;
+    PS_CUDA(cudaHostGetDevicePointer(&dev_src, const_cast<float*>(host_src), 0));
+    require((reinterpret_cast<uintptr_t>(dev_src) | reinterpret_cast<uintptr_t>(dst)) % 16 == 0,
+            "ps_rows_from_host: 16-byte alignment");
+    const int64_t n4 = n / 4;
+    const int grid = static_cast<int>(std::max<int64_t>(1, std::min<int64_t>((n4 + 255) / 256, 148)));
+    rows_from_host_kernel<<<grid, 256, 0, as_stream(stream)>>>(static_cast<const float4*>(dev_src), n4,
+                                                               reinterpret_cast<float4*>(dst), zero_copies,
+                                                               zero_stride / 4);
+    PS_LAUNCH_CHECK("rows_from_host_kernel");
   });
 }
 
