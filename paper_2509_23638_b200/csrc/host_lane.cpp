@@ -509,6 +509,22 @@ void by_token_chunks(int m, Fn&& fn) {  // fn(template MT, t0)
   }
 }
 
+// Dynamic chunks of (expert, 16-row block) units: a pool pass ends at its slowest
+// thread, and DRAM contention makes equal static ranges finish unevenly; chunks of
+// ~U/(8T) units (MiBs of contiguous weights) keep the streams long and balance the
+// tail. Units write disjoint outputs, so results do not depend on the assignment.
+template <typename Fn>
+void for_units(int64_t U, int T, std::atomic<int64_t>& next, Fn&& fn) {
+  static const bool coarse = [] {  // PS_HOST_LANE_CHUNKS=1: one chunk per thread (A/B runs)
+    const char* v = std::getenv("PS_HOST_LANE_CHUNKS");
+    return v && v[0] == '1';
+  }();
+  const int64_t per = coarse ? T : 8 * static_cast<int64_t>(T);
+  const int64_t C = std::max<int64_t>(1, (U + per - 1) / per);
+  for (int64_t c; (c = next.fetch_add(1, std::memory_order_relaxed)) * C < U;)
+    for (int64_t u = c * C, e = std::min(U, (c + 1) * C); u < e; ++u) fn(u);
+}
+
 }  // namespace
 }  // namespace ps
 
@@ -601,12 +617,10 @@ ps_status expert_ffn_batch(ps_host_lane l, int n, const uint16_t* const* slabs, 
             d[static_cast<size_t>(k >> 1) * kTok * 2 + 1] = xr[k + 1];
           }
         }
-      l->pool->run([&](int tid) {
-        int64_t u0, u1;
-        range(U1, tid, u0, u1);
-        if (u0 == u1) return;
+      std::atomic<int64_t> next1{0}, next2{0};
+      l->pool->run([&](int) {
         amx_config();
-        for (int64_t u = u0; u < u1; ++u) {
+        for_units(U1, T, next1, [&](int64_t u) {
           const int j = static_cast<int>(u / nb1), blk = static_cast<int>(u % nb1);
           const uint16_t* wg = slabs[j];
           const uint16_t* wu = wg + static_cast<size_t>(F) * H;
@@ -614,22 +628,19 @@ ps_status expert_ffn_batch(ps_host_lane l, int n, const uint16_t* const* slabs, 
             (tiled ? amx_gate_up_block<true> : amx_gate_up_block<false>)(
                 wg, wu, xb + xo[j] + static_cast<size_t>(g) * H * kTok, H, blk * 16,
                 hb + ho[j] + static_cast<size_t>(g) * F * kTok);
-        }
+        });
         amx_release();
       });
-      l->pool->run([&](int tid) {
-        int64_t u0, u1;
-        range(U2, tid, u0, u1);
-        if (u0 == u1) return;
+      l->pool->run([&](int) {
         amx_config();
-        for (int64_t u = u0; u < u1; ++u) {
+        for_units(U2, T, next2, [&](int64_t u) {
           const int j = static_cast<int>(u / nb2), blk = static_cast<int>(u % nb2);
           const uint16_t* wd = slabs[j] + static_cast<size_t>(2) * F * H;
           for (int g = 0; g * kTok < m[j]; ++g)
             (tiled ? amx_down_block<true> : amx_down_block<false>)(
                 wd, hb + ho[j] + static_cast<size_t>(g) * F * kTok, H, F, blk * 16, std::min(kTok, m[j] - g * kTok),
                 y + static_cast<size_t>(row0[j] + g * kTok) * H);
-        }
+        });
         amx_release();
       });
       return;
@@ -747,28 +758,25 @@ ps_status ps_host_expert_ffn_batch_z(ps_host_lane l, int n, const uint8_t* const
           d[static_cast<size_t>(k >> 1) * kTok * 2 + 1] = xr[k + 1];
         }
       }
-    l->pool->run([&](int tid) {
-      const int64_t u0 = U1 * tid / T, u1 = U1 * (tid + 1) / T;
-      if (u0 == u1) return;
+    std::atomic<int64_t> next1{0}, next2{0};
+    l->pool->run([&](int) {
       amx_config();
-      for (int64_t u = u0; u < u1; ++u) {
+      for_units(U1, T, next1, [&](int64_t u) {
         const int j = static_cast<int>(u / nb1), blk = static_cast<int>(u % nb1);
         for (int g = 0; g * kTok < m[j]; ++g)
           amx_gate_up_block_z(zv[j], zd[j], H, F, xb + xo[j] + static_cast<size_t>(g) * H * kTok, blk * 16,
                               hb + ho[j] + static_cast<size_t>(g) * F * kTok);
-      }
+      });
       amx_release();
     });
-    l->pool->run([&](int tid) {
-      const int64_t u0 = U2 * tid / T, u1 = U2 * (tid + 1) / T;
-      if (u0 == u1) return;
+    l->pool->run([&](int) {
       amx_config();
-      for (int64_t u = u0; u < u1; ++u) {
+      for_units(U2, T, next2, [&](int64_t u) {
         const int j = static_cast<int>(u / nb2), blk = static_cast<int>(u % nb2);
         for (int g = 0; g * kTok < m[j]; ++g)
           amx_down_block_z(zv[j], zd[j], hb + ho[j] + static_cast<size_t>(g) * F * kTok, H, F, blk * 16,
                            std::min(kTok, m[j] - g * kTok), y + static_cast<size_t>(row0[j] + g * kTok) * H);
-      }
+      });
       amx_release();
     });
   });
