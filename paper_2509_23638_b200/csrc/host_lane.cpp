@@ -509,20 +509,26 @@ void by_token_chunks(int m, Fn&& fn) {  // fn(template MT, t0)
   }
 }
 
-// Dynamic chunks of (expert, 16-row block) units: a pool pass ends at its slowest
-// thread, and DRAM contention makes equal static ranges finish unevenly; chunks of
-// ~U/(8T) units (MiBs of contiguous weights) keep the streams long and balance the
-// tail. Units write disjoint outputs, so results do not depend on the assignment.
+// Guided self-scheduling of (expert, 16-row block) units: a pool pass ends at its
+// slowest thread, and DRAM contention makes equal static ranges finish unevenly. Each
+// grab takes remaining/(2T) units (>= 2): long contiguous weight streams early, single
+// ~25 us units at the end, so the pass tail is about one unit. Units write disjoint
+// outputs, so results do not depend on the assignment.
 template <typename Fn>
 void for_units(int64_t U, int T, std::atomic<int64_t>& next, Fn&& fn) {
-  static const bool coarse = [] {  // PS_HOST_LANE_CHUNKS=1: one chunk per thread (A/B runs)
+  // A/B runs: PS_HOST_LANE_CHUNKS=1 one chunk per thread, =2 fixed chunks of U/(8T)
+  static const int mode = [] {
     const char* v = std::getenv("PS_HOST_LANE_CHUNKS");
-    return v && v[0] == '1';
+    return v ? std::atoi(v) : 0;
   }();
-  const int64_t per = coarse ? T : 8 * static_cast<int64_t>(T);
-  const int64_t C = std::max<int64_t>(1, (U + per - 1) / per);
-  for (int64_t c; (c = next.fetch_add(1, std::memory_order_relaxed)) * C < U;)
-    for (int64_t u = c * C, e = std::min(U, (c + 1) * C); u < e; ++u) fn(u);
+  const int64_t fixed = mode == 1 ? (U + T - 1) / T : std::max<int64_t>(1, (U + 8 * T - 1) / (8 * T));
+  int64_t cur = next.load(std::memory_order_relaxed);
+  while (cur < U) {
+    const int64_t c = mode ? fixed : std::max<int64_t>(2, (U - cur) / (2 * static_cast<int64_t>(T)));
+    if (!next.compare_exchange_weak(cur, cur + c, std::memory_order_relaxed)) continue;
+    for (int64_t u = cur, e = std::min(U, cur + c); u < e; ++u) fn(u);
+    cur = next.load(std::memory_order_relaxed);
+  }
 }
 
 }  // namespace
