@@ -443,16 +443,17 @@ def run_ours(args):
 
 
 def default_host_threads():
-    """Host expert lane threads: all cores but 2 (the engine and I/O threads mostly sleep
-    on futexes; the lane is pinned to the last CPUs), at most 14: on the B200 box's
-    16-core host 14 threads stream 153-159 GB/s vs 144-146 with 12 in the engine
-    (profiles/r01_bench_threads.jsonl); 0 without AVX512_BF16."""
+    """Host expert lane threads: one per core, at most 16 (the engine and I/O threads
+    mostly sleep on futexes/blocking events): on the B200 box's 16-core host 16 threads
+    stream 178-182 GB/s vs 170-177 with 15 and 168-175 with 14 in alternating runs
+    (profiles/r01_bench_lane_threads_14_15_16.jsonl; 14 beat 12 before,
+    r01_bench_threads.jsonl); 0 without AVX512_BF16."""
     try:
         if "avx512_bf16" not in open("/proc/cpuinfo").read():
             return 0
     except OSError:
         return 0
-    return max(0, min(14, (os.cpu_count() or 1) - 2))
+    return max(0, min(16, os.cpu_count() or 1))
 
 
 def decode_summary(st, dev_ms, N, B, L):
