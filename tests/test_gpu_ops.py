@@ -319,3 +319,23 @@ def test_bad_arguments_fail_loudly(torch_cuda):
     assert lib.ps_route_topk(None, None, None, None, None, 0, 4, 16, 300, 2, None, None, None, None, None,
                              None) == ps.capi.PS_EINVAL
     assert lib.ps_permute(None, 4, 2, 8, None, None, None, None, 16, None, None) == ps.capi.PS_EINVAL
+
+
+def test_rows_from_host_reads_mapped_pinned_rows(torch_cuda):
+    """ps_rows_from_host: the SMs copy f32 rows from mapped pinned host memory into
+    device memory (no copy engine) and zero-fill the extra split copies, bit for bit."""
+    torch = torch_cuda
+    lib = ps.load()
+    n, stride = 3 * 4096, 5 * 4096
+    src = torch.randn(n).pin_memory()
+    dst = torch.full((3 * stride,), float("nan"), device="cuda")
+    ps.check(lib.ps_rows_from_host(C.c_void_p(src.data_ptr()), n, C.c_void_p(dst.data_ptr()), 2, stride,
+                                   C.c_void_p(torch.cuda.current_stream().cuda_stream)))
+    torch.cuda.synchronize()
+    out = dst.cpu()
+    assert torch.equal(out[:n], src)
+    assert torch.isnan(out[n:stride]).all()  # untouched
+    for z in (1, 2):
+        assert torch.equal(out[z * stride:z * stride + n], torch.zeros(n))
+    with pytest.raises(RuntimeError):
+        ps.check(lib.ps_rows_from_host(C.c_void_p(src.data_ptr()), n - 1, C.c_void_p(dst.data_ptr()), 0, 0, None))
