@@ -623,6 +623,49 @@ ps_status expert_ffn_batch(ps_host_lane l, int n, const uint16_t* const* slabs, 
             d[static_cast<size_t>(k >> 1) * kTok * 2 + 1] = xr[k + 1];
           }
         }
+      // PS_HOST_LANE_ONEPASS=1: one pool pass (below). Opt-in: alternating engine runs
+      // show no measurable difference to two passes (profiles/r01_bench_lane_onepass.jsonl),
+      // and its spin-waits burn a core when lane threads oversubscribe the host.
+      static const bool two_pass = [] {
+        const char* v = std::getenv("PS_HOST_LANE_ONEPASS");
+        return !(v && v[0] == '1');
+      }();
+      if (!two_pass) {
+        // One pool pass: gate_up units (expert-major) then down units; a down unit of
+        // expert j waits (release/acquire counter) until all nb1 gate_up units of j have
+        // written h. All gate_up units are handed out before any down unit and never
+        // wait, so the spin always ends; threads that finish early start on the down
+        // projections instead of idling at a phase barrier.
+        std::unique_ptr<std::atomic<int>[]> done(new std::atomic<int>[n]);
+        for (int j = 0; j < n; ++j) done[j].store(0, std::memory_order_relaxed);
+        std::atomic<int64_t> next{0};
+        l->pool->run([&](int) {
+          amx_config();
+          for_units(U1 + U2, T, next, [&](int64_t u) {
+            if (u < U1) {
+              const int j = static_cast<int>(u / nb1), blk = static_cast<int>(u % nb1);
+              const uint16_t* wg = slabs[j];
+              const uint16_t* wu = wg + static_cast<size_t>(F) * H;
+              for (int g = 0; g * kTok < m[j]; ++g)
+                (tiled ? amx_gate_up_block<true> : amx_gate_up_block<false>)(
+                    wg, wu, xb + xo[j] + static_cast<size_t>(g) * H * kTok, H, blk * 16,
+                    hb + ho[j] + static_cast<size_t>(g) * F * kTok);
+              done[j].fetch_add(1, std::memory_order_release);
+            } else {
+              const int64_t v = u - U1;
+              const int j = static_cast<int>(v / nb2), blk = static_cast<int>(v % nb2);
+              while (done[j].load(std::memory_order_acquire) < nb1) _mm_pause();
+              const uint16_t* wd = slabs[j] + static_cast<size_t>(2) * F * H;
+              for (int g = 0; g * kTok < m[j]; ++g)
+                (tiled ? amx_down_block<true> : amx_down_block<false>)(
+                    wd, hb + ho[j] + static_cast<size_t>(g) * F * kTok, H, F, blk * 16,
+                    std::min(kTok, m[j] - g * kTok), y + static_cast<size_t>(row0[j] + g * kTok) * H);
+            }
+          });
+          amx_release();
+        });
+        return;
+      }
       std::atomic<int64_t> next1{0}, next2{0};
       l->pool->run([&](int) {
         amx_config();
