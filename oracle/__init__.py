@@ -104,6 +104,12 @@ def oracle_lib() -> C.CDLL:
                                          C.c_void_p, C.c_void_p, C.c_void_p, C.c_int, C.c_int]
         _oracle.or_expert_ffn.argtypes = [C.c_void_p, C.c_int, C.c_int, C.c_int, C.c_void_p, C.c_void_p, C.c_int]
         _oracle.or_init_slab.argtypes = [C.c_void_p, C.c_int, C.c_int, C.c_uint64, C.c_int, C.c_int]
+        _oracle.or_route_batch.argtypes = [C.c_void_p, C.c_void_p, C.c_void_p, C.c_void_p, C.c_int, C.c_int,
+                                           C.c_int, C.c_int, C.c_int, C.c_void_p, C.c_void_p, C.c_int]
+        _oracle.bl_moe_layer.argtypes = [C.c_void_p, C.c_int, C.c_int, C.c_int, C.c_int, C.c_int, C.c_void_p,
+                                         C.c_void_p, C.c_void_p, C.c_void_p, C.c_int]
+        _oracle.bl_init_slabs.argtypes = [C.c_void_p, C.c_void_p, C.c_void_p, C.c_int, C.c_int, C.c_int,
+                                          C.c_uint64, C.c_int]
     return _oracle
 
 
@@ -149,6 +155,12 @@ def ref_lib() -> C.CDLL:
         _ref.ref_spec_preset.argtypes = [C.c_char_p, C.POINTER(RefSpec)]
         _ref.ref_desk_scale.argtypes = [C.c_char_p, C.c_int, C.c_int, C.c_int, C.POINTER(RefSpec)]
         _ref.ref_topk.argtypes = [C.c_void_p, C.c_int, C.c_int, C.c_void_p, C.POINTER(C.c_int)]
+        _ref.ref_router_inputs.argtypes = [C.POINTER(RefGen), C.POINTER(RefSpec), C.c_int, C.c_uint64, C.c_void_p,
+                                           C.c_void_p, C.c_void_p]
+        _ref.ref_llapor_predict_batch.argtypes = [C.c_void_p, C.c_int, C.c_int, C.c_void_p, C.c_void_p, C.c_int,
+                                                  C.c_void_p, C.c_int, C.c_void_p, C.c_int]
+        _ref.ref_time_legs.argtypes = [C.POINTER(RefGen), C.POINTER(RefSpec), C.c_int, C.c_uint64, C.c_void_p,
+                                       C.c_uint64, C.POINTER(RefParams), C.c_double, C.c_void_p, C.c_void_p]
         _ref.ref_time_schedule_pass.argtypes = [C.POINTER(RefGen), C.POINTER(RefSpec), C.c_int, C.c_uint64,
                                                 C.c_uint64, C.POINTER(RefParams), C.c_int,
                                                 C.POINTER(C.c_double), C.POINTER(C.c_int64)]
@@ -172,6 +184,52 @@ def ref_spec_from(spec) -> RefSpec:
     """From a product capi.ModelSpec (same field order)."""
     return RefSpec(spec.num_layers, spec.experts_per_layer, spec.top_k, spec.hidden_dim, spec.expert_bytes,
                    spec.group_begin_middle, spec.group_begin_output)
+
+
+def ref_spec_preset(name: str) -> RefSpec:
+    s = RefSpec()
+    ref_check(ref_lib().ref_spec_preset(name.encode(), C.byref(s)))
+    return s
+
+
+def ref_router_inputs(gen: RefGen, spec: RefSpec, batch: int, seed: int):
+    """generate_trace's router inputs (ref_shim.cpp ref_router_inputs): gate [L,E,H],
+    follow [B,L] u8, zipf [L]."""
+    L, E, H = spec.num_layers, spec.experts, spec.hidden
+    gate = np.empty((L, E, H))
+    follow = np.empty((batch, L), np.uint8)
+    zipf = np.empty(L)
+    ref_check(ref_lib().ref_router_inputs(C.byref(gen), C.byref(spec), batch, seed, gate.ctypes.data,
+                                          follow.ctypes.data, zipf.ctypes.data))
+    return gate, follow, zipf
+
+
+def ref_llapor_predict_batch(handle, layer, hidden, active, gate_w, k, threads=16):
+    """Reference pca_apply + forward + predict_topk for a batch of layer-(layer-1)
+    features (threads over tokens) -> topk [B,k]."""
+    hidden = np.ascontiguousarray(hidden, np.float64)
+    active = np.ascontiguousarray(active, np.int32)
+    gate_w = np.ascontiguousarray(gate_w, np.float64)
+    B = hidden.shape[0]
+    out = np.empty((B, k), np.int32)
+    ref_check(ref_lib().ref_llapor_predict_batch(handle, layer, B, hidden.ctypes.data, active.ctypes.data,
+                                                 active.shape[1], gate_w.ctypes.data, k, out.ctypes.data, threads))
+    return out
+
+
+REF_LEGS = ["topk_indices", "aggregate_layer_loads", "pca_apply+forward+predict_topk (input-group net)",
+            "pca_apply+forward+predict_topk (middle-group net)", "build_hot_table+plan_residency",
+            "schedule_layer (PreSched)", "simulate_pipeline (presched, all layers)", "generate_trace (per token)"]
+
+
+def ref_time_legs(gen, spec, batch, seed, llapor, budget_bytes, params, min_seconds=0.25):
+    """1-core timing of the reference's hot-path functions (ref_shim.cpp ref_time_legs):
+    {leg name: (us per call, calls)}."""
+    us = np.zeros(8)
+    calls = np.zeros(8, np.int64)
+    ref_check(ref_lib().ref_time_legs(C.byref(gen), C.byref(spec), batch, seed, llapor, budget_bytes,
+                                      C.byref(RefParams(*params)), min_seconds, us.ctypes.data, calls.ctypes.data))
+    return {REF_LEGS[i]: (float(us[i]), int(calls[i])) for i in range(8)}
 
 
 def ref_trace(gen: RefGen, spec: RefSpec, batch: int, seed: int):
@@ -203,6 +261,21 @@ def or_route(gate, a, zipf, follow, prev_top1, k):
                           int(follow), int(prev_top1), k, lg.ctypes.data_as(C.c_void_p),
                           w.ctypes.data_as(C.c_void_p), ids.ctypes.data_as(C.c_void_p))
     return lg, w, ids
+
+
+def or_route_batch(gate, hidden, follow, zipf, k, threads=1):
+    """or_route_trace in one C call (OpenMP over tokens): weights [B,L,E], ids [B,L,k]."""
+    gate = np.ascontiguousarray(gate, np.float64)
+    hidden = np.ascontiguousarray(hidden, np.float64)
+    follow = np.ascontiguousarray(follow, np.uint8)
+    zipf = np.ascontiguousarray(zipf, np.float64)
+    B, L, H = hidden.shape
+    E = gate.shape[1]
+    w = np.empty((B, L, E))
+    ids = np.empty((B, L, k), np.int32)
+    oracle_lib().or_route_batch(gate.ctypes.data, hidden.ctypes.data, follow.ctypes.data, zipf.ctypes.data, B, L, E,
+                                H, k, w.ctypes.data, ids.ctypes.data, threads)
+    return w, ids
 
 
 def or_route_trace(gate, hidden, follow, zipf, k):
@@ -340,6 +413,35 @@ def or_moe_layer(slabs, H, F, x_bf16, ids, gate, round_h=True, threads=16):
     oracle_lib().or_moe_layer(ptrs, H, F, B, k, E, x.ctypes.data_as(C.c_void_p), ids.ctypes.data_as(C.c_void_p),
                               g.ctypes.data_as(C.c_void_p), y.ctypes.data_as(C.c_void_p), int(round_h), threads)
     return y
+
+
+def bl_moe_layer(slabs, H, F, x_bf16, ids, gate, threads=16):
+    """CPU-baseline port (oracle/cpu_port.c): same result as or_moe_layer (f32
+    accumulation), each routed expert streamed once for all its tokens."""
+    lib = oracle_lib()
+    ids = np.ascontiguousarray(ids, np.int32)
+    B, k = ids.shape
+    E = gate.shape[1]
+    ptrs = (C.c_void_p * E)(*[s.ctypes.data if s is not None else None for s in slabs])
+    x = np.ascontiguousarray(x_bf16, np.uint16)
+    g = np.ascontiguousarray(gate, np.float32)
+    y = np.empty((B, H), np.float32)
+    lib.bl_moe_layer(ptrs, H, F, B, k, E, x.ctypes.data_as(C.c_void_p), ids.ctypes.data_as(C.c_void_p),
+                     g.ctypes.data_as(C.c_void_p), y.ctypes.data_as(C.c_void_p), threads)
+    return y
+
+
+def bl_init_slabs(pairs, H, F, seed, threads=16):
+    """Synthetic bf16 slabs (or_init_slab values) for [(layer, expert)], one thread per slab."""
+    out = [np.empty(3 * H * F, np.uint16) for _ in pairs]
+    n = len(pairs)
+    if n:
+        ptrs = (C.c_void_p * n)(*[a.ctypes.data for a in out])
+        ls = np.array([p[0] for p in pairs], np.int32)
+        es = np.array([p[1] for p in pairs], np.int32)
+        oracle_lib().bl_init_slabs(ptrs, ls.ctypes.data_as(C.c_void_p), es.ctypes.data_as(C.c_void_p), n, H, F,
+                                   C.c_uint64(seed), threads)
+    return out
 
 
 def bf16_to_f32(a):

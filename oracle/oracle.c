@@ -75,6 +75,27 @@ void or_route(const double* gate, const double* a, int E, int H, double zipf, in
   or_topk(weights, E, k, ids);
 }
 
+/* The router of generate_trace (workload.cpp:176-202) over a whole batch: token t walks
+ * its layers in order (the kappa-follow input is its own previous top-1, workload.cpp:
+ * 184-188), tokens are independent (OpenMP over tokens; threads = 1 for the 1-core
+ * leg). gate [L,E,H], hidden [B,L,H], follow [B,L], zipf [L] -> weights [B,L,E],
+ * ids [B,L,k]. */
+void or_route_batch(const double* gate, const double* hidden, const uint8_t* follow, const double* zipf,
+                    int B, int L, int E, int H, int k, double* weights, int32_t* ids, int threads) {
+#pragma omp parallel for schedule(static) num_threads(threads > 0 ? threads : 1)
+  for (int t = 0; t < B; ++t) {
+    double* lg = (double*)malloc(sizeof(double) * E);
+    int prev = -1;
+    for (int l = 0; l < L; ++l) {
+      const size_t tl = (size_t)t * L + l;
+      or_route(gate + (size_t)l * E * H, hidden + tl * H, E, H, zipf[l], follow[tl], prev, k, lg,
+               weights + tl * E, ids + tl * k);
+      prev = ids[tl * k];
+    }
+    free(lg);
+  }
+}
+
 /* simulator.cpp:45-57 over the histogram of workload.cpp:283-288. */
 int or_sorted_loads(const int32_t* counts, int E, int layer, const uint8_t* exclude,
                     or_load* out) {

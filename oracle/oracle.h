@@ -39,6 +39,8 @@ void or_route(const double* gate /*E*H*/, const double* a /*H*/, int E, int H, d
               int follow, int prev_top1, int k, double* logits, double* weights, int32_t* ids);
 
 /* workload.cpp:283-288 + simulator.cpp:45-57: histogram then (tokens, expert) order. */
+void or_route_batch(const double* gate, const double* hidden, const uint8_t* follow, const double* zipf,
+                    int B, int L, int E, int H, int k, double* weights, int32_t* ids, int threads);
 int or_sorted_loads(const int32_t* counts /*E*/, int E, int layer, const uint8_t* exclude,
                     or_load* out);
 

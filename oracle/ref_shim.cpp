@@ -9,10 +9,15 @@
 // Every entry point returns 0 on success and maps the reference's exceptions the
 // same way the reference CLI does (tools/prescope_main.cpp:427-434):
 //   1 = std::invalid_argument, 2 = std::out_of_range, 3 = std::runtime_error/other.
+#include <algorithm>
+#include <cmath>
+#include <random>
 #include <chrono>
+#include <thread>
 #include <cstdint>
 #include <cstring>
 #include <fstream>
+#include <functional>
 #include <map>
 #include <memory>
 #include <set>
@@ -524,9 +529,11 @@ int ref_llapor_predict_loads(void* handle, const ref_gen* gen, int batch, uint64
   });
 }
 
-// CPU-baseline leg (bench.py --impl reference): the reference's own per-decode-step
-// host work on one trace — predict_loads with LLaPor, build_instance, plan_residency,
-// simulate_policy(presched) — timed here in C++ so no ctypes overhead is counted.
+// CPU-baseline leg: the reference's own per-decode-step scheduling work on one trace —
+// build_hot_table + plan_residency, predict_loads with the "perfect" PredictFn (the
+// LLaPor inference leg is timed separately by ref_time_legs / ref_llapor_predict_batch),
+// build_instance, simulate_policy(presched) — timed here in C++ so no ctypes overhead
+// is counted.
 // Returns mean seconds per call over `reps` in *sec_out.
 int ref_time_schedule_pass(const ref_gen* gen, const ref_spec* spec, int batch, uint64_t seed,
                            uint64_t budget_bytes, const ref_params* params, int reps,
@@ -546,6 +553,165 @@ int ref_time_schedule_pass(const ref_gen* gen, const ref_spec* spec, int batch, 
       ms = simulate_policy(inst, SchedulerPolicy::parse("presched"), to_params(*params)).timeline.makespan;
     *sec_out = std::chrono::duration<double>(std::chrono::steady_clock::now() - t0).count() / reps;
     *makespan_out = ms;
+  });
+}
+
+// LLaPor inference over a batch (bench.py --impl reference: the reference's
+// pca_apply + forward + predict_topk, predictor.cpp:116-124, 166-247, 669-672, per
+// token, tokens split over `threads` host threads; the model is read-only). hidden
+// [B*H], active [B*k_prev], gate [B*E] of layer-1 features -> topk_out [B*k].
+int ref_llapor_predict_batch(void* handle, int layer, int B, const double* hidden, const int32_t* active,
+                             int k_prev, const double* gate, int k, int32_t* topk_out, int threads) {
+  return guarded([&] {
+    const LLaPor& m = static_cast<LLaPorHandle*>(handle)->model;
+    const LLaPorNet& net = m.nets.at(layer);
+    const int H = m.spec.hidden_dim, E = net.experts_per_layer;
+    const int T = std::max(1, std::min(threads, B));
+    std::vector<std::string> errs(T);
+    auto work = [&](int w) {
+      try {
+        for (int t = B * w / T; t < B * (w + 1) / T; ++t) {
+          PredictorFeatures feat;
+          feat.hidden_reduced = pca_apply(net.pca, std::vector<double>(hidden + static_cast<size_t>(t) * H,
+                                                                       hidden + static_cast<size_t>(t + 1) * H));
+          feat.active_onehot.assign(E, 0.0);
+          for (int j = 0; j < k_prev; ++j) feat.active_onehot.at(active[t * k_prev + j]) = 1.0;
+          feat.gate_weights_prev.assign(gate + static_cast<size_t>(t) * E, gate + static_cast<size_t>(t + 1) * E);
+          std::vector<int> top = predict_topk(net, feat, k);
+          for (int j = 0; j < k; ++j) topk_out[t * k + j] = top.at(j);
+        }
+      } catch (const std::exception& ex) {
+        errs[w] = ex.what();
+      }
+    };
+    std::vector<std::thread> th;
+    for (int w = 1; w < T; ++w) th.emplace_back(work, w);
+    work(0);
+    for (auto& x : th) x.join();
+    for (auto& e : errs)
+      if (!e.empty()) throw std::runtime_error(e);
+  });
+}
+
+// Per-leg 1-core timing of the reference's hot-path functions (SURVEY.md §8d CPU
+// baseline) on one reference trace of `batch` tokens. Each leg repeats until
+// `min_seconds` elapsed; us_out[i] = mean microseconds per call, calls_out[i] = calls.
+//   0 topk_indices          (workload.cpp:110-119) on one (token, layer)'s gate weights
+//   1 aggregate_layer_loads (workload.cpp:283-288) for one layer of the batch
+//   2 pca_apply+forward+predict_topk, input-group net (predictor.cpp:116-124, 344-352, 669-672)
+//   3 the same, middle-group net (the wider PCA)
+//   4 build_hot_table + plan_residency (predictor.cpp:405-433)
+//   5 schedule_layer (scheduler.cpp:54-213) on one layer's LayerInputs (E_cur, E_next, E_next2)
+//   6 simulate_policy(presched) over all layers (simulator.cpp:61-242), per step
+//   7 generate_trace (RNG + router, workload.cpp:139-219), per token
+// Legs 2-3 need an LLaPor handle (nullable: reported as 0).
+int ref_time_legs(const ref_gen* gen, const ref_spec* spec, int batch, uint64_t seed, void* llapor,
+                  uint64_t budget_bytes, const ref_params* params, double min_seconds, double* us_out,
+                  int64_t* calls_out) {
+  return guarded([&] {
+    using clk = std::chrono::steady_clock;
+    const ModelSpec sp = to_spec(*spec);
+    Trace t = generate_trace(to_gen(*gen), sp, batch, seed);
+    const int L = sp.num_layers, K = sp.top_k, E = sp.experts_per_layer;
+    volatile int64_t sink = 0;
+    auto timed = [&](int leg, const std::function<void(int64_t)>& body) {
+      int64_t n = 0;
+      const auto t0 = clk::now();
+      double el = 0;
+      do {
+        body(n++);
+        el = std::chrono::duration<double>(clk::now() - t0).count();
+      } while (el < min_seconds);
+      us_out[leg] = el * 1e6 / static_cast<double>(n);
+      calls_out[leg] = n;
+    };
+    const size_t S = t.steps.size();
+    timed(0, [&](int64_t i) { sink = sink + topk_indices(t.steps[i % S].gate_weights, K).size(); });
+    timed(1, [&](int64_t i) { sink = sink + aggregate_layer_loads(t, static_cast<int>(i % L)).size(); });
+    for (int leg = 2; leg <= 3; ++leg) {
+      us_out[leg] = 0;
+      calls_out[leg] = 0;
+      if (!llapor) continue;
+      const LLaPor& m = static_cast<LLaPorHandle*>(llapor)->model;
+      const int l = leg == 2 ? 1 : sp.group_begin_middle;  // input group / middle group target
+      if (l < 1 || l >= static_cast<int>(m.nets.size()) || m.nets[l].blocks.empty()) continue;
+      const LLaPorNet& net = m.nets[l];
+      timed(leg, [&](int64_t i) {
+        const TraceStep& st = t.steps[static_cast<size_t>(i % batch) * L + (l - 1)];
+        PredictorFeatures feat;
+        feat.hidden_reduced = pca_apply(net.pca, st.hidden);
+        feat.active_onehot.assign(E, 0.0);
+        for (int e : st.active_experts) feat.active_onehot.at(e) = 1.0;
+        feat.gate_weights_prev = st.gate_weights;
+        sink = sink + predict_topk(net, feat, K).size();
+      });
+    }
+    std::set<std::pair<int, int>> resident;
+    timed(4, [&](int64_t) {
+      HotExpertTable table = build_hot_table({t});
+      auto res = plan_residency(table, budget_bytes, spec->expert_bytes);
+      sink = sink + res.size();
+      if (resident.empty())
+        for (auto key : res) resident.insert(key);
+    });
+    PredictFn perfect = make_predict_fn(PredictorChoice::parse("perfect"), nullptr, nullptr, K, 0);
+    PipelineInstance inst = build_instance(t, predict_loads(t, perfect), resident);
+    auto sorted = [&](const std::map<int, int>& m, int layer) {
+      std::vector<ExpertLoad> v;
+      for (auto [e, c] : m)
+        if (!resident.count({layer, e})) v.push_back({e, layer, c, ExpertLocation::Host});
+      std::sort(v.begin(), v.end(), [](const ExpertLoad& a, const ExpertLoad& b) {
+        return a.tokens != b.tokens ? a.tokens < b.tokens : a.expert < b.expert;
+      });
+      return v;
+    };
+    std::vector<LayerInputs> ins(L);
+    for (int l = 0; l < L; ++l) {
+      ins[l].e_cur = sorted(inst.layers[l].truth, l);
+      if (l + 1 < L) ins[l].e_next = sorted(inst.layers[l + 1].predicted, l + 1);
+      if (l + 2 < L) ins[l].e_next2 = sorted(inst.layers[l + 2].predicted, l + 2);
+      ins[l].params = to_params(*params);
+    }
+    timed(5, [&](int64_t i) { sink = sink + schedule_layer(ins[i % L]).split_index; });
+    timed(6, [&](int64_t) {
+      sink = sink + simulate_policy(inst, SchedulerPolicy::parse("presched"), to_params(*params)).timeline.makespan;
+    });
+    timed(7, [&](int64_t i) { sink = sink + generate_trace(to_gen(*gen), sp, 1, seed + 1 + i).steps.size(); });
+    (void)sink;
+  });
+}
+
+// Router inputs of generate_trace (workload.cpp:139-219) without the routing, for the
+// f64 router restatement (oracle.c or_route_batch) in bench.py's reference arm: the
+// gate matrices G [L*E*D] (the first L*E*D draws of the seeded engine), the
+// kappa-follow flags [batch*L] and zipf_s per layer [L]. The engine's draw sequence does
+// not depend on the routing (one uniform per layer >= 1, drawn before the follow test;
+// D normals per token and per layer transition), so it is replayed here with the same
+// libstdc++ distributions; tests/test_oracle.py checks that or_route_batch on these
+// inputs reproduces generate_trace's gate weights bit for bit.
+int ref_router_inputs(const ref_gen* gen, const ref_spec* spec, int batch, uint64_t seed, double* gate,
+                      uint8_t* follow, double* zipf) {
+  return guarded([&] {
+    const TraceGenConfig cfg = to_gen(*gen);
+    const ModelSpec sp = to_spec(*spec);
+    cfg.validate();
+    sp.validate();
+    std::mt19937_64 rng(seed);
+    std::normal_distribution<double> gauss(0.0, 1.0);
+    std::uniform_real_distribution<double> unif(0.0, 1.0);
+    const int L = sp.num_layers, E = sp.experts_per_layer, D = sp.hidden_dim;
+    const double wscale = 1.0 / std::sqrt(static_cast<double>(D));
+    for (size_t i = 0; i < static_cast<size_t>(L) * E * D; ++i) gate[i] = gauss(rng) * wscale;
+    for (int l = 0; l < L; ++l) zipf[l] = cfg.for_group(sp.group_of(l)).zipf_s;
+    for (int tok = 0; tok < batch; ++tok) {
+      for (int d = 0; d < D; ++d) (void)gauss(rng);
+      for (int l = 0; l < L; ++l) {
+        const GroupGenParams& gp = cfg.for_group(sp.group_of(l));
+        follow[static_cast<size_t>(tok) * L + l] = l > 0 && unif(rng) < gp.kappa;
+        if (l + 1 < L)
+          for (int d = 0; d < D; ++d) (void)gauss(rng);
+      }
+    }
   });
 }
 

@@ -220,6 +220,7 @@ class IoChannel {
                                  queue_.front() != j; });
         if (stop_) break;
         busy_ = false;
+        cv_.notify_all();  // drain() may be waiting for busy_ to clear (abandoned queue)
         continue;  // re-evaluate the front (it may have been cancelled)
       }
       queue_.pop_front();
@@ -1086,10 +1087,7 @@ void decode_step(ps_engine_s& e, const float* hidden, const uint8_t* follow, int
         const uint16_t* slab = e.host_slab[static_cast<size_t>(l) * E + ex];
         require(slab != nullptr, "host lane: cpu_set expert has no host copy");
         CpuJob j{l, ex, off[ex + 1] - off[ex], off[ex], slab};
-        if (!e.host_z.empty()) {  // the lane's z path reads 4-bit z-slabs only
-          const uint8_t* z = e.host_z[static_cast<size_t>(l) * E + ex];
-          if (z && reinterpret_cast<const ZHeader*>(z)->code_bits == 4) j.z = z;
-        }
+        if (!e.host_z.empty()) j.z = e.host_z[static_cast<size_t>(l) * E + ex];  // 3- or 4-bit codes
         for (int r = j.row0; r < j.row0 + j.m; ++r)
           std::memcpy(e.lane_xrows + static_cast<size_t>(r) * H, e.lane_x + static_cast<size_t>(perm[r] / Kt) * H,
                       sizeof(uint16_t) * H);
@@ -1626,7 +1624,12 @@ void create_engine(const ps_engine_config& cfg, ps_engine_s& e) {
 }
 
 void destroy_engine(ps_engine_s& e) {
-  if (e.io) e.io->drain();
+  // A step that failed mid-layer can leave on-demand jobs queued behind a slot
+  // generation that will never be recorded: forget them before draining the channel.
+  if (e.io) {
+    e.io->abandon_queued();
+    e.io->drain();
+  }
   e.io.reset();
   e.lane_drv.reset();
   if (e.lane) ps_host_lane_destroy(e.lane);

@@ -148,6 +148,8 @@ ps_status ps_rows_from_host(const float* host_src, int64_t n, float* dst, int ze
   return guarded([&] {
     require(n >= 0 && zero_copies >= 0 && n % 4 == 0 && zero_stride % 4 == 0 && (n == 0 || (host_src && dst)),
             "ps_rows_from_host: bad arguments");
+    // zero-filled copies must not overlap the copied range (or each other)
+    require(zero_copies == 0 || zero_stride >= n, "ps_rows_from_host: zero_stride must be >= n");
     if (n == 0) return;
     void* dev_src = nullptr;
     PS_CUDA(cudaHostGetDevicePointer(&dev_src, const_cast<float*>(host_src), 0));

@@ -31,8 +31,10 @@
 //    waits (acquire) until every F tile of its split is done, then reads h from L2.
 //    Items run in increasing index order per CTA and every gate_up index is below every
 //    down index, so a wait never blocks a producer of h; the producer keeps prefetching
-//    down weights meanwhile. The last down item of a split resets its counters for the
-//    next launch (per-stream workspace).
+//    down weights meanwhile. Counters live in a per-stream workspace of two sets used
+//    in alternation: block 0 of a launch zeroes the other set for the next launch (the
+//    stream's previous launch, which used it, is complete); a failed launch re-zeroes it
+//    on the host side.
 //  * Weight tensor maps are encoded on the host once per slab and kept in a device table
 //    (immutable entries; the kernel acquire-fences them before first use).
 #include <cuda.h>
@@ -670,11 +672,18 @@ void run_group(const ps_expert_group* group, int base, int count, const int32_t*
   const SyncSets ss = sync_workspace(s);  // one parity flip per launch
   p.sync = ss.cur;
   p.sync_next = ss.next;
-  switch (NT) {
-    case 1: launch<1, mt_for(1), CAP>(p, s); break;
-    case 2: launch<2, mt_for(2), CAP>(p, s); break;
-    case 4: launch<4, mt_for(4), CAP>(p, s); break;
-    default: launch<8, mt_for(8), CAP>(p, s); break;
+  try {
+    switch (NT) {
+      case 1: launch<1, mt_for(1), CAP>(p, s); break;
+      case 2: launch<2, mt_for(2), CAP>(p, s); break;
+      case 4: launch<4, mt_for(4), CAP>(p, s); break;
+      default: launch<8, mt_for(8), CAP>(p, s); break;
+    }
+  } catch (...) {
+    // The failed launch never zeroed the next launch's counter set: do it here, so the
+    // next launch on this stream does not count on top of stale values.
+    cudaMemsetAsync(ss.next, 0, sizeof(int) * kSyncEntries * kMaxSplit, s);
+    throw;
   }
 }
 

@@ -5,6 +5,9 @@ histograms, permutation); router/LLaPor logits within rel 1e-4 of the f64 oracle
 bf16 expert FFN + combine within rel 2e-2 (norm-wise) of the f64-accumulating oracle
 on identical bf16 weights (BASELINE.json north_star tolerances)."""
 import ctypes as C
+import json
+import os
+import pathlib
 
 import numpy as np
 import pytest
@@ -62,35 +65,53 @@ def _route_case(torch, spec, B, seed, gen=None):
     return out, (ref_logits, ref_w, ref_ids, hidden)
 
 
-@pytest.mark.parametrize("preset,L,E,H,B", [("mixtral", 4, 8, 16, 32),     # config[0] shape
-                                            ("mixtral", 3, 8, 4096, 16),    # Mixtral router
-                                            ("deepseek", 3, 64, 2048, 32),
-                                            ("qwen3", 3, 128, 2048, 32)])
-def test_route_topk_parity(torch_cuda, preset, L, E, H, B):
-    spec = ps.desk_scale(preset, L, E, H)
-    out, (rl, rw, rids, hidden) = _route_case(torch_cuda, spec, B, 11)
-    k = spec.top_k
-    near_ties = []
+NEAR_TIES = json.loads((GOLDEN / "near_ties.json").read_text())
+
+
+@pytest.mark.parametrize("case", list(NEAR_TIES["cases"]))
+def test_route_topk_parity(torch_cuda, case):
+    """K1 vs the reference router on the reference's own inputs (cases and near-tie list:
+    tests/golden/near_ties.json, made by make_near_ties.py from oracle/_ref).
+
+    * top-k ids bit-exact vs topk_indices on the kernel's own weights;
+    * histogram == aggregate_layer_loads of the kernel's ids;
+    * logits within LOGIT_RTOL of the f64 router, every (token, layer) — conditioned on
+      the GPU's own previous top-1 (the kappa-follow input), so no layer is skipped;
+    * ids == the reference's ids except at LISTED near-ties; a token whose listed flip
+      changed its top-1 is compared at later layers with the f64 router conditioned on
+      the GPU's top-1 (bit-exact there too, unless that is itself a near-tie)."""
+    c = NEAR_TIES["cases"][case]
+    spec = ps.spec_preset(c["preset"]) if c["full"] else ps.desk_scale(c["preset"], c["L"], c["E"], c["H"])
+    B, k, L, E = c["B"], c["k"], c["L"], c["E"]
+    out, (rl, rw, rids, hidden) = _route_case(torch_cuda, spec, B, c["seed"])
+    cfg = ps.TraceGenConfig(*[ps.GROUP_DEFAULT_GEN[g] for g in ("input", "middle", "output")])
+    gate, _, follow, zipf = ps.trace_inputs(cfg, spec, B, c["seed"])
+    listed = {(d["layer"], d["token"]) for d in c["near_ties"]}
+    observed, cascaded = [], []
     for l, (lg, w, ids, counts, xb) in enumerate(out):
-        # top-k bit-exact against topk_indices on the kernel's own weights
         for t in range(B):
             assert list(ids[t]) == orc.or_topk(w[t].astype(np.float64), k)
-        # histogram == aggregate_layer_loads of the kernel's routing
         assert np.array_equal(counts, np.bincount(ids.ravel(), minlength=E))
-        # logits vs f64 reference (layer >= 1 follows the GPU's own previous top-1)
-        scale = np.maximum(1.0, np.abs(rl[:, l]))
-        same_prev = l == 0 or np.array_equal(out[l - 1][2][:, 0], rids[:, l - 1, 0])
-        if same_prev:
-            assert (np.abs(lg - rl[:, l]) / scale).max() < LOGIT_RTOL
-        # ids vs reference: differences only at listed near-ties
         for t in range(B):
-            if list(ids[t]) != list(rids[t, l]):
-                srt = np.sort(rw[t, l])[::-1]
-                gap = srt[k - 1] - srt[k] if k < E else 1.0
-                near_ties.append((l, t, gap))
+            gpu_prev = int(out[l - 1][2][t, 0]) if l else -1
+            ref_prev = int(rids[t, l - 1, 0]) if l else -1
+            if gpu_prev == ref_prev:
+                ref_lg, ref_ids = rl[t, l], rids[t, l]
+            else:  # after a listed top-1 flip: the f64 router on the GPU's own previous top-1
+                ref_lg, _, ref_ids = orc.or_route(gate[l], hidden[t, l], zipf[l], follow[t, l], gpu_prev, k)
+                cascaded.append((l, t))
+            err = (np.abs(lg[t] - ref_lg) / np.maximum(1.0, np.abs(ref_lg))).max()
+            assert err < LOGIT_RTOL, (l, t, err)
+            if list(ids[t]) != list(ref_ids):
+                observed.append((l, t))
+                assert (l, t) in listed, f"top-k mismatch at unlisted (layer {l}, token {t}): {ids[t]} vs {ref_ids}"
         np.testing.assert_array_equal(xb, orc.f32_to_bf16(hidden[:, l].astype(np.float32)))
-    assert all(g < 1e-4 for _, _, g in near_ties), near_ties
-    assert len(near_ties) <= max(1, B * L // 100)
+    dest = os.environ.get("PS_NEAR_TIE_OUT")
+    if dest:  # observed flips of this run (gpurun: under gpurun_out/)
+        p = pathlib.Path(dest)
+        prev = json.loads(p.read_text()) if p.exists() else {}
+        prev[case] = {"listed": sorted(listed), "observed": observed, "cascaded": cascaded}
+        p.write_text(json.dumps(prev, indent=1))
 
 
 @pytest.mark.parametrize("B,k,E", [(1, 2, 8), (16, 2, 8), (32, 8, 128), (2048, 6, 64), (4096, 8, 128)])
@@ -339,3 +360,6 @@ def test_rows_from_host_reads_mapped_pinned_rows(torch_cuda):
         assert torch.equal(out[z * stride:z * stride + n], torch.zeros(n))
     with pytest.raises(RuntimeError):
         ps.check(lib.ps_rows_from_host(C.c_void_p(src.data_ptr()), n - 1, C.c_void_p(dst.data_ptr()), 0, 0, None))
+    for bad_stride in (n - 4, -stride):  # overlapping or negative zero-fill ranges are rejected
+        assert lib.ps_rows_from_host(C.c_void_p(src.data_ptr()), n, C.c_void_p(dst.data_ptr()), 1, bad_stride,
+                                     None) == ps.capi.PS_EINVAL

@@ -16,7 +16,24 @@ def _p(t):
     return C.c_void_p(t.data_ptr()) if t is not None else None
 
 
-def _prefill_case(torch, H, F, E, k, B, seed, skew=None, check_oracle_rows=None, with_decode=True):
+def _last_tile_tokens(offsets, perm_src, k):
+    """Tokens owning, for every expert, the last routed row, the first row of its last
+    128-row M tile (single-CTA kernel) and the first row the second CTA of its last
+    256-row pair tile computes (local rows 256*j + 128), when those exist."""
+    rows = []
+    for e in range(len(offsets) - 1):
+        m = int(offsets[e + 1] - offsets[e])
+        if m == 0:
+            continue
+        local = {m - 1, (m - 1) // 128 * 128}
+        r2 = (m - 1) // 256 * 256 + 128
+        if r2 < m:
+            local.add(r2)
+        rows += [int(offsets[e]) + r for r in local]
+    return np.unique(perm_src[np.array(rows)] // k)
+
+
+def _prefill_case(torch, H, F, E, k, B, seed, skew=None, check_oracle_rows=None, with_decode=True, last_tiles=False):
     lib = ps.load()
     s = C.c_void_p(torch.cuda.current_stream().cuda_stream)
     rng = np.random.default_rng(seed)
@@ -69,6 +86,8 @@ def _prefill_case(torch, H, F, E, k, B, seed, skew=None, check_oracle_rows=None,
         out["y_decode"] = y2.cpu().numpy()
     if check_oracle_rows:
         sel = np.arange(min(B, check_oracle_rows))
+        if last_tiles:  # + every expert's last rows: its last 128-row tile, the 2nd CTA of its last pair tile
+            sel = np.union1d(sel, _last_tile_tokens(offsets, src.cpu().numpy(), k))
         slabs_h = [t.cpu().numpy().view(np.uint16) if e in set(ids[sel].ravel()) else None
                    for e, t in enumerate(slabs_d)]
         out["y_oracle"] = orc.or_moe_layer(slabs_h, H, F, x[sel], ids[sel], gw[sel].astype(np.float32), True)
@@ -99,16 +118,20 @@ def test_prefill_vs_oracle_small(torch_cuda, prefill_kernel, H, F, E, k, B, skew
 
 
 def test_prefill_deepseek_shape(torch_cuda, prefill_kernel):
-    """DeepSeek-V2-Lite expert shape (H=2048, F=1408), 64 experts top-6, 2k-token chunk."""
-    out = _prefill_case(torch_cuda, 2048, 1408, 64, 6, 2048, 3, check_oracle_rows=6)
+    """DeepSeek-V2-Lite expert shape (H=2048, F=1408), 64 experts top-6, 2k-token chunk;
+    oracle rows include every expert's last (padded) M tile and 2nd pair CTA."""
+    out = _prefill_case(torch_cuda, 2048, 1408, 64, 6, 2048, 3, check_oracle_rows=6, last_tiles=True)
     assert _rel(out["y"], out["y_decode"]) < BF16_RTOL
     sel = out["sel"]
-    assert _rel(out["y"][sel], out["y_oracle"]) < BF16_RTOL
+    for i, t in enumerate(sel):  # per token: a bad padded-tile row cannot hide in a norm over many rows
+        assert _rel(out["y"][t], out["y_oracle"][i]) < BF16_RTOL, t
 
 
 def test_prefill_mixtral_shape(torch_cuda, prefill_kernel):
-    """Mixtral expert shape (H=4096, F=14336), 8 experts top-2, 1k tokens (m_e ~ 256)."""
-    out = _prefill_case(torch_cuda, 4096, 14336, 8, 2, 1024, 5, check_oracle_rows=2)
+    """Mixtral expert shape (H=4096, F=14336), 8 experts top-2, 1k tokens (m_e ~ 256);
+    oracle rows include every expert's last (padded) M tile and 2nd pair CTA."""
+    out = _prefill_case(torch_cuda, 4096, 14336, 8, 2, 1024, 5, check_oracle_rows=2, last_tiles=True)
     assert _rel(out["y"], out["y_decode"]) < BF16_RTOL
     sel = out["sel"]
-    assert _rel(out["y"][sel], out["y_oracle"]) < BF16_RTOL
+    for i, t in enumerate(sel):  # per token: a bad padded-tile row cannot hide in a norm over many rows
+        assert _rel(out["y"][t], out["y_oracle"][i]) < BF16_RTOL, t

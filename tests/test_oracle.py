@@ -1,5 +1,6 @@
 """Pins the CPU oracle (oracle/oracle.c) to the reference: golden vectors, KATs and the
 UNMODIFIED reference compiled in oracle/_ref. The oracle is only trusted after this."""
+import ctypes as C
 import json
 
 import numpy as np
@@ -184,3 +185,79 @@ def test_expert_ffn_oracle_linear_in_down_weights():
     g, u = wg @ xf, wu @ xf
     ref = wd @ (g / (1 + np.exp(-g)) * u)
     np.testing.assert_allclose(y[0], ref, rtol=1e-5, atol=1e-7)
+
+
+@needs_ref
+def test_near_tie_list_regenerates_from_reference():
+    """tests/golden/near_ties.json (the list test_route_topk_parity accepts top-k
+    mismatches from) is what make_near_ties.py derives from oracle/_ref today."""
+    import sys
+    sys.path.insert(0, str(GOLDEN))
+    import make_near_ties
+    fresh = make_near_ties.generate()
+    committed = json.loads((GOLDEN / "near_ties.json").read_text())
+    assert fresh == json.loads(json.dumps(committed))
+
+
+@needs_ref
+@pytest.mark.parametrize("preset,E,H,p_in,p_mid", [("mixtral", 8, 4096, 256, 512), ("qwen3", 128, 2048, 128, 256)])
+def test_llapor_oracle_full_shape_equals_reference(tmp_path, preset, E, H, p_in, p_mid):
+    """The f64 LLaPor restatement at paper dims (multi-chunk PCA, E=128 outputs) equals
+    the reference's load_checkpoint + pca_apply + forward + predict_topk bit for bit."""
+    from oracle.llpc import random_nets, write_llpc
+    spec = ps.desk_scale(preset, 3, E, H)
+    k = spec.top_k
+    path = tmp_path / "n.llpc"
+    write_llpc(path, spec, random_nets(spec, p_in, p_mid, 32, 48, seed=1))
+    _, onets = orc.llapor_net_from_ckpt(path)
+    h = orc.ref_lib().ref_llapor_load(str(path).encode())
+    assert h
+    rng = np.random.default_rng(2)
+    try:
+        for l in (1, 2):
+            for _ in range(4):
+                x = rng.standard_normal(H)
+                act = rng.choice(E, k, replace=False).astype(np.int32)
+                gw = np.exp(rng.standard_normal(E))
+                gw /= gw.sum()
+                P = p_mid if l == 1 else p_in
+                red, lg, top = np.empty(P), np.empty(E), np.empty(k, np.int32)
+                orc.ref_check(orc.ref_lib().ref_llapor_predict(h, l, x.ctypes.data, act.ctypes.data, k, gw.ctypes.data,
+                                                               k, red.ctypes.data, lg.ctypes.data, top.ctypes.data))
+                r2, lg2, top2 = orc.or_llapor_forward(onets[l], x, act, gw, k)
+                assert np.array_equal(red, r2) and np.array_equal(lg, lg2) and np.array_equal(top, top2)
+    finally:
+        orc.ref_lib().ref_llapor_free(h)
+
+
+@needs_ref
+@pytest.mark.parametrize("preset,L,E,H,B,seed", [("mixtral", 4, 8, 16, 32, 0), ("qwen3", 3, 128, 2048, 8, 5),
+                                                 ("mixtral", None, None, None, 4, 1000)])
+def test_reference_router_inputs_reproduce_generate_trace(preset, L, E, H, B, seed):
+    """bench.py's reference arm routes with or_route_batch on ref_router_inputs (the
+    reference engine's draws replayed in the shim) and the reference trace's hidden
+    states: bit-exact gate weights / top-k of generate_trace itself."""
+    spec = orc.ref_spec_preset(preset)
+    if L is not None:
+        orc.ref_check(orc.ref_lib().ref_desk_scale(preset.encode(), L, E, H, C.byref(spec)))
+    rg = orc.ref_gen(*[ps.GROUP_DEFAULT_GEN[g] for g in ("input", "middle", "output")])
+    hidden, gw, act = orc.ref_trace(rg, spec, B, seed)
+    gate, follow, zipf = orc.ref_router_inputs(rg, spec, B, seed)
+    w, ids = orc.or_route_batch(gate, hidden, follow, zipf, spec.top_k, threads=4)
+    assert np.array_equal(w, gw) and np.array_equal(ids, act)
+
+
+def test_cpu_port_moe_layer_matches_oracle():
+    """The CPU-baseline port (cpu_port.c: each expert streamed once, f32 AVX-512
+    accumulation) computes the oracle's MoE layer within fp32 rounding."""
+    rng = np.random.default_rng(0)
+    for H, F, E, k, B in ((256, 512, 8, 2, 16), (64, 96, 4, 2, 5), (512, 1408, 64, 6, 40)):
+        ids = np.stack([rng.choice(E, k, replace=False) for _ in range(B)]).astype(np.int32)
+        g = np.exp(rng.standard_normal((B, E)))
+        g = (g / g.sum(1, keepdims=True)).astype(np.float32)
+        x = orc.f32_to_bf16((rng.standard_normal((B, H)) / np.sqrt(H)).astype(np.float32))
+        slabs = orc.bl_init_slabs([(0, e) for e in range(E)], H, F, 3, 4)
+        assert all(np.array_equal(slabs[e], orc.or_init_slab(H, F, 3, 0, e)) for e in (0, E - 1))
+        y = orc.bl_moe_layer(slabs, H, F, x, ids, g, 4)
+        y2 = orc.or_moe_layer(slabs, H, F, x, ids, g, True, 4)
+        assert np.linalg.norm(y - y2) / np.linalg.norm(y2) < 1e-4
