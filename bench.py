@@ -116,66 +116,90 @@ def make_workload(args):
     return ps, spec, gen
 
 
-def cpu_sample(args, spec, gen, threads, sample_layers=1):
-    """Bounded CPU sample: `sample_layers` MoE layers of one decode step (B tokens) with
-    the oracle port (f64-accumulating SwiGLU + combine, all host cores), plus the
-    reference's own per-step scheduling (simulate_policy(presched), 1 core). Returns
-    seconds per full decode step (scaled to all L layers) and a description."""
-    import oracle as orc
-    import paper_2509_23638_b200 as ps
-    L, E, H, k = spec.num_layers, spec.experts_per_layer, spec.hidden_dim, spec.top_k
-    F = ps.ffn_dim(spec)
-    B = args.batch
-    gate, hidden, follow, zipf = ps.trace_inputs(gen, spec, B, 7)
-    _, w, ids = orc.or_route_trace(gate[:sample_layers], hidden[:, :sample_layers], follow[:, :sample_layers],
-                                   zipf[:sample_layers], k)
-    t_ffn = 0.0
-    for l in range(sample_layers):
-        used = sorted(set(ids[:, l].ravel().tolist()))
-        slabs = [orc.or_init_slab(H, F, args.weight_seed, l, e) if e in used else None for e in range(E)]
-        x = orc.f32_to_bf16(hidden[:, l].astype(np.float32))
+def host_info():
+    from oracle.cpu_arm import cpu_model
+    return {"cpu_model": cpu_model(), "nproc": os.cpu_count()}
+
+
+def cpu_sample(args, ffn_layers=(0, 1)):
+    """Bounded CPU sample for our arm's `cpu_baseline`: one decode step of the reference
+    CPU path (oracle/cpu_arm.py: the reference router, LLaPor at full shape and
+    simulate_policy(presched) through oracle/_ref for the WHOLE step, plus the expert
+    port on `ffn_layers` only, scaled to all layers), after one warm-up step; and the
+    1-core table of the reference's hot-path functions."""
+    from oracle.cpu_arm import RefArm
+    arm = RefArm(args.model, args.batch, args.budget, steps=2, weight_seed=args.weight_seed,
+                 ffn_layers=list(ffn_layers))
+    try:
+        arm.step(0)
+        sec, ph, _ = arm.step(1)
+        scale = arm.L / len(arm.ffn_layers)
+        step_s = sec - ph["experts"] + ph["experts"] * scale
+        legs = arm.legs_1core()
         t0 = time.perf_counter()
-        orc.or_moe_layer(slabs, H, F, x, ids[:, l], w[:, l].astype(np.float32), True, threads)
-        t_ffn += time.perf_counter() - t0
-    sched_s = 0.0
-    if orc.ref_available():
-        rg = orc.ref_gen(*[ps.GROUP_DEFAULT_GEN[g] for g in ("input", "middle", "output")])
-        sec, mk = C.c_double(), C.c_int64()
-        params = orc.RefParams(6406, 44, 349, 1e9, 0, 0)
-        orc.ref_check(orc.ref_lib().ref_time_schedule_pass(C.byref(rg), C.byref(orc.ref_spec_from(spec)), B, 7,
-                                                           int(args.budget * L * E) * spec.expert_bytes,
-                                                           C.byref(params), 3, C.byref(sec), C.byref(mk)))
-        sched_s = sec.value
-    step_s = t_ffn / sample_layers * L + sched_s
-    desc = (f"{sample_layers} of {L} MoE layers of one B={B} decode step on the oracle port (SwiGLU+combine, "
-            f"f64 accumulate, {threads} threads) scaled x{L}/{sample_layers}, + reference simulate_policy"
-            f"(presched) per step ({sched_s * 1e6:.0f} us, 1 core)")
-    return step_s, desc
+        from oracle import or_route_batch
+        or_route_batch(arm.gate, arm.hidden[:arm.B], arm.follow[:arm.B], arm.zipf, arm.k, 1)
+        route_us = (time.perf_counter() - t0) * 1e6 / (arm.B * arm.L)
+    finally:
+        arm.close()
+    legs_us = {"router (workload.cpp:176-202, f64 restatement), per token-layer": round(route_us, 3)}
+    legs_us.update({k: round(v[0], 3) for k, v in legs.items()})
+    desc = (f"one B={args.batch} decode step of the reference CPU path: router + LLaPor (P=256/512) + "
+            f"simulate_policy(presched) for all {arm.L} layers through oracle/_ref, experts+combine "
+            f"(oracle/cpu_port.c, {arm.threads} threads) on {len(ffn_layers)} of {arm.L} layers scaled "
+            f"x{scale:g}; phases {', '.join(f'{k} {v * 1e3:.1f} ms' for k, v in ph.items() if k != 'makespan_ticks')}")
+    return step_s, desc, legs_us, arm.threads
 
 
 def run_reference_arm(args):
-    """--impl reference: the reference's CPU path on this box's host cores."""
+    """--impl reference: the reference CPU path of the bench workload on this box's host
+    cores, WHOLE decode steps (W warm-up + K timed), loading only oracle/ (the
+    unmodified reference in oracle/_ref + the oracle/cpu_port.c expert port)."""
     rank = int(os.environ.get("RANK", "0"))
     if rank != 0:
         return
-    ps, spec, gen = make_workload(args)
-    threads = os.cpu_count() or 1
-    L = spec.num_layers
+    import oracle as orc
+    if not orc.ref_available():
+        print(json.dumps({"impl": "reference", "unavailable": "oracle/_ref/libprescope_ref.so not built"}))
+        return
+    from oracle.cpu_arm import RefArm
+    t_init = time.perf_counter()
+    arm = RefArm(args.model, args.batch, args.budget, steps=args.warmup + args.steps, weight_seed=args.weight_seed)
+    t_init = time.perf_counter() - t_init
+    phases = {}
     times = []
-    desc = ""
-    for i in range(args.warmup + args.steps):
-        s, desc = cpu_sample(args, spec, gen, threads)
-        if i >= args.warmup:
-            times.append(s)
-    step_s = statistics.mean(times)
+    wall0 = time.perf_counter()
+    for s in range(args.warmup + args.steps):
+        sec, ph, _ = arm.step(s)
+        if s >= args.warmup:
+            times.append(sec)
+            for k, v in ph.items():
+                phases[k] = phases.get(k, 0.0) + v / args.steps
+    wall = time.perf_counter() - wall0
+    legs = arm.legs_1core()
+    threads = arm.threads
+    L = arm.L
+    arm.close()
+    step_s = sum(times) / len(times)
     value = args.batch / step_s
+    desc = (f"whole B={args.batch} decode steps ({args.steps} timed after {args.warmup} warm-up, no extrapolation): "
+            f"reference router + LLaPor P=256/512 + simulate_policy(presched) via oracle/_ref, experts+combine via "
+            f"oracle/cpu_port.c on all {L} layers, {threads} host threads")
+    cfg = {"workload": f"{args.model}-shape MoE decode, {L} layers, batch {args.batch}, budget {args.budget:.0%}: "
+                       "the reference's CPU path (oracle/_ref) + CPU expert port",
+           "decode_batch": args.batch, "global_batch": args.batch, "budget_fraction": args.budget}
     line = {"impl": "reference", "metric": METRIC, "value": value, "unit": "tokens/s", "n_gpus": args.gpus,
             "steps": args.steps, "warmup": args.warmup, "ms_per_step": step_s * 1e3, "higher_is_better": True,
-            "scaling": "weak", "vs_baseline": None, "dtype": "bf16 weights, f64 accumulate", "data": "synthetic",
-            "config": workload_config(args, spec, "host_lane" if default_host_threads() > 0 else "gpu_only"),
-            "moe_layer_us": step_s / L * 1e6,
-            "cpu_baseline": {"value": value, "unit": "tokens/s", "cores": threads, "kind": "port", "sample": desc},
-            "e2e": {"value": value, "unit": "tokens/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0}}
+            "scaling": "weak", "vs_baseline": None, "dtype": "bf16 weights, f32/f64 accumulate",
+            "data": "synthetic (reference generate_trace, hash-init bf16 weights, random-init LLaPor)",
+            "config": cfg, "moe_layer_us": step_s / L * 1e6,
+            "phases_ms_per_step": {k: round(v * 1e3, 3) for k, v in phases.items() if k != "makespan_ticks"},
+            "cpu_baseline": {"value": value, "unit": "tokens/s", "cores": threads, "kind": "reference",
+                             "sample": desc, "host": host_info(),
+                             "legs_1core_us": {k: round(v[0], 3) for k, v in legs.items()}},
+            "e2e": {"value": value, "unit": "tokens/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
+            "consistency": {"timed_s": sum(times), "wall_s_steps": wall, "init_s": t_init,
+                            "fits_in_driver_run": True}}
     print(json.dumps(line))
 
 
@@ -324,6 +348,13 @@ def run_ours(args):
     h2d_in = hid_lm[0].numel() * 4 + fol_lm[0].numel()
     d2h_out = y_h.numel() * 4 + ids_h.numel() * 4
     e.close()
+    # In-bench checksum (outside every timed region): the last e2e step's outputs vs the
+    # CPU oracle — ids of all layers vs the f64 reference router, y of two layers vs the
+    # oracle SwiGLU/combine on the same bf16 weights (tests/ hold the full parity suite).
+    checksum = None
+    if rank == 0 and not args.no_checksum:
+        checksum = step_checksum(args, spec, gate, hidden[(S - 1) * B:S * B], follow[(S - 1) * B:S * B],
+                                 zipf, y_h.numpy(), ids_h.numpy())
 
     # Same steps with every expert resident (budget 100 %): the HBM-bound MoE layer.
     all_res = None
@@ -409,8 +440,8 @@ def run_ours(args):
     leg_summary = {name: decode_summary(lst, lms, N, B, L) for name, (lst, lms, _, _) in legs.items()}
     if "cpu_lane" in leg_summary.get("host_lane", {}):
         leg_summary["host_lane"]["cpu_lane"]["threads"] = host_threads
-    threads = os.cpu_count() or 1
-    cpu_step_s, cpu_desc = cpu_sample(args, spec, gen, threads) if not args.no_cpu_baseline else (None, "skipped")
+    cpu_step_s, cpu_desc, cpu_legs, cpu_threads = (cpu_sample(args) if not args.no_cpu_baseline
+                                                   else (None, "skipped", None, 0))
     line = {
         "metric": METRIC, "value": value, "unit": "tokens/s", "n_gpus": N, "steps": args.steps,
         "warmup": args.warmup, "ms_per_step": dev_ms, "higher_is_better": True, "scaling": "weak",
@@ -428,18 +459,56 @@ def run_ours(args):
         "executor": head,
         "host_lane": leg_summary.get("host_lane"),
         "gpu_only": leg_summary["gpu_only"],
-        "cpu_baseline": ({"value": args.batch / cpu_step_s, "unit": "tokens/s", "cores": threads, "kind": "port",
-                          "sample": cpu_desc} if cpu_step_s else None),
+        "cpu_baseline": ({"value": args.batch / cpu_step_s, "unit": "tokens/s", "cores": cpu_threads,
+                          "kind": "reference", "sample": cpu_desc, "host": host_info(),
+                          "legs_1core_us": cpu_legs} if cpu_step_s else None),
+        "checksum": checksum,
         "all_resident": all_res,
         "prefill": prefill,
         "clocks": clocks,
         "gpu_launches": st["kernel_launches"],
+        "nccl_init": nccl_init_lines() if world > 1 else None,
         "wall_s_timed": wall, "engine_create_s": t_create,
         "cost_params_us": st["cost"],
     }
     print(json.dumps(line))
     if dist:
         dist.destroy_process_group()
+
+
+def nccl_init_lines(limit=6):
+    """This process's NCCL INIT debug lines (NCCL_DEBUG_FILE set in main): communicator
+    size, rank and transport as NCCL reports them."""
+    import glob
+    import socket
+    pat = os.environ.get("NCCL_DEBUG_FILE", "").replace("%h", socket.gethostname()).replace("%p", str(os.getpid()))
+    lines = []
+    for path in glob.glob(pat) if pat else []:
+        for ln in open(path, errors="replace"):
+            if "Init COMPLETE" in ln or "nRanks" in ln or "comm 0x" in ln:
+                lines.append(ln.strip())
+    return lines[:limit]
+
+
+def step_checksum(args, spec, gate, hidden, follow, zipf, y, ids, layers=None):
+    import oracle as orc
+    L, E, H, k = spec.num_layers, spec.experts_per_layer, spec.hidden_dim, spec.top_k
+    F = spec.expert_bytes // (6 * H)
+    layers = layers or [0, L - 1]
+    _, ref_w, ref_ids = orc.or_route_trace(gate, hidden, follow, zipf, k)
+    ids_ok = bool(np.array_equal(ids, ref_ids.transpose(1, 0, 2)))
+    rel = []
+    for l in layers:
+        used = sorted(set(int(x) for x in np.unique(ids[l])))
+        slabs = orc.bl_init_slabs([(l, x) for x in used], H, F, args.weight_seed)
+        by_e = dict(zip(used, slabs))
+        x = orc.f32_to_bf16(hidden[:, l].astype(np.float32))
+        y_ref = orc.or_moe_layer([by_e.get(x_) for x_ in range(E)], H, F, x, ids[l],
+                                 ref_w[:, l].astype(np.float32), True, os.cpu_count() or 1)
+        rel.append(float(np.linalg.norm(y[l] - y_ref) / np.linalg.norm(y_ref)))
+    return {"tokens": int(hidden.shape[0]), "ids_match_reference_router": ids_ok, "layers": layers,
+            "y_rel_err_vs_oracle": rel, "tolerance": 2e-2, "ok": ids_ok and max(rel) < 2e-2,
+            "source": "last e2e step (ps_engine_decode_step_host) vs oracle/or_route_trace + or_moe_layer"}
 
 
 def default_host_threads():
@@ -504,6 +573,7 @@ def main():
     ap.add_argument("--weight-seed", type=int, default=1)
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--no-all-resident", action="store_true")
+    ap.add_argument("--no-checksum", action="store_true")
     ap.add_argument("--prefill-tokens", type=int, default=4096)
     ap.add_argument("--prefill-steps", type=int, default=5)
     ap.add_argument("--predictor", default="llapor", choices=["llapor", "gate", "perfect", "none"],
@@ -513,6 +583,25 @@ def main():
     ap.add_argument("--host-threads", type=int, default=-1,
                     help="host expert lane threads (-1 auto, 0 = GPU-only executor)")
     args = ap.parse_args()
+    if args.gpus > 1 and "WORLD_SIZE" not in os.environ:
+        # One process per GPU: relaunch under torchrun (the driver does this itself).
+        import socket
+        with socket.socket() as sk:
+            sk.bind(("127.0.0.1", 0))
+            port = sk.getsockname()[1]
+        cmd = [sys.executable, "-m", "torch.distributed.run", "--nnodes=1", f"--nproc-per-node={args.gpus}",
+               "--master-addr", "127.0.0.1", "--master-port", str(port), str(pathlib.Path(__file__).resolve()),
+               *sys.argv[1:]]
+        sys.exit(subprocess.call(cmd))
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    if world != args.gpus:
+        raise SystemExit(f"bench.py: WORLD_SIZE={world} but --gpus {args.gpus}")
+    if world > 1 and args.impl == "ours":
+        # NCCL init lines (communicator size/ranks) go to a per-process file; rank 0
+        # copies its own into the JSON line (stdout carries only the JSON line).
+        os.environ.setdefault("NCCL_DEBUG", "INFO")
+        os.environ.setdefault("NCCL_DEBUG_SUBSYS", "INIT")
+        os.environ.setdefault("NCCL_DEBUG_FILE", "/tmp/ps_bench_nccl.%h.%p.log")
     if args.impl == "reference":
         run_reference_arm(args)
     else:

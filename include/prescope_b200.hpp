@@ -470,6 +470,37 @@ inline std::vector<std::string> verify_timeline(const Timeline& timeline, const 
   return out;
 }
 
+struct Metrics {
+  std::vector<Ticks> per_layer_latency;
+  std::vector<Ticks> cpu_gpu_gap;
+  Ticks makespan = 0;
+  Ticks decode_latency = 0;
+  double throughput_tokens_per_s = 0.0;
+  double io_busy_fraction = 0.0;
+  double gpu_idle_fraction = 0.0;
+};
+
+inline Metrics compute_metrics(const Timeline& timeline, int output_tokens) {
+  std::vector<ps_timeline_event> ev;
+  for (const TimelineEvent& e : timeline.events)
+    ev.push_back({e.t_start, e.t_end, static_cast<int32_t>(e.resource), static_cast<int32_t>(e.kind), e.layer,
+                  e.expert, e.tokens});
+  const int L = static_cast<int>(timeline.layer_start.size());
+  Metrics m;
+  m.per_layer_latency.resize(L);
+  m.cpu_gpu_gap.resize(L);
+  ps_metrics c{};
+  ps_throw_if(ps_compute_metrics(ev.data(), static_cast<int>(ev.size()), timeline.layer_start.data(),
+                                 timeline.layer_end.data(), L, timeline.makespan, output_tokens, &c,
+                                 m.per_layer_latency.data(), m.cpu_gpu_gap.data()));
+  m.makespan = c.makespan;
+  m.decode_latency = c.decode_latency;
+  m.throughput_tokens_per_s = c.throughput_tokens_per_s;
+  m.io_busy_fraction = c.io_busy_fraction;
+  m.gpu_idle_fraction = c.gpu_idle_fraction;
+  return m;
+}
+
 // -------------------------------------------------------------- predictor.hpp:145-157
 inline std::vector<std::pair<int, int>> plan_residency_from_freq(const std::vector<std::vector<long>>& freq,
                                                                  std::uint64_t budget_bytes,

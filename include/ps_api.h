@@ -250,15 +250,18 @@ ps_status ps_verify_timeline_ex(const ps_timeline_event* events, int n_events,
  * reference). *needed = bytes incl. NUL; buf (nullable) receives at most cap-1 chars. */
 ps_status ps_export_timeline(const ps_timeline_event* events, int n, int64_t makespan, char* buf,
                              int cap, int* needed);
-/* compute_metrics (simulator.cpp:396-426). per_layer arrays nullable [L]. */
+/* compute_metrics (simulator.cpp:396-426) of a Timeline {events, layer_start/end [L],
+ * makespan}: makespan is the timeline's own field, as the reference reads it
+ * (simulate_pipeline sets it to max t_end, simulator.cpp:239-240). per_layer arrays
+ * nullable [L]. An event layer outside [0, L) -> PS_ERANGE (out_of_range). */
 typedef struct {
   int64_t makespan, decode_latency;
   double throughput_tokens_per_s, io_busy_fraction, gpu_idle_fraction;
 } ps_metrics;
 ps_status ps_compute_metrics(const ps_timeline_event* events, int n_events,
                              const int64_t* layer_start, const int64_t* layer_end, int L,
-                             int output_tokens, ps_metrics* out, int64_t* per_layer_latency,
-                             int64_t* cpu_gpu_gap);
+                             int64_t makespan, int output_tokens, ps_metrics* out,
+                             int64_t* per_layer_latency, int64_t* cpu_gpu_gap);
 
 /* ------------------------------------------------------------------ hot table / HBM budget
  * build_hot_table + plan_residency (predictor.cpp:405-433). freq [L*E]. */
@@ -467,6 +470,11 @@ ps_status ps_ep_recv_plan(const int32_t* recv_counts, int world, int E_loc, int3
 ps_status ps_ep_unique_id(char* out, int cap); /* 128 bytes, broadcast by the caller */
 ps_status ps_ep_comm_create(const char* unique_id, int rank, int world, int device, ps_ep_comm* out);
 ps_status ps_ep_comm_destroy(ps_ep_comm c);
+/* In-process transport with the same all-to-all contract: `world` communicators for
+ * `world` host threads of ONE process (one engine per thread, any devices). Lets the
+ * expert-parallel engine run at G > 1 on a single GPU (tests). No reference
+ * counterpart (the reference has no multi-GPU code). */
+ps_status ps_ep_loopback_create(int world, int device, ps_ep_comm* comms_out /* [world] */);
 int ps_ep_comm_rank(ps_ep_comm c);
 int ps_ep_comm_world(ps_ep_comm c);
 /* Segmented all-to-all: segment p of `send` (send_bytes[p]) goes to rank p, segment p

@@ -155,6 +155,8 @@ def ref_lib() -> C.CDLL:
         _ref.ref_spec_preset.argtypes = [C.c_char_p, C.POINTER(RefSpec)]
         _ref.ref_desk_scale.argtypes = [C.c_char_p, C.c_int, C.c_int, C.c_int, C.POINTER(RefSpec)]
         _ref.ref_topk.argtypes = [C.c_void_p, C.c_int, C.c_int, C.c_void_p, C.POINTER(C.c_int)]
+        _ref.ref_compute_metrics.argtypes = [C.c_void_p, C.c_int, C.c_void_p, C.c_void_p, C.c_int, C.c_int64,
+                                             C.c_int, C.c_void_p, C.c_void_p, C.c_void_p]
         _ref.ref_router_inputs.argtypes = [C.POINTER(RefGen), C.POINTER(RefSpec), C.c_int, C.c_uint64, C.c_void_p,
                                            C.c_void_p, C.c_void_p]
         _ref.ref_llapor_predict_batch.argtypes = [C.c_void_p, C.c_int, C.c_int, C.c_void_p, C.c_void_p, C.c_int,
@@ -375,6 +377,18 @@ def ref_simulate(truth, predicted, params, policy="presched", resident=None, gro
               for i in range(n.value)]
     return 0, {"events": events, "layer_start": list(map(int, ls)), "layer_end": list(map(int, le)),
                "makespan": mk.value, "plans": [tuple(map(int, summ[4 * i:4 * i + 4])) for i in range(L)]}
+
+
+def ref_compute_metrics(events, layer_start, layer_end, makespan, output_tokens):
+    """Reference compute_metrics -> (scalars (makespan, decode_latency, throughput,
+    io_busy, gpu_idle), per_layer_latency [L], cpu_gpu_gap [L])."""
+    L = len(layer_start)
+    ev = (RefEvent * max(1, len(events)))(*[RefEvent(*e) for e in events])
+    ls, le = np.ascontiguousarray(layer_start, np.int64), np.ascontiguousarray(layer_end, np.int64)
+    sc, pl, gap = np.empty(5), np.empty(L, np.int64), np.empty(L, np.int64)
+    ref_check(ref_lib().ref_compute_metrics(ev, len(events), ls.ctypes.data, le.ctypes.data, L, makespan,
+                                            output_tokens, sc.ctypes.data, pl.ctypes.data, gap.ctypes.data))
+    return sc, pl, gap
 
 
 def ref_verify(events, truth, params, resident=None):

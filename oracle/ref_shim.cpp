@@ -715,4 +715,31 @@ int ref_router_inputs(const ref_gen* gen, const ref_spec* spec, int batch, uint6
   });
 }
 
+// compute_metrics (simulator.cpp:396-426) on a caller-supplied Timeline. out_scalars:
+// makespan, decode_latency, throughput, io_busy_fraction, gpu_idle_fraction.
+int ref_compute_metrics(const ref_event* events, int n_events, const int64_t* layer_start,
+                        const int64_t* layer_end, int L, int64_t makespan, int output_tokens,
+                        double* out_scalars, int64_t* per_layer, int64_t* gap) {
+  return guarded([&] {
+    Timeline t;
+    for (int i = 0; i < n_events; ++i)
+      t.events.push_back({events[i].t_start, events[i].t_end, static_cast<Resource>(events[i].resource),
+                          static_cast<EventKind>(events[i].kind), events[i].layer, events[i].expert,
+                          events[i].tokens});
+    t.layer_start.assign(layer_start, layer_start + L);
+    t.layer_end.assign(layer_end, layer_end + L);
+    t.makespan = makespan;
+    Metrics m = compute_metrics(t, output_tokens);
+    out_scalars[0] = static_cast<double>(m.makespan);
+    out_scalars[1] = static_cast<double>(m.decode_latency);
+    out_scalars[2] = m.throughput_tokens_per_s;
+    out_scalars[3] = m.io_busy_fraction;
+    out_scalars[4] = m.gpu_idle_fraction;
+    for (int l = 0; l < L; ++l) {
+      per_layer[l] = m.per_layer_latency[l];
+      gap[l] = m.cpu_gpu_gap[l];
+    }
+  });
+}
+
 }  // extern "C"

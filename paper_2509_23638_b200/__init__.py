@@ -16,7 +16,7 @@ from . import capi
 from .capi import check, load
 
 __all__ = ["capi", "load", "check", "spec_preset", "desk_scale", "ffn_dim", "trace_inputs", "plan_layer",
-           "parse_policy", "simulate", "verify_timeline", "plan_residency", "Plan", "TraceGenConfig",
+           "parse_policy", "simulate", "verify_timeline", "compute_metrics", "plan_residency", "Plan", "TraceGenConfig",
            "GROUP_DEFAULT_GEN", "Trace", "read_trace", "write_trace"]
 
 # Default generator knobs of the benchmark workloads:
@@ -222,6 +222,21 @@ def verify_timeline(events, truth, params, resident=None):
     msgs = [m for m in buf.value.decode().split("\n") if m]
     assert len(msgs) == n.value or len(buf.value) >= len(buf) - 1
     return msgs
+
+
+def compute_metrics(events, layer_start, layer_end, makespan, output_tokens):
+    """compute_metrics (simulator.cpp:396-426) via ps_compute_metrics -> (ps_metrics,
+    per_layer_latency [L], cpu_gpu_gap [L]). events: (t_start, t_end, resource, kind,
+    layer, expert, tokens) tuples; makespan: the timeline's own field."""
+    L = len(layer_start)
+    arr = (capi.TimelineEvent * max(1, len(events)))(*[capi.TimelineEvent(*e) for e in events])
+    ls, le = np.ascontiguousarray(layer_start, np.int64), np.ascontiguousarray(layer_end, np.int64)
+    m = capi.Metrics()
+    pl, gap = np.empty(L, np.int64), np.empty(L, np.int64)
+    check(load().ps_compute_metrics(arr, len(events), ls.ctypes.data_as(C.c_void_p), le.ctypes.data_as(C.c_void_p),
+                                    L, int(makespan), int(output_tokens), C.byref(m), pl.ctypes.data_as(C.c_void_p),
+                                    gap.ctypes.data_as(C.c_void_p)))
+    return m, pl, gap
 
 
 def plan_residency(freq, budget_bytes: int, expert_bytes: int):

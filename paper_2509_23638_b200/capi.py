@@ -163,7 +163,7 @@ _SIGS = {
                                        C.POINTER(SimOptions), C.POINTER(Timeline)]),
     "ps_verify_timeline": (C.c_int, [C.POINTER(TimelineEvent), C.c_int, C.POINTER(PipelineInstance),
                                      C.POINTER(CostParams), C.POINTER(C.c_int), C.c_char_p, C.c_int]),
-    "ps_compute_metrics": (C.c_int, [C.POINTER(TimelineEvent), C.c_int, _P, _P, C.c_int, C.c_int,
+    "ps_compute_metrics": (C.c_int, [C.POINTER(TimelineEvent), C.c_int, _P, _P, C.c_int, C.c_int64, C.c_int,
                                      C.POINTER(Metrics), _P, _P]),
     "ps_plan_residency": (C.c_int, [_P, C.c_int, C.c_int, C.c_uint64, C.c_uint64, _P, C.POINTER(C.c_int)]),
     "ps_route_topk": (C.c_int, [_P, _P, _P, _P, _P, C.c_int, C.c_int, C.c_int, C.c_int, C.c_int,
@@ -222,6 +222,7 @@ _SIGS = {
     "ps_ep_unique_id": (C.c_int, [C.c_char_p, C.c_int]),
     "ps_ep_comm_create": (C.c_int, [C.c_char_p, C.c_int, C.c_int, C.c_int, C.POINTER(C.c_void_p)]),
     "ps_ep_comm_destroy": (C.c_int, [_P]),
+    "ps_ep_loopback_create": (C.c_int, [C.c_int, C.c_int, C.POINTER(C.c_void_p)]),
     "ps_ep_comm_rank": (C.c_int, [_P]),
     "ps_ep_comm_world": (C.c_int, [_P]),
     "ps_ep_all_to_all": (C.c_int, [_P, _P, _P, _P, _P, _P]),

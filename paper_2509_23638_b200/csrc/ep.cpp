@@ -13,6 +13,8 @@
 #include <nccl.h>
 
 #include <algorithm>
+#include <chrono>
+#include <condition_variable>
 #include <cstring>
 #include <memory>
 #include <mutex>
@@ -68,13 +70,118 @@ void nccl_check(ncclResult_t r, const char* what) {
   }
 }
 
+// In-process transport: `world` ranks of one process, one host thread per rank (each
+// driving its own engine and streams, on any devices). Same contract as the NCCL
+// grouped send/recv all-to-all — stream-ordered on every rank's stream, per-peer byte
+// counts, source/destination-major segments — built from CUDA events and peer copies:
+//   1. each rank records `ready` on its stream (its send buffer is written) and posts
+//      its buffers; host barrier;
+//   2. each rank waits on every peer's `ready`, copies the peer's segment for it into
+//      its own receive buffer on its own stream, records `done`; host barrier;
+//   3. each rank's stream waits on every peer's `done`, so nothing later on a rank's
+//      stream (the next write of its send buffer) overtakes a peer still reading it.
+// One process can thus run the real EP engine at G = 2/4/8 on one GPU (tests), with
+// exactly the engine code that runs over NCCL across GPUs.
+struct LoopGroup {
+  explicit LoopGroup(int w) : world(w), posts(w) {}
+  struct Post {
+    const char* send = nullptr;
+    char* recv = nullptr;
+    std::vector<uint64_t> sb, rb;
+    cudaStream_t stream = nullptr;
+    cudaEvent_t ready = nullptr, done = nullptr;
+    int device = 0;
+  };
+  int world;
+  std::vector<Post> posts;
+  std::mutex mu;
+  std::condition_variable cv;
+  int arrived = 0;
+  uint64_t gen = 0;
+  bool broken = false;
+  void barrier() {
+    std::unique_lock<std::mutex> g(mu);
+    const uint64_t my = gen;
+    if (++arrived == world) {
+      arrived = 0;
+      ++gen;
+      cv.notify_all();
+      return;
+    }
+    // A rank that failed outside the collective never arrives: time out instead of
+    // hanging every peer (NCCL would block the same way; tests want an error).
+    if (!cv.wait_for(g, std::chrono::seconds(300), [&] { return gen != my || broken; })) {
+      broken = true;
+      cv.notify_all();
+    }
+    if (broken) fail(PS_ENCCL, "loopback all-to-all: a peer rank failed or never arrived");
+  }
+  void abort() {
+    std::lock_guard<std::mutex> g(mu);
+    broken = true;
+    cv.notify_all();
+  }
+};
+
 }  // namespace
 }  // namespace ps
 
 struct ps_ep_comm_s {
   ncclComm_t comm = nullptr;
   int rank = 0, world = 1;
+  std::shared_ptr<ps::LoopGroup> loop;  // in-process transport (ps_ep_loopback_create)
+  cudaEvent_t ready = nullptr, done = nullptr;
 };
+
+namespace ps {
+namespace {
+
+void loop_all_to_all(ps_ep_comm_s* c, const void* send, const uint64_t* send_bytes, void* recv,
+                     const uint64_t* recv_bytes, cudaStream_t s) {
+  LoopGroup& g = *c->loop;
+  const int W = g.world, r = c->rank;
+  int dev = 0;
+  PS_CUDA(cudaGetDevice(&dev));
+  try {
+    PS_CUDA(cudaEventRecord(c->ready, s));
+    LoopGroup::Post& me = g.posts[r];
+    me.send = static_cast<const char*>(send);
+    me.recv = static_cast<char*>(recv);
+    me.sb.assign(send_bytes, send_bytes + W);
+    me.rb.assign(recv_bytes, recv_bytes + W);
+    me.stream = s;
+    me.ready = c->ready;
+    me.done = c->done;
+    me.device = dev;
+    g.barrier();  // every rank posted
+    uint64_t ro = 0;
+    for (int p = 0; p < W; ++p) {
+      const LoopGroup::Post& peer = g.posts[p];
+      uint64_t so = 0;
+      for (int q = 0; q < r; ++q) so += peer.sb[q];
+      require(peer.sb[r] == me.rb[p], "loopback all-to-all: send/recv byte counts disagree");
+      if (me.rb[p]) {
+        if (p != r) PS_CUDA(cudaStreamWaitEvent(s, peer.ready, 0));
+        if (peer.device == dev)
+          PS_CUDA(cudaMemcpyAsync(me.recv + ro, peer.send + so, me.rb[p], cudaMemcpyDeviceToDevice, s));
+        else
+          PS_CUDA(cudaMemcpyPeerAsync(me.recv + ro, dev, peer.send + so, peer.device, me.rb[p], s));
+      }
+      ro += me.rb[p];
+    }
+    PS_CUDA(cudaEventRecord(c->done, s));
+    g.barrier();  // every rank's copies are enqueued
+    for (int p = 0; p < W; ++p)
+      if (p != r) PS_CUDA(cudaStreamWaitEvent(s, g.posts[p].done, 0));
+    g.barrier();  // nobody re-posts (overwrites its entry) before every peer read it
+  } catch (...) {
+    g.abort();
+    throw;
+  }
+}
+
+}  // namespace
+}  // namespace ps
 
 using namespace ps;
 
@@ -143,10 +250,31 @@ ps_status ps_ep_comm_create(const char* unique_id, int rank, int world, int devi
   });
 }
 
+ps_status ps_ep_loopback_create(int world, int device, ps_ep_comm* comms) {
+  return guarded([&] {
+    require(world >= 1 && world <= 64 && comms, "ps_ep_loopback_create: bad world");
+    PS_CUDA(cudaSetDevice(device));
+    auto group = std::make_shared<LoopGroup>(world);
+    std::vector<std::unique_ptr<ps_ep_comm_s>> out;
+    for (int r = 0; r < world; ++r) {
+      auto c = std::make_unique<ps_ep_comm_s>();
+      c->rank = r;
+      c->world = world;
+      c->loop = group;
+      PS_CUDA(cudaEventCreateWithFlags(&c->ready, cudaEventDisableTiming));
+      PS_CUDA(cudaEventCreateWithFlags(&c->done, cudaEventDisableTiming));
+      out.push_back(std::move(c));
+    }
+    for (int r = 0; r < world; ++r) comms[r] = out[r].release();
+  });
+}
+
 ps_status ps_ep_comm_destroy(ps_ep_comm c) {
   return guarded([&] {
     if (!c) return;
     if (c->comm) nccl().CommDestroy(c->comm);
+    if (c->ready) cudaEventDestroy(c->ready);
+    if (c->done) cudaEventDestroy(c->done);
     delete c;
   });
 }
@@ -157,8 +285,12 @@ ps_status ps_ep_all_to_all(ps_ep_comm c, const void* send, const uint64_t* send_
                            const uint64_t* recv_bytes, void* stream) {
   return guarded([&] {
     require(c != nullptr, "ps_ep_all_to_all: null communicator");
-    const NcclApi& api = nccl();
     cudaStream_t s = as_stream(stream);
+    if (c->loop) {
+      loop_all_to_all(c, send, send_bytes, recv, recv_bytes, s);
+      return;
+    }
+    const NcclApi& api = nccl();
     uint64_t so = 0, ro = 0;
     nccl_check(api.GroupStart(), "ncclGroupStart");
     for (int p = 0; p < c->world; ++p) {

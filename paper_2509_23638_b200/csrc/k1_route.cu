@@ -8,7 +8,7 @@
 //
 // Top-k ranks the fp32 softmax WEIGHTS with the reference's tie-break (value desc,
 // lower index first), exactly what topk_indices does on the same numbers, so the
-// returned ids are bit-exact against topk_indices(weights) (tests/test_gpu_route.py).
+// returned ids are bit-exact against topk_indices(weights) (tests/test_gpu_ops.py::test_route_topk_parity).
 #include "device_common.cuh"
 #include "permute_device.cuh"
 

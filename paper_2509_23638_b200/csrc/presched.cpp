@@ -6,7 +6,7 @@
 // (O((n+n')^2), 551 us at n=n'=256); here each list is scanned once after one stable
 // sort, O((n+n') log(n+n')). All tick arithmetic is int64 and every double is formed
 // with the reference's operand order (compiled with -ffp-contract=off), so plans,
-// sweeps, f and xi are bit-identical (tests/test_presched.py).
+// sweeps, f and xi are bit-identical (tests/test_host_parity.py: test_presched_product_vs_reference_random_large, test_cost_model_kats).
 #include <algorithm>
 #include <cmath>
 #include <cstring>

@@ -5,7 +5,7 @@
 //
 // Dense (layer, expert) tables replace the reference's std::map/std::set state; the
 // event insertion order is kept identical so the final stable sort by (resource,
-// t_start, t_end) yields the same timeline (golden replays in tests/test_simulate.py).
+// t_start, t_end) yields the same timeline (golden replays in tests/test_host_parity.py).
 #include <algorithm>
 #include <cmath>
 #include <cstring>
@@ -393,11 +393,16 @@ ps_status ps_export_timeline(const ps_timeline_event* events, int n, int64_t mak
 }
 
 ps_status ps_compute_metrics(const ps_timeline_event* events, int n, const int64_t* layer_start,
-                             const int64_t* layer_end, int L, int output_tokens, ps_metrics* m,
+                             const int64_t* layer_end, int L, int64_t makespan, int output_tokens, ps_metrics* m,
                              int64_t* per_layer_latency, int64_t* cpu_gpu_gap) {
   return guarded([&] {
-    int64_t makespan = 0;
-    for (int i = 0; i < n; ++i) makespan = std::max(makespan, events[i].t_end);
+    require(n >= 0 && L >= 0 && m && (n == 0 || events) && (L == 0 || (layer_start && layer_end)),
+            "compute_metrics: null argument");
+    // The reference indexes per-layer arrays with event.layer (simulator.cpp:410-414);
+    // an event outside [0, L) is an index error here instead of undefined behaviour.
+    for (int i = 0; i < n; ++i)
+      if (events[i].layer < 0 || events[i].layer >= L)
+        fail(PS_ERANGE, "compute_metrics: event layer " + std::to_string(events[i].layer) + " out of range");
     *m = ps_metrics{};
     m->makespan = m->decode_latency = makespan;
     if (makespan > 0) m->throughput_tokens_per_s = output_tokens * 1e6 / static_cast<double>(makespan);
@@ -407,7 +412,6 @@ ps_status ps_compute_metrics(const ps_timeline_event* events, int n, const int64
       const auto& e = events[i];
       if (e.resource == PS_RES_IO) io_busy += e.t_end - e.t_start;
       if (e.resource == PS_RES_GPU) gpu_busy += e.t_end - e.t_start;
-      if (e.layer < 0 || e.layer >= L) continue;
       if (e.kind == PS_EV_ATTENTION) attn_end[e.layer] = e.t_end;
       if (e.kind == PS_EV_CPU_EXPERT) cpu_fin[e.layer] = std::max(cpu_fin[e.layer], e.t_end);
       if (e.kind == PS_EV_GPU_EXPERT) gpu_fin[e.layer] = std::max(gpu_fin[e.layer], e.t_end);

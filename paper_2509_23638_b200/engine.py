@@ -83,6 +83,20 @@ class EpComm:
         check(load().ps_ep_comm_create(uid, rank, world, device, C.byref(self.h)))
         self.rank, self.world = rank, world
 
+    @classmethod
+    def loopback(cls, world: int, device: int = 0):
+        """`world` communicators of the in-process transport (ps_ep_loopback_create), one
+        per host thread of this process: the EP engine at G > 1 on one GPU."""
+        arr = (C.c_void_p * world)()
+        check(load().ps_ep_loopback_create(world, device, arr))
+        out = []
+        for r in range(world):
+            c = cls.__new__(cls)
+            c.h = C.c_void_p(arr[r])
+            c.rank, c.world = r, world
+            out.append(c)
+        return out
+
     def owned(self, E: int):
         return [e for e in range(E) if e % self.world == self.rank]
 

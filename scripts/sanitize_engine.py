@@ -34,7 +34,35 @@ def main():
     run("mixtral", 3, 8, 256, 512, 256, 0.5)
     run("mixtral", 3, 8, 256, 512, 8, 0.25, compress_host=True)
     run("mixtral", 3, 8, 256, 512, 256, 0.5, compress_host=True)
+    lib = ps.load()
+    for kern, name in ((0, "single-CTA"), (1, "CTA-pair")):  # both tcgen05 prefill kernels explicitly
+        ps.check(lib.ps_set_prefill_kernel(kern))
+        print("prefill kernel", name)
+        run("mixtral", 2, 8, 256, 512, 512, 1.0)
+        run("deepseek", 2, 16, 256, 256, 512, 1.0, n_shared=2)
+    ps.check(lib.ps_set_prefill_kernel(2))
+    ep_loopback(2)
     print("sanitize run done")
+
+
+def ep_loopback(G):
+    """The EP engine over the in-process transport (G ranks, one thread each)."""
+    from concurrent.futures import ThreadPoolExecutor
+    spec = ps.desk_scale("mixtral", 2, 8, 256)
+    spec.expert_bytes = 6 * 256 * 512
+    gen = ps.TraceGenConfig(*[ps.GROUP_DEFAULT_GEN[g] for g in ("input", "middle", "output")])
+    B = 8
+    gate, hidden, follow, _ = ps.trace_inputs(gen, spec, B * G, 3)
+    comms = eng.EpComm.loopback(G)
+    es = [eng.Engine(spec, gen, max_batch=B, weight_seed=9, gate=gate, budget_bytes=spec.expert_bytes * 2,
+                     resident=[(0, r)], ep=comms[r]) for r in range(G)]
+    with ThreadPoolExecutor(G) as pool:
+        list(pool.map(lambda r: es[r].step_host(hidden[r * B:(r + 1) * B], follow[r * B:(r + 1) * B]), range(G)))
+    for e in es:
+        e.close()
+    for c in comms:
+        c.close()
+    print("ep loopback", G)
 
 
 if __name__ == "__main__":

@@ -89,6 +89,9 @@ int main() {
   CHECK(r.timeline.makespan == 53);
   CHECK(verify_timeline(r.timeline, inst, p).empty());
   CHECK(simulate_policy(inst, SchedulerPolicy::parse("ondemand"), p).timeline.makespan == 80);
+  Metrics met = compute_metrics(r.timeline, 1);  // simulator.cpp:396-426
+  CHECK(met.makespan == 53 && met.decode_latency == 53 && met.per_layer_latency.size() == 2);
+  CHECK(met.io_busy_fraction > 0.0 && met.gpu_idle_fraction < 1.0);
   Timeline bad = r.timeline;
   bad.events.push_back({100, 102, Resource::Gpu, EventKind::GpuExpert, 0, 7, 1});
   CHECK(!verify_timeline(bad, inst, p).empty());

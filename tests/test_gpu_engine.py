@@ -108,6 +108,13 @@ def test_measured_timeline_satisfies_reference_invariants(torch_cuda, budget, po
         if budget < 1.0:
             assert 3 in kinds  # on-demand loads
         assert all(a <= b for a, b in zip(ls, le)) and all(le[i] <= ls[i + 1] for i in range(len(ls) - 1))
+        if orc.ref_available():  # compute_metrics of the measured timeline == the reference's
+            mk = max(ev[1] for ev in events)
+            m, pl, gap = ps.compute_metrics(events, ls, le, mk, 8)
+            sc, pl2, gap2 = orc.ref_compute_metrics(events, ls, le, mk, 8)
+            assert np.array_equal([m.makespan, m.decode_latency, m.throughput_tokens_per_s, m.io_busy_fraction,
+                                   m.gpu_idle_fraction], sc)
+            assert np.array_equal(pl, pl2) and np.array_equal(gap, gap2)
         cost = e.calibrate()
         assert cost["t_io"] > cost["t_g"] >= 0 and cost["t_attn"] > 0
 

@@ -264,3 +264,39 @@ def test_export_timeline_text_matches_reference():
             rbuf = C.create_string_buffer(rneed.value)
             orc.ref_check(orc.ref_lib().ref_export_timeline(rarr, len(ev), mk, rbuf, rneed.value, C.byref(rneed)))
             assert rbuf.value.decode() == text
+
+
+def _metrics_pair(events, ls, le, makespan, tokens):
+    m, pl, gap = ps.compute_metrics(events, ls, le, makespan, tokens)
+    mine = np.array([m.makespan, m.decode_latency, m.throughput_tokens_per_s, m.io_busy_fraction,
+                     m.gpu_idle_fraction])
+    return (mine, pl, gap), orc.ref_compute_metrics(events, ls, le, makespan, tokens)
+
+
+@pytest.mark.skipif(not orc.ref_available(), reason="oracle/_ref not built")
+def test_compute_metrics_matches_reference():
+    """ps_compute_metrics == the reference's compute_metrics (simulator.cpp:396-426),
+    bitwise, on every golden timeline, on the random pipelines under all four policies,
+    and on a Timeline whose makespan field is NOT max(t_end) (the reference reads the
+    field; so does ps_compute_metrics)."""
+    timelines = []
+    for s in json.loads((GOLDEN / "golden_scenarios.json").read_text()):
+        truth, pred, params = _golden_instance(s)
+        for pol in (s["policy"], "presched"):
+            timelines.append(ps.simulate(truth, pred, params, pol))
+    for c in json.loads((GOLDEN / "sim_cases.json").read_text())[:100]:
+        truth, pred, res = np.array(c["truth"]), np.array(c["predicted"]), np.array(c["resident"])
+        for pol in c["runs"]:
+            timelines.append(ps.simulate(truth, pred, tuple(c["params"]), pol, resident=res, groups=c["groups"],
+                                         options=(1, 64, 1.0, 32)))
+    for i, r in enumerate(timelines):
+        for makespan in (r["makespan"], r["makespan"] + 17):
+            (a, pl, gap), (b, pl2, gap2) = _metrics_pair(r["events"], r["layer_start"], r["layer_end"], makespan,
+                                                        1 + i % 7)
+            assert np.array_equal(a, b) and np.array_equal(pl, pl2) and np.array_equal(gap, gap2), i
+    # an event of a layer outside the timeline is an index error (the reference would read out of bounds)
+    r = timelines[0]
+    bad = list(r["events"]) + [(0, 1, 0, 1, len(r["layer_start"]), 0, 1)]
+    with pytest.raises(ps.capi.PsError) as err:
+        ps.compute_metrics(bad, r["layer_start"], r["layer_end"], r["makespan"], 1)
+    assert err.value.status == ps.capi.PS_ERANGE
