@@ -534,6 +534,12 @@ typedef struct {
                                feeds PreSched's e_next (0 = LLaPor when `predictor` is set) */
   const int32_t* stats_ranking; /* PS_PRED_STATS: [L*E] experts of each layer in hot-table
                                order (build_hot_table ranking, predictor.cpp:405-424) */
+  const uint16_t* const* expert_weights; /* nullable: the caller's expert slabs, host memory,
+                               [L*(E+n_shared)] pointers (index l*(E+n_shared)+e) to bf16
+                               [W_gate F*H | W_up F*H | W_down H*F] (expert_bytes each),
+                               copied at create (resident -> HBM, others -> the pinned
+                               host arena); null = hash-initialised from weight_seed.
+                               Under EP only owned experts are read. */
 } ps_engine_config;
 
 ps_status ps_engine_create(const ps_engine_config* cfg, ps_engine* out);
@@ -556,6 +562,29 @@ ps_status ps_engine_decode_step_routed(ps_engine e, const float* hidden, const i
 ps_status ps_engine_decode_step_host(ps_engine e, const float* hidden_host,
                                      const uint8_t* follow_host, int B, float* y_host,
                                      int32_t* ids_host);
+
+/* Per-layer K5 ABI — the reference's per-layer seam (plan_fn(inputs, l), simulator.cpp:136)
+ * for a host model that runs its own attention between MoE layers:
+ *
+ *   ps_engine_step_begin(e, B);                  // a new decode pass (R1-R3 state)
+ *   for (l = 0; l < L; ++l) {
+ *     attention(l, ..., stream);                 // caller's kernels -> x_l
+ *     ps_engine_layer_forward(e, l, x_l, follow_l, y_l, ids_l, stream);
+ *   }
+ *   ps_engine_step_end(e);                       // drain, measurement, timeline
+ *
+ * x_l [B,H] f32 device (router input = FFN input of layer l), follow_l [B] u8 device
+ * (kappa-follow flags, nullable), y_l [B,H] f32 device out, ids_l [B,k] i32 device out
+ * (nullable). `stream` (nullable): the caller's stream — the engine's compute stream
+ * waits for the caller's prior work on it, and it waits for y_l (CUDA events). Layers
+ * run in order 0..L-1; the host returns after the layer's work is enqueued (one host
+ * sync per layer on the routing, as in a whole step). Same kernels, plans and loads as
+ * ps_engine_decode_step: the outputs are bit-identical (tests/test_gpu_layer_api.py).
+ * PS_PRED_PERFECT is rejected (it needs layer l+1's input). */
+ps_status ps_engine_step_begin(ps_engine e, int B);
+ps_status ps_engine_layer_forward(ps_engine e, int layer, const float* x, const uint8_t* follow,
+                                  float* y, int32_t* ids, void* stream);
+ps_status ps_engine_step_end(ps_engine e);
 
 typedef struct {
   int64_t steps, layers;

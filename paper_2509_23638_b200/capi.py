@@ -115,7 +115,7 @@ class EngineConfig(C.Structure):
                 ("cost", CostParams), ("predictor", C.c_void_p), ("device", C.c_int32),
                 ("host_pinned", C.c_int32), ("ep", C.c_void_p), ("n_shared", C.c_int32),
                 ("host_threads", C.c_int32), ("compress_host", C.c_int32), ("predictor_kind", C.c_int32),
-                ("stats_ranking", C.POINTER(C.c_int32))]
+                ("stats_ranking", C.POINTER(C.c_int32)), ("expert_weights", C.POINTER(C.c_void_p))]
 
 
 class EngineStats(C.Structure):
@@ -232,6 +232,9 @@ _SIGS = {
     "ps_engine_set_router": (C.c_int, [_P, _P]),
     "ps_engine_decode_step": (C.c_int, [_P, _P, _P, C.c_int, _P, _P]),
     "ps_engine_decode_step_host": (C.c_int, [_P, _P, _P, C.c_int, _P, _P]),
+    "ps_engine_step_begin": (C.c_int, [_P, C.c_int]),
+    "ps_engine_layer_forward": (C.c_int, [_P, C.c_int, _P, _P, _P, _P, _P]),
+    "ps_engine_step_end": (C.c_int, [_P]),
     "ps_engine_get_stats": (C.c_int, [_P, C.POINTER(EngineStats)]),
     "ps_engine_reset_stats": (C.c_int, [_P]),
     "ps_engine_last_timeline": (C.c_int, [_P, C.POINTER(Timeline), _P, _P]),

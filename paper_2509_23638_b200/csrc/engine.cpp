@@ -518,6 +518,14 @@ struct ps_engine_s {
   std::vector<int32_t> ep_seg, ep_send_rows;  // per-layer receive segments / send rows
   int ep_rows_recv = 0;
 
+  // step in progress (step_begin / layer_forward / step_end)
+  bool in_step = false;
+  int step_B = 0, next_layer = 0;
+  double host_t0_us = 0;
+  std::vector<ps_expert_load> cur, nxt, cpu_b, od_b, pf_b;  // per-layer scheduler scratch
+  std::vector<int32_t> counts_l, pred_l;
+  cudaEvent_t ev_in = nullptr, ev_out = nullptr;  // caller stream <-> compute stream (per-layer ABI)
+
   // measured timeline of the last step (row f2 of SURVEY.md §8f)
   int cur_layer = 0;
   std::vector<int32_t> step_truth;             // [L*E] routed tokens per (layer, expert)
@@ -792,11 +800,11 @@ struct NvtxRange {
   ~NvtxRange() { nvtxRangePop(); }
 };
 
-void decode_step(ps_engine_s& e, const float* hidden, const uint8_t* follow, int B, float* y, int32_t* ids_out,
-                 const int32_t* routed_ids = nullptr, const float* routed_w = nullptr) {
-  NvtxRange step_range("ps.decode_step");
-  const int L = e.L, E = e.E, K = e.K, H = e.H;
+// Step prologue (R1-R3 state of a new pass): settles anything a failed step left behind,
+// resets the per-step bookkeeping and marks the step start on the compute stream.
+void step_begin(ps_engine_s& e, int B) {
   require(B >= 1 && B <= e.maxB, "decode_step: batch out of range");
+  e.step_B = B;
   e.prefill_mode = B > kDecodeMaxBatch;
   // A step that threw mid-layer may have left jobs queued / a lane batch running: settle
   // both before this step recycles the job list (no-ops after a normal step).
@@ -815,19 +823,39 @@ void decode_step(ps_engine_s& e, const float* hidden, const uint8_t* follow, int
   e.ready.clear();
   e.pending_pf.clear();
   PS_CUDA(cudaEventRecord(e.ev_step0, e.sc));
-  const auto host_t0 = Clock::now();
-  const double host_t0_us = now_us();
+  e.host_t0_us = now_us();
   e.cpu_done.clear();
   if (e.lane_drv) e.lane_drv->drain();
+  e.cpu_b.assign(e.E, {});
+  e.od_b.assign(e.E, {});
+  e.pf_b.assign(e.E, {});
+  e.counts_l.assign(e.Et, 0);
+  e.pred_l.assign(e.E, 0);
+  e.step_truth.assign(static_cast<size_t>(e.L) * e.E, 0);
+  e.last_pred.assign(static_cast<size_t>(e.L) * e.E, 0);
+  e.next_layer = 0;
+  e.in_step = true;
+}
 
-  std::vector<ps_expert_load> cur, nxt, cpu_b(E), od_b(E), pf_b(E);
+// One MoE layer of the current step (rules R1-R8 for layer l): x [B,H] f32 gating input
+// (= FFN input), follow [B] u8 (nullable), y [B,H] f32 out. routed_ids / routed_w
+// (nullable, [B,k] / [B,E]): the routing is given (a reference trace's gating truth) and
+// replaces K1. x_next / follow_next: layer l+1's inputs (PS_PRED_PERFECT only).
+void layer_forward(ps_engine_s& e, int l, const float* x, const uint8_t* follow, float* y_l,
+                   const int32_t* routed_ids, const float* routed_w, const float* x_next, const uint8_t* follow_next) {
+  const int L = e.L, E = e.E, K = e.K, H = e.H, B = e.step_B;
+  require(e.in_step && l == e.next_layer, "layer_forward: layers must run in order 0..L-1 inside a step");
+  e.next_layer = l + 1;
+  std::vector<ps_expert_load>& cur = e.cur;
+  std::vector<ps_expert_load>& nxt = e.nxt;
+  std::vector<ps_expert_load>& cpu_b = e.cpu_b;
+  std::vector<ps_expert_load>& od_b = e.od_b;
+  std::vector<ps_expert_load>& pf_b = e.pf_b;
   const int Et = e.Et, Kt = e.Kt;
-  std::vector<int32_t> counts_l(Et), pred_l(E);
-  e.step_truth.assign(static_cast<size_t>(L) * E, 0);
-  e.last_pred.assign(static_cast<size_t>(L) * E, 0);
-
-  for (int l = 0; l < L; ++l) {
-    const float* x = hidden + static_cast<size_t>(l) * B * H;
+  std::vector<int32_t>& counts_l = e.counts_l;
+  std::vector<int32_t>& pred_l = e.pred_l;
+  const double host_t0_us = e.host_t0_us;
+  {
     e.cur_layer = l;
     LayerDev& ld = e.layer[l];
     // Layer start: a fresh mark (the previous combine's end would also count the host's
@@ -845,20 +873,16 @@ void decode_step(ps_engine_s& e, const float* hidden, const uint8_t* follow, int
     const bool fused_perm = !e.ep && e.S == 0 && !e.prefill_mode && !routed_ids;
     ps_status s;
     if (routed_ids) {
-      PS_CUDA(cudaMemcpyAsync(ld.ids, routed_ids + static_cast<size_t>(l) * B * K, sizeof(int32_t) * B * K,
-                              cudaMemcpyDeviceToDevice, e.sc));
-      PS_CUDA(cudaMemcpyAsync(ld.weights, routed_w + static_cast<size_t>(l) * B * E, sizeof(float) * B * E,
-                              cudaMemcpyDeviceToDevice, e.sc));
+      PS_CUDA(cudaMemcpyAsync(ld.ids, routed_ids, sizeof(int32_t) * B * K, cudaMemcpyDeviceToDevice, e.sc));
+      PS_CUDA(cudaMemcpyAsync(ld.weights, routed_w, sizeof(float) * B * E, cudaMemcpyDeviceToDevice, e.sc));
       s = ps_cast_bf16(x, static_cast<int64_t>(B) * H, e.x_bf16, e.sc);
     } else if (fused_perm)
       s = ps_route_permute(x, e.gate + static_cast<size_t>(l) * E * H, e.bias + static_cast<size_t>(l) * E,
-                           follow ? follow + static_cast<size_t>(l) * B : nullptr, l > 0 ? e.layer[l - 1].ids : nullptr,
-                           K, B, H, E, K, ld.weights, ld.ids, e.x_bf16, e.offsets, e.perm_src, e.inv, e.route_ws,
+                           follow, l > 0 ? e.layer[l - 1].ids : nullptr, K, B, H, E, K, ld.weights, ld.ids, e.x_bf16, e.offsets, e.perm_src, e.inv, e.route_ws,
                            e.sc);
     else
       s = ps_route_topk(x, e.gate + static_cast<size_t>(l) * E * H, e.bias + static_cast<size_t>(l) * E,
-                        follow ? follow + static_cast<size_t>(l) * B : nullptr, l > 0 ? e.layer[l - 1].ids : nullptr, K,
-                        B, H, E, K, nullptr, ld.weights, ld.ids, nullptr, e.x_bf16, e.sc);
+                        follow, l > 0 ? e.layer[l - 1].ids : nullptr, K, B, H, E, K, nullptr, ld.weights, ld.ids, nullptr, e.x_bf16, e.sc);
     if (s != PS_OK) fail(s, ps_last_error());
     e.st.kernel_launches += 1;
     // --- K4 LLaPor: predicted histogram of layer l+1 -------------------------
@@ -876,9 +900,9 @@ void decode_step(ps_engine_s& e, const float* hidden, const uint8_t* follow, int
       if (s != PS_OK) fail(s, ps_last_error());
       e.st.kernel_launches += 2;
     } else if (predict) {  // PERFECT: layer l+1's true routing, K1 one layer early
-      const float* xn = hidden + static_cast<size_t>(l + 1) * B * H;
-      s = ps_route_topk(xn, e.gate + static_cast<size_t>(l + 1) * E * H, e.bias + static_cast<size_t>(l + 1) * E,
-                        follow ? follow + static_cast<size_t>(l + 1) * B : nullptr, ld.ids, K, B, H, E, K, nullptr,
+      require(x_next != nullptr, "PS_PRED_PERFECT needs layer l+1's inputs (not available per layer)");
+      s = ps_route_topk(x_next, e.gate + static_cast<size_t>(l + 1) * E * H, e.bias + static_cast<size_t>(l + 1) * E,
+                        follow_next, ld.ids, K, B, H, E, K, nullptr,
                         e.pp_w, e.pp_ids, e.pred_dev, nullptr, e.sc);
       if (s != PS_OK) fail(s, ps_last_error());
       e.st.kernel_launches += 1;
@@ -1168,9 +1192,9 @@ void decode_step(ps_engine_s& e, const float* hidden, const uint8_t* follow, int
     }
     if (!e.ep) {
       s = ps_combine(e.y_part, e.step_split, e.inv, e.S ? e.ids_ext : ld.ids, e.S ? e.w_ext : ld.weights, B, Kt, Et, H,
-                     y + static_cast<size_t>(l) * B * H, e.sc);
+                     y_l, e.sc);
     } else {
-      s = ep_combine_rows(e, B, ld, y + static_cast<size_t>(l) * B * H);
+      s = ep_combine_rows(e, B, ld, y_l);
     }
     if (s != PS_OK) fail(s, ps_last_error());
     ph.comb1 = take_event(e);
@@ -1214,6 +1238,14 @@ void decode_step(ps_engine_s& e, const float* hidden, const uint8_t* follow, int
       }
     }
   }
+}
+
+// Step epilogue: end mark, drain of the serial channel (pending prefetches cancelled or
+// completed), and the step's measurement / measured timeline from its CUDA events.
+void step_end(ps_engine_s& e, int32_t* ids_out) {
+  require(e.in_step && e.next_layer == e.L, "step_end: not every layer of the step ran");
+  e.in_step = false;
+  const int L = e.L, E = e.E, K = e.K, B = e.step_B;
   if (ids_out)
     for (int l = 0; l < L; ++l)
       PS_CUDA(cudaMemcpyAsync(ids_out + static_cast<size_t>(l) * B * K, e.layer[l].ids, sizeof(int32_t) * B * K,
@@ -1291,7 +1323,23 @@ void decode_step(ps_engine_s& e, const float* hidden, const uint8_t* follow, int
   e.st.step_ms_total += ms;
   e.st.steps += 1;
   e.st.layers += L;
-  (void)host_t0;
+}
+
+void decode_step(ps_engine_s& e, const float* hidden, const uint8_t* follow, int B, float* y, int32_t* ids_out,
+                 const int32_t* routed_ids = nullptr, const float* routed_w = nullptr) {
+  NvtxRange step_range("ps.decode_step");
+  step_begin(e, B);
+  const int L = e.L, E = e.E, K = e.K, H = e.H;
+  for (int l = 0; l < L; ++l) {
+    const size_t xl = static_cast<size_t>(l) * B * H;
+    const bool nx = l + 1 < L;
+    layer_forward(e, l, hidden + xl, follow ? follow + static_cast<size_t>(l) * B : nullptr, y + xl,
+                  routed_ids ? routed_ids + static_cast<size_t>(l) * B * K : nullptr,
+                  routed_w ? routed_w + static_cast<size_t>(l) * B * E : nullptr,
+                  nx ? hidden + xl + static_cast<size_t>(B) * H : nullptr,
+                  nx && follow ? follow + static_cast<size_t>(l + 1) * B : nullptr);
+  }
+  step_end(e, ids_out);
 }
 
 void create_engine(const ps_engine_config& cfg, ps_engine_s& e) {
@@ -1387,15 +1435,26 @@ void create_engine(const ps_engine_config& cfg, ps_engine_s& e) {
     for (int ex = 0; ex < e.E; ++ex) {
       const size_t idx = static_cast<size_t>(l) * e.E + ex;
       if (!owned(ex)) continue;
+      // caller-supplied weights (cfg.expert_weights) or the hash-initialised synthetic ones
+      const uint16_t* given = cfg.expert_weights ? cfg.expert_weights[static_cast<size_t>(l) * e.Et + ex] : nullptr;
+      require(!cfg.expert_weights || given, "engine: expert_weights has a null slab for an owned expert");
       if (e.resident[idx]) {
         uint16_t* p = reinterpret_cast<uint16_t*>(static_cast<char*>(e.arena) + ri++ * sp.expert_bytes);
-        if (ps_init_expert_slab(p, e.H, e.F, cfg.weight_seed, l, ex, e.sc) != PS_OK) fail(PS_ECUDA, ps_last_error());
+        if (given)
+          PS_CUDA(cudaMemcpyAsync(p, given, sp.expert_bytes, cudaMemcpyHostToDevice, e.sc));
+        else if (ps_init_expert_slab(p, e.H, e.F, cfg.weight_seed, l, ex, e.sc) != PS_OK)
+          fail(PS_ECUDA, ps_last_error());
         e.dev_slab[idx] = p;
       } else {
-        uint16_t* st = reinterpret_cast<uint16_t*>(static_cast<char*>(stage) + (si++ % 2) * sp.expert_bytes);
-        if (ps_init_expert_slab(st, e.H, e.F, cfg.weight_seed, l, ex, e.sc) != PS_OK) fail(PS_ECUDA, ps_last_error());
         uint16_t* hp = reinterpret_cast<uint16_t*>(static_cast<char*>(e.host_arena) + hi++ * sp.expert_bytes);
-        PS_CUDA(cudaMemcpyAsync(hp, st, sp.expert_bytes, cudaMemcpyDeviceToHost, e.sc));
+        if (given) {
+          std::memcpy(hp, given, sp.expert_bytes);
+        } else {
+          uint16_t* st = reinterpret_cast<uint16_t*>(static_cast<char*>(stage) + (si++ % 2) * sp.expert_bytes);
+          if (ps_init_expert_slab(st, e.H, e.F, cfg.weight_seed, l, ex, e.sc) != PS_OK)
+            fail(PS_ECUDA, ps_last_error());
+          PS_CUDA(cudaMemcpyAsync(hp, st, sp.expert_bytes, cudaMemcpyDeviceToHost, e.sc));
+        }
         e.host_slab[idx] = hp;
       }
     }
@@ -1408,7 +1467,11 @@ void create_engine(const ps_engine_config& cfg, ps_engine_s& e) {
       for (int j = 0; j < e.S; ++j) {
         const size_t idx = static_cast<size_t>(l) * e.S + j;
         uint16_t* p = reinterpret_cast<uint16_t*>(static_cast<char*>(e.shared_arena) + idx * sp.expert_bytes);
-        if (ps_init_expert_slab(p, e.H, e.F, cfg.weight_seed, l, e.E + j, e.sc) != PS_OK)
+        const uint16_t* given = cfg.expert_weights ? cfg.expert_weights[static_cast<size_t>(l) * e.Et + e.E + j] : nullptr;
+        require(!cfg.expert_weights || given, "engine: expert_weights has a null shared-expert slab");
+        if (given)
+          PS_CUDA(cudaMemcpyAsync(p, given, sp.expert_bytes, cudaMemcpyHostToDevice, e.sc));
+        else if (ps_init_expert_slab(p, e.H, e.F, cfg.weight_seed, l, e.E + j, e.sc) != PS_OK)
           fail(PS_ECUDA, ps_last_error());
         e.shared_slab[idx] = p;
       }
@@ -1569,6 +1632,8 @@ void create_engine(const ps_engine_config& cfg, ps_engine_s& e) {
   PS_CUDA(cudaMalloc(&e.out_y, sizeof(float) * e.L * B * e.H));
   PS_CUDA(cudaMalloc(&e.out_ids, sizeof(int32_t) * e.L * rows));
   PS_CUDA(cudaEventCreateWithFlags(&e.ev_routed, cudaEventDisableTiming));
+  PS_CUDA(cudaEventCreateWithFlags(&e.ev_in, cudaEventDisableTiming));
+  PS_CUDA(cudaEventCreateWithFlags(&e.ev_out, cudaEventDisableTiming));
   PS_CUDA(cudaEventCreate(&e.ev_step0));
   PS_CUDA(cudaEventCreate(&e.ev_step1));
 
@@ -1666,7 +1731,7 @@ void destroy_engine(ps_engine_s& e) {
   }
   for (cudaEvent_t ev : e.event_pool) cudaEventDestroy(ev);
   for (cudaEvent_t ev : e.job_event_pool) cudaEventDestroy(ev);
-  for (cudaEvent_t ev : {e.ev_routed, e.ev_step0, e.ev_step1})
+  for (cudaEvent_t ev : {e.ev_routed, e.ev_step0, e.ev_step1, e.ev_in, e.ev_out})
     if (ev) cudaEventDestroy(ev);
   if (e.sc) cudaStreamDestroy(e.sc);
   if (e.s_d2h) cudaStreamDestroy(e.s_d2h);
@@ -1731,6 +1796,44 @@ ps_status ps_engine_decode_step_host(ps_engine e, const float* hidden_host, cons
     if (ids_host)
       PS_CUDA(cudaMemcpyAsync(ids_host, e->out_ids, sizeof(int32_t) * e->L * B * e->K, cudaMemcpyDeviceToHost, e->sc));
     PS_CUDA(cudaStreamSynchronize(e->sc));
+  });
+}
+
+ps_status ps_engine_step_begin(ps_engine e, int B) {
+  return guarded([&] {
+    require(e != nullptr, "ps_engine_step_begin: null engine");
+    step_begin(*e, B);
+  });
+}
+
+ps_status ps_engine_layer_forward(ps_engine e, int layer, const float* x, const uint8_t* follow, float* y,
+                                  int32_t* ids, void* stream) {
+  return guarded([&] {
+    require(e && x && y, "ps_engine_layer_forward: null argument");
+    require(e->in_step, "ps_engine_layer_forward: no step in progress (ps_engine_step_begin)");
+    require(layer >= 0 && layer < e->L, "ps_engine_layer_forward: layer out of range");
+    require(e->pred_kind != PS_PRED_PERFECT, "ps_engine_layer_forward: PS_PRED_PERFECT needs the whole step's inputs");
+    cudaStream_t cs = as_stream(stream);
+    const bool foreign = stream != nullptr && cs != e->sc;
+    if (foreign) {  // the layer's inputs were produced on the caller's stream
+      PS_CUDA(cudaEventRecord(e->ev_in, cs));
+      PS_CUDA(cudaStreamWaitEvent(e->sc, e->ev_in, 0));
+    }
+    layer_forward(*e, layer, x, follow, y, nullptr, nullptr, nullptr, nullptr);
+    if (ids)
+      PS_CUDA(cudaMemcpyAsync(ids, e->layer[layer].ids, sizeof(int32_t) * e->step_B * e->K, cudaMemcpyDeviceToDevice,
+                              e->sc));
+    if (foreign) {  // the caller's next kernels (attention of layer+1) read y
+      PS_CUDA(cudaEventRecord(e->ev_out, e->sc));
+      PS_CUDA(cudaStreamWaitEvent(cs, e->ev_out, 0));
+    }
+  });
+}
+
+ps_status ps_engine_step_end(ps_engine e) {
+  return guarded([&] {
+    require(e != nullptr, "ps_engine_step_end: null engine");
+    step_end(*e, nullptr);
   });
 }
 

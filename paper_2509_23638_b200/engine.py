@@ -114,7 +114,7 @@ class Engine:
                  resident=None, trace_hidden=None, trace_follow=None, policy: str = "presched",
                  predictor=None, cost=None, prefetch_slots: int = 8, device: int = 0, ep=None,
                  n_shared: int = 0, host_threads: int = 0, compress_host: bool = False,
-                 predictor_kind: str = "auto", stats_ranking=None):
+                 predictor_kind: str = "auto", stats_ranking=None, expert_weights=None):
         from . import parse_policy, plan_residency, trace_inputs  # noqa: F401
         self.lib = load()
         self.spec = spec
@@ -156,6 +156,11 @@ class Engine:
         if stats_ranking is not None:
             self._rank = np.ascontiguousarray(stats_ranking, np.int32).reshape(-1)
             cfg.stats_ranking = self._rank.ctypes.data_as(C.POINTER(C.c_int32))
+        if expert_weights is not None:  # caller-supplied slabs: list [L*(E+n_shared)] of uint16 arrays / None
+            self._weights = list(expert_weights)
+            self._wptrs = (C.c_void_p * len(self._weights))(
+                *[w.ctypes.data if w is not None else None for w in self._weights])
+            cfg.expert_weights = C.cast(self._wptrs, C.POINTER(C.c_void_p))
         self.host_threads = host_threads
         h = C.c_void_p()
         check(self.lib.ps_engine_create(C.byref(cfg), C.byref(h)))
@@ -199,6 +204,21 @@ class Engine:
         B = hidden_lbh.shape[1]
         check(self.lib.ps_engine_decode_step(self.h, _ptr(hidden_lbh), _ptr(follow_lb), B, _ptr(y_lbh),
                                              _ptr(ids_lbk)))
+
+    def step_begin(self, B: int):
+        """Per-layer ABI: start a decode pass of B tokens (ps_engine_step_begin)."""
+        check(self.lib.ps_engine_step_begin(self.h, B))
+
+    def layer_forward(self, layer: int, x_bh, follow_b, y_bh, ids_bk=None, stream=None):
+        """One MoE layer on device tensors (ps_engine_layer_forward); `stream`: a
+        torch.cuda.Stream the layer is ordered with (default: torch's current stream)."""
+        torch = _torch()
+        st = stream if stream is not None else torch.cuda.current_stream()
+        check(self.lib.ps_engine_layer_forward(self.h, layer, _ptr(x_bh), _ptr(follow_b), _ptr(y_bh), _ptr(ids_bk),
+                                               C.c_void_p(st.cuda_stream)))
+
+    def step_end(self):
+        check(self.lib.ps_engine_step_end(self.h))
 
     def stats(self) -> dict:
         s = capi.EngineStats()

@@ -38,8 +38,8 @@ def main():
     for kern, name in ((0, "single-CTA"), (1, "CTA-pair")):  # both tcgen05 prefill kernels explicitly
         ps.check(lib.ps_set_prefill_kernel(kern))
         print("prefill kernel", name)
-        run("mixtral", 2, 8, 256, 512, 512, 1.0)
-        run("deepseek", 2, 16, 256, 256, 512, 1.0, n_shared=2)
+        run("mixtral", 3, 8, 256, 512, 512, 1.0)
+        run("deepseek", 3, 16, 256, 256, 512, 1.0, n_shared=2)
     ps.check(lib.ps_set_prefill_kernel(2))
     ep_loopback(2)
     print("sanitize run done")
@@ -48,7 +48,7 @@ def main():
 def ep_loopback(G):
     """The EP engine over the in-process transport (G ranks, one thread each)."""
     from concurrent.futures import ThreadPoolExecutor
-    spec = ps.desk_scale("mixtral", 2, 8, 256)
+    spec = ps.desk_scale("mixtral", 3, 8, 256)
     spec.expert_bytes = 6 * 256 * 512
     gen = ps.TraceGenConfig(*[ps.GROUP_DEFAULT_GEN[g] for g in ("input", "middle", "output")])
     B = 8

@@ -86,7 +86,7 @@ def test_ep_engine_loopback_qwen3_like(torch_cuda):
 
 def test_ep_engine_loopback_prefill_chunk(torch_cuda):
     """B > 64 per rank: prefill mode through EP (gathered received rows, tcgen05 path)."""
-    spec = ps.desk_scale("mixtral", 2, 8, 256)
+    spec = ps.desk_scale("mixtral", 3, 8, 256)
     spec.expert_bytes = 6 * 256 * 512
     stats = _ep_run(spec, 2, 160, 1.0, steps=1)
     assert sum(s["tc_launches"] for s in stats) > 0
@@ -95,6 +95,6 @@ def test_ep_engine_loopback_prefill_chunk(torch_cuda):
 def test_ep_engine_loopback_mixtral_expert_shape(torch_cuda):
     """Full Mixtral expert shape (H=4096, F=14336), G=2, z-slab loads, 50 % budget."""
     full = ps.spec_preset("mixtral")
-    spec = ps.desk_scale("mixtral", 2, 8, 4096)
+    spec = ps.desk_scale("mixtral", 3, 8, 4096)
     spec.expert_bytes = full.expert_bytes
     _ep_run(spec, 2, 16, 0.5, compress=True, steps=1)
