@@ -211,6 +211,7 @@ def workload_config(args, spec, executor="gpu_only"):
                         f"F={ps.ffn_dim(spec)}, batch {args.batch}, HBM expert budget {args.budget:.0%} "
                         f"({n_res}/{L * E} experts resident, hot-table residency from a warm-up trace), "
                         f"other experts in pinned host DRAM, policy {args.policy}"
+                        + (f"+lookahead{args.lookahead}" if getattr(args, "lookahead", 0) else "")
                         + (", PreSched cpu_set on the host expert lane (AMX-BF16)" if executor == "host_lane" else
                            ", GPU-only executor")
                         + (", loads as lossless z-slabs decoded on the GPU" if getattr(args, "compress", 0)
@@ -221,7 +222,7 @@ def workload_config(args, spec, executor="gpu_only"):
             "decode_batch": args.batch, "global_batch": args.batch * args.gpus,
             "parallelism": (f"ep{args.gpus}" if args.gpus > 1 else "single"),
             "executor": executor,
-            "budget_fraction": args.budget, "policy": args.policy,
+            "budget_fraction": args.budget, "policy": args.policy, "lookahead": getattr(args, "lookahead", 0),
             "l2": "inputs larger than L2 (each expert slab 336 MiB > 126 MB L2)"}
 
 
@@ -280,7 +281,7 @@ def run_ours(args):
     e = eng.Engine(spec, gen, max_batch=B, weight_seed=args.weight_seed, gate=gate, budget_bytes=budget_bytes,
                    resident=resident, policy=args.policy, predictor=predictor, device=local, ep=ep,
                    host_threads=host_threads if world == 1 else 0, compress_host=bool(args.compress),
-                   predictor_kind=args.predictor)
+                   predictor_kind=args.predictor, lookahead=args.lookahead)
     t_create = time.perf_counter() - t_create
     measured_cost = e.stats()["cost"]
 
@@ -540,6 +541,7 @@ def decode_summary(st, dev_ms, N, B, L):
                    "ondemand_loads_per_step": st["ondemand_loads"] / steps,
                    "prefetches_per_step": st["prefetches_committed"] / steps,
                    "prefetch_hits_per_step": st["prefetch_hits"] / steps,
+                   "lookahead_prefetches_per_step": st["lookahead_prefetches"] / steps,
                    # 1 - (compute-stream stall on copy events) / (copy-engine busy time)
                    "hidden_fraction": (1.0 - st["compute_wait_ms"] / st["h2d_busy_ms"]) if st["h2d_busy_ms"] > 0
                    else 1.0},
@@ -580,6 +582,8 @@ def main():
                     help="next-layer load predictor feeding PreSched (the reference's PredictFn menu)")
     ap.add_argument("--compress", type=int, default=1,
                     help="1: non-resident experts cross PCIe as lossless z-slabs (decoded on the GPU)")
+    ap.add_argument("--lookahead", type=int, default=0, choices=[0, 1, 2],
+                    help="PreSched + lookahead top-up of the serial channel (0 = the reference executor)")
     ap.add_argument("--host-threads", type=int, default=-1,
                     help="host expert lane threads (-1 auto, 0 = GPU-only executor)")
     args = ap.parse_args()

@@ -435,6 +435,19 @@ ps_status ps_llapor_load(const char* path, ps_llapor* out, ps_model_spec* spec_o
 ps_status ps_llapor_random(const ps_model_spec* spec, int pca_in, int pca_mid, int width_in,
                            int width_mid, uint64_t seed, ps_llapor* out);
 ps_status ps_llapor_free(ps_llapor m);
+/* save_checkpoint (predictor.cpp:833-875): LLPC v1, every field of the loaded/fine-tuned
+ * model (byte-identical to the reference's file for the same model). Host only. */
+ps_status ps_llapor_save(ps_llapor m, const char* path);
+/* Online fine_tune (predictor.cpp:654-663) of net `layer` on n observed samples — the
+ * reference's build_samples pairs (predictor.cpp:596-613): features of layer-1 (hidden
+ * [n,H] f64, active experts [n,k_prev], full-softmax gate weights [n,E] f64) and the
+ * labels of layer `layer` (active experts [n,k] -> multi-hot). `steps` AdamW passes at
+ * learning rate lr with the model's TrainConfig (batch_size, lambda, gamma, weight decay
+ * of the net's group, seed); host f64, bit-identical to the reference. The net's GPU
+ * copy is refreshed before its next ps_llapor_forward. Host buffers; no GPU needed. */
+ps_status ps_llapor_fine_tune(ps_llapor m, int layer, int n, const double* hidden_prev,
+                              const int32_t* active_prev, int k_prev, const double* gate_prev,
+                              const int32_t* active, int k, int steps, double lr);
 /* Net for target layer `layer` (>=1) on features of layer-1 for B tokens:
  *   hidden [B,H] f32, prev_ids [B,k_prev] i32, prev_weights [B,E] f32.
  * Outputs: logits [B,E] f32 (nullable), ids [B,k] i32 (top-k on LOGITS),
@@ -540,6 +553,11 @@ typedef struct {
                                copied at create (resident -> HBM, others -> the pinned
                                host arena); null = hash-initialised from weight_seed.
                                Under EP only owned experts are read. */
+  int32_t lookahead;        /* 0: PreSched's plan only (the reference's executor semantics).
+                               d in {1, 2}: a labelled extension — behind PreSched's batch,
+                               queue the other predicted non-resident experts of layers
+                               l+1..l+d (hottest first, slot cap per target layer); those not
+                               started by the next scheduling point are cancelled (R2). */
 } ps_engine_config;
 
 ps_status ps_engine_create(const ps_engine_config* cfg, ps_engine* out);
@@ -605,6 +623,7 @@ typedef struct {
   int64_t z_decodes;        /* z-slab decodes (compressed loads landed) */
   double h2d_expert_bytes;  /* expert bytes the issued copies delivered (= h2d_bytes
                                without compression) */
+  int64_t lookahead_prefetches; /* prefetch jobs queued by the lookahead top-up */
 } ps_engine_stats;
 ps_status ps_engine_get_stats(ps_engine e, ps_engine_stats* out);
 ps_status ps_engine_reset_stats(ps_engine e);
@@ -620,6 +639,10 @@ ps_status ps_engine_last_timeline(ps_engine e, ps_timeline* out, int32_t* truth_
 /* Predicted per-expert token counts of the last step, [L*E] (row l = the prediction
  * made at layer l-1 for layer l; row 0 = 0). */
 ps_status ps_engine_last_predictions(ps_engine e, int32_t* out);
+/* Routing of the last completed step, host buffers (nullable): ids [L,B,k] i32 and the
+ * full-softmax gate weights [L,B,E] f32 — with the step's hidden states, the observed
+ * (features of l-1, labels of l) pairs an online ps_llapor_fine_tune consumes. */
+ps_status ps_engine_last_routing(ps_engine e, int32_t* ids_out, float* weights_out);
 /* Replace the cost parameters PreSched plans with (e.g. beta = 1e9 disables the host
  * lane's cpu_set for a GPU-only comparison on the same engine). */
 ps_status ps_engine_set_cost(ps_engine e, const ps_cost_params* cost);

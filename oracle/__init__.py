@@ -157,6 +157,9 @@ def ref_lib() -> C.CDLL:
         _ref.ref_topk.argtypes = [C.c_void_p, C.c_int, C.c_int, C.c_void_p, C.POINTER(C.c_int)]
         _ref.ref_compute_metrics.argtypes = [C.c_void_p, C.c_int, C.c_void_p, C.c_void_p, C.c_int, C.c_int64,
                                              C.c_int, C.c_void_p, C.c_void_p, C.c_void_p]
+        _ref.ref_llapor_fine_tune.argtypes = [C.c_void_p, C.c_int, C.c_int, C.c_void_p, C.c_void_p, C.c_int,
+                                              C.c_void_p, C.c_void_p, C.c_int, C.c_int, C.c_double]
+        _ref.ref_llapor_save.argtypes = [C.c_void_p, C.c_char_p]
         _ref.ref_router_inputs.argtypes = [C.POINTER(RefGen), C.POINTER(RefSpec), C.c_int, C.c_uint64, C.c_void_p,
                                            C.c_void_p, C.c_void_p]
         _ref.ref_llapor_predict_batch.argtypes = [C.c_void_p, C.c_int, C.c_int, C.c_void_p, C.c_void_p, C.c_int,

@@ -742,4 +742,36 @@ int ref_compute_metrics(const ref_event* events, int n_events, const int64_t* la
   });
 }
 
+// fine_tune (predictor.cpp:654-663) of a loaded model's net `layer` on explicit samples
+// built the way build_samples does (predictor.cpp:596-613), then save_checkpoint.
+int ref_llapor_fine_tune(void* handle, int layer, int n, const double* hidden_prev, const int32_t* active_prev,
+                         int k_prev, const double* gate_prev, const int32_t* active, int k, int steps, double lr) {
+  return guarded([&] {
+    LLaPor& m = static_cast<LLaPorHandle*>(handle)->model;
+    LLaPorNet& net = m.nets.at(layer);
+    const int H = m.spec.hidden_dim, E = net.experts_per_layer;
+    std::vector<Sample> samples;
+    for (int t = 0; t < n; ++t) {
+      Sample s;
+      s.features.hidden_reduced = pca_apply(net.pca, std::vector<double>(hidden_prev + static_cast<size_t>(t) * H,
+                                                                         hidden_prev + static_cast<size_t>(t + 1) * H));
+      s.features.active_onehot.assign(E, 0.0);
+      for (int j = 0; j < k_prev; ++j) s.features.active_onehot.at(active_prev[t * k_prev + j]) = 1.0;
+      s.features.gate_weights_prev.assign(gate_prev + static_cast<size_t>(t) * E,
+                                          gate_prev + static_cast<size_t>(t + 1) * E);
+      s.labels.assign(E, 0.0);
+      for (int j = 0; j < k; ++j) s.labels.at(active[t * k + j]) = 1.0;
+      samples.push_back(std::move(s));
+    }
+    fine_tune(net, samples, steps, lr, m.cfg);
+  });
+}
+
+int ref_llapor_save(void* handle, const char* path) {
+  return guarded([&] {
+    const LLaPorHandle* h = static_cast<LLaPorHandle*>(handle);
+    save_checkpoint(h->model, h->checksum, path);
+  });
+}
+
 }  // extern "C"

@@ -115,7 +115,8 @@ class EngineConfig(C.Structure):
                 ("cost", CostParams), ("predictor", C.c_void_p), ("device", C.c_int32),
                 ("host_pinned", C.c_int32), ("ep", C.c_void_p), ("n_shared", C.c_int32),
                 ("host_threads", C.c_int32), ("compress_host", C.c_int32), ("predictor_kind", C.c_int32),
-                ("stats_ranking", C.POINTER(C.c_int32)), ("expert_weights", C.POINTER(C.c_void_p))]
+                ("stats_ranking", C.POINTER(C.c_int32)), ("expert_weights", C.POINTER(C.c_void_p)),
+                ("lookahead", C.c_int32)]
 
 
 class EngineStats(C.Structure):
@@ -128,7 +129,8 @@ class EngineStats(C.Structure):
                 ("ffn_flops_total", C.c_double), ("tc_launches", C.c_int64), ("ffn_launches", C.c_int64),
                 ("kernel_launches", C.c_int64),
                 ("cost", CostParams), ("cpu_experts", C.c_int64), ("cpu_ms_total", C.c_double),
-                ("cpu_bytes_total", C.c_double), ("z_decodes", C.c_int64), ("h2d_expert_bytes", C.c_double)]
+                ("cpu_bytes_total", C.c_double), ("z_decodes", C.c_int64), ("h2d_expert_bytes", C.c_double),
+                ("lookahead_prefetches", C.c_int64)]
 
 
 PLAN_FN = C.CFUNCTYPE(C.c_int, C.c_void_p, C.POINTER(LayerInputs), C.c_int, C.POINTER(LayerPlan))
@@ -213,6 +215,8 @@ _SIGS = {
     "ps_llapor_random": (C.c_int, [C.POINTER(ModelSpec), C.c_int, C.c_int, C.c_int, C.c_int, C.c_uint64,
                                    C.POINTER(C.c_void_p)]),
     "ps_llapor_free": (C.c_int, [_P]),
+    "ps_llapor_save": (C.c_int, [_P, C.c_char_p]),
+    "ps_llapor_fine_tune": (C.c_int, [_P, C.c_int, C.c_int, _P, _P, C.c_int, _P, _P, C.c_int, C.c_int, C.c_double]),
     "ps_llapor_scratch_bytes": (C.c_size_t, [_P, C.c_int]),
     "ps_llapor_forward": (C.c_int, [_P, C.c_int, _P, _P, C.c_int, _P, C.c_int, C.c_int, _P, _P, _P, _P, _P]),
     "ps_ep_local_experts": (C.c_int, [C.c_int, C.c_int, C.c_int]),
@@ -233,6 +237,7 @@ _SIGS = {
     "ps_engine_decode_step": (C.c_int, [_P, _P, _P, C.c_int, _P, _P]),
     "ps_engine_decode_step_host": (C.c_int, [_P, _P, _P, C.c_int, _P, _P]),
     "ps_engine_step_begin": (C.c_int, [_P, C.c_int]),
+    "ps_engine_last_routing": (C.c_int, [_P, _P, _P]),
     "ps_engine_layer_forward": (C.c_int, [_P, C.c_int, _P, _P, _P, _P, _P]),
     "ps_engine_step_end": (C.c_int, [_P]),
     "ps_engine_get_stats": (C.c_int, [_P, C.POINTER(EngineStats)]),

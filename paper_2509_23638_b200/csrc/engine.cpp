@@ -464,9 +464,11 @@ struct ps_engine_s {
   // step buffers
   std::vector<ps::LayerDev> layer;
   int32_t* counts_dev = nullptr;     // [Et]
-  int32_t* pred_dev = nullptr;       // [E]
+  int32_t* pred_dev = nullptr;       // [E] predicted tokens per expert of layer l+1
+  int32_t* pred2_dev = nullptr;      // [E] ... of layer l+2 (e_next2, lookahead)
   // Scheduling-point block, one device allocation mirrored in pinned host memory so the
-  // per-layer D2H is ONE copy: counts [Et] | pred [Et] | offsets [Et+1] | perm_src [maxB*Kt]
+  // per-layer D2H is ONE copy: counts [Et] | pred [Et] | pred2 [Et] | offsets [Et+1] |
+  // perm_src [maxB*Kt]
   int32_t* sched_dev = nullptr;
   int32_t* route_ws = nullptr;       // ticket counter of the fused route+permute launch
   int32_t* pinned_counts = nullptr;  // host mirror of sched_dev
@@ -522,8 +524,8 @@ struct ps_engine_s {
   bool in_step = false;
   int step_B = 0, next_layer = 0;
   double host_t0_us = 0;
-  std::vector<ps_expert_load> cur, nxt, cpu_b, od_b, pf_b;  // per-layer scheduler scratch
-  std::vector<int32_t> counts_l, pred_l;
+  std::vector<ps_expert_load> cur, nxt, nxt2, cpu_b, od_b, pf_b;  // per-layer scheduler scratch
+  std::vector<int32_t> counts_l, pred_l, pred2_l;
   cudaEvent_t ev_in = nullptr, ev_out = nullptr;  // caller stream <-> compute stream (per-layer ABI)
 
   // measured timeline of the last step (row f2 of SURVEY.md §8f)
@@ -831,6 +833,7 @@ void step_begin(ps_engine_s& e, int B) {
   e.pf_b.assign(e.E, {});
   e.counts_l.assign(e.Et, 0);
   e.pred_l.assign(e.E, 0);
+  e.pred2_l.assign(e.E, 0);
   e.step_truth.assign(static_cast<size_t>(e.L) * e.E, 0);
   e.last_pred.assign(static_cast<size_t>(e.L) * e.E, 0);
   e.next_layer = 0;
@@ -907,6 +910,17 @@ void layer_forward(ps_engine_s& e, int l, const float* x, const uint8_t* follow,
       if (s != PS_OK) fail(s, ps_last_error());
       e.st.kernel_launches += 1;
     }
+    // --- K4 for layer l+2: e_next2 of the widened window (simulator.cpp:128-131) and the
+    // lookahead top-up. The reference predicts l+2 from the true layer-(l+1) features,
+    // which do not exist yet at layer l: nets[l+2] is applied to layer-l features instead.
+    const bool want_pred2 = !e.ep && l + 2 < L && !e.prefill_mode && e.has_host[l + 2];
+    const bool predict2 = want_pred2 && e.pred_kind == PS_PRED_LLAPOR;
+    if (predict2) {
+      s = ps_llapor_forward(e.cfg.predictor, l + 2, x, ld.ids, K, ld.weights, B, K, nullptr, nullptr, e.pred2_dev,
+                            e.llapor_scratch, e.sc);
+      if (s != PS_OK) fail(s, ps_last_error());
+      e.st.kernel_launches += 2;
+    }
     // --- K2 permute indices ------------------------------------------------------
     // Prefill-sized batches gather x into contiguous permuted rows (TMA operand of the
     // tcgen05 path) and need the offsets on the host for tile scheduling.
@@ -926,13 +940,13 @@ void layer_forward(ps_engine_s& e, int l, const float* x, const uint8_t* follow,
       // counts | pred | offsets (| perm_src for the host lane) in one copy, on the side
       // stream: the compute stream goes straight on to the resident FFN while the copy
       // engine brings the scheduling inputs to the host.
-      const size_t n_sched = 3 * static_cast<size_t>(Et) + 1 + (e.lane ? static_cast<size_t>(B) * Kt : 0);
+      const size_t n_sched = 4 * static_cast<size_t>(Et) + 1 + (e.lane ? static_cast<size_t>(B) * Kt : 0);
       ph.route1 = take_event(e);  // end of the scheduling-point kernels = start of the early FFN
       PS_CUDA(cudaEventRecord(ph.route1, e.sc));
       PS_CUDA(cudaStreamWaitEvent(e.s_d2h, ph.route1, 0));
       PS_CUDA(cudaMemcpyAsync(e.pinned_counts, e.sched_dev, sizeof(int32_t) * n_sched, cudaMemcpyDeviceToHost,
                               e.s_d2h));
-      e.src = {e.offsets, e.perm_src, Kt, e.x_bf16, B * Kt, e.pinned_counts + 2 * Et};
+      e.src = {e.offsets, e.perm_src, Kt, e.x_bf16, B * Kt, e.pinned_counts + 3 * Et};
       if (e.lane)  // the host lane gathers its rows from x
         PS_CUDA(cudaMemcpyAsync(e.lane_x, e.x_bf16, sizeof(uint16_t) * B * H, cudaMemcpyDeviceToHost, e.s_d2h));
       PS_CUDA(cudaEventRecord(e.ev_routed, e.s_d2h));
@@ -1001,7 +1015,7 @@ void layer_forward(ps_engine_s& e, int l, const float* x, const uint8_t* follow,
     // Wait for the routing result on the host (the only per-layer host sync).
     PS_CUDA(cudaEventSynchronize(e.ev_routed));
     if (!e.ep) {
-      const int32_t* off_h = e.pinned_counts + 2 * Et;  // aggregate_layer_loads = diff of K2's offsets
+      const int32_t* off_h = e.pinned_counts + 3 * Et;  // aggregate_layer_loads = diff of K2's offsets
       for (int ex = 0; ex < Et; ++ex) counts_l[ex] = off_h[ex + 1] - off_h[ex];
       if (predict) {
         std::memcpy(pred_l.data(), e.pinned_counts + Et, sizeof(int32_t) * E);
@@ -1013,8 +1027,17 @@ void layer_forward(ps_engine_s& e, int l, const float* x, const uint8_t* follow,
       } else {
         std::fill(pred_l.begin(), pred_l.end(), dense_next ? (B * K) / E : 0);
       }
+      std::fill(e.pred2_l.begin(), e.pred2_l.end(), 0);
+      if (predict2) {
+        std::memcpy(e.pred2_l.data(), e.pinned_counts + 2 * Et, sizeof(int32_t) * E);
+      } else if (want_pred2 && e.pred_kind == PS_PRED_GATE) {
+        std::copy(counts_l.begin(), counts_l.begin() + E, e.pred2_l.begin());
+      } else if (want_pred2 && e.pred_kind == PS_PRED_STATS) {
+        for (int j = 0; j < K; ++j) e.pred2_l[e.stats_rank[static_cast<size_t>(l + 2) * E + j]] = B;
+      }
     } else {
       ep_dispatch_rows(e, B, counts_l, pred_l);
+      std::fill(e.pred2_l.begin(), e.pred2_l.end(), 0);
     }
     if (!early) {
       ffn(e, grp, counts_l.data(), B, true, true);
@@ -1069,24 +1092,28 @@ void layer_forward(ps_engine_s& e, int l, const float* x, const uint8_t* follow,
     // --- R4: scheduler inputs ------------------------------------------------------
     cur.clear();
     nxt.clear();
+    e.nxt2.clear();
     for (int ex = 0; ex < E; ++ex) {
       if (counts_l[ex] > 0 && !e.resident[static_cast<size_t>(l) * E + ex] && !is_ready(l, ex))
         cur.push_back({ex, l, counts_l[ex], PS_LOC_HOST});
       if (l + 1 < L && pred_l[ex] > 0 && !e.resident[static_cast<size_t>(l + 1) * E + ex] && !is_ready(l + 1, ex))
         nxt.push_back({ex, l + 1, pred_l[ex], PS_LOC_HOST});
+      if (l + 2 < L && e.pred2_l[ex] > 0 && !e.resident[static_cast<size_t>(l + 2) * E + ex] && !is_ready(l + 2, ex))
+        e.nxt2.push_back({ex, l + 2, e.pred2_l[ex], PS_LOC_HOST});
     }
     auto by_tokens = [](const ps_expert_load& a, const ps_expert_load& b) {
       return a.tokens != b.tokens ? a.tokens < b.tokens : a.expert < b.expert;
     };
     std::sort(cur.begin(), cur.end(), by_tokens);
     std::sort(nxt.begin(), nxt.end(), by_tokens);
+    std::sort(e.nxt2.begin(), e.nxt2.end(), by_tokens);
     ps_layer_inputs in{};
     in.e_cur = cur.data();
     in.n_cur = static_cast<int32_t>(cur.size());
     in.e_next = nxt.data();
     in.n_next = static_cast<int32_t>(nxt.size());
-    in.e_next2 = nullptr;
-    in.n_next2 = 0;
+    in.e_next2 = e.nxt2.empty() ? nullptr : e.nxt2.data();
+    in.n_next2 = static_cast<int32_t>(e.nxt2.size());
     in.params = e.cfg.cost;
     in.params.alpha = static_cast<int64_t>(std::max(0.0, e.io_free_us - now_us()));
     in.stats = e.stats[group_of_layer(e.cfg.spec, l)];
@@ -1104,8 +1131,8 @@ void layer_forward(ps_engine_s& e, int l, const float* x, const uint8_t* follow,
     // GPU-only executor loads them after ondemand_seq.
     e.cpu_jobs.clear();
     if (e.lane && plan.n_cpu > 0) {
-      const int32_t* off = e.pinned_counts + 2 * Et;
-      const int32_t* perm = e.pinned_counts + 3 * Et + 1;
+      const int32_t* off = e.pinned_counts + 3 * Et;
+      const int32_t* perm = e.pinned_counts + 4 * Et + 1;
       for (int i = 0; i < plan.n_cpu; ++i) {
         const int ex = plan.cpu_set[i].expert;
         const uint16_t* slab = e.host_slab[static_cast<size_t>(l) * E + ex];
@@ -1237,6 +1264,35 @@ void layer_forward(ps_engine_s& e, int l, const float* x, const uint8_t* follow,
         e.io->push(job);
       }
     }
+    // --- lookahead top-up (cfg.lookahead = d > 0; a labelled extension of PreSched, off
+    // in the reference configuration): behind PreSched's own batch, queue the remaining
+    // predicted non-resident experts of layers l+1 .. l+d (d <= 2), hottest first, up to
+    // each target layer's slot cap. Whatever has not started by the next scheduling
+    // point is cancelled there (R2), so the channel never idles while a predicted expert
+    // is still missing; the host lane takes whatever did not arrive in time.
+    if (e.cfg.lookahead > 0 && !e.ep) {
+      auto pending = [&](int layer, int ex) {
+        for (IoJob* j : e.pending_pf)
+          if (j->layer == layer && j->expert == ex) return true;
+        return is_ready(layer, ex);
+      };
+      for (int d = 1; d <= std::min(2, e.cfg.lookahead) && l + d < L; ++d) {
+        const std::vector<ps_expert_load>& cand = d == 1 ? nxt : e.nxt2;
+        int used = 0;
+        for (auto& sl : e.pf_pool) used += sl->in_use && sl->target_layer == l + d;
+        for (auto it = cand.rbegin(); it != cand.rend() && used < e.cfg.prefetch_slots; ++it) {
+          if (pending(l + d, it->expert)) continue;
+          Slot* slot = take_prefetch_slot(e, l + d);
+          IoJob* job = new_job(e, kPrefetch, l + d, it->expert, it->tokens, slot);
+          job->issue_group = group_of_layer(e.cfg.spec, l);
+          e.pending_pf.push_back(job);
+          push_modelled(e);
+          e.io->push(job);
+          ++used;
+          e.st.lookahead_prefetches++;
+        }
+      }
+    }
   }
 }
 
@@ -1360,6 +1416,7 @@ void create_engine(const ps_engine_config& cfg, ps_engine_s& e) {
   require(e.S >= 0 && e.S <= 32, "engine: n_shared out of range [0, 32]");
   require(e.S == 0 || !cfg.ep, "engine: shared experts are not supported with expert parallelism");
   if (e.cfg.prefetch_slots <= 0) e.cfg.prefetch_slots = 8;
+  require(e.cfg.lookahead >= 0 && e.cfg.lookahead <= 2, "engine: lookahead must be 0, 1 or 2");
   e.n_split = ps_ffn_down_splits(e.H, e.F);
   e.slab_elems = sp.expert_bytes / 2;
   for (auto& h : e.stats) h = {1.0, 0.0, 32};
@@ -1553,7 +1610,9 @@ void create_engine(const ps_engine_config& cfg, ps_engine_s& e) {
   }
   // Prefetch slots for two live target layers (R8 cap per layer) up front: a cudaMalloc
   // of an expert-sized buffer inside a step costs milliseconds of host time.
-  for (size_t i = 0; i < std::min<size_t>(2 * static_cast<size_t>(e.cfg.prefetch_slots), n_host); ++i) {
+  // (lookahead 2 keeps a third target layer live: l+1 and l+2 queued while l's land)
+  const size_t live_layers = e.cfg.lookahead >= 2 ? 3 : 2;
+  for (size_t i = 0; i < std::min<size_t>(live_layers * static_cast<size_t>(e.cfg.prefetch_slots), n_host); ++i) {
     auto s = std::make_unique<Slot>();
     PS_CUDA(cudaMalloc(&s->dev, sp.expert_bytes));
     if (e.z_cap) PS_CUDA(cudaMalloc(&s->zdev, e.z_cap));
@@ -1582,7 +1641,7 @@ void create_engine(const ps_engine_config& cfg, ps_engine_s& e) {
     PS_CUDA(cudaMalloc(&ld.weights, sizeof(float) * B * e.E));
     PS_CUDA(cudaMalloc(&ld.ids, sizeof(int32_t) * rows));
   }
-  const size_t n_sched = 3 * static_cast<size_t>(e.Et) + 1 + rows_t;
+  const size_t n_sched = 4 * static_cast<size_t>(e.Et) + 1 + rows_t;
   PS_CUDA(cudaMalloc(&e.sched_dev, sizeof(int32_t) * n_sched));
   PS_CUDA(cudaMemsetAsync(e.sched_dev, 0, sizeof(int32_t) * n_sched, e.sc));
   PS_CUDA(cudaHostAlloc(&e.pinned_counts, sizeof(int32_t) * n_sched, cudaHostAllocDefault));
@@ -1590,8 +1649,9 @@ void create_engine(const ps_engine_config& cfg, ps_engine_s& e) {
   PS_CUDA(cudaMalloc(&e.route_ws, sizeof(int32_t)));
   PS_CUDA(cudaMemsetAsync(e.route_ws, 0, sizeof(int32_t), e.sc));
   e.pred_dev = e.sched_dev + e.Et;
-  e.offsets = e.sched_dev + 2 * e.Et;
-  e.perm_src = e.sched_dev + 3 * e.Et + 1;
+  e.pred2_dev = e.sched_dev + 2 * e.Et;
+  e.offsets = e.sched_dev + 3 * e.Et;
+  e.perm_src = e.sched_dev + 4 * e.Et + 1;
   if (e.S) {
     PS_CUDA(cudaMalloc(&e.ids_ext, sizeof(int32_t) * rows_t));
     PS_CUDA(cudaMalloc(&e.w_ext, sizeof(float) * B * e.Et));
@@ -1868,6 +1928,21 @@ ps_status ps_engine_last_timeline(ps_engine e, ps_timeline* out, int32_t* truth_
     if (out->layer_end) std::copy(e->last_layer_end.begin(), e->last_layer_end.end(), out->layer_end);
     if (truth_out) std::copy(e->last_truth.begin(), e->last_truth.end(), truth_out);
     if (resident_out) std::copy(e->resident.begin(), e->resident.end(), resident_out);
+  });
+}
+
+ps_status ps_engine_last_routing(ps_engine e, int32_t* ids_out, float* weights_out) {
+  return guarded([&] {
+    require(e != nullptr, "ps_engine_last_routing: null engine");
+    require(!e->in_step && e->step_B > 0, "ps_engine_last_routing: no completed step");
+    const size_t B = static_cast<size_t>(e->step_B);
+    for (int l = 0; l < e->L; ++l) {
+      if (ids_out)
+        PS_CUDA(cudaMemcpy(ids_out + l * B * e->K, e->layer[l].ids, sizeof(int32_t) * B * e->K, cudaMemcpyDeviceToHost));
+      if (weights_out)
+        PS_CUDA(cudaMemcpy(weights_out + l * B * e->E, e->layer[l].weights, sizeof(float) * B * e->E,
+                           cudaMemcpyDeviceToHost));
+    }
   });
 }
 

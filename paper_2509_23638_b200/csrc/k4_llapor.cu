@@ -24,6 +24,7 @@
 #include <vector>
 
 #include "device_common.cuh"
+#include "llapor_model.hpp"
 
 namespace ps {
 
@@ -52,7 +53,9 @@ struct NetDev {  // device pointers into one allocation; kernel parameter
 
 struct ps_llapor_s {
   ps_model_spec spec{};
+  ps::HostModel host;            // f64 checkpoint model (fine_tune / save operate on it)
   std::vector<ps::NetDev> nets;  // index = target layer; nets[0] unused
+  std::vector<uint8_t> stale;    // host net changed since its device copy (or never uploaded)
   std::vector<void*> allocs;
   int max_p = 0, max_in = 0, max_width = 0;
 };
@@ -342,19 +345,8 @@ mlp_kernel(const __grid_constant__ NetDev net, const float* __restrict__ part, i
 
 // ------------------------------------------------------------------ host side
 
-struct HostNet {
-  int target = 0, group = 1, E = 0;
-  std::vector<double> mean;
-  int p_rows = 0, p_cols = 0;
-  std::vector<double> comp;
-  struct Blk { int rows, cols; std::vector<double> w, b; };
-  std::vector<Blk> blocks, res;
-  std::vector<double> gate_w;
-  double gate_b = 0;
-  Blk out;
-};
-
-void upload(ps_llapor_s& m, int layer, const HostNet& hn) {
+// Shape checks of a trained net (the GPU kernels' limits) and its NetDev dimensions.
+NetDev net_dims(const ps_llapor_s& m, const HostNet& hn) {
   NetDev d{};
   d.P = hn.p_rows;
   d.E = hn.E;
@@ -362,6 +354,8 @@ void upload(ps_llapor_s& m, int layer, const HostNet& hn) {
   d.n_res = static_cast<int>(hn.res.size());
   require(d.n_blocks >= 1 && d.n_blocks <= kMaxBlocks && d.n_res <= kMaxBlocks, "LLaPor: unsupported block count");
   require(hn.E == m.spec.experts_per_layer && hn.E <= kMaxE, "LLaPor: expert count mismatch");
+  require(hn.p_cols == m.spec.hidden_dim || hn.p_rows == 0, "LLaPor: PCA width != hidden_dim");
+  require(static_cast<int>(hn.mean.size()) == hn.p_cols, "LLaPor: PCA mean size != hidden_dim");
   d.in_dim = d.P + 2 * d.E;
   d.dims[0] = hn.blocks[0].cols;
   require(d.dims[0] == d.in_dim, "LLaPor: first block input dim != pca + 2E");
@@ -370,15 +364,41 @@ void upload(ps_llapor_s& m, int layer, const HostNet& hn) {
     d.dims[j + 1] = hn.blocks[j].rows;
   }
   d.width = d.dims[d.n_blocks];
+  for (const HostBlk& r : hn.res) require(r.rows == d.width && r.cols == d.width, "LLaPor: residual block shape");
+  require(hn.res.empty() || static_cast<int>(hn.gate_w.size()) == d.P, "LLaPor: gate size != pca dim");
   require(hn.out.cols == d.width && hn.out.rows == d.E, "LLaPor: output block shape");
+  return d;
+}
 
+// Host nets -> kernel-side bookkeeping (no device work): validates every trained net and
+// marks it for upload before its first forward.
+void adopt(ps_llapor_s& m) {
+  const int n = static_cast<int>(m.host.nets.size());
+  m.nets.assign(std::max(n, 1), NetDev{});
+  m.stale.assign(std::max(n, 1), 0);
+  for (int l = 0; l < n; ++l) {
+    const HostNet& hn = m.host.nets[l];
+    if (hn.blocks.empty()) continue;  // untrained (nets[0])
+    NetDev d = net_dims(m, hn);
+    d.valid = 1;
+    m.nets[l] = d;
+    m.stale[l] = 1;
+    m.max_p = std::max(m.max_p, d.P);
+    m.max_in = std::max(m.max_in, d.in_dim);
+    m.max_width = std::max(m.max_width, d.width);
+  }
+}
+
+// One contiguous f32 device copy of net `layer` (arrays 16-byte aligned). Earlier copies
+// stay allocated until ps_llapor_free: kernels already enqueued may still read them.
+void upload(ps_llapor_s& m, int layer) {
+  const HostNet& hn = m.host.nets[layer];
+  NetDev d = net_dims(m, hn);
   std::vector<float> buf;
-  std::vector<size_t> offs;
   auto put = [&](const std::vector<double>& v) {
     size_t o = buf.size();
-    offs.push_back(o);
     for (double x : v) buf.push_back(static_cast<float>(x));
-    while (buf.size() % 4) buf.push_back(0.f);  // 16-byte alignment of every array
+    while (buf.size() % 4) buf.push_back(0.f);
     return o;
   };
   size_t o_mean = put(hn.mean), o_comp = put(hn.comp);
@@ -407,44 +427,9 @@ void upload(ps_llapor_s& m, int layer, const HostNet& hn) {
   d.o_ow = rel(o_ow);
   d.o_ob = rel(o_ob);
   d.valid = 1;
-  if (layer >= static_cast<int>(m.nets.size())) m.nets.resize(layer + 1);
   m.nets[layer] = d;
-  m.max_p = std::max(m.max_p, d.P);
-  m.max_in = std::max(m.max_in, d.in_dim);
-  m.max_width = std::max(m.max_width, d.width);
+  m.stale[layer] = 0;
 }
-
-// LLPC v1 reader (layout written by save_checkpoint, predictor.cpp:833-864).
-struct Reader {
-  std::ifstream in;
-  template <typename T> T rd() {
-    T v{};
-    in.read(reinterpret_cast<char*>(&v), sizeof(T));
-    if (!in) fail(PS_ERUNTIME, "checkpoint: truncated file");
-    return v;
-  }
-  std::vector<double> vec() {
-    uint64_t n = rd<uint64_t>();
-    if (n > (1ull << 31)) fail(PS_ERUNTIME, "checkpoint: corrupt vector length");
-    std::vector<double> v(n);
-    in.read(reinterpret_cast<char*>(v.data()), static_cast<std::streamsize>(n * sizeof(double)));
-    if (!in) fail(PS_ERUNTIME, "checkpoint: truncated file");
-    return v;
-  }
-  void mat(int& r, int& c, std::vector<double>& a) {
-    r = rd<int32_t>();
-    c = rd<int32_t>();
-    a = vec();
-    if (a.size() != static_cast<size_t>(r) * c) fail(PS_ERUNTIME, "checkpoint: corrupt matrix");
-  }
-  HostNet::Blk blk() {
-    HostNet::Blk b;
-    mat(b.rows, b.cols, b.w);
-    b.b = vec();
-    return b;
-  }
-  void hyper() { rd<double>(); rd<double>(); rd<int32_t>(); rd<int32_t>(); rd<int32_t>(); }
-};
 
 }  // namespace
 }  // namespace ps
@@ -455,51 +440,12 @@ extern "C" {
 
 ps_status ps_llapor_load(const char* path, ps_llapor* out, ps_model_spec* spec_out) {
   return guarded([&] {
-    Reader r;
-    r.in.open(path, std::ios::binary);
-    if (!r.in) fail(PS_ERUNTIME, std::string("load_checkpoint: cannot open ") + path);
-    char magic[4];
-    r.in.read(magic, 4);
-    if (!r.in || std::memcmp(magic, "LLPC", 4) != 0) fail(PS_ERUNTIME, "load_checkpoint: bad magic");
-    if (r.rd<uint32_t>() != 1) fail(PS_ERUNTIME, "load_checkpoint: unsupported version");
-    r.rd<uint64_t>();  // trace checksum
+    require(path && out, "ps_llapor_load: null argument");
     auto m = std::make_unique<ps_llapor_s>();
-    ps_model_spec& s = m->spec;
-    s.num_layers = r.rd<int32_t>();
-    s.experts_per_layer = r.rd<int32_t>();
-    s.top_k = r.rd<int32_t>();
-    s.expert_bytes = r.rd<uint64_t>();
-    s.hidden_dim = r.rd<int32_t>();
-    s.group_begin_middle = r.rd<int32_t>();
-    s.group_begin_output = r.rd<int32_t>();
-    r.rd<double>(); r.rd<double>(); r.rd<int32_t>(); r.rd<int32_t>();  // lambda gamma epochs warmup
-    r.hyper(); r.hyper(); r.hyper();
-    r.rd<double>(); r.rd<double>(); r.rd<double>(); r.rd<int32_t>(); r.rd<uint64_t>();
-    const uint32_t num = r.rd<uint32_t>();
-    m->nets.resize(std::max<uint32_t>(num, 1));
-    for (uint32_t i = 0; i < num; ++i) {
-      HostNet hn;
-      hn.target = r.rd<int32_t>();
-      hn.group = r.rd<uint8_t>();
-      hn.E = r.rd<int32_t>();
-      r.rd<double>();  // dropout
-      hn.mean = r.vec();
-      r.mat(hn.p_rows, hn.p_cols, hn.comp);
-      r.vec();  // eigenvalues
-      r.rd<int32_t>();
-      r.rd<int32_t>();
-      const uint32_t nb = r.rd<uint32_t>();
-      for (uint32_t j = 0; j < nb; ++j) hn.blocks.push_back(r.blk());
-      const uint32_t nr = r.rd<uint32_t>();
-      for (uint32_t j = 0; j < nr; ++j) hn.res.push_back(r.blk());
-      hn.gate_w = r.vec();
-      hn.gate_b = r.rd<double>();
-      hn.out = r.blk();
-      if (hn.blocks.empty()) continue;  // untrained (nets[0])
-      require(hn.p_cols == s.hidden_dim || hn.p_rows == 0, "LLaPor: PCA width != hidden_dim");
-      upload(*m, static_cast<int>(i), hn);
-    }
-    if (spec_out) *spec_out = s;
+    m->host = read_llpc(path);
+    m->spec = m->host.spec;
+    adopt(*m);
+    if (spec_out) *spec_out = m->spec;
     *out = m.release();
   });
 }
@@ -509,24 +455,32 @@ ps_status ps_llapor_random(const ps_model_spec* spec, int pca_in, int pca_mid, i
   return guarded([&] {
     auto m = std::make_unique<ps_llapor_s>();
     m->spec = *spec;
+    m->host.spec = *spec;
     const int L = spec->num_layers, E = spec->experts_per_layer, H = spec->hidden_dim;
-    m->nets.resize(L);
+    m->host.nets.resize(L);
+    m->host.nets[0].E = E;
+    m->host.nets[0].group = 0;
     for (int l = 1; l < L; ++l) {
       const int g = l < spec->group_begin_middle ? 0 : l < spec->group_begin_output ? 1 : 2;
       const int P = std::min(g == 1 ? pca_mid : pca_in, H);
       const int width = g == 1 ? width_mid : width_in;
       const int nblocks = g == 1 ? 3 : 2;  // TrainConfig defaults (predictor.hpp:97-100)
       std::mt19937_64 rng(seed ^ (0x9e3779b97f4a7c15ull * (l + 1)));
-      HostNet hn;
+      HostNet& hn = m->host.nets[l];
+      hn.target = l;
+      hn.group = g;
       hn.E = E;
+      hn.dropout = m->host.cfg.dropout;
       hn.p_rows = P;
       hn.p_cols = H;
+      hn.req_dim = hn.eff_dim = P;
       hn.mean.assign(H, 0.0);
+      hn.eigen.assign(P, 1.0);
       std::normal_distribution<double> gauss(0.0, 1.0 / std::sqrt(static_cast<double>(H)));
       hn.comp.resize(static_cast<size_t>(P) * H);
       for (double& v : hn.comp) v = gauss(rng);
       auto init = [&](int o, int i) {  // Xavier-uniform (predictor.cpp:486-494)
-        HostNet::Blk b{o, i, std::vector<double>(static_cast<size_t>(o) * i), std::vector<double>(o, 0.0)};
+        HostBlk b{o, i, std::vector<double>(static_cast<size_t>(o) * i), std::vector<double>(o, 0.0)};
         std::uniform_real_distribution<double> u(-std::sqrt(6.0 / (i + o)), std::sqrt(6.0 / (i + o)));
         for (double& v : b.w) v = u(rng);
         return b;
@@ -540,8 +494,8 @@ ps_status ps_llapor_random(const ps_model_spec* spec, int pca_in, int pca_mid, i
         for (double& v : hn.gate_w) v = u(rng);
       }
       hn.out = init(E, width);
-      upload(*m, l, hn);
     }
+    adopt(*m);
     *out = m.release();
   });
 }
@@ -551,6 +505,45 @@ ps_status ps_llapor_free(ps_llapor m) {
     if (!m) return;
     for (void* p : m->allocs) cudaFree(p);
     delete m;
+  });
+}
+
+ps_status ps_llapor_save(ps_llapor m, const char* path) {
+  return guarded([&] {
+    require(m && path, "ps_llapor_save: null argument");
+    write_llpc(m->host, path);
+  });
+}
+
+ps_status ps_llapor_fine_tune(ps_llapor m, int layer, int n, const double* hidden_prev, const int32_t* active_prev,
+                              int k_prev, const double* gate_prev, const int32_t* active, int k, int steps, double lr) {
+  return guarded([&] {
+    require(m && (n == 0 || (hidden_prev && active_prev && gate_prev && active)), "ps_llapor_fine_tune: null argument");
+    if (layer < 1 || layer >= static_cast<int>(m->host.nets.size()) || m->host.nets[layer].blocks.empty())
+      fail(PS_ERANGE, "llapor net for layer " + std::to_string(layer) + " is untrained/out of range");
+    require(n >= 1 && steps >= 0 && k >= 1 && k_prev >= 1, "ps_llapor_fine_tune: bad n/k/steps");
+    HostNet& net = m->host.nets[layer];
+    const int H = m->spec.hidden_dim, E = net.E;
+    std::vector<HostSample> samples(n);
+    for (int t = 0; t < n; ++t) {  // build_samples (predictor.cpp:596-613) on the caller's observations
+      HostSample& s = samples[t];
+      s.reduced = host_pca_apply(net, hidden_prev + static_cast<size_t>(t) * H);
+      s.onehot.assign(E, 0.0);
+      s.labels.assign(E, 0.0);
+      for (int j = 0; j < k_prev; ++j) {
+        const int e = active_prev[static_cast<size_t>(t) * k_prev + j];
+        if (e < 0 || e >= E) fail(PS_ERANGE, "ps_llapor_fine_tune: expert id out of range");
+        s.onehot[e] = 1.0;
+      }
+      for (int j = 0; j < k; ++j) {
+        const int e = active[static_cast<size_t>(t) * k + j];
+        if (e < 0 || e >= E) fail(PS_ERANGE, "ps_llapor_fine_tune: expert id out of range");
+        s.labels[e] = 1.0;
+      }
+      s.gate.assign(gate_prev + static_cast<size_t>(t) * E, gate_prev + static_cast<size_t>(t + 1) * E);
+    }
+    host_fine_tune(net, samples, steps, lr, m->host.cfg);
+    m->stale[layer] = 1;  // re-uploaded before the next forward of this net
   });
 }
 
@@ -567,6 +560,7 @@ ps_status ps_llapor_forward(ps_llapor m, int layer, const float* hidden, const i
     require(m != nullptr, "ps_llapor_forward: null model");
     if (layer < 1 || layer >= static_cast<int>(m->nets.size()) || !m->nets[layer].valid)
       fail(PS_ERANGE, "llapor net for layer " + std::to_string(layer) + " is untrained/out of range");
+    if (m->stale[layer]) upload(*m, layer);  // first use, or fine-tuned since the last upload
     const NetDev& net = m->nets[layer];
     require(k >= 1 && k <= net.E && k_prev >= 1 && k_prev <= 32 && B >= 0, "ps_llapor_forward: bad k/B");
     require(m->spec.hidden_dim <= 16 * kPcaChunk, "ps_llapor_forward: hidden_dim > 8192 unsupported");

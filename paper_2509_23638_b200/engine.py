@@ -114,7 +114,7 @@ class Engine:
                  resident=None, trace_hidden=None, trace_follow=None, policy: str = "presched",
                  predictor=None, cost=None, prefetch_slots: int = 8, device: int = 0, ep=None,
                  n_shared: int = 0, host_threads: int = 0, compress_host: bool = False,
-                 predictor_kind: str = "auto", stats_ranking=None, expert_weights=None):
+                 predictor_kind: str = "auto", stats_ranking=None, expert_weights=None, lookahead: int = 0):
         from . import parse_policy, plan_residency, trace_inputs  # noqa: F401
         self.lib = load()
         self.spec = spec
@@ -151,6 +151,7 @@ class Engine:
         cfg.n_shared = n_shared
         cfg.host_threads = host_threads
         cfg.compress_host = int(bool(compress_host))
+        cfg.lookahead = lookahead
         kinds = {"auto": 0, "llapor": 1, "gate": 2, "stats": 3, "perfect": 4, "none": 5}
         cfg.predictor_kind = kinds[predictor_kind]
         if stats_ranking is not None:
@@ -271,6 +272,31 @@ class Engine:
         out = np.zeros((self.spec.num_layers, self.spec.experts_per_layer), np.int32)
         check(self.lib.ps_engine_last_predictions(self.h, out.ctypes.data_as(C.c_void_p)))
         return out
+
+    def last_routing(self, B: int):
+        """(ids [L,B,k] i32, gate weights [L,B,E] f32) of the last completed step."""
+        L, E, k = self.spec.num_layers, self.spec.experts_per_layer, self.spec.top_k
+        ids = np.empty((L, B, k), np.int32)
+        w = np.empty((L, B, E), np.float32)
+        check(self.lib.ps_engine_last_routing(self.h, ids.ctypes.data_as(C.c_void_p), w.ctypes.data_as(C.c_void_p)))
+        return ids, w
+
+    def fine_tune_predictor(self, predictor, hidden_lbh, steps: int = 1, lr: float = 1e-3, layers=None):
+        """Online LLaPor fine_tune (predictor.cpp:654-663) on the last step's observations:
+        net l learns (hidden, routing) of layer l-1 -> routing of layer l. hidden_lbh:
+        the step's gating inputs [L,B,H] (host). The engine's next step uses the
+        updated nets (their GPU copies refresh before the next forward)."""
+        L = self.spec.num_layers
+        B = hidden_lbh.shape[1]
+        ids, w = self.last_routing(B)
+        k = self.spec.top_k
+        for l in (layers or range(1, L)):
+            hid = np.ascontiguousarray(hidden_lbh[l - 1], np.float64)
+            gp = np.ascontiguousarray(w[l - 1], np.float64)
+            ap, a = np.ascontiguousarray(ids[l - 1]), np.ascontiguousarray(ids[l])
+            check(self.lib.ps_llapor_fine_tune(predictor, l, B, hid.ctypes.data_as(C.c_void_p),
+                                               ap.ctypes.data_as(C.c_void_p), k, gp.ctypes.data_as(C.c_void_p),
+                                               a.ctypes.data_as(C.c_void_p), k, steps, lr))
 
     def set_cost(self, t_io, t_g, t_attn, beta, startup):
         """Replace the PreSched cost parameters (ps_engine_set_cost)."""
