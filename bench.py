@@ -276,12 +276,12 @@ def run_ours(args):
     lib = ps.load()
     predictor = C.c_void_p()
     ps.check(lib.ps_llapor_random(C.byref(spec), 256, 512, 32, 48, 3, C.byref(predictor)))
-    host_threads = args.host_threads if args.host_threads >= 0 else default_host_threads()
+    host_threads = args.host_threads if args.host_threads >= 0 else default_host_threads(world)
     t_create = time.perf_counter()
     e = eng.Engine(spec, gen, max_batch=B, weight_seed=args.weight_seed, gate=gate, budget_bytes=budget_bytes,
                    resident=resident, policy=args.policy, predictor=predictor, device=local, ep=ep,
-                   host_threads=host_threads if world == 1 else 0, compress_host=bool(args.compress),
-                   predictor_kind=args.predictor, lookahead=args.lookahead)
+                   host_threads=host_threads, compress_host=bool(args.compress),
+                   predictor_kind=args.predictor, lookahead=args.lookahead, steal_late=bool(args.steal_late))
     t_create = time.perf_counter() - t_create
     measured_cost = e.stats()["cost"]
 
@@ -356,6 +356,13 @@ def run_ours(args):
     if rank == 0 and not args.no_checksum:
         checksum = step_checksum(args, spec, gate, hidden[(S - 1) * B:S * B], follow[(S - 1) * B:S * B],
                                  zipf, y_h.numpy(), ids_h.numpy())
+
+    # BASELINE config 5 (N > 1 only): Mixtral EP with a GLOBAL batch of 64 decode tokens
+    # and a 4096-token prefill chunk, split over the ranks, same budget and executor.
+    config5 = None
+    if world > 1 and not args.no_config5:
+        config5 = config5_legs(args, spec, gen, gate, zipf, ep, resident, budget_bytes, predictor, host_threads,
+                               local, rank, world, dist)
 
     # Same steps with every expert resident (budget 100 %): the HBM-bound MoE layer.
     all_res = None
@@ -469,12 +476,72 @@ def run_ours(args):
         "clocks": clocks,
         "gpu_launches": st["kernel_launches"],
         "nccl_init": nccl_init_lines() if world > 1 else None,
+        "config5_ep": config5,
         "wall_s_timed": wall, "engine_create_s": t_create,
         "cost_params_us": st["cost"],
     }
     print(json.dumps(line))
     if dist:
         dist.destroy_process_group()
+
+
+def config5_legs(args, spec, gen, gate, zipf, ep, resident, budget_bytes, predictor, host_threads, local, rank, world,
+                 dist):
+    """EP decode at a global batch of 64 and a 4096-token prefill chunk (BASELINE config 5):
+    each rank routes 64/N (4096/N) tokens of one trace, dispatches them to the owners over
+    NCCL, runs its experts through its own cache/loader/lane, combines at home. Device
+    time per step is the max over ranks; value = global tokens / that time."""
+    import torch
+
+    import paper_2509_23638_b200 as ps
+    from paper_2509_23638_b200 import engine as eng
+    L, H = spec.num_layers, spec.hidden_dim
+    Bd, Tp = 64 // world, 4096 // world
+    e = eng.Engine(spec, gen, max_batch=max(Bd, Tp), weight_seed=args.weight_seed, gate=gate,
+                   budget_bytes=budget_bytes, resident=resident, policy=args.policy, predictor=predictor,
+                   device=local, ep=ep, host_threads=host_threads, compress_host=bool(args.compress),
+                   lookahead=args.lookahead, steal_late=bool(args.steal_late))
+    out = {}
+    try:
+        S = args.warmup + args.steps
+        _, hd, fd, _ = ps.trace_inputs(gen, spec, 64 * S, 2000, want_gate=False)
+
+        def timed(inputs, steps, warm):
+            y = torch.empty(L, inputs[0][0].shape[1], H, dtype=torch.float32, device="cuda")
+            for i in range(warm):
+                e.step_device(inputs[i][0], inputs[i][1], y)
+            torch.cuda.synchronize()
+            e.reset_stats()
+            dist.barrier()
+            for i in range(warm, warm + steps):
+                e.step_device(inputs[i % len(inputs)][0], inputs[i % len(inputs)][1], y)
+            torch.cuda.synchronize()
+            st = e.stats()
+            t = torch.tensor([st["step_ms_total"] / max(1, st["steps"])], device="cuda")
+            dist.all_reduce(t, op=dist.ReduceOp.MAX)
+            return float(t.item()), st
+
+        dec = []
+        for s_ in range(S):
+            tok = hd[s_ * 64 + rank * Bd:s_ * 64 + (rank + 1) * Bd]
+            fol = fd[s_ * 64 + rank * Bd:s_ * 64 + (rank + 1) * Bd]
+            dec.append((torch.as_tensor(np.ascontiguousarray(tok.transpose(1, 0, 2), np.float32), device="cuda"),
+                        torch.as_tensor(np.ascontiguousarray(fol.T), device="cuda")))
+        ms, st = timed(dec, args.steps, args.warmup)
+        out["decode_global_batch_64"] = {"value": 64 / (ms / 1e3), "unit": "tokens/s", "ms_per_step": ms,
+                                         "tokens_per_rank": Bd, "cpu_experts_per_step_rank0": st["cpu_experts"] /
+                                         max(1, st["steps"]), "ondemand_loads_per_step_rank0":
+                                         st["ondemand_loads"] / max(1, st["steps"])}
+        g = torch.Generator(device="cuda").manual_seed(11 + rank)
+        ph = torch.randn(L, Tp, H, device="cuda", generator=g)
+        ph /= ph.norm(dim=-1, keepdim=True)
+        pf = torch.zeros(L, Tp, dtype=torch.uint8, device="cuda")
+        ms, st = timed([(ph, pf)], max(2, args.prefill_steps), 2)
+        out["prefill_4096"] = {"value": 4096 / (ms / 1e3), "unit": "tokens/s", "ms_per_step": ms,
+                               "tokens_per_rank": Tp, "tc_launches_rank0": st["tc_launches"]}
+    finally:
+        e.close()
+    return out
 
 
 def nccl_init_lines(limit=6):
@@ -512,7 +579,7 @@ def step_checksum(args, spec, gate, hidden, follow, zipf, y, ids, layers=None):
             "source": "last e2e step (ps_engine_decode_step_host) vs oracle/or_route_trace + or_moe_layer"}
 
 
-def default_host_threads():
+def default_host_threads(world=1):
     """Host expert lane threads: one per core, at most 16 (the engine and I/O threads
     mostly sleep on futexes/blocking events): on the B200 box's 16-core host 16 threads
     stream 178-182 GB/s vs 170-177 with 15 and 168-175 with 14 in alternating runs
@@ -523,7 +590,9 @@ def default_host_threads():
             return 0
     except OSError:
         return 0
-    return max(0, min(16, os.cpu_count() or 1))
+    # one lane per rank (EP: every rank's lane computes its own cpu_set): the host's
+    # cores split between the ranks of this node
+    return max(1, min(16, (os.cpu_count() or 1) // max(1, world)))
 
 
 def decode_summary(st, dev_ms, N, B, L):
@@ -542,6 +611,7 @@ def decode_summary(st, dev_ms, N, B, L):
                    "prefetches_per_step": st["prefetches_committed"] / steps,
                    "prefetch_hits_per_step": st["prefetch_hits"] / steps,
                    "lookahead_prefetches_per_step": st["lookahead_prefetches"] / steps,
+                   "stolen_prefetches_per_step": st["stolen_prefetches"] / steps,
                    # 1 - (compute-stream stall on copy events) / (copy-engine busy time)
                    "hidden_fraction": (1.0 - st["compute_wait_ms"] / st["h2d_busy_ms"]) if st["h2d_busy_ms"] > 0
                    else 1.0},
@@ -576,14 +646,17 @@ def main():
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--no-all-resident", action="store_true")
     ap.add_argument("--no-checksum", action="store_true")
+    ap.add_argument("--no-config5", action="store_true", help="N>1: skip the BASELINE config-5 EP legs")
     ap.add_argument("--prefill-tokens", type=int, default=4096)
     ap.add_argument("--prefill-steps", type=int, default=5)
     ap.add_argument("--predictor", default="llapor", choices=["llapor", "gate", "perfect", "none"],
                     help="next-layer load predictor feeding PreSched (the reference's PredictFn menu)")
     ap.add_argument("--compress", type=int, default=1,
                     help="1: non-resident experts cross PCIe as lossless z-slabs (decoded on the GPU)")
-    ap.add_argument("--lookahead", type=int, default=0, choices=[0, 1, 2],
+    ap.add_argument("--lookahead", type=int, default=0, choices=[0, 1, 2, 3],
                     help="PreSched + lookahead top-up of the serial channel (0 = the reference executor)")
+    ap.add_argument("--steal-late", type=int, default=0,
+                    help="1: the host lane computes committed prefetches whose copies land too late")
     ap.add_argument("--host-threads", type=int, default=-1,
                     help="host expert lane threads (-1 auto, 0 = GPU-only executor)")
     args = ap.parse_args()

@@ -557,7 +557,12 @@ typedef struct {
                                d in {1, 2}: a labelled extension — behind PreSched's batch,
                                queue the other predicted non-resident experts of layers
                                l+1..l+d (hottest first, slot cap per target layer); those not
-                               started by the next scheduling point are cancelled (R2). */
+                               started by the next scheduling point are cancelled (R2).
+                               3: layer l+2 only, at most two top-up copies per layer. */
+  int32_t steal_late;       /* host lane only, 1: a committed prefetch whose copy has not
+                               landed when the lane finishes its cpu_set is computed by the
+                               lane if the copy needs longer than cpu_cost(m) (the copy's
+                               bytes are then unused); 0: the GPU waits for it (R6). */
 } ps_engine_config;
 
 ps_status ps_engine_create(const ps_engine_config* cfg, ps_engine* out);
@@ -624,6 +629,7 @@ typedef struct {
   double h2d_expert_bytes;  /* expert bytes the issued copies delivered (= h2d_bytes
                                without compression) */
   int64_t lookahead_prefetches; /* prefetch jobs queued by the lookahead top-up */
+  int64_t stolen_prefetches;    /* late prefetched experts the host lane computed (steal_late) */
 } ps_engine_stats;
 ps_status ps_engine_get_stats(ps_engine e, ps_engine_stats* out);
 ps_status ps_engine_reset_stats(ps_engine e);

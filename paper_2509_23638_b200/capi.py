@@ -116,7 +116,7 @@ class EngineConfig(C.Structure):
                 ("host_pinned", C.c_int32), ("ep", C.c_void_p), ("n_shared", C.c_int32),
                 ("host_threads", C.c_int32), ("compress_host", C.c_int32), ("predictor_kind", C.c_int32),
                 ("stats_ranking", C.POINTER(C.c_int32)), ("expert_weights", C.POINTER(C.c_void_p)),
-                ("lookahead", C.c_int32)]
+                ("lookahead", C.c_int32), ("steal_late", C.c_int32)]
 
 
 class EngineStats(C.Structure):
@@ -130,7 +130,7 @@ class EngineStats(C.Structure):
                 ("kernel_launches", C.c_int64),
                 ("cost", CostParams), ("cpu_experts", C.c_int64), ("cpu_ms_total", C.c_double),
                 ("cpu_bytes_total", C.c_double), ("z_decodes", C.c_int64), ("h2d_expert_bytes", C.c_double),
-                ("lookahead_prefetches", C.c_int64)]
+                ("lookahead_prefetches", C.c_int64), ("stolen_prefetches", C.c_int64)]
 
 
 PLAN_FN = C.CFUNCTYPE(C.c_int, C.c_void_p, C.POINTER(LayerInputs), C.c_int, C.POINTER(LayerPlan))

@@ -121,6 +121,8 @@ struct IoJob {
   bool critical = false;
   int issue_group = 1;
   const uint8_t* zhost = nullptr;  // z-slab source (header read on the host), null = raw copy
+  double t_io_us = 0;              // modelled transfer time (cost.t_io)
+  std::atomic<double> est_done_us{0};  // host-clock estimate of the copy's end (set at issue)
 };
 
 // The serial I/O channel: one copy stream, one host thread, FIFO with cancel.
@@ -230,6 +232,9 @@ class IoChannel {
       if (e == cudaSuccess) e = cudaEventRecord(j->start_ev, stream_);
       if (e == cudaSuccess) e = cudaMemcpyAsync(j->dst, j->src, j->bytes, cudaMemcpyHostToDevice, stream_);
       if (e == cudaSuccess) e = cudaEventRecord(j->done_ev, stream_);
+      // FIFO channel: this copy ends t_io after the later of now and the previous end
+      est_end_ = std::max(est_end_, now_us()) + j->t_io_us;
+      j->est_done_us.store(est_end_);
       g.lock();
       if (e != cudaSuccess) set_error(e);
       in_flight.push_back(j->done_ev);
@@ -251,6 +256,7 @@ class IoChannel {
   std::mutex mu_;
   std::condition_variable cv_;
   std::deque<IoJob*> queue_;
+  double est_end_ = 0;  // modelled end of the last issued copy (I/O thread only)
   bool stop_ = false, busy_ = false, error_ = false;
   std::string err_msg_;
 };
@@ -420,6 +426,8 @@ struct ps_engine_s {
   ps_host_lane lane = nullptr;
   std::unique_ptr<ps::LaneDriver> lane_drv;
   uint16_t* lane_x = nullptr;    // pinned: [maxB, H] bf16 x (D2H at the scheduling point)
+  uint16_t* lane_recv = nullptr;   // pinned (EP): [rows_max, H] bf16 rows received by this rank
+  cudaEvent_t ev_lane_rows = nullptr;  // (EP) received rows are on the host
   uint16_t* lane_xrows = nullptr;  // pinned: [maxB*Kt, H] bf16 gathered rows of CPU experts
   float* lane_yrows = nullptr;     // pinned: [maxB*Kt, H] f32 their outputs
   std::vector<ps::CpuJob> cpu_jobs;      // current layer
@@ -692,6 +700,7 @@ IoJob* new_job(ps_engine_s& e, int kind, int layer, int expert, int tokens, Slot
     j->bytes = e.host_z_bytes[idx];
   }
   j->wait_gen = slot->next_gen;  // the slot's latest reader must be done
+  j->t_io_us = static_cast<double>(e.cfg.cost.t_io);
   j->start_ev = take_job_event(e);
   j->done_ev = take_job_event(e);
   e.jobs.push_back(std::move(j));
@@ -761,6 +770,10 @@ void ep_dispatch_rows(ps_engine_s& e, int B, std::vector<int32_t>& counts_l, std
   }
   st = ps_ep_all_to_all(e.ep, e.ep_send_x, sb.data(), e.ep_recv_x, rb.data(), e.sc);
   if (st != PS_OK) fail(st, ps_last_error());
+  if (e.lane && rows > 0) {  // the host lane computes its cpu_set from the received rows
+    PS_CUDA(cudaMemcpyAsync(e.lane_recv, e.ep_recv_x, sizeof(uint16_t) * rows * H, cudaMemcpyDeviceToHost, e.sc));
+    PS_CUDA(cudaEventRecord(e.ev_lane_rows, e.sc));
+  }
   e.ep_rows_recv = rows;
   const int32_t* plan = e.ep_plan_dev;
   e.src = {plan, plan + (E + 1), 1, e.ep_recv_x, rows, og};
@@ -1079,14 +1092,25 @@ void layer_forward(ps_engine_s& e, int l, const float* x, const uint8_t* follow,
         if (r.layer == layer && r.expert == ex) return true;
       return false;
     };
-    for (auto& r : e.ready) {
-      if (r.layer != l || counts_l[r.expert] == 0) continue;
+    // With the host lane, a committed prefetch whose copy has not landed yet is deferred:
+    // once the lane's batch is done it either lands (GPU) or, if its copy still needs more
+    // than the lane's cost for it, the lane computes it instead (steal_late).
+    std::vector<const ps_engine_s::Ready*> late;
+    auto gpu_ready = [&](const ps_engine_s::Ready& r) {
       land(e, r.job);
       ps_expert_group one{};
       one.n = 1;
       one.experts[0] = r.expert;
       one.slabs[0] = static_cast<const uint16_t*>(r.slot->dev);
       ffn(e, one, counts_l.data(), B, true);
+    };
+    for (auto& r : e.ready) {
+      if (r.layer != l || counts_l[r.expert] == 0) continue;
+      if (e.lane && e.cfg.steal_late && cudaEventQuery(r.job->done_ev) == cudaErrorNotReady) {
+        late.push_back(&r);
+        continue;
+      }
+      gpu_ready(r);
     }
 
     // --- R4: scheduler inputs ------------------------------------------------------
@@ -1130,20 +1154,26 @@ void layer_forward(ps_engine_s& e, int l, const float* x, const uint8_t* follow,
     // R5: cpu_set on the host lane (concurrent with the loads below); without a lane the
     // GPU-only executor loads them after ondemand_seq.
     e.cpu_jobs.clear();
-    if (e.lane && plan.n_cpu > 0) {
-      const int32_t* off = e.pinned_counts + 3 * Et;
-      const int32_t* perm = e.pinned_counts + 4 * Et + 1;
-      for (int i = 0; i < plan.n_cpu; ++i) {
-        const int ex = plan.cpu_set[i].expert;
-        const uint16_t* slab = e.host_slab[static_cast<size_t>(l) * E + ex];
-        require(slab != nullptr, "host lane: cpu_set expert has no host copy");
-        CpuJob j{l, ex, off[ex + 1] - off[ex], off[ex], slab};
-        if (!e.host_z.empty()) j.z = e.host_z[static_cast<size_t>(l) * E + ex];  // 3- or 4-bit codes
-        for (int r = j.row0; r < j.row0 + j.m; ++r)
-          std::memcpy(e.lane_xrows + static_cast<size_t>(r) * H, e.lane_x + static_cast<size_t>(perm[r] / Kt) * H,
-                      sizeof(uint16_t) * H);
-        e.cpu_jobs.push_back(j);
+    // Host-lane jobs read their rows from the FFN source on the host: the local routing
+    // (x of the B tokens, k slots per token) or, under EP, the rows received from all
+    // ranks (copied to the host after the dispatch, one row per permuted row).
+    auto lane_job = [&](int ex) {
+      const uint16_t* slab = e.host_slab[static_cast<size_t>(l) * E + ex];
+      require(slab != nullptr, "host lane: expert has no host copy");
+      const int32_t* off = e.ep ? e.ep_plan_host : e.pinned_counts + 3 * Et;
+      const int32_t* perm = e.ep ? e.ep_plan_host + (E + 1) : e.pinned_counts + 4 * Et + 1;
+      CpuJob j{l, ex, off[ex + 1] - off[ex], off[ex], slab};
+      if (!e.host_z.empty()) j.z = e.host_z[static_cast<size_t>(l) * E + ex];  // 3- or 4-bit codes
+      for (int r = j.row0; r < j.row0 + j.m; ++r) {
+        const uint16_t* src = e.ep ? e.lane_recv + static_cast<size_t>(perm[r]) * H
+                                   : e.lane_x + static_cast<size_t>(perm[r] / Kt) * H;
+        std::memcpy(e.lane_xrows + static_cast<size_t>(r) * H, src, sizeof(uint16_t) * H);
       }
+      return j;
+    };
+    if (e.lane && plan.n_cpu > 0) {
+      if (e.ep) PS_CUDA(cudaEventSynchronize(e.ev_lane_rows));  // received rows on the host
+      for (int i = 0; i < plan.n_cpu; ++i) e.cpu_jobs.push_back(lane_job(plan.cpu_set[i].expert));
       e.lane_drv->submit(&e.cpu_jobs, e.lane_xrows, e.lane_yrows);
     } else {
       loads.insert(loads.end(), plan.cpu_set, plan.cpu_set + plan.n_cpu);
@@ -1211,6 +1241,45 @@ void layer_forward(ps_engine_s& e, int l, const float* x, const uint8_t* follow,
       e.cpu_jobs.clear();
     }
 
+    // Deferred prefetches (see `late` above): land on the GPU if the copy is done or ends
+    // sooner than the lane would take; otherwise the lane computes the expert (the copy's
+    // bytes are then unused, like a mispredicted prefetch's).
+    if (!late.empty()) {
+      e.cpu_jobs.clear();
+      if (e.ep) PS_CUDA(cudaEventSynchronize(e.ev_lane_rows));
+      for (const ps_engine_s::Ready* r : late) {
+        const int m = counts_l[r->expert];
+        const double cost = e.cfg.cost.beta * m + static_cast<double>(e.cfg.cost.startup);
+        const bool landed = cudaEventQuery(r->job->done_ev) != cudaErrorNotReady;
+        if (landed || r->job->est_done_us.load() - now_us() <= cost) {
+          gpu_ready(*r);
+          continue;
+        }
+        e.cpu_jobs.push_back(lane_job(r->expert));
+        e.st.stolen_prefetches++;
+      }
+      if (!e.cpu_jobs.empty()) {
+        e.lane_drv->submit(&e.cpu_jobs, e.lane_xrows, e.lane_yrows);
+        e.lane_drv->wait();
+        e.last_ffn_end = nullptr;
+        const size_t total_rows = static_cast<size_t>(e.src.rows);
+        for (CpuJob& j : e.cpu_jobs) {
+          const ps_status cs = ps_rows_from_host(e.lane_yrows + static_cast<size_t>(j.row0) * H,
+                                                 static_cast<int64_t>(j.m) * H, e.y_part + static_cast<size_t>(j.row0) * H,
+                                                 e.step_split - 1, static_cast<int64_t>(total_rows) * H, e.sc);
+          if (cs != PS_OK) fail(cs, ps_last_error());
+          e.st.kernel_launches += 1;
+          e.st.cpu_experts += 1;
+          e.st.cpu_bytes_total += static_cast<double>(e.cfg.spec.expert_bytes);
+          e.st.cpu_ms_total += (j.t1_us - j.t0_us) / 1e3 / static_cast<double>(e.cpu_jobs.size());
+          j.t0_us -= host_t0_us;
+          j.t1_us -= host_t0_us;
+          e.cpu_done.push_back(j);
+        }
+        e.cpu_jobs.clear();
+      }
+    }
+
     // --- combine -> y_l ------------------------------------------------------------
     ph.comb0 = e.last_ffn_end;  // nothing enqueued since the last FFN ended (else a new mark)
     if (!ph.comb0) {
@@ -1276,11 +1345,18 @@ void layer_forward(ps_engine_s& e, int l, const float* x, const uint8_t* follow,
           if (j->layer == layer && j->expert == ex) return true;
         return is_ready(layer, ex);
       };
-      for (int d = 1; d <= std::min(2, e.cfg.lookahead) && l + d < L; ++d) {
+      // lookahead 3 = layer l+2 only, at most two copies per layer: a copy issued now for
+      // l+1 lands after l+1's scheduling point and stalls its GPU work, one for l+2 has a
+      // whole layer to land (measured: profiles/r02_bench_lookahead_ab*.jsonl).
+      const int d0 = e.cfg.lookahead == 3 ? 2 : 1, d1 = std::min(2, e.cfg.lookahead);
+      const int per_layer_cap = e.cfg.lookahead == 3 ? 2 : e.cfg.prefetch_slots;
+      int queued = 0;
+      for (int d = d0; d <= d1 && l + d < L; ++d) {
         const std::vector<ps_expert_load>& cand = d == 1 ? nxt : e.nxt2;
         int used = 0;
         for (auto& sl : e.pf_pool) used += sl->in_use && sl->target_layer == l + d;
-        for (auto it = cand.rbegin(); it != cand.rend() && used < e.cfg.prefetch_slots; ++it) {
+        for (auto it = cand.rbegin(); it != cand.rend() && used < e.cfg.prefetch_slots && queued < per_layer_cap;
+             ++it) {
           if (pending(l + d, it->expert)) continue;
           Slot* slot = take_prefetch_slot(e, l + d);
           IoJob* job = new_job(e, kPrefetch, l + d, it->expert, it->tokens, slot);
@@ -1289,6 +1365,7 @@ void layer_forward(ps_engine_s& e, int l, const float* x, const uint8_t* follow,
           push_modelled(e);
           e.io->push(job);
           ++used;
+          ++queued;
           e.st.lookahead_prefetches++;
         }
       }
@@ -1416,7 +1493,7 @@ void create_engine(const ps_engine_config& cfg, ps_engine_s& e) {
   require(e.S >= 0 && e.S <= 32, "engine: n_shared out of range [0, 32]");
   require(e.S == 0 || !cfg.ep, "engine: shared experts are not supported with expert parallelism");
   if (e.cfg.prefetch_slots <= 0) e.cfg.prefetch_slots = 8;
-  require(e.cfg.lookahead >= 0 && e.cfg.lookahead <= 2, "engine: lookahead must be 0, 1 or 2");
+  require(e.cfg.lookahead >= 0 && e.cfg.lookahead <= 3, "engine: lookahead must be 0..3");
   e.n_split = ps_ffn_down_splits(e.H, e.F);
   e.slab_elems = sp.expert_bytes / 2;
   for (auto& h : e.stats) h = {1.0, 0.0, 32};
@@ -1611,7 +1688,7 @@ void create_engine(const ps_engine_config& cfg, ps_engine_s& e) {
   // Prefetch slots for two live target layers (R8 cap per layer) up front: a cudaMalloc
   // of an expert-sized buffer inside a step costs milliseconds of host time.
   // (lookahead 2 keeps a third target layer live: l+1 and l+2 queued while l's land)
-  const size_t live_layers = e.cfg.lookahead >= 2 ? 3 : 2;
+  const size_t live_layers = e.cfg.lookahead >= 2 ? 3 : 2;  // (3: l+2 only, also three live layers)
   for (size_t i = 0; i < std::min<size_t>(live_layers * static_cast<size_t>(e.cfg.prefetch_slots), n_host); ++i) {
     auto s = std::make_unique<Slot>();
     PS_CUDA(cudaMalloc(&s->dev, sp.expert_bytes));
@@ -1698,11 +1775,15 @@ void create_engine(const ps_engine_config& cfg, ps_engine_s& e) {
   PS_CUDA(cudaEventCreate(&e.ev_step1));
 
   if (cfg.host_threads > 0) {
-    require(!e.ep, "engine: the host expert lane is not supported with expert parallelism");
     if (ps_host_lane_create(cfg.host_threads, &e.lane) != PS_OK) fail(PS_ERUNTIME, ps_last_error());
     PS_CUDA(cudaHostAlloc(&e.lane_x, sizeof(uint16_t) * B * e.H, cudaHostAllocDefault));
-    PS_CUDA(cudaHostAlloc(&e.lane_xrows, sizeof(uint16_t) * rows_t * e.H, cudaHostAllocDefault));
-    PS_CUDA(cudaHostAlloc(&e.lane_yrows, sizeof(float) * rows_t * e.H, cudaHostAllocMapped));
+    // lane rows: this rank's routed rows, or under EP every row routed here by all ranks
+    PS_CUDA(cudaHostAlloc(&e.lane_xrows, sizeof(uint16_t) * frows * e.H, cudaHostAllocDefault));
+    PS_CUDA(cudaHostAlloc(&e.lane_yrows, sizeof(float) * frows * e.H, cudaHostAllocMapped));
+    if (e.ep) {
+      PS_CUDA(cudaHostAlloc(&e.lane_recv, sizeof(uint16_t) * frows * e.H, cudaHostAllocDefault));
+      PS_CUDA(cudaEventCreateWithFlags(&e.ev_lane_rows, cudaEventDisableTiming | cudaEventBlockingSync));
+    }
     e.lane_drv = std::make_unique<LaneDriver>(e.lane, e.H, e.F);
     e.lane_drv->tiled = e.host_tiled;
     // cpu_cost = beta*m + C (cost_model.cpp:34-37) measured on this host: the lane on a
@@ -1758,7 +1839,7 @@ void destroy_engine(ps_engine_s& e) {
   e.io.reset();
   e.lane_drv.reset();
   if (e.lane) ps_host_lane_destroy(e.lane);
-  for (void* p : {(void*)e.lane_x, (void*)e.lane_xrows, (void*)e.lane_yrows})
+  for (void* p : {(void*)e.lane_x, (void*)e.lane_xrows, (void*)e.lane_yrows, (void*)e.lane_recv})
     if (p) cudaFreeHost(p);
   if (e.sc) cudaStreamSynchronize(e.sc);
   if (e.s_d2h) cudaStreamSynchronize(e.s_d2h);
@@ -1791,7 +1872,7 @@ void destroy_engine(ps_engine_s& e) {
   }
   for (cudaEvent_t ev : e.event_pool) cudaEventDestroy(ev);
   for (cudaEvent_t ev : e.job_event_pool) cudaEventDestroy(ev);
-  for (cudaEvent_t ev : {e.ev_routed, e.ev_step0, e.ev_step1, e.ev_in, e.ev_out})
+  for (cudaEvent_t ev : {e.ev_routed, e.ev_step0, e.ev_step1, e.ev_in, e.ev_out, e.ev_lane_rows})
     if (ev) cudaEventDestroy(ev);
   if (e.sc) cudaStreamDestroy(e.sc);
   if (e.s_d2h) cudaStreamDestroy(e.s_d2h);

@@ -14,8 +14,9 @@
 // code width with the smaller estimated size). Decoding is bit-exact
 // (tests/test_gpu_zexpert.py), so every downstream result is identical to loading the
 // raw slab. Encoder: host C++ (at engine create, multithreaded over blocks); decoder:
-// one warp per 1024-value block, 32 values per lane, escape ranks by a warp scan,
-// 16-byte loads/stores (HBM-bound: 1.5 B read + 2 B written per value).
+// one warp per 1024-value block in four 256-value chunks (8 values per lane), escape
+// ranks by a warp scan, coalesced 512-byte warp stores (HBM-bound: 1.41 B read + 2 B
+// written per value).
 #include <algorithm>
 #include <cstdlib>
 #include <cstring>
@@ -27,6 +28,113 @@
 
 namespace ps {
 namespace {
+
+// One warp per 1024-value block, in four chunks of 256 values; in chunk q lane L decodes
+// the 8 consecutive values at 256q + 8L. Every warp-wide load and store is contiguous
+// (lo: 256 B as 8-byte lane loads, codes: the 8 segments' words, output: 512 B as
+// 16-byte lane stores; a tiled slab's 32-value tile row is 64 contiguous output bytes),
+// and the four chunks' loads are independent, so they are all in flight together. The
+// escape rank of a lane's values = the block's escape offset + escapes in earlier chunks
+// + a warp exclusive scan within the chunk. The block's escape bytes (contiguous, ~30 at
+// 3-bit codes) are staged in shared memory by one coalesced warp load.
+constexpr int kZEscStage = 256;  // staged escapes per block (more: read from global)
+
+// Codes of values 8j..8j+7 of a 32-value segment whose code words start at `cw`:
+// BITS*8 bits from bit 8*BITS*j of a little-endian word array.
+template <int BITS>
+__device__ __forceinline__ uint32_t z_codes8(const uint32_t* __restrict__ cw, int j) {
+  if constexpr (BITS == 4) {
+    return __ldg(cw + j);
+  } else {
+    const int bit = 24 * j, w = bit >> 5, sh = bit & 31;
+    uint32_t c = __ldg(cw + w) >> sh;
+    if (sh > 8) c |= __ldg(cw + w + 1) << (32 - sh);
+    return c & 0xffffffu;
+  }
+}
+
+// Row-major start of the 32-value tile row at tiled index v (z_untile in 32-bit
+// arithmetic: the host checks 3HF < 2^32 for tiled slabs).
+__device__ __forceinline__ uint32_t z_untile32(uint32_t v, uint32_t H, uint32_t F) {
+  const uint32_t fh = F * H;
+  const uint32_t base = v < fh ? 0u : (v < 2u * fh ? fh : 2u * fh);
+  const uint32_t K = v < 2u * fh ? H : F;
+  const uint32_t t = v - base, tile = t >> 9, i = (t >> 5) & 15u, nkb = K >> 5;
+  const uint32_t rb = tile / nkb, kb = tile - rb * nkb;
+  return base + (rb * 16u + i) * K + kb * 32u;
+}
+
+template <int BITS>
+__global__ void __launch_bounds__(256, 5)
+z_decode_kernel(const uint8_t* __restrict__ z, uint64_t n, uint32_t base, uint32_t nb, uint32_t tile_h,
+                uint32_t tile_f, uint16_t* __restrict__ out) {
+  constexpr uint32_t kEsc = (1u << BITS) - 1u, kMask = (1u << BITS) - 1u;
+  __shared__ uint8_t s_esc[8][kZEscStage];
+  const uint64_t n_pad = static_cast<uint64_t>(nb) * kZBlock;
+  const uint8_t* lo = z + z_lo_off();
+  const uint32_t* codes = reinterpret_cast<const uint32_t*>(z + z_codes_off(n_pad));
+  const uint32_t* esc_off = reinterpret_cast<const uint32_t*>(z + z_escoff_off(n_pad, BITS));
+  const uint8_t* esc = z + z_esc_off(n_pad, nb, BITS);
+  const int lane = threadIdx.x & 31, j = lane & 3;
+  const uint32_t warps = (gridDim.x * blockDim.x) >> 5;
+  uint8_t* se = s_esc[threadIdx.x >> 5];
+  for (uint32_t b = (blockIdx.x * blockDim.x + threadIdx.x) >> 5; b < nb; b += warps) {
+    const uint64_t vb = static_cast<uint64_t>(b) * kZBlock;
+    uint2 lw[4];
+    uint32_t cc[4];
+#pragma unroll
+    for (int q = 0; q < 4; ++q) {  // all four chunks' loads first
+      const uint32_t o = 256u * q + 8u * lane;
+      lw[q] = __ldg(reinterpret_cast<const uint2*>(lo + vb + o));
+      const uint64_t seg = (vb + o) >> 5;
+      cc[q] = z_codes8<BITS>(codes + seg * BITS, j);
+    }
+    const uint32_t eoff = __ldg(esc_off + b), eend = __ldg(esc_off + b + 1);
+    const uint32_t n_stage = min(eend - eoff, static_cast<uint32_t>(kZEscStage));
+    for (uint32_t k = lane; k < n_stage; k += 32) se[k] = esc[eoff + k];
+    __syncwarp();
+    uint32_t run = eoff;  // escapes before this chunk in value order
+#pragma unroll
+    for (int q = 0; q < 4; ++q) {
+      int cnt = 0;
+#pragma unroll
+      for (int i = 0; i < 8; ++i) cnt += ((cc[q] >> (BITS * i)) & kMask) == kEsc;
+      int incl = cnt;
+#pragma unroll
+      for (int d = 1; d < 32; d <<= 1) {
+        const int t = __shfl_up_sync(0xffffffffu, incl, d);
+        if (lane >= d) incl += t;
+      }
+      uint32_t e_at = run + static_cast<uint32_t>(incl - cnt);
+      run += static_cast<uint32_t>(__shfl_sync(0xffffffffu, incl, 31));
+      uint32_t pk[4];
+#pragma unroll
+      for (int i = 0; i < 8; ++i) {
+        const uint32_t c = (cc[q] >> (BITS * i)) & kMask;
+        const uint32_t l = ((i < 4 ? lw[q].x : lw[q].y) >> (8 * (i & 3))) & 0xffu;
+        uint32_t ex = base + c;
+        if (c == kEsc) {
+          const uint32_t r = e_at - eoff;
+          ex = r < static_cast<uint32_t>(kZEscStage) ? se[r] : esc[e_at];
+          ++e_at;
+        }
+        const uint32_t v = ((l & 0x80u) << 8) | (ex << 7) | (l & 0x7fu);
+        if (i & 1) pk[i >> 1] |= v << 16;
+        else pk[i >> 1] = v;
+      }
+      const uint64_t v0 = vb + 256u * q + 8u * lane;
+      if (tile_h) {  // tiled slab (n = 3HF, a multiple of 1024: always full)
+        uint16_t* dst = out + z_untile32(static_cast<uint32_t>(v0) & ~31u, tile_h, tile_f) + 8 * j;
+        *reinterpret_cast<uint4*>(dst) = make_uint4(pk[0], pk[1], pk[2], pk[3]);
+      } else if (v0 + 8 <= n) {
+        *reinterpret_cast<uint4*>(out + v0) = make_uint4(pk[0], pk[1], pk[2], pk[3]);
+      } else {
+        for (int i = 0; i < 8 && v0 + i < n; ++i) out[v0 + i] = static_cast<uint16_t>(pk[i >> 1] >> (16 * (i & 1)));
+      }
+    }
+    __syncwarp();  // every lane done with s_esc before the next block restages it
+  }
+}
 
 // Escapes (all-ones codes) among a lane's 32 codes with word-level bit tricks.
 template <int BITS>
@@ -54,18 +162,17 @@ __device__ __forceinline__ uint32_t z_code(const uint32_t (&cw)[BITS + 1], int i
   return c & ((1u << BITS) - 1u);
 }
 
-// One warp per 1024-value block, 32 values per lane: lane L's codes are the BITS 32-bit
+// v1 decoder (round 1; PS_ZDECODE=1): one warp per 1024-value block, 32 values per lane: lane L's codes are the BITS 32-bit
 // words at BITS*L of the block's code region (bit BITS*i.. of a little-endian array).
 // Codes are extracted twice (escape count for the warp scan, then the values) instead of
 // kept in registers: <= 64 registers, 4 CTAs of 256 threads per SM for latency hiding.
 // The block's escape bytes (contiguous, ~30 at 3-bit codes) are staged in shared memory
 // by one coalesced warp load, so a lane's escapes cost a shared-memory read instead of a
 // dependent global load after the scan.
-constexpr int kZEscStage = 256;  // staged escapes per block (more: read from global)
 
 template <int BITS>
 __global__ void __launch_bounds__(256, 4)
-z_decode_kernel(const uint8_t* __restrict__ z, uint64_t n, uint32_t base, uint32_t nb, uint32_t tile_h,
+z_decode_kernel_v1(const uint8_t* __restrict__ z, uint64_t n, uint32_t base, uint32_t nb, uint32_t tile_h,
                 uint32_t tile_f, uint16_t* __restrict__ out) {
   constexpr uint32_t kEsc = (1u << BITS) - 1u;
   __shared__ uint8_t s_esc[8][kZEscStage];
@@ -337,15 +444,27 @@ ps_status ps_zslab_decode(const uint8_t* z_dev, const uint8_t* z_host_header, ui
     require(h.magic == kZMagic, "ps_zslab_decode: not a z-slab");
     const int threads = 256;
     const int grid = static_cast<int>(std::min<uint64_t>((static_cast<uint64_t>(h.nb) * 32 + threads - 1) / threads,
-                                                         4 * 148));
+                                                         5 * 148));
     require(h.code_bits == 3 || h.code_bits == 4, "ps_zslab_decode: bad code width");
     const uint32_t th = h.tiled ? h.tile_h : 0, tf = h.tiled ? h.tile_f : 0;
-    require(!h.tiled || (th % 32 == 0 && tf % 32 == 0 && th && tf && h.n == 3ull * th * tf),
+    require(!h.tiled || (th % 32 == 0 && tf % 32 == 0 && th && tf && h.n == 3ull * th * tf && h.n < (1ull << 32)),
             "ps_zslab_decode: bad tiled header");
-    if (h.code_bits == 3)
+    static const int version = [] {
+      const char* v = std::getenv("PS_ZDECODE");
+      return v && v[0] == '1' ? 1 : 2;
+    }();
+    if (version == 1) {
+      const int grid1 = static_cast<int>(std::min<uint64_t>((static_cast<uint64_t>(h.nb) * 32 + threads - 1) / threads,
+                                                            4 * 148));
+      if (h.code_bits == 3)
+        z_decode_kernel_v1<3><<<grid1, threads, 0, as_stream(stream)>>>(z_dev, h.n, h.base, h.nb, th, tf, out);
+      else
+        z_decode_kernel_v1<4><<<grid1, threads, 0, as_stream(stream)>>>(z_dev, h.n, h.base, h.nb, th, tf, out);
+    } else if (h.code_bits == 3) {
       z_decode_kernel<3><<<grid, threads, 0, as_stream(stream)>>>(z_dev, h.n, h.base, h.nb, th, tf, out);
-    else
+    } else {
       z_decode_kernel<4><<<grid, threads, 0, as_stream(stream)>>>(z_dev, h.n, h.base, h.nb, th, tf, out);
+    }
     PS_LAUNCH_CHECK("z_decode_kernel");
   });
 }

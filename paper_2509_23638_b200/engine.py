@@ -114,7 +114,8 @@ class Engine:
                  resident=None, trace_hidden=None, trace_follow=None, policy: str = "presched",
                  predictor=None, cost=None, prefetch_slots: int = 8, device: int = 0, ep=None,
                  n_shared: int = 0, host_threads: int = 0, compress_host: bool = False,
-                 predictor_kind: str = "auto", stats_ranking=None, expert_weights=None, lookahead: int = 0):
+                 predictor_kind: str = "auto", stats_ranking=None, expert_weights=None, lookahead: int = 0,
+                 steal_late: bool = False):
         from . import parse_policy, plan_residency, trace_inputs  # noqa: F401
         self.lib = load()
         self.spec = spec
@@ -152,6 +153,7 @@ class Engine:
         cfg.host_threads = host_threads
         cfg.compress_host = int(bool(compress_host))
         cfg.lookahead = lookahead
+        cfg.steal_late = int(bool(steal_late))
         kinds = {"auto": 0, "llapor": 1, "gate": 2, "stats": 3, "perfect": 4, "none": 5}
         cfg.predictor_kind = kinds[predictor_kind]
         if stats_ranking is not None:

@@ -17,7 +17,11 @@ from paper_2509_23638_b200 import engine as eng  # noqa: E402
 
 
 def main():
+    import argparse
     import torch
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--lookahead", type=int, default=0)
+    args = ap.parse_args()
     spec = ps.spec_preset("mixtral")
     gen = ps.TraceGenConfig(*[ps.GROUP_DEFAULT_GEN[g] for g in ("input", "middle", "output")])
     L, E, H = spec.num_layers, spec.experts_per_layer, spec.hidden_dim
@@ -31,7 +35,8 @@ def main():
     pred = C.c_void_p()
     ps.check(lib.ps_llapor_random(C.byref(spec), 256, 512, 32, 48, 3, C.byref(pred)))
     e = eng.Engine(spec, gen, max_batch=B, weight_seed=1, gate=gate, budget_bytes=budget, resident=resident,
-                   policy="presched", predictor=pred, host_threads=bench.default_host_threads(), compress_host=True)
+                   policy="presched", predictor=pred, host_threads=bench.default_host_threads(), compress_host=True,
+                   lookahead=args.lookahead)
     hid = [torch.as_tensor(np.ascontiguousarray(hidden[s * B:(s + 1) * B].transpose(1, 0, 2), np.float32),
                            device="cuda") for s in range(S)]
     fol = [torch.as_tensor(np.ascontiguousarray(follow[s * B:(s + 1) * B].T), device="cuda") for s in range(S)]
@@ -51,7 +56,10 @@ def main():
         ld = [x for x in ev if x[3] == 3]
         pf = [x for x in events if x[3] == 4 and x[4] == l + 1]
         gpu = [x for x in ev if x[3] == 1]
+        io = sorted([x for x in events if x[2] == 2 and x[0] < le[l] and x[1] > ls[l]])
+        io_busy = sum(min(x[1], le[l]) - max(x[0], ls[l]) for x in io)
         rows.append({"layer": l, "start": ls[l], "end": le[l], "sched_end": att[0][1] if att else None,
+                     "io_busy_in_layer": io_busy, "gpu_expert_starts": [x[0] for x in gpu],
                      "cpu_start": cpu[0][0] if cpu else None, "cpu_end": cpu[0][1] if cpu else None,
                      "n_cpu": len(cpu), "n_load": len(ld), "n_prefetch_next": len(pf),
                      "load_us": [x[1] - x[0] for x in ld + pf], "load_end": max((x[1] for x in ld), default=None),

@@ -27,6 +27,17 @@ def run(preset, L, E, H, F, B, budget, **kw):
 
 
 def main():
+    import argparse
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--only", default="all", choices=["all", "prefill_single", "prefill_pair"],
+                    help="prefill_*: only that tcgen05 kernel (to attribute sanitizer reports)")
+    args = ap.parse_args()
+    if args.only != "all":
+        lib = ps.load()
+        ps.check(lib.ps_set_prefill_kernel(0 if args.only == "prefill_single" else 1))
+        run("mixtral", 3, 8, 256, 512, 512, 1.0)
+        print("sanitize run done")
+        return
     cost = (1000, 5, 10, 1.0, 1, 0)
     run("mixtral", 3, 8, 256, 512, 8, 0.25)
     run("mixtral", 3, 8, 256, 512, 8, 0.25, host_threads=2, cost=cost)

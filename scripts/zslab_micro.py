@@ -20,12 +20,17 @@ def main():
     n = 3 * H * F
     slab = np.empty(n, np.uint16)
     ps.check(lib.ps_init_expert_slab_host(slab.ctypes.data, H, F, 1, 0, 0))
-    for bits in ("3", "4"):
+    tiled_slab = slab.copy()
+    ps.check(lib.ps_host_slab_tile(tiled_slab.ctypes.data, H, F))
+    for bits, tiled in (("3", 0), ("4", 0), ("3", 1)):
         os.environ["PS_ZSLAB_BITS"] = bits
         cap = lib.ps_zslab_bound(n)
         z = np.zeros(cap, np.uint8)
         nb = C.c_uint64()
-        ps.check(lib.ps_zslab_encode(slab.ctypes.data, n, z.ctypes.data, cap, C.byref(nb), 0))
+        if tiled:  # the engine's host-lane configuration: z-slab of the lane's tile layout
+            ps.check(lib.ps_zslab_encode_tiled(tiled_slab.ctypes.data, H, F, z.ctypes.data, cap, C.byref(nb), 0))
+        else:
+            ps.check(lib.ps_zslab_encode(slab.ctypes.data, n, z.ctypes.data, cap, C.byref(nb), 0))
         z = z[:nb.value].copy()
         zd = torch.as_tensor(z, device="cuda")
         outs = [torch.empty(n, dtype=torch.int16, device="cuda") for _ in range(3)]
@@ -43,7 +48,7 @@ def main():
         torch.cuda.synchronize()
         us = a.elapsed_time(b) * 1e3 / iters
         assert np.array_equal(outs[0].cpu().numpy().view(np.uint16), slab)
-        print(json.dumps({"bits": int(bits), "z_bytes": int(nb.value), "us": us,
+        print(json.dumps({"bits": int(bits), "tiled": tiled, "z_bytes": int(nb.value), "us": us,
                           "hbm_gbs": (nb.value + 2 * n) / (us * 1e-6) / 1e9}))
 
 

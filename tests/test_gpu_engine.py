@@ -260,3 +260,20 @@ def test_engine_predictor_menu_matches_reference_predict_loads(torch_cuda):
                 assert not pred[l].any()
     for kind in ("gate", "stats", "none"):
         np.testing.assert_array_equal(outs[kind], outs["perfect"])
+
+
+@pytest.mark.parametrize("lookahead", [0, 1, 2, 3])
+def test_engine_host_lane_lookahead_and_late_steal(torch_cuda, lookahead):
+    """Executor extensions (perf mode, off in the reference configuration): the lookahead
+    top-up of the serial channel (1: l+1, 2: l+1 and l+2, 3: l+2 only) and steal_late
+    (the lane computes committed prefetches whose copies would land after it). Outputs
+    still match the oracle, every routed expert is computed exactly once (verify_timeline
+    conservation), and the top-up queued copies."""
+    spec = _small_spec(L=5, F=2048)
+    cost = (1000, 5, 10, 0.5, 1, 0)
+    y, y_ref, ids, st, resident, agree = _run(spec, 8, 0.25, host_threads=4, cost=cost, lookahead=lookahead,
+                                              steal_late=True, steps=3, predictor_kind="gate")
+    assert agree >= 0.98
+    assert np.linalg.norm(y - y_ref) / np.linalg.norm(y_ref) < BF16_RTOL
+    assert (st["lookahead_prefetches"] > 0) == (lookahead > 0)
+    assert st["stolen_prefetches"] <= st["prefetches_committed"]

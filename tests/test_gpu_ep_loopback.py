@@ -19,7 +19,7 @@ pytestmark = pytest.mark.gpu
 BF16_RTOL = 2e-2
 
 
-def _ep_run(spec, G, B, budget, seed=5, compress=False, steps=2, host_threads=0):
+def _ep_run(spec, G, B, budget, seed=5, compress=False, steps=2, host_threads=0, cost=None):
     L, E = spec.num_layers, spec.experts_per_layer
     cfg = ps.TraceGenConfig(*[ps.GROUP_DEFAULT_GEN[g] for g in ("input", "middle", "output")])
     gate, hidden, follow, zipf = ps.trace_inputs(cfg, spec, B * G, seed)
@@ -37,7 +37,7 @@ def _ep_run(spec, G, B, budget, seed=5, compress=False, steps=2, host_threads=0)
             resident = [(l, x) for (l, x) in ps.plan_residency(f, budget_bytes, spec.expert_bytes) if x % G == r]
             engines.append(eng.Engine(spec, cfg, max_batch=B, weight_seed=9, gate=gate, budget_bytes=budget_bytes,
                                       resident=resident, ep=comms[r], compress_host=compress,
-                                      host_threads=host_threads))
+                                      host_threads=host_threads, cost=cost))
 
         def rank_step(r):
             sl = slice(r * B, (r + 1) * B)
@@ -98,3 +98,14 @@ def test_ep_engine_loopback_mixtral_expert_shape(torch_cuda):
     spec = ps.desk_scale("mixtral", 3, 8, 4096)
     spec.expert_bytes = full.expert_bytes
     _ep_run(spec, 2, 16, 0.5, compress=True, steps=1)
+
+
+@pytest.mark.parametrize("G", [2, 4])
+def test_ep_engine_loopback_with_host_lane(torch_cuda, G):
+    """The same executor at every G: each rank's PreSched cpu_set runs on its own host
+    expert lane from the rows routed to it by all ranks (copied to the host after the
+    dispatch), with PCIe priced far above the lane."""
+    spec = ps.desk_scale("mixtral", 3, 8, 256)
+    spec.expert_bytes = 6 * 256 * 512
+    stats = _ep_run(spec, G, 8, 0.25, host_threads=2, cost=(1000, 5, 10, 1.0, 1, 0))
+    assert sum(s["cpu_experts"] for s in stats) > 0
