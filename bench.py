@@ -211,8 +211,8 @@ def workload_config(args, spec, executor="gpu_only"):
                         f"F={ps.ffn_dim(spec)}, batch {args.batch}, HBM expert budget {args.budget:.0%} "
                         f"({n_res}/{L * E} experts resident, hot-table residency from a warm-up trace), "
                         f"other experts in pinned host DRAM, policy {args.policy}"
-                        + (f"+lookahead{args.lookahead}" if getattr(args, "lookahead", 0) else "")
-                        + (", PreSched cpu_set on the host expert lane (AMX-BF16)" if executor == "host_lane" else
+
+                        + (", PreSched cpu_set on the host expert lane (AMX-BF16, reading the z-slabs)" if executor == "host_lane" else
                            ", GPU-only executor")
                         + (", loads as lossless z-slabs decoded on the GPU" if getattr(args, "compress", 0)
                            else "")
@@ -222,7 +222,10 @@ def workload_config(args, spec, executor="gpu_only"):
             "decode_batch": args.batch, "global_batch": args.batch * args.gpus,
             "parallelism": (f"ep{args.gpus}" if args.gpus > 1 else "single"),
             "executor": executor,
-            "budget_fraction": args.budget, "policy": args.policy, "lookahead": getattr(args, "lookahead", 0),
+            "budget_fraction": args.budget, "policy": args.policy,
+            "extra_leg": (f"host_lane_lookahead: PreSched + lookahead {args.lookahead}"
+                          + (" + steal_late" if getattr(args, "steal_late", 0) else "")
+                          if getattr(args, "lookahead", 0) or getattr(args, "steal_late", 0) else None),
             "l2": "inputs larger than L2 (each expert slab 336 MiB > 126 MB L2)"}
 
 
@@ -277,12 +280,16 @@ def run_ours(args):
     predictor = C.c_void_p()
     ps.check(lib.ps_llapor_random(C.byref(spec), 256, 512, 32, 48, 3, C.byref(predictor)))
     host_threads = args.host_threads if args.host_threads >= 0 else default_host_threads(world)
+    torch.cuda.synchronize()
+    free0 = torch.cuda.mem_get_info(local)[0]
     t_create = time.perf_counter()
     e = eng.Engine(spec, gen, max_batch=B, weight_seed=args.weight_seed, gate=gate, budget_bytes=budget_bytes,
                    resident=resident, policy=args.policy, predictor=predictor, device=local, ep=ep,
                    host_threads=host_threads, compress_host=bool(args.compress),
                    predictor_kind=args.predictor, lookahead=args.lookahead, steal_late=bool(args.steal_late))
     t_create = time.perf_counter() - t_create
+    torch.cuda.synchronize()
+    hbm_engine = free0 - torch.cuda.mem_get_info(local)[0]
     measured_cost = e.stats()["cost"]
 
     # device-resident step inputs (layer-major), outputs
@@ -318,11 +325,22 @@ def run_ours(args):
 
     # GPU-only executor: PreSched with beta = 1e9 (cpu_set always empty).
     e.set_cost(measured_cost["t_io"], measured_cost["t_g"], measured_cost["t_attn"], 1e9, 0)
+    e.set_lookahead(0, False)
     legs = {"gpu_only": decode_leg()}
     if e.host_threads:
-        # Host expert lane: PreSched with the host's measured cpu_cost (beta*m + C).
+        # Host expert lane: PreSched with the host's measured cpu_cost (beta*m + C) —
+        # plain PreSched (the reference executor), then the headline configuration with
+        # the executor extensions (--lookahead / --steal-late) on the same engine.
         e.set_cost(**measured_cost)
         legs["host_lane"] = decode_leg(calibrate=True)
+        head_cost = e.stats()["cost"]
+        if args.lookahead or args.steal_late:
+            e.set_cost(**measured_cost)
+            e.set_lookahead(args.lookahead, bool(args.steal_late))
+            legs["host_lane_lookahead"] = decode_leg(calibrate=True)
+            # the e2e leg below measures the headline executor: plain PreSched again
+            e.set_lookahead(0, False)
+            e.set_cost(**head_cost)
     head = "host_lane" if "host_lane" in legs else "gpu_only"
     st, dev_ms, wall, clocks = legs[head]
 
@@ -446,8 +464,9 @@ def run_ours(args):
         traffic = tj["traffic_over_algorithmic"] * ffn_bytes / ffn_launches
         traffic_src = f"{tj['source']}: traffic/algorithmic = {tj['traffic_over_algorithmic']:.4f}"
     leg_summary = {name: decode_summary(lst, lms, N, B, L) for name, (lst, lms, _, _) in legs.items()}
-    if "cpu_lane" in leg_summary.get("host_lane", {}):
-        leg_summary["host_lane"]["cpu_lane"]["threads"] = host_threads
+    for name in ("host_lane", "host_lane_lookahead"):
+        if "cpu_lane" in leg_summary.get(name, {}):
+            leg_summary[name]["cpu_lane"]["threads"] = host_threads
     cpu_step_s, cpu_desc, cpu_legs, cpu_threads = (cpu_sample(args) if not args.no_cpu_baseline
                                                    else (None, "skipped", None, 0))
     line = {
@@ -466,6 +485,7 @@ def run_ours(args):
         "h2d": leg_summary[head]["h2d"],
         "executor": head,
         "host_lane": leg_summary.get("host_lane"),
+        "host_lane_lookahead": leg_summary.get("host_lane_lookahead"),
         "gpu_only": leg_summary["gpu_only"],
         "cpu_baseline": ({"value": args.batch / cpu_step_s, "unit": "tokens/s", "cores": cpu_threads,
                           "kind": "reference", "sample": cpu_desc, "host": host_info(),
@@ -477,6 +497,12 @@ def run_ours(args):
         "gpu_launches": st["kernel_launches"],
         "nccl_init": nccl_init_lines() if world > 1 else None,
         "config5_ep": config5,
+        "hbm_footprint_gb": {"budget_resident_experts": budget_bytes / 1e9,
+                             "resident_arena": len(resident) * spec.expert_bytes / 1e9,
+                             "engine_total_device": hbm_engine / 1e9,
+                             "note": "engine_total_device = device memory the engine allocated at create "
+                                     "(resident arena + 2 on-demand and the prefetch staging slots with "
+                                     "their z-slab landing buffers + routing/FFN scratch), cudaMemGetInfo delta"},
         "wall_s_timed": wall, "engine_create_s": t_create,
         "cost_params_us": st["cost"],
     }
@@ -499,8 +525,7 @@ def config5_legs(args, spec, gen, gate, zipf, ep, resident, budget_bytes, predic
     Bd, Tp = 64 // world, 4096 // world
     e = eng.Engine(spec, gen, max_batch=max(Bd, Tp), weight_seed=args.weight_seed, gate=gate,
                    budget_bytes=budget_bytes, resident=resident, policy=args.policy, predictor=predictor,
-                   device=local, ep=ep, host_threads=host_threads, compress_host=bool(args.compress),
-                   lookahead=args.lookahead, steal_late=bool(args.steal_late))
+                   device=local, ep=ep, host_threads=host_threads, compress_host=bool(args.compress))
     out = {}
     try:
         S = args.warmup + args.steps
@@ -615,7 +640,7 @@ def decode_summary(st, dev_ms, N, B, L):
                    # 1 - (compute-stream stall on copy events) / (copy-engine busy time)
                    "hidden_fraction": (1.0 - st["compute_wait_ms"] / st["h2d_busy_ms"]) if st["h2d_busy_ms"] > 0
                    else 1.0},
-           "cost_params_us": st["cost"]}
+           "cost_params_us": st["cost"], "calibration_fit_cost_params": bool(st["calibration_fit"])}
     if st["cpu_experts"]:
         out["cpu_lane"] = {"experts_per_step": st["cpu_experts"] / steps,
                            "busy_ms_per_step": st["cpu_ms_total"] / steps,
@@ -653,9 +678,10 @@ def main():
                     help="next-layer load predictor feeding PreSched (the reference's PredictFn menu)")
     ap.add_argument("--compress", type=int, default=1,
                     help="1: non-resident experts cross PCIe as lossless z-slabs (decoded on the GPU)")
-    ap.add_argument("--lookahead", type=int, default=0, choices=[0, 1, 2, 3],
-                    help="PreSched + lookahead top-up of the serial channel (0 = the reference executor)")
-    ap.add_argument("--steal-late", type=int, default=0,
+    ap.add_argument("--lookahead", type=int, default=3, choices=[0, 1, 2, 3],
+                    help="extra leg host_lane_lookahead: PreSched + lookahead top-up of the serial channel "
+                         "(0 with --steal-late 0: no extra leg; the headline is always plain PreSched)")
+    ap.add_argument("--steal-late", type=int, default=1,
                     help="1: the host lane computes committed prefetches whose copies land too late")
     ap.add_argument("--host-threads", type=int, default=-1,
                     help="host expert lane threads (-1 auto, 0 = GPU-only executor)")

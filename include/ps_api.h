@@ -630,6 +630,7 @@ typedef struct {
                                without compression) */
   int64_t lookahead_prefetches; /* prefetch jobs queued by the lookahead top-up */
   int64_t stolen_prefetches;    /* late prefetched experts the host lane computed (steal_late) */
+  int64_t calibration_fit;      /* 1: the last ps_engine_calibrate took beta/C from fit_cost_params */
 } ps_engine_stats;
 ps_status ps_engine_get_stats(ps_engine e, ps_engine_stats* out);
 ps_status ps_engine_reset_stats(ps_engine e);
@@ -652,6 +653,9 @@ ps_status ps_engine_last_routing(ps_engine e, int32_t* ids_out, float* weights_o
 /* Replace the cost parameters PreSched plans with (e.g. beta = 1e9 disables the host
  * lane's cpu_set for a GPU-only comparison on the same engine). */
 ps_status ps_engine_set_cost(ps_engine e, const ps_cost_params* cost);
+/* Switch the executor extensions between steps (ps_engine_config.lookahead / steal_late;
+ * an engine created with lookahead >= 2 pre-allocates slots for three live layers). */
+ps_status ps_engine_set_lookahead(ps_engine e, int lookahead, int steal_late);
 /* Calibration (cost_model.cpp:45-72 fit + simulator cost semantics): replace the
  * engine's PreSched costs with the means measured since the last stats reset —
  * t_io = mean copy time per expert, t_g = mean FFN time per routed expert, t_attn =

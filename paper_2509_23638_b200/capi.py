@@ -130,7 +130,8 @@ class EngineStats(C.Structure):
                 ("kernel_launches", C.c_int64),
                 ("cost", CostParams), ("cpu_experts", C.c_int64), ("cpu_ms_total", C.c_double),
                 ("cpu_bytes_total", C.c_double), ("z_decodes", C.c_int64), ("h2d_expert_bytes", C.c_double),
-                ("lookahead_prefetches", C.c_int64), ("stolen_prefetches", C.c_int64)]
+                ("lookahead_prefetches", C.c_int64), ("stolen_prefetches", C.c_int64),
+                ("calibration_fit", C.c_int64)]
 
 
 PLAN_FN = C.CFUNCTYPE(C.c_int, C.c_void_p, C.POINTER(LayerInputs), C.c_int, C.POINTER(LayerPlan))
@@ -237,6 +238,7 @@ _SIGS = {
     "ps_engine_decode_step": (C.c_int, [_P, _P, _P, C.c_int, _P, _P]),
     "ps_engine_decode_step_host": (C.c_int, [_P, _P, _P, C.c_int, _P, _P]),
     "ps_engine_step_begin": (C.c_int, [_P, C.c_int]),
+    "ps_engine_set_lookahead": (C.c_int, [_P, C.c_int, C.c_int]),
     "ps_engine_last_routing": (C.c_int, [_P, _P, _P]),
     "ps_engine_layer_forward": (C.c_int, [_P, C.c_int, _P, _P, _P, _P, _P]),
     "ps_engine_step_end": (C.c_int, [_P]),

@@ -277,10 +277,12 @@ struct CpuJob {
   double t0_us = 0, t1_us = 0;  // host clock, filled by the driver
 };
 
-// The lane can read z-slabs (1.5 instead of 2 B of host DRAM per weight) but decoding
-// them tile by tile costs more CPU than the bytes save on the 16-core B200 host (75-79
-// vs 88-135 GB/s of expert weights, profiles/r01_host_lane_micro_z.jsonl): raw bf16 by
-// default, PS_HOST_LANE_Z=1 opts in.
+// The lane reads the z-slabs (1.41 instead of 2 B of host DRAM per weight, 3- or 4-bit
+// codes) when every slab of its batch has one: in the engine the lane shares host DRAM
+// with the PCIe DMA of the loads, so the 30 % fewer bytes win over the decode cost —
+// 96-100 vs 70-87 tok/s, lane 208-234 vs 153-180 GB/s of bf16 weights in alternating
+// runs (profiles/r02_bench_lane_z_ab.jsonl). (Round 1 measured no gain only because a
+// 3-bit slab disabled the z path for its whole batch.) PS_HOST_LANE_Z=0 opts out.
 bool lane_tiles_enabled() {  // PS_HOST_LANE_TILED=0 keeps the row-major host slabs
   static const bool on = [] {
     const char* v = std::getenv("PS_HOST_LANE_TILED");
@@ -289,10 +291,10 @@ bool lane_tiles_enabled() {  // PS_HOST_LANE_TILED=0 keeps the row-major host sl
   return on;
 }
 
-bool lane_z_enabled() {
+bool lane_z_enabled() {  // PS_HOST_LANE_Z=0 keeps the lane on raw bf16 slabs
   static const bool on = [] {
     const char* v = std::getenv("PS_HOST_LANE_Z");
-    return v && v[0] == '1';
+    return !(v && v[0] == '0');
   }();
   return on;
 }
@@ -433,6 +435,9 @@ struct ps_engine_s {
   std::vector<ps::CpuJob> cpu_jobs;      // current layer
   std::vector<ps::CpuJob> cpu_done;      // this step (timeline)
   double cpu_ms_cal = 0, cpu_tokens_cal = 0;  // calibration samples
+  std::vector<int32_t> probe_m;               // create-time lane probe (tokens, us)
+  std::vector<int64_t> probe_us;
+  int last_fit_used = 0;                      // last calibrate used fit_cost_params
   std::vector<int32_t> cal_m;
   std::vector<int64_t> cal_us;
   uint64_t slab_elems = 0;
@@ -1821,6 +1826,8 @@ void create_engine(const ps_engine_config& cfg, ps_engine_s& e) {
       const int m1 = prefill ? 16 : 1;
       const int m2 = std::min<int>(prefill ? 128 : std::max(1, std::min(16, e.maxB)), static_cast<int>(rows_t));
       const double t1 = best(m1), t2 = m2 > m1 ? best(m2) : t1;
+      e.probe_m = {m1, m2};
+      e.probe_us = {ps_to_ticks(t1), ps_to_ticks(t2)};
       const double beta = m2 > m1 ? std::max(0.0, (t2 - t1) / (m2 - m1)) : 0.0;
       e.cfg.cost.beta = std::max(beta, 1e-3);
       e.cfg.cost.startup = std::max<int64_t>(0, ps_to_ticks(t1 - beta * m1));
@@ -1982,6 +1989,7 @@ ps_status ps_engine_get_stats(ps_engine e, ps_engine_stats* out) {
   return guarded([&] {
     *out = e->st;
     out->cost = e->cfg.cost;
+    out->calibration_fit = e->last_fit_used;
   });
 }
 
@@ -2034,6 +2042,17 @@ ps_status ps_engine_last_predictions(ps_engine e, int32_t* out) {
   });
 }
 
+ps_status ps_engine_set_lookahead(ps_engine e, int lookahead, int steal_late) {
+  return guarded([&] {
+    require(e != nullptr, "ps_engine_set_lookahead: null engine");
+    require(lookahead >= 0 && lookahead <= 3 && (steal_late == 0 || steal_late == 1),
+            "ps_engine_set_lookahead: lookahead in 0..3, steal_late in {0, 1}");
+    require(!e->in_step, "ps_engine_set_lookahead: a step is in progress");
+    e->cfg.lookahead = lookahead;
+    e->cfg.steal_late = steal_late;
+  });
+}
+
 ps_status ps_engine_set_cost(ps_engine e, const ps_cost_params* cost) {
   return guarded([&] {
     require(e && cost, "ps_engine_set_cost: null argument");
@@ -2050,15 +2069,31 @@ ps_status ps_engine_calibrate(ps_engine e, ps_cost_params* out) {
     if (e->ffn_experts > 0) c.t_g = std::max<int64_t>(0, std::llround(1000.0 * e->ffn_expert_ms_total / e->ffn_experts));
     if (e->st.layers > 0) c.t_attn = std::llround(1000.0 * e->route_ms_total_cal / static_cast<double>(e->st.layers));
     if (c.t_g >= c.t_io) c.t_g = c.t_io - 1;  // CostParams invariant t_g < t_io (cost_model.cpp:16)
-    // Host lane: cpu_cost = beta*m + C. The lane is DRAM-bound, so the in-step samples
-    // (per-layer batches, mean tokens vs mean time per expert, under PCIe contention)
-    // span too few token counts for a stable slope: beta stays the create-time probe's
-    // (m = 1 vs 16 in isolation) and C is refit as the median residual of the samples.
+    // Host lane: cpu_cost = beta*m + C, refit with fit_cost_params (OLS, cost_model.cpp:
+    // 45-72) over the in-step samples (one per layer batch: mean tokens vs mean time per
+    // expert, measured under PCIe contention) plus the create-time probe points (m1, m2
+    // in isolation), which anchor the slope when the steps' token counts barely vary.
+    // The fit is used when it is physical (beta > 0, C >= 0, R^2 >= 0.3); otherwise beta
+    // stays the probe's and C is the median residual of the in-step samples.
+    e->last_fit_used = 0;
     if (!e->cal_m.empty()) {
-      std::vector<double> res;
-      for (size_t i = 0; i < e->cal_m.size(); ++i) res.push_back(e->cal_us[i] - c.beta * e->cal_m[i]);
-      std::nth_element(res.begin(), res.begin() + res.size() / 2, res.end());
-      c.startup = std::max<int64_t>(0, ps_to_ticks(res[res.size() / 2]));
+      std::vector<int32_t> m(e->cal_m.begin(), e->cal_m.end());
+      std::vector<int64_t> us(e->cal_us.begin(), e->cal_us.end());
+      m.insert(m.end(), e->probe_m.begin(), e->probe_m.end());
+      us.insert(us.end(), e->probe_us.begin(), e->probe_us.end());
+      double beta = 0, startup = 0, r2 = 0;
+      const bool fit_ok = ps_fit_cost_params(m.data(), us.data(), static_cast<int>(m.size()), &beta, &startup, &r2) ==
+                              PS_OK && beta > 0 && startup >= 0 && r2 >= 0.3;
+      if (fit_ok) {
+        c.beta = beta;
+        c.startup = ps_to_ticks(startup);
+        e->last_fit_used = 1;
+      } else {
+        std::vector<double> res;
+        for (size_t i = 0; i < e->cal_m.size(); ++i) res.push_back(e->cal_us[i] - c.beta * e->cal_m[i]);
+        std::nth_element(res.begin(), res.begin() + res.size() / 2, res.end());
+        c.startup = std::max<int64_t>(0, ps_to_ticks(res[res.size() / 2]));
+      }
     }
     if (ps_cost_params_validate(&c) != PS_OK) fail(PS_EINVAL, ps_last_error());
     e->cfg.cost = c;

@@ -29,113 +29,6 @@
 namespace ps {
 namespace {
 
-// One warp per 1024-value block, in four chunks of 256 values; in chunk q lane L decodes
-// the 8 consecutive values at 256q + 8L. Every warp-wide load and store is contiguous
-// (lo: 256 B as 8-byte lane loads, codes: the 8 segments' words, output: 512 B as
-// 16-byte lane stores; a tiled slab's 32-value tile row is 64 contiguous output bytes),
-// and the four chunks' loads are independent, so they are all in flight together. The
-// escape rank of a lane's values = the block's escape offset + escapes in earlier chunks
-// + a warp exclusive scan within the chunk. The block's escape bytes (contiguous, ~30 at
-// 3-bit codes) are staged in shared memory by one coalesced warp load.
-constexpr int kZEscStage = 256;  // staged escapes per block (more: read from global)
-
-// Codes of values 8j..8j+7 of a 32-value segment whose code words start at `cw`:
-// BITS*8 bits from bit 8*BITS*j of a little-endian word array.
-template <int BITS>
-__device__ __forceinline__ uint32_t z_codes8(const uint32_t* __restrict__ cw, int j) {
-  if constexpr (BITS == 4) {
-    return __ldg(cw + j);
-  } else {
-    const int bit = 24 * j, w = bit >> 5, sh = bit & 31;
-    uint32_t c = __ldg(cw + w) >> sh;
-    if (sh > 8) c |= __ldg(cw + w + 1) << (32 - sh);
-    return c & 0xffffffu;
-  }
-}
-
-// Row-major start of the 32-value tile row at tiled index v (z_untile in 32-bit
-// arithmetic: the host checks 3HF < 2^32 for tiled slabs).
-__device__ __forceinline__ uint32_t z_untile32(uint32_t v, uint32_t H, uint32_t F) {
-  const uint32_t fh = F * H;
-  const uint32_t base = v < fh ? 0u : (v < 2u * fh ? fh : 2u * fh);
-  const uint32_t K = v < 2u * fh ? H : F;
-  const uint32_t t = v - base, tile = t >> 9, i = (t >> 5) & 15u, nkb = K >> 5;
-  const uint32_t rb = tile / nkb, kb = tile - rb * nkb;
-  return base + (rb * 16u + i) * K + kb * 32u;
-}
-
-template <int BITS>
-__global__ void __launch_bounds__(256, 5)
-z_decode_kernel(const uint8_t* __restrict__ z, uint64_t n, uint32_t base, uint32_t nb, uint32_t tile_h,
-                uint32_t tile_f, uint16_t* __restrict__ out) {
-  constexpr uint32_t kEsc = (1u << BITS) - 1u, kMask = (1u << BITS) - 1u;
-  __shared__ uint8_t s_esc[8][kZEscStage];
-  const uint64_t n_pad = static_cast<uint64_t>(nb) * kZBlock;
-  const uint8_t* lo = z + z_lo_off();
-  const uint32_t* codes = reinterpret_cast<const uint32_t*>(z + z_codes_off(n_pad));
-  const uint32_t* esc_off = reinterpret_cast<const uint32_t*>(z + z_escoff_off(n_pad, BITS));
-  const uint8_t* esc = z + z_esc_off(n_pad, nb, BITS);
-  const int lane = threadIdx.x & 31, j = lane & 3;
-  const uint32_t warps = (gridDim.x * blockDim.x) >> 5;
-  uint8_t* se = s_esc[threadIdx.x >> 5];
-  for (uint32_t b = (blockIdx.x * blockDim.x + threadIdx.x) >> 5; b < nb; b += warps) {
-    const uint64_t vb = static_cast<uint64_t>(b) * kZBlock;
-    uint2 lw[4];
-    uint32_t cc[4];
-#pragma unroll
-    for (int q = 0; q < 4; ++q) {  // all four chunks' loads first
-      const uint32_t o = 256u * q + 8u * lane;
-      lw[q] = __ldg(reinterpret_cast<const uint2*>(lo + vb + o));
-      const uint64_t seg = (vb + o) >> 5;
-      cc[q] = z_codes8<BITS>(codes + seg * BITS, j);
-    }
-    const uint32_t eoff = __ldg(esc_off + b), eend = __ldg(esc_off + b + 1);
-    const uint32_t n_stage = min(eend - eoff, static_cast<uint32_t>(kZEscStage));
-    for (uint32_t k = lane; k < n_stage; k += 32) se[k] = esc[eoff + k];
-    __syncwarp();
-    uint32_t run = eoff;  // escapes before this chunk in value order
-#pragma unroll
-    for (int q = 0; q < 4; ++q) {
-      int cnt = 0;
-#pragma unroll
-      for (int i = 0; i < 8; ++i) cnt += ((cc[q] >> (BITS * i)) & kMask) == kEsc;
-      int incl = cnt;
-#pragma unroll
-      for (int d = 1; d < 32; d <<= 1) {
-        const int t = __shfl_up_sync(0xffffffffu, incl, d);
-        if (lane >= d) incl += t;
-      }
-      uint32_t e_at = run + static_cast<uint32_t>(incl - cnt);
-      run += static_cast<uint32_t>(__shfl_sync(0xffffffffu, incl, 31));
-      uint32_t pk[4];
-#pragma unroll
-      for (int i = 0; i < 8; ++i) {
-        const uint32_t c = (cc[q] >> (BITS * i)) & kMask;
-        const uint32_t l = ((i < 4 ? lw[q].x : lw[q].y) >> (8 * (i & 3))) & 0xffu;
-        uint32_t ex = base + c;
-        if (c == kEsc) {
-          const uint32_t r = e_at - eoff;
-          ex = r < static_cast<uint32_t>(kZEscStage) ? se[r] : esc[e_at];
-          ++e_at;
-        }
-        const uint32_t v = ((l & 0x80u) << 8) | (ex << 7) | (l & 0x7fu);
-        if (i & 1) pk[i >> 1] |= v << 16;
-        else pk[i >> 1] = v;
-      }
-      const uint64_t v0 = vb + 256u * q + 8u * lane;
-      if (tile_h) {  // tiled slab (n = 3HF, a multiple of 1024: always full)
-        uint16_t* dst = out + z_untile32(static_cast<uint32_t>(v0) & ~31u, tile_h, tile_f) + 8 * j;
-        *reinterpret_cast<uint4*>(dst) = make_uint4(pk[0], pk[1], pk[2], pk[3]);
-      } else if (v0 + 8 <= n) {
-        *reinterpret_cast<uint4*>(out + v0) = make_uint4(pk[0], pk[1], pk[2], pk[3]);
-      } else {
-        for (int i = 0; i < 8 && v0 + i < n; ++i) out[v0 + i] = static_cast<uint16_t>(pk[i >> 1] >> (16 * (i & 1)));
-      }
-    }
-    __syncwarp();  // every lane done with s_esc before the next block restages it
-  }
-}
-
 // Escapes (all-ones codes) among a lane's 32 codes with word-level bit tricks.
 template <int BITS>
 __device__ __forceinline__ int z_count_esc(const uint32_t (&cw)[BITS + 1]) {
@@ -149,6 +42,103 @@ __device__ __forceinline__ int z_count_esc(const uint32_t (&cw)[BITS + 1]) {
     const uint64_t hi = (static_cast<uint64_t>(cw[1]) >> 31) | (static_cast<uint64_t>(cw[2]) << 1);
     return __popcll(lo & (lo >> 1) & (lo >> 2) & 0x1249249249249249ull) +
            __popcll(hi & (hi >> 1) & (hi >> 2) & 0x49249249ull);
+  }
+}
+
+constexpr int kZEscStage = 256;  // staged escapes per block (more: read from global)
+
+// Two codes (values i, i+1; i even) as 16-bit lanes of one word: the 2*BITS bits at
+// BITS*i of the lane's little-endian code words (funnel shift, constant after unrolling).
+template <int BITS>
+__device__ __forceinline__ uint32_t z_code_pair(const uint32_t (&cw)[BITS + 1], int i) {
+  const int bit = BITS * i, w = bit >> 5, sh = bit & 31;
+  const uint32_t t = __funnelshift_r(cw[w], cw[w + 1], sh);
+  constexpr uint32_t m = (1u << BITS) - 1u;
+  return (t & m) | ((t << (16 - BITS)) & (m << 16));
+}
+
+// Decoder (PS_ZDECODE=3, default): one warp per 1024-value block, 32 consecutive values
+// per lane (the v1 mapping: 2 x 16 B of lo bytes, BITS words of codes, 4 x 16 B
+// stores), with the value assembly done two bf16 at a time in 32-bit registers:
+//   L = two lo bytes in 16-bit lanes (one byte permute), C = two codes (funnel shift,
+//   mask), E = C + (base | base << 16),
+//   out = ((L << 8) & 0x80008000) | (E << 7) | (L & 0x007f007f)     (two LOP3s)
+// i.e. ~5 instructions per value instead of ~12 for the per-value path; a pair with an
+// escape (C lane == all ones, ~3 % of values at 3-bit codes) takes the per-value path.
+// The per-value version issue-limited at 70 % issue-active (ncu, profiles/r02_z_decode.md).
+template <int BITS>
+__global__ void __launch_bounds__(256, 4)
+z_decode_kernel(const uint8_t* __restrict__ z, uint64_t n, uint32_t base, uint32_t nb, uint32_t tile_h,
+                uint32_t tile_f, uint16_t* __restrict__ out) {
+  constexpr uint32_t kEsc = (1u << BITS) - 1u;
+  constexpr uint32_t kEscPair = (1u << BITS) | (1u << (16 + BITS));  // carry out of an all-ones lane
+  __shared__ uint8_t s_esc[8][kZEscStage];
+  const uint64_t n_pad = static_cast<uint64_t>(nb) * kZBlock;
+  const uint8_t* lo = z + z_lo_off();
+  const uint32_t* codes = reinterpret_cast<const uint32_t*>(z + z_codes_off(n_pad));
+  const uint32_t* esc_off = reinterpret_cast<const uint32_t*>(z + z_escoff_off(n_pad, BITS));
+  const uint8_t* esc = z + z_esc_off(n_pad, nb, BITS);
+  const int lane = threadIdx.x & 31;
+  const uint32_t warps = (gridDim.x * blockDim.x) >> 5;
+  const uint32_t base2 = base | (base << 16);
+  uint8_t* se = s_esc[threadIdx.x >> 5];
+  for (uint32_t b = (blockIdx.x * blockDim.x + threadIdx.x) >> 5; b < nb; b += warps) {
+    const uint64_t seg = static_cast<uint64_t>(b) * 32 + lane;
+    const uint64_t v0 = seg * 32;
+    const uint4 l0 = __ldg(reinterpret_cast<const uint4*>(lo + v0));
+    const uint4 l1 = __ldg(reinterpret_cast<const uint4*>(lo + v0 + 16));
+    uint32_t cw[BITS + 1];
+#pragma unroll
+    for (int q = 0; q < BITS; ++q) cw[q] = __ldg(codes + seg * BITS + q);
+    cw[BITS] = 0;
+    const uint32_t eoff = __ldg(esc_off + b), eend = __ldg(esc_off + b + 1);
+    const uint32_t n_stage = min(eend - eoff, static_cast<uint32_t>(kZEscStage));
+    for (uint32_t k = lane; k < n_stage; k += 32) se[k] = esc[eoff + k];
+    __syncwarp();
+    const int n_e = z_count_esc<BITS>(cw);  // escapes of this lane, then the warp's exclusive scan
+    int incl = n_e;
+#pragma unroll
+    for (int o = 1; o < 32; o <<= 1) {
+      const int t = __shfl_up_sync(0xffffffffu, incl, o);
+      if (lane >= o) incl += t;
+    }
+    uint32_t e_at = eoff + static_cast<uint32_t>(incl - n_e);
+    const uint32_t lw[8] = {l0.x, l0.y, l0.z, l0.w, l1.x, l1.y, l1.z, l1.w};
+    const bool full = v0 + 32 <= n;
+    uint16_t* dst = tile_h ? out + z_untile(v0, tile_h, tile_f) : out + v0;
+#pragma unroll
+    for (int q = 0; q < 4; ++q) {  // 8 values -> one 16-byte store
+      uint32_t pk[4];
+#pragma unroll
+      for (int h = 0; h < 4; ++h) {
+        const int p = 4 * q + h;                       // pair index: values 2p, 2p+1
+        const uint32_t L = __byte_perm(lw[p >> 1], 0u, (p & 1) ? 0x4342u : 0x4140u);
+        const uint32_t C = z_code_pair<BITS>(cw, 2 * p);
+        uint32_t E = C + base2;
+        if ((C + 0x00010001u) & kEscPair) {  // an escape in this pair: its raw exponent(s)
+          uint32_t e_lo = E & 0xffffu, e_hi = E >> 16;
+          if ((C & kEsc) == kEsc) {
+            const uint32_t r = e_at - eoff;
+            e_lo = r < static_cast<uint32_t>(kZEscStage) ? se[r] : esc[e_at];
+            ++e_at;
+          }
+          if (((C >> 16) & kEsc) == kEsc) {
+            const uint32_t r = e_at - eoff;
+            e_hi = r < static_cast<uint32_t>(kZEscStage) ? se[r] : esc[e_at];
+            ++e_at;
+          }
+          E = e_lo | (e_hi << 16);
+        }
+        pk[h] = ((L << 8) & 0x80008000u) | (E << 7) | (L & 0x007f007fu);
+      }
+      if (full) {
+        reinterpret_cast<uint4*>(dst)[q] = make_uint4(pk[0], pk[1], pk[2], pk[3]);
+      } else {
+        for (int j = 0; j < 8 && v0 + 8 * q + j < n; ++j)
+          out[v0 + 8 * q + j] = static_cast<uint16_t>(pk[j >> 1] >> (16 * (j & 1)));
+      }
+    }
+    __syncwarp();  // every lane done with s_esc before the next block restages it
   }
 }
 
@@ -444,14 +434,14 @@ ps_status ps_zslab_decode(const uint8_t* z_dev, const uint8_t* z_host_header, ui
     require(h.magic == kZMagic, "ps_zslab_decode: not a z-slab");
     const int threads = 256;
     const int grid = static_cast<int>(std::min<uint64_t>((static_cast<uint64_t>(h.nb) * 32 + threads - 1) / threads,
-                                                         5 * 148));
+                                                         4 * 148));
     require(h.code_bits == 3 || h.code_bits == 4, "ps_zslab_decode: bad code width");
     const uint32_t th = h.tiled ? h.tile_h : 0, tf = h.tiled ? h.tile_f : 0;
     require(!h.tiled || (th % 32 == 0 && tf % 32 == 0 && th && tf && h.n == 3ull * th * tf && h.n < (1ull << 32)),
             "ps_zslab_decode: bad tiled header");
-    static const int version = [] {
+    static const int version = [] {  // PS_ZDECODE=1: the round-1 per-value decoder (A/B)
       const char* v = std::getenv("PS_ZDECODE");
-      return v && v[0] == '1' ? 1 : 2;
+      return v && v[0] == '1' ? 1 : 3;
     }();
     if (version == 1) {
       const int grid1 = static_cast<int>(std::min<uint64_t>((static_cast<uint64_t>(h.nb) * 32 + threads - 1) / threads,

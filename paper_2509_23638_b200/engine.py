@@ -300,6 +300,9 @@ class Engine:
                                                ap.ctypes.data_as(C.c_void_p), k, gp.ctypes.data_as(C.c_void_p),
                                                a.ctypes.data_as(C.c_void_p), k, steps, lr))
 
+    def set_lookahead(self, lookahead: int, steal_late: bool = False):
+        check(self.lib.ps_engine_set_lookahead(self.h, lookahead, int(bool(steal_late))))
+
     def set_cost(self, t_io, t_g, t_attn, beta, startup):
         """Replace the PreSched cost parameters (ps_engine_set_cost)."""
         check(self.lib.ps_engine_set_cost(self.h, C.byref(capi.CostParams(t_io, t_g, t_attn, beta, startup, 0))))
