@@ -58,92 +58,142 @@ __device__ __forceinline__ uint32_t z_code_pair(const uint32_t (&cw)[BITS + 1], 
 }
 
 // Decoder (PS_ZDECODE=3, default): one warp per 1024-value block, 32 consecutive values
-// per lane (the v1 mapping: 2 x 16 B of lo bytes, BITS words of codes, 4 x 16 B
-// stores), with the value assembly done two bf16 at a time in 32-bit registers:
+// per lane (2 x 16 B of lo bytes, BITS words of codes), branch-free: every value is
+// assembled as if its code were not an escape, two bf16 at a time in 32-bit registers —
 //   L = two lo bytes in 16-bit lanes (one byte permute), C = two codes (funnel shift,
-//   mask), E = C + (base | base << 16),
-//   out = ((L << 8) & 0x80008000) | (E << 7) | (L & 0x007f007f)     (two LOP3s)
-// i.e. ~5 instructions per value instead of ~12 for the per-value path; a pair with an
-// escape (C lane == all ones, ~3 % of values at 3-bit codes) takes the per-value path.
-// The per-value version issue-limited at 70 % issue-active (ncu, profiles/r02_z_decode.md).
+//   masks), out = ((L << 8) & 0x80008000) | ((C + (base | base << 16)) << 7) | (L & 0x007f007f)
+// — then the lane's escapes (all-ones codes, ~3 % of values at 3-bit codes, found with
+// word-level bit tricks) are patched. The block is staged in shared memory (XOR-swizzled
+// 16-byte chunks) and written out as whole sectors: 512 contiguous bytes per warp store
+// (row-major) or 64 per 4 lanes (a tiled slab's 32-value tile rows). Per-lane 16-byte
+// stores at a 64-byte stride made every write a half-sector request and the L1->XBAR
+// request path the limiter (72 % busy, DRAM 40 %; profiles/r02_z_decode.md). The next
+// block's loads are issued before the current block is assembled (software pipeline).
 template <int BITS>
 __global__ void __launch_bounds__(256, 4)
 z_decode_kernel(const uint8_t* __restrict__ z, uint64_t n, uint32_t base, uint32_t nb, uint32_t tile_h,
                 uint32_t tile_f, uint16_t* __restrict__ out) {
-  constexpr uint32_t kEsc = (1u << BITS) - 1u;
-  constexpr uint32_t kEscPair = (1u << BITS) | (1u << (16 + BITS));  // carry out of an all-ones lane
   __shared__ uint8_t s_esc[8][kZEscStage];
+  __shared__ __align__(16) uint4 s_out[8][128];  // per warp: 32 lanes x 4 chunks of 8 bf16
   const uint64_t n_pad = static_cast<uint64_t>(nb) * kZBlock;
   const uint8_t* lo = z + z_lo_off();
   const uint32_t* codes = reinterpret_cast<const uint32_t*>(z + z_codes_off(n_pad));
   const uint32_t* esc_off = reinterpret_cast<const uint32_t*>(z + z_escoff_off(n_pad, BITS));
   const uint8_t* esc = z + z_esc_off(n_pad, nb, BITS);
-  const int lane = threadIdx.x & 31;
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
   const uint32_t warps = (gridDim.x * blockDim.x) >> 5;
   const uint32_t base2 = base | (base << 16);
-  uint8_t* se = s_esc[threadIdx.x >> 5];
-  for (uint32_t b = (blockIdx.x * blockDim.x + threadIdx.x) >> 5; b < nb; b += warps) {
-    const uint64_t seg = static_cast<uint64_t>(b) * 32 + lane;
-    const uint64_t v0 = seg * 32;
-    const uint4 l0 = __ldg(reinterpret_cast<const uint4*>(lo + v0));
-    const uint4 l1 = __ldg(reinterpret_cast<const uint4*>(lo + v0 + 16));
+  uint8_t* se = s_esc[warp];
+  uint4* so = s_out[warp];
+  // swizzled 16-byte slot: a quarter-warp's 16-byte stores (fixed q) hit 8 distinct bank groups
+  auto chunk = [](int ln, int q) { return ln * 4 + (q ^ ((ln >> 1) & 3)); };
+  struct Blk {
+    uint4 l0, l1;
+    uint32_t cw[BITS];
+    uint32_t eoff, eend;
+  };
+  auto fetch = [&](uint32_t bb, Blk& k) {
+    const uint64_t seg = static_cast<uint64_t>(bb) * 32 + lane;
+    k.l0 = __ldg(reinterpret_cast<const uint4*>(lo + seg * 32));
+    k.l1 = __ldg(reinterpret_cast<const uint4*>(lo + seg * 32 + 16));
+#pragma unroll
+    for (int q = 0; q < BITS; ++q) k.cw[q] = __ldg(codes + seg * BITS + q);
+    k.eoff = __ldg(esc_off + bb);
+    k.eend = __ldg(esc_off + bb + 1);
+  };
+  uint32_t b = (blockIdx.x * blockDim.x + threadIdx.x) >> 5;
+  Blk nxt{};
+  if (b < nb) fetch(b, nxt);
+  for (; b < nb; b += warps) {
+    const Blk cur = nxt;
+    if (b + warps < nb) fetch(b + warps, nxt);
+    const uint64_t vb = static_cast<uint64_t>(b) * kZBlock;
+    const uint64_t v0 = vb + 32u * lane;
     uint32_t cw[BITS + 1];
 #pragma unroll
-    for (int q = 0; q < BITS; ++q) cw[q] = __ldg(codes + seg * BITS + q);
+    for (int q = 0; q < BITS; ++q) cw[q] = cur.cw[q];
     cw[BITS] = 0;
-    const uint32_t eoff = __ldg(esc_off + b), eend = __ldg(esc_off + b + 1);
-    const uint32_t n_stage = min(eend - eoff, static_cast<uint32_t>(kZEscStage));
-    for (uint32_t k = lane; k < n_stage; k += 32) se[k] = esc[eoff + k];
-    __syncwarp();
-    const int n_e = z_count_esc<BITS>(cw);  // escapes of this lane, then the warp's exclusive scan
-    int incl = n_e;
+    const uint32_t lw[8] = {cur.l0.x, cur.l0.y, cur.l0.z, cur.l0.w, cur.l1.x, cur.l1.y, cur.l1.z, cur.l1.w};
 #pragma unroll
-    for (int o = 1; o < 32; o <<= 1) {
-      const int t = __shfl_up_sync(0xffffffffu, incl, o);
-      if (lane >= o) incl += t;
-    }
-    uint32_t e_at = eoff + static_cast<uint32_t>(incl - n_e);
-    const uint32_t lw[8] = {l0.x, l0.y, l0.z, l0.w, l1.x, l1.y, l1.z, l1.w};
-    const bool full = v0 + 32 <= n;
-    uint16_t* dst = tile_h ? out + z_untile(v0, tile_h, tile_f) : out + v0;
-#pragma unroll
-    for (int q = 0; q < 4; ++q) {  // 8 values -> one 16-byte store
+    for (int q = 0; q < 4; ++q) {  // 8 values -> one 16-byte chunk in shared memory
       uint32_t pk[4];
 #pragma unroll
       for (int h = 0; h < 4; ++h) {
-        const int p = 4 * q + h;                       // pair index: values 2p, 2p+1
+        const int p = 4 * q + h;  // values 2p, 2p+1
         const uint32_t L = __byte_perm(lw[p >> 1], 0u, (p & 1) ? 0x4342u : 0x4140u);
-        const uint32_t C = z_code_pair<BITS>(cw, 2 * p);
-        uint32_t E = C + base2;
-        if ((C + 0x00010001u) & kEscPair) {  // an escape in this pair: its raw exponent(s)
-          uint32_t e_lo = E & 0xffffu, e_hi = E >> 16;
-          if ((C & kEsc) == kEsc) {
-            const uint32_t r = e_at - eoff;
-            e_lo = r < static_cast<uint32_t>(kZEscStage) ? se[r] : esc[e_at];
-            ++e_at;
-          }
-          if (((C >> 16) & kEsc) == kEsc) {
-            const uint32_t r = e_at - eoff;
-            e_hi = r < static_cast<uint32_t>(kZEscStage) ? se[r] : esc[e_at];
-            ++e_at;
-          }
-          E = e_lo | (e_hi << 16);
-        }
-        pk[h] = ((L << 8) & 0x80008000u) | (E << 7) | (L & 0x007f007fu);
+        pk[h] = ((L << 8) & 0x80008000u) | ((z_code_pair<BITS>(cw, 2 * p) + base2) << 7) | (L & 0x007f007fu);
       }
-      if (full) {
-        reinterpret_cast<uint4*>(dst)[q] = make_uint4(pk[0], pk[1], pk[2], pk[3]);
+      so[chunk(lane, q)] = make_uint4(pk[0], pk[1], pk[2], pk[3]);
+    }
+    if (cur.eend != cur.eoff) {  // escapes in this block (warp-uniform): patch them in smem
+      const uint32_t eoff = cur.eoff;
+      const uint32_t n_stage = min(cur.eend - eoff, static_cast<uint32_t>(kZEscStage));
+      for (uint32_t k = lane; k < n_stage; k += 32) se[k] = esc[eoff + k];
+      __syncwarp();
+      const int n_e = z_count_esc<BITS>(cw);
+      int incl = n_e;  // warp exclusive scan of escape counts -> this lane's first rank
+#pragma unroll
+      for (int o = 1; o < 32; o <<= 1) {
+        const int t = __shfl_up_sync(0xffffffffu, incl, o);
+        if (lane >= o) incl += t;
+      }
+      uint32_t e_at = eoff + static_cast<uint32_t>(incl - n_e);
+      uint16_t* so16 = reinterpret_cast<uint16_t*>(so);
+      auto patch = [&](int i) {  // value i of this lane, in value (= escape) order
+        const uint32_t r = e_at - eoff;
+        const uint32_t ex = r < static_cast<uint32_t>(kZEscStage) ? se[r] : esc[e_at];
+        ++e_at;
+        const uint32_t l = __ldg(lo + v0 + i);  // lo byte (L1 hit)
+        so16[chunk(lane, i >> 3) * 8 + (i & 7)] = static_cast<uint16_t>(((l & 0x80u) << 8) | (ex << 7) | (l & 0x7fu));
+      };
+      if constexpr (BITS == 3) {
+        const uint64_t A = static_cast<uint64_t>(cw[0]) | (static_cast<uint64_t>(cw[1]) << 32);
+        const uint64_t B = (static_cast<uint64_t>(cw[1]) >> 31) | (static_cast<uint64_t>(cw[2]) << 1);
+        uint64_t ma = A & (A >> 1) & (A >> 2) & 0x1249249249249249ull;  // codes 0..20: bit 3i
+        uint64_t mb = B & (B >> 1) & (B >> 2) & 0x49249249ull;          // codes 21..31
+        while (ma) {
+          const int pos = __ffsll(static_cast<long long>(ma)) - 1;
+          ma &= ma - 1;
+          patch(pos / 3);
+        }
+        while (mb) {
+          const int pos = __ffsll(static_cast<long long>(mb)) - 1;
+          mb &= mb - 1;
+          patch(21 + pos / 3);
+        }
       } else {
-        for (int j = 0; j < 8 && v0 + 8 * q + j < n; ++j)
-          out[v0 + 8 * q + j] = static_cast<uint16_t>(pk[j >> 1] >> (16 * (j & 1)));
+#pragma unroll
+        for (int q = 0; q < 4; ++q) {
+          uint32_t m = cw[q] & (cw[q] >> 1) & (cw[q] >> 2) & (cw[q] >> 3) & 0x11111111u;
+          while (m) {
+            const int pos = __ffs(m) - 1;
+            m &= m - 1;
+            patch(8 * q + pos / 4);
+          }
+        }
       }
     }
-    __syncwarp();  // every lane done with s_esc before the next block restages it
+    __syncwarp();
+    // write-out: 16-byte chunk c = lane + 32 r is values 8c..8c+7 of the block (segment
+    // c / 4 = the lane that assembled it, quarter c % 4)
+    if (vb + kZBlock <= n) {
+      const uint64_t my_off = tile_h ? z_untile(v0, tile_h, tile_f) : v0;  // this lane's segment start
+#pragma unroll
+      for (int r = 0; r < 4; ++r) {
+        const int c = lane + 32 * r, sl = c >> 2, q = c & 3;
+        const uint64_t seg_off = __shfl_sync(0xffffffffu, my_off, sl);
+        *reinterpret_cast<uint4*>(out + seg_off + 8 * q) = so[chunk(sl, q)];
+      }
+    } else {  // the last, partial block of a row-major slab (tiled slabs are whole blocks)
+      const uint16_t* so16 = reinterpret_cast<const uint16_t*>(so);
+      for (int i = 0; i < 32; ++i)
+        if (v0 + i < n) out[v0 + i] = so16[chunk(lane, i >> 3) * 8 + (i & 7)];
+    }
+    __syncwarp();  // staging buffers are reused by the next block
   }
 }
 
-// One warp per 1024-value block, 32 values per lane: lane L's codes are the BITS*4 bytes
-// at BITS*4*L of the block's code region (bit 3i.. of a little-endian word array).
+// Code i of a lane's 32 (v1 decoder): BITS bits at BITS*i of its little-endian words.
 template <int BITS>
 __device__ __forceinline__ uint32_t z_code(const uint32_t (&cw)[BITS + 1], int i) {
   const int bit = BITS * i, w = bit >> 5, sh = bit & 31;
