@@ -635,6 +635,9 @@ def decode_summary(st, dev_ms, N, B, L):
                    "ondemand_loads_per_step": st["ondemand_loads"] / steps,
                    "prefetches_per_step": st["prefetches_committed"] / steps,
                    "prefetch_hits_per_step": st["prefetch_hits"] / steps,
+                   # committed prefetches the target layer actually routed tokens to
+                   "prefetch_use_rate": (st["prefetches_used"] / st["prefetches_committed"]
+                                         if st["prefetches_committed"] else None),
                    "lookahead_prefetches_per_step": st["lookahead_prefetches"] / steps,
                    "stolen_prefetches_per_step": st["stolen_prefetches"] / steps,
                    # 1 - (compute-stream stall on copy events) / (copy-engine busy time)

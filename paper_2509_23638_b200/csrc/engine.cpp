@@ -1109,13 +1109,28 @@ void layer_forward(ps_engine_s& e, int l, const float* x, const uint8_t* follow,
       one.slabs[0] = static_cast<const uint16_t*>(r.slot->dev);
       ffn(e, one, counts_l.data(), B, true);
     };
+    // Prefetches whose copies have already landed share ONE FFN launch (a single-expert
+    // decode launch streams at ~65 % of HBM, a group at ~90 %); the others each wait for
+    // their copy in their own launch (or, with steal_late, are deferred).
+    // (landed ones first: a later wait on an in-flight copy would hold the group back)
+    ps_expert_group landed{};
+    std::vector<const ps_engine_s::Ready*> in_flight;
     for (auto& r : e.ready) {
       if (r.layer != l || counts_l[r.expert] == 0) continue;
-      if (e.lane && e.cfg.steal_late && cudaEventQuery(r.job->done_ev) == cudaErrorNotReady) {
-        late.push_back(&r);
-        continue;
+      e.st.prefetches_used++;  // a committed prefetch its target layer routed tokens to
+      if (cudaEventQuery(r.job->done_ev) == cudaSuccess && landed.n < PS_MAX_GROUP) {
+        land(e, r.job);
+        landed.experts[landed.n] = r.expert;
+        landed.slabs[landed.n] = static_cast<const uint16_t*>(r.slot->dev);
+        ++landed.n;
+      } else {
+        in_flight.push_back(&r);
       }
-      gpu_ready(r);
+    }
+    if (landed.n > 0) ffn(e, landed, counts_l.data(), B, true);
+    for (const ps_engine_s::Ready* r : in_flight) {
+      if (e.lane && e.cfg.steal_late) late.push_back(r);
+      else gpu_ready(*r);
     }
 
     // --- R4: scheduler inputs ------------------------------------------------------

@@ -247,3 +247,39 @@ def test_host_lane_reads_tiled_zslabs_bitwise(bits, monkeypatch):
         np.testing.assert_array_equal(y_raw, y_z)
     finally:
         lib.ps_host_lane_destroy(lane)
+
+
+@needs_bf16
+@pytest.mark.skipif(not (_has("amx_bf16") and _has("avx512_vbmi2")), reason="z-slab lane path needs AMX-BF16 + VBMI2")
+def test_host_lane_full_mixtral_expert_tiled_z_vs_oracle():
+    """The bench's lane configuration at the bench's shape: one Mixtral expert (H=4096,
+    F=14336) in the tile layout, read as a 3-bit tiled z-slab (ps_host_expert_ffn_batch_z,
+    the engine's default) — bitwise equal to the tiled raw path, and per token within the
+    bf16 tolerance of the f64 oracle (4 decode tokens, as a B=16 step routes ~4 per expert)."""
+    lib = ps.load()
+    H, F, m = 4096, 14336, 4
+    s = orc.or_init_slab(H, F, 1, 3, 5)
+    t = s.copy()
+    ps.check(lib.ps_host_slab_tile(t.ctypes.data, H, F))
+    cap = lib.ps_zslab_bound(s.size)
+    z = np.zeros(cap, np.uint8)
+    nb = C.c_uint64()
+    ps.check(lib.ps_zslab_encode_tiled(t.ctypes.data, H, F, z.ctypes.data, cap, C.byref(nb), 0))
+    assert z[40:44].view(np.uint32)[0] == 3  # the encoder picks 3-bit codes on these weights
+    x = orc.f32_to_bf16((np.random.default_rng(1).standard_normal((m, H)) / np.sqrt(H)).astype(np.float32))
+    lane = _lane(os.cpu_count() or 1, "amx")
+    try:
+        ma, ra = np.array([m], np.int32), np.array([0], np.int32)
+        y_t = np.full((m, H), np.nan, np.float32)
+        y_z = np.full((m, H), np.nan, np.float32)
+        ps.check(lib.ps_host_expert_ffn_batch_tiled(lane, 1, (C.c_void_p * 1)(t.ctypes.data), ma.ctypes.data,
+                                                    ra.ctypes.data, H, F, x.ctypes.data, y_t.ctypes.data))
+        ps.check(lib.ps_host_expert_ffn_batch_z(lane, 1, (C.c_void_p * 1)(z.ctypes.data), ma.ctypes.data,
+                                                ra.ctypes.data, H, F, x.ctypes.data, y_z.ctypes.data))
+        np.testing.assert_array_equal(y_t, y_z)
+    finally:
+        lib.ps_host_lane_destroy(lane)
+    yr = np.empty((m, H), np.float32)
+    orc.oracle_lib().or_expert_ffn(s.ctypes.data, H, F, m, x.ctypes.data, yr.ctypes.data, 1)
+    for tok in range(m):
+        assert np.linalg.norm(y_z[tok] - yr[tok]) / np.linalg.norm(yr[tok]) < BF16_RTOL
