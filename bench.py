@@ -644,12 +644,31 @@ def decode_summary(st, dev_ms, N, B, L):
                    "hidden_fraction": (1.0 - st["compute_wait_ms"] / st["h2d_busy_ms"]) if st["h2d_busy_ms"] > 0
                    else 1.0},
            "cost_params_us": st["cost"], "calibration_fit_cost_params": bool(st["calibration_fit"])}
+    # host DRAM: everything non-resident is read from it, by the lane (its z-slab reads)
+    # or by the PCIe DMA; roofline = the host's measured read bandwidth
+    # (scripts/probes/host_stream.c on the GPU box, profiles/r02_host_stream.jsonl)
+    step_s = dev_ms / 1e3
+    lane_gbs = st["cpu_read_bytes"] / steps / step_s / 1e9
+    dma_gbs = st["h2d_bytes"] / steps / step_s / 1e9
+    peak = host_dram_peak()
+    out["host_dram"] = {"lane_read_gbs": lane_gbs, "pcie_dma_read_gbs": dma_gbs, "total_gbs": lane_gbs + dma_gbs,
+                        "peak_gbs": peak, "frac": (lane_gbs + dma_gbs) / peak if peak else None,
+                        "peak_source": "profiles/r02_host_stream.jsonl (16-thread AVX-512 read stream, 32 GB)"}
     if st["cpu_experts"]:
         out["cpu_lane"] = {"experts_per_step": st["cpu_experts"] / steps,
                            "busy_ms_per_step": st["cpu_ms_total"] / steps,
                            "achieved_gbs": st["cpu_bytes_total"] / (st["cpu_ms_total"] / 1e3) / 1e9,
                            "threads": None}
     return out
+
+
+def host_dram_peak():
+    """Best host-DRAM read bandwidth measured on the pool's GPU boxes (GB/s), if recorded."""
+    p = ROOT / "profiles" / "r02_host_stream.jsonl"
+    try:
+        return max(json.loads(l)["best_gbs"] for l in p.read_text().splitlines() if l.strip())
+    except (OSError, ValueError, KeyError):
+        return None
 
 
 def N_world(dist):

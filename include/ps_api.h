@@ -632,6 +632,7 @@ typedef struct {
   int64_t stolen_prefetches;    /* late prefetched experts the host lane computed (steal_late) */
   int64_t calibration_fit;      /* 1: the last ps_engine_calibrate took beta/C from fit_cost_params */
   int64_t prefetches_used;      /* committed prefetches whose target layer routed tokens to them */
+  double cpu_read_bytes;        /* host-DRAM bytes the lane read (z-slab or raw bytes) */
 } ps_engine_stats;
 ps_status ps_engine_get_stats(ps_engine e, ps_engine_stats* out);
 ps_status ps_engine_reset_stats(ps_engine e);

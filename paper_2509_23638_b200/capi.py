@@ -131,7 +131,8 @@ class EngineStats(C.Structure):
                 ("cost", CostParams), ("cpu_experts", C.c_int64), ("cpu_ms_total", C.c_double),
                 ("cpu_bytes_total", C.c_double), ("z_decodes", C.c_int64), ("h2d_expert_bytes", C.c_double),
                 ("lookahead_prefetches", C.c_int64), ("stolen_prefetches", C.c_int64),
-                ("calibration_fit", C.c_int64), ("prefetches_used", C.c_int64)]
+                ("calibration_fit", C.c_int64), ("prefetches_used", C.c_int64),
+                ("cpu_read_bytes", C.c_double)]
 
 
 PLAN_FN = C.CFUNCTYPE(C.c_int, C.c_void_p, C.POINTER(LayerInputs), C.c_int, C.POINTER(LayerPlan))

@@ -725,6 +725,14 @@ void land(ps_engine_s& e, IoJob* j) {
   }
 }
 
+// Host-DRAM bytes the lane reads for one expert: its z-slab when the lane takes the z
+// path (every host slab has one and this host can decode them), else the raw slab.
+double lane_read_bytes(const ps_engine_s& e, const CpuJob& j) {
+  if (j.z && lane_z_enabled() && ps_host_lane_reads_z(e.lane))
+    return static_cast<double>(reinterpret_cast<const ZHeader*>(j.z)->bytes);
+  return static_cast<double>(e.cfg.spec.expert_bytes);
+}
+
 double push_modelled(ps_engine_s& e) {  // channel busy-until model for alpha (R4)
   const double now = now_us();
   e.io_free_us = std::max(e.io_free_us, now) + static_cast<double>(e.cfg.cost.t_io);
@@ -1254,6 +1262,7 @@ void layer_forward(ps_engine_s& e, int l, const float* x, const uint8_t* follow,
         e.st.kernel_launches += 1;
         e.st.cpu_experts += 1;
         e.st.cpu_bytes_total += static_cast<double>(e.cfg.spec.expert_bytes);
+        e.st.cpu_read_bytes += lane_read_bytes(e, j);
         j.t0_us -= host_t0_us;
         j.t1_us -= host_t0_us;
         e.cpu_done.push_back(j);
@@ -1291,6 +1300,7 @@ void layer_forward(ps_engine_s& e, int l, const float* x, const uint8_t* follow,
           e.st.kernel_launches += 1;
           e.st.cpu_experts += 1;
           e.st.cpu_bytes_total += static_cast<double>(e.cfg.spec.expert_bytes);
+          e.st.cpu_read_bytes += lane_read_bytes(e, j);
           e.st.cpu_ms_total += (j.t1_us - j.t0_us) / 1e3 / static_cast<double>(e.cpu_jobs.size());
           j.t0_us -= host_t0_us;
           j.t1_us -= host_t0_us;
