@@ -625,6 +625,8 @@ def decode_summary(st, dev_ms, N, B, L):
     steps = max(1, st["steps"])
     h2d_gbs = st["h2d_bytes"] / (st["h2d_busy_ms"] / 1e3) / 1e9 if st["h2d_busy_ms"] > 0 else 0.0
     out = {"value": N * B / (dev_ms / 1e3), "unit": "tokens/s", "ms_per_step": dev_ms,
+           "host_outside_device_ms_per_step": {"prologue": st["host_head_ms_total"] / steps,
+                                               "drain_and_measurement": st["host_tail_ms_total"] / steps},
            "moe_layer_us": dev_ms * 1e3 / L,
            "h2d": {"achieved_gbs": h2d_gbs, "peak_gbs": PCIE_H2D_PEAK_GBS, "frac": h2d_gbs / PCIE_H2D_PEAK_GBS,
                    "bytes_per_step": st["h2d_bytes"] / steps,

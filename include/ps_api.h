@@ -586,6 +586,41 @@ ps_status ps_engine_decode_step_host(ps_engine e, const float* hidden_host,
                                      const uint8_t* follow_host, int B, float* y_host,
                                      int32_t* ids_host);
 
+/* Stand-alone K5 expert cache: the AsyncIO channel of simulate_pipeline
+ * (simulator.cpp:61-242) for a caller that runs its own layer loop and FFN kernels.
+ * Resident pairs live in one HBM arena (<= budget); other experts are copied from the
+ * caller's host slabs into n_slots HBM staging slots by one serial copy channel (FIFO,
+ * queued prefetches cancellable, started copies non-interruptible). A slot keeps its
+ * expert after release. prefetch queues at the tail, ondemand ahead of queued prefetches
+ * (promoting a queued prefetch of the same expert); acquire makes `stream` wait for the
+ * copy and pins the slot; release records when `stream` is done with it (the next copy
+ * into that slot waits — R7's dual buffer generalised). No free slot -> PS_ERUNTIME (the
+ * simulator's prefetch-buffer overflow, simulator.cpp:209-212). Host slabs should be
+ * pinned for asynchronous copies. */
+typedef struct ps_cache_s* ps_cache;
+typedef struct {
+  int32_t num_layers, experts;
+  uint64_t expert_bytes;
+  const void* const* host_slabs;  /* [L*E] host pointers (caller-owned, outlive the cache) */
+  const int32_t* resident;        /* nullable [2*n_resident] (layer, expert) kept in HBM */
+  int32_t n_resident;
+  uint64_t budget_bytes;          /* n_resident * expert_bytes must fit */
+  int32_t n_slots;                /* staging slots for non-resident experts, >= 2 */
+  int32_t device;
+} ps_cache_config;
+typedef struct {
+  int64_t prefetches, ondemand_loads, prefetches_cancelled, slot_hits, resident_hits;
+} ps_cache_stats;
+ps_status ps_cache_create(const ps_cache_config* cfg, ps_cache* out);
+ps_status ps_cache_destroy(ps_cache c);
+ps_status ps_cache_prefetch(ps_cache c, int layer, int expert);
+ps_status ps_cache_ondemand(ps_cache c, int layer, int expert);
+ps_status ps_cache_acquire(ps_cache c, int layer, int expert, void* stream, const void** dev_slab);
+ps_status ps_cache_release(ps_cache c, int layer, int expert, void* stream);
+ps_status ps_cache_cancel_prefetches(ps_cache c, int* n_cancelled);  /* R2 at a scheduling point */
+ps_status ps_cache_sync(ps_cache c);  /* host: until every issued copy completed */
+ps_status ps_cache_get_stats(ps_cache c, ps_cache_stats* out);
+
 /* Per-layer K5 ABI — the reference's per-layer seam (plan_fn(inputs, l), simulator.cpp:136)
  * for a host model that runs its own attention between MoE layers:
  *
@@ -633,6 +668,8 @@ typedef struct {
   int64_t calibration_fit;      /* 1: the last ps_engine_calibrate took beta/C from fit_cost_params */
   int64_t prefetches_used;      /* committed prefetches whose target layer routed tokens to them */
   double cpu_read_bytes;        /* host-DRAM bytes the lane read (z-slab or raw bytes) */
+  double host_head_ms_total;    /* host time of each step's prologue (before its first GPU mark) */
+  double host_tail_ms_total;    /* host time after each step's GPU work: channel drain + measurement */
 } ps_engine_stats;
 ps_status ps_engine_get_stats(ps_engine e, ps_engine_stats* out);
 ps_status ps_engine_reset_stats(ps_engine e);

@@ -108,6 +108,17 @@ class ExpertGroup(C.Structure):
     _fields_ = [("n", C.c_int32), ("experts", C.c_int32 * PS_MAX_GROUP), ("slabs", C.c_void_p * PS_MAX_GROUP)]
 
 
+class CacheConfig(C.Structure):
+    _fields_ = [("num_layers", C.c_int32), ("experts", C.c_int32), ("expert_bytes", C.c_uint64),
+                ("host_slabs", C.POINTER(C.c_void_p)), ("resident", C.POINTER(C.c_int32)), ("n_resident", C.c_int32),
+                ("budget_bytes", C.c_uint64), ("n_slots", C.c_int32), ("device", C.c_int32)]
+
+
+class CacheStats(C.Structure):
+    _fields_ = [("prefetches", C.c_int64), ("ondemand_loads", C.c_int64), ("prefetches_cancelled", C.c_int64),
+                ("slot_hits", C.c_int64), ("resident_hits", C.c_int64)]
+
+
 class EngineConfig(C.Structure):
     _fields_ = [("spec", ModelSpec), ("gen", TraceGenConfig), ("weight_seed", C.c_uint64),
                 ("budget_bytes", C.c_uint64), ("resident", C.POINTER(C.c_int32)), ("n_resident", C.c_int32),
@@ -132,7 +143,8 @@ class EngineStats(C.Structure):
                 ("cpu_bytes_total", C.c_double), ("z_decodes", C.c_int64), ("h2d_expert_bytes", C.c_double),
                 ("lookahead_prefetches", C.c_int64), ("stolen_prefetches", C.c_int64),
                 ("calibration_fit", C.c_int64), ("prefetches_used", C.c_int64),
-                ("cpu_read_bytes", C.c_double)]
+                ("cpu_read_bytes", C.c_double), ("host_head_ms_total", C.c_double),
+                ("host_tail_ms_total", C.c_double)]
 
 
 PLAN_FN = C.CFUNCTYPE(C.c_int, C.c_void_p, C.POINTER(LayerInputs), C.c_int, C.POINTER(LayerPlan))
@@ -238,6 +250,15 @@ _SIGS = {
     "ps_engine_set_router": (C.c_int, [_P, _P]),
     "ps_engine_decode_step": (C.c_int, [_P, _P, _P, C.c_int, _P, _P]),
     "ps_engine_decode_step_host": (C.c_int, [_P, _P, _P, C.c_int, _P, _P]),
+    "ps_cache_create": (C.c_int, [C.POINTER(CacheConfig), C.POINTER(C.c_void_p)]),
+    "ps_cache_destroy": (C.c_int, [_P]),
+    "ps_cache_prefetch": (C.c_int, [_P, C.c_int, C.c_int]),
+    "ps_cache_ondemand": (C.c_int, [_P, C.c_int, C.c_int]),
+    "ps_cache_acquire": (C.c_int, [_P, C.c_int, C.c_int, _P, C.POINTER(C.c_void_p)]),
+    "ps_cache_release": (C.c_int, [_P, C.c_int, C.c_int, _P]),
+    "ps_cache_cancel_prefetches": (C.c_int, [_P, C.POINTER(C.c_int)]),
+    "ps_cache_sync": (C.c_int, [_P]),
+    "ps_cache_get_stats": (C.c_int, [_P, C.POINTER(CacheStats)]),
     "ps_engine_step_begin": (C.c_int, [_P, C.c_int]),
     "ps_engine_set_lookahead": (C.c_int, [_P, C.c_int, C.c_int]),
     "ps_engine_last_routing": (C.c_int, [_P, _P, _P]),

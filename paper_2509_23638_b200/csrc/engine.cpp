@@ -36,6 +36,7 @@
 #include <sys/mman.h>
 
 #include "cuda_host.hpp"
+#include "io_channel.hpp"
 #include "zslab_format.hpp"
 
 namespace ps {
@@ -94,171 +95,6 @@ struct PinnedArena {
     }
     ptr = nullptr;
   }
-};
-
-struct Slot {
-  void* dev = nullptr;
-  void* zdev = nullptr;            // landing buffer of a z-slab copy (decoded into dev)
-  cudaEvent_t free_ev = nullptr;   // recorded on the compute stream after the last reader
-  std::atomic<int64_t> recorded_gen{0};
-  int64_t next_gen = 0;            // generation a new copy must wait for
-  bool in_use = false;
-  int target_layer = -1;
-};
-
-enum JobKind { kOnDemand = 0, kPrefetch = 1 };
-
-struct IoJob {
-  int kind = kOnDemand;
-  int layer = 0, expert = 0, tokens = 0;
-  void* dst = nullptr;
-  const void* src = nullptr;
-  size_t bytes = 0;
-  Slot* slot = nullptr;
-  int64_t wait_gen = 0;        // slot->recorded_gen must reach this before issue
-  cudaEvent_t start_ev = nullptr, done_ev = nullptr;
-  std::atomic<int> state{0};   // 0 queued, 1 issued, 2 cancelled
-  bool critical = false;
-  int issue_group = 1;
-  const uint8_t* zhost = nullptr;  // z-slab source (header read on the host), null = raw copy
-  double t_io_us = 0;              // modelled transfer time (cost.t_io)
-  std::atomic<double> est_done_us{0};  // host-clock estimate of the copy's end (set at issue)
-};
-
-// The serial I/O channel: one copy stream, one host thread, FIFO with cancel.
-class IoChannel {
- public:
-  IoChannel(int device, int depth) : depth_(depth) {
-    device_ = device;
-    PS_CUDA(cudaStreamCreateWithFlags(&stream_, cudaStreamNonBlocking));
-    thread_ = std::thread([this] { run(); });
-  }
-  ~IoChannel() {
-    {
-      std::lock_guard<std::mutex> g(mu_);
-      stop_ = true;
-    }
-    cv_.notify_all();
-    thread_.join();
-    cudaStreamDestroy(stream_);
-  }
-  cudaStream_t stream() const { return stream_; }
-
-  void push(IoJob* j) {
-    {
-      std::lock_guard<std::mutex> g(mu_);
-      queue_.push_back(j);
-    }
-    cv_.notify_all();
-  }
-  void notify() { cv_.notify_all(); }
-  void wait_issued(IoJob* j) {
-    std::unique_lock<std::mutex> g(mu_);
-    cv_.wait(g, [&] { return j->state.load() != 0 || error_; });
-    if (error_) fail(PS_ECUDA, "I/O channel: " + err_msg_);
-  }
-  // Cancel queued (not yet issued) prefetch jobs; returns them (R2).
-  std::vector<IoJob*> cancel_queued_prefetches() {
-    std::vector<IoJob*> out;
-    std::lock_guard<std::mutex> g(mu_);
-    for (auto it = queue_.begin(); it != queue_.end();) {
-      if ((*it)->kind == kPrefetch && (*it)->state.load() == 0) {
-        (*it)->state = 2;
-        out.push_back(*it);
-        it = queue_.erase(it);
-      } else {
-        ++it;
-      }
-    }
-    return out;
-  }
-  // Step entry after a failed step: forget every job still queued (their FFNs were never
-  // launched, so slot generations they wait for would never come).
-  void abandon_queued() {
-    std::lock_guard<std::mutex> g(mu_);
-    for (IoJob* j : queue_) j->state = 2;
-    queue_.clear();
-    cv_.notify_all();
-  }
-  void drain() {  // wait until the queue is empty and every issued copy completed
-    std::unique_lock<std::mutex> g(mu_);
-    cv_.wait(g, [&] { return (queue_.empty() && !busy_) || error_; });
-    g.unlock();
-    PS_CUDA(cudaStreamSynchronize(stream_));
-  }
-  void check() {
-    std::lock_guard<std::mutex> g(mu_);
-    if (error_) fail(PS_ECUDA, "I/O channel: " + err_msg_);
-  }
-
- private:
-  void run() {
-    cudaSetDevice(device_);
-    std::deque<cudaEvent_t> in_flight;
-    std::unique_lock<std::mutex> g(mu_);
-    while (true) {
-      cv_.wait(g, [&] { return stop_ || !queue_.empty(); });
-      if (stop_) break;
-      busy_ = true;
-      // Throttle: at most depth_ copies in flight, so later queue entries stay
-      // cancellable until the channel is about to free up.
-      while (static_cast<int>(in_flight.size()) >= depth_) {
-        cudaEvent_t ev = in_flight.front();
-        g.unlock();
-        cudaError_t e = cudaEventSynchronize(ev);
-        g.lock();
-        in_flight.pop_front();
-        if (e != cudaSuccess) set_error(e);
-      }
-      if (queue_.empty()) {
-        busy_ = false;
-        cv_.notify_all();
-        continue;
-      }
-      IoJob* j = queue_.front();
-      if (j->slot && j->slot->recorded_gen.load() < j->wait_gen) {
-        // Slot still owned by an FFN the engine has not launched yet: wait for it.
-        cv_.wait(g, [&] { return stop_ || j->slot->recorded_gen.load() >= j->wait_gen || queue_.empty() ||
-                                 queue_.front() != j; });
-        if (stop_) break;
-        busy_ = false;
-        cv_.notify_all();  // drain() may be waiting for busy_ to clear (abandoned queue)
-        continue;  // re-evaluate the front (it may have been cancelled)
-      }
-      queue_.pop_front();
-      g.unlock();
-      cudaError_t e = cudaSuccess;
-      if (j->slot && j->wait_gen > 0) e = cudaStreamWaitEvent(stream_, j->slot->free_ev, 0);
-      if (e == cudaSuccess) e = cudaEventRecord(j->start_ev, stream_);
-      if (e == cudaSuccess) e = cudaMemcpyAsync(j->dst, j->src, j->bytes, cudaMemcpyHostToDevice, stream_);
-      if (e == cudaSuccess) e = cudaEventRecord(j->done_ev, stream_);
-      // FIFO channel: this copy ends t_io after the later of now and the previous end
-      est_end_ = std::max(est_end_, now_us()) + j->t_io_us;
-      j->est_done_us.store(est_end_);
-      g.lock();
-      if (e != cudaSuccess) set_error(e);
-      in_flight.push_back(j->done_ev);
-      j->state = 1;
-      busy_ = !queue_.empty();
-      cv_.notify_all();
-    }
-  }
-  void set_error(cudaError_t e) {
-    error_ = true;
-    err_msg_ = cudaGetErrorString(e);
-    cv_.notify_all();
-  }
-
-  int device_ = 0;
-  int depth_;
-  cudaStream_t stream_ = nullptr;
-  std::thread thread_;
-  std::mutex mu_;
-  std::condition_variable cv_;
-  std::deque<IoJob*> queue_;
-  double est_end_ = 0;  // modelled end of the last issued copy (I/O thread only)
-  bool stop_ = false, busy_ = false, error_ = false;
-  std::string err_msg_;
 };
 
 struct LayerDev {  // per-layer device outputs kept for the step
@@ -832,6 +668,7 @@ struct NvtxRange {
 // resets the per-step bookkeeping and marks the step start on the compute stream.
 void step_begin(ps_engine_s& e, int B) {
   require(B >= 1 && B <= e.maxB, "decode_step: batch out of range");
+  const double t_head0 = now_us();
   e.step_B = B;
   e.prefill_mode = B > kDecodeMaxBatch;
   // A step that threw mid-layer may have left jobs queued / a lane batch running: settle
@@ -864,6 +701,7 @@ void step_begin(ps_engine_s& e, int B) {
   e.last_pred.assign(static_cast<size_t>(e.L) * e.E, 0);
   e.next_layer = 0;
   e.in_step = true;
+  e.st.host_head_ms_total += (now_us() - t_head0) / 1e3;
 }
 
 // One MoE layer of the current step (rules R1-R8 for layer l): x [B,H] f32 gating input
@@ -1415,6 +1253,7 @@ void step_end(ps_engine_s& e, int32_t* ids_out) {
                               cudaMemcpyDeviceToDevice, e.sc));
   PS_CUDA(cudaEventRecord(e.ev_step1, e.sc));
   PS_CUDA(cudaEventSynchronize(e.ev_step1));
+  const double t_tail0 = now_us();  // host time after the step's GPU work (drain + measurement)
   // Prefetches still pending at the end of the pass are cancelled or drained.
   for (IoJob* j : e.io->cancel_queued_prefetches()) j->slot->in_use = false;
   e.io->drain();
@@ -1486,6 +1325,7 @@ void step_end(ps_engine_s& e, int32_t* ids_out) {
   e.st.step_ms_total += ms;
   e.st.steps += 1;
   e.st.layers += L;
+  e.st.host_tail_ms_total += (now_us() - t_tail0) / 1e3;
 }
 
 void decode_step(ps_engine_s& e, const float* hidden, const uint8_t* follow, int B, float* y, int32_t* ids_out,

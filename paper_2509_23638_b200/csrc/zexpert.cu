@@ -69,6 +69,18 @@ __device__ __forceinline__ uint32_t z_code_pair(const uint32_t (&cw)[BITS + 1], 
 // stores at a 64-byte stride made every write a half-sector request and the L1->XBAR
 // request path the limiter (72 % busy, DRAM 40 %; profiles/r02_z_decode.md). The next
 // block's loads are issued before the current block is assembled (software pipeline).
+// Row-major start of the 32-value tile row at tiled index v, in 32-bit arithmetic
+// (z_untile's 64-bit division is a ~100-instruction subroutine; the host checks
+// n = 3HF < 2^32 for tiled slabs).
+__device__ __forceinline__ uint32_t z_untile32(uint32_t v, uint32_t H, uint32_t F) {
+  const uint32_t fh = F * H;
+  const uint32_t base = v < fh ? 0u : (v < 2u * fh ? fh : 2u * fh);
+  const uint32_t K = v < 2u * fh ? H : F;
+  const uint32_t t = v - base, tile = t >> 9, i = (t >> 5) & 15u, nkb = K >> 5;
+  const uint32_t rb = tile / nkb, kb = tile - rb * nkb;
+  return base + (rb * 16u + i) * K + kb * 32u;
+}
+
 template <int BITS>
 __global__ void __launch_bounds__(256, 4)
 z_decode_kernel(const uint8_t* __restrict__ z, uint64_t n, uint32_t base, uint32_t nb, uint32_t tile_h,
@@ -177,7 +189,8 @@ z_decode_kernel(const uint8_t* __restrict__ z, uint64_t n, uint32_t base, uint32
     // write-out: 16-byte chunk c = lane + 32 r is values 8c..8c+7 of the block (segment
     // c / 4 = the lane that assembled it, quarter c % 4)
     if (vb + kZBlock <= n) {
-      const uint64_t my_off = tile_h ? z_untile(v0, tile_h, tile_f) : v0;  // this lane's segment start
+      const uint64_t my_off = tile_h ? static_cast<uint64_t>(z_untile32(static_cast<uint32_t>(v0), tile_h, tile_f))
+                                     : v0;  // this lane's segment start
 #pragma unroll
       for (int r = 0; r < 4; ++r) {
         const int c = lane + 32 * r, sl = c >> 2, q = c & 3;
