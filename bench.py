@@ -290,6 +290,7 @@ def run_ours(args):
     t_create = time.perf_counter() - t_create
     torch.cuda.synchronize()
     hbm_engine = free0 - torch.cuda.mem_get_info(local)[0]
+    thp_gb = anon_huge_gb()  # the host arenas ask for transparent huge pages (lane TLB reach)
     measured_cost = e.stats()["cost"]
 
     # device-resident step inputs (layer-major), outputs
@@ -503,6 +504,8 @@ def run_ours(args):
                              "note": "engine_total_device = device memory the engine allocated at create "
                                      "(resident arena + 2 on-demand and the prefetch staging slots with "
                                      "their z-slab landing buffers + routing/FFN scratch), cudaMemGetInfo delta"},
+        "host_memory": {"anon_huge_pages_gb": thp_gb, "note": "transparent huge pages backing the pinned host "
+                        "arenas after engine create (/proc/self/smaps_rollup); the lane streams them"},
         "wall_s_timed": wall, "engine_create_s": t_create,
         "cost_params_us": st["cost"],
     }
@@ -662,6 +665,16 @@ def decode_summary(st, dev_ms, N, B, L):
                            "achieved_gbs": st["cpu_bytes_total"] / (st["cpu_ms_total"] / 1e3) / 1e9,
                            "threads": None}
     return out
+
+
+def anon_huge_gb():
+    try:
+        for line in open("/proc/self/smaps_rollup"):
+            if line.startswith("AnonHugePages:"):
+                return int(line.split()[1]) / 1e6  # kB -> GB
+    except OSError:
+        pass
+    return None
 
 
 def host_dram_peak():

@@ -83,7 +83,7 @@ void request(ps_cache_s& c, int layer, int expert, bool ondemand) {
   auto it = c.by_key.find(key);
   if (it != c.by_key.end()) {  // already present or on its way
     ps_cache_s::Entry* e = it->second;
-    if (ondemand && e->job && e->job->state.load() == 0) {  // promote a queued prefetch
+    if (ondemand && e->job && e->job->kind == kPrefetch && e->job->state.load() == 0) {  // promote a queued prefetch
       for (IoJob* j : c.io->cancel_queued_prefetches()) {  // the others go back in their order
         j->state = 0;
         if (j != e->job) c.io->push(j);

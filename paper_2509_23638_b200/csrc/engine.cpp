@@ -279,6 +279,9 @@ struct ps_engine_s {
   uint64_t slab_elems = 0;
   cudaStream_t sc = nullptr;  // compute stream
   cudaStream_t s_d2h = nullptr;  // scheduling-point D2H (off the compute stream's critical path)
+  cudaStream_t s_pred[2] = {nullptr, nullptr};  // K4 for l+1 / l+2 (off the compute stream)
+  cudaEvent_t ev_k1 = nullptr, ev_pred[2] = {nullptr, nullptr};
+  void* llapor_scratch2 = nullptr;
   cudaEvent_t last_ffn_end = nullptr;  // end event of the last FFN enqueued (reused as a start mark)
   std::unique_ptr<ps::IoChannel> io;
 
@@ -761,30 +764,42 @@ void layer_forward(ps_engine_s& e, int l, const float* x, const uint8_t* follow,
     const bool dense_next = e.prefill_mode && B * K >= 16 * E && l + 1 < L;
     const bool want_pred = l + 1 < L && !dense_next && e.has_host[l + 1];
     const bool predict = want_pred && (e.pred_kind == PS_PRED_LLAPOR || e.pred_kind == PS_PRED_PERFECT);
-    if (predict && e.pred_kind == PS_PRED_LLAPOR) {
-      s = ps_llapor_forward(e.cfg.predictor, l + 1, x, ld.ids, K, ld.weights, B, K, nullptr, nullptr, e.pred_dev,
-                            e.llapor_scratch, e.sc);
-      if (s != PS_OK) fail(s, ps_last_error());
-      e.st.kernel_launches += 2;
-    } else if (predict) {  // PERFECT: layer l+1's true routing, K1 one layer early
-      require(x_next != nullptr, "PS_PRED_PERFECT needs layer l+1's inputs (not available per layer)");
-      s = ps_route_topk(x_next, e.gate + static_cast<size_t>(l + 1) * E * H, e.bias + static_cast<size_t>(l + 1) * E,
-                        follow_next, ld.ids, K, B, H, E, K, nullptr,
-                        e.pp_w, e.pp_ids, e.pred_dev, nullptr, e.sc);
-      if (s != PS_OK) fail(s, ps_last_error());
-      e.st.kernel_launches += 1;
-    }
     // --- K4 for layer l+2: e_next2 of the widened window (simulator.cpp:128-131) and the
     // lookahead top-up. The reference predicts l+2 from the true layer-(l+1) features,
     // which do not exist yet at layer l: nets[l+2] is applied to layer-l features instead.
     const bool want_pred2 = !e.ep && l + 2 < L && !e.prefill_mode && e.has_host[l + 2];
     const bool predict2 = want_pred2 && e.pred_kind == PS_PRED_LLAPOR;
-    if (predict2) {
-      s = ps_llapor_forward(e.cfg.predictor, l + 2, x, ld.ids, K, ld.weights, B, K, nullptr, nullptr, e.pred2_dev,
-                            e.llapor_scratch, e.sc);
+    // The two predictions run concurrently on two side streams forked after K1 and
+    // joined back into Sc before K2 / the resident FFN. (Left unjoined they would queue
+    // behind the persistent FFN kernel, which holds every SM, and delay the host's plan:
+    // layer-start-to-lane-start 370 vs 220 us, profiles/timelines/r02_hybrid_k4_unjoined.json.)
+    if (predict || predict2) PS_CUDA(cudaEventRecord(e.ev_k1, e.sc));
+    if (predict && e.pred_kind == PS_PRED_LLAPOR) {
+      PS_CUDA(cudaStreamWaitEvent(e.s_pred[0], e.ev_k1, 0));
+      s = ps_llapor_forward(e.cfg.predictor, l + 1, x, ld.ids, K, ld.weights, B, K, nullptr, nullptr, e.pred_dev,
+                            e.llapor_scratch, e.s_pred[0]);
       if (s != PS_OK) fail(s, ps_last_error());
       e.st.kernel_launches += 2;
+    } else if (predict) {  // PERFECT: layer l+1's true routing, K1 one layer early
+      require(x_next != nullptr, "PS_PRED_PERFECT needs layer l+1's inputs (not available per layer)");
+      PS_CUDA(cudaStreamWaitEvent(e.s_pred[0], e.ev_k1, 0));
+      s = ps_route_topk(x_next, e.gate + static_cast<size_t>(l + 1) * E * H, e.bias + static_cast<size_t>(l + 1) * E,
+                        follow_next, ld.ids, K, B, H, E, K, nullptr,
+                        e.pp_w, e.pp_ids, e.pred_dev, nullptr, e.s_pred[0]);
+      if (s != PS_OK) fail(s, ps_last_error());
+      e.st.kernel_launches += 1;
     }
+    if (predict) PS_CUDA(cudaEventRecord(e.ev_pred[0], e.s_pred[0]));
+    if (predict2) {
+      PS_CUDA(cudaStreamWaitEvent(e.s_pred[1], e.ev_k1, 0));
+      s = ps_llapor_forward(e.cfg.predictor, l + 2, x, ld.ids, K, ld.weights, B, K, nullptr, nullptr, e.pred2_dev,
+                            e.llapor_scratch2, e.s_pred[1]);
+      if (s != PS_OK) fail(s, ps_last_error());
+      e.st.kernel_launches += 2;
+      PS_CUDA(cudaEventRecord(e.ev_pred[1], e.s_pred[1]));
+    }
+    if (predict) PS_CUDA(cudaStreamWaitEvent(e.sc, e.ev_pred[0], 0));  // join
+    if (predict2) PS_CUDA(cudaStreamWaitEvent(e.sc, e.ev_pred[1], 0));
     // --- K2 permute indices ------------------------------------------------------
     // Prefill-sized batches gather x into contiguous permuted rows (TMA operand of the
     // tcgen05 path) and need the offsets on the host for tile scheduling.
@@ -1380,6 +1395,9 @@ void create_engine(const ps_engine_config& cfg, ps_engine_s& e) {
 
   PS_CUDA(cudaStreamCreateWithFlags(&e.sc, cudaStreamNonBlocking));
   PS_CUDA(cudaStreamCreateWithFlags(&e.s_d2h, cudaStreamNonBlocking));
+  for (auto& st : e.s_pred) PS_CUDA(cudaStreamCreateWithFlags(&st, cudaStreamNonBlocking));
+  PS_CUDA(cudaEventCreateWithFlags(&e.ev_k1, cudaEventDisableTiming));
+  for (auto& ev : e.ev_pred) PS_CUDA(cudaEventCreateWithFlags(&ev, cudaEventDisableTiming));
   e.io = std::make_unique<IoChannel>(cfg.device, 2);
 
   // Expert parallelism: this rank owns experts e % G == rank of every layer.
@@ -1629,7 +1647,10 @@ void create_engine(const ps_engine_config& cfg, ps_engine_s& e) {
     PS_CUDA(cudaMemcpy(e.ep_ones, ones.data(), sizeof(float) * frows, cudaMemcpyHostToDevice));
     PS_CUDA(cudaMemset(e.ep_zeros, 0, sizeof(int32_t) * frows));
   }
-  if (cfg.predictor) PS_CUDA(cudaMalloc(&e.llapor_scratch, ps_llapor_scratch_bytes(cfg.predictor, e.maxB)));
+  if (cfg.predictor) {
+    PS_CUDA(cudaMalloc(&e.llapor_scratch, ps_llapor_scratch_bytes(cfg.predictor, e.maxB)));
+    PS_CUDA(cudaMalloc(&e.llapor_scratch2, ps_llapor_scratch_bytes(cfg.predictor, e.maxB)));
+  }
   if (e.pred_kind == PS_PRED_PERFECT) {
     PS_CUDA(cudaMalloc(&e.pp_ids, sizeof(int32_t) * B * e.K));
     PS_CUDA(cudaMalloc(&e.pp_w, sizeof(float) * B * e.E));
@@ -1721,7 +1742,7 @@ void destroy_engine(ps_engine_s& e) {
   }
   for (void* p : {(void*)e.arena, (void*)e.gate, (void*)e.bias, (void*)e.sched_dev, (void*)e.route_ws, (void*)e.pp_ids, (void*)e.pp_w,
                   (void*)e.x_bf16, (void*)e.x_perm, (void*)e.inv, (void*)e.hbuf,
-                  (void*)e.y_part, e.llapor_scratch, (void*)e.in_hidden, (void*)e.in_follow, (void*)e.out_y,
+                  (void*)e.y_part, e.llapor_scratch, e.llapor_scratch2, (void*)e.in_hidden, (void*)e.in_follow, (void*)e.out_y,
                   (void*)e.out_ids, (void*)e.ep_vids, (void*)e.ep_off_v, (void*)e.ep_perm_v, (void*)e.ep_inv_v,
                   (void*)e.ep_send_x, (void*)e.ep_recv_x, (void*)e.ep_y_recv, (void*)e.ep_y_back,
                   (void*)e.ep_cnt_send, (void*)e.ep_cnt_recv, (void*)e.ep_plan_dev, (void*)e.ep_ones,
@@ -1744,8 +1765,14 @@ void destroy_engine(ps_engine_s& e) {
   }
   for (cudaEvent_t ev : e.event_pool) cudaEventDestroy(ev);
   for (cudaEvent_t ev : e.job_event_pool) cudaEventDestroy(ev);
-  for (cudaEvent_t ev : {e.ev_routed, e.ev_step0, e.ev_step1, e.ev_in, e.ev_out, e.ev_lane_rows})
+  for (cudaEvent_t ev : {e.ev_routed, e.ev_step0, e.ev_step1, e.ev_in, e.ev_out, e.ev_lane_rows, e.ev_k1, e.ev_pred[0],
+                         e.ev_pred[1]})
     if (ev) cudaEventDestroy(ev);
+  for (cudaStream_t st : e.s_pred)
+    if (st) {
+      cudaStreamSynchronize(st);
+      cudaStreamDestroy(st);
+    }
   if (e.sc) cudaStreamDestroy(e.sc);
   if (e.s_d2h) cudaStreamDestroy(e.s_d2h);
 }

@@ -56,6 +56,7 @@ struct ps_llapor_s {
   ps::HostModel host;            // f64 checkpoint model (fine_tune / save operate on it)
   std::vector<ps::NetDev> nets;  // index = target layer; nets[0] unused
   std::vector<uint8_t> stale;    // host net changed since its device copy (or never uploaded)
+  std::vector<std::pair<float*, size_t>> net_buf;  // per net: its device buffer and size (floats)
   std::vector<void*> allocs;
   int max_p = 0, max_in = 0, max_width = 0;
 };
@@ -407,9 +408,17 @@ void upload(ps_llapor_s& m, int layer) {
   for (auto& b : hn.res) { o_rw.push_back(put(b.w)); o_rb.push_back(put(b.b)); }
   size_t o_gate = put(hn.gate_w.empty() ? std::vector<double>{0.0} : hn.gate_w);
   size_t o_ow = put(hn.out.w), o_ob = put(hn.out.b);
-  float* dev = nullptr;
-  PS_CUDA(cudaMalloc(&dev, buf.size() * sizeof(float)));
-  m.allocs.push_back(dev);
+  // A re-upload (after fine_tune: same shapes) reuses the net's buffer once every kernel
+  // that may still read it has finished; a first upload allocates it.
+  if (m.net_buf.size() < m.nets.size()) m.net_buf.resize(m.nets.size(), {nullptr, 0});
+  float*& dev = m.net_buf[layer].first;
+  if (dev && m.net_buf[layer].second == buf.size()) {
+    PS_CUDA(cudaDeviceSynchronize());
+  } else {
+    PS_CUDA(cudaMalloc(&dev, buf.size() * sizeof(float)));
+    m.allocs.push_back(dev);
+    m.net_buf[layer].second = buf.size();
+  }
   PS_CUDA(cudaMemcpy(dev, buf.data(), buf.size() * sizeof(float), cudaMemcpyHostToDevice));
   d.mean = dev + o_mean;
   d.comp = dev + o_comp;
