@@ -1398,7 +1398,18 @@ void create_engine(const ps_engine_config& cfg, ps_engine_s& e) {
   for (auto& st : e.s_pred) PS_CUDA(cudaStreamCreateWithFlags(&st, cudaStreamNonBlocking));
   PS_CUDA(cudaEventCreateWithFlags(&e.ev_k1, cudaEventDisableTiming));
   for (auto& ev : e.ev_pred) PS_CUDA(cudaEventCreateWithFlags(&ev, cudaEventDisableTiming));
-  e.io = std::make_unique<IoChannel>(cfg.device, 2);
+  // Copies the channel keeps enqueued on the copy stream: with 1, "issued" = "started"
+  // (the reference's R2: prefetches that started before the next scheduling point commit,
+  // the rest are cancelled); with 2, a second copy is enqueued behind the running one and
+  // commits although it has not started — the layer then waits ~9 ms for two serial
+  // copies while the lane idles (profiles/timelines/r02_hybrid_k4_joined.json, layers
+  // 1/3/16/18). Depth 1: +2.3 % tok/s in 4 alternating pairs
+  // (profiles/r02_bench_io_depth_ab.jsonl). PS_IO_DEPTH=2 restores the old behaviour.
+  static const int io_depth = [] {
+    const char* v = std::getenv("PS_IO_DEPTH");
+    return v && v[0] == '2' ? 2 : 1;
+  }();
+  e.io = std::make_unique<IoChannel>(cfg.device, io_depth);
 
   // Expert parallelism: this rank owns experts e % G == rank of every layer.
   e.ep = cfg.ep;

@@ -1,6 +1,7 @@
 // The serial I/O channel of AsyncIO (simulator.cpp:181-227, rules R2/R7/R8) on real
 // hardware: one copy stream owned by one host thread, a FIFO of expert copies with
-// cancellable queued prefetches, at most `depth` copies in flight, and HBM slots whose
+// cancellable queued prefetches, at most `depth` copies enqueued on the copy stream
+// (1 in the engine: issued = started, as R2 needs), and HBM slots whose
 // reuse waits for the compute that last read them. Shared by the decode engine
 // (engine.cpp) and the stand-alone expert cache (cache.cpp).
 #pragma once
