@@ -138,8 +138,11 @@ class IoChannel {
       if (stop_) break;
       busy_ = true;
       // Throttle: at most depth_ copies in flight, so later queue entries stay
-      // cancellable until the channel is about to free up.
-      while (static_cast<int>(in_flight.size()) >= depth_) {
+      // cancellable until the channel is about to free up. An on-demand load is never
+      // cancelled, so it may always be enqueued behind one running copy (back-to-back
+      // loads keep the link busy); the limit applies to prefetches.
+      auto limit = [&] { return !queue_.empty() && queue_.front()->kind == kOnDemand ? std::max(depth_, 2) : depth_; };
+      while (static_cast<int>(in_flight.size()) >= limit()) {
         cudaEvent_t ev = in_flight.front();
         g.unlock();
         cudaError_t e = cudaEventSynchronize(ev);

@@ -16,10 +16,12 @@
 // fp32 throughout (the reference is fp64: logits within rel 1e-4, top-k bit-exact
 // against topk_indices on the kernel's own logits).
 #include <cmath>
+#include <cstdlib>
 #include <cstdio>
 #include <cstring>
 #include <fstream>
 #include <memory>
+#include <mutex>
 #include <random>
 #include <vector>
 
@@ -67,7 +69,8 @@ namespace {
 constexpr int kPcaWarps = 8;     // warps per CTA (two component rows each)
 constexpr int kPcaChunk = 512;   // H elements per CTA (grid.y splits H)
 constexpr int kPcaTok = 16;      // tokens per pass
-constexpr int kMlpTok = 16;      // tokens per MLP CTA
+constexpr int kMlpTokBig = 16;   // tokens per MLP CTA (batches > 16)
+constexpr int kMlpTokSmall = 4;  // tokens per MLP CTA (decode batches <= 16)
 constexpr int kMlpThreads = 512;
 
 // Stage 1 of pca_apply: part[s][t][p] = sum_{h in chunk s} comp[p][h] * (x[t][h] - mean[h]).
@@ -155,44 +158,48 @@ pca_partial_kernel(const float* __restrict__ comp, const float* __restrict__ mea
 
 __device__ __forceinline__ float gelu_erf(float v) { return 0.5f * v * (1.0f + erff(v * 0.70710678118654752f)); }
 
-// out[t][r] = act(W[r,:] . in[t,:] + b[r]) for all tokens of the CTA. A warp owns two rows;
-// lanes stride the columns so every activation read from shared memory feeds two FMAs, and
-// the 2 x kMlpTok partial sums are reduced with one transpose-reduce (lane L ends up owning
-// row r0 + L / kMlpTok, token L % kMlpTok and applies bias + activation itself).
+// out[t][r] = act(W[r,:] . in[t,:] + b[r]) for the TOK tokens of the CTA. A warp owns
+// R = 32 / TOK rows; lanes stride the columns so every activation read from shared memory
+// feeds R FMAs, and the R x TOK partial sums are reduced with one transpose-reduce (lane L
+// ends up owning row r0 + L / TOK, token L % TOK and applies bias + activation itself).
+// TOK = 16 (two rows per warp) for big batches; TOK = 4 (eight rows per warp, four CTAs
+// for a 16-token decode batch) halves the per-layer rounds and spreads a decode batch
+// over more SMs.
+template <int TOK>
 __device__ __forceinline__ void affine_tokens(const float* __restrict__ W, const float* __restrict__ bvec, int rows,
                                               int cols, const float* in, int in_stride, float* out, int out_stride,
                                               int nt, bool gelu) {
-  static_assert(2 * kMlpTok == 32, "transpose-reduce maps (2 rows x kMlpTok tokens) onto the 32 lanes");
+  constexpr int R = 32 / TOK;
+  static_assert(R * TOK == 32, "transpose-reduce maps (R rows x TOK tokens) onto the 32 lanes");
+  constexpr int kU = TOK >= 16 ? 4 : 2;  // weight loads in flight per lane and row
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31, nw = blockDim.x >> 5;
-  constexpr int kU = 4;  // weight loads in flight per lane and row
-  for (int r0 = 2 * warp; r0 < rows; r0 += 2 * nw) {
-    const bool two = r0 + 1 < rows;
-    float acc[2 * kMlpTok];
+  for (int r0 = R * warp; r0 < rows; r0 += R * nw) {
+    float acc[32];
 #pragma unroll
-    for (int i = 0; i < 2 * kMlpTok; ++i) acc[i] = 0.f;
+    for (int i = 0; i < 32; ++i) acc[i] = 0.f;
     for (int c0 = 0; c0 < cols; c0 += 32 * kU) {
-      float w0[kU], w1[kU];
+      float w[R][kU];
 #pragma unroll
       for (int u = 0; u < kU; ++u) {
         const int c = c0 + lane + 32 * u;
-        w0[u] = c < cols ? W[r0 * cols + c] : 0.f;
-        w1[u] = c < cols && two ? W[(r0 + 1) * cols + c] : 0.f;
+#pragma unroll
+        for (int ri = 0; ri < R; ++ri) w[ri][u] = c < cols && r0 + ri < rows ? W[(r0 + ri) * cols + c] : 0.f;
       }
 #pragma unroll
       for (int u = 0; u < kU; ++u) {
         const int c = c0 + lane + 32 * u;
         if (c < cols) {
 #pragma unroll
-          for (int t = 0; t < kMlpTok; ++t) {
+          for (int t = 0; t < TOK; ++t) {
             const float a = in[t * in_stride + c];
-            acc[t] += w0[u] * a;
-            acc[kMlpTok + t] += w1[u] * a;
+#pragma unroll
+            for (int ri = 0; ri < R; ++ri) acc[ri * TOK + t] += w[ri][u] * a;
           }
         }
       }
     }
     const float s = warp_transpose_sum(acc);
-    const int t = lane % kMlpTok, r = r0 + lane / kMlpTok;
+    const int t = lane % TOK, r = r0 + lane / TOK;
     if (t < nt && r < rows) {
       const float v = s + bvec[r];
       out[t * out_stride + r] = gelu ? gelu_erf(v) : v;
@@ -202,25 +209,25 @@ __device__ __forceinline__ void affine_tokens(const float* __restrict__ W, const
 
 // Feature concat [pca | onehot(prev top-k) | prev gate weights] (predictor.cpp:214-220),
 // GELU blocks, middle-group gated residual (229-240), logits (242-245), top-k on
-// logits (669-672), predicted histogram (experiment.cpp:104-112). kMlpTok tokens/CTA.
+// logits (669-672), predicted histogram (experiment.cpp:104-112). TOK tokens/CTA.
 // kStage: every MLP parameter is staged in shared memory first (one L2 round trip) and
 // addressed as smem + offset, so the layer loops issue LDS rather than generic loads.
-template <bool kStage>
+template <int TOK, bool kStage>
 __global__ void __launch_bounds__(kMlpThreads)
 mlp_kernel(const __grid_constant__ NetDev net, const float* __restrict__ part, int n_part,
            const int32_t* __restrict__ prev_ids, int k_prev, const float* __restrict__ prev_w, int B, int k,
            float* __restrict__ logits_out, int32_t* __restrict__ ids_out, int32_t* __restrict__ pred_counts) {
   extern __shared__ __align__(16) float smem[];
   const int P = net.P, E = net.E, D = net.in_dim, Wd = net.width;
-  const int t0 = blockIdx.x * kMlpTok, nt = min(kMlpTok, B - t0);
+  const int t0 = blockIdx.x * TOK, nt = min(TOK, B - t0);
   int maxh = Wd;
   for (int j = 1; j <= net.n_blocks; ++j) maxh = max(maxh, net.dims[j]);
   float* wsm = smem;                                       // [mlp_floats] staged parameters
-  float* feat = smem + (kStage ? (net.mlp_floats + 3) / 4 * 4 : 0);  // [kMlpTok][D]
-  float* h1 = feat + kMlpTok * D;                          // [kMlpTok][maxh]
-  float* h2 = h1 + kMlpTok * maxh;
-  float* h3 = h2 + kMlpTok * maxh;
-  float* lg = h3 + kMlpTok * maxh;                         // [kMlpTok][E]
+  float* feat = smem + (kStage ? (net.mlp_floats + 3) / 4 * 4 : 0);  // [TOK][D]
+  float* h1 = feat + TOK * D;                          // [TOK][maxh]
+  float* h2 = h1 + TOK * maxh;
+  float* h3 = h2 + TOK * maxh;
+  float* lg = h3 + TOK * maxh;                         // [TOK][E]
   const float* base = kStage ? wsm : net.w[0];
 
   if (kStage) {
@@ -234,7 +241,7 @@ mlp_kernel(const __grid_constant__ NetDev net, const float* __restrict__ part, i
   constexpr int kMaxParts = 16;
   const bool vecP = (P & 3) == 0;
   const int Pq = vecP ? P / 4 : P;
-  for (int i = threadIdx.x; i < kMlpTok * Pq; i += blockDim.x) {
+  for (int i = threadIdx.x; i < TOK * Pq; i += blockDim.x) {
     const int t = i / Pq, q = i % Pq;
     if (vecP) {
       float4 a = make_float4(0.f, 0.f, 0.f, 0.f);
@@ -258,7 +265,7 @@ mlp_kernel(const __grid_constant__ NetDev net, const float* __restrict__ part, i
     }
   }
   // onehot(prev top-k) | prev gate weights
-  for (int i = threadIdx.x; i < kMlpTok * 2 * E; i += blockDim.x) {
+  for (int i = threadIdx.x; i < TOK * 2 * E; i += blockDim.x) {
     const int t = i / (2 * E), j = i % (2 * E);
     float v = 0.f;
     if (t < nt) {
@@ -279,7 +286,7 @@ mlp_kernel(const __grid_constant__ NetDev net, const float* __restrict__ part, i
   float* bufs[2] = {h1, h2};
   for (int j = 0; j < net.n_blocks; ++j) {
     float* o = bufs[j & 1];
-    affine_tokens(base + net.o_w[j], base + net.o_b[j], net.dims[j + 1], net.dims[j], cur, cur_stride, o, maxh, nt,
+    affine_tokens<TOK>(base + net.o_w[j], base + net.o_b[j], net.dims[j + 1], net.dims[j], cur, cur_stride, o, maxh, nt,
                   true);
     __syncthreads();
     cur = o;
@@ -292,11 +299,11 @@ mlp_kernel(const __grid_constant__ NetDev net, const float* __restrict__ part, i
     float* u = nullptr;
     for (int j = 0; j < net.n_res; ++j) {
       u = ubuf[j & 1];
-      affine_tokens(base + net.o_rw[j], base + net.o_rb[j], Wd, Wd, uin, maxh, u, maxh, nt, true);
+      affine_tokens<TOK>(base + net.o_rw[j], base + net.o_rb[j], Wd, Wd, uin, maxh, u, maxh, nt, true);
       __syncthreads();
       uin = u;
     }
-    __shared__ float s_gate[kMlpTok];
+    __shared__ float s_gate[TOK];
     const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
     const float* gw = base + net.o_gate;
     for (int t = warp; t < nt; t += blockDim.x >> 5) {
@@ -313,7 +320,7 @@ mlp_kernel(const __grid_constant__ NetDev net, const float* __restrict__ part, i
     __syncthreads();
     cur = u;
   }
-  affine_tokens(base + net.o_ow, base + net.o_ob, E, Wd, cur, maxh, lg, E, nt, false);
+  affine_tokens<TOK>(base + net.o_ow, base + net.o_ob, E, Wd, cur, maxh, lg, E, nt, false);
   __syncthreads();
   if (logits_out)
     for (int i = threadIdx.x; i < nt * E; i += blockDim.x) logits_out[static_cast<size_t>(t0) * E + i] = lg[i];
@@ -584,24 +591,34 @@ ps_status ps_llapor_forward(ps_llapor m, int layer, const float* hidden, const i
     PS_LAUNCH_CHECK("pca_partial_kernel");
     int maxh = net.width;
     for (int j = 1; j <= net.n_blocks; ++j) maxh = std::max(maxh, net.dims[j]);
-    const size_t act = sizeof(float) * kMlpTok * (net.in_dim + 3 * maxh + net.E);
+    static const bool force_big = [] {  // PS_LLAPOR_TOK=16: the one-CTA-per-16-tokens kernel (A/B)
+      const char* v = std::getenv("PS_LLAPOR_TOK");
+      return v && v[0] == '1' && v[1] == '6';
+    }();
+    const bool small = B <= 16 && !force_big;
+    const int tok = small ? kMlpTokSmall : kMlpTokBig;
+    const size_t act = sizeof(float) * tok * (net.in_dim + 3 * maxh + net.E);
     const size_t staged = act + sizeof(float) * ((net.mlp_floats + 3) / 4 * 4);
     const bool stage_w = staged <= 200 * 1024;
     const size_t smem = stage_w ? staged : act;
     require(smem <= 227 * 1024, "ps_llapor_forward: predictor too wide for one CTA's shared memory");
-    static size_t smem_set[2] = {0, 0};
-    const void* fn = stage_w ? reinterpret_cast<const void*>(mlp_kernel<true>) : reinterpret_cast<const void*>(mlp_kernel<false>);
-    if (smem > smem_set[stage_w]) {
-      PS_CUDA(cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(smem)));
-      smem_set[stage_w] = smem;
+    using Kfn = void (*)(NetDev, const float*, int, const int32_t*, int, const float*, int, int, float*, int32_t*,
+                         int32_t*);
+    const Kfn fn = small ? (stage_w ? mlp_kernel<kMlpTokSmall, true> : mlp_kernel<kMlpTokSmall, false>)
+                         : (stage_w ? mlp_kernel<kMlpTokBig, true> : mlp_kernel<kMlpTokBig, false>);
+    {  // opt in to the dynamic shared memory this net needs (per kernel variant, once)
+      static std::mutex mu;
+      static size_t smem_set[2][2] = {{0, 0}, {0, 0}};
+      std::lock_guard<std::mutex> g(mu);
+      if (smem > smem_set[small][stage_w]) {
+        PS_CUDA(cudaFuncSetAttribute(reinterpret_cast<const void*>(fn), cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                     static_cast<int>(smem)));
+        smem_set[small][stage_w] = smem;
+      }
     }
-    const int grid_m = (B + kMlpTok - 1) / kMlpTok;
-    if (stage_w)
-      mlp_kernel<true><<<grid_m, kMlpThreads, smem, s>>>(net, part, n_part, prev_ids, k_prev, prev_weights, B, k, logits,
-                                                         ids, pred_counts);
-    else
-      mlp_kernel<false><<<grid_m, kMlpThreads, smem, s>>>(net, part, n_part, prev_ids, k_prev, prev_weights, B, k,
-                                                          logits, ids, pred_counts);
+    const int grid_m = (B + tok - 1) / tok;
+    fn<<<grid_m, kMlpThreads, smem, s>>>(net, part, n_part, prev_ids, k_prev, prev_weights, B, k, logits, ids,
+                                         pred_counts);
     PS_LAUNCH_CHECK("mlp_kernel");
   });
 }
