@@ -354,9 +354,10 @@ ps_status ps_expert_ffn(const ps_expert_group* group, const int32_t* counts_host
 ps_status ps_expert_ffn_prefill(const ps_expert_group* group, const int32_t* counts_host,
                                 const int32_t* offsets_host, const uint16_t* x_perm, int total_rows,
                                 int H, int F, uint16_t* h_perm, float* y_perm, void* stream);
-/* Prefill kernel choice (process-wide): 0 = single-CTA M=128 tiles, 1 = CTA pairs
- * (cta_group::2, M=256), 2 = auto (default: pairs unless their extra padding of the
- * experts' last M tiles exceeds 8 % of the routed rows). */
+/* Prefill kernel choice (process-wide): 0 = single-CTA M=128 token tiles, 1 = CTA pairs
+ * (cta_group::2, M=256 token tiles), 3 = token-N CTA pairs (weights as M=256, an
+ * expert's tokens as N <= 256 in steps of 16; gate_up and down in one launch),
+ * 2 = auto (default) = 3. */
 ps_status ps_set_prefill_kernel(int mode);
 /* Split-K factor ps_expert_ffn expects for the down projection at this shape. */
 int ps_ffn_down_splits(int H, int F);

@@ -23,6 +23,11 @@
 //                 tile i+1).
 // Tiles are ordered m-fastest within (expert, n-tile) so CTAs working on the same weight
 // tile run concurrently and the B tile is fetched from HBM once, then served by L2.
+//
+// Three kernels (ps_set_prefill_kernel): the single-CTA M=128 kernel (0), the CTA-pair
+// M=256 kernel (1), and the default token-N CTA-pair kernel (2 = auto, 3): weights on
+// the M side, an expert's tokens on the N side (no padding of ragged experts beyond 16
+// rows), gate_up and down in one launch with per-expert release/acquire counters.
 #include <cuda.h>
 
 #include <algorithm>
@@ -360,6 +365,14 @@ __device__ __forceinline__ void tma_load_2d_pair(void* dst, const CUtensorMap* m
       "l"(map), "r"(c0), "r"(c1), "r"(leader_bar)
       : "memory");
 }
+__device__ __forceinline__ void tma_load_2d_pair_s(uint32_t dst, const CUtensorMap* map, uint32_t leader_bar, int c0,
+                                                   int c1) {
+  asm volatile(
+      "cp.async.bulk.tensor.2d.cta_group::2.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1, {%2, %3}], "
+      "[%4];" ::"r"(dst),
+      "l"(map), "r"(c0), "r"(c1), "r"(leader_bar)
+      : "memory");
+}
 __device__ __forceinline__ void umma_f16_pair(uint32_t tmem_d, uint64_t adesc, uint64_t bdesc, uint32_t accumulate) {
   asm volatile(
       "{\n"
@@ -561,6 +574,312 @@ ffn_prefill_pair_kernel(const __grid_constant__ PrefillParams p) {
   }
 }
 
+// ------------------------------------------------------------------ token-N CTA-pair variant
+// The weights are the M side and the tokens the N side of the MMA (D^T = W . X^T): a
+// pair tile is 256 weight rows x N tokens with N = the expert's remaining rows rounded
+// up to 16 (<= 256). The M-side kernels above pad every expert's last tile to 128 or
+// 256 token rows; at DeepSeek-V2-Lite prefill (m_e ~ 192) that is 25 % of the tensor
+// time, while here an expert of 192 rows is one N = 192 tile with no padding.
+//   gate_up: CTA r's 128 A rows = gate rows [f0 + 64r, +64) then the same up rows (two
+//            {64 x 64} TMA boxes), so TMEM lanes 0-63 hold gate and 64-127 up for the
+//            same 64 features; a gate warp and the up warp of the same features swap
+//            half of every 32-token chunk through shared memory (tcgen05.ld reaches only
+//            a warp's own 32-lane quarter) and each writes h = SiLU(g) * u for 16 tokens
+//            (64 B of one token row per store).
+//   down:    CTA r's 128 A rows = W_down rows [h0 + 128r, +128) (one {64 x 128} box);
+//            y_perm[token][h] fp32, 128 B of one token row per warp store.
+//   B:       CTA r stages tokens [N/2 r, +N/2) of the tile (cta_group::2 splits N), from
+//            a tensor map whose box is N/2 rows (the shared 128-row map or the entry's
+//            own map for its last, shorter tile).
+// ONE launch runs both phases: tiles [0, T0) are gate_up, [T0, T0 + T1) down, and every
+// CTA pair walks its tiles in index order, so the gate_up tail overlaps the first down
+// tiles and there is no second launch. A down tile of entry e needs all of e's h rows:
+// every epilogue warp of a gate_up tile of e adds 1 to done[e] (release) after its h
+// stores; the producer acquires done[e] >= target[e] before it TMA-loads h (the counters
+// only grow: targets are host-side running sums per map-ring slot, nothing is reset). A
+// pair waits only on gate_up tiles, which never wait, and all pairs are co-resident (grid
+// <= the device's max active 2-CTA clusters), so the wait cannot deadlock.
+constexpr int kTnStages = 6;
+constexpr int kTnABytes = 128 * kBK * 2;                 // 16 KiB of weight rows
+constexpr int kTnBMaxBytes = 128 * kBK * 2;              // <= 128 token rows per CTA
+constexpr int kTnStageBytes = kTnABytes + kTnBMaxBytes;  // 32 KiB
+constexpr int kTnXchgBytes = 2 * 2 * 2 * 16 * 32 * 4;    // gate <-> up hand-off: 2 bufs x 2 pairs x 2 senders x 16 x 32
+constexpr int kTnSmemBytes = kTnStages * kTnStageBytes + kTnXchgBytes + 1024 + 256;
+constexpr int kTnMaxN = 256;
+constexpr uint32_t kTnSignalsPerTile = 2 * 4;            // epilogue warps of both CTAs
+
+struct TnPhase {
+  int K;                            // H (gate_up) or F (down)
+  int n_tiles_n;                    // weight-row tiles per expert (F/128 gate_up, H/256 down)
+  int tile_start[kMaxExperts + 1];  // prefix of this phase's tiles per entry
+  const CUtensorMap* tok_full;      // token operand (x_perm or h_perm), box {64, 128}
+  const CUtensorMap* tok_last;      // [n_experts]: box {64, N_last / 2} of the entry's last tile
+  const CUtensorMap* w_maps;        // [n_experts]: [Wg; Wu] box {64, 64} or Wd box {64, 128}
+  void* out;                        // h_perm (bf16) or y_perm (f32)
+  int out_ld;
+};
+
+struct TnParams {
+  int n_experts;
+  int F, H;
+  int t_tiles[kMaxExperts];         // token tiles per entry (ceil(m_e / 256))
+  int row0[kMaxExperts];
+  int rows[kMaxExperts];
+  TnPhase ph[2];                    // 0 = gate_up, 1 = down
+  unsigned* done;                   // [n_experts] gate_up signals (this map-ring slot's counters)
+  unsigned target[kMaxExperts];     // done[e] value once all of e's gate_up tiles are stored
+};
+
+struct TnTile {
+  int phase, entry, n_tile, tok0, n;  // n = MMA N (tokens, multiple of 16)
+  bool last;
+};
+
+__device__ __forceinline__ TnTile tn_tile(const TnParams& p, int t) {
+  TnTile c;
+  const int t0 = p.ph[0].tile_start[p.n_experts];
+  c.phase = t < t0 ? 0 : 1;
+  if (c.phase) t -= t0;
+  const int* ts = p.ph[c.phase].tile_start;
+  int lo = 0, hi = p.n_experts - 1;
+  while (lo < hi) {
+    const int mid = (lo + hi + 1) >> 1;
+    if (ts[mid] <= t) lo = mid;
+    else hi = mid - 1;
+  }
+  const int local = t - ts[lo], tt = p.t_tiles[lo];
+  const int t_tile = local % tt;  // token tiles fastest: concurrent tiles share the weight rows
+  c.entry = lo;
+  c.n_tile = local / tt;
+  c.tok0 = t_tile * kTnMaxN;
+  const int rem = p.rows[lo] - c.tok0;
+  c.n = rem >= kTnMaxN ? kTnMaxN : (rem + 15) & ~15;
+  c.last = t_tile == tt - 1;
+  return c;
+}
+
+__device__ __forceinline__ void named_bar_sync(int id, int n) {
+  asm volatile("bar.sync %0, %1;" ::"r"(id), "r"(n) : "memory");
+}
+
+
+__global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads, 1)
+ffn_prefill_tn_kernel(const __grid_constant__ TnParams p) {
+  extern __shared__ __align__(1024) uint8_t smem_raw[];
+  uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
+  float* xchg = reinterpret_cast<float*>(smem + kTnStages * kTnStageBytes);  // [2][2][2][16][32]
+  uint64_t* full_bar = reinterpret_cast<uint64_t*>(smem + kTnStages * kTnStageBytes + kTnXchgBytes);
+  uint64_t* empty_bar = full_bar + kTnStages;
+  uint64_t* tfull_bar = empty_bar + kTnStages;
+  uint64_t* tempty_bar = tfull_bar + 2;
+  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(tempty_bar + 2);
+
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const uint32_t rank = cluster_rank();
+  const bool leader = rank == 0;
+  const int pair = blockIdx.x >> 1, n_pairs = gridDim.x >> 1;
+  const int n_tiles = p.ph[0].tile_start[p.n_experts] + p.ph[1].tile_start[p.n_experts];
+
+  if (warp == 0 && lane == 0) {
+    for (int s = 0; s < kTnStages; ++s) {
+      mbar_init(&full_bar[s], 1);
+      mbar_init(&empty_bar[s], 1);
+    }
+    for (int s = 0; s < 2; ++s) {
+      mbar_init(&tfull_bar[s], 1);
+      mbar_init(&tempty_bar[s], 2 * 128);
+    }
+    asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+  }
+  if (warp == 1) {
+    asm volatile("tcgen05.alloc.cta_group::2.sync.aligned.shared::cta.b32 [%0], 512;" ::"r"(smem_u32(tmem_slot)));
+    asm volatile("tcgen05.relinquish_alloc_permit.cta_group::2.sync.aligned;");
+  }
+  tc_fence_before();
+  __syncthreads();
+  cluster_sync_all();
+  tc_fence_after();
+  const uint32_t tmem_base = *tmem_slot;
+
+  if (warp == 0) {
+    for (int ph = 0; ph < 2; ++ph)
+      for (int i = lane; i <= 2 * p.n_experts; i += 32) {
+        const CUtensorMap* m = i == 0 ? p.ph[ph].tok_full
+                                      : (i <= p.n_experts ? p.ph[ph].tok_last + (i - 1)
+                                                          : p.ph[ph].w_maps + (i - 1 - p.n_experts));
+        if (m) asm volatile("fence.proxy.tensormap::generic.acquire.gpu [%0], 128;" ::"l"(m) : "memory");
+      }
+    __syncwarp();
+    if (lane == 0) {  // ---------------------------------------------- TMA producer (both CTAs)
+      int stage = 0;
+      uint32_t phase = 0;
+      for (int t = pair; t < n_tiles; t += n_pairs) {
+        const TnTile tc = tn_tile(p, t);
+        const TnPhase& ph = p.ph[tc.phase];
+        const CUtensorMap* wmap = ph.w_maps + tc.entry;
+        const CUtensorMap* tmap = (tc.last && tc.n < kTnMaxN) ? ph.tok_last + tc.entry : ph.tok_full;
+        const int half = tc.n >> 1;
+        const int trow = p.row0[tc.entry] + tc.tok0 + static_cast<int>(rank) * half;
+        const uint32_t bytes = 2u * (kTnABytes + static_cast<uint32_t>(half) * kBK * 2);
+        const int k_blocks = (ph.K + kBK - 1) / kBK;
+        if (tc.phase == 1) {  // h of this entry complete (acquire), then visible to the async proxy
+          const unsigned* d = p.done + tc.entry;
+          const unsigned want = p.target[tc.entry];
+          unsigned v;
+          while (true) {
+            asm volatile("ld.acquire.gpu.global.u32 %0, [%1];" : "=r"(v) : "l"(d) : "memory");
+            if (static_cast<int>(v - want) >= 0) break;
+            __nanosleep(64);
+          }
+          asm volatile("fence.proxy.async.global;" ::: "memory");
+        }
+        for (int kb = 0; kb < k_blocks; ++kb) {
+          mbar_wait(&empty_bar[stage], phase ^ 1);
+          const uint32_t sa = smem_u32(smem + stage * kTnStageBytes);
+          const uint32_t lbar = mapa_shared(smem_u32(&full_bar[stage]), 0);
+          if (leader) mbar_expect_tx(&full_bar[stage], bytes);
+          if (tc.phase == 0) {
+            const int f = tc.n_tile * 128 + static_cast<int>(rank) * 64;
+            tma_load_2d_pair_s(sa, wmap, lbar, kb * kBK, f);                          // gate rows
+            tma_load_2d_pair_s(sa + kTnABytes / 2, wmap, lbar, kb * kBK, p.F + f);    // up rows
+          } else {
+            tma_load_2d_pair_s(sa, wmap, lbar, kb * kBK, tc.n_tile * 256 + static_cast<int>(rank) * 128);
+          }
+          tma_load_2d_pair_s(sa + kTnABytes, tmap, lbar, kb * kBK, trow);
+          if (++stage == kTnStages) {
+            stage = 0;
+            phase ^= 1;
+          }
+        }
+      }
+    }
+  } else if (warp == 1) {
+    if (leader && lane == 0) {  // ------------------------------------ MMA issuer (leader only)
+      int stage = 0;
+      uint32_t phase = 0;
+      int as = 0;
+      uint32_t aphase = 0;
+      for (int t = pair; t < n_tiles; t += n_pairs) {
+        const TnTile tc = tn_tile(p, t);
+        const int k_blocks = (p.ph[tc.phase].K + kBK - 1) / kBK;
+        const uint32_t idesc = (1u << 4) | (1u << 7) | (1u << 10) | (static_cast<uint32_t>(tc.n >> 3) << 17) |
+                               (static_cast<uint32_t>(256 >> 4) << 24);
+        mbar_wait(&tempty_bar[as], aphase ^ 1);
+        tc_fence_after();
+        const uint32_t d = tmem_base + static_cast<uint32_t>(as * kTnMaxN);
+        for (int kb = 0; kb < k_blocks; ++kb) {
+          mbar_wait(&full_bar[stage], phase);
+          tc_fence_after();
+          const uint32_t sa = smem_u32(smem + stage * kTnStageBytes);
+          const uint32_t sb = sa + kTnABytes;
+#pragma unroll
+          for (int kk = 0; kk < kBK / 16; ++kk) {
+            const uint32_t acc = (kb | kk) != 0 ? 1u : 0u;
+            asm volatile(
+                "{\n"
+                ".reg .pred p;\n"
+                "setp.ne.b32 p, %4, 0;\n"
+                "tcgen05.mma.cta_group::2.kind::f16 [%0], %1, %2, %3, p;\n"
+                "}\n" ::"r"(d),
+                "l"(make_desc(sa + kk * 32)), "l"(make_desc(sb + kk * 32)), "r"(idesc), "r"(acc));
+          }
+          umma_commit_pair(&empty_bar[stage]);
+          if (++stage == kTnStages) {
+            stage = 0;
+            phase ^= 1;
+          }
+        }
+        umma_commit_pair(&tfull_bar[as]);
+        as ^= 1;
+        if (as == 0) aphase ^= 1;
+      }
+    }
+  } else {  // ------------------------------------------------------- epilogue (4 warps, both CTAs)
+    const int quarter = warp & 3;
+    const uint32_t tempty_leader[2] = {mapa_shared(smem_u32(&tempty_bar[0]), 0), mapa_shared(smem_u32(&tempty_bar[1]), 0)};
+    int as = 0;
+    uint32_t aphase = 0;
+    int buf = 0;  // hand-off buffer: one barrier per chunk orders its reuse two chunks later
+    const uint32_t xchg_s = smem_u32(xchg);
+    for (int t = pair; t < n_tiles; t += n_pairs) {
+      const TnTile tc = tn_tile(p, t);
+      const TnPhase& ph = p.ph[tc.phase];
+      mbar_wait(&tfull_bar[as], aphase);
+      tc_fence_after();
+      const uint32_t tbase = tmem_base + static_cast<uint32_t>(as * kTnMaxN) + (static_cast<uint32_t>(quarter * 32) << 16);
+      const int m_left = p.rows[tc.entry] - tc.tok0;  // valid token columns of this tile
+      const size_t row_base = static_cast<size_t>(p.row0[tc.entry] + tc.tok0);
+      if (tc.phase == 0) {
+        // quarters 0/1 hold gate, 2/3 up of features [32 (q & 1), +32) of this CTA's 64.
+        // Per 32-token chunk the two warps of a feature group swap halves through shared
+        // memory (gate sends tokens 16-31, up sends 0-15) and each computes 16 tokens of h.
+        const bool is_gate = quarter < 2;
+        const int f = tc.n_tile * 128 + static_cast<int>(rank) * 64 + (quarter & 1) * 32 + lane;
+        uint16_t* out = static_cast<uint16_t*>(ph.out) + row_base * ph.out_ld + f;
+        const int jb = is_gate ? 0 : 16;  // this warp's tokens in the chunk
+#pragma unroll 1
+        for (int c = 0; c < tc.n; c += 32, buf ^= 1) {  // buf alternates across tiles too
+          uint32_t v[32];
+          tmem_ld32(tbase + c, v);
+          tmem_ld_wait();
+          // xchg[buf][pair q&1][sender][16 tokens][32 lanes] (shared-window addresses: the
+          // aligned smem pointer has lost its address space, so generic accesses would be used)
+          const uint32_t xb = xchg_s + static_cast<uint32_t>(((buf * 2 + (quarter & 1)) * 2) * 16 * 32 * 4);
+          const uint32_t mine = xb + (is_gate ? 0u : 16u * 32u * 4u) + lane * 4u;
+          const uint32_t theirs = xb + (is_gate ? 16u * 32u * 4u : 0u) + lane * 4u;
+#pragma unroll
+          for (int j = 0; j < 16; ++j)
+            asm volatile("st.shared.b32 [%0], %1;" ::"r"(mine + j * 128u), "r"(is_gate ? v[16 + j] : v[j]) : "memory");
+          named_bar_sync(1, 128);
+          const int nj = min(16, m_left - c - jb);
+#pragma unroll
+          for (int j = 0; j < 16; ++j) {
+            uint32_t ob;
+            asm volatile("ld.shared.b32 %0, [%1];" : "=r"(ob) : "r"(theirs + j * 128u) : "memory");
+            const float o = __uint_as_float(ob);
+            const float own = __uint_as_float(is_gate ? v[j] : v[16 + j]);
+            const float g = is_gate ? own : o;
+            const float u = is_gate ? o : own;
+            // fast-math SiLU (ex2.approx + rcp.approx, ~2 ulp of fp32 before the bf16 rounding):
+            // the IEEE expf / division slow paths made this epilogue longer than a tile's MMAs
+            const float h = __fdividef(g, 1.0f + __expf(-g)) * u;
+            if (j < nj) out[static_cast<size_t>(c + jb + j) * ph.out_ld] = f32_to_bf16_rne(h);
+          }
+        }
+        // release this warp's h rows to the down tiles of the entry (TMA readers)
+        asm volatile("fence.proxy.async.global;" ::: "memory");
+        __syncwarp();
+        if (lane == 0)
+          asm volatile("red.release.gpu.global.add.u32 [%0], 1;" ::"l"(p.done + tc.entry) : "memory");
+      } else {
+        const int hrow = tc.n_tile * 256 + static_cast<int>(rank) * 128 + quarter * 32 + lane;
+        float* out = static_cast<float*>(ph.out) + row_base * ph.out_ld + hrow;
+#pragma unroll 1
+        for (int c = 0; c < tc.n; c += 32) {
+          uint32_t v[32];
+          tmem_ld32(tbase + c, v);
+          tmem_ld_wait();
+          const int nj = min(32, m_left - c);
+#pragma unroll
+          for (int j = 0; j < 32; ++j)
+            if (j < nj) out[static_cast<size_t>(c + j) * ph.out_ld] = __uint_as_float(v[j]);
+        }
+      }
+      tc_fence_before();
+      mbar_arrive_cluster(tempty_leader[as]);
+      as ^= 1;
+      if (as == 0) aphase ^= 1;
+    }
+  }
+  tc_fence_before();
+  __syncthreads();
+  cluster_sync_all();
+  if (warp == 1) {
+    tc_fence_after();
+    asm volatile("tcgen05.dealloc.cta_group::2.sync.aligned.b32 %0, 512;" ::"r"(tmem_base));
+  }
+}
+
 // ------------------------------------------------------------------ host helpers
 using EncodeFn = CUresult (*)(CUtensorMap*, CUtensorMapDataType, cuuint32_t, void*, const cuuint64_t*,
                               const cuuint64_t*, const cuuint32_t*, const cuuint32_t*, CUtensorMapInterleave,
@@ -600,7 +919,7 @@ CUtensorMap make_map(const void* base, uint64_t rows, uint64_t cols, uint32_t bo
 // copies are still in flight).
 struct MapRing {
   static constexpr int kSlots = 64;
-  static constexpr int kPerSlot = 2 * kMaxExperts + 2;  // [a_x, a_h, gate_up maps, down maps]
+  static constexpr int kPerSlot = 4 * kMaxExperts + 2;  // [a_x, a_h, gate_up maps, down maps, (token-N: x_last, h_last)]
   CUtensorMap* dev = nullptr;
   CUtensorMap* host = nullptr;
   cudaEvent_t ev[kSlots] = {};
@@ -634,12 +953,40 @@ void launch_pair(PrefillParams& p, cudaStream_t s) {
   PS_LAUNCH_CHECK("ffn_prefill_pair_kernel");
 }
 
-// Kernel choice: 0 = single-CTA, 1 = CTA pairs, 2 = auto (pairs unless padding costs
-// more than they gain). Initial value from PS_PREFILL_PAIR, else auto.
+void launch_tn(TnParams& p, cudaStream_t s) {
+  static int max_pairs = 0;
+  if (!max_pairs) {
+    PS_CUDA(cudaFuncSetAttribute(ffn_prefill_tn_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, kTnSmemBytes));
+    // every pair must be co-resident (a down tile may wait on any pair's gate_up tile)
+    cudaLaunchConfig_t cfg{};
+    cfg.gridDim = dim3(2 * (kNumSMs / 2));
+    cfg.blockDim = dim3(kThreads);
+    cfg.dynamicSmemBytes = kTnSmemBytes;
+    cudaLaunchAttribute attr[1];
+    attr[0].id = cudaLaunchAttributeClusterDimension;
+    attr[0].val.clusterDim.x = 2;
+    attr[0].val.clusterDim.y = 1;
+    attr[0].val.clusterDim.z = 1;
+    cfg.attrs = attr;
+    cfg.numAttrs = 1;
+    int clusters = 0;
+    PS_CUDA(cudaOccupancyMaxActiveClusters(&clusters, ffn_prefill_tn_kernel, &cfg));
+    if (clusters < 1) fail(PS_ECUDA, "ffn_prefill_tn_kernel: no 2-CTA cluster fits on this device");
+    max_pairs = std::min(clusters, kNumSMs / 2);
+  }
+  const int tiles = p.ph[0].tile_start[p.n_experts] + p.ph[1].tile_start[p.n_experts];
+  if (tiles == 0) return;
+  const int grid = 2 * std::min(tiles, max_pairs);
+  ffn_prefill_tn_kernel<<<grid, kThreads, kTnSmemBytes, s>>>(p);
+  PS_LAUNCH_CHECK("ffn_prefill_tn_kernel");
+}
+
+// Kernel choice: 0 = single-CTA, 1 = CTA pairs, 2 = auto, 3 = token-N CTA pairs.
+// Initial value from PS_PREFILL_PAIR, else auto.
 std::atomic<int>& prefill_mode() {
   static std::atomic<int> mode{[] {
     const char* v = std::getenv("PS_PREFILL_PAIR");
-    return v && (v[0] == '0' || v[0] == '1') ? v[0] - '0' : 2;
+    return v && v[0] >= '0' && v[0] <= '3' ? v[0] - '0' : 2;
   }()};
   return mode;
 }
@@ -682,18 +1029,80 @@ extern "C" ps_status ps_expert_ffn_prefill(const ps_expert_group* group, const i
     // instead of 127, yet with ~6 % extra padding (Mixtral, 4096 tokens routed at random)
     // pairs are still 1.03x faster end to end (scripts/prefill_micro.py). Pairs unless
     // their extra padding exceeds 8 % of the routed rows.
+    // auto (2) = the token-N kernel: no M padding, one launch for both phases; it matched
+    // or beat the M-side kernels at every expert shape measured (profiles/r02_prefill_tn.md)
     const int mode = prefill_mode().load();
-    bool pair = mode != 0;
-    if (mode == 2) {
-      int64_t rows = 0, pad1 = 0, pad2 = 0;
-      for (int i = 0; i < group->n; ++i) {
-        const int64_t m = counts_host[group->experts[i]];
-        rows += m;
-        pad1 += (m + kBM - 1) / kBM * kBM - m;
-        pad2 += (m + 2 * kBM - 1) / (2 * kBM) * (2 * kBM) - m;
+    if (mode == 3 || mode == 2) {
+      static unsigned* done_dev = nullptr;  // [MapRing::kSlots][kMaxExperts] gate_up signals
+      static std::vector<unsigned> done_host(MapRing::kSlots * kMaxExperts, 0u);  // their running targets
+      if (!done_dev) {
+        PS_CUDA(cudaMalloc(&done_dev, sizeof(unsigned) * MapRing::kSlots * kMaxExperts));
+        PS_CUDA(cudaMemset(done_dev, 0, sizeof(unsigned) * MapRing::kSlots * kMaxExperts));
       }
-      if (pad2 - pad1 > rows * 8 / 100) pair = false;
+      TnParams tp{};
+      tp.F = F;
+      tp.H = H;
+      tp.ph[0].K = H;
+      tp.ph[1].K = F;
+      tp.ph[0].n_tiles_n = F / 128;
+      tp.ph[1].n_tiles_n = H / 256;
+      const int G = group->n;
+      CUtensorMap* wgu = maps_host + 2;
+      CUtensorMap* wdn = maps_host + 2 + G;
+      CUtensorMap* xl = maps_host + 2 + 2 * G;
+      CUtensorMap* hl = maps_host + 2 + 3 * G;
+      unsigned* shadow = done_host.data() + slot * kMaxExperts;
+      int n = 0;
+      for (int i = 0; i < G; ++i) {
+        const int e = group->experts[i];
+        const int m = counts_host[e];
+        if (m == 0) continue;
+        const uint16_t* slab = group->slabs[i];
+        wgu[n] = make_map(slab, 2ull * F, H, 64);
+        wdn[n] = make_map(slab + 2ull * F * H, static_cast<uint64_t>(H), F, 128);
+        const int tt = (m + kTnMaxN - 1) / kTnMaxN;
+        const int rem = m - (tt - 1) * kTnMaxN;
+        const uint32_t half = static_cast<uint32_t>(((rem + 15) & ~15) / 2);
+        xl[n] = make_map(x_perm, static_cast<uint64_t>(total_rows), H, half);
+        hl[n] = make_map(h_perm, static_cast<uint64_t>(total_rows), F, half);
+        tp.t_tiles[n] = tt;
+        tp.row0[n] = offsets_host[e];
+        tp.rows[n] = m;
+        for (TnPhase& ph : tp.ph) ph.tile_start[n + 1] = ph.tile_start[n] + tt * ph.n_tiles_n;
+        shadow[n] += kTnSignalsPerTile * static_cast<unsigned>(tt * tp.ph[0].n_tiles_n);
+        tp.target[n] = shadow[n];
+        ++n;
+      }
+      if (n == 0) return;
+      tp.n_experts = n;
+      tp.done = done_dev + slot * kMaxExperts;
+      maps_host[0] = make_map(x_perm, static_cast<uint64_t>(total_rows), H, 128);
+      maps_host[1] = make_map(h_perm, static_cast<uint64_t>(total_rows), F, 128);
+      PS_CUDA(cudaMemcpyAsync(maps_dev, maps_host, sizeof(CUtensorMap) * (2 + 4 * G), cudaMemcpyHostToDevice, s));
+      tp.ph[0].tok_full = maps_dev;
+      tp.ph[1].tok_full = maps_dev + 1;
+      tp.ph[0].w_maps = maps_dev + 2;
+      tp.ph[1].w_maps = maps_dev + 2 + G;
+      tp.ph[0].tok_last = maps_dev + 2 + 2 * G;
+      tp.ph[1].tok_last = maps_dev + 2 + 3 * G;
+      tp.ph[0].out = h_perm;
+      tp.ph[0].out_ld = F;
+      tp.ph[1].out = y_perm;
+      tp.ph[1].out_ld = H;
+      const char* merge = std::getenv("PS_TN_MERGE");  // A/B knob: 0 runs the phases as two launches
+      if (merge && merge[0] == '0') {
+        TnParams second = tp;
+        for (int i = 0; i <= n; ++i) tp.ph[1].tile_start[i] = 0;
+        for (int i = 0; i <= n; ++i) second.ph[0].tile_start[i] = 0;
+        launch_tn(tp, s);
+        launch_tn(second, s);
+      } else {
+        launch_tn(tp, s);
+      }
+      PS_CUDA(cudaEventRecord(ring.ev[slot], s));
+      return;
     }
+    const bool pair = mode == 1;
     PrefillParams gu{}, dn{};
     gu.mode = kSwiGLU;
     dn.mode = kStoreF32;
@@ -746,7 +1155,8 @@ extern "C" ps_status ps_expert_ffn_prefill(const ps_expert_group* group, const i
 
 extern "C" ps_status ps_set_prefill_kernel(int mode) {
   return guarded([&] {
-    require(mode >= 0 && mode <= 2, "ps_set_prefill_kernel: mode 0 (single CTA), 1 (CTA pairs) or 2 (auto)");
+    require(mode >= 0 && mode <= 3,
+            "ps_set_prefill_kernel: mode 0 (single CTA), 1 (CTA pairs), 2 (auto) or 3 (token-N CTA pairs)");
     prefill_mode().store(mode);
   });
 }

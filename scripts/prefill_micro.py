@@ -26,8 +26,11 @@ def main():
     ap.add_argument("--k", type=int, default=2)
     ap.add_argument("--T", type=int, default=4096)
     ap.add_argument("--iters", type=int, default=10)
+    ap.add_argument("--ab-env", default="", help="NAME=v1,v2,...: alternate an env knob between timed runs")
+    ap.add_argument("--kernel", type=int, default=2, help="ps_set_prefill_kernel mode (0 single, 1 pair, 2 auto, 3 token-N pair)")
     args = ap.parse_args()
     lib = ps.load()
+    ps.check(lib.ps_set_prefill_kernel(args.kernel))
     H, F, E, k, T = args.H, args.F, args.E, args.k, args.T
     s = torch.cuda.current_stream()
     sp = C.c_void_p(s.cuda_stream)
@@ -63,6 +66,31 @@ def main():
     for _ in range(3):
         run()
     torch.cuda.synchronize()
+    if args.ab_env:
+        import os
+        name, vals = args.ab_env.split("=")
+        res = {v: [] for v in vals.split(",")}
+        for rep in range(args.iters):
+            for v in res:  # the host runs ahead of the GPU as in the plain loop (map encoding hidden)
+                if name == "kernel":
+                    ps.check(lib.ps_set_prefill_kernel(int(v)))
+                else:
+                    os.environ[name] = v
+                run()
+                run()
+                a, b = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+                a.record(s)
+                for _ in range(5):
+                    run()
+                b.record(s)
+                b.synchronize()
+                res[v].append(a.elapsed_time(b) / 5)
+        flops = 2.0 * rows * 3 * H * F
+        for v, t in res.items():
+            ms = float(np.median(t))
+            print(json.dumps({"H": H, "F": F, "E": E, "k": k, "T": T, name: v, "ms": ms, "tflops": flops / ms / 1e9,
+                              "kernel": args.kernel}))
+        return
     ts = []
     for _ in range(args.iters):
         a, b = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
@@ -77,7 +105,7 @@ def main():
     peak = json.loads(peaks.read_text())["bf16_tflops"] if peaks.exists() else 1590.0
     print(json.dumps({"H": H, "F": F, "E": E, "k": k, "T": T, "rows": rows, "ms": ms,
                       "tflops": flops / ms / 1e9, "frac_bf16_peak": flops / ms / 1e9 / peak,
-                      "m_per_expert": float(counts.mean())}))
+                      "m_per_expert": float(counts.mean()), "kernel": args.kernel}))
 
 
 if __name__ == "__main__":

@@ -29,12 +29,12 @@ def run(preset, L, E, H, F, B, budget, **kw):
 def main():
     import argparse
     ap = argparse.ArgumentParser()
-    ap.add_argument("--only", default="all", choices=["all", "prefill_single", "prefill_pair"],
+    ap.add_argument("--only", default="all", choices=["all", "prefill_single", "prefill_pair", "prefill_tn"],
                     help="prefill_*: only that tcgen05 kernel (to attribute sanitizer reports)")
     args = ap.parse_args()
     if args.only != "all":
         lib = ps.load()
-        ps.check(lib.ps_set_prefill_kernel(0 if args.only == "prefill_single" else 1))
+        ps.check(lib.ps_set_prefill_kernel({"prefill_single": 0, "prefill_pair": 1, "prefill_tn": 3}[args.only]))
         run("mixtral", 3, 8, 256, 512, 512, 1.0)
         print("sanitize run done")
         return
@@ -46,7 +46,7 @@ def main():
     run("mixtral", 3, 8, 256, 512, 8, 0.25, compress_host=True)
     run("mixtral", 3, 8, 256, 512, 256, 0.5, compress_host=True)
     lib = ps.load()
-    for kern, name in ((0, "single-CTA"), (1, "CTA-pair")):  # both tcgen05 prefill kernels explicitly
+    for kern, name in ((0, "single-CTA"), (1, "CTA-pair"), (3, "token-N")):  # every tcgen05 prefill kernel
         ps.check(lib.ps_set_prefill_kernel(kern))
         print("prefill kernel", name)
         run("mixtral", 3, 8, 256, 512, 512, 1.0)

@@ -46,7 +46,7 @@ def test_product_does_not_import_oracle():
 def test_argument_validation_before_any_launch():
     """Entry points reject bad shapes with PS_EINVAL before touching the GPU (CPU safe)."""
     lib = ps.load()
-    assert lib.ps_set_prefill_kernel(3) == ps.capi.PS_EINVAL
+    assert lib.ps_set_prefill_kernel(4) == ps.capi.PS_EINVAL
     assert lib.ps_set_prefill_kernel(2) == ps.capi.PS_OK
     # fused route+permute is a decode-only launch: B <= 64
     p = C.c_void_p(16)

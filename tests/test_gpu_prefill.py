@@ -99,9 +99,9 @@ def _rel(a, b):
     return np.linalg.norm(a - b) / np.linalg.norm(b)
 
 
-@pytest.fixture(params=[0, 1], ids=["single_cta", "cta_pair"])
+@pytest.fixture(params=[0, 1, 3], ids=["single_cta", "cta_pair", "token_n_pair"])
 def prefill_kernel(request):
-    """Both tcgen05 kernels explicitly (ps_set_prefill_kernel), auto mode restored after."""
+    """Every tcgen05 kernel explicitly (ps_set_prefill_kernel), auto mode restored after."""
     lib = ps.load()
     ps.check(lib.ps_set_prefill_kernel(request.param))
     yield request.param
@@ -135,3 +135,66 @@ def test_prefill_mixtral_shape(torch_cuda, prefill_kernel):
     sel = out["sel"]
     for i, t in enumerate(sel):  # per token: a bad padded-tile row cannot hide in a norm over many rows
         assert _rel(out["y"][t], out["y_oracle"][i]) < BF16_RTOL, t
+
+
+def _explicit_counts_case(torch, H, F, counts, seed, reps=1):
+    """k = 1 routing with exactly counts[e] tokens on expert e; y of the prefill path
+    (every launch of `reps`) and the oracle on all rows."""
+    lib = ps.load()
+    s = C.c_void_p(torch.cuda.current_stream().cuda_stream)
+    E = len(counts)
+    rng = np.random.default_rng(seed)
+    ids = rng.permutation(np.repeat(np.arange(E, dtype=np.int32), counts))[:, None].copy()
+    B = ids.shape[0]
+    x = orc.f32_to_bf16((rng.standard_normal((B, H)) / np.sqrt(H)).astype(np.float32))
+    slabs_d = []
+    for e in range(E):
+        t = torch.empty(3 * H * F, dtype=torch.int16, device="cuda")
+        ps.check(lib.ps_init_expert_slab(_p(t), H, F, seed, 0, e, s))
+        slabs_d.append(t)
+    di = torch.as_tensor(ids, device="cuda")
+    dx = torch.as_tensor(x.view(np.int16), device="cuda")
+    off = torch.empty(E + 1, dtype=torch.int32, device="cuda")
+    src = torch.empty(B, dtype=torch.int32, device="cuda")
+    inv = torch.empty(B, dtype=torch.int32, device="cuda")
+    xp = torch.empty(B, H, dtype=torch.int16, device="cuda")
+    ps.check(lib.ps_permute(_p(di), B, 1, E, _p(off), _p(src), _p(inv), _p(dx), H, _p(xp), s))
+    cnt = np.asarray(counts, dtype=np.int32)
+    offsets = off.cpu().numpy()
+    grp = ps.capi.ExpertGroup()
+    grp.n = E
+    for e in range(E):
+        grp.experts[e] = e
+        grp.slabs[e] = slabs_d[e].data_ptr()
+    h = torch.empty(B, F, dtype=torch.int16, device="cuda")
+    gate = np.zeros((B, E), np.float32)
+    gate[np.arange(B), ids[:, 0]] = 1.0
+    ones = torch.as_tensor(gate, device="cuda")
+    ys = []
+    for _ in range(reps):
+        yp = torch.full((B, H), float("nan"), dtype=torch.float32, device="cuda")
+        ps.check(lib.ps_expert_ffn_prefill(C.byref(grp), cnt.ctypes.data, offsets.ctypes.data, _p(xp), B, H, F,
+                                           _p(h), _p(yp), s))
+        y = torch.empty(B, H, dtype=torch.float32, device="cuda")
+        ps.check(lib.ps_combine(_p(yp), 1, _p(inv), _p(di), _p(ones), B, 1, E, H, _p(y), s))
+        ys.append(y.cpu().numpy())
+    slabs_h = [t.cpu().numpy().view(np.uint16) for t in slabs_d]
+    y_ref = orc.or_moe_layer(slabs_h, H, F, x, ids, gate, True)
+    return ys, y_ref
+
+
+def test_prefill_token_n_ragged_counts(torch_cuda):
+    """Token-N kernel at every N-tile boundary case: 1, 15, 16, 17, 255, 256, 257, 300,
+    513 rows (last token tile N = 16 .. 256, 1-3 token tiles per expert), one launch for
+    gate_up + down; every row vs the oracle, and the launch repeated 70 times (map-ring
+    slots reused: the per-slot gate_up counters only grow) with bit-identical outputs."""
+    lib = ps.load()
+    ps.check(lib.ps_set_prefill_kernel(3))
+    try:
+        ys, y_ref = _explicit_counts_case(torch_cuda, 256, 384, [1, 15, 16, 17, 255, 256, 257, 300, 513], 11, reps=70)
+    finally:
+        ps.check(lib.ps_set_prefill_kernel(2))
+    for t in range(y_ref.shape[0]):
+        assert _rel(ys[0][t], y_ref[t]) < BF16_RTOL, t
+    for y in ys[1:]:
+        assert np.array_equal(y, ys[0])
