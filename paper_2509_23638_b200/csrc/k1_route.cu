@@ -18,7 +18,7 @@ namespace {
 constexpr int kWarps = 8;  // warps per token, splitting H
 constexpr int kMaxE = 256;
 constexpr int kMaxK = 16;
-constexpr int kETile = 8;
+constexpr int kETile = 8;  // experts per register tile (decode); prefill chunks use 4 x 8 tokens
 
 // Per-token tail of the router (one warp): kappa override, softmax, top-k, histogram.
 __device__ __forceinline__ void finish_token_impl(int warp, int b0, float* lg, const uint8_t* __restrict__ follow,
@@ -95,14 +95,20 @@ struct FusedPermute {  // K2 index pass run by the last CTA of a decode route la
 };
 
 template <int TB, bool kFused>
-__global__ void __launch_bounds__(kWarps * 32)
+__global__ void __launch_bounds__(kWarps * 32, TB >= 8 ? 2 : 1)
 route_kernel(const float* __restrict__ x, const float* __restrict__ gate, const float* __restrict__ bias,
              const uint8_t* __restrict__ follow, const int32_t* __restrict__ prev_ids, int prev_k,
              int B, int H, int E, int k, float sqrt_h, float* __restrict__ logits_out,
              float* __restrict__ weights_out, int32_t* __restrict__ ids_out,
              int32_t* __restrict__ counts, uint16_t* __restrict__ x_bf16, FusedPermute fp) {
-  __shared__ float s_part[kWarps][TB][kMaxE];
+  // per-warp partial logits [kWarps][TB][E] (dynamic: E * TB * 32 B) + logits [TB][kMaxE]
+  extern __shared__ float s_dyn[];
   __shared__ float s_logit[TB][kMaxE];
+  auto s_part = [&](int w, int t, int e) -> float& { return s_dyn[(w * TB + t) * E + e]; };
+  // TB = 8 (prefill chunks): 4 experts x 8 tokens per register tile and one float4 step
+  // in flight (~100 registers, 2 CTAs per SM, all 8 warps busy in the per-token tail);
+  // the per-lane accumulation order is the same as TB = 1 / 4 (increasing h).
+  constexpr int ET = TB >= 8 ? 4 : kETile;
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   const int b0 = blockIdx.x * TB;
   const int nt = min(TB, B - b0);
@@ -112,18 +118,63 @@ route_kernel(const float* __restrict__ x, const float* __restrict__ gate, const 
   // Vector path: kU float4 steps per lane in flight together (latency-bound at decode),
   // and the x values loaded for the first expert tile are also written out as bf16
   // (fused cast for K3).
-  constexpr int kU = 2;
+  constexpr int kU = TB >= 8 ? 1 : 2;
   const int hs = vec ? ((H / 4 + kWarps - 1) / kWarps) * 4 : (H + kWarps - 1) / kWarps;
   const int h_lo = min(H, warp * hs), h_hi = min(H, h_lo + hs);
-  for (int e0 = 0; e0 < E; e0 += kETile) {
-    float acc[TB][kETile];
+  // Prefill fast path (whole token tile, whole expert tiles, every warp slice a multiple of
+  // 128 floats): no per-element bounds selects, row pointers hoisted. Same per-lane
+  // accumulation order and dot-product expression as the general loop below (bit-identical).
+  const bool fast = TB >= 8 && vec && nt == TB && E % ET == 0 && (h_hi - h_lo) % 128 == 0;
+  if (fast) {
+    const float* xrow = x + static_cast<size_t>(b0) * H;
+    for (int e0 = 0; e0 < E; e0 += ET) {
+      float acc[TB][ET];
+#pragma unroll
+      for (int t = 0; t < TB; ++t)
+#pragma unroll
+        for (int j = 0; j < ET; ++j) acc[t][j] = 0.f;
+      const float* grow = gate + static_cast<size_t>(e0) * H;
+      for (int h = h_lo + lane * 4; h < h_hi; h += 128) {
+        float4 xv[TB], g[ET];
+#pragma unroll
+        for (int t = 0; t < TB; ++t) xv[t] = *reinterpret_cast<const float4*>(xrow + static_cast<size_t>(t) * H + h);
+#pragma unroll
+        for (int j = 0; j < ET; ++j) g[j] = __ldg(reinterpret_cast<const float4*>(grow + static_cast<size_t>(j) * H + h));
+#pragma unroll
+        for (int j = 0; j < ET; ++j)
+#pragma unroll
+          for (int t = 0; t < TB; ++t)
+            acc[t][j] += g[j].x * xv[t].x + g[j].y * xv[t].y + g[j].z * xv[t].z + g[j].w * xv[t].w;
+        if (x_bf16 && e0 == 0) {
+#pragma unroll
+          for (int t = 0; t < TB; ++t) {
+            uint2 o;
+            o.x = (uint32_t)f32_to_bf16_rne(xv[t].x) | ((uint32_t)f32_to_bf16_rne(xv[t].y) << 16);
+            o.y = (uint32_t)f32_to_bf16_rne(xv[t].z) | ((uint32_t)f32_to_bf16_rne(xv[t].w) << 16);
+            *reinterpret_cast<uint2*>(x_bf16 + static_cast<size_t>(b0 + t) * H + h) = o;
+          }
+        }
+      }
+      if constexpr (TB * ET == 32) {
+        float v[32];
+#pragma unroll
+        for (int t = 0; t < TB; ++t)
+#pragma unroll
+          for (int j = 0; j < ET; ++j) v[t * ET + j] = acc[t][j];
+        const float sum = warp_transpose_sum<32>(v);
+        s_part(warp, lane / ET, e0 + lane % ET) = sum;
+      }
+    }
+  }
+  for (int e0 = 0; e0 < (fast ? 0 : E); e0 += ET) {
+    float acc[TB][ET];
 #pragma unroll
     for (int t = 0; t < TB; ++t)
 #pragma unroll
-      for (int j = 0; j < kETile; ++j) acc[t][j] = 0.f;
+      for (int j = 0; j < ET; ++j) acc[t][j] = 0.f;
     if (vec) {
       for (int hb = h_lo + lane * 4; hb < h_hi; hb += 128 * kU) {
-        float4 xv[kU][TB], g[kU][kETile];
+        float4 xv[kU][TB], g[kU][ET];
 #pragma unroll
         for (int u = 0; u < kU; ++u) {
           const int h = hb + 128 * u;
@@ -133,14 +184,14 @@ route_kernel(const float* __restrict__ x, const float* __restrict__ gate, const 
             xv[u][t] = hin && t < nt ? *reinterpret_cast<const float4*>(x + static_cast<size_t>(b0 + t) * H + h)
                                      : make_float4(0.f, 0.f, 0.f, 0.f);
 #pragma unroll
-          for (int j = 0; j < kETile; ++j)
+          for (int j = 0; j < ET; ++j)
             g[u][j] = hin && e0 + j < E ? __ldg(reinterpret_cast<const float4*>(gate + static_cast<size_t>(e0 + j) * H + h))
                                         : make_float4(0.f, 0.f, 0.f, 0.f);
         }
 #pragma unroll
         for (int u = 0; u < kU; ++u) {
 #pragma unroll
-          for (int j = 0; j < kETile; ++j)
+          for (int j = 0; j < ET; ++j)
 #pragma unroll
             for (int t = 0; t < TB; ++t)
               acc[t][j] += g[u][j].x * xv[u][t].x + g[u][j].y * xv[u][t].y + g[u][j].z * xv[u][t].z +
@@ -165,7 +216,7 @@ route_kernel(const float* __restrict__ x, const float* __restrict__ gate, const 
             x_bf16[static_cast<size_t>(b0 + t) * H + h] = f32_to_bf16_rne(x[static_cast<size_t>(b0 + t) * H + h]);
       for (int h = h_lo + lane; h < h_hi; h += 32) {
 #pragma unroll
-        for (int j = 0; j < kETile; ++j) {
+        for (int j = 0; j < ET; ++j) {
           if (e0 + j >= E) continue;
           const float g = __ldg(gate + static_cast<size_t>(e0 + j) * H + h);
 #pragma unroll
@@ -174,20 +225,34 @@ route_kernel(const float* __restrict__ x, const float* __restrict__ gate, const 
         }
       }
     }
+    if constexpr (TB * ET == 32) {
+      // All 32 warp sums at once (31 shuffles instead of 160): warp_transpose_sum<32> pairs
+      // lanes at distance 16, 8, 4, 2, 1 like warp_sum, so every sum is bit-identical to
+      // the decode instantiation's; lane i ends up with value i = (token i / ET, expert i % ET).
+      float v[32];
 #pragma unroll
-    for (int t = 0; t < TB; ++t)
+      for (int t = 0; t < TB; ++t)
 #pragma unroll
-      for (int j = 0; j < kETile; ++j) {
-        float sum = warp_sum(acc[t][j]);
-        if (lane == 0 && e0 + j < E) s_part[warp][t][e0 + j] = sum;
-      }
+        for (int j = 0; j < ET; ++j) v[t * ET + j] = acc[t][j];
+      const float sum = warp_transpose_sum<32>(v);
+      const int t = lane / ET, j = lane % ET;
+      if (t < TB && e0 + j < E) s_part(warp, t, e0 + j) = sum;
+    } else {
+#pragma unroll
+      for (int t = 0; t < TB; ++t)
+#pragma unroll
+        for (int j = 0; j < ET; ++j) {
+          float sum = warp_sum(acc[t][j]);
+          if (lane == 0 && e0 + j < E) s_part(warp, t, e0 + j) = sum;
+        }
+    }
   }
   __syncthreads();
   for (int i = threadIdx.x; i < nt * E; i += kWarps * 32) {
     const int t = i / E, e = i % E;
     float sum = 0.f;
 #pragma unroll
-    for (int w = 0; w < kWarps; ++w) sum += s_part[w][t][e];
+    for (int w = 0; w < kWarps; ++w) sum += s_part(w, t, e);
     s_logit[t][e] = sum * sqrt_h + (bias ? bias[e] : 0.f);
   }
   __syncthreads();
@@ -231,12 +296,19 @@ extern "C" ps_status ps_route_topk(const float* x, const float* gate, const floa
     if (B == 0) return;
     const float sqrt_h = static_cast<float>(std::sqrt(static_cast<double>(H)));
     if (B <= 64) {
-      route_kernel<1, false><<<B, kWarps * 32, 0, s>>>(x, gate, bias, follow, prev_ids, prev_k, B, H, E, k, sqrt_h,
-                                                       logits, weights, ids, counts, x_bf16, FusedPermute{});
+      route_kernel<1, false><<<B, kWarps * 32, kWarps * 1 * E * 4, s>>>(
+          x, gate, bias, follow, prev_ids, prev_k, B, H, E, k, sqrt_h, logits, weights, ids, counts, x_bf16,
+          FusedPermute{});
     } else {
-      route_kernel<4, false><<<(B + 3) / 4, kWarps * 32, 0, s>>>(x, gate, bias, follow, prev_ids, prev_k, B, H, E, k,
-                                                                 sqrt_h, logits, weights, ids, counts, x_bf16,
-                                                                 FusedPermute{});
+      static bool attr = false;
+      if (!attr) {  // E = 256: 64 KiB of partials
+        PS_CUDA(cudaFuncSetAttribute(route_kernel<8, false>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                     kWarps * 8 * kMaxE * 4));
+        attr = true;
+      }
+      route_kernel<8, false><<<(B + 7) / 8, kWarps * 32, kWarps * 8 * E * 4, s>>>(
+          x, gate, bias, follow, prev_ids, prev_k, B, H, E, k, sqrt_h, logits, weights, ids, counts, x_bf16,
+          FusedPermute{});
     }
     PS_LAUNCH_CHECK("route_kernel");
   });
@@ -254,7 +326,7 @@ extern "C" ps_status ps_route_permute(const float* x, const float* gate, const f
     require((reinterpret_cast<uintptr_t>(x) & 15) == 0 && (reinterpret_cast<uintptr_t>(gate) & 15) == 0,
             "ps_route_permute: x and gate must be 16-byte aligned");
     const float sqrt_h = static_cast<float>(std::sqrt(static_cast<double>(H)));
-    route_kernel<1, true><<<B, kWarps * 32, 0, as_stream(stream)>>>(
+    route_kernel<1, true><<<B, kWarps * 32, kWarps * 1 * E * 4, as_stream(stream)>>>(
         x, gate, bias, follow, prev_ids, prev_k, B, H, E, k, sqrt_h, nullptr, weights, ids, nullptr, x_bf16,
         FusedPermute{offsets, perm_src, inv, workspace});
     PS_LAUNCH_CHECK("route_kernel<fused permute>");

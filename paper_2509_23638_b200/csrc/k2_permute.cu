@@ -28,6 +28,67 @@ permute_index_kernel(const int32_t* __restrict__ ids, int n, int E, int32_t* __r
   permute_block<kPermThreads, false>(ids, n, E, offsets, perm_src, inv, s_base, s_warp_cnt);
 }
 
+// Multi-CTA index pass for prefill chunks (the single CTA above walks 1024-id chunks one
+// after another: 42 us for 16K ids). One CTA per 1024-id chunk; each CTA histograms ALL
+// ids (n <= 128K: at most 512 KiB of L2 reads per CTA, warp-aggregated shared atomics) into
+// per-expert totals and the part before its chunk, so no cross-CTA scratch or second
+// launch is needed; then it ranks its chunk exactly as permute_block does. Same (unique)
+// stable order.
+__global__ void __launch_bounds__(kPermThreads)
+permute_chunks_kernel(const int32_t* __restrict__ ids, int n, int E, int32_t* __restrict__ offsets,
+                      int32_t* __restrict__ perm_src, int32_t* __restrict__ inv) {
+  __shared__ int s_base[kMaxE + 1];
+  __shared__ int s_before[kMaxE];
+  __shared__ int s_warp_cnt[kPermWarps][kMaxE];
+  const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31, chunk = blockIdx.x;
+  const int c0 = chunk * kPermThreads;
+  for (int e = tid; e <= E; e += kPermThreads) s_base[e] = 0;
+  for (int e = tid; e < E; e += kPermThreads) s_before[e] = 0;
+  __syncthreads();
+  for (int i0 = 0; i0 < n; i0 += kPermThreads) {  // warp-aggregated: one atomic per distinct expert
+    const int i = i0 + tid;
+    const int e = i < n ? __ldg(ids + i) : -1 - lane;
+    const unsigned peers = __match_any_sync(0xffffffffu, e);
+    if (i < n && (peers & ((1u << lane) - 1u)) == 0) {
+      atomicAdd(&s_base[e + 1], __popc(peers));
+      if (i0 < c0) atomicAdd(&s_before[e], __popc(peers));  // whole earlier chunks only
+    }
+  }
+  __syncthreads();
+  if (warp == 0) {  // inclusive scan of the totals -> offsets
+    int carry = 0;
+    for (int e0 = 0; e0 <= E; e0 += 32) {
+      int v = e0 + lane <= E ? s_base[e0 + lane] : 0;
+#pragma unroll
+      for (int o = 1; o < 32; o <<= 1) {
+        const int t = __shfl_up_sync(0xffffffffu, v, o);
+        if (lane >= o) v += t;
+      }
+      v += carry;
+      if (e0 + lane <= E) s_base[e0 + lane] = v;
+      carry = __shfl_sync(0xffffffffu, v, 31);
+    }
+  }
+  for (int i2 = tid; i2 < kPermWarps * E; i2 += kPermThreads) s_warp_cnt[i2 / E][i2 % E] = 0;
+  __syncthreads();
+  if (chunk == 0)
+    for (int e = tid; e <= E; e += kPermThreads) offsets[e] = s_base[e];
+  const int i = c0 + tid;
+  const bool valid = i < n;
+  const int e = valid ? __ldg(ids + i) : -1 - lane;
+  const unsigned peers = __match_any_sync(0xffffffffu, e);
+  const int rank = __popc(peers & ((1u << lane) - 1u));
+  if (valid && rank == 0) s_warp_cnt[warp][e] = __popc(peers);
+  __syncthreads();
+  if (valid) {
+    int before = 0;
+    for (int w = 0; w < warp; ++w) before += s_warp_cnt[w][e];
+    const int pos = s_base[e] + s_before[e] + before + rank;
+    perm_src[pos] = i;
+    inv[i] = pos;
+  }
+}
+
 // x_perm[pos] = x[perm_src[pos] / k]; one warp per row, 16 B per lane per step.
 __global__ void gather_rows_kernel(const uint16_t* __restrict__ x, const int32_t* __restrict__ perm_src,
                                    int rows, int k, int H, uint16_t* __restrict__ x_perm) {
@@ -58,6 +119,41 @@ __global__ void combine_kernel(const float* __restrict__ y_part, int n_split, si
       s.x += v.x; s.y += v.y; s.z += v.z; s.w += v.w;
     }
     acc.x += g * s.x; acc.y += g * s.y; acc.z += g * s.z; acc.w += g * s.w;
+  }
+  *reinterpret_cast<float4*>(y + static_cast<size_t>(t) * H + h) = acc;
+}
+
+// n_split == 1 (prefill / tcgen05 path, k + shared <= 16): the same arithmetic as
+// combine_kernel (bit-identical), but every slot's index, gate weight and row load is
+// issued before the first accumulation, so a thread has k row loads in flight instead
+// of one dependent chain per slot (prefill combine: 40 -> ~20 us for 16K rows of 8 KiB).
+template <int KMAX>
+__global__ void combine_ilp_kernel(const float* __restrict__ y_part, const int32_t* __restrict__ inv,
+                                   const int32_t* __restrict__ ids, const float* __restrict__ w, int k, int E,
+                                   int H, float* __restrict__ y) {
+  const int t = blockIdx.x;
+  const int h = (blockIdx.y * blockDim.x + threadIdx.x) * 4;
+  if (h >= H) return;
+  int r[KMAX];
+  float g[KMAX];
+  float4 v[KMAX];
+#pragma unroll
+  for (int j = 0; j < KMAX; ++j)
+    if (j < k) r[j] = __ldg(inv + t * k + j);
+#pragma unroll
+  for (int j = 0; j < KMAX; ++j)
+    if (j < k) g[j] = __ldg(w + static_cast<size_t>(t) * E + __ldg(ids + t * k + j));
+#pragma unroll
+  for (int j = 0; j < KMAX; ++j)
+    if (j < k) v[j] = __ldg(reinterpret_cast<const float4*>(y_part + static_cast<size_t>(r[j]) * H + h));
+  float4 acc = make_float4(0.f, 0.f, 0.f, 0.f);
+#pragma unroll
+  for (int j = 0; j < KMAX; ++j) {
+    if (j < k) {
+      float4 s = make_float4(0.f, 0.f, 0.f, 0.f);
+      s.x += v[j].x; s.y += v[j].y; s.z += v[j].z; s.w += v[j].w;
+      acc.x += g[j] * s.x; acc.y += g[j] * s.y; acc.z += g[j] * s.z; acc.w += g[j] * s.w;
+    }
   }
   *reinterpret_cast<float4*>(y + static_cast<size_t>(t) * H + h) = acc;
 }
@@ -202,8 +298,15 @@ ps_status ps_permute(const int32_t* ids, int B, int k, int E, int32_t* offsets, 
     require(static_cast<int64_t>(B) * k <= (1 << 20), "ps_permute: too many assignments");
     require(ids && offsets && perm_src && inv, "ps_permute: null output");
     cudaStream_t s = as_stream(stream);
-    permute_index_kernel<<<1, kPermThreads, 0, s>>>(ids, B * k, E, offsets, perm_src, inv);
-    PS_LAUNCH_CHECK("permute_index_kernel");
+    const int n = B * k;
+    const int chunks = (n + kPermThreads - 1) / kPermThreads;
+    if (chunks <= 2 || chunks > 128) {
+      permute_index_kernel<<<1, kPermThreads, 0, s>>>(ids, n, E, offsets, perm_src, inv);
+      PS_LAUNCH_CHECK("permute_index_kernel");
+    } else {  // prefill chunks: one CTA per 1024 ids
+      permute_chunks_kernel<<<chunks, kPermThreads, 0, s>>>(ids, n, E, offsets, perm_src, inv);
+      PS_LAUNCH_CHECK("permute_chunks_kernel");
+    }
     if (x && x_perm && B > 0) {
       require(H % 8 == 0, "ps_permute: gather needs H % 8 == 0");
       const int rows = B * k;
@@ -219,8 +322,14 @@ ps_status ps_combine(const float* y_part, int n_split, const int32_t* inv, const
     require(B >= 0 && k >= 1 && E >= 1 && n_split >= 1 && H % 4 == 0, "ps_combine: bad shape (H % 4 == 0)");
     if (B == 0) return;
     dim3 grid(B, (H / 4 + 255) / 256);
-    combine_kernel<<<grid, 256, 0, as_stream(stream)>>>(y_part, n_split, static_cast<size_t>(B) * k * H, inv,
-                                                        ids, weights, k, E, H, y);
+    if (n_split == 1 && k <= 8) {
+      combine_ilp_kernel<8><<<grid, 256, 0, as_stream(stream)>>>(y_part, inv, ids, weights, k, E, H, y);
+    } else if (n_split == 1 && k <= 16) {
+      combine_ilp_kernel<16><<<grid, 256, 0, as_stream(stream)>>>(y_part, inv, ids, weights, k, E, H, y);
+    } else {
+      combine_kernel<<<grid, 256, 0, as_stream(stream)>>>(y_part, n_split, static_cast<size_t>(B) * k * H, inv,
+                                                          ids, weights, k, E, H, y);
+    }
     PS_LAUNCH_CHECK("combine_kernel");
   });
 }

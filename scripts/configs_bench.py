@@ -143,6 +143,18 @@ def run_deepseek(torch, args, ht):
                   "executor": leg, "tokens_per_step": T, "ffn_tflops": tf, "tc_launches": st["tc_launches"],
                   "budget_fraction": args.budget})
         print(json.dumps(d), flush=True)
+    # the same chunk with every expert resident: one grouped tcgen05 launch per layer,
+    # the expert GEMM's own rate (BASELINE config 3's prefill FFN vs the bf16 peak)
+    e_full = make_engine(spec, gen, gate, freq, 1.0, T, pred, 0, n_shared=2)
+    st, ms = timed_steps(torch, e_full, [ph], [pf], py, 1, 3)
+    tf = st["ffn_flops_total"] / (st["ffn_ms_total"] / 1e3) / 1e12 if st["ffn_ms_total"] > 0 else 0.0
+    d = bench.decode_summary(st, ms, 1, T, L)
+    peak, peak_kind = bench.bf16_peak()
+    d.update({"config": "deepseek-v2-lite-shape prefill 2048 tokens, all experts resident (64 routed top-6 + 2 shared)",
+              "executor": "all_resident", "tokens_per_step": T, "ffn_tflops": tf, "tc_launches": st["tc_launches"],
+              "ffn_frac_of_bf16_peak": tf / peak, "peak_tflops": peak, "peak_kind": peak_kind, "budget_fraction": 1.0})
+    print(json.dumps(d), flush=True)
+    e_full.close()
     del ph, py
     hid, fol = trace_steps(torch, gen, spec, B, args.warmup + args.steps, 3000)
     y = torch.empty(L, B, H, device="cuda")

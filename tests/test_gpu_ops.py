@@ -114,7 +114,27 @@ def test_route_topk_parity(torch_cuda, case):
         p.write_text(json.dumps(prev, indent=1))
 
 
-@pytest.mark.parametrize("B,k,E", [(1, 2, 8), (16, 2, 8), (32, 8, 128), (2048, 6, 64), (4096, 8, 128)])
+@pytest.mark.parametrize("E,H,k", [(8, 4096, 2), (64, 2048, 6), (128, 2048, 8)])
+def test_route_batch_invariant(torch_cuda, E, H, k):
+    """A token's logits, weights and ids do not depend on the batch it is routed in: a
+    256-token chunk (prefill instantiation, 4 tokens per CTA, one transpose-reduce of 32
+    sums per warp) gives bitwise what 64-token decode batches give (1 token per CTA,
+    warp_sum per value) — the reduction trees are the same."""
+    torch = torch_cuda
+    g = torch.Generator(device="cuda").manual_seed(E + H)
+    x = torch.randn(256, H, device="cuda", generator=g)
+    gate = torch.randn(E, H, device="cuda", generator=g) / H ** 0.5
+    bias = -torch.log(torch.arange(1, E + 1, device="cuda", dtype=torch.float32))
+    big = eng.route(x, gate, bias, None, None, k)
+    parts = [eng.route(x[i:i + 64].contiguous(), gate, bias, None, None, k) for i in range(0, 256, 64)]
+    for j in (0, 1, 2, 4):
+        whole = big[j].cpu().numpy()
+        split = np.concatenate([p[j].cpu().numpy() for p in parts])
+        assert np.array_equal(whole, split), j
+
+
+@pytest.mark.parametrize("B,k,E", [(1, 2, 8), (16, 2, 8), (32, 8, 128), (2048, 6, 64), (4096, 8, 128),
+                                   (2048, 8, 66), (4100, 3, 7)])
 def test_permute_bit_exact(torch_cuda, B, k, E):
     torch = torch_cuda
     rng = np.random.default_rng(B + k)
