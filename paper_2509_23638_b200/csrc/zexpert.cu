@@ -14,9 +14,9 @@
 // code width with the smaller estimated size). Decoding is bit-exact
 // (tests/test_gpu_zexpert.py), so every downstream result is identical to loading the
 // raw slab. Encoder: host C++ (at engine create, multithreaded over blocks); decoder:
-// one warp per 1024-value block in four 256-value chunks (8 values per lane), escape
-// ranks by a warp scan, coalesced 512-byte warp stores (HBM-bound: 1.41 B read + 2 B
-// written per value).
+// one warp per 1024-value block, 32 values per lane, escape ranks by a warp scan, the
+// block staged in shared memory and written as coalesced 512-byte warp stores (1.41 B
+// read + 2 B written per value; v4 for 3-bit codes at 0.77 of HBM, v3 for 4-bit at 0.82).
 #include <algorithm>
 #include <cstdlib>
 #include <cstring>
@@ -203,6 +203,187 @@ z_decode_kernel(const uint8_t* __restrict__ z, uint64_t n, uint32_t base, uint32
         if (v0 + i < n) out[v0 + i] = so16[chunk(lane, i >> 3) * 8 + (i & 7)];
     }
     __syncwarp();  // staging buffers are reused by the next block
+  }
+}
+
+// v4 (default, PS_ZDECODE=3 selects v3): v3's structure with ~25 % fewer instructions —
+//  * assembly per bf16 pair: one byte permute DUPLICATES each lo byte into both halves of
+//    its 16-bit lane ([b b]: bit 15 = sign, bits 0-6 = mantissa), so the value is
+//    (P & 0x807f807f) | ((C << 7) + (base << 7 | base << 23)) — PRMT, funnel shift, three
+//    mask/shift ops, one IMAD, one LOP3 instead of eleven instructions;
+//  * escapes: per-value 32-bit masks (codes 0-10 | 11-20 | 21-31), index by a multiply-high
+//    division, and the patch rewrites only the exponent of the value already staged in
+//    shared memory (no dependent global load of its lo byte). Requires base + 2^BITS - 1 <
+//    256 (an escape code's provisional exponent must not carry into the sign); the host
+//    falls back to v3 otherwise.
+template <int BITS>
+__global__ void __launch_bounds__(256, 4)
+z_decode_kernel_v4(const uint8_t* __restrict__ z, uint64_t n, uint32_t base, uint32_t nb, uint32_t tile_h,
+                   uint32_t tile_f, uint16_t* __restrict__ out) {
+  __shared__ uint8_t s_esc[8][kZEscStage];
+  __shared__ __align__(16) uint4 s_out[8][128];
+  const uint64_t n_pad = static_cast<uint64_t>(nb) * kZBlock;
+  const uint8_t* lo = z + z_lo_off();
+  const uint32_t* codes = reinterpret_cast<const uint32_t*>(z + z_codes_off(n_pad));
+  const uint32_t* esc_off = reinterpret_cast<const uint32_t*>(z + z_escoff_off(n_pad, BITS));
+  const uint8_t* esc = z + z_esc_off(n_pad, nb, BITS);
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+  const uint32_t warps = (gridDim.x * blockDim.x) >> 5;
+  const uint32_t ebase = (base << 7) | (base << 23);
+  uint8_t* se = s_esc[warp];
+  uint4* so = s_out[warp];
+  const uint32_t so_s = static_cast<uint32_t>(__cvta_generic_to_shared(so));
+  auto chunk = [](int ln, int q) { return ln * 4 + (q ^ ((ln >> 1) & 3)); };
+  struct Blk {
+    uint4 l0, l1;
+    uint32_t cw[BITS];
+    uint32_t eoff, eend;
+  };
+  auto fetch = [&](uint32_t bb, Blk& k) {
+    const uint64_t seg = static_cast<uint64_t>(bb) * 32 + lane;
+    k.l0 = __ldg(reinterpret_cast<const uint4*>(lo + seg * 32));
+    k.l1 = __ldg(reinterpret_cast<const uint4*>(lo + seg * 32 + 16));
+#pragma unroll
+    for (int q = 0; q < BITS; ++q) k.cw[q] = __ldg(codes + seg * BITS + q);
+    k.eoff = __ldg(esc_off + bb);
+    k.eend = __ldg(esc_off + bb + 1);
+  };
+  uint32_t b = (blockIdx.x * blockDim.x + threadIdx.x) >> 5;
+  Blk nxt{};
+  if (b < nb) fetch(b, nxt);
+  for (; b < nb; b += warps) {
+    const Blk cur = nxt;
+    if (b + warps < nb) fetch(b + warps, nxt);
+    const uint64_t vb = static_cast<uint64_t>(b) * kZBlock;
+    const uint64_t v0 = vb + 32u * lane;
+    uint32_t cw[BITS + 1];
+#pragma unroll
+    for (int q = 0; q < BITS; ++q) cw[q] = cur.cw[q];
+    cw[BITS] = 0;
+    const uint32_t lw[8] = {cur.l0.x, cur.l0.y, cur.l0.z, cur.l0.w, cur.l1.x, cur.l1.y, cur.l1.z, cur.l1.w};
+#pragma unroll
+    for (int q = 0; q < 4; ++q) {
+      uint32_t pk[4];
+#pragma unroll
+      for (int h = 0; h < 4; ++h) {
+        const int p = 4 * q + h;  // values 2p, 2p+1
+        const uint32_t P = __byte_perm(lw[p >> 1], 0u, (p & 1) ? 0x3322u : 0x1100u);
+        pk[h] = (P & 0x807f807fu) | (z_code_pair<BITS>(cw, 2 * p) * 128u + ebase);
+      }
+      so[chunk(lane, q)] = make_uint4(pk[0], pk[1], pk[2], pk[3]);
+    }
+    if (cur.eend != cur.eoff) {  // escapes in this block (warp-uniform)
+      const uint32_t eoff = cur.eoff;
+      const uint32_t n_stage = min(cur.eend - eoff, static_cast<uint32_t>(kZEscStage));
+      for (uint32_t k = lane; k < n_stage; k += 32) se[k] = esc[eoff + k];
+      __syncwarp();
+      // per-value escape masks: m[0] codes 0-10 at bit 3i (BITS 3) ..., see v3's word tricks
+      uint32_t m[3];
+      int first[3];
+      if constexpr (BITS == 3) {
+        const uint64_t A = static_cast<uint64_t>(cw[0]) | (static_cast<uint64_t>(cw[1]) << 32);
+        const uint64_t B = (static_cast<uint64_t>(cw[1]) >> 31) | (static_cast<uint64_t>(cw[2]) << 1);
+        const uint64_t ma = A & (A >> 1) & (A >> 2) & 0x1249249249249249ull;  // codes 0..20: bit 3i
+        m[0] = static_cast<uint32_t>(ma);         // codes 0..10 (bits 0..30)
+        m[1] = static_cast<uint32_t>(ma >> 32);   // codes 11..20 (bits 1..28 = 3i - 32)
+        m[2] = static_cast<uint32_t>(B & (B >> 1) & (B >> 2) & 0x49249249ull);  // codes 21..31: bit 3(i-21)
+        first[0] = 0;
+        first[1] = 32;
+        first[2] = 63;  // (pos + 63) / 3 = 21 + pos / 3
+      } else {
+        m[0] = m[1] = m[2] = 0;
+        first[0] = first[1] = first[2] = 0;
+      }
+      int n_e;
+      if constexpr (BITS == 3) {
+        n_e = __popc(m[0]) + __popc(m[1]) + __popc(m[2]);
+      } else {
+        n_e = z_count_esc<BITS>(cw);
+      }
+      int incl = n_e;
+#pragma unroll
+      for (int o = 1; o < 32; o <<= 1) {
+        const int t = __shfl_up_sync(0xffffffffu, incl, o);
+        if (lane >= o) incl += t;
+      }
+      uint32_t r = static_cast<uint32_t>(incl - n_e);  // this lane's first escape rank in the block
+      const uint32_t key = (lane >> 1) & 3;
+      auto patch = [&](int i, uint32_t ex) {
+        const uint32_t addr = so_s + static_cast<uint32_t>(lane * 64) + ((static_cast<uint32_t>(i >> 3) ^ key) << 4) +
+                              static_cast<uint32_t>((i & 7) * 2);
+        uint32_t v;
+        asm volatile("ld.shared.u16 %0, [%1];" : "=r"(v) : "r"(addr));
+        v = (v & 0x807fu) | (ex << 7);
+        asm volatile("st.shared.u16 [%0], %1;" ::"r"(addr), "h"(static_cast<uint16_t>(v)));
+      };
+      if (cur.eend - eoff <= static_cast<uint32_t>(kZEscStage)) {  // all staged (the common case)
+        if constexpr (BITS == 3) {
+          // one loop over the three masks in value order (the warp runs max-over-lanes
+          // iterations: one merged loop instead of three)
+          while (m[0] | m[1] | m[2]) {
+            const int w = m[0] ? 0 : (m[1] ? 1 : 2);
+            const uint32_t mm = w == 0 ? m[0] : (w == 1 ? m[1] : m[2]);
+            const uint32_t pos = static_cast<uint32_t>(__ffs(mm) - 1) + (w == 0 ? 0u : (w == 1 ? 32u : 63u));
+            const uint32_t cleared = mm & (mm - 1);
+            if (w == 0) m[0] = cleared;
+            else if (w == 1) m[1] = cleared;
+            else m[2] = cleared;
+            patch(static_cast<int>(__umulhi(pos, 0x55555556u)), se[r++]);
+          }
+        } else {
+#pragma unroll
+          for (int q = 0; q < 4; ++q) {
+            uint32_t mm = cw[q] & (cw[q] >> 1) & (cw[q] >> 2) & (cw[q] >> 3) & 0x11111111u;
+            while (mm) {
+              const int pos = __ffs(mm) - 1;
+              mm &= mm - 1;
+              patch(8 * q + (pos >> 2), se[r++]);
+            }
+          }
+        }
+      } else {  // > kZEscStage escapes in the block: ranks past the staged ones read global memory
+        auto ex_at = [&](uint32_t rk) {
+          return rk < static_cast<uint32_t>(kZEscStage) ? static_cast<uint32_t>(se[rk]) : static_cast<uint32_t>(esc[eoff + rk]);
+        };
+        if constexpr (BITS == 3) {
+#pragma unroll
+          for (int w = 0; w < 3; ++w) {
+            uint32_t mm = m[w];
+            while (mm) {
+              const int pos = __ffs(mm) - 1;
+              mm &= mm - 1;
+              patch(static_cast<int>(__umulhi(static_cast<uint32_t>(pos + first[w]), 0x55555556u)), ex_at(r++));
+            }
+          }
+        } else {
+#pragma unroll
+          for (int q = 0; q < 4; ++q) {
+            uint32_t mm = cw[q] & (cw[q] >> 1) & (cw[q] >> 2) & (cw[q] >> 3) & 0x11111111u;
+            while (mm) {
+              const int pos = __ffs(mm) - 1;
+              mm &= mm - 1;
+              patch(8 * q + (pos >> 2), ex_at(r++));
+            }
+          }
+        }
+      }
+    }
+    __syncwarp();
+    if (vb + kZBlock <= n) {
+      const uint64_t my_off = tile_h ? static_cast<uint64_t>(z_untile32(static_cast<uint32_t>(v0), tile_h, tile_f))
+                                     : v0;
+#pragma unroll
+      for (int rr = 0; rr < 4; ++rr) {
+        const int c = lane + 32 * rr, sl = c >> 2, q = c & 3;
+        const uint64_t seg_off = __shfl_sync(0xffffffffu, my_off, sl);
+        *reinterpret_cast<uint4*>(out + seg_off + 8 * q) = so[chunk(sl, q)];
+      }
+    } else {
+      const uint16_t* so16 = reinterpret_cast<const uint16_t*>(so);
+      for (int i = 0; i < 32; ++i)
+        if (v0 + i < n) out[v0 + i] = so16[chunk(lane, i >> 3) * 8 + (i & 7)];
+    }
+    __syncwarp();
   }
 }
 
@@ -502,9 +683,9 @@ ps_status ps_zslab_decode(const uint8_t* z_dev, const uint8_t* z_host_header, ui
     const uint32_t th = h.tiled ? h.tile_h : 0, tf = h.tiled ? h.tile_f : 0;
     require(!h.tiled || (th % 32 == 0 && tf % 32 == 0 && th && tf && h.n == 3ull * th * tf && h.n < (1ull << 32)),
             "ps_zslab_decode: bad tiled header");
-    static const int version = [] {  // PS_ZDECODE=1: the round-1 per-value decoder (A/B)
+    const int version = [] {  // PS_ZDECODE=1 / 3: the round-1 / v3 decoders (A/B), else v4
       const char* v = std::getenv("PS_ZDECODE");
-      return v && v[0] == '1' ? 1 : 3;
+      return v && (v[0] == '1' || v[0] == '3') ? v[0] - '0' : 4;
     }();
     if (version == 1) {
       const int grid1 = static_cast<int>(std::min<uint64_t>((static_cast<uint64_t>(h.nb) * 32 + threads - 1) / threads,
@@ -513,6 +694,10 @@ ps_status ps_zslab_decode(const uint8_t* z_dev, const uint8_t* z_host_header, ui
         z_decode_kernel_v1<3><<<grid1, threads, 0, as_stream(stream)>>>(z_dev, h.n, h.base, h.nb, th, tf, out);
       else
         z_decode_kernel_v1<4><<<grid1, threads, 0, as_stream(stream)>>>(z_dev, h.n, h.base, h.nb, th, tf, out);
+    } else if (version == 4 && h.code_bits == 3 && h.base + z_escape(h.code_bits) < 256) {
+      // v4 for 3-bit codes (151 -> 119 us per Mixtral expert); 4-bit codes (0.01 % escapes)
+      // gain nothing from its escape path and stay on v3 (113-116 us either way)
+      z_decode_kernel_v4<3><<<grid, threads, 0, as_stream(stream)>>>(z_dev, h.n, h.base, h.nb, th, tf, out);
     } else if (h.code_bits == 3) {
       z_decode_kernel<3><<<grid, threads, 0, as_stream(stream)>>>(z_dev, h.n, h.base, h.nb, th, tf, out);
     } else {

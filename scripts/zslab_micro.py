@@ -38,18 +38,22 @@ def main():
         for i in range(3):
             ps.check(lib.ps_zslab_decode(C.c_void_p(zd.data_ptr()), z.ctypes.data, C.c_void_p(outs[i].data_ptr()),
                                          C.c_void_p(s.cuda_stream)))
-        a, b = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
-        a.record()
-        iters = 20
-        for i in range(iters):
-            ps.check(lib.ps_zslab_decode(C.c_void_p(zd.data_ptr()), z.ctypes.data, C.c_void_p(outs[i % 3].data_ptr()),
-                                         C.c_void_p(s.cuda_stream)))
-        b.record()
-        torch.cuda.synchronize()
-        us = a.elapsed_time(b) * 1e3 / iters
-        assert np.array_equal(outs[0].cpu().numpy().view(np.uint16), slab)
-        print(json.dumps({"bits": int(bits), "tiled": tiled, "z_bytes": int(nb.value), "us": us,
-                          "hbm_gbs": (nb.value + 2 * n) / (us * 1e-6) / 1e9}))
+        for ver in os.environ.get("ZMICRO_VERSIONS", "4").split(","):  # PS_ZDECODE A/B, same process
+            os.environ["PS_ZDECODE"] = ver
+            for o in outs:
+                o.zero_()
+            a, b = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+            a.record()
+            iters = 20
+            for i in range(iters):
+                ps.check(lib.ps_zslab_decode(C.c_void_p(zd.data_ptr()), z.ctypes.data,
+                                             C.c_void_p(outs[i % 3].data_ptr()), C.c_void_p(s.cuda_stream)))
+            b.record()
+            torch.cuda.synchronize()
+            us = a.elapsed_time(b) * 1e3 / iters
+            assert np.array_equal(outs[0].cpu().numpy().view(np.uint16), slab)
+            print(json.dumps({"bits": int(bits), "tiled": tiled, "version": ver, "z_bytes": int(nb.value), "us": us,
+                              "hbm_gbs": (nb.value + 2 * n) / (us * 1e-6) / 1e9}), flush=True)
 
 
 if __name__ == "__main__":

@@ -61,6 +61,34 @@ def test_zslab_roundtrip_bit_exact(torch_cuda, case, zbits):
     np.testing.assert_array_equal(out.cpu().numpy().view(np.uint16), slab)
 
 
+@pytest.mark.parametrize("case", ["dense_escapes", "high_base"])
+@pytest.mark.parametrize("version", ["1", "3", "4"])
+def test_zslab_decoder_versions_edge_blocks(torch_cuda, zbits, case, version, monkeypatch):
+    """Every device decoder (PS_ZDECODE = 1 / 3 / 4 (default)) on the blocks that take
+    their slow paths: > 256 escapes in one 1024-value block (ranks past the shared-memory
+    staging read global memory), and a base exponent so high that base + escape code
+    reaches 256 (v4 hands those slabs to v3)."""
+    torch = torch_cuda
+    lib = ps.load()
+    H, F = 256, 256
+    slab = np.empty(3 * H * F, np.uint16)
+    ps.check(lib.ps_init_expert_slab_host(slab.ctypes.data, H, F, 4, 0, 3))
+    rng = np.random.default_rng(7)
+    if case == "dense_escapes":  # blocks 3..6 all-random: ~97 % of their values escape
+        slab[3 * 1024:7 * 1024] = rng.integers(0, 65536, 4 * 1024, dtype=np.uint16)
+    else:  # exponents 251..255 (255: inf / NaN bit patterns): the window must reach 255
+        e = rng.integers(251, 256, slab.size).astype(np.uint16)
+        slab[:] = (slab & 0x807F) | (e << 7)
+    z = _encode(slab)
+    monkeypatch.setenv("PS_ZDECODE", version)
+    zd = torch.as_tensor(z, device="cuda")
+    out = torch.zeros(slab.size, dtype=torch.int16, device="cuda")
+    ps.check(lib.ps_zslab_decode(C.c_void_p(zd.data_ptr()), z.ctypes.data, C.c_void_p(out.data_ptr()),
+                                 C.c_void_p(torch.cuda.current_stream().cuda_stream)))
+    torch.cuda.synchronize()
+    np.testing.assert_array_equal(out.cpu().numpy().view(np.uint16), slab)
+
+
 @pytest.mark.parametrize("escapes", [False, True])
 def test_tiled_zslab_decodes_to_row_major(torch_cuda, zbits, escapes):
     """A z-slab of a slab in the lane's tile layout (ps_host_slab_tile +
