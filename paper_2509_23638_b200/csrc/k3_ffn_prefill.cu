@@ -35,6 +35,7 @@
 #include <cstdlib>
 #include <cstring>
 #include <mutex>
+#include <unordered_map>
 #include <vector>
 
 #include "device_common.cuh"
@@ -628,6 +629,13 @@ struct TnParams {
   TnPhase ph[2];                    // 0 = gate_up, 1 = down
   unsigned* done;                   // [n_experts] gate_up signals (this map-ring slot's counters)
   unsigned target[kMaxExperts];     // done[e] value once all of e's gate_up tiles are stored
+  // Tile order: segments of (phase, entry) — gu(0..D-1), then gu(e), dn(e - D) for e >= D,
+  // then the last D down segments (D >= n: every gate_up tile first, the default). A down
+  // segment trailing its gate_up by a few experts finds its h rows still in L2, but its
+  // acquire may wait (profiles/r02_prefill_tn.md). seg_code = entry | phase << 16.
+  int n_seg;
+  int seg_start[2 * kMaxExperts + 1];
+  int seg_code[2 * kMaxExperts];
 };
 
 struct TnTile {
@@ -637,17 +645,16 @@ struct TnTile {
 
 __device__ __forceinline__ TnTile tn_tile(const TnParams& p, int t) {
   TnTile c;
-  const int t0 = p.ph[0].tile_start[p.n_experts];
-  c.phase = t < t0 ? 0 : 1;
-  if (c.phase) t -= t0;
-  const int* ts = p.ph[c.phase].tile_start;
-  int lo = 0, hi = p.n_experts - 1;
+  int lo = 0, hi = p.n_seg - 1;
   while (lo < hi) {
     const int mid = (lo + hi + 1) >> 1;
-    if (ts[mid] <= t) lo = mid;
+    if (p.seg_start[mid] <= t) lo = mid;
     else hi = mid - 1;
   }
-  const int local = t - ts[lo], tt = p.t_tiles[lo];
+  const int local = t - p.seg_start[lo];
+  c.phase = p.seg_code[lo] >> 16;
+  lo = p.seg_code[lo] & 0xffff;
+  const int tt = p.t_tiles[lo];
   const int t_tile = local % tt;  // token tiles fastest: concurrent tiles share the weight rows
   c.entry = lo;
   c.n_tile = local / tt;
@@ -678,7 +685,7 @@ ffn_prefill_tn_kernel(const __grid_constant__ TnParams p) {
   const uint32_t rank = cluster_rank();
   const bool leader = rank == 0;
   const int pair = blockIdx.x >> 1, n_pairs = gridDim.x >> 1;
-  const int n_tiles = p.ph[0].tile_start[p.n_experts] + p.ph[1].tile_start[p.n_experts];
+  const int n_tiles = p.seg_start[p.n_seg];
 
   if (warp == 0 && lane == 0) {
     for (int s = 0; s < kTnStages; ++s) {
@@ -900,7 +907,7 @@ EncodeFn encode_fn() {
 }
 
 // 2D bf16 row-major [rows, cols] tensor map with a {64, box_rows} box, 128B swizzle.
-CUtensorMap make_map(const void* base, uint64_t rows, uint64_t cols, uint32_t box_rows) {
+CUtensorMap encode_map(const void* base, uint64_t rows, uint64_t cols, uint32_t box_rows) {
   CUtensorMap m;
   cuuint64_t dims[2] = {cols, rows};
   cuuint64_t strides[1] = {cols * 2};
@@ -910,6 +917,32 @@ CUtensorMap make_map(const void* base, uint64_t rows, uint64_t cols, uint32_t bo
                            CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_128B,
                            CU_TENSOR_MAP_L2_PROMOTION_L2_256B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
   if (r != CUDA_SUCCESS) fail(PS_ECUDA, "cuTensorMapEncodeTiled failed: " + std::to_string(static_cast<int>(r)));
+  return m;
+}
+
+// Tensor maps are pure functions of (base, rows, cols, box): resident slabs, staging slots
+// and the chunk buffers keep their addresses, so a prefill launch looks its 4 maps per
+// expert up instead of encoding them (264 cuTensorMapEncodeTiled calls per DeepSeek layer
+// kept the GPU idle ~100 us per layer). Callers hold the prefill mutex.
+CUtensorMap make_map(const void* base, uint64_t rows, uint64_t cols, uint32_t box_rows) {
+  struct Key {
+    const void* base;
+    uint64_t rows, cols;
+    uint32_t box;
+    bool operator==(const Key& o) const { return base == o.base && rows == o.rows && cols == o.cols && box == o.box; }
+  };
+  struct Hash {
+    size_t operator()(const Key& k) const {
+      return std::hash<const void*>()(k.base) ^ (k.rows * 0x9e3779b97f4a7c15ull) ^ (k.cols << 20) ^ k.box;
+    }
+  };
+  static std::unordered_map<Key, CUtensorMap, Hash> cache;
+  const Key key{base, rows, cols, box_rows};
+  auto it = cache.find(key);
+  if (it != cache.end()) return it->second;
+  if (cache.size() >= 16384) cache.clear();  // bounded: buffers of engines long gone
+  const CUtensorMap m = encode_map(base, rows, cols, box_rows);
+  cache.emplace(key, m);
   return m;
 }
 
@@ -974,7 +1007,7 @@ void launch_tn(TnParams& p, cudaStream_t s) {
     if (clusters < 1) fail(PS_ECUDA, "ffn_prefill_tn_kernel: no 2-CTA cluster fits on this device");
     max_pairs = std::min(clusters, kNumSMs / 2);
   }
-  const int tiles = p.ph[0].tile_start[p.n_experts] + p.ph[1].tile_start[p.n_experts];
+  const int tiles = p.seg_start[p.n_seg];
   if (tiles == 0) return;
   const int grid = 2 * std::min(tiles, max_pairs);
   ffn_prefill_tn_kernel<<<grid, kThreads, kTnSmemBytes, s>>>(p);
@@ -1076,6 +1109,34 @@ extern "C" ps_status ps_expert_ffn_prefill(const ps_expert_group* group, const i
       if (n == 0) return;
       tp.n_experts = n;
       tp.done = done_dev + slot * kMaxExperts;
+      // PS_TN_LAG: experts between a gate_up segment and its down segment. Default: all
+      // gate_up tiles first (DeepSeek shape, same process: lag 10 277 us, all-first 283,
+      // lag 6 296, lag 0 554 — the acquires wait; Mixtral: all-first best), knob kept for A/B.
+      const int lag = [] {
+        const char* v = std::getenv("PS_TN_LAG");
+        const int d = v ? std::atoi(v) : kMaxExperts;
+        return d < 0 ? 0 : d;
+      }();
+      // phases: 3 = both (interleaved with lag D), 1 = gate_up only, 2 = down only
+      auto build_segments = [&](TnParams& q, int phases) {
+        const int D = std::min(lag, n);
+        int t = 0;
+        q.n_seg = 0;
+        auto seg = [&](int ph, int e) {
+          if (!(phases & (1 << ph))) return;
+          q.seg_start[q.n_seg] = t;
+          q.seg_code[q.n_seg] = e | (ph << 16);
+          t += q.ph[ph].tile_start[e + 1] - q.ph[ph].tile_start[e];
+          ++q.n_seg;
+        };
+        for (int e = 0; e < n; ++e) {
+          seg(0, e);
+          if (e >= D) seg(1, e - D);
+        }
+        for (int e = n - D; e < n; ++e) seg(1, e);
+        q.seg_start[q.n_seg] = t;
+      };
+      build_segments(tp, 3);
       maps_host[0] = make_map(x_perm, static_cast<uint64_t>(total_rows), H, 128);
       maps_host[1] = make_map(h_perm, static_cast<uint64_t>(total_rows), F, 128);
       PS_CUDA(cudaMemcpyAsync(maps_dev, maps_host, sizeof(CUtensorMap) * (2 + 4 * G), cudaMemcpyHostToDevice, s));
@@ -1092,8 +1153,8 @@ extern "C" ps_status ps_expert_ffn_prefill(const ps_expert_group* group, const i
       const char* merge = std::getenv("PS_TN_MERGE");  // A/B knob: 0 runs the phases as two launches
       if (merge && merge[0] == '0') {
         TnParams second = tp;
-        for (int i = 0; i <= n; ++i) tp.ph[1].tile_start[i] = 0;
-        for (int i = 0; i <= n; ++i) second.ph[0].tile_start[i] = 0;
+        build_segments(tp, 1);
+        build_segments(second, 2);
         launch_tn(tp, s);
         launch_tn(second, s);
       } else {
