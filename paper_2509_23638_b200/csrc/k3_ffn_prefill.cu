@@ -33,8 +33,10 @@
 #include <algorithm>
 #include <atomic>
 #include <cstdlib>
+#include <cstdio>
 #include <cstring>
 #include <mutex>
+#include <string>
 #include <unordered_map>
 #include <vector>
 
@@ -605,7 +607,8 @@ constexpr int kTnABytes = 128 * kBK * 2;                 // 16 KiB of weight row
 constexpr int kTnBMaxBytes = 128 * kBK * 2;              // <= 128 token rows per CTA
 constexpr int kTnStageBytes = kTnABytes + kTnBMaxBytes;  // 32 KiB
 constexpr int kTnXchgBytes = 2 * 2 * 2 * 16 * 32 * 4;    // gate <-> up hand-off: 2 bufs x 2 pairs x 2 senders x 16 x 32
-constexpr int kTnSmemBytes = kTnStages * kTnStageBytes + kTnXchgBytes + 1024 + 256;
+constexpr int kTnStageOutBytes = 4 * 32 * 32 * 4;         // y staging: 4 epilogue warps x 32 tokens x 32 features f32
+constexpr int kTnSmemBytes = kTnStages * kTnStageBytes + kTnXchgBytes + kTnStageOutBytes + 1024 + 256;
 constexpr int kTnMaxN = 256;
 constexpr uint32_t kTnSignalsPerTile = 2 * 4;            // epilogue warps of both CTAs
 
@@ -618,6 +621,7 @@ struct TnPhase {
   const CUtensorMap* w_maps;        // [n_experts]: [Wg; Wu] box {64, 64} or Wd box {64, 128}
   void* out;                        // h_perm (bf16) or y_perm (f32)
   int out_ld;
+  const CUtensorMap* out_maps;      // down: [n_experts] y rows of the entry, box {32 features, 32 tokens}
 };
 
 struct TnParams {
@@ -675,7 +679,8 @@ ffn_prefill_tn_kernel(const __grid_constant__ TnParams p) {
   extern __shared__ __align__(1024) uint8_t smem_raw[];
   uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
   float* xchg = reinterpret_cast<float*>(smem + kTnStages * kTnStageBytes);  // [2][2][2][16][32]
-  uint64_t* full_bar = reinterpret_cast<uint64_t*>(smem + kTnStages * kTnStageBytes + kTnXchgBytes);
+  float* ystage = reinterpret_cast<float*>(smem + kTnStages * kTnStageBytes + kTnXchgBytes);  // [4][32][32]
+  uint64_t* full_bar = reinterpret_cast<uint64_t*>(smem + kTnStages * kTnStageBytes + kTnXchgBytes + kTnStageOutBytes);
   uint64_t* empty_bar = full_bar + kTnStages;
   uint64_t* tfull_bar = empty_bar + kTnStages;
   uint64_t* tempty_bar = tfull_bar + 2;
@@ -808,6 +813,10 @@ ffn_prefill_tn_kernel(const __grid_constant__ TnParams p) {
     uint32_t aphase = 0;
     int buf = 0;  // hand-off buffer: one barrier per chunk orders its reuse two chunks later
     const uint32_t xchg_s = smem_u32(xchg);
+    if (p.ph[1].out_maps)  // the y maps (TMA stores) live in a reused ring slot too
+      for (int i = lane; i < p.n_experts; i += 32)
+        asm volatile("fence.proxy.tensormap::generic.acquire.gpu [%0], 128;" ::"l"(p.ph[1].out_maps + i) : "memory");
+    __syncwarp();
     for (int t = pair; t < n_tiles; t += n_pairs) {
       const TnTile tc = tn_tile(p, t);
       const TnPhase& ph = p.ph[tc.phase];
@@ -859,17 +868,33 @@ ffn_prefill_tn_kernel(const __grid_constant__ TnParams p) {
         if (lane == 0)
           asm volatile("red.release.gpu.global.add.u32 [%0], 1;" ::"l"(p.done + tc.entry) : "memory");
       } else {
-        const int hrow = tc.n_tile * 256 + static_cast<int>(rank) * 128 + quarter * 32 + lane;
-        float* out = static_cast<float*>(ph.out) + row_base * ph.out_ld + hrow;
+        // y rows leave through shared memory and one TMA store per 32x32 chunk and warp
+        // (scalar global stores, 128 B per warp instruction, cost ~12 % of a DeepSeek-shape
+        // launch): lane l writes feature column l of the warp's [32 tokens][32 features]
+        // tile, lane 0 stores it; rows past the expert's m_e are clipped by the entry's map.
+        const CUtensorMap* ymap = ph.out_maps + tc.entry;
+        const int h0 = tc.n_tile * 256 + static_cast<int>(rank) * 128 + quarter * 32;
+        const uint32_t ys = smem_u32(ystage) + static_cast<uint32_t>(quarter) * 32u * 32u * 4u;
 #pragma unroll 1
         for (int c = 0; c < tc.n; c += 32) {
           uint32_t v[32];
           tmem_ld32(tbase + c, v);
+          if (lane == 0) asm volatile("cp.async.bulk.wait_group.read 0;" ::: "memory");  // staging free
+          __syncwarp();
           tmem_ld_wait();
-          const int nj = min(32, m_left - c);
 #pragma unroll
           for (int j = 0; j < 32; ++j)
-            if (j < nj) out[static_cast<size_t>(c + j) * ph.out_ld] = __uint_as_float(v[j]);
+            asm volatile("st.shared.b32 [%0], %1;" ::"r"(ys + static_cast<uint32_t>(j * 128 + lane * 4)), "r"(v[j])
+                         : "memory");
+          asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+          __syncwarp();
+          if (lane == 0) {
+            asm volatile(
+                "cp.async.bulk.tensor.2d.global.shared::cta.bulk_group [%0, {%1, %2}], [%3];" ::"l"(ymap), "r"(h0),
+                "r"(tc.tok0 + c), "r"(ys)
+                : "memory");
+            asm volatile("cp.async.bulk.commit_group;" ::: "memory");
+          }
         }
       }
       tc_fence_before();
@@ -877,6 +902,7 @@ ffn_prefill_tn_kernel(const __grid_constant__ TnParams p) {
       as ^= 1;
       if (as == 0) aphase ^= 1;
     }
+    if (lane == 0) asm volatile("cp.async.bulk.wait_group 0;" ::: "memory");  // y stores complete
   }
   tc_fence_before();
   __syncthreads();
@@ -946,13 +972,36 @@ CUtensorMap make_map(const void* base, uint64_t rows, uint64_t cols, uint32_t bo
   return m;
 }
 
+// fp32 row-major [rows, cols] map with a {box_cols, box_rows} box, no swizzle (the y
+// output tiles of the token-N kernel, TMA-stored from shared memory; cached like make_map).
+CUtensorMap make_map_f32(const void* base, uint64_t rows, uint64_t cols, uint32_t box_cols, uint32_t box_rows) {
+  static std::unordered_map<std::string, CUtensorMap> cache;
+  char k[96];
+  std::snprintf(k, sizeof(k), "%p/%llu/%llu/%u/%u", base, static_cast<unsigned long long>(rows),
+                static_cast<unsigned long long>(cols), box_cols, box_rows);
+  auto it = cache.find(k);
+  if (it != cache.end()) return it->second;
+  if (cache.size() >= 16384) cache.clear();
+  CUtensorMap m;
+  cuuint64_t dims[2] = {cols, rows};
+  cuuint64_t strides[1] = {cols * 4};
+  cuuint32_t box[2] = {box_cols, box_rows};
+  cuuint32_t estr[2] = {1, 1};
+  CUresult r = encode_fn()(&m, CU_TENSOR_MAP_DATA_TYPE_FLOAT32, 2, const_cast<void*>(base), dims, strides, box, estr,
+                           CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_NONE,
+                           CU_TENSOR_MAP_L2_PROMOTION_NONE, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+  if (r != CUDA_SUCCESS) fail(PS_ECUDA, "cuTensorMapEncodeTiled (f32) failed: " + std::to_string(static_cast<int>(r)));
+  cache.emplace(k, m);
+  return m;
+}
+
 // Ring of per-launch weight tensor-map slots (device array + pinned staging). A slot is
 // rewritten only after the event recorded behind its last kernels has completed, so no
 // launch ever waits on the host for the GPU (on-demand experts are launched while their
 // copies are still in flight).
 struct MapRing {
   static constexpr int kSlots = 64;
-  static constexpr int kPerSlot = 4 * kMaxExperts + 2;  // [a_x, a_h, gate_up maps, down maps, (token-N: x_last, h_last)]
+  static constexpr int kPerSlot = 5 * kMaxExperts + 2;  // [a_x, a_h, gate_up maps, down maps, (token-N: x_last, h_last)]
   CUtensorMap* dev = nullptr;
   CUtensorMap* host = nullptr;
   cudaEvent_t ev[kSlots] = {};
@@ -1084,6 +1133,7 @@ extern "C" ps_status ps_expert_ffn_prefill(const ps_expert_group* group, const i
       CUtensorMap* wdn = maps_host + 2 + G;
       CUtensorMap* xl = maps_host + 2 + 2 * G;
       CUtensorMap* hl = maps_host + 2 + 3 * G;
+      CUtensorMap* ym = maps_host + 2 + 4 * G;
       unsigned* shadow = done_host.data() + slot * kMaxExperts;
       int n = 0;
       for (int i = 0; i < G; ++i) {
@@ -1098,6 +1148,7 @@ extern "C" ps_status ps_expert_ffn_prefill(const ps_expert_group* group, const i
         const uint32_t half = static_cast<uint32_t>(((rem + 15) & ~15) / 2);
         xl[n] = make_map(x_perm, static_cast<uint64_t>(total_rows), H, half);
         hl[n] = make_map(h_perm, static_cast<uint64_t>(total_rows), F, half);
+        ym[n] = make_map_f32(y_perm + static_cast<size_t>(offsets_host[e]) * H, static_cast<uint64_t>(m), H, 32, 32);
         tp.t_tiles[n] = tt;
         tp.row0[n] = offsets_host[e];
         tp.rows[n] = m;
@@ -1139,7 +1190,8 @@ extern "C" ps_status ps_expert_ffn_prefill(const ps_expert_group* group, const i
       build_segments(tp, 3);
       maps_host[0] = make_map(x_perm, static_cast<uint64_t>(total_rows), H, 128);
       maps_host[1] = make_map(h_perm, static_cast<uint64_t>(total_rows), F, 128);
-      PS_CUDA(cudaMemcpyAsync(maps_dev, maps_host, sizeof(CUtensorMap) * (2 + 4 * G), cudaMemcpyHostToDevice, s));
+      PS_CUDA(cudaMemcpyAsync(maps_dev, maps_host, sizeof(CUtensorMap) * (2 + 5 * G), cudaMemcpyHostToDevice, s));
+      tp.ph[1].out_maps = maps_dev + 2 + 4 * G;
       tp.ph[0].tok_full = maps_dev;
       tp.ph[1].tok_full = maps_dev + 1;
       tp.ph[0].w_maps = maps_dev + 2;
