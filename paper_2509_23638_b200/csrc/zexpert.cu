@@ -72,6 +72,17 @@ __device__ __forceinline__ uint32_t z_code_pair(const uint32_t (&cw)[BITS + 1], 
 // Row-major start of the 32-value tile row at tiled index v, in 32-bit arithmetic
 // (z_untile's 64-bit division is a ~100-instruction subroutine; the host checks
 // n = 3HF < 2^32 for tiled slabs).
+// z_untile32 with the two divisions by K/32 done as multiply-highs: q = umulhi(n, m),
+// m = ceil(2^32 / d), exact for n * d < 2^32 (n = tile index < 3HF/512 < 2^23, d <= 2^11).
+__device__ __forceinline__ uint32_t z_untile32m(uint32_t v, uint32_t H, uint32_t F, uint32_t mh, uint32_t mf) {
+  const uint32_t fh = F * H;
+  const uint32_t base = v < fh ? 0u : (v < 2u * fh ? fh : 2u * fh);
+  const bool gu = v < 2u * fh;
+  const uint32_t K = gu ? H : F;
+  const uint32_t t = v - base, tile = t >> 9, i = (t >> 5) & 15u, nkb = K >> 5;
+  const uint32_t rb = __umulhi(tile, gu ? mh : mf), kb = tile - rb * nkb;
+  return base + (rb * 16u + i) * K + kb * 32u;
+}
 __device__ __forceinline__ uint32_t z_untile32(uint32_t v, uint32_t H, uint32_t F) {
   const uint32_t fh = F * H;
   const uint32_t base = v < fh ? 0u : (v < 2u * fh ? fh : 2u * fh);
@@ -220,6 +231,8 @@ template <int BITS>
 __global__ void __launch_bounds__(256, 4)
 z_decode_kernel_v4(const uint8_t* __restrict__ z, uint64_t n, uint32_t base, uint32_t nb, uint32_t tile_h,
                    uint32_t tile_f, uint16_t* __restrict__ out) {
+  const uint32_t mh = tile_h ? static_cast<uint32_t>((0x100000000ull + (tile_h >> 5) - 1) / (tile_h >> 5)) : 0u;
+  const uint32_t mf = tile_f ? static_cast<uint32_t>((0x100000000ull + (tile_f >> 5) - 1) / (tile_f >> 5)) : 0u;
   __shared__ uint8_t s_esc[8][kZEscStage];
   __shared__ __align__(16) uint4 s_out[8][128];
   const uint64_t n_pad = static_cast<uint64_t>(nb) * kZBlock;
@@ -234,26 +247,46 @@ z_decode_kernel_v4(const uint8_t* __restrict__ z, uint64_t n, uint32_t base, uin
   uint4* so = s_out[warp];
   const uint32_t so_s = static_cast<uint32_t>(__cvta_generic_to_shared(so));
   auto chunk = [](int ln, int q) { return ln * 4 + (q ^ ((ln >> 1) & 3)); };
+  // Software pipeline: block b is assembled while the lo/code words AND the first 64
+  // escape bytes of block b + W are in flight, and the escape offsets of block b + 2W
+  // (the escape loads need their block's offsets: a same-iteration dependent load
+  // stalled on the offset, profiles/r02_z_decode.md).
   struct Blk {
     uint4 l0, l1;
     uint32_t cw[BITS];
     uint32_t eoff, eend;
+    uint32_t e0, e1;  // escape bytes eoff + lane, eoff + 32 + lane (when present)
   };
-  auto fetch = [&](uint32_t bb, Blk& k) {
+  auto fetch = [&](uint32_t bb, uint32_t eo, uint32_t ee, Blk& k) {
     const uint64_t seg = static_cast<uint64_t>(bb) * 32 + lane;
     k.l0 = __ldg(reinterpret_cast<const uint4*>(lo + seg * 32));
     k.l1 = __ldg(reinterpret_cast<const uint4*>(lo + seg * 32 + 16));
 #pragma unroll
     for (int q = 0; q < BITS; ++q) k.cw[q] = __ldg(codes + seg * BITS + q);
-    k.eoff = __ldg(esc_off + bb);
-    k.eend = __ldg(esc_off + bb + 1);
+    k.eoff = eo;
+    k.eend = ee;
+    k.e0 = eo + lane < ee ? __ldg(esc + eo + lane) : 0u;
+    k.e1 = eo + 32 + lane < ee ? __ldg(esc + eo + 32 + lane) : 0u;
   };
   uint32_t b = (blockIdx.x * blockDim.x + threadIdx.x) >> 5;
   Blk nxt{};
-  if (b < nb) fetch(b, nxt);
+  uint32_t o2_lo = 0, o2_hi = 0;  // escape offsets of block b + W (then of b + 2W)
+  if (b < nb) {
+    fetch(b, __ldg(esc_off + b), __ldg(esc_off + b + 1), nxt);
+    if (b + warps < nb) {
+      o2_lo = __ldg(esc_off + b + warps);
+      o2_hi = __ldg(esc_off + b + warps + 1);
+    }
+  }
   for (; b < nb; b += warps) {
     const Blk cur = nxt;
-    if (b + warps < nb) fetch(b + warps, nxt);
+    if (b + warps < nb) {
+      fetch(b + warps, o2_lo, o2_hi, nxt);
+      if (b + 2 * warps < nb) {
+        o2_lo = __ldg(esc_off + b + 2 * warps);
+        o2_hi = __ldg(esc_off + b + 2 * warps + 1);
+      }
+    }
     const uint64_t vb = static_cast<uint64_t>(b) * kZBlock;
     const uint64_t v0 = vb + 32u * lane;
     uint32_t cw[BITS + 1];
@@ -275,7 +308,9 @@ z_decode_kernel_v4(const uint8_t* __restrict__ z, uint64_t n, uint32_t base, uin
     if (cur.eend != cur.eoff) {  // escapes in this block (warp-uniform)
       const uint32_t eoff = cur.eoff;
       const uint32_t n_stage = min(cur.eend - eoff, static_cast<uint32_t>(kZEscStage));
-      for (uint32_t k = lane; k < n_stage; k += 32) se[k] = esc[eoff + k];
+      se[lane] = static_cast<uint8_t>(cur.e0);  // prefetched with the block
+      se[32 + lane] = static_cast<uint8_t>(cur.e1);
+      for (uint32_t k = 64 + lane; k < n_stage; k += 32) se[k] = esc[eoff + k];  // > 64 escapes: rare
       __syncwarp();
       // per-value escape masks: m[0] codes 0-10 at bit 3i (BITS 3) ..., see v3's word tricks
       uint32_t m[3];
@@ -370,7 +405,7 @@ z_decode_kernel_v4(const uint8_t* __restrict__ z, uint64_t n, uint32_t base, uin
     }
     __syncwarp();
     if (vb + kZBlock <= n) {
-      const uint64_t my_off = tile_h ? static_cast<uint64_t>(z_untile32(static_cast<uint32_t>(v0), tile_h, tile_f))
+      const uint64_t my_off = tile_h ? static_cast<uint64_t>(z_untile32m(static_cast<uint32_t>(v0), tile_h, tile_f, mh, mf))
                                      : v0;
 #pragma unroll
       for (int rr = 0; rr < 4; ++rr) {
