@@ -40,6 +40,10 @@
 #include "zslab_format.hpp"
 
 namespace ps {
+int prefill_launches_per_call();  // k3_ffn_prefill.cu
+}  // namespace ps
+
+namespace ps {
 void plan_layer(const ps_layer_inputs& in, ps_policy pol, ps_layer_plan& out);
 }
 
@@ -464,9 +468,10 @@ void ffn(ps_engine_s& e, const ps_expert_group& g, const int32_t* counts_host, i
   if (e.prefill_mode && max_m >= 128 && e.H % 256 == 0 && e.F % 128 == 0) {
     s = ps_expert_ffn_prefill(&g, counts_host, src.offsets_host, e.x_perm, src.rows, e.H, e.F, e.hbuf, e.y_part,
                               e.sc);
-    e.st.tc_launches += 2;
-    e.st.ffn_launches += 2;  // gate_up + down
-    e.st.kernel_launches += 2;
+    const int n_launch = prefill_launches_per_call();  // gate_up + down: one launch (token-N) or two
+    e.st.tc_launches += n_launch;
+    e.st.ffn_launches += n_launch;
+    e.st.kernel_launches += n_launch;
   } else {
     s = ps_expert_ffn(&g, counts_host, src.offsets_dev, src.perm_dev, src.k, src.x, e.H, e.F, e.hbuf, e.y_part,
                       e.step_split, src.rows, e.sc);

@@ -33,10 +33,8 @@
 #include <algorithm>
 #include <atomic>
 #include <cstdlib>
-#include <cstdio>
 #include <cstring>
 #include <mutex>
-#include <string>
 #include <unordered_map>
 #include <vector>
 
@@ -975,11 +973,22 @@ CUtensorMap make_map(const void* base, uint64_t rows, uint64_t cols, uint32_t bo
 // fp32 row-major [rows, cols] map with a {box_cols, box_rows} box, no swizzle (the y
 // output tiles of the token-N kernel, TMA-stored from shared memory; cached like make_map).
 CUtensorMap make_map_f32(const void* base, uint64_t rows, uint64_t cols, uint32_t box_cols, uint32_t box_rows) {
-  static std::unordered_map<std::string, CUtensorMap> cache;
-  char k[96];
-  std::snprintf(k, sizeof(k), "%p/%llu/%llu/%u/%u", base, static_cast<unsigned long long>(rows),
-                static_cast<unsigned long long>(cols), box_cols, box_rows);
-  auto it = cache.find(k);
+  struct Key {
+    const void* base;
+    uint64_t rows, cols;
+    uint32_t bc, br;
+    bool operator==(const Key& o) const {
+      return base == o.base && rows == o.rows && cols == o.cols && bc == o.bc && br == o.br;
+    }
+  };
+  struct Hash {
+    size_t operator()(const Key& k) const {
+      return std::hash<const void*>()(k.base) ^ (k.rows * 0x9e3779b97f4a7c15ull) ^ (k.cols << 20) ^ (k.bc << 8) ^ k.br;
+    }
+  };
+  static std::unordered_map<Key, CUtensorMap, Hash> cache;
+  const Key key{base, rows, cols, box_cols, box_rows};
+  auto it = cache.find(key);
   if (it != cache.end()) return it->second;
   if (cache.size() >= 16384) cache.clear();
   CUtensorMap m;
@@ -991,7 +1000,7 @@ CUtensorMap make_map_f32(const void* base, uint64_t rows, uint64_t cols, uint32_
                            CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_NONE,
                            CU_TENSOR_MAP_L2_PROMOTION_NONE, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
   if (r != CUDA_SUCCESS) fail(PS_ECUDA, "cuTensorMapEncodeTiled (f32) failed: " + std::to_string(static_cast<int>(r)));
-  cache.emplace(k, m);
+  cache.emplace(key, m);
   return m;
 }
 
@@ -1087,6 +1096,14 @@ void launch(PrefillParams& p, cudaStream_t s) {
 }
 
 }  // namespace
+
+// Kernel launches one ps_expert_ffn_prefill call makes (engine launch statistics).
+int prefill_launches_per_call() {
+  const int mode = prefill_mode().load();
+  const char* merge = std::getenv("PS_TN_MERGE");
+  return (mode == 2 || mode == 3) && !(merge && merge[0] == '0') ? 1 : 2;
+}
+
 }  // namespace ps
 
 using namespace ps;

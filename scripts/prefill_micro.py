@@ -100,12 +100,19 @@ def main():
         b.synchronize()
         ts.append(a.elapsed_time(b))
     ms = float(np.median(ts))
+    import time
+    t0 = time.perf_counter()
+    for _ in range(20):
+        run()
+    host_us = (time.perf_counter() - t0) / 20 * 1e6
+    torch.cuda.synchronize()
     flops = 2.0 * rows * 3 * H * F
     peaks = ROOT / "MEASURED_PEAKS.json"
     peak = json.loads(peaks.read_text())["bf16_tflops"] if peaks.exists() else 1590.0
     print(json.dumps({"H": H, "F": F, "E": E, "k": k, "T": T, "rows": rows, "ms": ms,
                       "tflops": flops / ms / 1e9, "frac_bf16_peak": flops / ms / 1e9 / peak,
-                      "m_per_expert": float(counts.mean()), "kernel": args.kernel}))
+                      "m_per_expert": float(counts.mean()), "kernel": args.kernel,
+                      "host_enqueue_us": host_us}))
 
 
 if __name__ == "__main__":
