@@ -152,3 +152,43 @@ def test_engine_bench_config_vs_oracle(torch_cuda, executor):
         for l in range(spec.num_layers):
             rel = np.linalg.norm(ys[s][l] - y_ref[l]) / np.linalg.norm(y_ref[l])
             assert rel < BF16_RTOL, (s, l, rel)
+
+
+@pytest.mark.parametrize("budget,threads", [(1.0, 0), (0.5, 0), (0.5, -1)])
+def test_engine_deepseek_prefill_full_shape_vs_oracle(torch_cuda, budget, threads):
+    """BASELINE config 3 at full expert shape: 3 layers of DeepSeek-V2-Lite (H=2048,
+    F=1408, 64 routed experts top-6 + 2 shared), one 2048-token prefill chunk through the
+    engine (token-N tcgen05 kernel; all resident / 50 % budget with PCIe loads / + the
+    host lane). ids vs the reference router on every token, y vs the oracle on 40 tokens
+    per layer (the f64 oracle over all 2048 tokens would take minutes)."""
+    if threads < 0:
+        threads = _lane_threads()
+        if threads == 0:
+            pytest.skip("host has no AVX512_BF16 (no host expert lane)")
+    full = ps.spec_preset("deepseek")
+    spec = ps.desk_scale("deepseek", 3, 64, 2048)
+    spec.expert_bytes = full.expert_bytes  # F = 1408
+    F = ps.ffn_dim(spec)
+    assert F == 1408
+    B = 2048
+    cfg = ps.TraceGenConfig(*[ps.GROUP_DEFAULT_GEN[g] for g in ("input", "middle", "output")])
+    gate, hidden, follow, zipf = ps.trace_inputs(cfg, spec, B, 23)
+    with eng.Engine(spec, cfg, budget_fraction=budget, max_batch=B, weight_seed=2, gate=gate, trace_hidden=hidden,
+                    trace_follow=follow, n_shared=2, host_threads=threads, compress_host=budget < 1.0) as e:
+        y, ids = e.step_host(hidden, follow)
+        st = e.stats()
+    assert st["tc_launches"] > 0, st
+    if budget < 1.0:
+        assert st["ondemand_loads"] + st["prefetches_committed"] + st["cpu_experts"] > 0, st
+    if threads:
+        assert st["cpu_experts"] > 0, st
+    _, ref_w, ref_ids = orc.or_route_trace(gate, hidden, follow, zipf, spec.top_k)
+    agree = (np.sort(ids, -1) == np.sort(ref_ids.transpose(1, 0, 2), -1)).all(-1).mean()
+    assert agree >= 0.999, agree
+    sel = np.linspace(0, B - 1, 40).astype(int)
+    y_ref = orc.or_engine_reference(spec, F, 2, hidden[sel], ids[:, sel], ref_w.transpose(1, 0, 2)[:, sel],
+                                    n_shared=2)
+    for l in range(spec.num_layers):
+        for i, t in enumerate(sel):
+            rel = np.linalg.norm(y[l, t] - y_ref[l, i]) / np.linalg.norm(y_ref[l, i])
+            assert rel < BF16_RTOL, (l, t, rel)
