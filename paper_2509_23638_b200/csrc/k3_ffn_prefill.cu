@@ -610,19 +610,22 @@ constexpr int kTnSmemBytes = kTnStages * kTnStageBytes + kTnXchgBytes + kTnStage
 constexpr int kTnMaxN = 256;
 constexpr uint32_t kTnSignalsPerTile = 2 * 4;            // epilogue warps of both CTAs
 
+// Tensor maps live in a persistent device table (MapTable below: every map is a pure
+// function of its address, shape and box, written once, never modified), so a launch
+// passes table indices instead of uploading ~5 maps per expert.
 struct TnPhase {
   int K;                            // H (gate_up) or F (down)
   int n_tiles_n;                    // weight-row tiles per expert (F/128 gate_up, H/256 down)
   int tile_start[kMaxExperts + 1];  // prefix of this phase's tiles per entry
-  const CUtensorMap* tok_full;      // token operand (x_perm or h_perm), box {64, 128}
-  const CUtensorMap* tok_last;      // [n_experts]: box {64, N_last / 2} of the entry's last tile
-  const CUtensorMap* w_maps;        // [n_experts]: [Wg; Wu] box {64, 64} or Wd box {64, 128}
+  int w_idx[kMaxExperts];           // weights of entry i: [Wg; Wu] box {64, 64} or Wd box {64, 128}
+  int tok_idx[17];                  // token operand (x_perm or h_perm) with a {64, 8j}-row box, j = 1..16
   void* out;                        // h_perm (bf16) or y_perm (f32)
   int out_ld;
-  const CUtensorMap* out_maps;      // down: [n_experts] y rows of the entry, box {32 features, 32 tokens}
+  int out_idx;                      // down: y_perm as [total_rows, H] f32, box {32 features, 32 tokens}
 };
 
 struct TnParams {
+  const CUtensorMap* maps;          // the device map table
   int n_experts;
   int F, H;
   int t_tiles[kMaxExperts];         // token tiles per entry (ceil(m_e / 256))
@@ -713,11 +716,10 @@ ffn_prefill_tn_kernel(const __grid_constant__ TnParams p) {
 
   if (warp == 0) {
     for (int ph = 0; ph < 2; ++ph)
-      for (int i = lane; i <= 2 * p.n_experts; i += 32) {
-        const CUtensorMap* m = i == 0 ? p.ph[ph].tok_full
-                                      : (i <= p.n_experts ? p.ph[ph].tok_last + (i - 1)
-                                                          : p.ph[ph].w_maps + (i - 1 - p.n_experts));
-        if (m) asm volatile("fence.proxy.tensormap::generic.acquire.gpu [%0], 128;" ::"l"(m) : "memory");
+      for (int i = lane; i < p.n_experts + 16; i += 32) {
+        const int idx = i < p.n_experts ? p.ph[ph].w_idx[i] : p.ph[ph].tok_idx[i - p.n_experts + 1];
+        if (idx >= 0)
+          asm volatile("fence.proxy.tensormap::generic.acquire.gpu [%0], 128;" ::"l"(p.maps + idx) : "memory");
       }
     __syncwarp();
     if (lane == 0) {  // ---------------------------------------------- TMA producer (both CTAs)
@@ -726,9 +728,9 @@ ffn_prefill_tn_kernel(const __grid_constant__ TnParams p) {
       for (int t = pair; t < n_tiles; t += n_pairs) {
         const TnTile tc = tn_tile(p, t);
         const TnPhase& ph = p.ph[tc.phase];
-        const CUtensorMap* wmap = ph.w_maps + tc.entry;
-        const CUtensorMap* tmap = (tc.last && tc.n < kTnMaxN) ? ph.tok_last + tc.entry : ph.tok_full;
+        const CUtensorMap* wmap = p.maps + ph.w_idx[tc.entry];
         const int half = tc.n >> 1;
+        const CUtensorMap* tmap = p.maps + ph.tok_idx[half >> 3];
         const int trow = p.row0[tc.entry] + tc.tok0 + static_cast<int>(rank) * half;
         const uint32_t bytes = 2u * (kTnABytes + static_cast<uint32_t>(half) * kBK * 2);
         const int k_blocks = (ph.K + kBK - 1) / kBK;
@@ -811,9 +813,8 @@ ffn_prefill_tn_kernel(const __grid_constant__ TnParams p) {
     uint32_t aphase = 0;
     int buf = 0;  // hand-off buffer: one barrier per chunk orders its reuse two chunks later
     const uint32_t xchg_s = smem_u32(xchg);
-    if (p.ph[1].out_maps)  // the y maps (TMA stores) live in a reused ring slot too
-      for (int i = lane; i < p.n_experts; i += 32)
-        asm volatile("fence.proxy.tensormap::generic.acquire.gpu [%0], 128;" ::"l"(p.ph[1].out_maps + i) : "memory");
+    if (p.ph[1].out_idx >= 0 && lane == 0)  // the y map (TMA stores)
+      asm volatile("fence.proxy.tensormap::generic.acquire.gpu [%0], 128;" ::"l"(p.maps + p.ph[1].out_idx) : "memory");
     __syncwarp();
     for (int t = pair; t < n_tiles; t += n_pairs) {
       const TnTile tc = tn_tile(p, t);
@@ -869,14 +870,24 @@ ffn_prefill_tn_kernel(const __grid_constant__ TnParams p) {
         // y rows leave through shared memory and one TMA store per 32x32 chunk and warp
         // (scalar global stores, 128 B per warp instruction, cost ~12 % of a DeepSeek-shape
         // launch): lane l writes feature column l of the warp's [32 tokens][32 features]
-        // tile, lane 0 stores it; rows past the expert's m_e are clipped by the entry's map.
-        const CUtensorMap* ymap = ph.out_maps + tc.entry;
+        // tile, lane 0 stores it. A chunk with fewer than 32 of the expert's rows (its last)
+        // uses scalar stores: a full box would overwrite the next expert's rows.
+        const CUtensorMap* ymap = p.maps + ph.out_idx;
         const int h0 = tc.n_tile * 256 + static_cast<int>(rank) * 128 + quarter * 32;
         const uint32_t ys = smem_u32(ystage) + static_cast<uint32_t>(quarter) * 32u * 32u * 4u;
+        float* out = static_cast<float*>(ph.out) + row_base * ph.out_ld + h0 + lane;
 #pragma unroll 1
         for (int c = 0; c < tc.n; c += 32) {
           uint32_t v[32];
           tmem_ld32(tbase + c, v);
+          const int nj = min(32, m_left - c);
+          if (nj < 32) {
+            tmem_ld_wait();
+#pragma unroll
+            for (int j = 0; j < 32; ++j)
+              if (j < nj) out[static_cast<size_t>(c + j) * ph.out_ld] = __uint_as_float(v[j]);
+            continue;
+          }
           if (lane == 0) asm volatile("cp.async.bulk.wait_group.read 0;" ::: "memory");  // staging free
           __syncwarp();
           tmem_ld_wait();
@@ -889,7 +900,7 @@ ffn_prefill_tn_kernel(const __grid_constant__ TnParams p) {
           if (lane == 0) {
             asm volatile(
                 "cp.async.bulk.tensor.2d.global.shared::cta.bulk_group [%0, {%1, %2}], [%3];" ::"l"(ymap), "r"(h0),
-                "r"(tc.tok0 + c), "r"(ys)
+                "r"(static_cast<int>(row_base) + c), "r"(ys)
                 : "memory");
             asm volatile("cp.async.bulk.commit_group;" ::: "memory");
           }
@@ -1004,13 +1015,56 @@ CUtensorMap make_map_f32(const void* base, uint64_t rows, uint64_t cols, uint32_
   return m;
 }
 
+// Persistent device table of tensor maps for the token-N kernel. A map is a pure function
+// of (address, rows, cols, box, element size), so an entry is encoded once, copied to the
+// device once (in stream order, before the first kernel that uses it) and never modified:
+// launches pass indices. Capacity 32768 maps (4 MiB); a full table is an error (the
+// engines of a process use ~2 maps per resident slab plus a few dozen per chunk buffer).
+struct MapKey {
+  const void* base;
+  uint64_t rows, cols;
+  uint32_t box_cols, box_rows, esize;
+  bool operator==(const MapKey& o) const {
+    return base == o.base && rows == o.rows && cols == o.cols && box_cols == o.box_cols && box_rows == o.box_rows &&
+           esize == o.esize;
+  }
+};
+struct MapKeyHash {
+  size_t operator()(const MapKey& k) const {
+    return std::hash<const void*>()(k.base) ^ (k.rows * 0x9e3779b97f4a7c15ull) ^ (k.cols << 20) ^
+           (static_cast<size_t>(k.box_cols) << 40) ^ (static_cast<size_t>(k.box_rows) << 50) ^ k.esize;
+  }
+};
+struct MapTable {
+  static constexpr int kCap = 32768;
+  CUtensorMap* dev = nullptr;
+  CUtensorMap* host = nullptr;  // pinned mirror: entry i is written once, before its copy
+  int used = 0;
+  std::unordered_map<MapKey, int, MapKeyHash> index;
+  int get(const MapKey& k, cudaStream_t s) {
+    auto it = index.find(k);
+    if (it != index.end()) return it->second;
+    if (!dev) {
+      PS_CUDA(cudaMalloc(&dev, sizeof(CUtensorMap) * kCap));
+      PS_CUDA(cudaHostAlloc(&host, sizeof(CUtensorMap) * kCap, cudaHostAllocDefault));
+    }
+    if (used >= kCap) fail(PS_ERUNTIME, "ps_expert_ffn_prefill: tensor-map table full");
+    const int i = used++;
+    host[i] = k.esize == 4 ? make_map_f32(k.base, k.rows, k.cols, k.box_cols, k.box_rows)
+                           : encode_map(k.base, k.rows, k.cols, k.box_rows);
+    PS_CUDA(cudaMemcpyAsync(dev + i, host + i, sizeof(CUtensorMap), cudaMemcpyHostToDevice, s));
+    index.emplace(k, i);
+    return i;
+  }
+};
+
 // Ring of per-launch weight tensor-map slots (device array + pinned staging). A slot is
 // rewritten only after the event recorded behind its last kernels has completed, so no
 // launch ever waits on the host for the GPU (on-demand experts are launched while their
 // copies are still in flight).
 struct MapRing {
   static constexpr int kSlots = 64;
-  static constexpr int kPerSlot = 5 * kMaxExperts + 2;  // [a_x, a_h, gate_up maps, down maps, (token-N: x_last, h_last)]
+  static constexpr int kPerSlot = 2 * kMaxExperts + 2;  // [a_x, a_h, gate_up maps, down maps] (M-side kernels)
   CUtensorMap* dev = nullptr;
   CUtensorMap* host = nullptr;
   cudaEvent_t ev[kSlots] = {};
@@ -1138,6 +1192,7 @@ extern "C" ps_status ps_expert_ffn_prefill(const ps_expert_group* group, const i
         PS_CUDA(cudaMalloc(&done_dev, sizeof(unsigned) * MapRing::kSlots * kMaxExperts));
         PS_CUDA(cudaMemset(done_dev, 0, sizeof(unsigned) * MapRing::kSlots * kMaxExperts));
       }
+      static MapTable table;
       TnParams tp{};
       tp.F = F;
       tp.H = H;
@@ -1145,27 +1200,21 @@ extern "C" ps_status ps_expert_ffn_prefill(const ps_expert_group* group, const i
       tp.ph[1].K = F;
       tp.ph[0].n_tiles_n = F / 128;
       tp.ph[1].n_tiles_n = H / 256;
-      const int G = group->n;
-      CUtensorMap* wgu = maps_host + 2;
-      CUtensorMap* wdn = maps_host + 2 + G;
-      CUtensorMap* xl = maps_host + 2 + 2 * G;
-      CUtensorMap* hl = maps_host + 2 + 3 * G;
-      CUtensorMap* ym = maps_host + 2 + 4 * G;
       unsigned* shadow = done_host.data() + slot * kMaxExperts;
       int n = 0;
-      for (int i = 0; i < G; ++i) {
+      bool used_half[17] = {};
+      for (int i = 0; i < group->n; ++i) {
         const int e = group->experts[i];
         const int m = counts_host[e];
         if (m == 0) continue;
         const uint16_t* slab = group->slabs[i];
-        wgu[n] = make_map(slab, 2ull * F, H, 64);
-        wdn[n] = make_map(slab + 2ull * F * H, static_cast<uint64_t>(H), F, 128);
+        tp.ph[0].w_idx[n] = table.get(MapKey{slab, 2ull * F, static_cast<uint64_t>(H), 64, 64, 2}, s);
+        tp.ph[1].w_idx[n] = table.get(MapKey{slab + 2ull * F * H, static_cast<uint64_t>(H), static_cast<uint64_t>(F),
+                                             64, 128, 2}, s);
         const int tt = (m + kTnMaxN - 1) / kTnMaxN;
         const int rem = m - (tt - 1) * kTnMaxN;
-        const uint32_t half = static_cast<uint32_t>(((rem + 15) & ~15) / 2);
-        xl[n] = make_map(x_perm, static_cast<uint64_t>(total_rows), H, half);
-        hl[n] = make_map(h_perm, static_cast<uint64_t>(total_rows), F, half);
-        ym[n] = make_map_f32(y_perm + static_cast<size_t>(offsets_host[e]) * H, static_cast<uint64_t>(m), H, 32, 32);
+        used_half[((rem + 15) & ~15) / 16] = true;  // last tile: N/2 = 8j rows
+        if (tt > 1) used_half[16] = true;
         tp.t_tiles[n] = tt;
         tp.row0[n] = offsets_host[e];
         tp.rows[n] = m;
@@ -1175,6 +1224,19 @@ extern "C" ps_status ps_expert_ffn_prefill(const ps_expert_group* group, const i
         ++n;
       }
       if (n == 0) return;
+      for (int j = 0; j <= 16; ++j) {
+        tp.ph[0].tok_idx[j] = tp.ph[1].tok_idx[j] = -1;
+        if (!used_half[j] || j == 0) continue;
+        const uint32_t box = static_cast<uint32_t>(8 * j);
+        tp.ph[0].tok_idx[j] = table.get(MapKey{x_perm, static_cast<uint64_t>(total_rows), static_cast<uint64_t>(H), 64,
+                                               box, 2}, s);
+        tp.ph[1].tok_idx[j] = table.get(MapKey{h_perm, static_cast<uint64_t>(total_rows), static_cast<uint64_t>(F), 64,
+                                               box, 2}, s);
+      }
+      tp.ph[0].out_idx = -1;
+      tp.ph[1].out_idx = table.get(MapKey{y_perm, static_cast<uint64_t>(total_rows), static_cast<uint64_t>(H), 32,
+                                          32, 4}, s);
+      tp.maps = table.dev;
       tp.n_experts = n;
       tp.done = done_dev + slot * kMaxExperts;
       // PS_TN_LAG: experts between a gate_up segment and its down segment. Default: all
@@ -1205,16 +1267,6 @@ extern "C" ps_status ps_expert_ffn_prefill(const ps_expert_group* group, const i
         q.seg_start[q.n_seg] = t;
       };
       build_segments(tp, 3);
-      maps_host[0] = make_map(x_perm, static_cast<uint64_t>(total_rows), H, 128);
-      maps_host[1] = make_map(h_perm, static_cast<uint64_t>(total_rows), F, 128);
-      PS_CUDA(cudaMemcpyAsync(maps_dev, maps_host, sizeof(CUtensorMap) * (2 + 5 * G), cudaMemcpyHostToDevice, s));
-      tp.ph[1].out_maps = maps_dev + 2 + 4 * G;
-      tp.ph[0].tok_full = maps_dev;
-      tp.ph[1].tok_full = maps_dev + 1;
-      tp.ph[0].w_maps = maps_dev + 2;
-      tp.ph[1].w_maps = maps_dev + 2 + G;
-      tp.ph[0].tok_last = maps_dev + 2 + 2 * G;
-      tp.ph[1].tok_last = maps_dev + 2 + 3 * G;
       tp.ph[0].out = h_perm;
       tp.ph[0].out_ld = F;
       tp.ph[1].out = y_perm;
