@@ -738,9 +738,10 @@ ffn_prefill_tn_kernel(const __grid_constant__ TnParams p) {
           const unsigned* d = p.done + tc.entry;
           const unsigned want = p.target[tc.entry];
           unsigned v;
-          while (true) {
+          for (uint32_t spin = 0;; ++spin) {
             asm volatile("ld.acquire.gpu.global.u32 %0, [%1];" : "=r"(v) : "l"(d) : "memory");
             if (static_cast<int>(v - want) >= 0) break;
+            if (spin == (1u << 26)) __trap();  // ~seconds: a lost signal fails the launch instead of hanging
             __nanosleep(64);
           }
           asm volatile("fence.proxy.async.global;" ::: "memory");
@@ -1219,8 +1220,7 @@ extern "C" ps_status ps_expert_ffn_prefill(const ps_expert_group* group, const i
         tp.row0[n] = offsets_host[e];
         tp.rows[n] = m;
         for (TnPhase& ph : tp.ph) ph.tile_start[n + 1] = ph.tile_start[n] + tt * ph.n_tiles_n;
-        shadow[n] += kTnSignalsPerTile * static_cast<unsigned>(tt * tp.ph[0].n_tiles_n);
-        tp.target[n] = shadow[n];
+        tp.target[n] = shadow[n] + kTnSignalsPerTile * static_cast<unsigned>(tt * tp.ph[0].n_tiles_n);
         ++n;
       }
       if (n == 0) return;
@@ -1281,6 +1281,9 @@ extern "C" ps_status ps_expert_ffn_prefill(const ps_expert_group* group, const i
       } else {
         launch_tn(tp, s);
       }
+      // the slot's counters advance only once the launch is enqueued (a failed launch
+      // leaves them where the next use of the slot expects them)
+      for (int i = 0; i < n; ++i) shadow[i] = tp.target[i];
       PS_CUDA(cudaEventRecord(ring.ev[slot], s));
       return;
     }
