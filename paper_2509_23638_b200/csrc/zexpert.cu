@@ -405,13 +405,24 @@ z_decode_kernel_v4(const uint8_t* __restrict__ z, uint64_t n, uint32_t base, uin
     }
     __syncwarp();
     if (vb + kZBlock <= n) {
-      const uint64_t my_off = tile_h ? static_cast<uint64_t>(z_untile32m(static_cast<uint32_t>(v0), tile_h, tile_f, mh, mf))
-                                     : v0;
+      if (tile_h) {
+        // A tiled block is two 16x32 tiles of the same 16 weight rows, K-adjacent (K/32 is
+        // even): segment i and 16 + i are one 128 B run of output row i. Each warp store
+        // writes 4 rows x 128 B (whole lines) instead of 8 tile rows x 64 B.
+        const uint64_t my_off = static_cast<uint64_t>(z_untile32m(static_cast<uint32_t>(v0), tile_h, tile_f, mh, mf));
 #pragma unroll
-      for (int rr = 0; rr < 4; ++rr) {
-        const int c = lane + 32 * rr, sl = c >> 2, q = c & 3;
-        const uint64_t seg_off = __shfl_sync(0xffffffffu, my_off, sl);
-        *reinterpret_cast<uint4*>(out + seg_off + 8 * q) = so[chunk(sl, q)];
+        for (int rr = 0; rr < 4; ++rr) {
+          const int row = 4 * rr + (lane >> 3), j = lane & 7;
+          const int sl = j < 4 ? row : 16 + row, q = j & 3;
+          const uint64_t row_off = __shfl_sync(0xffffffffu, my_off, row);
+          *reinterpret_cast<uint4*>(out + row_off + 8 * j) = so[chunk(sl, q)];
+        }
+      } else {
+#pragma unroll
+        for (int rr = 0; rr < 4; ++rr) {
+          const int c = lane + 32 * rr, sl = c >> 2, q = c & 3;
+          *reinterpret_cast<uint4*>(out + vb + 8 * c) = so[chunk(sl, q)];
+        }
       }
     } else {
       const uint16_t* so16 = reinterpret_cast<const uint16_t*>(so);
