@@ -354,6 +354,13 @@ ps_status ps_expert_ffn(const ps_expert_group* group, const int32_t* counts_host
 ps_status ps_expert_ffn_prefill(const ps_expert_group* group, const int32_t* counts_host,
                                 const int32_t* offsets_host, const uint16_t* x_perm, int total_rows,
                                 int H, int F, uint16_t* h_perm, float* y_perm, void* stream);
+/* Same FFN with the counts on the DEVICE: offsets_dev [E+1] (K2's offsets on the stream);
+ * the tile schedule is built by a one-CTA kernel in stream order, so a caller can launch
+ * the resident group before it has read the routing back (token-N kernel; experts with
+ * no routed rows cost nothing). */
+ps_status ps_expert_ffn_prefill_dev(const ps_expert_group* group, const int32_t* offsets_dev,
+                                    const uint16_t* x_perm, int total_rows, int H, int F, uint16_t* h_perm,
+                                    float* y_perm, void* stream);
 /* Prefill kernel choice (process-wide): 0 = single-CTA M=128 token tiles, 1 = CTA pairs
  * (cta_group::2, M=256 token tiles), 3 = token-N CTA pairs (weights as M=256, an
  * expert's tokens as N <= 256 in steps of 16; gate_up and down in one launch),

@@ -223,6 +223,7 @@ _SIGS = {
     "ps_set_prefill_kernel": (C.c_int, [C.c_int]),
     "ps_expert_ffn_prefill": (C.c_int, [C.POINTER(ExpertGroup), _P, _P, _P, C.c_int, C.c_int, C.c_int, _P, _P,
                                         _P]),
+    "ps_expert_ffn_prefill_dev": (C.c_int, [C.POINTER(ExpertGroup), _P, _P, C.c_int, C.c_int, C.c_int, _P, _P, _P]),
     "ps_init_expert_slab": (C.c_int, [_P, C.c_int, C.c_int, C.c_uint64, C.c_int, C.c_int, _P]),
     "ps_init_expert_slab_host": (C.c_int, [_P, C.c_int, C.c_int, C.c_uint64, C.c_int, C.c_int]),
     "ps_llapor_load": (C.c_int, [C.c_char_p, C.POINTER(C.c_void_p), C.POINTER(ModelSpec)]),

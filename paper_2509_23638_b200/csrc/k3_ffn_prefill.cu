@@ -624,15 +624,15 @@ struct TnPhase {
   int out_idx;                      // down: y_perm as [total_rows, H] f32, box {32 features, 32 tokens}
 };
 
-struct TnParams {
-  const CUtensorMap* maps;          // the device map table
-  int n_experts;
-  int F, H;
+// The tile schedule: built on the host from host counts (in the launch parameters), or on
+// the device from K2's offsets by tn_schedule_kernel (ps_expert_ffn_prefill_dev: the
+// engine launches the resident group before the host has the counts).
+struct TnSched {
+  int n_experts;                    // active entries (m_e > 0)
+  int gidx[kMaxExperts];            // group index of active entry i (its w_idx)
   int t_tiles[kMaxExperts];         // token tiles per entry (ceil(m_e / 256))
   int row0[kMaxExperts];
   int rows[kMaxExperts];
-  TnPhase ph[2];                    // 0 = gate_up, 1 = down
-  unsigned* done;                   // [n_experts] gate_up signals (this map-ring slot's counters)
   unsigned target[kMaxExperts];     // done[e] value once all of e's gate_up tiles are stored
   // Tile order: segments of (phase, entry) — gu(0..D-1), then gu(e), dn(e - D) for e >= D,
   // then the last D down segments (D >= n: every gate_up tile first, the default). A down
@@ -643,12 +643,22 @@ struct TnParams {
   int seg_code[2 * kMaxExperts];
 };
 
+struct TnParams {
+  const CUtensorMap* maps;          // the device map table
+  int n_group;                      // valid w_idx entries
+  int F, H;
+  TnPhase ph[2];                    // 0 = gate_up, 1 = down
+  unsigned* done;                   // gate_up signals per active entry (this map-ring slot's counters)
+  const TnSched* sched_dev;         // device-built schedule, or null: `sched` below
+  TnSched sched;
+};
+
 struct TnTile {
   int phase, entry, n_tile, tok0, n;  // n = MMA N (tokens, multiple of 16)
   bool last;
 };
 
-__device__ __forceinline__ TnTile tn_tile(const TnParams& p, int t) {
+__device__ __forceinline__ TnTile tn_tile(const TnSched& p, int t) {
   TnTile c;
   int lo = 0, hi = p.n_seg - 1;
   while (lo < hi) {
@@ -691,7 +701,8 @@ ffn_prefill_tn_kernel(const __grid_constant__ TnParams p) {
   const uint32_t rank = cluster_rank();
   const bool leader = rank == 0;
   const int pair = blockIdx.x >> 1, n_pairs = gridDim.x >> 1;
-  const int n_tiles = p.seg_start[p.n_seg];
+  const TnSched& S = p.sched_dev ? *p.sched_dev : p.sched;
+  const int n_tiles = S.seg_start[S.n_seg];
 
   if (warp == 0 && lane == 0) {
     for (int s = 0; s < kTnStages; ++s) {
@@ -716,8 +727,8 @@ ffn_prefill_tn_kernel(const __grid_constant__ TnParams p) {
 
   if (warp == 0) {
     for (int ph = 0; ph < 2; ++ph)
-      for (int i = lane; i < p.n_experts + 16; i += 32) {
-        const int idx = i < p.n_experts ? p.ph[ph].w_idx[i] : p.ph[ph].tok_idx[i - p.n_experts + 1];
+      for (int i = lane; i < p.n_group + 16; i += 32) {
+        const int idx = i < p.n_group ? p.ph[ph].w_idx[i] : p.ph[ph].tok_idx[i - p.n_group + 1];
         if (idx >= 0)
           asm volatile("fence.proxy.tensormap::generic.acquire.gpu [%0], 128;" ::"l"(p.maps + idx) : "memory");
       }
@@ -726,17 +737,17 @@ ffn_prefill_tn_kernel(const __grid_constant__ TnParams p) {
       int stage = 0;
       uint32_t phase = 0;
       for (int t = pair; t < n_tiles; t += n_pairs) {
-        const TnTile tc = tn_tile(p, t);
+        const TnTile tc = tn_tile(S, t);
         const TnPhase& ph = p.ph[tc.phase];
-        const CUtensorMap* wmap = p.maps + ph.w_idx[tc.entry];
+        const CUtensorMap* wmap = p.maps + ph.w_idx[S.gidx[tc.entry]];
         const int half = tc.n >> 1;
         const CUtensorMap* tmap = p.maps + ph.tok_idx[half >> 3];
-        const int trow = p.row0[tc.entry] + tc.tok0 + static_cast<int>(rank) * half;
+        const int trow = S.row0[tc.entry] + tc.tok0 + static_cast<int>(rank) * half;
         const uint32_t bytes = 2u * (kTnABytes + static_cast<uint32_t>(half) * kBK * 2);
         const int k_blocks = (ph.K + kBK - 1) / kBK;
         if (tc.phase == 1) {  // h of this entry complete (acquire), then visible to the async proxy
           const unsigned* d = p.done + tc.entry;
-          const unsigned want = p.target[tc.entry];
+          const unsigned want = S.target[tc.entry];
           unsigned v;
           for (uint32_t spin = 0;; ++spin) {
             asm volatile("ld.acquire.gpu.global.u32 %0, [%1];" : "=r"(v) : "l"(d) : "memory");
@@ -773,7 +784,7 @@ ffn_prefill_tn_kernel(const __grid_constant__ TnParams p) {
       int as = 0;
       uint32_t aphase = 0;
       for (int t = pair; t < n_tiles; t += n_pairs) {
-        const TnTile tc = tn_tile(p, t);
+        const TnTile tc = tn_tile(S, t);
         const int k_blocks = (p.ph[tc.phase].K + kBK - 1) / kBK;
         const uint32_t idesc = (1u << 4) | (1u << 7) | (1u << 10) | (static_cast<uint32_t>(tc.n >> 3) << 17) |
                                (static_cast<uint32_t>(256 >> 4) << 24);
@@ -818,13 +829,13 @@ ffn_prefill_tn_kernel(const __grid_constant__ TnParams p) {
       asm volatile("fence.proxy.tensormap::generic.acquire.gpu [%0], 128;" ::"l"(p.maps + p.ph[1].out_idx) : "memory");
     __syncwarp();
     for (int t = pair; t < n_tiles; t += n_pairs) {
-      const TnTile tc = tn_tile(p, t);
+      const TnTile tc = tn_tile(S, t);
       const TnPhase& ph = p.ph[tc.phase];
       mbar_wait(&tfull_bar[as], aphase);
       tc_fence_after();
       const uint32_t tbase = tmem_base + static_cast<uint32_t>(as * kTnMaxN) + (static_cast<uint32_t>(quarter * 32) << 16);
-      const int m_left = p.rows[tc.entry] - tc.tok0;  // valid token columns of this tile
-      const size_t row_base = static_cast<size_t>(p.row0[tc.entry] + tc.tok0);
+      const int m_left = S.rows[tc.entry] - tc.tok0;  // valid token columns of this tile
+      const size_t row_base = static_cast<size_t>(S.row0[tc.entry] + tc.tok0);
       if (tc.phase == 0) {
         // quarters 0/1 hold gate, 2/3 up of features [32 (q & 1), +32) of this CTA's 64.
         // Per 32-token chunk the two warps of a feature group swap halves through shared
@@ -920,6 +931,72 @@ ffn_prefill_tn_kernel(const __grid_constant__ TnParams p) {
   if (warp == 1) {
     tc_fence_after();
     asm volatile("tcgen05.dealloc.cta_group::2.sync.aligned.b32 %0, 512;" ::"r"(tmem_base));
+  }
+}
+
+// Device-side tile schedule (one CTA of kMaxExperts threads): thread i takes group entry
+// i, reads its row count from K2's offsets, and block scans give the compacted entry
+// index and both phases' tile prefixes; every gate_up tile comes first (the host path's
+// default order). Also zeroes the active entries' gate_up counters (the slot's previous
+// kernels are complete: the host reuses a ring slot only after its event).
+struct TnSchedArgs {
+  int n_group;
+  int expert[kMaxExperts];
+  int n0, n1;  // weight-row tiles per expert: gate_up, down
+};
+
+__global__ void __launch_bounds__(kMaxExperts)
+tn_schedule_kernel(const int32_t* __restrict__ offsets, const __grid_constant__ TnSchedArgs a, TnSched* __restrict__ out,
+                   unsigned* __restrict__ done) {
+  __shared__ int s_scan[3][kMaxExperts / 32];
+  const int i = threadIdx.x, lane = i & 31, warp = i >> 5;
+  int m = 0;
+  if (i < a.n_group) m = __ldg(offsets + a.expert[i] + 1) - __ldg(offsets + a.expert[i]);
+  const int row0 = i < a.n_group ? __ldg(offsets + a.expert[i]) : 0;
+  const int act = m > 0 ? 1 : 0;
+  const int tt = (m + kTnMaxN - 1) / kTnMaxN;
+  int v[3] = {act, tt * a.n0, tt * a.n1};
+  int incl[3];
+#pragma unroll
+  for (int q = 0; q < 3; ++q) {  // inclusive warp scans, then warp totals
+    incl[q] = v[q];
+#pragma unroll
+    for (int o = 1; o < 32; o <<= 1) {
+      const int t = __shfl_up_sync(0xffffffffu, incl[q], o);
+      if (lane >= o) incl[q] += t;
+    }
+    if (lane == 31) s_scan[q][warp] = incl[q];
+  }
+  __syncthreads();
+  int excl[3], total[3];
+#pragma unroll
+  for (int q = 0; q < 3; ++q) {
+    int before = 0, tot = 0;
+    for (int w = 0; w < kMaxExperts / 32; ++w) {
+      if (w < warp) before += s_scan[q][w];
+      tot += s_scan[q][w];
+    }
+    excl[q] = before + incl[q] - v[q];
+    total[q] = tot;
+  }
+  const int n = total[0];
+  if (act) {
+    const int e = excl[0];
+    out->gidx[e] = i;
+    out->t_tiles[e] = tt;
+    out->row0[e] = row0;
+    out->rows[e] = m;
+    out->target[e] = kTnSignalsPerTile * static_cast<unsigned>(tt * a.n0);
+    out->seg_start[e] = excl[1];
+    out->seg_code[e] = e;
+    out->seg_start[n + e] = total[1] + excl[2];
+    out->seg_code[n + e] = e | (1 << 16);
+    done[e] = 0u;
+  }
+  if (i == 0) {
+    out->n_experts = n;
+    out->n_seg = 2 * n;
+    out->seg_start[2 * n] = total[1] + total[2];
   }
 }
 
@@ -1120,7 +1197,7 @@ void launch_tn(TnParams& p, cudaStream_t s) {
     if (clusters < 1) fail(PS_ECUDA, "ffn_prefill_tn_kernel: no 2-CTA cluster fits on this device");
     max_pairs = std::min(clusters, kNumSMs / 2);
   }
-  const int tiles = p.seg_start[p.n_seg];
+  const int tiles = p.sched_dev ? max_pairs : p.sched.seg_start[p.sched.n_seg];  // device schedule: all pairs
   if (tiles == 0) return;
   const int grid = 2 * std::min(tiles, max_pairs);
   ffn_prefill_tn_kernel<<<grid, kThreads, kTnSmemBytes, s>>>(p);
@@ -1216,11 +1293,12 @@ extern "C" ps_status ps_expert_ffn_prefill(const ps_expert_group* group, const i
         const int rem = m - (tt - 1) * kTnMaxN;
         used_half[((rem + 15) & ~15) / 16] = true;  // last tile: N/2 = 8j rows
         if (tt > 1) used_half[16] = true;
-        tp.t_tiles[n] = tt;
-        tp.row0[n] = offsets_host[e];
-        tp.rows[n] = m;
+        tp.sched.gidx[n] = n;
+        tp.sched.t_tiles[n] = tt;
+        tp.sched.row0[n] = offsets_host[e];
+        tp.sched.rows[n] = m;
         for (TnPhase& ph : tp.ph) ph.tile_start[n + 1] = ph.tile_start[n] + tt * ph.n_tiles_n;
-        tp.target[n] = shadow[n] + kTnSignalsPerTile * static_cast<unsigned>(tt * tp.ph[0].n_tiles_n);
+        tp.sched.target[n] = shadow[n] + kTnSignalsPerTile * static_cast<unsigned>(tt * tp.ph[0].n_tiles_n);
         ++n;
       }
       if (n == 0) return;
@@ -1237,7 +1315,8 @@ extern "C" ps_status ps_expert_ffn_prefill(const ps_expert_group* group, const i
       tp.ph[1].out_idx = table.get(MapKey{y_perm, static_cast<uint64_t>(total_rows), static_cast<uint64_t>(H), 32,
                                           32, 4}, s);
       tp.maps = table.dev;
-      tp.n_experts = n;
+      tp.sched.n_experts = n;
+      tp.n_group = n;
       tp.done = done_dev + slot * kMaxExperts;
       // PS_TN_LAG: experts between a gate_up segment and its down segment. Default: all
       // gate_up tiles first (DeepSeek shape, same process: lag 10 277 us, all-first 283,
@@ -1251,20 +1330,21 @@ extern "C" ps_status ps_expert_ffn_prefill(const ps_expert_group* group, const i
       auto build_segments = [&](TnParams& q, int phases) {
         const int D = std::min(lag, n);
         int t = 0;
-        q.n_seg = 0;
+        TnSched& S = q.sched;
+        S.n_seg = 0;
         auto seg = [&](int ph, int e) {
           if (!(phases & (1 << ph))) return;
-          q.seg_start[q.n_seg] = t;
-          q.seg_code[q.n_seg] = e | (ph << 16);
+          S.seg_start[S.n_seg] = t;
+          S.seg_code[S.n_seg] = e | (ph << 16);
           t += q.ph[ph].tile_start[e + 1] - q.ph[ph].tile_start[e];
-          ++q.n_seg;
+          ++S.n_seg;
         };
         for (int e = 0; e < n; ++e) {
           seg(0, e);
           if (e >= D) seg(1, e - D);
         }
         for (int e = n - D; e < n; ++e) seg(1, e);
-        q.seg_start[q.n_seg] = t;
+        S.seg_start[S.n_seg] = t;
       };
       build_segments(tp, 3);
       tp.ph[0].out = h_perm;
@@ -1283,7 +1363,7 @@ extern "C" ps_status ps_expert_ffn_prefill(const ps_expert_group* group, const i
       }
       // the slot's counters advance only once the launch is enqueued (a failed launch
       // leaves them where the next use of the slot expects them)
-      for (int i = 0; i < n; ++i) shadow[i] = tp.target[i];
+      for (int i = 0; i < n; ++i) shadow[i] = tp.sched.target[i];
       PS_CUDA(cudaEventRecord(ring.ev[slot], s));
       return;
     }
@@ -1334,6 +1414,70 @@ extern "C" ps_status ps_expert_ffn_prefill(const ps_expert_group* group, const i
       launch(gu, s);
       launch(dn, s);
     }
+    PS_CUDA(cudaEventRecord(ring.ev[slot], s));
+  });
+}
+
+extern "C" ps_status ps_expert_ffn_prefill_dev(const ps_expert_group* group, const int32_t* offsets_dev,
+                                               const uint16_t* x_perm, int total_rows, int H, int F,
+                                               uint16_t* h_perm, float* y_perm, void* stream) {
+  return guarded([&] {
+    require(group && offsets_dev && x_perm && h_perm && y_perm, "ps_expert_ffn_prefill_dev: null argument");
+    require(H % 256 == 0 && F % 128 == 0, "ps_expert_ffn_prefill_dev: needs H % 256 == 0 and F % 128 == 0");
+    require(group->n >= 0 && group->n <= kMaxExperts, "ps_expert_ffn_prefill_dev: too many experts");
+    require(total_rows >= 1, "ps_expert_ffn_prefill_dev: total_rows >= 1");
+    if (group->n == 0) return;
+    cudaStream_t s = as_stream(stream);
+    static MapRing ring;
+    static MapTable table;
+    static TnSched* sched_dev = nullptr;  // [MapRing::kSlots]
+    static unsigned* done_dev = nullptr;  // [MapRing::kSlots][kMaxExperts]
+    static std::mutex mu;
+    std::lock_guard<std::mutex> lock(mu);
+    if (!sched_dev) {
+      PS_CUDA(cudaMalloc(&sched_dev, sizeof(TnSched) * MapRing::kSlots));
+      PS_CUDA(cudaMalloc(&done_dev, sizeof(unsigned) * MapRing::kSlots * kMaxExperts));
+    }
+    const int slot = ring.acquire();
+    TnParams tp{};
+    tp.F = F;
+    tp.H = H;
+    tp.ph[0].K = H;
+    tp.ph[1].K = F;
+    tp.ph[0].n_tiles_n = F / 128;
+    tp.ph[1].n_tiles_n = H / 256;
+    TnSchedArgs sa{};
+    sa.n_group = group->n;
+    sa.n0 = tp.ph[0].n_tiles_n;
+    sa.n1 = tp.ph[1].n_tiles_n;
+    for (int i = 0; i < group->n; ++i) {
+      const uint16_t* slab = group->slabs[i];
+      sa.expert[i] = group->experts[i];
+      tp.ph[0].w_idx[i] = table.get(MapKey{slab, 2ull * F, static_cast<uint64_t>(H), 64, 64, 2}, s);
+      tp.ph[1].w_idx[i] = table.get(MapKey{slab + 2ull * F * H, static_cast<uint64_t>(H), static_cast<uint64_t>(F),
+                                           64, 128, 2}, s);
+    }
+    tp.ph[0].tok_idx[0] = tp.ph[1].tok_idx[0] = -1;
+    for (int j = 1; j <= 16; ++j) {  // every last-tile width: the counts are on the device
+      const uint32_t box = static_cast<uint32_t>(8 * j);
+      tp.ph[0].tok_idx[j] = table.get(MapKey{x_perm, static_cast<uint64_t>(total_rows), static_cast<uint64_t>(H), 64,
+                                             box, 2}, s);
+      tp.ph[1].tok_idx[j] = table.get(MapKey{h_perm, static_cast<uint64_t>(total_rows), static_cast<uint64_t>(F), 64,
+                                             box, 2}, s);
+    }
+    tp.ph[0].out_idx = -1;
+    tp.ph[1].out_idx = table.get(MapKey{y_perm, static_cast<uint64_t>(total_rows), static_cast<uint64_t>(H), 32, 32, 4}, s);
+    tp.maps = table.dev;
+    tp.n_group = group->n;
+    tp.done = done_dev + slot * kMaxExperts;
+    tp.sched_dev = sched_dev + slot;
+    tp.ph[0].out = h_perm;
+    tp.ph[0].out_ld = F;
+    tp.ph[1].out = y_perm;
+    tp.ph[1].out_ld = H;
+    tn_schedule_kernel<<<1, kMaxExperts, 0, s>>>(offsets_dev, sa, sched_dev + slot, tp.done);
+    PS_LAUNCH_CHECK("tn_schedule_kernel");
+    launch_tn(tp, s);
     PS_CUDA(cudaEventRecord(ring.ev[slot], s));
   });
 }

@@ -198,3 +198,55 @@ def test_prefill_token_n_ragged_counts(torch_cuda):
         assert _rel(ys[0][t], y_ref[t]) < BF16_RTOL, t
     for y in ys[1:]:
         assert np.array_equal(y, ys[0])
+
+
+@pytest.mark.parametrize("H,F,E,k,B", [(2048, 1408, 64, 6, 2048), (256, 384, 9, 1, 1500), (512, 512, 16, 4, 300)])
+def test_prefill_device_schedule_matches_host_schedule(torch_cuda, H, F, E, k, B):
+    """ps_expert_ffn_prefill_dev (tile schedule built on the device from K2's offsets, the
+    engine's early resident-group launch) gives bitwise the h / y of the host-count call,
+    with experts that get no rows in the group (they cost nothing) and ragged counts."""
+    torch = torch_cuda
+    lib = ps.load()
+    s = C.c_void_p(torch.cuda.current_stream().cuda_stream)
+    rng = np.random.default_rng(B + E)
+    p = rng.dirichlet(np.ones(E) * 0.3)
+    p[E // 3] = 0.0  # an expert nobody routes to
+    p /= p.sum()
+    ids = np.stack([rng.choice(E, k, replace=False, p=p) for _ in range(B)]).astype(np.int32)
+    x = orc.f32_to_bf16((rng.standard_normal((B, H)) / np.sqrt(H)).astype(np.float32))
+    slabs = []
+    for e in range(E):
+        t = torch.empty(3 * H * F, dtype=torch.int16, device="cuda")
+        ps.check(lib.ps_init_expert_slab(_p(t), H, F, 5, 0, e, s))
+        slabs.append(t)
+    rows = B * k
+    di = torch.as_tensor(ids, device="cuda")
+    dx = torch.as_tensor(x.view(np.int16), device="cuda")
+    off = torch.empty(E + 1, dtype=torch.int32, device="cuda")
+    src = torch.empty(rows, dtype=torch.int32, device="cuda")
+    inv = torch.empty(rows, dtype=torch.int32, device="cuda")
+    xp = torch.empty(rows, H, dtype=torch.int16, device="cuda")
+    ps.check(lib.ps_permute(_p(di), B, k, E, _p(off), _p(src), _p(inv), _p(dx), H, _p(xp), s))
+    counts = np.bincount(ids.ravel(), minlength=E).astype(np.int32)
+    offsets = off.cpu().numpy()
+    grp = ps.capi.ExpertGroup()
+    grp.n = E
+    for e in range(E):
+        grp.experts[e] = e
+        grp.slabs[e] = slabs[e].data_ptr()
+    outs = []
+    for dev in (False, True, True):
+        h = torch.zeros(rows, F, dtype=torch.int16, device="cuda")
+        yp = torch.full((rows, H), float("nan"), dtype=torch.float32, device="cuda")
+        if dev:
+            ps.check(lib.ps_expert_ffn_prefill_dev(C.byref(grp), _p(off), _p(xp), rows, H, F, _p(h), _p(yp), s))
+        else:
+            ps.check(lib.ps_set_prefill_kernel(3))
+            ps.check(lib.ps_expert_ffn_prefill(C.byref(grp), counts.ctypes.data, offsets.ctypes.data, _p(xp), rows,
+                                               H, F, _p(h), _p(yp), s))
+            ps.check(lib.ps_set_prefill_kernel(2))
+        outs.append((h.cpu().numpy(), yp.cpu().numpy()))
+    assert np.isfinite(outs[0][1]).all()
+    for h, yp in outs[1:]:
+        assert np.array_equal(h, outs[0][0])
+        assert np.array_equal(yp, outs[0][1])
