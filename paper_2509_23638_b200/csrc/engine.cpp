@@ -465,7 +465,14 @@ void ffn(ps_engine_s& e, const ps_expert_group& g, const int32_t* counts_host, i
   ps_status s;
   (void)B;
   const auto& src = e.src;
-  if (e.prefill_mode && max_m >= 128 && e.H % 256 == 0 && e.F % 128 == 0) {
+  if (e.prefill_mode && !exact_counts && e.H % 256 == 0 && e.F % 128 == 0) {
+    // early resident-group launch of a prefill chunk: the tile schedule is built on the
+    // device from K2's offsets (no host round trip before the FFN)
+    s = ps_expert_ffn_prefill_dev(&g, src.offsets_dev, e.x_perm, src.rows, e.H, e.F, e.hbuf, e.y_part, e.sc);
+    e.st.tc_launches += 1;
+    e.st.ffn_launches += 1;
+    e.st.kernel_launches += 2;  // schedule + FFN
+  } else if (e.prefill_mode && max_m >= 128 && e.H % 256 == 0 && e.F % 128 == 0) {
     s = ps_expert_ffn_prefill(&g, counts_host, src.offsets_host, e.x_perm, src.rows, e.H, e.F, e.hbuf, e.y_part,
                               e.sc);
     const int n_launch = prefill_launches_per_call();  // gate_up + down: one launch (token-N) or two
@@ -859,7 +866,7 @@ void layer_forward(ps_engine_s& e, int l, const float* x, const uint8_t* follow,
     // --- resident experts (R6). Decode: start now, before the host knows the counts —
     // the kernels read per-expert row counts from the device offsets, the grid is sized
     // for the worst case m_e = B and warps of unrouted experts exit immediately.
-    // Prefill: launched after the host sync with exact counts (tile scheduling).
+    // Prefill: the same, the token-N kernel scheduling its tiles on the device.
     ps_expert_group grp{};
     std::vector<int32_t> worst(Et, B);
     for (int ex = 0; ex < E; ++ex)
@@ -874,7 +881,7 @@ void layer_forward(ps_engine_s& e, int l, const float* x, const uint8_t* follow,
       ++grp.n;
     }
     const size_t resident_timing = e.ffn_t.size();
-    const bool early = !e.prefill_mode && !e.ep;
+    const bool early = !e.ep && (!e.prefill_mode || (e.H % 256 == 0 && e.F % 128 == 0));
     if (early) ffn(e, grp, worst.data(), B, true, false, ph.route1);
 
     // --- R2: resolve the previous layer's prefetch batch at this scheduling point
