@@ -319,6 +319,12 @@ ps_status ps_cast_bf16(const float* x, int64_t n, uint16_t* out, void* stream);
  * engine), and dst[z*zero_stride, +n) = 0 for z = 1..zero_copies. n, zero_stride % 4 == 0. */
 ps_status ps_rows_from_host(const float* host_src, int64_t n, float* dst, int zero_copies, int64_t zero_stride,
                             void* stream);
+/* The same for several row ranges of one mapped pinned buffer in one launch: rows
+ * [row0[i], row0[i] + m[i]) of host_base (f32, row length H) -> the same rows of dst, and
+ * zero_copies zero-filled copies at zero_stride (floats; >= the largest row end * H).
+ * n_ranges <= 128, H % 4 == 0. */
+ps_status ps_rows_from_host_ranges(const float* host_base, const int32_t* row0, const int32_t* m, int n_ranges,
+                                   int H, float* dst, int zero_copies, int64_t zero_stride, void* stream);
 
 /* Shared experts (BASELINE config 3, DeepSeek-V2-Lite: 2 always-active experts with gate
  * weight 1; a north_star extension — the reference's ModelSpec has none): appends

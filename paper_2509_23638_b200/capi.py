@@ -209,6 +209,7 @@ _SIGS = {
     "ps_zslab_encode_tiled": (C.c_int, [_P, C.c_int, C.c_int, _P, C.c_uint64, C.POINTER(C.c_uint64), C.c_int]),
     "ps_host_expert_ffn_batch_z": (C.c_int, [_P, C.c_int, _P, _P, _P, C.c_int, C.c_int, _P, _P]),
     "ps_rows_from_host": (C.c_int, [_P, C.c_int64, _P, C.c_int, C.c_int64, _P]),
+    "ps_rows_from_host_ranges": (C.c_int, [_P, _P, _P, C.c_int, C.c_int, _P, C.c_int, C.c_int64, _P]),
     "ps_cast_bf16": (C.c_int, [_P, C.c_int64, _P, _P]),
     "ps_engine_decode_step_routed": (C.c_int, [_P, _P, _P, _P, C.c_int, _P]),
     "ps_zslab_bound": (C.c_uint64, [C.c_uint64]),

@@ -27,6 +27,8 @@
 #include <cstdlib>
 #include <cstring>
 #include <deque>
+#include <map>
+#include <tuple>
 #include <memory>
 #include <mutex>
 #include <thread>
@@ -40,7 +42,9 @@
 #include "zslab_format.hpp"
 
 namespace ps {
-int prefill_launches_per_call();  // k3_ffn_prefill.cu
+int prefill_launches_per_call();                  // k3_ffn_prefill.cu
+void llapor_prepare(ps_llapor m, int layer);      // k4_llapor.cu
+uint64_t llapor_generation(ps_llapor m);
 }  // namespace ps
 
 namespace ps {
@@ -327,6 +331,13 @@ struct ps_engine_s {
   // perm_src [maxB*Kt]
   int32_t* sched_dev = nullptr;
   int32_t* route_ws = nullptr;       // ticket counter of the fused route+permute launch
+  // Decode scheduling point as a CUDA graph per (layer, B, variant): K1 (+ fused K2 index
+  // pass) and the two K4 predictions on their forked side streams, replayed from staged
+  // inputs (x_stage / fol_stage) — one launch instead of ~13 stream operations.
+  float* x_stage = nullptr;
+  uint8_t* fol_stage = nullptr;
+  std::map<std::tuple<int, int, int, uint64_t>, cudaGraphExec_t> sched_graphs;
+  bool use_graphs = true;
   int32_t* pinned_counts = nullptr;  // host mirror of sched_dev
   uint16_t* x_bf16 = nullptr;
   uint16_t* x_perm = nullptr;        // [maxB*k, H] bf16 (prefill gather)
@@ -723,6 +734,23 @@ void step_begin(ps_engine_s& e, int B) {
 // (= FFN input), follow [B] u8 (nullable), y [B,H] f32 out. routed_ids / routed_w
 // (nullable, [B,k] / [B,E]): the routing is given (a reference trace's gating truth) and
 // replaces K1. x_next / follow_next: layer l+1's inputs (PS_PRED_PERFECT only).
+// The host lane's output rows of e.cpu_jobs -> y_part (split 0; the other splits' rows
+// zeroed), one launch for all of them.
+void rows_to_device(ps_engine_s& e, size_t total_rows) {
+  std::vector<int32_t> row0, m;
+  for (const CpuJob& j : e.cpu_jobs) {
+    row0.push_back(j.row0);
+    m.push_back(j.m);
+  }
+  for (size_t i = 0; i < row0.size(); i += 128) {
+    const int n = static_cast<int>(std::min<size_t>(128, row0.size() - i));
+    const ps_status cs = ps_rows_from_host_ranges(e.lane_yrows, row0.data() + i, m.data() + i, n, e.H, e.y_part,
+                                                  e.step_split - 1, static_cast<int64_t>(total_rows) * e.H, e.sc);
+    if (cs != PS_OK) fail(cs, ps_last_error());
+    e.st.kernel_launches += 1;
+  }
+}
+
 void layer_forward(ps_engine_s& e, int l, const float* x, const uint8_t* follow, float* y_l,
                    const int32_t* routed_ids, const float* routed_w, const float* x_next, const uint8_t* follow_next) {
   const int L = e.L, E = e.E, K = e.K, H = e.H, B = e.step_B;
@@ -753,20 +781,7 @@ void layer_forward(ps_engine_s& e, int l, const float* x, const uint8_t* follow,
     // Decode without shared experts / EP: K1 and K2's index pass in one launch (the last
     // route CTA permutes). Otherwise K1 here and K2 below. Histogram: diff of K2 offsets.
     const bool fused_perm = !e.ep && e.S == 0 && !e.prefill_mode && !routed_ids;
-    ps_status s;
-    if (routed_ids) {
-      PS_CUDA(cudaMemcpyAsync(ld.ids, routed_ids, sizeof(int32_t) * B * K, cudaMemcpyDeviceToDevice, e.sc));
-      PS_CUDA(cudaMemcpyAsync(ld.weights, routed_w, sizeof(float) * B * E, cudaMemcpyDeviceToDevice, e.sc));
-      s = ps_cast_bf16(x, static_cast<int64_t>(B) * H, e.x_bf16, e.sc);
-    } else if (fused_perm)
-      s = ps_route_permute(x, e.gate + static_cast<size_t>(l) * E * H, e.bias + static_cast<size_t>(l) * E,
-                           follow, l > 0 ? e.layer[l - 1].ids : nullptr, K, B, H, E, K, ld.weights, ld.ids, e.x_bf16, e.offsets, e.perm_src, e.inv, e.route_ws,
-                           e.sc);
-    else
-      s = ps_route_topk(x, e.gate + static_cast<size_t>(l) * E * H, e.bias + static_cast<size_t>(l) * E,
-                        follow, l > 0 ? e.layer[l - 1].ids : nullptr, K, B, H, E, K, nullptr, ld.weights, ld.ids, nullptr, e.x_bf16, e.sc);
-    if (s != PS_OK) fail(s, ps_last_error());
-    e.st.kernel_launches += 1;
+    ps_status s = PS_OK;
     // --- K4 LLaPor: predicted histogram of layer l+1 -------------------------
     // Prefill chunks (B > 64 and >= 16 routed rows per expert on average) activate every
     // expert of the next layer with near certainty: the prediction is then the dense
@@ -781,37 +796,95 @@ void layer_forward(ps_engine_s& e, int l, const float* x, const uint8_t* follow,
     // which do not exist yet at layer l: nets[l+2] is applied to layer-l features instead.
     const bool want_pred2 = !e.ep && l + 2 < L && !e.prefill_mode && e.has_host[l + 2];
     const bool predict2 = want_pred2 && e.pred_kind == PS_PRED_LLAPOR;
-    // The two predictions run concurrently on two side streams forked after K1 and
-    // joined back into Sc before K2 / the resident FFN. (Left unjoined they would queue
-    // behind the persistent FFN kernel, which holds every SM, and delay the host's plan:
-    // layer-start-to-lane-start 370 vs 220 us, profiles/timelines/r02_hybrid_k4_unjoined.json.)
-    if (predict || predict2) PS_CUDA(cudaEventRecord(e.ev_k1, e.sc));
-    if (predict && e.pred_kind == PS_PRED_LLAPOR) {
-      PS_CUDA(cudaStreamWaitEvent(e.s_pred[0], e.ev_k1, 0));
-      s = ps_llapor_forward(e.cfg.predictor, l + 1, x, ld.ids, K, ld.weights, B, K, nullptr, nullptr, e.pred_dev,
-                            e.llapor_scratch, e.s_pred[0]);
+    // K1 (+ K2's index pass when fused) and the K4 predictions, on x / fol.
+    auto sched_kernels = [&](const float* xk, const uint8_t* fk) {
+      // --- K1 route (+fused bf16 cast) ----------------------------------------------
+      // Decode without shared experts / EP: K1 and K2's index pass in one launch (the last
+      // route CTA permutes). Otherwise K1 here and K2 below. Histogram: diff of K2 offsets.
+      if (routed_ids) {
+        PS_CUDA(cudaMemcpyAsync(ld.ids, routed_ids, sizeof(int32_t) * B * K, cudaMemcpyDeviceToDevice, e.sc));
+        PS_CUDA(cudaMemcpyAsync(ld.weights, routed_w, sizeof(float) * B * E, cudaMemcpyDeviceToDevice, e.sc));
+        s = ps_cast_bf16(xk, static_cast<int64_t>(B) * H, e.x_bf16, e.sc);
+      } else if (fused_perm)
+        s = ps_route_permute(xk, e.gate + static_cast<size_t>(l) * E * H, e.bias + static_cast<size_t>(l) * E,
+                             fk, l > 0 ? e.layer[l - 1].ids : nullptr, K, B, H, E, K, ld.weights, ld.ids, e.x_bf16,
+                             e.offsets, e.perm_src, e.inv, e.route_ws, e.sc);
+      else
+        s = ps_route_topk(xk, e.gate + static_cast<size_t>(l) * E * H, e.bias + static_cast<size_t>(l) * E,
+                          fk, l > 0 ? e.layer[l - 1].ids : nullptr, K, B, H, E, K, nullptr, ld.weights, ld.ids, nullptr,
+                          e.x_bf16, e.sc);
       if (s != PS_OK) fail(s, ps_last_error());
-      e.st.kernel_launches += 2;
-    } else if (predict) {  // PERFECT: layer l+1's true routing, K1 one layer early
-      require(x_next != nullptr, "PS_PRED_PERFECT needs layer l+1's inputs (not available per layer)");
-      PS_CUDA(cudaStreamWaitEvent(e.s_pred[0], e.ev_k1, 0));
-      s = ps_route_topk(x_next, e.gate + static_cast<size_t>(l + 1) * E * H, e.bias + static_cast<size_t>(l + 1) * E,
-                        follow_next, ld.ids, K, B, H, E, K, nullptr,
-                        e.pp_w, e.pp_ids, e.pred_dev, nullptr, e.s_pred[0]);
-      if (s != PS_OK) fail(s, ps_last_error());
-      e.st.kernel_launches += 1;
+      // The two predictions run concurrently on two side streams forked after K1 and
+      // joined back into Sc before K2 / the resident FFN. (Left unjoined they would queue
+      // behind the persistent FFN kernel, which holds every SM, and delay the host's plan:
+      // layer-start-to-lane-start 370 vs 220 us, profiles/timelines/r02_hybrid_k4_unjoined.json.)
+      if (predict || predict2) PS_CUDA(cudaEventRecord(e.ev_k1, e.sc));
+      if (predict && e.pred_kind == PS_PRED_LLAPOR) {
+        PS_CUDA(cudaStreamWaitEvent(e.s_pred[0], e.ev_k1, 0));
+        s = ps_llapor_forward(e.cfg.predictor, l + 1, xk, ld.ids, K, ld.weights, B, K, nullptr, nullptr, e.pred_dev,
+                              e.llapor_scratch, e.s_pred[0]);
+        if (s != PS_OK) fail(s, ps_last_error());
+      } else if (predict) {  // PERFECT: layer l+1's true routing, K1 one layer early
+        require(x_next != nullptr, "PS_PRED_PERFECT needs layer l+1's inputs (not available per layer)");
+        PS_CUDA(cudaStreamWaitEvent(e.s_pred[0], e.ev_k1, 0));
+        s = ps_route_topk(x_next, e.gate + static_cast<size_t>(l + 1) * E * H,
+                          e.bias + static_cast<size_t>(l + 1) * E, follow_next, ld.ids, K, B, H, E, K, nullptr,
+                          e.pp_w, e.pp_ids, e.pred_dev, nullptr, e.s_pred[0]);
+        if (s != PS_OK) fail(s, ps_last_error());
+      }
+      if (predict) PS_CUDA(cudaEventRecord(e.ev_pred[0], e.s_pred[0]));
+      if (predict2) {
+        PS_CUDA(cudaStreamWaitEvent(e.s_pred[1], e.ev_k1, 0));
+        s = ps_llapor_forward(e.cfg.predictor, l + 2, xk, ld.ids, K, ld.weights, B, K, nullptr, nullptr, e.pred2_dev,
+                              e.llapor_scratch2, e.s_pred[1]);
+        if (s != PS_OK) fail(s, ps_last_error());
+        PS_CUDA(cudaEventRecord(e.ev_pred[1], e.s_pred[1]));
+      }
+      if (predict) PS_CUDA(cudaStreamWaitEvent(e.sc, e.ev_pred[0], 0));  // join
+      if (predict2) PS_CUDA(cudaStreamWaitEvent(e.sc, e.ev_pred[1], 0));
+    };
+    e.st.kernel_launches += 1 + (predict ? (e.pred_kind == PS_PRED_LLAPOR ? 2 : 1) : 0) + (predict2 ? 2 : 0);
+    // Graph replay: decode with the fused route+permute and LLaPor (or no) prediction.
+    const bool graph_ok = e.use_graphs && fused_perm && !(predict && e.pred_kind == PS_PRED_PERFECT) &&
+                          B <= e.maxB && e.x_stage;
+    if (graph_ok) {
+      if (predict) llapor_prepare(e.cfg.predictor, l + 1);  // device copies current before a capture/replay
+      if (predict2) llapor_prepare(e.cfg.predictor, l + 2);
+      PS_CUDA(cudaMemcpyAsync(e.x_stage, x, sizeof(float) * B * H, cudaMemcpyDeviceToDevice, e.sc));
+      if (follow) PS_CUDA(cudaMemcpyAsync(e.fol_stage, follow, B, cudaMemcpyDeviceToDevice, e.sc));
+      const int variant = (follow ? 1 : 0) | (predict ? 2 : 0) | (predict2 ? 4 : 0);
+      const auto key = std::make_tuple(l, B, variant, (predict || predict2) ? llapor_generation(e.cfg.predictor) : 0);
+      auto it = e.sched_graphs.find(key);
+      if (it == e.sched_graphs.end()) {
+        for (auto jt = e.sched_graphs.begin(); jt != e.sched_graphs.end();) {  // older predictor uploads
+          if (std::get<0>(jt->first) == l && std::get<1>(jt->first) == B && std::get<2>(jt->first) == variant) {
+            cudaGraphExecDestroy(jt->second);
+            jt = e.sched_graphs.erase(jt);
+          } else {
+            ++jt;
+          }
+        }
+        cudaGraph_t graph = nullptr;
+        PS_CUDA(cudaStreamBeginCapture(e.sc, cudaStreamCaptureModeThreadLocal));
+        try {
+          sched_kernels(e.x_stage, follow ? e.fol_stage : nullptr);
+        } catch (...) {
+          cudaGraph_t dead = nullptr;
+          cudaStreamEndCapture(e.sc, &dead);
+          if (dead) cudaGraphDestroy(dead);
+          throw;
+        }
+        PS_CUDA(cudaStreamEndCapture(e.sc, &graph));
+        cudaGraphExec_t exec = nullptr;
+        const cudaError_t ie = cudaGraphInstantiate(&exec, graph, 0);
+        cudaGraphDestroy(graph);
+        if (ie != cudaSuccess) fail(PS_ECUDA, std::string("scheduling-point graph: ") + cudaGetErrorString(ie));
+        it = e.sched_graphs.emplace(key, exec).first;
+      }
+      PS_CUDA(cudaGraphLaunch(it->second, e.sc));
+    } else {
+      sched_kernels(x, follow);
     }
-    if (predict) PS_CUDA(cudaEventRecord(e.ev_pred[0], e.s_pred[0]));
-    if (predict2) {
-      PS_CUDA(cudaStreamWaitEvent(e.s_pred[1], e.ev_k1, 0));
-      s = ps_llapor_forward(e.cfg.predictor, l + 2, x, ld.ids, K, ld.weights, B, K, nullptr, nullptr, e.pred2_dev,
-                            e.llapor_scratch2, e.s_pred[1]);
-      if (s != PS_OK) fail(s, ps_last_error());
-      e.st.kernel_launches += 2;
-      PS_CUDA(cudaEventRecord(e.ev_pred[1], e.s_pred[1]));
-    }
-    if (predict) PS_CUDA(cudaStreamWaitEvent(e.sc, e.ev_pred[0], 0));  // join
-    if (predict2) PS_CUDA(cudaStreamWaitEvent(e.sc, e.ev_pred[1], 0));
     // --- K2 permute indices ------------------------------------------------------
     // Prefill-sized batches gather x into contiguous permuted rows (TMA operand of the
     // tcgen05 path) and need the offsets on the host for tile scheduling.
@@ -1115,16 +1188,11 @@ void layer_forward(ps_engine_s& e, int l, const float* x, const uint8_t* follow,
         e.cal_m.push_back(static_cast<int32_t>(std::lround(tok / n)));
         e.cal_us.push_back(ps_to_ticks(us / n));
       }
+      // SM-driven read of the mapped pinned rows (a copy-engine H2D here would queue behind
+      // an in-flight expert load on the same engine, up to ~4.5 ms), every expert's rows in
+      // one launch
+      rows_to_device(e, total_rows);
       for (CpuJob& j : e.cpu_jobs) {
-        const size_t bytes = sizeof(float) * static_cast<size_t>(j.m) * H;
-        (void)bytes;
-        // SM-driven read of the mapped pinned rows: a copy-engine H2D here would queue
-        // behind an in-flight expert load on the same engine (up to ~4.5 ms)
-        const ps_status cs = ps_rows_from_host(e.lane_yrows + static_cast<size_t>(j.row0) * H,
-                                               static_cast<int64_t>(j.m) * H, e.y_part + static_cast<size_t>(j.row0) * H,
-                                               e.step_split - 1, static_cast<int64_t>(total_rows) * H, e.sc);
-        if (cs != PS_OK) fail(cs, ps_last_error());
-        e.st.kernel_launches += 1;
         e.st.cpu_experts += 1;
         e.st.cpu_bytes_total += static_cast<double>(e.cfg.spec.expert_bytes);
         e.st.cpu_read_bytes += lane_read_bytes(e, j);
@@ -1157,12 +1225,8 @@ void layer_forward(ps_engine_s& e, int l, const float* x, const uint8_t* follow,
         e.lane_drv->wait();
         e.last_ffn_end = nullptr;
         const size_t total_rows = static_cast<size_t>(e.src.rows);
+        rows_to_device(e, total_rows);
         for (CpuJob& j : e.cpu_jobs) {
-          const ps_status cs = ps_rows_from_host(e.lane_yrows + static_cast<size_t>(j.row0) * H,
-                                                 static_cast<int64_t>(j.m) * H, e.y_part + static_cast<size_t>(j.row0) * H,
-                                                 e.step_split - 1, static_cast<int64_t>(total_rows) * H, e.sc);
-          if (cs != PS_OK) fail(cs, ps_last_error());
-          e.st.kernel_launches += 1;
           e.st.cpu_experts += 1;
           e.st.cpu_bytes_total += static_cast<double>(e.cfg.spec.expert_bytes);
           e.st.cpu_read_bytes += lane_read_bytes(e, j);
@@ -1635,6 +1699,12 @@ void create_engine(const ps_engine_config& cfg, ps_engine_s& e) {
   PS_CUDA(cudaHostAlloc(&e.pinned_counts, sizeof(int32_t) * n_sched, cudaHostAllocDefault));
   e.counts_dev = e.sched_dev;
   PS_CUDA(cudaMalloc(&e.route_ws, sizeof(int32_t)));
+  if (e.use_graphs) {
+    const char* g = std::getenv("PS_SCHED_GRAPH");  // 0: eager scheduling point (A/B)
+    e.use_graphs = !(g && g[0] == '0');
+  }
+  PS_CUDA(cudaMalloc(&e.x_stage, sizeof(float) * static_cast<size_t>(e.maxB) * e.H));
+  PS_CUDA(cudaMalloc(&e.fol_stage, static_cast<size_t>(e.maxB)));
   PS_CUDA(cudaMemsetAsync(e.route_ws, 0, sizeof(int32_t), e.sc));
   e.pred_dev = e.sched_dev + e.Et;
   e.pred2_dev = e.sched_dev + 2 * e.Et;
@@ -1759,6 +1829,10 @@ void destroy_engine(ps_engine_s& e) {
     if (p) cudaFreeHost(p);
   if (e.sc) cudaStreamSynchronize(e.sc);
   if (e.s_d2h) cudaStreamSynchronize(e.s_d2h);
+  for (auto& kv : e.sched_graphs) cudaGraphExecDestroy(kv.second);
+  e.sched_graphs.clear();
+  if (e.x_stage) cudaFree(e.x_stage);
+  if (e.fol_stage) cudaFree(e.fol_stage);
   for (auto& ld : e.layer) {
     cudaFree(ld.weights);
     cudaFree(ld.ids);

@@ -10,6 +10,8 @@
 // ranks equal experts with __match_any_sync, per-warp counts go through a [warps][E]
 // shared table, so positions are deterministic without global atomics.
 // Gather/combine passes: HBM-bound, 16-byte vectorised, one CTA row-slab each.
+#include <algorithm>
+
 #include "device_common.cuh"
 #include "permute_device.cuh"
 
@@ -248,6 +250,37 @@ __global__ void rows_from_host_kernel(const float4* __restrict__ src, int64_t n4
   }
 }
 
+// Several row ranges of the same mapped pinned buffer in ONE launch (the host lane's
+// experts of a layer): one launch per expert serialised ~3-35 us each behind the PCIe
+// traffic of the in-flight expert loads (Qwen3 shape: 8 launches, ~150 us per layer);
+// here every range's reads are in flight together. Rows [row0, row0 + m) of src/dst.
+constexpr int kMaxRowRanges = 128;
+struct RowRanges {
+  int n;
+  int row0[kMaxRowRanges];
+  int m[kMaxRowRanges];
+  int start[kMaxRowRanges + 1];  // prefix of m: flat row index -> range
+};
+
+__global__ void rows_from_host_ranges_kernel(const float4* __restrict__ src, float4* __restrict__ dst, int H4,
+                                             const __grid_constant__ RowRanges r, int zero_copies,
+                                             int64_t zero_stride4) {
+  const int64_t total = static_cast<int64_t>(r.start[r.n]) * H4;
+  for (int64_t i = blockIdx.x * static_cast<int64_t>(blockDim.x) + threadIdx.x; i < total;
+       i += static_cast<int64_t>(gridDim.x) * blockDim.x) {
+    const int flat = static_cast<int>(i / H4), c = static_cast<int>(i - static_cast<int64_t>(flat) * H4);
+    int lo = 0, hi = r.n - 1;
+    while (lo < hi) {
+      const int mid = (lo + hi + 1) >> 1;
+      if (r.start[mid] <= flat) lo = mid;
+      else hi = mid - 1;
+    }
+    const int64_t o = static_cast<int64_t>(r.row0[lo] + flat - r.start[lo]) * H4 + c;
+    dst[o] = src[o];
+    for (int z = 1; z <= zero_copies; ++z) dst[o + z * zero_stride4] = make_float4(0.f, 0.f, 0.f, 0.f);
+  }
+}
+
 // Shared experts (DeepSeek-style, always active, gate weight 1): appended as virtual
 // experts E..E+S-1 so permute / FFN / combine treat them like routed ones.
 __global__ void append_shared_kernel(const int32_t* __restrict__ ids, const float* __restrict__ w, int B, int k,
@@ -307,6 +340,40 @@ ps_status ps_rows_from_host(const float* host_src, int64_t n, float* dst, int ze
                                                                reinterpret_cast<float4*>(dst), zero_copies,
                                                                zero_stride / 4);
     PS_LAUNCH_CHECK("rows_from_host_kernel");
+  });
+}
+
+ps_status ps_rows_from_host_ranges(const float* host_base, const int32_t* row0, const int32_t* m, int n_ranges,
+                                   int H, float* dst, int zero_copies, int64_t zero_stride, void* stream) {
+  return guarded([&] {
+    require(n_ranges >= 0 && n_ranges <= kMaxRowRanges && H > 0 && H % 4 == 0 && zero_copies >= 0 &&
+                zero_stride % 4 == 0 && (n_ranges == 0 || (host_base && row0 && m && dst)),
+            "ps_rows_from_host_ranges: bad arguments (<= 128 ranges, H % 4 == 0)");
+    if (n_ranges == 0) return;
+    RowRanges r{};
+    r.n = n_ranges;
+    int64_t max_end = 0;
+    for (int i = 0; i < n_ranges; ++i) {
+      require(row0[i] >= 0 && m[i] >= 0, "ps_rows_from_host_ranges: negative range");
+      r.row0[i] = row0[i];
+      r.m[i] = m[i];
+      r.start[i + 1] = r.start[i] + m[i];
+      max_end = std::max<int64_t>(max_end, static_cast<int64_t>(row0[i]) + m[i]);
+    }
+    // zero-filled copies must not overlap any copied row
+    require(zero_copies == 0 || zero_stride >= max_end * H, "ps_rows_from_host_ranges: zero_stride too small");
+    if (r.start[n_ranges] == 0) return;
+    void* dev_src = nullptr;
+    PS_CUDA(cudaHostGetDevicePointer(&dev_src, const_cast<float*>(host_base), 0));
+    require((reinterpret_cast<uintptr_t>(dev_src) | reinterpret_cast<uintptr_t>(dst)) % 16 == 0,
+            "ps_rows_from_host_ranges: 16-byte alignment");
+    const int H4 = H / 4;
+    const int64_t total = static_cast<int64_t>(r.start[n_ranges]) * H4;
+    const int grid = static_cast<int>(std::max<int64_t>(1, std::min<int64_t>((total + 255) / 256, 148)));
+    rows_from_host_ranges_kernel<<<grid, 256, 0, as_stream(stream)>>>(static_cast<const float4*>(dev_src),
+                                                                       reinterpret_cast<float4*>(dst), H4, r,
+                                                                       zero_copies, zero_stride / 4);
+    PS_LAUNCH_CHECK("rows_from_host_ranges_kernel");
   });
 }
 

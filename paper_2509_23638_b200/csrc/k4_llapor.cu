@@ -61,6 +61,7 @@ struct ps_llapor_s {
   std::vector<std::pair<float*, size_t>> net_buf;  // per net: its device buffer and size (floats)
   std::vector<void*> allocs;
   int max_p = 0, max_in = 0, max_width = 0;
+  uint64_t generation = 0;       // bumped by every upload (a captured forward holds NetDev by value)
 };
 
 namespace ps {
@@ -69,8 +70,8 @@ namespace {
 constexpr int kPcaWarps = 8;     // warps per CTA (two component rows each)
 constexpr int kPcaChunk = 512;   // H elements per CTA (grid.y splits H)
 constexpr int kPcaTok = 16;      // tokens per pass
-constexpr int kMlpTokBig = 16;   // tokens per MLP CTA (batches > 16)
-constexpr int kMlpTokSmall = 4;  // tokens per MLP CTA (decode batches <= 16)
+constexpr int kMlpTokBig = 16;   // tokens per MLP CTA (batches > 64)
+constexpr int kMlpTokSmall = 4;  // tokens per MLP CTA (decode batches <= 64)
 constexpr int kMlpThreads = 512;
 
 // Stage 1 of pca_apply: part[s][t][p] = sum_{h in chunk s} comp[p][h] * (x[t][h] - mean[h]).
@@ -445,12 +446,23 @@ void upload(ps_llapor_s& m, int layer) {
   d.valid = 1;
   m.nets[layer] = d;
   m.stale[layer] = 0;
+  ++m.generation;
 }
 
 }  // namespace
 }  // namespace ps
 
 using namespace ps;
+
+// Engine helpers (C++ linkage): make net `layer`'s device copy current (outside any stream
+// capture), and the upload generation a CUDA graph of ps_llapor_forward was captured at.
+namespace ps {
+void llapor_prepare(ps_llapor m, int layer) {
+  if (m && layer >= 1 && layer < static_cast<int>(m->nets.size()) && m->nets[layer].valid && m->stale[layer])
+    upload(*m, layer);
+}
+uint64_t llapor_generation(ps_llapor m) { return m ? m->generation : 0; }
+}  // namespace ps
 
 extern "C" {
 
@@ -595,7 +607,7 @@ ps_status ps_llapor_forward(ps_llapor m, int layer, const float* hidden, const i
       const char* v = std::getenv("PS_LLAPOR_TOK");
       return v && v[0] == '1' && v[1] == '6';
     }();
-    const bool small = B <= 16 && !force_big;
+    const bool small = B <= 64 && !force_big;  // decode batches: 4 tokens per CTA (B = 32: 8 CTAs, not 2)
     const int tok = small ? kMlpTokSmall : kMlpTokBig;
     const size_t act = sizeof(float) * tok * (net.in_dim + 3 * maxh + net.E);
     const size_t staged = act + sizeof(float) * ((net.mlp_floats + 3) / 4 * 4);

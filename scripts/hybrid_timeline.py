@@ -21,11 +21,14 @@ def main():
     import torch
     ap = argparse.ArgumentParser()
     ap.add_argument("--lookahead", type=int, default=0)
+    ap.add_argument("--model", default="mixtral")
+    ap.add_argument("--batch", type=int, default=16)
+    ap.add_argument("--summary", action="store_true", help="omit the per-layer rows")
     args = ap.parse_args()
-    spec = ps.spec_preset("mixtral")
+    spec = ps.spec_preset(args.model)
     gen = ps.TraceGenConfig(*[ps.GROUP_DEFAULT_GEN[g] for g in ("input", "middle", "output")])
     L, E, H = spec.num_layers, spec.experts_per_layer, spec.hidden_dim
-    B, S = 16, 6
+    B, S = args.batch, 6
     gate, hidden, follow, zipf = ps.trace_inputs(gen, spec, B * S, 1000)
     _, wh, wf, _ = ps.trace_inputs(gen, spec, 64, 1000, want_gate=False)
     freq = eng.hot_table(spec, gate, wh, wf, zipf)
@@ -33,7 +36,8 @@ def main():
     resident = ps.plan_residency(freq, budget, spec.expert_bytes)
     lib = ps.load()
     pred = C.c_void_p()
-    ps.check(lib.ps_llapor_random(C.byref(spec), 256, 512, 32, 48, 3, C.byref(pred)))
+    p_in, p_mid = (256, 512) if args.model == "mixtral" else (128, 256)
+    ps.check(lib.ps_llapor_random(C.byref(spec), p_in, p_mid, 32, 48, 3, C.byref(pred)))
     e = eng.Engine(spec, gen, max_batch=B, weight_seed=1, gate=gate, budget_bytes=budget, resident=resident,
                    policy="presched", predictor=pred, host_threads=bench.default_host_threads(), compress_host=True,
                    lookahead=args.lookahead)
@@ -69,7 +73,12 @@ def main():
     gaps = [(r["cpu_start"] - r["start"]) for r in rows if r["cpu_start"] is not None]
     tails = [(r["end"] - r["cpu_end"]) for r in rows if r["cpu_end"] is not None]
     print(json.dumps({"cost": e.stats()["cost"], "step_us": tot, "cpu_busy_us": cpu_busy, "layer_start_to_lane_start_us_mean": float(np.mean(gaps)),
-                      "lane_end_to_layer_end_us_mean": float(np.mean(tails)), "layers": rows}))
+                      "lane_end_to_layer_end_us_mean": float(np.mean(tails)),
+                      "sched_end_minus_start_us_mean": float(np.mean([r["sched_end"] - r["start"] for r in rows
+                                                                      if r["sched_end"] is not None])),
+                      "n_cpu_mean": float(np.mean([r["n_cpu"] for r in rows])),
+                      "n_load_mean": float(np.mean([r["n_load"] for r in rows])),
+                      "layers": [] if args.summary else rows}))
     e.close()
 
 

@@ -383,3 +383,33 @@ def test_rows_from_host_reads_mapped_pinned_rows(torch_cuda):
     for bad_stride in (n - 4, -stride):  # overlapping or negative zero-fill ranges are rejected
         assert lib.ps_rows_from_host(C.c_void_p(src.data_ptr()), n, C.c_void_p(dst.data_ptr()), 1, bad_stride,
                                      None) == ps.capi.PS_EINVAL
+
+
+def test_rows_from_host_ranges_one_launch(torch_cuda):
+    """ps_rows_from_host_ranges: several row ranges of one mapped pinned buffer (the host
+    lane's experts of a layer) in one launch — exactly those rows copied, the rows between
+    ranges untouched, the zero-filled split copies of the copied rows zero."""
+    torch = torch_cuda
+    lib = ps.load()
+    H, rows, splits = 2048, 40, 3
+    src = torch.randn(rows * H).pin_memory()
+    dst = torch.full((splits * rows * H,), float("nan"), device="cuda")
+    row0 = np.array([0, 3, 10, 11, 30], np.int32)
+    m = np.array([2, 5, 1, 0, 10], np.int32)
+    ps.check(lib.ps_rows_from_host_ranges(C.c_void_p(src.data_ptr()), row0.ctypes.data, m.ctypes.data, len(row0), H,
+                                          C.c_void_p(dst.data_ptr()), splits - 1, rows * H,
+                                          C.c_void_p(torch.cuda.current_stream().cuda_stream)))
+    torch.cuda.synchronize()
+    out = dst.cpu().view(splits, rows, H)
+    s2 = src.view(rows, H)
+    copied = np.zeros(rows, bool)
+    for r0, mm in zip(row0, m):
+        copied[r0:r0 + mm] = True
+    for r in range(rows):
+        if copied[r]:
+            assert torch.equal(out[0, r], s2[r])
+            assert torch.equal(out[1:, r], torch.zeros(splits - 1, H))
+        else:
+            assert torch.isnan(out[:, r]).all()
+    assert lib.ps_rows_from_host_ranges(C.c_void_p(src.data_ptr()), row0.ctypes.data, m.ctypes.data, len(row0), H,
+                                        C.c_void_p(dst.data_ptr()), 1, 39 * H, None) == ps.capi.PS_EINVAL
