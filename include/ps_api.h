@@ -288,8 +288,8 @@ ps_status ps_route_topk(const float* x, const float* gate, const float* bias,
 /* K1 + K2 index pass in ONE launch for decode batches (1 <= B <= 64): the route CTAs as
  * in ps_route_topk (no histogram: counts = diff of offsets), then the last CTA to finish
  * runs the counting-sort permute of ps_permute over all B*k ids (bit-identical outputs).
- * workspace: one int32 on the device, zero before the first call (the kernel leaves it
- * zero); one workspace per stream. */
+ * workspace: 65 int32 on the device (a launch ticket + per-token tickets of the E >= 64
+ * split), zero before the first call (the kernel leaves them zero); one per stream. */
 ps_status ps_route_permute(const float* x, const float* gate, const float* bias,
                            const uint8_t* follow, const int32_t* prev_ids, int prev_k, int B,
                            int H, int E, int k, float* weights, int32_t* ids, uint16_t* x_bf16,

@@ -1698,14 +1698,14 @@ void create_engine(const ps_engine_config& cfg, ps_engine_s& e) {
   PS_CUDA(cudaMemsetAsync(e.sched_dev, 0, sizeof(int32_t) * n_sched, e.sc));
   PS_CUDA(cudaHostAlloc(&e.pinned_counts, sizeof(int32_t) * n_sched, cudaHostAllocDefault));
   e.counts_dev = e.sched_dev;
-  PS_CUDA(cudaMalloc(&e.route_ws, sizeof(int32_t)));
+  PS_CUDA(cudaMalloc(&e.route_ws, sizeof(int32_t) * 65));
   if (e.use_graphs) {
     const char* g = std::getenv("PS_SCHED_GRAPH");  // 0: eager scheduling point (A/B)
     e.use_graphs = !(g && g[0] == '0');
   }
   PS_CUDA(cudaMalloc(&e.x_stage, sizeof(float) * static_cast<size_t>(e.maxB) * e.H));
   PS_CUDA(cudaMalloc(&e.fol_stage, static_cast<size_t>(e.maxB)));
-  PS_CUDA(cudaMemsetAsync(e.route_ws, 0, sizeof(int32_t), e.sc));
+  PS_CUDA(cudaMemsetAsync(e.route_ws, 0, sizeof(int32_t) * 65, e.sc));
   e.pred_dev = e.sched_dev + e.Et;
   e.pred2_dev = e.sched_dev + 2 * e.Et;
   e.offsets = e.sched_dev + 3 * e.Et;

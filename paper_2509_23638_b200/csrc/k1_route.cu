@@ -275,6 +275,103 @@ route_kernel(const float* __restrict__ x, const float* __restrict__ gate, const 
   }
 }
 
+// Decode route + permute with many experts (E >= 64): the token's experts are split over
+// E/32 CTAs (B * E/32 CTAs instead of B), each computing 32 logits exactly as
+// route_kernel<1> does (same per-warp H slice, same per-lane order, warp_sum, warp sums
+// in fixed order: bitwise the same logits); the last CTA of a token (per-token ticket)
+// gathers its logits and finishes it (kappa override, softmax, top-k); the last CTA of
+// the launch permutes. The logits go through `weights` (overwritten by the softmax
+// weights). Qwen3 shape (E = 128, B = 32): 32 CTAs each streaming the whole 1 MiB gate
+// matrix took ~27 us.
+constexpr int kSplitE = 32;
+
+__global__ void __launch_bounds__(kWarps * 32)
+route_split_kernel(const float* __restrict__ x, const float* __restrict__ gate, const float* __restrict__ bias,
+                   const uint8_t* __restrict__ follow, const int32_t* __restrict__ prev_ids, int prev_k, int B, int H,
+                   int E, int k, float sqrt_h, float* __restrict__ weights_out, int32_t* __restrict__ ids_out,
+                   uint16_t* __restrict__ x_bf16, FusedPermute fp, int* __restrict__ tok_cnt) {
+  __shared__ float s_part[kWarps][kSplitE];
+  __shared__ float s_logit[kMaxE];
+  __shared__ int s_flag;
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const int groups = (E + kSplitE - 1) / kSplitE;
+  const int b = blockIdx.x / groups, grp = blockIdx.x - b * groups;
+  const int e_lo = grp * kSplitE, e_hi = min(E, e_lo + kSplitE);
+  constexpr int kU = 2;
+  const int hs = ((H / 4 + kWarps - 1) / kWarps) * 4;
+  const int h_lo = min(H, warp * hs), h_hi = min(H, h_lo + hs);
+  for (int e0 = e_lo; e0 < e_hi; e0 += kETile) {
+    float acc[kETile];
+#pragma unroll
+    for (int j = 0; j < kETile; ++j) acc[j] = 0.f;
+    for (int hb = h_lo + lane * 4; hb < h_hi; hb += 128 * kU) {
+      float4 xv[kU], g[kU][kETile];
+#pragma unroll
+      for (int u = 0; u < kU; ++u) {
+        const int h = hb + 128 * u;
+        const bool hin = h < h_hi;
+        xv[u] = hin ? *reinterpret_cast<const float4*>(x + static_cast<size_t>(b) * H + h) : make_float4(0.f, 0.f, 0.f, 0.f);
+#pragma unroll
+        for (int j = 0; j < kETile; ++j)
+          g[u][j] = hin && e0 + j < E ? __ldg(reinterpret_cast<const float4*>(gate + static_cast<size_t>(e0 + j) * H + h))
+                                      : make_float4(0.f, 0.f, 0.f, 0.f);
+      }
+#pragma unroll
+      for (int u = 0; u < kU; ++u) {
+#pragma unroll
+        for (int j = 0; j < kETile; ++j)
+          acc[j] += g[u][j].x * xv[u].x + g[u][j].y * xv[u].y + g[u][j].z * xv[u].z + g[u][j].w * xv[u].w;
+        const int h = hb + 128 * u;
+        if (x_bf16 && e0 == 0 && h < h_hi) {
+          uint2 o;
+          o.x = (uint32_t)f32_to_bf16_rne(xv[u].x) | ((uint32_t)f32_to_bf16_rne(xv[u].y) << 16);
+          o.y = (uint32_t)f32_to_bf16_rne(xv[u].z) | ((uint32_t)f32_to_bf16_rne(xv[u].w) << 16);
+          *reinterpret_cast<uint2*>(x_bf16 + static_cast<size_t>(b) * H + h) = o;
+        }
+      }
+    }
+#pragma unroll
+    for (int j = 0; j < kETile; ++j) {
+      const float sum = warp_sum(acc[j]);
+      if (lane == 0 && e0 + j < e_hi) s_part[warp][e0 + j - e_lo] = sum;
+    }
+  }
+  __syncthreads();
+  if (threadIdx.x < e_hi - e_lo) {
+    float sum = 0.f;
+#pragma unroll
+    for (int w = 0; w < kWarps; ++w) sum += s_part[w][threadIdx.x];
+    const int e = e_lo + threadIdx.x;
+    weights_out[static_cast<size_t>(b) * E + e] = sum * sqrt_h + (bias ? bias[e] : 0.f);
+  }
+  __threadfence();
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    s_flag = atomicAdd(tok_cnt + b, 1) == groups - 1;
+    if (s_flag) tok_cnt[b] = 0;  // every group of this token has arrived
+  }
+  __syncthreads();
+  if (s_flag) {  // this token's last CTA: all of its logits are in `weights` (L2)
+    __threadfence();
+    for (int e = threadIdx.x; e < E; e += kWarps * 32) s_logit[e] = __ldcg(weights_out + static_cast<size_t>(b) * E + e);
+    __syncthreads();
+    if (warp == 0)
+      finish_token_impl(0, b, s_logit, follow, prev_ids, prev_k, E, k, nullptr, weights_out, ids_out, nullptr);
+  }
+  // the launch's last CTA permutes all B*k ids (as route_kernel<1, true>)
+  __shared__ int s_last;
+  __shared__ int s_base[kPermMaxE + 1];
+  __shared__ int s_warp_cnt[kWarps][kPermMaxE];
+  __threadfence();
+  __syncthreads();
+  if (threadIdx.x == 0) s_last = atomicAdd(fp.done, 1) == static_cast<int>(gridDim.x) - 1;
+  __syncthreads();
+  if (!s_last) return;
+  __threadfence();
+  permute_block<kWarps * 32, true>(ids_out, B * k, E, fp.offsets, fp.perm_src, fp.inv, s_base, s_warp_cnt);
+  if (threadIdx.x == 0) *fp.done = 0;
+}
+
 }  // namespace
 }  // namespace ps
 
@@ -326,6 +423,14 @@ extern "C" ps_status ps_route_permute(const float* x, const float* gate, const f
     require((reinterpret_cast<uintptr_t>(x) & 15) == 0 && (reinterpret_cast<uintptr_t>(gate) & 15) == 0,
             "ps_route_permute: x and gate must be 16-byte aligned");
     const float sqrt_h = static_cast<float>(std::sqrt(static_cast<double>(H)));
+    if (E >= 2 * kSplitE && (H & 3) == 0) {
+      const int groups = (E + kSplitE - 1) / kSplitE;
+      route_split_kernel<<<B * groups, kWarps * 32, 0, as_stream(stream)>>>(
+          x, gate, bias, follow, prev_ids, prev_k, B, H, E, k, sqrt_h, weights, ids, x_bf16,
+          FusedPermute{offsets, perm_src, inv, workspace}, workspace + 1);
+      PS_LAUNCH_CHECK("route_split_kernel");
+      return;
+    }
     route_kernel<1, true><<<B, kWarps * 32, kWarps * 1 * E * 4, as_stream(stream)>>>(
         x, gate, bias, follow, prev_ids, prev_k, B, H, E, k, sqrt_h, nullptr, weights, ids, nullptr, x_bf16,
         FusedPermute{offsets, perm_src, inv, workspace});

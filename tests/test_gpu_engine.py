@@ -179,7 +179,10 @@ def test_engine_set_cost_and_calibrate_semantics(torch_cuda):
         e.step_host(hidden, follow)
         assert e.stats()["cpu_experts"] > 0
         c = e.calibrate()
-        assert c["beta"] == 1.0 and c["startup"] >= 0 and c["t_io"] > c["t_g"]
+        # beta is kept unless fit_cost_params found a physical fit of the lane samples
+        # (timing-dependent), in which case the fitted beta is positive
+        fitted = e.stats()["calibration_fit"]
+        assert (c["beta"] == 1.0 or (fitted and c["beta"] > 0)) and c["startup"] >= 0 and c["t_io"] > c["t_g"]
 
 
 @pytest.mark.parametrize("budget,host_threads", [(0.5, 0), (0.25, 2)])
