@@ -210,7 +210,8 @@ void amx_config() {
 // of 32 row streams — the hardware prefetchers keep far more lines in flight per core.
 template <bool kTiled>
 __attribute__((target("amx-tile,amx-bf16,avx512f")))
-void amx_gate_up_block(const uint16_t* wg, const uint16_t* wu, const uint16_t* xb, int H, int r, uint16_t* hb) {
+void amx_gate_up_block(const uint16_t* wg, const uint16_t* wu, const uint16_t* xb, int H, int r, uint16_t* hb,
+                       int mt) {
   alignas(64) float cg[16 * 16], cu[16 * 16];
   const size_t pitch = kTiled ? 64 : static_cast<size_t>(H) * 2;
   const uint16_t* ag = wg + static_cast<size_t>(r) * H;
@@ -239,9 +240,10 @@ void amx_gate_up_block(const uint16_t* wg, const uint16_t* wu, const uint16_t* x
   }
   _tile_stored(0, cg, 64);
   _tile_stored(1, cu, 64);
-  // C[i][t] = row r+i, token t -> hb[((r+i)/2)*16 + t][(r+i)%2]
+  // C[i][t] = row r+i, token t -> hb[((r+i)/2)*16 + t][(r+i)%2]. Only the group's mt real
+  // tokens: a padded column of hb only feeds its own (discarded) output column in phase 2.
   for (int i = 0; i < 16; ++i)
-    for (int t = 0; t < kTok; ++t) {
+    for (int t = 0; t < mt; ++t) {
       const float g = cg[i * 16 + t], u = cu[i * 16 + t];
       hb[(static_cast<size_t>((r + i) >> 1) * kTok + t) * 2 + ((r + i) & 1)] = f32_to_bf16_rn(g / (1.0f + std::exp(-g)) * u);
     }
@@ -430,7 +432,8 @@ inline void z_tile2(const ZView& z, const ZRegs& r, uint32_t seg_bytes, uint64_t
 }
 
 __attribute__((target("amx-tile,amx-bf16,avx512f,avx512bw,avx512vl,avx512vbmi,avx512vbmi2")))
-void amx_gate_up_block_z(const ZView& z, const ZDec& d, int H, int F, const uint16_t* xb, int r, uint16_t* hb) {
+void amx_gate_up_block_z(const ZView& z, const ZDec& d, int H, int F, const uint16_t* xb, int r, uint16_t* hb,
+                         int mt) {
   alignas(64) float cg[16 * 16], cu[16 * 16];
   // two scratch sets, alternated per step: the next step's decode stores do not wait for
   // this step's tile loads (write-after-read on one buffer serialises decode and AMX)
@@ -461,8 +464,8 @@ void amx_gate_up_block_z(const ZView& z, const ZDec& d, int H, int F, const uint
   }
   _tile_stored(0, cg, 64);
   _tile_stored(1, cu, 64);
-  for (int i = 0; i < 16; ++i)
-    for (int t = 0; t < kTok; ++t) {
+  for (int i = 0; i < 16; ++i)  // the group's mt real tokens only (see amx_gate_up_block)
+    for (int t = 0; t < mt; ++t) {
       const float g = cg[i * 16 + t], u = cu[i * 16 + t];
       hb[(static_cast<size_t>((r + i) >> 1) * kTok + t) * 2 + ((r + i) & 1)] = f32_to_bf16_rn(g / (1.0f + std::exp(-g)) * u);
     }
@@ -649,7 +652,7 @@ ps_status expert_ffn_batch(ps_host_lane l, int n, const uint16_t* const* slabs, 
               for (int g = 0; g * kTok < m[j]; ++g)
                 (tiled ? amx_gate_up_block<true> : amx_gate_up_block<false>)(
                     wg, wu, xb + xo[j] + static_cast<size_t>(g) * H * kTok, H, blk * 16,
-                    hb + ho[j] + static_cast<size_t>(g) * F * kTok);
+                    hb + ho[j] + static_cast<size_t>(g) * F * kTok, std::min(kTok, m[j] - g * kTok));
               done[j].fetch_add(1, std::memory_order_release);
             } else {
               const int64_t v = u - U1;
@@ -676,7 +679,7 @@ ps_status expert_ffn_batch(ps_host_lane l, int n, const uint16_t* const* slabs, 
           for (int g = 0; g * kTok < m[j]; ++g)
             (tiled ? amx_gate_up_block<true> : amx_gate_up_block<false>)(
                 wg, wu, xb + xo[j] + static_cast<size_t>(g) * H * kTok, H, blk * 16,
-                hb + ho[j] + static_cast<size_t>(g) * F * kTok);
+                hb + ho[j] + static_cast<size_t>(g) * F * kTok, std::min(kTok, m[j] - g * kTok));
         });
         amx_release();
       });
@@ -814,7 +817,7 @@ ps_status ps_host_expert_ffn_batch_z(ps_host_lane l, int n, const uint8_t* const
         const int j = static_cast<int>(u / nb1), blk = static_cast<int>(u % nb1);
         for (int g = 0; g * kTok < m[j]; ++g)
           amx_gate_up_block_z(zv[j], zd[j], H, F, xb + xo[j] + static_cast<size_t>(g) * H * kTok, blk * 16,
-                              hb + ho[j] + static_cast<size_t>(g) * F * kTok);
+                              hb + ho[j] + static_cast<size_t>(g) * F * kTok, std::min(kTok, m[j] - g * kTok));
       });
       amx_release();
     });
