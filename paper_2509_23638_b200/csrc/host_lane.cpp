@@ -812,6 +812,18 @@ ps_status ps_host_expert_ffn_batch_z(ps_host_lane l, int n, const uint8_t* const
       }
     std::atomic<int64_t> next1{0}, next2{0};
     std::atomic<int> arrived{0};
+    auto phase2 = [&] {
+      for_units(U2, T, next2, [&](int64_t u) {
+        const int j = static_cast<int>(u / nb2), blk = static_cast<int>(u % nb2);
+        for (int g = 0; g * kTok < m[j]; ++g)
+          amx_down_block_z(zv[j], zd[j], hb + ho[j] + static_cast<size_t>(g) * F * kTok, H, F, blk * 16,
+                           std::min(kTok, m[j] - g * kTok), y + static_cast<size_t>(row0[j] + g * kTok) * H);
+      });
+    };
+    static const bool split_runs = [] {  // PS_HOST_LANE_SPLITRUN=1: one pool run per phase (A/B)
+      const char* v = std::getenv("PS_HOST_LANE_SPLITRUN");
+      return v && v[0] == '1';
+    }();
     // One pool run for both phases with a spin barrier between them: a second run wakes
     // the workers through the futex again (~10-30 us per pass, a large share of a layer's
     // lane time when the experts are small: Qwen3, 9 MiB).
@@ -823,17 +835,22 @@ ps_status ps_host_expert_ffn_batch_z(ps_host_lane l, int n, const uint8_t* const
           amx_gate_up_block_z(zv[j], zd[j], H, F, xb + xo[j] + static_cast<size_t>(g) * H * kTok, blk * 16,
                               hb + ho[j] + static_cast<size_t>(g) * F * kTok, std::min(kTok, m[j] - g * kTok));
       });
+      if (split_runs) {
+        amx_release();
+        return;
+      }
       // phase barrier: every h row written (release) before any down unit reads it (acquire)
       arrived.fetch_add(1, std::memory_order_acq_rel);
       while (arrived.load(std::memory_order_acquire) < T) _mm_pause();
-      for_units(U2, T, next2, [&](int64_t u) {
-        const int j = static_cast<int>(u / nb2), blk = static_cast<int>(u % nb2);
-        for (int g = 0; g * kTok < m[j]; ++g)
-          amx_down_block_z(zv[j], zd[j], hb + ho[j] + static_cast<size_t>(g) * F * kTok, H, F, blk * 16,
-                           std::min(kTok, m[j] - g * kTok), y + static_cast<size_t>(row0[j] + g * kTok) * H);
-      });
+      phase2();
       amx_release();
     });
+    if (split_runs)
+      l->pool->run([&](int) {
+        amx_config();
+        phase2();
+        amx_release();
+      });
   });
 }
 

@@ -45,6 +45,7 @@ def main():
     run("mixtral", 3, 8, 256, 512, 256, 0.5)
     run("mixtral", 3, 8, 256, 512, 8, 0.25, compress_host=True)
     run("mixtral", 3, 8, 256, 512, 256, 0.5, compress_host=True)
+    run("qwen3", 3, 128, 256, 256, 32, 0.5, host_threads=2, cost=cost)  # split router, ranged lane rows
     lib = ps.load()
     for kern, name in ((0, "single-CTA"), (1, "CTA-pair"), (3, "token-N")):  # every tcgen05 prefill kernel
         ps.check(lib.ps_set_prefill_kernel(kern))
