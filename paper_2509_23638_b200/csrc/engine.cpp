@@ -842,11 +842,27 @@ void layer_forward(ps_engine_s& e, int l, const float* x, const uint8_t* follow,
       }
       if (predict) PS_CUDA(cudaStreamWaitEvent(e.sc, e.ev_pred[0], 0));  // join
       if (predict2) PS_CUDA(cudaStreamWaitEvent(e.sc, e.ev_pred[1], 0));
+      // --- K2 permute indices (non-EP; EP permutes owner-major below) ----------------
+      // Prefill-sized batches gather x into contiguous permuted rows (TMA operand of the
+      // tcgen05 path).
+      if (!e.ep) {
+        if (e.S) {
+          s = ps_append_shared(ld.ids, ld.weights, B, K, E, e.S, e.ids_ext, e.w_ext, nullptr, e.sc);
+          if (s != PS_OK) fail(s, ps_last_error());
+        }
+        if (!fused_perm) {
+          s = ps_permute(e.S ? e.ids_ext : ld.ids, B, Kt, Et, e.offsets, e.perm_src, e.inv,
+                         e.prefill_mode ? e.x_bf16 : nullptr, H, e.prefill_mode ? e.x_perm : nullptr, e.sc);
+          if (s != PS_OK) fail(s, ps_last_error());
+        }
+      }
     };
-    e.st.kernel_launches += 1 + (predict ? (e.pred_kind == PS_PRED_LLAPOR ? 2 : 1) : 0) + (predict2 ? 2 : 0);
-    // Graph replay: decode with the fused route+permute and LLaPor (or no) prediction.
-    const bool graph_ok = e.use_graphs && fused_perm && !(predict && e.pred_kind == PS_PRED_PERFECT) &&
-                          B <= e.maxB && e.x_stage;
+    e.st.kernel_launches += 1 + (predict ? (e.pred_kind == PS_PRED_LLAPOR ? 2 : 1) : 0) + (predict2 ? 2 : 0) +
+                            (!e.ep && e.S ? 1 : 0) + (!e.ep && !fused_perm ? (e.prefill_mode ? 2 : 1) : 0);
+    // Graph replay: decode (fused or separate route + permute, shared experts) with the
+    // LLaPor (or no) prediction; EP, prefill chunks and trace replay stay eager.
+    const bool graph_ok = e.use_graphs && !e.ep && !e.prefill_mode && !routed_ids &&
+                          !(predict && e.pred_kind == PS_PRED_PERFECT) && B <= e.maxB && e.x_stage;
     if (graph_ok) {
       if (predict) llapor_prepare(e.cfg.predictor, l + 1);  // device copies current before a capture/replay
       if (predict2) llapor_prepare(e.cfg.predictor, l + 2);
@@ -890,17 +906,6 @@ void layer_forward(ps_engine_s& e, int l, const float* x, const uint8_t* follow,
     // tcgen05 path) and need the offsets on the host for tile scheduling.
     const int Ev = e.G * e.E_loc;  // owner-major virtual expert count under EP
     if (!e.ep) {
-      if (e.S) {
-        s = ps_append_shared(ld.ids, ld.weights, B, K, E, e.S, e.ids_ext, e.w_ext, nullptr, e.sc);
-        if (s != PS_OK) fail(s, ps_last_error());
-        e.st.kernel_launches += 1;
-      }
-      if (!fused_perm) {
-        s = ps_permute(e.S ? e.ids_ext : ld.ids, B, Kt, Et, e.offsets, e.perm_src, e.inv,
-                       e.prefill_mode ? e.x_bf16 : nullptr, H, e.prefill_mode ? e.x_perm : nullptr, e.sc);
-        if (s != PS_OK) fail(s, ps_last_error());
-        e.st.kernel_launches += e.prefill_mode ? 2 : 1;
-      }
       // counts | pred | offsets (| perm_src for the host lane) in one copy, on the side
       // stream: the compute stream goes straight on to the resident FFN while the copy
       // engine brings the scheduling inputs to the host.
