@@ -1096,8 +1096,9 @@ CUtensorMap make_map_f32(const void* base, uint64_t rows, uint64_t cols, uint32_
 // Persistent device table of tensor maps for the token-N kernel. A map is a pure function
 // of (address, rows, cols, box, element size), so an entry is encoded once, copied to the
 // device once (in stream order, before the first kernel that uses it) and never modified:
-// launches pass indices. Capacity 32768 maps (4 MiB); a full table is an error (the
-// engines of a process use ~2 maps per resident slab plus a few dozen per chunk buffer).
+// launches pass indices. Capacity 32768 maps (4 MiB); a full table is emptied after a
+// device synchronisation (the engines of a process use ~2 maps per resident slab plus a
+// few dozen per chunk size).
 struct MapKey {
   const void* base;
   uint64_t rows, cols;
@@ -1114,11 +1115,26 @@ struct MapKeyHash {
   }
 };
 struct MapTable {
-  static constexpr int kCap = 32768;
+  // capacity (maps): PS_MAPTABLE_CAP for tests of the overflow path, else 32768
+  const int kCap = [] {
+    const char* v = std::getenv("PS_MAPTABLE_CAP");
+    const int c = v ? std::atoi(v) : 32768;
+    return c >= 64 ? c : 32768;
+  }();
   CUtensorMap* dev = nullptr;
   CUtensorMap* host = nullptr;  // pinned mirror: entry i is written once, before its copy
   int used = 0;
   std::unordered_map<MapKey, int, MapKeyHash> index;
+  // Called once per launch, before its get()s: room for `n` new entries. A full table
+  // (engines come and go, chunk sizes vary) is emptied once every enqueued kernel has run —
+  // launches happen under the caller's mutex, so every user of the table is enqueued —
+  // and nothing references an entry any more.
+  void reserve(int n) {
+    if (used + n <= kCap) return;
+    PS_CUDA(cudaDeviceSynchronize());
+    index.clear();
+    used = 0;
+  }
   int get(const MapKey& k, cudaStream_t s) {
     auto it = index.find(k);
     if (it != index.end()) return it->second;
@@ -1126,7 +1142,7 @@ struct MapTable {
       PS_CUDA(cudaMalloc(&dev, sizeof(CUtensorMap) * kCap));
       PS_CUDA(cudaHostAlloc(&host, sizeof(CUtensorMap) * kCap, cudaHostAllocDefault));
     }
-    if (used >= kCap) fail(PS_ERUNTIME, "ps_expert_ffn_prefill: tensor-map table full");
+    if (used >= kCap) fail(PS_ERUNTIME, "ps_expert_ffn_prefill: tensor-map table: reserve() missing");
     const int i = used++;
     host[i] = k.esize == 4 ? make_map_f32(k.base, k.rows, k.cols, k.box_cols, k.box_rows)
                            : encode_map(k.base, k.rows, k.cols, k.box_rows);
@@ -1271,6 +1287,7 @@ extern "C" ps_status ps_expert_ffn_prefill(const ps_expert_group* group, const i
         PS_CUDA(cudaMemset(done_dev, 0, sizeof(unsigned) * MapRing::kSlots * kMaxExperts));
       }
       static MapTable table;
+      table.reserve(2 * group->n + 2 * 17 + 1);
       TnParams tp{};
       tp.F = F;
       tp.H = H;
@@ -1439,6 +1456,7 @@ extern "C" ps_status ps_expert_ffn_prefill_dev(const ps_expert_group* group, con
       PS_CUDA(cudaMalloc(&done_dev, sizeof(unsigned) * MapRing::kSlots * kMaxExperts));
     }
     const int slot = ring.acquire();
+    table.reserve(2 * group->n + 2 * 17 + 1);
     TnParams tp{};
     tp.F = F;
     tp.H = H;

@@ -250,3 +250,33 @@ def test_prefill_device_schedule_matches_host_schedule(torch_cuda, H, F, E, k, B
     for h, yp in outs[1:]:
         assert np.array_equal(h, outs[0][0])
         assert np.array_equal(yp, outs[0][1])
+
+
+def test_prefill_map_table_overflow_restarts(tmp_path):
+    """The token-N kernel's persistent tensor-map table (weights by slab, tokens by chunk
+    size) empties itself after a device sync when full: in a process whose table holds only
+    64 maps, 12 prefill calls with 12 different chunk sizes (and both entry points) still
+    match the oracle. Subprocess: the capacity is read once per process."""
+    import subprocess
+    import sys
+    code = r"""
+import ctypes as C, sys, numpy as np, torch
+sys.path.insert(0, %r)
+sys.path.insert(0, %r)
+import oracle as orc, paper_2509_23638_b200 as ps
+from test_gpu_prefill import _explicit_counts_case, _rel
+lib = ps.load()
+for i in range(12):
+    counts = [5 + 17 * i, 33, 1 + i, 64]
+    ys, y_ref = _explicit_counts_case(torch, 256, 256, counts, 100 + i, reps=1)
+    assert _rel(ys[0], y_ref) < 2e-2, (i, _rel(ys[0], y_ref))
+print("ok")
+""" % (str(tests_root()), str(tests_root().parent))
+    env = dict(__import__("os").environ, PS_MAPTABLE_CAP="64")
+    r = subprocess.run([sys.executable, "-c", code], env=env, capture_output=True, text=True, timeout=600)
+    assert r.returncode == 0 and "ok" in r.stdout, r.stdout + r.stderr
+
+
+def tests_root():
+    import pathlib
+    return pathlib.Path(__file__).resolve().parent
