@@ -271,12 +271,12 @@ for i in range(12):
     ys, y_ref = _explicit_counts_case(torch, 256, 256, counts, 100 + i, reps=1)
     assert _rel(ys[0], y_ref) < 2e-2, (i, _rel(ys[0], y_ref))
 print("ok")
-""" % (str(tests_root()), str(tests_root().parent))
+""" % (str(_tests_dir()), str(_tests_dir().parent))
     env = dict(__import__("os").environ, PS_MAPTABLE_CAP="64")
     r = subprocess.run([sys.executable, "-c", code], env=env, capture_output=True, text=True, timeout=600)
     assert r.returncode == 0 and "ok" in r.stdout, r.stdout + r.stderr
 
 
-def tests_root():
+def _tests_dir():
     import pathlib
     return pathlib.Path(__file__).resolve().parent
