@@ -163,8 +163,11 @@ def run_reference_arm(args):
         print(json.dumps({"impl": "reference", "unavailable": "oracle/_ref/libprescope_ref.so not built"}))
         return
     from oracle.cpu_arm import RefArm
+    # our arm's workload at N GPUs is a global batch of N x batch tokens per step (weak
+    # scaling): the reference arm steps the same global batch on the host cores
+    gb = args.batch * max(1, args.gpus)
     t_init = time.perf_counter()
-    arm = RefArm(args.model, args.batch, args.budget, steps=args.warmup + args.steps, weight_seed=args.weight_seed)
+    arm = RefArm(args.model, gb, args.budget, steps=args.warmup + args.steps, weight_seed=args.weight_seed)
     t_init = time.perf_counter() - t_init
     phases = {}
     times = []
@@ -181,13 +184,13 @@ def run_reference_arm(args):
     L = arm.L
     arm.close()
     step_s = sum(times) / len(times)
-    value = args.batch / step_s
-    desc = (f"whole B={args.batch} decode steps ({args.steps} timed after {args.warmup} warm-up, no extrapolation): "
+    value = gb / step_s
+    desc = (f"whole B={gb} decode steps ({args.steps} timed after {args.warmup} warm-up, no extrapolation): "
             f"reference router + LLaPor P=256/512 + simulate_policy(presched) via oracle/_ref, experts+combine via "
             f"oracle/cpu_port.c on all {L} layers, {threads} host threads")
-    cfg = {"workload": f"{args.model}-shape MoE decode, {L} layers, batch {args.batch}, budget {args.budget:.0%}: "
+    cfg = {"workload": f"{args.model}-shape MoE decode, {L} layers, batch {gb}, budget {args.budget:.0%}: "
                        "the reference's CPU path (oracle/_ref) + CPU expert port",
-           "decode_batch": args.batch, "global_batch": args.batch, "budget_fraction": args.budget}
+           "decode_batch": args.batch, "global_batch": gb, "budget_fraction": args.budget}
     line = {"impl": "reference", "metric": METRIC, "value": value, "unit": "tokens/s", "n_gpus": args.gpus,
             "steps": args.steps, "warmup": args.warmup, "ms_per_step": step_s * 1e3, "higher_is_better": True,
             "scaling": "weak", "vs_baseline": None, "dtype": "bf16 weights, f32/f64 accumulate",
