@@ -820,13 +820,14 @@ ps_status ps_host_expert_ffn_batch_z(ps_host_lane l, int n, const uint8_t* const
                            std::min(kTok, m[j] - g * kTok), y + static_cast<size_t>(row0[j] + g * kTok) * H);
       });
     };
-    static const bool split_runs = [] {  // PS_HOST_LANE_SPLITRUN=1: one pool run per phase (A/B)
+    // One pool run per phase (default). PS_HOST_LANE_SPLITRUN=0: both phases in one run
+    // with a spin barrier between them (saves a futex wake per batch, but in the engine a
+    // descheduled lane thread — the engine and I/O threads share the cores — holds 15
+    // spinning threads: Qwen3 host lane 900 -> 400-560 tok/s, r02_configs_qwen3_splitrun.jsonl).
+    static const bool split_runs = [] {
       const char* v = std::getenv("PS_HOST_LANE_SPLITRUN");
-      return v && v[0] == '1';
+      return !(v && v[0] == '0');
     }();
-    // One pool run for both phases with a spin barrier between them: a second run wakes
-    // the workers through the futex again (~10-30 us per pass, a large share of a layer's
-    // lane time when the experts are small: Qwen3, 9 MiB).
     l->pool->run([&](int) {
       amx_config();
       for_units(U1, T, next1, [&](int64_t u) {

@@ -92,6 +92,23 @@ def trace_steps(torch, gen, spec, B, S, seed):
     return hid, fol
 
 
+def finetune(torch, e, pred, spec, gen, B, steps, seed=4242, epochs=3, lr=3e-3):
+    """Online LLaPor fine_tune (ps_llapor_fine_tune = predictor.cpp:654-663) on a separate
+    warm-up trace before any measurement: decode a step, fine-tune every net on its
+    observations, repeat. Replaces the random-init predictor by one trained the way the
+    reference's online path trains it."""
+    if steps <= 0 or pred is None:
+        return
+    _, hidden, follow, _ = ps.trace_inputs(gen, spec, B * steps, seed, want_gate=False)
+    y = torch.empty(spec.num_layers, B, spec.hidden_dim, device="cuda")
+    for s in range(steps):
+        h = np.ascontiguousarray(hidden[s * B:(s + 1) * B].transpose(1, 0, 2), np.float32)
+        f = np.ascontiguousarray(follow[s * B:(s + 1) * B].T)
+        e.step_device(torch.as_tensor(h, device="cuda"), torch.as_tensor(f, device="cuda"), y)
+        torch.cuda.synchronize()
+        e.fine_tune_predictor(pred, h, steps=epochs, lr=lr)
+
+
 def setup(model):
     spec = ps.spec_preset(model)
     gen = ps.TraceGenConfig(*[ps.GROUP_DEFAULT_GEN[g] for g in ("input", "middle", "output")])
@@ -112,10 +129,13 @@ def run_qwen3(torch, args, ht):
     B = 32
     pred = llapor(spec, 128, 256)
     e = make_engine(spec, gen, gate, freq, args.budget, B, pred, ht)
+    finetune(torch, e, pred, spec, gen, B, args.finetune)
     hid, fol = trace_steps(torch, gen, spec, B, args.warmup + args.steps, 2000)
     y = torch.empty(spec.num_layers, B, spec.hidden_dim, device="cuda")
-    decode_points(torch, "qwen3-30b-a3b-shape decode B=32, LLaPor-driven prefetch (random-init LLaPor P=128/256)",
-                  spec, e, B, hid, fol, y, args, {"budget_fraction": args.budget})
+    tag = (f"LLaPor P=128/256 fine-tuned online on {args.finetune} warm-up steps" if args.finetune
+           else "random-init LLaPor P=128/256")
+    decode_points(torch, f"qwen3-30b-a3b-shape decode B=32, LLaPor-driven prefetch ({tag})",
+                  spec, e, B, hid, fol, y, args, {"budget_fraction": args.budget, "llapor_finetune_steps": args.finetune})
     e.close()
     ps.load().ps_llapor_free(pred)
 
@@ -188,6 +208,7 @@ def main():
     ap.add_argument("--warmup", type=int, default=2)
     ap.add_argument("--host-threads", type=int, default=-1)
     ap.add_argument("--compress", type=int, default=1)
+    ap.add_argument("--finetune", type=int, default=0, help="warm-up steps of online LLaPor fine_tune (qwen3)")
     args = ap.parse_args()
     import torch
     torch.cuda.set_device(0)
