@@ -220,7 +220,10 @@ def workload_config(args, spec, executor="gpu_only"):
                         + (", loads as lossless z-slabs decoded on the GPU" if getattr(args, "compress", 0)
                            else "")
                         + f", predictor {getattr(args, 'predictor', 'llapor')}"
-                        + (" (random-init at full shape)" if getattr(args, "predictor", "llapor") == "llapor" else ""),
+                        + ((f" (full shape, fine-tuned online on {args.llapor_finetune} warm-up steps of a separate "
+                            "trace: ps_llapor_fine_tune = predictor.cpp:654-663)" if getattr(args, "llapor_finetune", 0)
+                            else " (random-init at full shape)")
+                           if getattr(args, "predictor", "llapor") == "llapor" else ""),
             "expert_shape": f"{args.model}-8x7b" if args.model == "mixtral" else args.model,
             "decode_batch": args.batch, "global_batch": args.batch * args.gpus,
             "parallelism": (f"ep{args.gpus}" if args.gpus > 1 else "single"),
@@ -293,6 +296,15 @@ def run_ours(args):
     t_create = time.perf_counter() - t_create
     torch.cuda.synchronize()
     hbm_engine = free0 - torch.cuda.mem_get_info(local)[0]
+    t_ft = 0.0
+    if args.llapor_finetune and args.predictor == "llapor":
+        # online LLaPor fine_tune on a separate warm-up trace (not the measured steps), before
+        # any timed region: the reference trains its predictor, random init is the weak case
+        sys.path.insert(0, str(ROOT / "scripts"))
+        import configs_bench
+        t_ft = time.perf_counter()
+        configs_bench.finetune(torch, e, predictor, spec, gen, B, args.llapor_finetune, seed=4242 + rank)
+        t_ft = time.perf_counter() - t_ft
     thp_gb = anon_huge_gb()  # the host arenas ask for transparent huge pages (lane TLB reach)
     measured_cost = e.stats()["cost"]
 
@@ -509,7 +521,7 @@ def run_ours(args):
                                      "their z-slab landing buffers + routing/FFN scratch), cudaMemGetInfo delta"},
         "host_memory": {"anon_huge_pages_gb": thp_gb, "note": "transparent huge pages backing the pinned host "
                         "arenas after engine create (/proc/self/smaps_rollup); the lane streams them"},
-        "wall_s_timed": wall, "engine_create_s": t_create,
+        "wall_s_timed": wall, "engine_create_s": t_create, "llapor_finetune_s": t_ft,
         "cost_params_us": st["cost"],
     }
     print(json.dumps(line))
@@ -723,6 +735,8 @@ def main():
                          "(0 with --steal-late 0: no extra leg; the headline is always plain PreSched)")
     ap.add_argument("--steal-late", type=int, default=1,
                     help="1: the host lane computes committed prefetches whose copies land too late")
+    ap.add_argument("--llapor-finetune", type=int, default=0,
+                    help="warm-up steps of online LLaPor fine_tune on a separate trace before measuring")
     ap.add_argument("--host-threads", type=int, default=-1,
                     help="host expert lane threads (-1 auto, 0 = GPU-only executor)")
     args = ap.parse_args()
