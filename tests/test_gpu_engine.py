@@ -280,3 +280,35 @@ def test_engine_host_lane_lookahead_and_late_steal(torch_cuda, lookahead):
     assert np.linalg.norm(y - y_ref) / np.linalg.norm(y_ref) < BF16_RTOL
     assert (st["lookahead_prefetches"] > 0) == (lookahead > 0)
     assert st["stolen_prefetches"] <= st["prefetches_committed"]
+
+
+@pytest.mark.parametrize("preset,E,n_shared", [("mixtral", 8, 0), ("qwen3", 128, 0), ("deepseek", 64, 2)])
+def test_engine_scheduling_point_graph_equals_eager(torch_cuda, monkeypatch, preset, E, n_shared):
+    """The decode scheduling point replayed from CUDA graphs (default) gives bitwise the
+    outputs and routing of the eager launches (PS_SCHED_GRAPH=0), over several steps
+    (graph reuse) and with LLaPor predictions."""
+    import ctypes as C
+    lib = ps.load()
+    spec = _small_spec(L=4, E=E, H=256, F=256, preset=preset)
+    cfg = ps.TraceGenConfig(*[ps.GROUP_DEFAULT_GEN[g] for g in ("input", "middle", "output")])
+    B = 8
+    gate, hidden, follow, _ = ps.trace_inputs(cfg, spec, 3 * B, 5)
+    pred = C.c_void_p()
+    ps.check(lib.ps_llapor_random(C.byref(spec), 16, 32, 16, 24, 3, C.byref(pred)))
+    outs = []
+    try:
+        for graph in ("1", "0"):
+            monkeypatch.setenv("PS_SCHED_GRAPH", graph)
+            with eng.Engine(spec, cfg, budget_fraction=0.5, max_batch=B, weight_seed=9, gate=gate,
+                            trace_hidden=hidden[:B], trace_follow=follow[:B], predictor=pred,
+                            n_shared=n_shared) as e:
+                res = []
+                for s in range(3):
+                    y, ids = e.step_host(hidden[s * B:(s + 1) * B], follow[s * B:(s + 1) * B])
+                    res.append((y.copy(), ids.copy()))
+                outs.append(res)
+    finally:
+        lib.ps_llapor_free(pred)
+    for (ya, ia), (yb, ib) in zip(*outs):
+        assert np.array_equal(ia, ib)
+        assert np.array_equal(ya, yb)
