@@ -176,11 +176,13 @@ def run_deepseek(torch, args, ht):
     print(json.dumps(d), flush=True)
     e_full.close()
     del ph, py
+    e.set_cost(**cost)
+    finetune(torch, e, pred, spec, gen, B, args.finetune)
     hid, fol = trace_steps(torch, gen, spec, B, args.warmup + args.steps, 3000)
     y = torch.empty(L, B, H, device="cuda")
-    e.set_cost(**cost)
-    decode_points(torch, "deepseek-v2-lite-shape decode B=16 after prefill (64 routed top-6 + 2 shared)", spec, e, B,
-                  hid, fol, y, args, {"budget_fraction": args.budget})
+    decode_points(torch, "deepseek-v2-lite-shape decode B=16 after prefill (64 routed top-6 + 2 shared)"
+                  + (f", LLaPor fine-tuned online on {args.finetune} warm-up steps" if args.finetune else ""),
+                  spec, e, B, hid, fol, y, args, {"budget_fraction": args.budget, "llapor_finetune_steps": args.finetune})
     e.close()
     ps.load().ps_llapor_free(pred)
 
