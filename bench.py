@@ -382,6 +382,20 @@ def run_ours(args):
         e2e_s = float(t.item())
     h2d_in = hid_lm[0].numel() * 4 + fol_lm[0].numel()
     d2h_out = y_h.numel() * 4 + ids_h.numel() * 4
+    # Extra leg (after the headline's e2e): the same plain PreSched executor with the LLaPor
+    # nets fine-tuned online (ps_llapor_fine_tune = predictor.cpp:654-663) on a separate
+    # warm-up trace. The trained nets predict the hot, resident experts, PreSched then issues
+    # no prefetches and the few loads are on-demand (so little H2D time is hidden), and the
+    # lane takes the rest: faster in paired runs (profiles/README.md), reported beside.
+    if args.ft_leg and e.host_threads and args.predictor == "llapor" and not args.llapor_finetune:
+        sys.path.insert(0, str(ROOT / "scripts"))
+        import configs_bench
+        t_ft = time.perf_counter()
+        configs_bench.finetune(torch, e, predictor, spec, gen, B, args.ft_leg, seed=4242 + rank)
+        t_ft = time.perf_counter() - t_ft
+        e.set_cost(**measured_cost)
+        e.set_lookahead(0, False)
+        legs["host_lane_llapor_ft"] = decode_leg(calibrate=True)
     e.close()
     # In-bench checksum (outside every timed region): the last e2e step's outputs vs the
     # CPU oracle — ids of all layers vs the f64 reference router, y of two layers vs the
@@ -480,7 +494,7 @@ def run_ours(args):
         traffic = tj["traffic_over_algorithmic"] * ffn_bytes / ffn_launches
         traffic_src = f"{tj['source']}: traffic/algorithmic = {tj['traffic_over_algorithmic']:.4f}"
     leg_summary = {name: decode_summary(lst, lms, N, B, L) for name, (lst, lms, _, _) in legs.items()}
-    for name in ("host_lane", "host_lane_lookahead"):
+    for name in ("host_lane", "host_lane_lookahead", "host_lane_llapor_ft"):
         if "cpu_lane" in leg_summary.get(name, {}):
             leg_summary[name]["cpu_lane"]["threads"] = host_threads
     cpu_step_s, cpu_desc, cpu_legs, cpu_threads = (cpu_sample(args) if not args.no_cpu_baseline
@@ -502,6 +516,8 @@ def run_ours(args):
         "executor": head,
         "host_lane": leg_summary.get("host_lane"),
         "host_lane_lookahead": leg_summary.get("host_lane_lookahead"),
+        "host_lane_llapor_ft": (dict(leg_summary["host_lane_llapor_ft"], llapor_finetune_steps=args.ft_leg,
+                                     llapor_finetune_s=t_ft) if "host_lane_llapor_ft" in leg_summary else None),
         "gpu_only": leg_summary["gpu_only"],
         "cpu_baseline": ({"value": args.batch / cpu_step_s, "unit": "tokens/s", "cores": cpu_threads,
                           "kind": "reference", "sample": cpu_desc, "host": host_info(),
@@ -737,6 +753,9 @@ def main():
                     help="1: the host lane computes committed prefetches whose copies land too late")
     ap.add_argument("--llapor-finetune", type=int, default=0,
                     help="warm-up steps of online LLaPor fine_tune on a separate trace before measuring")
+    ap.add_argument("--ft-leg", type=int, default=16,
+                    help="extra leg host_lane_llapor_ft: plain PreSched after N warm-up steps of online "
+                         "LLaPor fine_tune (0: skip)")
     ap.add_argument("--host-threads", type=int, default=-1,
                     help="host expert lane threads (-1 auto, 0 = GPU-only executor)")
     args = ap.parse_args()
