@@ -72,17 +72,6 @@ __device__ __forceinline__ uint32_t z_code_pair(const uint32_t (&cw)[BITS + 1], 
 // Row-major start of the 32-value tile row at tiled index v, in 32-bit arithmetic
 // (z_untile's 64-bit division is a ~100-instruction subroutine; the host checks
 // n = 3HF < 2^32 for tiled slabs).
-// z_untile32 with the two divisions by K/32 done as multiply-highs: q = umulhi(n, m),
-// m = ceil(2^32 / d), exact for n * d < 2^32 (n = tile index < 3HF/512 < 2^23, d <= 2^11).
-__device__ __forceinline__ uint32_t z_untile32m(uint32_t v, uint32_t H, uint32_t F, uint32_t mh, uint32_t mf) {
-  const uint32_t fh = F * H;
-  const uint32_t base = v < fh ? 0u : (v < 2u * fh ? fh : 2u * fh);
-  const bool gu = v < 2u * fh;
-  const uint32_t K = gu ? H : F;
-  const uint32_t t = v - base, tile = t >> 9, i = (t >> 5) & 15u, nkb = K >> 5;
-  const uint32_t rb = __umulhi(tile, gu ? mh : mf), kb = tile - rb * nkb;
-  return base + (rb * 16u + i) * K + kb * 32u;
-}
 __device__ __forceinline__ uint32_t z_untile32(uint32_t v, uint32_t H, uint32_t F) {
   const uint32_t fh = F * H;
   const uint32_t base = v < fh ? 0u : (v < 2u * fh ? fh : 2u * fh);
@@ -406,16 +395,21 @@ z_decode_kernel_v4(const uint8_t* __restrict__ z, uint64_t n, uint32_t base, uin
     __syncwarp();
     if (vb + kZBlock <= n) {
       if (tile_h) {
-        // A tiled block is two 16x32 tiles of the same 16 weight rows, K-adjacent (K/32 is
-        // even): segment i and 16 + i are one 128 B run of output row i. Each warp store
-        // writes 4 rows x 128 B (whole lines) instead of 8 tile rows x 64 B.
-        const uint64_t my_off = static_cast<uint64_t>(z_untile32m(static_cast<uint32_t>(v0), tile_h, tile_f, mh, mf));
+        // A tiled block is two 16x32 tiles of the same 16 weight rows, K-adjacent (K/64 is
+        // whole, checked by the host): segment i and 16 + i are one 128 B run of output row
+        // i. The block's (row, column) origin is computed once per block (warp-uniform);
+        // each warp store writes 4 rows x 128 B (whole lines).
+        const uint32_t vbl = static_cast<uint32_t>(vb), fh = tile_f * tile_h;
+        const uint32_t mat = vbl < fh ? 0u : (vbl < 2u * fh ? 1u : 2u);
+        const uint32_t K = mat < 2 ? tile_h : tile_f;
+        const uint32_t T = (vbl - mat * fh) >> 9;  // even tile index within the matrix
+        const uint32_t rb = __umulhi(T, mat < 2 ? mh : mf), kb = T - rb * (K >> 5);
+        uint16_t* blk = out + mat * fh + rb * 16u * K + kb * 32u;
 #pragma unroll
         for (int rr = 0; rr < 4; ++rr) {
           const int row = 4 * rr + (lane >> 3), j = lane & 7;
           const int sl = j < 4 ? row : 16 + row, q = j & 3;
-          const uint64_t row_off = __shfl_sync(0xffffffffu, my_off, row);
-          *reinterpret_cast<uint4*>(out + row_off + 8 * j) = so[chunk(sl, q)];
+          *reinterpret_cast<uint4*>(blk + static_cast<uint32_t>(row) * K + 8 * j) = so[chunk(sl, q)];
         }
       } else {
 #pragma unroll
@@ -740,7 +734,8 @@ ps_status ps_zslab_decode(const uint8_t* z_dev, const uint8_t* z_host_header, ui
         z_decode_kernel_v1<3><<<grid1, threads, 0, as_stream(stream)>>>(z_dev, h.n, h.base, h.nb, th, tf, out);
       else
         z_decode_kernel_v1<4><<<grid1, threads, 0, as_stream(stream)>>>(z_dev, h.n, h.base, h.nb, th, tf, out);
-    } else if (version == 4 && h.code_bits == 3 && h.base + z_escape(h.code_bits) < 256) {
+    } else if (version == 4 && h.code_bits == 3 && h.base + z_escape(h.code_bits) < 256 &&
+               (!h.tiled || (th % 64 == 0 && tf % 64 == 0))) {
       // v4 for 3-bit codes (151 -> 119 us per Mixtral expert); 4-bit codes (0.01 % escapes)
       // gain nothing from its escape path and stay on v3 (113-116 us either way)
       z_decode_kernel_v4<3><<<grid, threads, 0, as_stream(stream)>>>(z_dev, h.n, h.base, h.nb, th, tf, out);

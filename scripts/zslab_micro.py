@@ -22,7 +22,8 @@ def main():
     ps.check(lib.ps_init_expert_slab_host(slab.ctypes.data, H, F, 1, 0, 0))
     tiled_slab = slab.copy()
     ps.check(lib.ps_host_slab_tile(tiled_slab.ctypes.data, H, F))
-    for bits, tiled in (("3", 0), ("4", 0), ("3", 1)):
+    for bits, tiled in [tuple(c.split(":")) for c in os.environ.get("ZMICRO_CASES", "3:0,4:0,3:1").split(",")]:
+        tiled = int(tiled)
         os.environ["PS_ZSLAB_BITS"] = bits
         cap = lib.ps_zslab_bound(n)
         z = np.zeros(cap, np.uint8)
