@@ -396,7 +396,12 @@ inline void z_decode64(const ZView& z, const ZRegs& r, uint32_t seg_bytes, uint6
 // prefetched 4 blocks ahead.
 __attribute__((target("avx512f,avx512bw,avx512vl,avx512vbmi,avx512vbmi2")))
 inline void z_run1024(const ZView& z, const ZRegs& r, uint32_t seg_bytes, uint64_t v, uint64_t vend, uint16_t* out) {
-  if (v + 4096 < vend) {
+  // Prefetch 4 blocks ahead, across the unit's end too: a thread's next unit is usually the
+  // adjacent 16-row block of the same slab, and small units (Qwen3's W_down: 12 blocks)
+  // otherwise start cold on every unit. (Prefetches never fault; past the slab they only
+  // touch other host memory.)
+  (void)vend;
+  {
     const char* pl = reinterpret_cast<const char*>(z.lo + v + 4096);
     for (int q = 0; q < 16; ++q) _mm_prefetch(pl + 64 * q, _MM_HINT_T0);
     const char* pc = reinterpret_cast<const char*>(z.codes + (v + 4096) / 64 * seg_bytes);
