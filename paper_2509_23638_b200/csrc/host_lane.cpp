@@ -400,11 +400,19 @@ inline void z_run1024(const ZView& z, const ZRegs& r, uint32_t seg_bytes, uint64
   // adjacent 16-row block of the same slab, and small units (Qwen3's W_down: 12 blocks)
   // otherwise start cold on every unit. (Prefetches never fault; past the slab they only
   // touch other host memory.)
-  (void)vend;
-  {
-    const char* pl = reinterpret_cast<const char*>(z.lo + v + 4096);
+  static const bool unit_only = [] {  // PS_LANE_PF_UNIT=1: round 1's within-unit prefetch (A/B)
+    const char* e = std::getenv("PS_LANE_PF_UNIT");
+    return e && e[0] == '1';
+  }();
+  static const uint64_t ahead = [] {  // PS_LANE_PF_BLOCKS: prefetch distance in 1024-value blocks (A/B)
+    const char* e = std::getenv("PS_LANE_PF_BLOCKS");
+    const int b = e ? std::atoi(e) : 4;
+    return static_cast<uint64_t>(b >= 1 && b <= 64 ? b : 4) * 1024;
+  }();
+  if (!unit_only || v + ahead < vend) {
+    const char* pl = reinterpret_cast<const char*>(z.lo + v + ahead);
     for (int q = 0; q < 16; ++q) _mm_prefetch(pl + 64 * q, _MM_HINT_T0);
-    const char* pc = reinterpret_cast<const char*>(z.codes + (v + 4096) / 64 * seg_bytes);
+    const char* pc = reinterpret_cast<const char*>(z.codes + (v + ahead) / 64 * seg_bytes);
     for (uint32_t q = 0; q < seg_bytes / 4; ++q) _mm_prefetch(pc + 64 * q, _MM_HINT_T0);  // 16 x seg_bytes
   }
   const uint8_t* ep = z.esc + z.esc_off[v / kZBlock];
