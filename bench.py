@@ -368,6 +368,12 @@ def run_ours(args):
     fol_lm = [torch.from_numpy(np.ascontiguousarray(f.numpy().T)).pin_memory() for f in fol_h]
     y_h = torch.empty(L, B, H, dtype=torch.float32).pin_memory()
     ids_h = torch.empty(L, B, k, dtype=torch.int32).pin_memory()
+    def step_host(s):
+        ps.check(lib.ps_engine_decode_step_host(e.h, C.c_void_p(hid_lm[s].data_ptr()),
+                                                C.c_void_p(fol_lm[s].data_ptr()), B,
+                                                C.c_void_p(y_h.data_ptr()), C.c_void_p(ids_h.data_ptr())))
+    for s in range(args.warmup):  # untimed warm-up of the host-buffer entry point (its staging)
+        step_host(s)
     if dist:
         dist.barrier()
     t0 = time.perf_counter()
