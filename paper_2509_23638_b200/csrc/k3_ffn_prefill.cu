@@ -600,14 +600,20 @@ ffn_prefill_pair_kernel(const __grid_constant__ PrefillParams p) {
 // only grow: targets are host-side running sums per map-ring slot, nothing is reset). A
 // pair waits only on gate_up tiles, which never wait, and all pairs are co-resident (grid
 // <= the device's max active 2-CTA clusters), so the wait cannot deadlock.
-constexpr int kTnStages = 6;
 constexpr int kTnABytes = 128 * kBK * 2;                 // 16 KiB of weight rows
-constexpr int kTnBMaxBytes = 128 * kBK * 2;              // <= 128 token rows per CTA
-constexpr int kTnStageBytes = kTnABytes + kTnBMaxBytes;  // 32 KiB
 constexpr int kTnXchgBytes = 2 * 2 * 2 * 16 * 32 * 4;    // gate <-> up hand-off: 2 bufs x 2 pairs x 2 senders x 16 x 32
 constexpr int kTnStageOutBytes = 4 * 32 * 32 * 4;         // y staging: 4 epilogue warps x 32 tokens x 32 features f32
-constexpr int kTnSmemBytes = kTnStages * kTnStageBytes + kTnXchgBytes + kTnStageOutBytes + 1024 + 256;
-constexpr int kTnMaxN = 256;
+constexpr int kTnMaxN = 256;                              // largest token tile (MMA N)
+// Ring geometry per maximum token tile MAXN (256: 6 stages of 16 + 16 KiB; 128: 8 stages
+// of 16 + 8 KiB, i.e. a third more weight bytes in flight per SM, and an expert of more
+// than 128 rows is split into equal token tiles that share the weight rows through L2).
+template <int MAXN> struct TnGeo {
+  static constexpr int kBMaxBytes = (MAXN / 2) * kBK * 2;
+  static constexpr int kStageBytes = kTnABytes + kBMaxBytes;
+  static constexpr int kStages = MAXN == 256 ? 6 : 8;
+  static constexpr int kSmem = kStages * kStageBytes + kTnXchgBytes + kTnStageOutBytes + 1024 + 256;
+  static_assert(kSmem <= 227 * 1024, "token-N smem");
+};
 constexpr uint32_t kTnSignalsPerTile = 2 * 4;            // epilogue warps of both CTAs
 
 // Tensor maps live in a persistent device table (MapTable below: every map is a pure
@@ -630,7 +636,7 @@ struct TnPhase {
 struct TnSched {
   int n_experts;                    // active entries (m_e > 0)
   int gidx[kMaxExperts];            // group index of active entry i (its w_idx)
-  int t_tiles[kMaxExperts];         // token tiles per entry (ceil(m_e / 256))
+  int t_tiles[kMaxExperts];         // token tiles per entry (ceil(m_e / MAXN), equal widths)
   int row0[kMaxExperts];
   int rows[kMaxExperts];
   unsigned target[kMaxExperts];     // done[e] value once all of e's gate_up tiles are stored
@@ -638,6 +644,7 @@ struct TnSched {
   // then the last D down segments (D >= n: every gate_up tile first, the default). A down
   // segment trailing its gate_up by a few experts finds its h rows still in L2, but its
   // acquire may wait (profiles/r02_prefill_tn.md). seg_code = entry | phase << 16.
+  int maxn, even;                   // largest token tile; equal-width token tiles (default)
   int n_seg;
   int seg_start[2 * kMaxExperts + 1];
   int seg_code[2 * kMaxExperts];
@@ -658,6 +665,15 @@ struct TnTile {
   bool last;
 };
 
+// Token tiles of an expert with m rows split into tt tiles: ceil(m / tt) rounded up to 32
+// (the epilogue's chunk width; <= MAXN since MAXN is a multiple of 32), the last tile
+// takes the rest.
+// even == 0 (PS_TN_EVEN=0, A/B knob): MAXN-wide tiles, the last takes the rest.
+__host__ __device__ __forceinline__ int tn_tile_width(int m, int tt, int even, int maxn) {
+  if (!even && tt > 1) return maxn;
+  return tt == 1 ? (m + 15) & ~15 : ((m + tt - 1) / tt + 31) & ~31;
+}
+
 __device__ __forceinline__ TnTile tn_tile(const TnSched& p, int t) {
   TnTile c;
   int lo = 0, hi = p.n_seg - 1;
@@ -673,9 +689,10 @@ __device__ __forceinline__ TnTile tn_tile(const TnSched& p, int t) {
   const int t_tile = local % tt;  // token tiles fastest: concurrent tiles share the weight rows
   c.entry = lo;
   c.n_tile = local / tt;
-  c.tok0 = t_tile * kTnMaxN;
+  const int ts = tn_tile_width(p.rows[lo], tt, p.even, p.maxn);  // equal widths (multiples of 32)
+  c.tok0 = t_tile * ts;
   const int rem = p.rows[lo] - c.tok0;
-  c.n = rem >= kTnMaxN ? kTnMaxN : (rem + 15) & ~15;
+  c.n = rem >= ts ? ts : (rem + 15) & ~15;
   c.last = t_tile == tt - 1;
   return c;
 }
@@ -685,8 +702,12 @@ __device__ __forceinline__ void named_bar_sync(int id, int n) {
 }
 
 
+template <int MAXN>
 __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads, 1)
 ffn_prefill_tn_kernel(const __grid_constant__ TnParams p) {
+  using G = TnGeo<MAXN>;
+  constexpr int kTnStages = G::kStages;
+  constexpr int kTnStageBytes = G::kStageBytes;
   extern __shared__ __align__(1024) uint8_t smem_raw[];
   uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
   float* xchg = reinterpret_cast<float*>(smem + kTnStages * kTnStageBytes);  // [2][2][2][16][32]
@@ -790,7 +811,7 @@ ffn_prefill_tn_kernel(const __grid_constant__ TnParams p) {
                                (static_cast<uint32_t>(256 >> 4) << 24);
         mbar_wait(&tempty_bar[as], aphase ^ 1);
         tc_fence_after();
-        const uint32_t d = tmem_base + static_cast<uint32_t>(as * kTnMaxN);
+        const uint32_t d = tmem_base + static_cast<uint32_t>(as * MAXN);
         for (int kb = 0; kb < k_blocks; ++kb) {
           mbar_wait(&full_bar[stage], phase);
           tc_fence_after();
@@ -833,8 +854,8 @@ ffn_prefill_tn_kernel(const __grid_constant__ TnParams p) {
       const TnPhase& ph = p.ph[tc.phase];
       mbar_wait(&tfull_bar[as], aphase);
       tc_fence_after();
-      const uint32_t tbase = tmem_base + static_cast<uint32_t>(as * kTnMaxN) + (static_cast<uint32_t>(quarter * 32) << 16);
-      const int m_left = S.rows[tc.entry] - tc.tok0;  // valid token columns of this tile
+      const uint32_t tbase = tmem_base + static_cast<uint32_t>(as * MAXN) + (static_cast<uint32_t>(quarter * 32) << 16);
+      const int m_left = min(S.rows[tc.entry] - tc.tok0, tc.n);  // valid token columns of this tile
       const size_t row_base = static_cast<size_t>(S.row0[tc.entry] + tc.tok0);
       if (tc.phase == 0) {
         // quarters 0/1 hold gate, 2/3 up of features [32 (q & 1), +32) of this CTA's 64.
@@ -940,6 +961,7 @@ ffn_prefill_tn_kernel(const __grid_constant__ TnParams p) {
 // default order). Also zeroes the active entries' gate_up counters (the slot's previous
 // kernels are complete: the host reuses a ring slot only after its event).
 struct TnSchedArgs {
+  int maxn, even;  // largest token tile; equal-width tiles
   int n_group;
   int expert[kMaxExperts];
   int n0, n1;  // weight-row tiles per expert: gate_up, down
@@ -954,7 +976,7 @@ tn_schedule_kernel(const int32_t* __restrict__ offsets, const __grid_constant__ 
   if (i < a.n_group) m = __ldg(offsets + a.expert[i] + 1) - __ldg(offsets + a.expert[i]);
   const int row0 = i < a.n_group ? __ldg(offsets + a.expert[i]) : 0;
   const int act = m > 0 ? 1 : 0;
-  const int tt = (m + kTnMaxN - 1) / kTnMaxN;
+  const int tt = (m + a.maxn - 1) / a.maxn;
   int v[3] = {act, tt * a.n0, tt * a.n1};
   int incl[3];
 #pragma unroll
@@ -994,6 +1016,8 @@ tn_schedule_kernel(const int32_t* __restrict__ offsets, const __grid_constant__ 
     done[e] = 0u;
   }
   if (i == 0) {
+    out->maxn = a.maxn;
+    out->even = a.even;
     out->n_experts = n;
     out->n_seg = 2 * n;
     out->seg_start[2 * n] = total[1] + total[2];
@@ -1192,15 +1216,31 @@ void launch_pair(PrefillParams& p, cudaStream_t s) {
   PS_LAUNCH_CHECK("ffn_prefill_pair_kernel");
 }
 
-void launch_tn(TnParams& p, cudaStream_t s) {
+// Largest token tile of the token-N kernel: 256 (default) or 128 (PS_TN_MAXN; read per
+// call, A/B knob).
+int tn_maxn() {
+  const char* v = std::getenv("PS_TN_MAXN");
+  return v && std::atoi(v) == 128 ? 128 : 256;
+}
+
+// Equal-width token tiles for experts with more than MAXN rows (default 1; PS_TN_EVEN=0
+// restores MAXN-wide tiles + a remainder tile; read per call, A/B knob).
+int tn_even() {
+  const char* v = std::getenv("PS_TN_EVEN");
+  return v && v[0] == '0' ? 0 : 1;
+}
+
+template <int MAXN>
+void launch_tn_t(TnParams& p, cudaStream_t s) {
+  using G = TnGeo<MAXN>;
   static int max_pairs = 0;
   if (!max_pairs) {
-    PS_CUDA(cudaFuncSetAttribute(ffn_prefill_tn_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, kTnSmemBytes));
+    PS_CUDA(cudaFuncSetAttribute(ffn_prefill_tn_kernel<MAXN>, cudaFuncAttributeMaxDynamicSharedMemorySize, G::kSmem));
     // every pair must be co-resident (a down tile may wait on any pair's gate_up tile)
     cudaLaunchConfig_t cfg{};
     cfg.gridDim = dim3(2 * (kNumSMs / 2));
     cfg.blockDim = dim3(kThreads);
-    cfg.dynamicSmemBytes = kTnSmemBytes;
+    cfg.dynamicSmemBytes = G::kSmem;
     cudaLaunchAttribute attr[1];
     attr[0].id = cudaLaunchAttributeClusterDimension;
     attr[0].val.clusterDim.x = 2;
@@ -1209,15 +1249,20 @@ void launch_tn(TnParams& p, cudaStream_t s) {
     cfg.attrs = attr;
     cfg.numAttrs = 1;
     int clusters = 0;
-    PS_CUDA(cudaOccupancyMaxActiveClusters(&clusters, ffn_prefill_tn_kernel, &cfg));
+    PS_CUDA(cudaOccupancyMaxActiveClusters(&clusters, ffn_prefill_tn_kernel<MAXN>, &cfg));
     if (clusters < 1) fail(PS_ECUDA, "ffn_prefill_tn_kernel: no 2-CTA cluster fits on this device");
     max_pairs = std::min(clusters, kNumSMs / 2);
   }
   const int tiles = p.sched_dev ? max_pairs : p.sched.seg_start[p.sched.n_seg];  // device schedule: all pairs
   if (tiles == 0) return;
   const int grid = 2 * std::min(tiles, max_pairs);
-  ffn_prefill_tn_kernel<<<grid, kThreads, kTnSmemBytes, s>>>(p);
+  ffn_prefill_tn_kernel<MAXN><<<grid, kThreads, G::kSmem, s>>>(p);
   PS_LAUNCH_CHECK("ffn_prefill_tn_kernel");
+}
+
+void launch_tn(TnParams& p, cudaStream_t s, int maxn) {
+  if (maxn == 128) launch_tn_t<128>(p, s);
+  else launch_tn_t<256>(p, s);
 }
 
 // Kernel choice: 0 = single-CTA, 1 = CTA pairs, 2 = auto, 3 = token-N CTA pairs.
@@ -1296,6 +1341,9 @@ extern "C" ps_status ps_expert_ffn_prefill(const ps_expert_group* group, const i
       tp.ph[0].n_tiles_n = F / 128;
       tp.ph[1].n_tiles_n = H / 256;
       unsigned* shadow = done_host.data() + slot * kMaxExperts;
+      const int maxn = tn_maxn();
+      tp.sched.maxn = maxn;
+      tp.sched.even = tn_even();
       int n = 0;
       bool used_half[17] = {};
       for (int i = 0; i < group->n; ++i) {
@@ -1306,10 +1354,11 @@ extern "C" ps_status ps_expert_ffn_prefill(const ps_expert_group* group, const i
         tp.ph[0].w_idx[n] = table.get(MapKey{slab, 2ull * F, static_cast<uint64_t>(H), 64, 64, 2}, s);
         tp.ph[1].w_idx[n] = table.get(MapKey{slab + 2ull * F * H, static_cast<uint64_t>(H), static_cast<uint64_t>(F),
                                              64, 128, 2}, s);
-        const int tt = (m + kTnMaxN - 1) / kTnMaxN;
-        const int rem = m - (tt - 1) * kTnMaxN;
+        const int tt = (m + maxn - 1) / maxn;
+        const int ts = tn_tile_width(m, tt, tp.sched.even, maxn);
+        const int rem = m - (tt - 1) * ts;
         used_half[((rem + 15) & ~15) / 16] = true;  // last tile: N/2 = 8j rows
-        if (tt > 1) used_half[16] = true;
+        if (tt > 1) used_half[ts / 16] = true;
         tp.sched.gidx[n] = n;
         tp.sched.t_tiles[n] = tt;
         tp.sched.row0[n] = offsets_host[e];
@@ -1373,10 +1422,10 @@ extern "C" ps_status ps_expert_ffn_prefill(const ps_expert_group* group, const i
         TnParams second = tp;
         build_segments(tp, 1);
         build_segments(second, 2);
-        launch_tn(tp, s);
-        launch_tn(second, s);
+        launch_tn(tp, s, maxn);
+        launch_tn(second, s, maxn);
       } else {
-        launch_tn(tp, s);
+        launch_tn(tp, s, maxn);
       }
       // the slot's counters advance only once the launch is enqueued (a failed launch
       // leaves them where the next use of the slot expects them)
@@ -1466,6 +1515,8 @@ extern "C" ps_status ps_expert_ffn_prefill_dev(const ps_expert_group* group, con
     tp.ph[1].n_tiles_n = H / 256;
     TnSchedArgs sa{};
     sa.n_group = group->n;
+    sa.maxn = tn_maxn();
+    sa.even = tn_even();
     sa.n0 = tp.ph[0].n_tiles_n;
     sa.n1 = tp.ph[1].n_tiles_n;
     for (int i = 0; i < group->n; ++i) {
@@ -1495,7 +1546,7 @@ extern "C" ps_status ps_expert_ffn_prefill_dev(const ps_expert_group* group, con
     tp.ph[1].out_ld = H;
     tn_schedule_kernel<<<1, kMaxExperts, 0, s>>>(offsets_dev, sa, sched_dev + slot, tp.done);
     PS_LAUNCH_CHECK("tn_schedule_kernel");
-    launch_tn(tp, s);
+    launch_tn(tp, s, sa.maxn);
     PS_CUDA(cudaEventRecord(ring.ev[slot], s));
   });
 }
