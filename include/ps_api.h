@@ -352,6 +352,19 @@ ps_status ps_expert_ffn(const ps_expert_group* group, const int32_t* counts_host
                         const int32_t* offsets, const int32_t* perm_src, int k,
                         const uint16_t* x, int H, int F, uint16_t* h, float* y_part,
                         int n_split, int total_rows, void* stream);
+/* K3 decode path reading the experts' weights as z-slabs (device copies of
+ * ps_zslab_encode_tiled output for [H, F] experts, e.g. a prefetch or on-demand copy that
+ * just landed): the consumer warps decode their MMA fragments from the z bytes in
+ * registers, so the expert's HBM traffic is its z bytes (~70 % of bf16) instead of a
+ * decode pass (z read + bf16 write) and the bf16 read. Results are bitwise equal to
+ * ps_zslab_decode + ps_expert_ffn. group->slabs is ignored; zslabs[i] is entry i's z-slab.
+ * Requires <= 8 tokens per expert, H % 64 == 0, F % 64 == 0, 3*H*F < 2^32 and a down split
+ * width (ps_ffn_down_splits) that is a multiple of 64; a slab whose header does not
+ * describe a tiled [H, F] expert fails the launch (device trap). */
+ps_status ps_expert_ffn_zslab(const ps_expert_group* group, const void* const* zslabs,
+                              const int32_t* counts_host, const int32_t* offsets,
+                              const int32_t* perm_src, int k, const uint16_t* x, int H, int F,
+                              uint16_t* h, float* y_part, int n_split, int total_rows, void* stream);
 /* K3 prefill path (tensor-bound): tcgen05/TMEM/TMA grouped GEMM over contiguous
  * permuted rows. x_perm [total_rows, H] bf16 (K2 gather); offsets_host [E+1] / counts_host
  * [E] are host copies of K2's offsets / K1's histogram. Outputs h_perm [total_rows, F]

@@ -220,6 +220,8 @@ _SIGS = {
     "ps_append_shared": (C.c_int, [_P, _P, C.c_int, C.c_int, C.c_int, C.c_int, _P, _P, _P, _P]),
     "ps_expert_ffn": (C.c_int, [C.POINTER(ExpertGroup), _P, _P, _P, C.c_int, _P, C.c_int, C.c_int, _P, _P,
                                 C.c_int, C.c_int, _P]),
+    "ps_expert_ffn_zslab": (C.c_int, [C.POINTER(ExpertGroup), _P, _P, _P, _P, C.c_int, _P, C.c_int, C.c_int, _P,
+                                      _P, C.c_int, C.c_int, _P]),
     "ps_ffn_down_splits": (C.c_int, [C.c_int, C.c_int]),
     "ps_set_prefill_kernel": (C.c_int, [C.c_int]),
     "ps_expert_ffn_prefill": (C.c_int, [C.POINTER(ExpertGroup), _P, _P, _P, C.c_int, C.c_int, C.c_int, _P, _P,

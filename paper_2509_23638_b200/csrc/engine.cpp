@@ -314,6 +314,7 @@ struct ps_engine_s {
   std::vector<const uint8_t*> host_z;      // [L*E] or empty
   std::vector<uint64_t> host_z_bytes;      // [L*E]
   bool host_tiled = false;                 // host_slab in the lane's tile layout (lane-only; PCIe reads host_z)
+  bool zfuse = false;                      // PS_ZFUSE=1: landed z-slabs feed K3 directly (ps_expert_ffn_zslab)
   ps::Slot od_slot[2];
   std::vector<std::unique_ptr<ps::Slot>> pf_pool;
 
@@ -455,7 +456,7 @@ int group_of_layer(const ps_model_spec& s, int l) {
 // marks the launch point (`start`) instead of recording a new one, and the last FFN's end
 // event is reused as the combine's start.
 void ffn(ps_engine_s& e, const ps_expert_group& g, const int32_t* counts_host, int B, bool timed,
-         bool exact_counts = true, cudaEvent_t start = nullptr) {
+         bool exact_counts = true, cudaEvent_t start = nullptr, const void* const* zslabs = nullptr) {
   if (g.n == 0) return;
   cudaEvent_t a = nullptr, b = nullptr;
   if (timed) {
@@ -490,6 +491,11 @@ void ffn(ps_engine_s& e, const ps_expert_group& g, const int32_t* counts_host, i
     e.st.tc_launches += n_launch;
     e.st.ffn_launches += n_launch;
     e.st.kernel_launches += n_launch;
+  } else if (zslabs) {  // landed z-slabs decoded inside K3 (<= 8 tokens per expert)
+    s = ps_expert_ffn_zslab(&g, zslabs, counts_host, src.offsets_dev, src.perm_dev, src.k, src.x, e.H, e.F, e.hbuf,
+                            e.y_part, e.step_split, src.rows, e.sc);
+    e.st.ffn_launches += 1;
+    e.st.kernel_launches += 1;
   } else {
     s = ps_expert_ffn(&g, counts_host, src.offsets_dev, src.perm_dev, src.k, src.x, e.H, e.F, e.hbuf, e.y_part,
                       e.step_split, src.rows, e.sc);
@@ -576,9 +582,12 @@ IoJob* new_job(ps_engine_s& e, int kind, int layer, int expert, int tokens, Slot
 
 // Make a landed copy usable by the FFN: after the copy event, decode a z-slab into the
 // slot's bf16 buffer (no-op for raw copies). Compute stream.
-void land(ps_engine_s& e, IoJob* j) {
+// fused: the FFN reads the landed z-slab itself (ps_expert_ffn_zslab), no decode here.
+bool fuse_z(const ps_engine_s& e, const IoJob* j, int tokens) { return e.zfuse && j->zhost && tokens <= 8; }
+
+void land(ps_engine_s& e, IoJob* j, bool fused = false) {
   PS_CUDA(cudaStreamWaitEvent(e.sc, j->done_ev, 0));
-  if (j->zhost) {
+  if (j->zhost && !fused) {
     if (ps_zslab_decode(static_cast<const uint8_t*>(j->dst), j->zhost, static_cast<uint16_t*>(j->slot->dev), e.sc) !=
         PS_OK)
       fail(PS_ECUDA, ps_last_error());
@@ -1053,32 +1062,39 @@ void layer_forward(ps_engine_s& e, int l, const float* x, const uint8_t* follow,
     // than the lane's cost for it, the lane computes it instead (steal_late).
     std::vector<const ps_engine_s::Ready*> late;
     auto gpu_ready = [&](const ps_engine_s::Ready& r) {
-      land(e, r.job);
+      const bool fz = fuse_z(e, r.job, counts_l[r.expert]);
+      land(e, r.job, fz);
       ps_expert_group one{};
       one.n = 1;
       one.experts[0] = r.expert;
       one.slabs[0] = static_cast<const uint16_t*>(r.slot->dev);
-      ffn(e, one, counts_l.data(), B, true);
+      const void* zp[1] = {r.job->dst};
+      ffn(e, one, counts_l.data(), B, true, true, nullptr, fz ? zp : nullptr);
     };
     // Prefetches whose copies have already landed share ONE FFN launch (a single-expert
     // decode launch streams at ~65 % of HBM, a group at ~90 %); the others each wait for
     // their copy in their own launch (or, with steal_late, are deferred).
     // (landed ones first: a later wait on an in-flight copy would hold the group back)
-    ps_expert_group landed{};
+    ps_expert_group landed{}, landed_z{};
+    const void* landed_zp[PS_MAX_GROUP];
     std::vector<const ps_engine_s::Ready*> in_flight;
     for (auto& r : e.ready) {
       if (r.layer != l || counts_l[r.expert] == 0) continue;
       e.st.prefetches_used++;  // a committed prefetch its target layer routed tokens to
-      if (cudaEventQuery(r.job->done_ev) == cudaSuccess && landed.n < PS_MAX_GROUP) {
-        land(e, r.job);
-        landed.experts[landed.n] = r.expert;
-        landed.slabs[landed.n] = static_cast<const uint16_t*>(r.slot->dev);
-        ++landed.n;
+      if (cudaEventQuery(r.job->done_ev) == cudaSuccess && landed.n + landed_z.n < PS_MAX_GROUP) {
+        const bool fz = fuse_z(e, r.job, counts_l[r.expert]);
+        land(e, r.job, fz);
+        ps_expert_group& g = fz ? landed_z : landed;
+        if (fz) landed_zp[landed_z.n] = r.job->dst;
+        g.experts[g.n] = r.expert;
+        g.slabs[g.n] = static_cast<const uint16_t*>(r.slot->dev);
+        ++g.n;
       } else {
         in_flight.push_back(&r);
       }
     }
     if (landed.n > 0) ffn(e, landed, counts_l.data(), B, true);
+    if (landed_z.n > 0) ffn(e, landed_z, counts_l.data(), B, true, true, nullptr, landed_zp);
     for (const ps_engine_s::Ready* r : in_flight) {
       if (e.lane && e.cfg.steal_late) late.push_back(r);
       else gpu_ready(*r);
@@ -1167,13 +1183,15 @@ void layer_forward(ps_engine_s& e, int l, const float* x, const uint8_t* follow,
       PS_CUDA(cudaEventRecord(p.before, e.sc));
       PS_CUDA(cudaStreamWaitEvent(e.sc, job->done_ev, 0));
       PS_CUDA(cudaEventRecord(p.after, e.sc));
-      land(e, job);
+      const bool fz = fuse_z(e, job, counts_l[job->expert]);
+      land(e, job, fz);
       e.stall_t.push_back(p);
       ps_expert_group one{};
       one.n = 1;
       one.experts[0] = job->expert;
       one.slabs[0] = static_cast<const uint16_t*>(job->slot->dev);
-      ffn(e, one, counts_l.data(), B, true, true, job->zhost ? nullptr : p.after);
+      const void* zp[1] = {job->dst};
+      ffn(e, one, counts_l.data(), B, true, true, job->zhost && !fz ? nullptr : p.after, fz ? zp : nullptr);
       release_slot_after_compute(e, job->slot);
       e.st.ondemand_loads++;
     }
@@ -1650,6 +1668,12 @@ void create_engine(const ps_engine_config& cfg, ps_engine_s& e) {
       tiled = false;
     }
     e.host_tiled = tiled;
+    {  // opt-in: K3 decodes landed tiled z-slabs itself (no z_decode pass, no bf16 copy)
+      const char* zf = std::getenv("PS_ZFUSE");
+      const int kch = ((e.F + e.n_split - 1) / e.n_split + 31) / 32 * 32;
+      e.zfuse = zf && zf[0] == '1' && tiled && e.H % 64 == 0 && e.F % 64 == 0 && kch % 64 == 0 &&
+                3ull * e.H * e.F < (1ull << 32);
+    }
   }
   if (auto_cost && e.z_cap) {  // provisional t_io from the mean z-slab size
     double zb = 0, cnt = 0;

@@ -41,10 +41,12 @@
 
 #include <algorithm>
 #include <mutex>
+#include <type_traits>
 #include <unordered_map>
 #include <vector>
 
 #include "device_common.cuh"
+#include "zslab_format.hpp"
 
 // Timeline hooks for scripts/probes/ffn_trace.cu (which includes this file with
 // PS_FFN_TRACE defined); compiled out of the product.
@@ -77,7 +79,7 @@ static_assert(256 + 3 * kSyncEntries * 4 + kMailbox * 4 + 4 <= kBarBytes, "smem 
 // bytes per stage scale with tokens / rows, so more tokens use taller items (MT = 4): the
 // activations are re-read from L2 once per item and would otherwise approach the L2
 // bandwidth at 16+ tokens per expert.
-template <int NT, int MT> struct Geo {
+template <int NT, int MT, bool ZS = false> struct Geo {
   static constexpr int kCols = 2 * 512 / MT;          // K elements per stage
   static constexpr int kKb = 2;                       // K blocks per consumer warp and stage
   static constexpr int kWarpsPerStage = kCols / 64;   // 8 (MT = 2) or 4 (MT = 4)
@@ -86,7 +88,8 @@ template <int NT, int MT> struct Geo {
   static constexpr int kRedBytes = kCWarps * MT * NT * 4 * 32 * 4;
   static constexpr int kStages = (227 * 1024 - kBarBytes - kRedBytes) / kStageBytes > 6
                                      ? 6 : (227 * 1024 - kBarBytes - kRedBytes) / kStageBytes;
-  static constexpr int kSmem = kBarBytes + kStages * kStageBytes + kRedBytes;
+  // ZS (z-slab source): no ring; the small footprint lets 2 CTAs share an SM
+  static constexpr int kSmem = kBarBytes + (ZS ? 0 : kStages * kStageBytes) + kRedBytes;
   static_assert(kStages >= 3 && kSmem <= 227 * 1024, "decode FFN smem budget");
 };
 
@@ -111,6 +114,7 @@ struct DecodeParams {
   size_t split_stride;
   int* sync;                      // this launch's [kSyncEntries * kMaxSplit] gate_up-items-done counters
   int* sync_next;                 // the other parity's set: zeroed here for the next launch
+  const uint8_t* z[CAP];          // ZS: entry i's z-slab (device; lane tile layout of an [H, F] expert)
 };
 
 struct Item {
@@ -220,9 +224,160 @@ __device__ __forceinline__ void load_act(uint4 (&xv)[KB][NT], const uint16_t* co
   }
 }
 
-template <int NT, int MT, int CAP>
-__global__ void __launch_bounds__(kThreads, 1) ffn_decode_kernel(const __grid_constant__ DecodeParams<CAP> p) {
-  using G = Geo<NT, MT>;
+
+// ------------------------------------------------------------------ z-slab source (ZS)
+// The consumer warps read the experts' weights as z-slabs (zexpert.cu: lossless 11-12 bit
+// format, lane tile layout: 16 x 32 tiles) and decode their MMA A fragments in registers —
+// no shared-memory ring, no decode pass, no bf16 copy. A consumer warp's share of a ring
+// stage (64 K columns x 16 rows of one m-tile) is exactly one 1024-value z block: tile u
+// of the block is the warp's K block u, and lane (g, t) needs values 8t..8t+7 of tile rows
+// g and g + 8 — 8 lo bytes and 24 (3-bit) or 32 (4-bit) code bits per fragment. Escapes
+// (all-ones codes) are ranked by a warp scan in the block's value order (tile, row, lane
+// quarter) and patched from the block's escape bytes. The fragments are the bytes a TMA
+// load of the decoded slab would deliver, so every partial sum is bitwise the bf16 path's.
+struct ZSrc {
+  const uint8_t* lo;
+  const uint32_t* codes;
+  const uint32_t* esc_off;
+  const uint8_t* esc;
+  uint32_t base, bits, n_esc;
+};
+
+__device__ __forceinline__ ZSrc z_src(const uint8_t* z, int H, int F) {
+  const uint32_t* h32 = reinterpret_cast<const uint32_t*>(z);
+  const uint32_t base = __ldg(h32 + 4), nb = __ldg(h32 + 5), n_esc = __ldg(h32 + 6);
+  const uint32_t bits = __ldg(h32 + 10), tiled = __ldg(h32 + 11), th = __ldg(h32 + 12), tf = __ldg(h32 + 13);
+  if (!tiled || th != static_cast<uint32_t>(H) || tf != static_cast<uint32_t>(F) || (bits != 3 && bits != 4)) __trap();
+  const uint64_t n_pad = static_cast<uint64_t>(nb) * kZBlock;
+  ZSrc r;
+  r.lo = z + z_lo_off();
+  r.codes = reinterpret_cast<const uint32_t*>(z + z_codes_off(n_pad));
+  r.esc_off = reinterpret_cast<const uint32_t*>(z + z_escoff_off(n_pad, bits));
+  r.esc = z + z_esc_off(n_pad, nb, bits);
+  r.base = base;
+  r.bits = bits;
+  r.n_esc = n_esc;
+  return r;
+}
+
+// One lane's raw share of a z block: fragments f = 2u + r (tile u, row gid + 8r).
+struct ZRaw {
+  uint2 lo[4];
+  uint32_t c0[4], c1[4];  // the code words holding the fragment's field
+  uint32_t eoff, eend;
+  bool valid;
+};
+
+template <int BITS>
+__device__ __forceinline__ void z_fetch(const ZSrc& zs, int b, int gid, int tig, ZRaw& r) {
+  r.valid = b >= 0;
+  if (!r.valid) return;
+#pragma unroll
+  for (int f = 0; f < 4; ++f) {
+    const uint32_t seg = static_cast<uint32_t>(b) * 32u + (f >> 1) * 16u + gid + 8u * (f & 1);
+    r.lo[f] = __ldg(reinterpret_cast<const uint2*>(zs.lo + static_cast<size_t>(seg) * 32 + 8 * tig));
+    if constexpr (BITS == 3) {
+      const uint32_t w = seg * 3u + ((24u * tig) >> 5);
+      r.c0[f] = __ldg(zs.codes + w);
+      r.c1[f] = tig == 3 ? 0u : __ldg(zs.codes + w + 1);
+    } else {
+      r.c0[f] = __ldg(zs.codes + seg * 4u + tig);
+      r.c1[f] = 0u;
+    }
+  }
+  r.eoff = __ldg(zs.esc_off + b);
+  r.eend = __ldg(zs.esc_off + b + 1);
+}
+
+// Decode the 4 fragments of a fetched block (zeros for a block past the K range).
+template <int BITS>
+__device__ __forceinline__ void z_frags(const ZSrc& zs, const ZRaw& r, int lane, int tig, uint4 (&a)[4]) {
+  if (!r.valid) {
+#pragma unroll
+    for (int f = 0; f < 4; ++f) a[f] = zero4();
+    return;
+  }
+  constexpr bool b3 = BITS == 3;
+  const uint32_t base2 = zs.base | (zs.base << 16);
+  uint32_t fld[4], em[4];
+#pragma unroll
+  for (int f = 0; f < 4; ++f) {
+    fld[f] = b3 ? __funnelshift_r(r.c0[f], r.c1[f], (24u * tig) & 31u) & 0xffffffu : r.c0[f];
+    em[f] = b3 ? fld[f] & (fld[f] >> 1) & (fld[f] >> 2) & 0x249249u
+               : fld[f] & (fld[f] >> 1) & (fld[f] >> 2) & (fld[f] >> 3) & 0x11111111u;
+#pragma unroll
+    for (int pq = 0; pq < 4; ++pq) {  // values 2pq, 2pq + 1
+      const uint32_t lw = pq < 2 ? r.lo[f].x : r.lo[f].y;
+      const uint32_t L = __byte_perm(lw, 0u, (pq & 1) ? 0x4342u : 0x4140u);
+      uint32_t C;
+      if (b3) {
+        const uint32_t t = fld[f] >> (6 * pq);
+        C = (t & 7u) | ((t << 13) & (7u << 16));
+      } else {
+        const uint32_t t = fld[f] >> (8 * pq);
+        C = (t & 15u) | ((t << 12) & (15u << 16));
+      }
+      const uint32_t v = ((L << 8) & 0x80008000u) | (((C + base2) << 7) & 0x7f807f80u) | (L & 0x007f007fu);
+      if (pq == 0) a[f].x = v;
+      else if (pq == 1) a[f].y = v;
+      else if (pq == 2) a[f].z = v;
+      else a[f].w = v;
+    }
+  }
+  if (r.eend == r.eoff) return;  // warp-uniform: no escapes in this block
+  // ranks: fragment class f holds keys [32 f, 32 f + 32) of the block's value order in lane order
+  int cnt[4];
+#pragma unroll
+  for (int f = 0; f < 4; ++f) cnt[f] = __popc(em[f]);
+  uint32_t S = static_cast<uint32_t>(cnt[0]) | (static_cast<uint32_t>(cnt[1]) << 16);
+  uint32_t T = static_cast<uint32_t>(cnt[2]) | (static_cast<uint32_t>(cnt[3]) << 16);
+  const uint32_t S0 = S, T0 = T;
+#pragma unroll
+  for (int o = 1; o < 32; o <<= 1) {
+    const uint32_t s2 = __shfl_up_sync(0xffffffffu, S, o), t2 = __shfl_up_sync(0xffffffffu, T, o);
+    if (lane >= o) {
+      S += s2;
+      T += t2;
+    }
+  }
+  const uint32_t St = __shfl_sync(0xffffffffu, S, 31), Tt = __shfl_sync(0xffffffffu, T, 31);
+  const uint32_t eS = S - S0, eT = T - T0;
+  const uint32_t tot0 = St & 0xffffu, tot1 = St >> 16, tot2 = Tt & 0xffffu;
+  uint32_t pre[4] = {eS & 0xffffu, tot0 + (eS >> 16), tot0 + tot1 + (eT & 0xffffu), tot0 + tot1 + tot2 + (eT >> 16)};
+  uint32_t eb[4];
+#pragma unroll
+  for (int f = 0; f < 4; ++f) {  // up to 4 escape bytes per fragment in one register
+    eb[f] = 0u;
+    if (cnt[f] > 0) {
+      const uint32_t at = r.eoff + pre[f], a4 = at & ~3u;
+      const uint32_t w0 = __ldg(reinterpret_cast<const uint32_t*>(zs.esc + a4));
+      const uint32_t w1 = a4 + 4u < zs.n_esc ? __ldg(reinterpret_cast<const uint32_t*>(zs.esc + a4 + 4)) : 0u;
+      eb[f] = __funnelshift_r(w0, w1, (at & 3u) * 8u);
+    }
+  }
+#pragma unroll
+  for (int f = 0; f < 4; ++f) {
+    uint32_t m = em[f];
+    uint32_t rk = 0;
+    while (m) {
+      const int pos = __ffs(m) - 1;
+      m &= m - 1;
+      const int v = b3 ? pos / 3 : pos / 4;  // value 0..7 of the fragment
+      const uint32_t ex = rk < 4 ? (eb[f] >> (8 * rk)) & 0xffu : static_cast<uint32_t>(zs.esc[r.eoff + pre[f] + rk]);
+      ++rk;
+      const uint32_t sh = 7u + 16u * (v & 1), keep = ~(0xffu << sh), put = ex << sh;
+      const int w = v >> 1;
+      if (w == 0) a[f].x = (a[f].x & keep) | put;
+      else if (w == 1) a[f].y = (a[f].y & keep) | put;
+      else if (w == 2) a[f].z = (a[f].z & keep) | put;
+      else a[f].w = (a[f].w & keep) | put;
+    }
+  }
+}
+
+template <int NT, int MT, int CAP, bool ZS>
+__global__ void __launch_bounds__(kThreads, ZS ? 2 : 1) ffn_decode_kernel(const __grid_constant__ DecodeParams<CAP> p) {
+  using G = Geo<NT, MT, ZS>;
   constexpr int KB = G::kKb;
   constexpr int kHalves = 4 / MT;  // 256-col halves per stage
   extern __shared__ __align__(1024) uint8_t smem[];
@@ -236,7 +391,7 @@ __global__ void __launch_bounds__(kThreads, 1) ffn_decode_kernel(const __grid_co
   int* s_act = s_mb + kMailbox;                               // active entries (device m_e > 0), in order
   int* s_nact = s_act + kSyncEntries;
   uint8_t* ring = smem + kBarBytes;
-  float* red = reinterpret_cast<float*>(ring + G::kStages * kStageBytes);  // [warp][mt][j][q][lane]
+  float* red = reinterpret_cast<float*>(ring + (ZS ? 0 : G::kStages * kStageBytes));  // [warp][mt][j][q][lane]
 
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   if (threadIdx.x == 0) {
@@ -295,6 +450,7 @@ __global__ void __launch_bounds__(kThreads, 1) ffn_decode_kernel(const __grid_co
     return;
   }
 
+  if (ZS && warp == kCWarps) return;  // z-slab source: the consumers fetch their own weights
   if (warp == kCWarps) {
     // ---------------------------------------------------------------- producer lane
     // Table maps are written by host copies: order them before tensormap-proxy use
@@ -410,7 +566,49 @@ __global__ void __launch_bounds__(kThreads, 1) ffn_decode_kernel(const __grid_co
       load_act<NT, KB>(xv, xr, it.down, kcol0 + st * G::kCols, it.kend, 0, tig);
     };
     constexpr int GS = G::kGroups;
-    if constexpr (NT >= 8) {  // 64 tokens: no registers for a second activation buffer
+    if constexpr (ZS) {
+      // z-slab weights: this warp's z block per m-tile and stage (one stage of raw z data
+      // and activations in flight ahead of the decode + MMAs)
+      const ZSrc zs = z_src(p.z[it.i], p.H, p.F);
+      auto blk = [&](int st, int mt) -> int {
+        const int col = kcol0 + st * G::kCols;
+        if (col >= it.kend) return -1;
+        int r0m, K;
+        uint32_t vb;
+        if (!it.down) {
+          r0m = it.r0 + 16 * (mt < MT / 2 ? mt : mt - MT / 2);
+          vb = mt < MT / 2 ? 0u : static_cast<uint32_t>(p.F) * p.H;
+          K = p.H;
+        } else {
+          r0m = it.r0 + 16 * mt;
+          vb = 2u * static_cast<uint32_t>(p.F) * p.H;
+          K = p.F;
+        }
+        return static_cast<int>(vb / kZBlock + (((r0m >> 4) * (K >> 5) + (col >> 5)) >> 1));
+      };
+      // no register prefetch: 2 CTAs per SM (20 warps) hide the load latency instead
+      auto run = [&](auto bits_tag) {
+        constexpr int BITS = decltype(bits_tag)::value;
+        for (int st = grp; st < nst; st += GS) {
+          ZRaw ra[MT];
+          uint4 xa[KB][NT];
+#pragma unroll
+          for (int mt = 0; mt < MT; ++mt) z_fetch<BITS>(zs, blk(st, mt), gid, tig, ra[mt]);
+          load(xa, st);
+#pragma unroll
+          for (int mt = 0; mt < MT; ++mt) {
+            uint4 a[4];
+            z_frags<BITS>(zs, ra[mt], lane, tig, a);
+#pragma unroll
+            for (int u = 0; u < KB; ++u)
+#pragma unroll
+              for (int j = 0; j < NT; ++j) mma_block(acc[mt][j], a[2 * u], a[2 * u + 1], xa[u][j]);
+          }
+        }
+      };
+      if (zs.bits == 3) run(std::integral_constant<int, 3>{});
+      else run(std::integral_constant<int, 4>{});
+    } else if constexpr (NT >= 8) {  // 64 tokens: no registers for a second activation buffer
       uint4 xa[KB][NT];
       for (int st = grp; st < nst; st += GS) {
         load(xa, st);
@@ -605,16 +803,16 @@ SyncSets sync_workspace(cudaStream_t s) {
   return SyncSets{w.base + par * set, w.base + (par ^ 1) * set};
 }
 
-template <int NT, int MT, int CAP>
+template <int NT, int MT, int CAP, bool ZS>
 void launch(const DecodeParams<CAP>& p, cudaStream_t s) {
   DeviceInfo& d = device_info();
-  const size_t smem = Geo<NT, MT>::kSmem;
-  const void* fn = reinterpret_cast<const void*>(ffn_decode_kernel<NT, MT, CAP>);
+  const size_t smem = Geo<NT, MT, ZS>::kSmem;
+  const void* fn = reinterpret_cast<const void*>(ffn_decode_kernel<NT, MT, CAP, ZS>);
   int& bps = d.blocks_per_sm[fn];
   if (bps == 0) {
-    PS_CUDA(cudaFuncSetAttribute(ffn_decode_kernel<NT, MT, CAP>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+    PS_CUDA(cudaFuncSetAttribute(ffn_decode_kernel<NT, MT, CAP, ZS>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                  static_cast<int>(smem)));
-    PS_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&bps, ffn_decode_kernel<NT, MT, CAP>, kThreads, smem));
+    PS_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&bps, ffn_decode_kernel<NT, MT, CAP, ZS>, kThreads, smem));
     require(bps >= 1, "ffn_decode_kernel: does not fit on an SM");
   }
   const int total = p.n * (p.gu_per + p.dn_per);  // upper bound (entries with m_e = 0 are dropped on device)
@@ -629,7 +827,7 @@ void launch(const DecodeParams<CAP>& p, cudaStream_t s) {
   attr[0].val.cooperative = 1;
   cfg.attrs = attr;
   cfg.numAttrs = 1;  // measured cost of the attribute: ~1.5 us per launch
-  PS_CUDA(cudaLaunchKernelEx(&cfg, ffn_decode_kernel<NT, MT, CAP>, p));
+  PS_CUDA(cudaLaunchKernelEx(&cfg, ffn_decode_kernel<NT, MT, CAP, ZS>, p));
 }
 
 struct Shape {
@@ -642,7 +840,7 @@ constexpr int mt_for(int NT) { return NT == 1 || NT == 8 ? 2 : 4; }
 template <int CAP>
 void run_group(const ps_expert_group* group, int base, int count, const int32_t* counts_host, const Shape& sh,
                int tok_base, int NT, const int32_t* offsets, const int32_t* perm_src, const uint16_t* x, uint16_t* h,
-               float* y_part, size_t split_stride, cudaStream_t s) {
+               float* y_part, size_t split_stride, cudaStream_t s, const uint8_t* const* zslabs = nullptr) {
   DecodeParams<CAP> p;
   p.n = 0;
   p.H = sh.H;
@@ -664,7 +862,14 @@ void run_group(const ps_expert_group* group, int base, int count, const int32_t*
   for (int i = base; i < base + count; ++i) {
     const int e = group->experts[i];
     if (counts_host[e] <= tok_base) continue;
-    p.map_idx[p.n] = slab_map_index(group->slabs[i], sh.H, sh.F, s, &p.maps);
+    if (zslabs) {
+      p.z[p.n] = zslabs[i];
+      p.map_idx[p.n] = 0;
+      p.maps = nullptr;
+    } else {
+      p.map_idx[p.n] = slab_map_index(group->slabs[i], sh.H, sh.F, s, &p.maps);
+      p.z[p.n] = nullptr;
+    }
     p.expert[p.n] = e;
     ++p.n;
   }
@@ -673,11 +878,15 @@ void run_group(const ps_expert_group* group, int base, int count, const int32_t*
   p.sync = ss.cur;
   p.sync_next = ss.next;
   try {
-    switch (NT) {
-      case 1: launch<1, mt_for(1), CAP>(p, s); break;
-      case 2: launch<2, mt_for(2), CAP>(p, s); break;
-      case 4: launch<4, mt_for(4), CAP>(p, s); break;
-      default: launch<8, mt_for(8), CAP>(p, s); break;
+    if (zslabs) {  // z-slab source: decode batches of <= 8 tokens per expert
+      launch<1, mt_for(1), CAP, true>(p, s);
+    } else {
+      switch (NT) {
+        case 1: launch<1, mt_for(1), CAP, false>(p, s); break;
+        case 2: launch<2, mt_for(2), CAP, false>(p, s); break;
+        case 4: launch<4, mt_for(4), CAP, false>(p, s); break;
+        default: launch<8, mt_for(8), CAP, false>(p, s); break;
+      }
     }
   } catch (...) {
     // The failed launch never zeroed the next launch's counter set: do it here, so the
@@ -736,6 +945,42 @@ ps_status ps_expert_ffn(const ps_expert_group* group, const int32_t* counts_host
           run_group<kSyncEntries>(group, base, count, counts_host, sh, tok_base, NT, offsets, perm_src, x, h, y_part,
                                   split_stride, s);
       }
+    }
+  });
+}
+
+ps_status ps_expert_ffn_zslab(const ps_expert_group* group, const void* const* zslabs, const int32_t* counts_host,
+                              const int32_t* offsets, const int32_t* perm_src, int k, const uint16_t* x, int H, int F,
+                              uint16_t* h, float* y_part, int n_split, int total_rows, void* stream) {
+  return guarded([&] {
+    require(group && zslabs && counts_host && offsets && perm_src && x && h && y_part,
+            "ps_expert_ffn_zslab: null argument");
+    require(H % 64 == 0 && F % 64 == 0 && H >= 64 && F >= 64, "ps_expert_ffn_zslab: H and F must be multiples of 64");
+    require(n_split >= 1 && n_split <= kMaxSplit && group->n >= 0 && group->n <= PS_MAX_GROUP,
+            "ps_expert_ffn_zslab: bad group/split");
+    require(3ull * H * F < (1ull << 32), "ps_expert_ffn_zslab: expert too large");
+    cudaStream_t s = as_stream(stream);
+    int max_m = 0;
+    for (int i = 0; i < group->n; ++i) {
+      require(zslabs[i] != nullptr, "ps_expert_ffn_zslab: null z-slab");
+      max_m = std::max(max_m, counts_host[group->experts[i]]);
+    }
+    if (max_m == 0) return;
+    require(max_m <= 8, "ps_expert_ffn_zslab: more than 8 tokens for an expert (decode batches only)");
+    require(total_rows >= max_m, "ps_expert_ffn_zslab: total_rows smaller than an expert's rows");
+    Shape sh{H, F, k, n_split, 0};
+    sh.kchunk = (F + n_split - 1) / n_split;
+    sh.kchunk = (sh.kchunk + 31) / 32 * 32;
+    require(sh.kchunk % 64 == 0, "ps_expert_ffn_zslab: the down split width must be a multiple of 64");
+    const size_t split_stride = static_cast<size_t>(total_rows) * H;
+    const auto* z = reinterpret_cast<const uint8_t* const*>(zslabs);
+    for (int base = 0; base < group->n; base += kSyncEntries) {
+      const int count = std::min(kSyncEntries, group->n - base);
+      if (count <= 8)
+        run_group<8>(group, base, count, counts_host, sh, 0, 1, offsets, perm_src, x, h, y_part, split_stride, s, z);
+      else
+        run_group<kSyncEntries>(group, base, count, counts_host, sh, 0, 1, offsets, perm_src, x, h, y_part,
+                                split_stride, s, z);
     }
   });
 }
