@@ -272,16 +272,20 @@ template <int BITS>
 __device__ __forceinline__ void z_fetch(const ZSrc& zs, int b, int gid, int tig, ZRaw& r) {
   r.valid = b >= 0;
   if (!r.valid) return;
+  // fragment f = 2u + rr is segment 16u + gid + 8rr of the block: constant offsets from
+  // this lane's first fragment
+  const uint8_t* lo = zs.lo + static_cast<size_t>(b) * 1024 + gid * 32 + 8 * tig;
+  const uint32_t* cw = zs.codes + static_cast<size_t>(b) * (32 * BITS) + gid * BITS;
 #pragma unroll
   for (int f = 0; f < 4; ++f) {
-    const uint32_t seg = static_cast<uint32_t>(b) * 32u + (f >> 1) * 16u + gid + 8u * (f & 1);
-    r.lo[f] = __ldg(reinterpret_cast<const uint2*>(zs.lo + static_cast<size_t>(seg) * 32 + 8 * tig));
+    const int so = (f >> 1) * 16 + 8 * (f & 1);  // segment offset of fragment f
+    r.lo[f] = __ldg(reinterpret_cast<const uint2*>(lo + so * 32));
     if constexpr (BITS == 3) {
-      const uint32_t w = seg * 3u + ((24u * tig) >> 5);
-      r.c0[f] = __ldg(zs.codes + w);
-      r.c1[f] = tig == 3 ? 0u : __ldg(zs.codes + w + 1);
+      const uint32_t* w = cw + so * 3 + ((24 * tig) >> 5);
+      r.c0[f] = __ldg(w);
+      r.c1[f] = tig == 3 ? 0u : __ldg(w + 1);
     } else {
-      r.c0[f] = __ldg(zs.codes + seg * 4u + tig);
+      r.c0[f] = __ldg(cw + so * 4 + tig);
       r.c1[f] = 0u;
     }
   }
@@ -429,6 +433,7 @@ __global__ void __launch_bounds__(kThreads, ZS ? 2 : 1) ffn_decode_kernel(const 
   const int n_act = *s_nact;
   const int total = n_act * (p.gu_per + p.dn_per);
 
+  if (ZS && warp == kCWarps + 1) return;  // ZS: consumer thread 0 publishes (a polling lane costs issue slots)
   if (warp == kCWarps + 1) {
     // ---------------------------------------------------------------- signaler lane
     // Publishes finished gate_up items to the down items of their split: acquire the
@@ -666,7 +671,12 @@ __global__ void __launch_bounds__(kThreads, ZS ? 2 : 1) ffn_decode_kernel(const 
     }
     consumer_sync();  // red reusable; every h store of this item issued
     if (threadIdx.x == 0) PS_TRACE(ord, 3);
-    if (!it.down) {  // hand this F tile to the signaler (mbarrier arrive = release.cta)
+    if (ZS && !it.down) {  // publish this F tile to the down items of its split
+      if (threadIdx.x == 0) {
+        __threadfence();
+        atomicAdd(p.sync + slot, 1);
+      }
+    } else if (!it.down) {  // hand this F tile to the signaler (mbarrier arrive = release.cta)
       if (threadIdx.x == 0) {
         const int b = gu_done % kMailbox;
         mbar_wait(&freed[b], ((gu_done / kMailbox) & 1) ^ 1);

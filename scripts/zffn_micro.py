@@ -4,6 +4,7 @@ same process, alternating. HBM bytes: fused = z bytes; two-pass = z read + bf16 
 bf16 read. Prints one JSON line per (experts, tokens) case."""
 import ctypes as C
 import json
+import os
 import sys
 from pathlib import Path
 
@@ -21,6 +22,7 @@ def main():
     sp = C.c_void_p(s.cuda_stream)
     P = lambda t: C.c_void_p(t.data_ptr())  # noqa: E731
     E = 8
+    bits = os.environ.get("PS_ZSLAB_BITS", "auto")  # pins the encoder's code width (3 or 4)
     zs_h, zs_d = [], []
     for e in range(E):
         slab = np.empty(3 * H * F, np.uint16)
@@ -94,7 +96,7 @@ def main():
                 b.synchronize()
                 res[name].append(a.elapsed_time(b) * 1e3)
         med = {k: float(np.median(v)) for k, v in res.items()}
-        line = {"experts": n_exp, "tokens_per_expert": m, "us": med,
+        line = {"code_bits": bits, "experts": n_exp, "tokens_per_expert": m, "us": med,
                 "z_bytes_per_expert": zbytes, "bf16_bytes_per_expert": 6.0 * H * F,
                 "fused_z_gbs": n_exp * zbytes / med["fused"] / 1e3,
                 "fused_bf16_equiv_gbs": n_exp * 6.0 * H * F / med["fused"] / 1e3,
