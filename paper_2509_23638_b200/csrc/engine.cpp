@@ -583,7 +583,11 @@ IoJob* new_job(ps_engine_s& e, int kind, int layer, int expert, int tokens, Slot
 // Make a landed copy usable by the FFN: after the copy event, decode a z-slab into the
 // slot's bf16 buffer (no-op for raw copies). Compute stream.
 // fused: the FFN reads the landed z-slab itself (ps_expert_ffn_zslab), no decode here.
-bool fuse_z(const ps_engine_s& e, const IoJob* j, int tokens) { return e.zfuse && j->zhost && tokens <= 8; }
+// Only 4-bit-code slabs: with 3-bit codes (~3 % escapes) the in-register patching makes the
+// fused kernel slower than z_decode + K3 (profiles/README.md).
+bool fuse_z(const ps_engine_s& e, const IoJob* j, int tokens) {
+  return e.zfuse && j->zhost && tokens <= 8 && reinterpret_cast<const ZHeader*>(j->zhost)->code_bits == 4;
+}
 
 void land(ps_engine_s& e, IoJob* j, bool fused = false) {
   PS_CUDA(cudaStreamWaitEvent(e.sc, j->done_ev, 0));

@@ -122,15 +122,16 @@ def test_zslab_ffn_rejects_unsupported(torch_cuda):
 
 
 def test_engine_zfuse_bitwise_equals_decode_pass(torch_cuda, monkeypatch):
-    """PS_ZFUSE=1: the engine feeds landed z-slabs (prefetches and on-demand loads) straight
-    to K3 instead of decoding them into the slot first — outputs bitwise equal, no z_decode
-    launches (batches of <= 8 tokens per expert)."""
+    """PS_ZFUSE=1: the engine feeds landed 4-bit-code z-slabs (prefetches and on-demand
+    loads) straight to K3 instead of decoding them into the slot first — outputs bitwise
+    equal, no z_decode launches (batches of <= 8 tokens per expert)."""
     from paper_2509_23638_b200 import engine as eng
     spec = ps.desk_scale("mixtral", 4, 8, 256)
     spec.expert_bytes = 6 * 256 * 512
     cfg = ps.TraceGenConfig(*[ps.GROUP_DEFAULT_GEN[g] for g in ("input", "middle", "output")])
     gate, hidden, follow, _ = ps.trace_inputs(cfg, spec, 8, 3)
     outs, stats = [], []
+    monkeypatch.setenv("PS_ZSLAB_BITS", "4")  # the engine fuses 4-bit-code slabs only
     for fuse in ("0", "1"):
         monkeypatch.setenv("PS_ZFUSE", fuse)
         with eng.Engine(spec, cfg, budget_fraction=0.25, max_batch=8, weight_seed=9, gate=gate, trace_hidden=hidden,
