@@ -36,6 +36,7 @@ def main():
         lib = ps.load()
         ps.check(lib.ps_set_prefill_kernel({"prefill_single": 0, "prefill_pair": 1, "prefill_tn": 3}[args.only]))
         run("mixtral", 3, 8, 256, 512, 512, 1.0)
+        run("mixtral", 3, 8, 256, 512, 1200, 1.0)  # m_e ~ 300: equal-width multi-tile experts
         print("sanitize run done")
         return
     cost = (1000, 5, 10, 1.0, 1, 0)
