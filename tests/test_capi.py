@@ -3,6 +3,8 @@ include/ps_api.h declares (no compute calls — CPU safe)."""
 import ctypes as C
 import subprocess
 
+import numpy as np
+
 import paper_2509_23638_b200 as ps
 from conftest import ROOT
 
@@ -58,3 +60,19 @@ def test_argument_validation_before_any_launch():
     assert lib.ps_zslab_bound(1024) > 1024
     # shared-expert append: S out of range
     assert lib.ps_append_shared(p, p, 4, 2, 8, 0, p, p, None, None) == ps.capi.PS_EINVAL
+    # K3 on z-slabs: shape / token-count checks, and an all-idle group is a no-op (no launch)
+    grp = ps.capi.ExpertGroup()
+    grp.n = 2
+    grp.experts[0], grp.experts[1] = 0, 1
+    zp = (C.c_void_p * 2)(16, 32)
+    idle = np.zeros(2, np.int32)
+    assert lib.ps_expert_ffn_zslab(C.byref(grp), zp, idle.ctypes.data, p, p, 1, p, 256, 512, p, p, 1, 8,
+                                   None) == ps.capi.PS_OK
+    busy = np.array([9, 0], np.int32)
+    assert lib.ps_expert_ffn_zslab(C.byref(grp), zp, busy.ctypes.data, p, p, 1, p, 256, 512, p, p, 1, 9,
+                                   None) == ps.capi.PS_EINVAL
+    assert b"8 tokens" in lib.ps_last_error()
+    assert lib.ps_expert_ffn_zslab(C.byref(grp), zp, idle.ctypes.data, p, p, 1, p, 96, 512, p, p, 1, 8,
+                                   None) == ps.capi.PS_EINVAL
+    assert lib.ps_expert_ffn_zslab(C.byref(grp), None, idle.ctypes.data, p, p, 1, p, 256, 512, p, p, 1, 8,
+                                   None) == ps.capi.PS_EINVAL
